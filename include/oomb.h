@@ -1,0 +1,201 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * oomb.h — C ABI of the B200-native OOMB hot path (liboomb.so).
+ *
+ * The reference (/root/reference/proj) has no FFI: its operator API is the C++
+ * template surface of paged_kv.hpp / attention.hpp / tiered_memory.hpp. Each
+ * entry point below replaces one of those calls; the citation next to it is
+ * the reference interface it stands in for (paths relative to
+ * /root/reference/proj/core/include/chunktrain/). The host-side mirror of that
+ * API lives in paper_2602_02108_b200/ (Python, ctypes); INTEGRATION.md shows
+ * the binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *  - Every function returns an oomb_status; OOMB_OK == 0. The codes map 1:1
+ *    onto the reference's exception classes (common.hpp:15-29) plus
+ *    OOMB_CUDA_ERROR. oomb_last_error() holds the message (thread-local).
+ *  - Tensor arguments are DEVICE pointers unless the name ends in _host.
+ *    Layouts are the reference's row-major ones: q/out/dout/dq [tokens][Hq][hd],
+ *    k/v/k_cur/v_cur/dk_cur/dv_cur [rows][Hkv][hd], lse [tokens][Hq].
+ *  - Element types: q, k, v, k_cur, v_cur, out, dout use the pool dtype
+ *    (OOMB_F32 or OOMB_BF16); lse, votes, dq, dk_cur, dv_cur and the gradient
+ *    pool are always fp32.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *    every call is stream-ordered and asynchronous unless documented.
+ *  - Handles are not thread-safe.
+ */
+#ifndef OOMB_H_
+#define OOMB_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define OOMB_API __attribute__((visibility("default")))
+#else
+#define OOMB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    OOMB_OK = 0,
+    OOMB_CONFIG_ERROR = 1,    /* chunktrain::ConfigError    common.hpp:15-17 */
+    OOMB_SHAPE_ERROR = 2,     /* chunktrain::ShapeError     common.hpp:18-20 */
+    OOMB_STATE_ERROR = 3,     /* chunktrain::StateError     common.hpp:21-23 */
+    OOMB_RESIDENCY_ERROR = 4, /* chunktrain::ResidencyError common.hpp:24-26 */
+    OOMB_IO_ERROR = 5,        /* chunktrain::IoError        common.hpp:27-29 */
+    OOMB_CUDA_ERROR = 6,
+    OOMB_ERROR = 9
+} oomb_status;
+
+typedef enum { OOMB_F32 = 0, OOMB_BF16 = 1 } oomb_dtype;
+
+/* ModelConfig fields on the path (config.hpp:19-49) + device sizing. */
+typedef struct {
+    int n_layers;
+    int n_q_heads;
+    int n_kv_heads;
+    int head_dim;
+    int chunk_size;       /* C */
+    int page_size;        /* P */
+    int retrieval_budget; /* B tokens; k = B / P pages per query page (config.hpp:41) */
+    int local_window;     /* W pages */
+    int score_scale;      /* 0 = unscaled vote (config.hpp:35-37) */
+    int dtype;            /* oomb_dtype of the KV pool and the attention inputs */
+    int64_t max_tokens;   /* per-layer capacity of the device page table */
+    int64_t device_capacity_pages; /* KV page slots on the device, all layers; <= 0: n_layers*max_pages */
+} oomb_config;
+
+typedef struct {
+    uint64_t device_bytes; /* MemoryReport paged_kv.hpp:25-32 */
+    uint64_t host_bytes;
+    uint64_t grad_bytes;
+    int64_t pages;
+    int64_t reallocs;      /* always 0 */
+    uint64_t copied_bytes; /* always 0 */
+    int64_t arena_blocks;  /* PagedCache::arena_blocks_allocated paged_kv.hpp:249 */
+    int64_t free_list;     /* PagedCache::free_list_size        paged_kv.hpp:250 */
+} oomb_memory_report;
+
+typedef struct oomb_pool_s* oomb_pool_t;           /* PagedCache<Real>          paged_kv.hpp:41 */
+typedef struct oomb_selection_s* oomb_selection_t; /* AttnSaved::selected       attention.hpp:117-124 */
+typedef struct oomb_pagetable_s* oomb_pagetable_t; /* PagedCache page table only (host logic) */
+
+OOMB_API const char* oomb_last_error(void);
+OOMB_API int oomb_version(void);
+/* Number of sm_100a kernel launches issued by this process (for bench evidence). */
+OOMB_API int64_t oomb_kernel_launches(void);
+
+/* ---- lifecycle ---------------------------------------------------------- */
+/* PagedCache(const ModelConfig&) + ModelConfig::validate  paged_kv.hpp:44-50, config.cpp:30-51 */
+OOMB_API int oomb_pool_create(const oomb_config* cfg, int device, oomb_pool_t* out);
+OOMB_API int oomb_pool_destroy(oomb_pool_t pool);
+/* PagedCache::reset  paged_kv.hpp:227-242 */
+OOMB_API int oomb_pool_reset(oomb_pool_t pool, void* stream);
+/* PagedCache::zero_grad_pages  paged_kv.hpp:214-223 */
+OOMB_API int oomb_zero_grad_pages(oomb_pool_t pool, void* stream);
+/* PagedCache::memory_report  paged_kv.hpp:185-197 */
+OOMB_API int oomb_memory_report_get(oomb_pool_t pool, oomb_memory_report* out);
+/* Device-side error flag raised by kernels (e.g. a non-resident page was read). Synchronises. */
+OOMB_API int oomb_check_device_errors(oomb_pool_t pool);
+
+/* ---- page table --------------------------------------------------------- */
+/* PagedCache::append_chunk  paged_kv.hpp:73-108. k, v: [rows][Hkv][hd] device, pool dtype.
+ * Writes tail slots in place and updates the K_avg fp32 sums in append order. */
+OOMB_API int oomb_append_chunk(oomb_pool_t pool, int layer, const void* k, const void* v, int64_t rows, void* stream,
+                      int64_t* slot_begin, int64_t* slot_end);
+OOMB_API int oomb_n_pages(oomb_pool_t pool, int layer, int* n_pages);   /* paged_kv.hpp:62 */
+OOMB_API int oomb_filled(oomb_pool_t pool, int layer, int64_t* filled); /* paged_kv.hpp:61 */
+/* Reference arena ids {k_phys, v_phys, gk_phys, gv_phys} per logical page (PageEntry paged_kv.hpp:256-262). */
+OOMB_API int oomb_page_table_get(oomb_pool_t pool, int layer, int32_t* out_host);
+/* Device slots {kv_slot, grad_slot} per logical page (-1 = none / not resident). */
+OOMB_API int oomb_device_slots_get(oomb_pool_t pool, int layer, int32_t* out_host);
+/* PagedCache::page_mean_keys  paged_kv.hpp:170-183 -> out [n][Hkv][hd] fp32 device. */
+OOMB_API int oomb_page_mean_keys(oomb_pool_t pool, int layer, int n_candidates, float* out, void* stream, int* n_out);
+/* Raw K_avg state (sums fp32 [n][Hkv][hd] device, counts int32 [n] device). */
+OOMB_API int oomb_kavg_raw(oomb_pool_t pool, int layer, float* sum_out, int32_t* count_out, void* stream);
+/* PagedCache::gather_pages / gather_grad_pages  paged_kv.hpp:118-130. ids on host; k/v out
+ * [n*P][Hkv][hd] device (pool dtype for KV, fp32 for grads); valid [n*P] uint8 device. */
+OOMB_API int oomb_gather_pages(oomb_pool_t pool, int layer, const int32_t* ids_host, int n, int grads, void* k_out,
+                      void* v_out, uint8_t* valid_out, void* stream);
+/* PagedCache::scatter_add_grads  paged_kv.hpp:135-164. dk/dv fp32 [n*P][Hkv][hd] device. */
+OOMB_API int oomb_scatter_add_grads(oomb_pool_t pool, int layer, const int32_t* ids_host, int n, const float* dk,
+                           const float* dv, void* stream);
+/* Tier tags and residency enforcement  paged_kv.hpp:199-211. */
+OOMB_API int oomb_set_tier(oomb_pool_t pool, int layer, int page, int tier);
+OOMB_API int oomb_get_tier(oomb_pool_t pool, int layer, int page, int* tier);
+OOMB_API int oomb_set_residency_enforced(oomb_pool_t pool, int on);
+OOMB_API int oomb_grads_allocated(oomb_pool_t pool, int layer, int page, int* allocated);
+
+/* ---- selection ---------------------------------------------------------- */
+/* A selection is per query page: CSR (offsets[m+1], ids[]) in device memory, with an
+ * asynchronously-maintained pinned host mirror. */
+OOMB_API int oomb_selection_create(oomb_pool_t pool, int max_query_pages, int max_ids, oomb_selection_t* out);
+OOMB_API int oomb_selection_destroy(oomb_selection_t sel);
+/* Upload caller-provided lists (the reference's vector<vector<int32_t>>). */
+OOMB_API int oomb_selection_set_host(oomb_selection_t sel, const int32_t* offsets_host, const int32_t* ids_host, int m,
+                            void* stream);
+/* Read back (waits for the mirror). offsets_host needs m+1 entries; ids_host nnz entries. */
+OOMB_API int oomb_selection_get_host(oomb_selection_t sel, int32_t* offsets_host, int32_t* ids_host, int* m, int* nnz);
+/* Device CSR pointers (int32). */
+OOMB_API int oomb_selection_device(oomb_selection_t sel, const int32_t** offsets, const int32_t** ids, int* m);
+/* select_all / select_recent  attention.hpp:99-111, broadcast to m query pages (chunk_trainer.hpp:301-304). */
+OOMB_API int oomb_select_all(oomb_selection_t sel, int n_pages, int m, void* stream);
+OOMB_API int oomb_select_recent(oomb_selection_t sel, int n_pages, int window, int m, void* stream);
+/* select_topk_row per row of a device vote matrix [m][n] fp32  attention.hpp:71-96:
+ * k largest, ties to the lower id, ascending; k >= n -> all; k < 0 -> SHAPE_ERROR. */
+OOMB_API int oomb_select_topk(oomb_selection_t sel, const float* vote, int m, int n, int k, void* stream);
+
+/* ---- scoring ------------------------------------------------------------ */
+/* score_pages  attention.hpp:32-67 on explicit representatives:
+ * q [tokens][Hq][hd] (dtype), k_avg [n][Hkv][hd] fp32 -> vote [ceil(tokens/P)][n] fp32 device. */
+OOMB_API int oomb_score_pages(const void* q, int64_t tokens, int n_q_heads, int head_dim, const float* k_avg, int64_t n,
+                     int n_kv_heads, int page_size, int score_scale, int dtype, float* vote, void* stream);
+/* The trainer's top-k selector in one call (chunk_trainer.hpp:305-311): K_avg of the first
+ * n_candidates pages of `layer` (pinned metadata) -> score_pages -> select_topk_row per query page. */
+OOMB_API int oomb_select_pages_topk(oomb_pool_t pool, int layer, const void* q, int64_t tokens, int n_candidates,
+                           oomb_selection_t sel, float* vote_scratch, void* stream);
+
+/* ---- attention ---------------------------------------------------------- */
+/* attn_forward  attention.hpp:156-208: q [C][Hq][hd], k_cur/v_cur [C][Hkv][hd] (pool dtype) ->
+ * out [C][Hq][hd] (pool dtype), lse [C][Hq] fp32 (natural log). */
+OOMB_API int oomb_attn_forward(oomb_pool_t pool, int layer, const void* q, int64_t tokens, oomb_selection_t sel,
+                      const void* k_cur, const void* v_cur, void* out, float* lse, void* stream);
+/* attn_backward  attention.hpp:222-293: rebuilds P from the saved lse, D from the saved out;
+ * past-page dK/dV are accumulated IN PLACE into the fp32 gradient pool (lazily allocated
+ * and zeroed per page, reference order); dq/dk_cur/dv_cur fp32 are overwritten. */
+OOMB_API int oomb_attn_backward(oomb_pool_t pool, int layer, const void* dout, const void* q, int64_t tokens,
+                       oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out,
+                       const float* lse, float* dq, float* dk_cur, float* dv_cur, void* stream);
+/* Kernel family selection: 0 = auto (tcgen05 when dtype bf16, hd 128, P % 128 == 0),
+ * 1 = force the SIMT kernels, 2 = force tcgen05 (error if the shape is unsupported). */
+OOMB_API int oomb_set_kernel_policy(oomb_pool_t pool, int policy);
+
+/* ---- page-table host logic (no device) -----------------------------------
+ * The arena / LIFO free-list / lazy-gradient-page bookkeeping of PagedCache
+ * (paged_kv.hpp:73-108,135-164,227-242,280-288), exposed on its own so that it is
+ * testable without a GPU. The pool owns one of these. */
+OOMB_API int oomb_pagetable_create(int n_layers, int page_size, int n_kv_heads, int head_dim, int kv_elem_bytes,
+                          int grad_elem_bytes, oomb_pagetable_t* out);
+OOMB_API int oomb_pagetable_destroy(oomb_pagetable_t pt);
+OOMB_API int oomb_pagetable_append(oomb_pagetable_t pt, int layer, int64_t rows, int64_t* slot_begin, int64_t* slot_end);
+OOMB_API int oomb_pagetable_scatter(oomb_pagetable_t pt, int layer, const int32_t* ids_host, int n);
+OOMB_API int oomb_pagetable_reset(oomb_pagetable_t pt);
+OOMB_API int oomb_pagetable_n_pages(oomb_pagetable_t pt, int layer, int* n);
+OOMB_API int oomb_pagetable_get(oomb_pagetable_t pt, int layer, int32_t* out_host);
+OOMB_API int oomb_pagetable_set_tier(oomb_pagetable_t pt, int layer, int page, int tier);
+OOMB_API int oomb_pagetable_memory_report(oomb_pagetable_t pt, oomb_memory_report* out);
+
+/* ---- debug / evidence ------------------------------------------------------ */
+/* One 128xNxK bf16 tcgen05 GEMM tile through the same TMA/UMMA building blocks the
+ * attention kernels use (validation of descriptor layouts). mode 0: C = A B^T with
+ * A [M][K], B [N][K] (both K-major); mode 1: C = A B with B [K][N] (MN-major B).
+ * M = 128, N in {64,128,256}, K % 64 == 0. C fp32 [M][N]. */
+OOMB_API int oomb_debug_tc_gemm(int mode, const void* a, const void* b, float* c, int m, int n, int k, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OOMB_H_ */

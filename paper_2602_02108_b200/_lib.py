@@ -1,0 +1,121 @@
+"""ctypes binding of liboomb.so (include/oomb.h).
+
+The product path has no fallback: if the library is missing or cannot be
+loaded, importing the operator modules raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import raise_for_status
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "liboomb.so")
+
+I32P = C.POINTER(C.c_int32)
+
+
+class OombConfig(C.Structure):
+    _fields_ = [
+        ("n_layers", C.c_int), ("n_q_heads", C.c_int), ("n_kv_heads", C.c_int), ("head_dim", C.c_int),
+        ("chunk_size", C.c_int), ("page_size", C.c_int), ("retrieval_budget", C.c_int), ("local_window", C.c_int),
+        ("score_scale", C.c_int), ("dtype", C.c_int), ("max_tokens", C.c_int64),
+        ("device_capacity_pages", C.c_int64),
+    ]
+
+
+class OombMemoryReport(C.Structure):
+    _fields_ = [
+        ("device_bytes", C.c_uint64), ("host_bytes", C.c_uint64), ("grad_bytes", C.c_uint64), ("pages", C.c_int64),
+        ("reallocs", C.c_int64), ("copied_bytes", C.c_uint64), ("arena_blocks", C.c_int64), ("free_list", C.c_int64),
+    ]
+
+
+VP = C.c_void_p
+I = C.c_int
+I64 = C.c_int64
+
+# name -> argtypes (all return int status unless listed in _RESTYPE)
+_PROTOS = {
+    "oomb_last_error": [],
+    "oomb_version": [],
+    "oomb_kernel_launches": [],
+    "oomb_pool_create": [C.POINTER(OombConfig), I, C.POINTER(VP)],
+    "oomb_pool_destroy": [VP],
+    "oomb_pool_reset": [VP, VP],
+    "oomb_zero_grad_pages": [VP, VP],
+    "oomb_memory_report_get": [VP, C.POINTER(OombMemoryReport)],
+    "oomb_check_device_errors": [VP],
+    "oomb_append_chunk": [VP, I, VP, VP, I64, VP, C.POINTER(I64), C.POINTER(I64)],
+    "oomb_n_pages": [VP, I, C.POINTER(I)],
+    "oomb_filled": [VP, I, C.POINTER(I64)],
+    "oomb_page_table_get": [VP, I, VP],
+    "oomb_device_slots_get": [VP, I, VP],
+    "oomb_page_mean_keys": [VP, I, I, VP, VP, C.POINTER(I)],
+    "oomb_kavg_raw": [VP, I, VP, VP, VP],
+    "oomb_gather_pages": [VP, I, VP, I, I, VP, VP, VP, VP],
+    "oomb_scatter_add_grads": [VP, I, VP, I, VP, VP, VP],
+    "oomb_set_tier": [VP, I, I, I],
+    "oomb_get_tier": [VP, I, I, C.POINTER(I)],
+    "oomb_set_residency_enforced": [VP, I],
+    "oomb_grads_allocated": [VP, I, I, C.POINTER(I)],
+    "oomb_selection_create": [VP, I, I, C.POINTER(VP)],
+    "oomb_selection_destroy": [VP],
+    "oomb_selection_set_host": [VP, VP, VP, I, VP],
+    "oomb_selection_get_host": [VP, VP, VP, C.POINTER(I), C.POINTER(I)],
+    "oomb_selection_device": [VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(I)],
+    "oomb_select_all": [VP, I, I, VP],
+    "oomb_select_recent": [VP, I, I, I, VP],
+    "oomb_select_topk": [VP, VP, I, I, I, VP],
+    "oomb_score_pages": [VP, I64, I, I, VP, I64, I, I, I, I, VP, VP],
+    "oomb_select_pages_topk": [VP, I, VP, I64, I, VP, VP, VP],
+    "oomb_attn_forward": [VP, I, VP, I64, VP, VP, VP, VP, VP, VP],
+    "oomb_attn_backward": [VP, I, VP, VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP],
+    "oomb_set_kernel_policy": [VP, I],
+    "oomb_pagetable_create": [I, I, I, I, I, I, C.POINTER(VP)],
+    "oomb_pagetable_destroy": [VP],
+    "oomb_pagetable_append": [VP, I, I64, C.POINTER(I64), C.POINTER(I64)],
+    "oomb_pagetable_scatter": [VP, I, VP, I],
+    "oomb_pagetable_reset": [VP],
+    "oomb_pagetable_n_pages": [VP, I, C.POINTER(I)],
+    "oomb_pagetable_get": [VP, I, VP],
+    "oomb_pagetable_set_tier": [VP, I, I, I],
+    "oomb_pagetable_memory_report": [VP, C.POINTER(OombMemoryReport)],
+    "oomb_debug_tc_gemm": [I, VP, VP, VP, I, I, I, VP],
+}
+_RESTYPE = {"oomb_last_error": C.c_char_p, "oomb_kernel_launches": C.c_int64}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load liboomb.so once; raise loudly when it is absent (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} not found: build it with `python -m paper_2602_02108_b200.build` "
+                "(the OOMB operators have no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, args in _PROTOS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = _RESTYPE.get(name, C.c_int)
+        _lib = L
+    return _lib
+
+
+def call(name: str, *args) -> None:
+    L = lib()
+    rc = getattr(L, name)(*args)
+    if rc != 0:
+        raise_for_status(rc, L.oomb_last_error().decode(errors="replace"))
+
+
+def kernel_launches() -> int:
+    return int(lib().oomb_kernel_launches())
+
+
+def exported_symbols() -> list[str]:
+    return list(_PROTOS)

@@ -1,0 +1,674 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// SIMT kernels of the hot path: page append + K_avg, page mean keys,
+// gather / scatter-add of page data, lazy gradient-page initialisation,
+// exact page scoring (vote), top-k page selection, and the SIMT paged
+// attention forward / backward used for fp32 mode (the 1e-5 parity mode) and
+// for shapes the tcgen05 kernels do not cover.
+//
+// Pool layout (device, per slot): K, V  [Hkv][P][hd] (pool dtype);
+// gradient pool dK, dV [Hkv][P][hd] fp32. Page tables map logical page ->
+// slot per layer (d_kvslot / d_gslot, -1 = none).
+
+#include <cub/block/block_scan.cuh>
+
+#include "oomb_internal.h"
+#include "ptx.cuh"
+
+namespace oomb {
+
+std::atomic<int64_t> g_kernel_launches{0};
+
+void check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(OOMB_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+    count_launch();
+}
+
+template <typename T>
+__device__ __forceinline__ float to_f(T x);
+template <>
+__device__ __forceinline__ float to_f<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+template <typename T>
+__device__ __forceinline__ T from_f(float x);
+template <>
+__device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ int valid_in_page(int64_t filled, int pid, int P) {
+    int64_t v = filled - static_cast<int64_t>(pid) * P;
+    return static_cast<int>(v < 0 ? 0 : (v > P ? P : v));
+}
+
+// ===========================================================================
+// append_chunk + K_avg  (paged_kv.hpp:73-108)
+// One thread per (page touched, h, d): copies the page's new rows in order and
+// accumulates kavg_sum in append order -> bit-identical fp32 sums.
+// ===========================================================================
+template <typename T>
+__global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, int64_t rows, int64_t filled,
+                              int P, int Hkv, int hd, int first_page, NewSlots ns, int32_t* __restrict__ kvslot,
+                              T* __restrict__ kpool, T* __restrict__ vpool, float* __restrict__ ksum,
+                              int32_t* __restrict__ kcnt) {
+    const int re = Hkv * hd;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int pg = first_page + blockIdx.y;
+    if (blockIdx.x == 0 && blockIdx.y == 0) {
+        for (int i = threadIdx.x; i < ns.n; i += blockDim.x) kvslot[ns.first_page + i] = ns.slot[i];
+    }
+    if (e >= re) return;
+    const bool is_new = pg >= ns.first_page && pg < ns.first_page + ns.n;
+    const int slot = is_new ? ns.slot[pg - ns.first_page] : kvslot[pg];
+    const int h = e / hd, d = e - (e / hd) * hd;
+    const int64_t s0 = max(filled, static_cast<int64_t>(pg) * P);
+    const int64_t s1 = min(filled + rows, static_cast<int64_t>(pg + 1) * P);
+    float sum = is_new ? 0.f : ksum[static_cast<int64_t>(pg) * re + e];
+    for (int64_t s = s0; s < s1; ++s) {
+        const int64_t r = s - filled;
+        const int off = static_cast<int>(s - static_cast<int64_t>(pg) * P);
+        const T kv = k[r * re + e];
+        const T vv = v[r * re + e];
+        const size_t dst = ((static_cast<size_t>(slot) * Hkv + h) * P + off) * hd + d;
+        kpool[dst] = kv;
+        vpool[dst] = vv;
+        sum = __fadd_rn(sum, to_f(kv));
+    }
+    ksum[static_cast<int64_t>(pg) * re + e] = sum;
+    if (e == 0) kcnt[pg] = (is_new ? 0 : kcnt[pg]) + static_cast<int>(s1 - s0);
+}
+
+void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_t filled_before, int P, int Hkv,
+                   int hd, int first_page, int n_pages_touched, const NewSlots& ns, int32_t* d_kvslot_layer,
+                   void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, cudaStream_t st) {
+    if (rows <= 0 || n_pages_touched <= 0) return;
+    const int re = Hkv * hd;
+    dim3 grid((re + 127) / 128, n_pages_touched);
+    if (dtype == OOMB_BF16)
+        append_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), rows, filled_before, P, Hkv,
+            hd, first_page, ns, d_kvslot_layer, static_cast<__nv_bfloat16*>(kpool), static_cast<__nv_bfloat16*>(vpool),
+            kavg_sum_layer, kavg_cnt_layer);
+    else
+        append_kernel<float><<<grid, 128, 0, st>>>(static_cast<const float*>(k), static_cast<const float*>(v), rows,
+                                                   filled_before, P, Hkv, hd, first_page, ns, d_kvslot_layer,
+                                                   static_cast<float*>(kpool), static_cast<float*>(vpool),
+                                                   kavg_sum_layer, kavg_cnt_layer);
+    check_launch("append_kernel");
+}
+
+// ===========================================================================
+// page_mean_keys (paged_kv.hpp:170-183): sum * (1/count), IEEE ops.
+// ===========================================================================
+__global__ void mean_keys_kernel(const float* __restrict__ sum, const int32_t* __restrict__ cnt, int n, int re,
+                                 float* __restrict__ out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<int64_t>(n) * re) return;
+    const int p = static_cast<int>(i / re);
+    const float inv = __fdiv_rn(1.0f, static_cast<float>(cnt[p]));
+    out[i] = __fmul_rn(sum[i], inv);
+}
+
+void launch_mean_keys(const float* kavg_sum_layer, const int32_t* kavg_cnt_layer, int n, int row_elems, float* out,
+                      cudaStream_t st) {
+    if (n <= 0) return;
+    const int64_t tot = static_cast<int64_t>(n) * row_elems;
+    mean_keys_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(kavg_sum_layer, kavg_cnt_layer, n,
+                                                                              row_elems, out);
+    check_launch("mean_keys_kernel");
+}
+
+// ===========================================================================
+// gather_pages / gather_grad_pages (paged_kv.hpp:118-130, 314-347)
+// Output in the reference layout [n*P][Hkv][hd]; unfilled slots zero + masked.
+// ===========================================================================
+template <typename T, typename TO>
+__global__ void gather_kernel(const int32_t* __restrict__ ids, int n, const int32_t* __restrict__ slotmap,
+                              const T* __restrict__ pk, const T* __restrict__ pv, int64_t filled, int P, int Hkv,
+                              int hd, int grads, TO* __restrict__ ko, TO* __restrict__ vo, uint8_t* __restrict__ valid,
+                              int* err) {
+    const int re = Hkv * hd;
+    const int64_t total = static_cast<int64_t>(n) * P * re;
+    for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(idx / (static_cast<int64_t>(P) * re));
+        const int rem = static_cast<int>(idx - static_cast<int64_t>(i) * P * re);
+        const int s = rem / re, e = rem - (rem / re) * re;
+        const int h = e / hd, d = e - (e / hd) * hd;
+        const int pid = ids[i];
+        const int vs = valid_in_page(filled, pid, P);
+        const int slot = slotmap[pid];
+        float kv = 0.f, vv = 0.f;
+        if (slot < 0) {
+            if (!grads) atomicOr(err, DERR_NOT_RESIDENT);
+        } else if (s < vs) {
+            const size_t src = ((static_cast<size_t>(slot) * Hkv + h) * P + s) * hd + d;
+            kv = to_f(pk[src]);
+            vv = to_f(pv[src]);
+        }
+        ko[idx] = from_f<TO>(kv);
+        vo[idx] = from_f<TO>(vv);
+        if (e == 0) valid[static_cast<int64_t>(i) * P + s] = s < vs ? 1 : 0;
+    }
+}
+
+void launch_gather(int dtype, int grads, const int32_t* d_ids, int n, const int32_t* d_slot_layer, const void* pk,
+                   const void* pv, int64_t filled, int P, int Hkv, int hd, void* k_out, void* v_out,
+                   uint8_t* valid_out, int* d_err, cudaStream_t st) {
+    if (n <= 0) return;
+    const int64_t total = static_cast<int64_t>(n) * P * Hkv * hd;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 32));
+    if (grads) {
+        gather_kernel<float, float><<<blocks, 256, 0, st>>>(d_ids, n, d_slot_layer, static_cast<const float*>(pk),
+                                                            static_cast<const float*>(pv), filled, P, Hkv, hd, 1,
+                                                            static_cast<float*>(k_out), static_cast<float*>(v_out),
+                                                            valid_out, d_err);
+    } else if (dtype == OOMB_BF16) {
+        gather_kernel<__nv_bfloat16, __nv_bfloat16><<<blocks, 256, 0, st>>>(
+            d_ids, n, d_slot_layer, static_cast<const __nv_bfloat16*>(pk), static_cast<const __nv_bfloat16*>(pv),
+            filled, P, Hkv, hd, 0, static_cast<__nv_bfloat16*>(k_out), static_cast<__nv_bfloat16*>(v_out), valid_out,
+            d_err);
+    } else {
+        gather_kernel<float, float><<<blocks, 256, 0, st>>>(d_ids, n, d_slot_layer, static_cast<const float*>(pk),
+                                                            static_cast<const float*>(pv), filled, P, Hkv, hd, 0,
+                                                            static_cast<float*>(k_out), static_cast<float*>(v_out),
+                                                            valid_out, d_err);
+    }
+    check_launch("gather_kernel");
+}
+
+// ===========================================================================
+// scatter_add_grads (paged_kv.hpp:135-164): valid slots only, in place.
+// ===========================================================================
+__global__ void scatter_kernel(const int32_t* __restrict__ ids, int n, const int32_t* __restrict__ gslot,
+                               float* __restrict__ gk, float* __restrict__ gv, const float* __restrict__ dk,
+                               const float* __restrict__ dv, int64_t filled, int P, int Hkv, int hd, int* err) {
+    const int re = Hkv * hd;
+    const int64_t total = static_cast<int64_t>(n) * P * re;
+    for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(idx / (static_cast<int64_t>(P) * re));
+        const int rem = static_cast<int>(idx - static_cast<int64_t>(i) * P * re);
+        const int s = rem / re, e = rem - (rem / re) * re;
+        const int h = e / hd, d = e - (e / hd) * hd;
+        const int pid = ids[i];
+        if (s >= valid_in_page(filled, pid, P)) continue;
+        const int g = gslot[pid];
+        if (g < 0) {
+            atomicOr(err, DERR_NOT_RESIDENT);
+            continue;
+        }
+        const size_t dst = ((static_cast<size_t>(g) * Hkv + h) * P + s) * hd + d;
+        atomicAdd(gk + dst, dk[idx]);
+        atomicAdd(gv + dst, dv[idx]);
+    }
+}
+
+void launch_scatter(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, float* gk, float* gv,
+                    const float* dk, const float* dv, int64_t filled, int P, int Hkv, int hd, int* d_err,
+                    cudaStream_t st) {
+    if (n <= 0) return;
+    const int64_t total = static_cast<int64_t>(n) * P * Hkv * hd;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 32));
+    scatter_kernel<<<blocks, 256, 0, st>>>(d_ids, n, d_gslot_layer, gk, gv, dk, dv, filled, P, Hkv, hd, d_err);
+    check_launch("scatter_kernel");
+}
+
+// Lazy gradient pages: publish slot + zero (paged_kv.hpp:148-153).
+__global__ void grad_init_kernel(const int32_t* __restrict__ pages, const int32_t* __restrict__ slots, int n,
+                                 int32_t* __restrict__ gslot, float* __restrict__ gk, float* __restrict__ gv,
+                                 int64_t page_elems) {
+    const int i = blockIdx.y;
+    if (i >= n) return;
+    const int64_t base = static_cast<int64_t>(slots[i]) * page_elems;
+    float4* pk = reinterpret_cast<float4*>(gk + base);
+    float4* pv = reinterpret_cast<float4*>(gv + base);
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < page_elems / 4;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        pk[j] = z;
+        pv[j] = z;
+    }
+    if (pages != nullptr && blockIdx.x == 0 && threadIdx.x == 0) gslot[pages[i]] = slots[i];
+}
+
+void launch_grad_init(const int32_t* d_pages, const int32_t* d_slots, int n, int32_t* d_gslot_layer, float* gk,
+                      float* gv, int64_t page_elems, cudaStream_t st) {
+    if (n <= 0) return;
+    dim3 grid(static_cast<unsigned>(std::min<int64_t>((page_elems / 4 + 255) / 256, 16)), n);
+    grad_init_kernel<<<grid, 256, 0, st>>>(d_pages, d_slots, n, d_gslot_layer, gk, gv, page_elems);
+    check_launch("grad_init_kernel");
+}
+
+void launch_zero_slots(const int32_t* d_slots, int n, float* gk, float* gv, int64_t page_elems, cudaStream_t st) {
+    launch_grad_init(nullptr, d_slots, n, nullptr, gk, gv, page_elems, st);
+}
+
+// ===========================================================================
+// score_pages (attention.hpp:32-67), exact SIMT form.
+// Pass 1: per (token, head) row max and 1/sum over candidates (warp per row).
+// Pass 2: per (query page, candidate) thread, sum over tokens asc then heads asc
+//         — the reference's accumulation order for the vote.
+// Dot products use the reference's sequential order with no FMA contraction.
+// ===========================================================================
+template <typename T>
+__device__ __forceinline__ float dot_seq(const T* __restrict__ q, const float* __restrict__ k, int hd) {
+    float dot = 0.f;
+    for (int j = 0; j < hd; ++j) dot = __fadd_rn(dot, __fmul_rn(to_f(q[j]), k[j]));
+    return dot;
+}
+
+template <typename T>
+__global__ void score_stats_kernel(const T* __restrict__ q, int64_t tokens, int Hq, int hd,
+                                   const float* __restrict__ kavg, int64_t n, int Hkv, float scale,
+                                   float2* __restrict__ stats) {
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= tokens * Hq) return;
+    const int h = static_cast<int>(row % Hq);
+    const int kvh = h / (Hq / Hkv);
+    const T* qv = q + row * hd;
+    float mx = -INFINITY;
+    for (int64_t p = lane; p < n; p += 32) {
+        const float raw = __fmul_rn(dot_seq(qv, kavg + (p * Hkv + kvh) * hd, hd), scale);
+        mx = fmaxf(mx, raw);
+    }
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int64_t p = lane; p < n; p += 32) {
+        const float raw = __fmul_rn(dot_seq(qv, kavg + (p * Hkv + kvh) * hd, hd), scale);
+        sum += expf(raw - mx);
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) stats[row] = make_float2(mx, __fdiv_rn(1.0f, sum));
+}
+
+template <typename T>
+__global__ void score_vote_kernel(const T* __restrict__ q, int64_t tokens, int Hq, int hd,
+                                  const float* __restrict__ kavg, int64_t n, int Hkv, int P, float scale,
+                                  const float2* __restrict__ stats, float* __restrict__ vote) {
+    extern __shared__ float qs[];  // [hd]
+    const int qp = blockIdx.y;
+    const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int group = Hq / Hkv;
+    float acc = 0.f;
+    const int64_t t0 = static_cast<int64_t>(qp) * P;
+    const int64_t t1 = min(tokens, t0 + P);
+    for (int64_t t = t0; t < t1; ++t) {
+        for (int h = 0; h < Hq; ++h) {
+            __syncthreads();
+            for (int j = threadIdx.x; j < hd; j += blockDim.x) qs[j] = to_f(q[(t * Hq + h) * hd + j]);
+            __syncthreads();
+            if (p < n) {
+                const float* kv = kavg + (p * Hkv + h / group) * hd;
+                float dot = 0.f;
+                for (int j = 0; j < hd; ++j) dot = __fadd_rn(dot, __fmul_rn(qs[j], kv[j]));
+                const float2 st = stats[t * Hq + h];
+                acc = __fadd_rn(acc, __fmul_rn(expf(__fmul_rn(dot, scale) - st.x), st.y));
+            }
+        }
+    }
+    if (p < n) vote[static_cast<int64_t>(qp) * n + p] = acc;
+}
+
+void launch_score_simt(int dtype, const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, int64_t n,
+                       int Hkv, int P, float scale, float* vote, float* stats_scratch, cudaStream_t st) {
+    const int64_t rows = tokens * Hq;
+    const int m = static_cast<int>((tokens + P - 1) / P);
+    float2* stats = reinterpret_cast<float2*>(stats_scratch);
+    dim3 g1(static_cast<unsigned>((rows + 7) / 8));
+    dim3 g2(static_cast<unsigned>((n + 127) / 128), m);
+    if (dtype == OOMB_BF16) {
+        auto qq = static_cast<const __nv_bfloat16*>(q);
+        score_stats_kernel<<<g1, 256, 0, st>>>(qq, tokens, Hq, hd, k_avg, n, Hkv, scale, stats);
+        check_launch("score_stats_kernel");
+        score_vote_kernel<<<g2, 128, hd * sizeof(float), st>>>(qq, tokens, Hq, hd, k_avg, n, Hkv, P, scale, stats,
+                                                               vote);
+    } else {
+        auto qq = static_cast<const float*>(q);
+        score_stats_kernel<<<g1, 256, 0, st>>>(qq, tokens, Hq, hd, k_avg, n, Hkv, scale, stats);
+        check_launch("score_stats_kernel");
+        score_vote_kernel<<<g2, 128, hd * sizeof(float), st>>>(qq, tokens, Hq, hd, k_avg, n, Hkv, P, scale, stats,
+                                                               vote);
+    }
+    check_launch("score_vote_kernel");
+}
+
+// ===========================================================================
+// select_topk_row (attention.hpp:71-96): per row, the k largest scores with ties
+// to the lower id, emitted ascending. One CTA per row: 4-pass MSB radix select of
+// the k-th largest order-preserving key, then id-ordered compaction in which the
+// threshold-equal elements are admitted lowest-id first. Exact and deterministic.
+// ===========================================================================
+__device__ __forceinline__ uint32_t order_key(float f) {
+    uint32_t u = __float_as_uint(f);
+    if (f == 0.f) u = 0u;  // the reference compares doubles: -0 == +0 (tie -> id order)
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+constexpr int kTopkThreads = 1024;
+
+__global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restrict__ vote, int m, int n, int k,
+                                                            int32_t* __restrict__ off, int32_t* __restrict__ ids) {
+    using Scan = cub::BlockScan<int, kTopkThreads>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t s_prefix, s_mask;
+    __shared__ int s_remaining;
+    const int row = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int kk = k < n ? k : n;
+    if (tid == 0) {
+        off[row] = row * kk;
+        if (row == m - 1) off[m] = m * kk;
+    }
+    int32_t* out = ids + static_cast<int64_t>(row) * kk;
+    const float* s = vote + static_cast<int64_t>(row) * n;
+    if (kk == n) {
+        for (int i = tid; i < n; i += kTopkThreads) out[i] = i;
+        return;
+    }
+    if (kk == 0) return;
+    if (tid == 0) {
+        s_prefix = 0;
+        s_mask = 0;
+        s_remaining = kk;
+    }
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        if (tid < 256) hist[tid] = 0;
+        __syncthreads();
+        const uint32_t prefix = s_prefix, mask = s_mask;
+        for (int i = tid; i < n; i += kTopkThreads) {
+            const uint32_t key = order_key(s[i]);
+            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int rem = s_remaining;
+            uint32_t cum = 0;
+            int chosen = 0;
+            for (int b = 255; b >= 0; --b) {
+                if (cum + hist[b] >= static_cast<uint32_t>(rem)) {
+                    chosen = b;
+                    rem -= static_cast<int>(cum);
+                    break;
+                }
+                cum += hist[b];
+            }
+            s_remaining = rem;
+            s_prefix = prefix | (static_cast<uint32_t>(chosen) << shift);
+            s_mask = mask | (255u << shift);
+        }
+        __syncthreads();
+    }
+    const uint32_t thr = s_prefix;
+    const int take_eq = s_remaining;  // threshold-equal elements to admit, lowest ids first
+    const int ipt = (n + kTopkThreads - 1) / kTopkThreads;
+    const int i0 = min(n, tid * ipt), i1 = min(n, i0 + ipt);
+    int n_eq = 0;
+    for (int i = i0; i < i1; ++i) n_eq += order_key(s[i]) == thr;
+    int eq_before;
+    Scan(scan_tmp).ExclusiveSum(n_eq, eq_before);
+    __syncthreads();
+    int n_sel = 0;
+    {
+        int r = eq_before;
+        for (int i = i0; i < i1; ++i) {
+            const uint32_t key = order_key(s[i]);
+            if (key > thr) ++n_sel;
+            else if (key == thr) n_sel += (r++ < take_eq);
+        }
+    }
+    int pos;
+    Scan(scan_tmp).ExclusiveSum(n_sel, pos);
+    int r = eq_before;
+    for (int i = i0; i < i1; ++i) {
+        const uint32_t key = order_key(s[i]);
+        bool take = key > thr;
+        if (key == thr) take = (r++ < take_eq);
+        if (take) out[pos++] = i;
+    }
+}
+
+void launch_topk(const float* vote, int m, int n, int k, int32_t* sel_off, int32_t* sel_ids, cudaStream_t st) {
+    if (m <= 0) return;
+    topk_kernel<<<m, kTopkThreads, 0, st>>>(vote, m, n, k, sel_off, sel_ids);
+    check_launch("topk_kernel");
+}
+
+// select_all / select_recent broadcast to m query pages: ids first..first+count-1.
+__global__ void fill_csr_kernel(int32_t* off, int32_t* ids, int m, int first, int count) {
+    const int qp = blockIdx.x;
+    if (threadIdx.x == 0) {
+        off[qp] = qp * count;
+        if (qp == m - 1) off[m] = m * count;
+    }
+    for (int i = threadIdx.x; i < count; i += blockDim.x) ids[static_cast<int64_t>(qp) * count + i] = first + i;
+}
+
+void launch_fill_csr_all(int32_t* off, int32_t* ids, int m, int first, int count, cudaStream_t st) {
+    if (m <= 0) return;
+    fill_csr_kernel<<<m, 256, 0, st>>>(off, ids, m, first, count);
+    check_launch("fill_csr_kernel");
+}
+
+// ===========================================================================
+// SIMT paged attention (attention.hpp:156-293): one warp per (token, q-head).
+// Forward = the reference's OnlineRow over past valid slots in list order, then
+// the chunk's causal prefix. Backward rebuilds p from the saved lse and D from
+// the saved O; dK/dV go to the fp32 gradient pool / dk_cur, dv_cur by atomics.
+// ===========================================================================
+constexpr int kMaxLaneElems = 8;  // hd <= 256
+
+template <typename T>
+__global__ void attn_fwd_simt_kernel(AttnGeom g, const T* __restrict__ q, const int32_t* __restrict__ sel_off,
+                                     const int32_t* __restrict__ sel_ids, const int32_t* __restrict__ kvslot,
+                                     const T* __restrict__ kpool, const T* __restrict__ vpool,
+                                     const T* __restrict__ k_cur, const T* __restrict__ v_cur, T* __restrict__ out,
+                                     float* __restrict__ lse, int* err) {
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= static_cast<int64_t>(g.C) * g.Hq) return;
+    const int t = static_cast<int>(row / g.Hq), h = static_cast<int>(row % g.Hq);
+    const int kvh = h / g.group, qp = t / g.P, hd = g.hd;
+    const int nd = (hd + 31) / 32;
+    float qv[kMaxLaneElems], acc[kMaxLaneElems];
+#pragma unroll
+    for (int i = 0; i < kMaxLaneElems; ++i) {
+        const int d = lane + 32 * i;
+        qv[i] = (i < nd && d < hd) ? to_f(q[row * hd + d]) : 0.f;
+        acc[i] = 0.f;
+    }
+    float m = -INFINITY, l = 0.f;
+    auto visit = [&](const T* kr, const T* vr) {
+        float part = 0.f;
+#pragma unroll
+        for (int i = 0; i < kMaxLaneElems; ++i) {
+            const int d = lane + 32 * i;
+            if (i < nd && d < hd) part += qv[i] * to_f(kr[d]);
+        }
+        const float logit = warp_sum(part) * g.scale;
+        if (logit > m) {
+            const float corr = (l == 0.f) ? 0.f : expf(m - logit);
+#pragma unroll
+            for (int i = 0; i < kMaxLaneElems; ++i) acc[i] *= corr;
+            l *= corr;
+            m = logit;
+        }
+        const float w = expf(logit - m);
+        l += w;
+#pragma unroll
+        for (int i = 0; i < kMaxLaneElems; ++i) {
+            const int d = lane + 32 * i;
+            if (i < nd && d < hd) acc[i] += w * to_f(vr[d]);
+        }
+    };
+    for (int idx = sel_off[qp]; idx < sel_off[qp + 1]; ++idx) {
+        const int pid = sel_ids[idx];
+        if (pid < 0 || pid >= g.max_pages) {
+            if (lane == 0) atomicOr(err, DERR_BAD_ID);
+            continue;
+        }
+        const int slot = kvslot[pid];
+        if (slot < 0) {
+            if (lane == 0) atomicOr(err, DERR_NOT_RESIDENT);
+            continue;
+        }
+        const int vs = valid_in_page(g.filled, pid, g.P);
+        const size_t base = (static_cast<size_t>(slot) * g.Hkv + kvh) * g.P * hd;
+        for (int s = 0; s < vs; ++s) visit(kpool + base + static_cast<size_t>(s) * hd, vpool + base + static_cast<size_t>(s) * hd);
+    }
+    for (int s = 0; s <= t; ++s) {
+        const size_t o = (static_cast<size_t>(s) * g.Hkv + kvh) * hd;
+        visit(k_cur + o, v_cur + o);
+    }
+    const float inv = 1.f / l;
+#pragma unroll
+    for (int i = 0; i < kMaxLaneElems; ++i) {
+        const int d = lane + 32 * i;
+        if (i < nd && d < hd) out[row * hd + d] = from_f<T>(acc[i] * inv);
+    }
+    if (lane == 0) lse[row] = m + logf(l);
+}
+
+template <typename T>
+__global__ void attn_bwd_simt_kernel(AttnGeom g, const T* __restrict__ dout, const T* __restrict__ q,
+                                     const int32_t* __restrict__ sel_off, const int32_t* __restrict__ sel_ids,
+                                     const int32_t* __restrict__ kvslot, const int32_t* __restrict__ gslot,
+                                     const T* __restrict__ kpool, const T* __restrict__ vpool, float* __restrict__ gk,
+                                     float* __restrict__ gv, const T* __restrict__ k_cur, const T* __restrict__ v_cur,
+                                     const T* __restrict__ o, const float* __restrict__ lse, float* __restrict__ dq,
+                                     float* __restrict__ dk_cur, float* __restrict__ dv_cur, int* err) {
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= static_cast<int64_t>(g.C) * g.Hq) return;
+    const int t = static_cast<int>(row / g.Hq), h = static_cast<int>(row % g.Hq);
+    const int kvh = h / g.group, qp = t / g.P, hd = g.hd;
+    const int nd = (hd + 31) / 32;
+    float qv[kMaxLaneElems], dov[kMaxLaneElems], dqa[kMaxLaneElems];
+    float dpart = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMaxLaneElems; ++i) {
+        const int d = lane + 32 * i;
+        const bool ok = i < nd && d < hd;
+        qv[i] = ok ? to_f(q[row * hd + d]) : 0.f;
+        dov[i] = ok ? to_f(dout[row * hd + d]) : 0.f;
+        dpart += ok ? dov[i] * to_f(o[row * hd + d]) : 0.f;
+        dqa[i] = 0.f;
+    }
+    const float D = warp_sum(dpart);
+    const float L = lse[row];
+    auto visit = [&](const T* kr, const T* vr, float* dkr, float* dvr) {
+        float p1 = 0.f, p2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < kMaxLaneElems; ++i) {
+            const int d = lane + 32 * i;
+            if (i < nd && d < hd) {
+                p1 += qv[i] * to_f(kr[d]);
+                p2 += dov[i] * to_f(vr[d]);
+            }
+        }
+        const float dot = warp_sum(p1);
+        const float dpv = warp_sum(p2);
+        const float p = expf(dot * g.scale - L);
+        const float dlogit = p * (dpv - D) * g.scale;
+#pragma unroll
+        for (int i = 0; i < kMaxLaneElems; ++i) {
+            const int d = lane + 32 * i;
+            if (i < nd && d < hd) {
+                dqa[i] += dlogit * to_f(kr[d]);
+                atomicAdd(dkr + d, dlogit * qv[i]);
+                atomicAdd(dvr + d, p * dov[i]);
+            }
+        }
+    };
+    for (int idx = sel_off[qp]; idx < sel_off[qp + 1]; ++idx) {
+        const int pid = sel_ids[idx];
+        if (pid < 0 || pid >= g.max_pages) {
+            if (lane == 0) atomicOr(err, DERR_BAD_ID);
+            continue;
+        }
+        const int slot = kvslot[pid], gs = gslot[pid];
+        if (slot < 0 || gs < 0) {
+            if (lane == 0) atomicOr(err, DERR_NOT_RESIDENT);
+            continue;
+        }
+        const int vs = valid_in_page(g.filled, pid, g.P);
+        const size_t base = (static_cast<size_t>(slot) * g.Hkv + kvh) * g.P * hd;
+        const size_t gbase = (static_cast<size_t>(gs) * g.Hkv + kvh) * g.P * hd;
+        for (int s = 0; s < vs; ++s) {
+            const size_t so = static_cast<size_t>(s) * hd;
+            visit(kpool + base + so, vpool + base + so, gk + gbase + so, gv + gbase + so);
+        }
+    }
+    for (int s = 0; s <= t; ++s) {
+        const size_t so = (static_cast<size_t>(s) * g.Hkv + kvh) * hd;
+        visit(k_cur + so, v_cur + so, dk_cur + so, dv_cur + so);
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxLaneElems; ++i) {
+        const int d = lane + 32 * i;
+        if (i < nd && d < hd) dq[row * hd + d] = dqa[i];
+    }
+}
+
+void launch_attn_fwd_simt(int dtype, const AttnGeom& g, const void* q, const int32_t* sel_off, const int32_t* sel_ids,
+                          const int32_t* d_kvslot_layer, const void* kpool, const void* vpool, const void* k_cur,
+                          const void* v_cur, void* out, float* lse, int* d_err, cudaStream_t st) {
+    const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
+    const unsigned blocks = static_cast<unsigned>((rows + 3) / 4);
+    if (dtype == OOMB_BF16) {
+        using T = __nv_bfloat16;
+        attn_fwd_simt_kernel<T><<<blocks, 128, 0, st>>>(g, static_cast<const T*>(q), sel_off, sel_ids, d_kvslot_layer,
+                                                        static_cast<const T*>(kpool), static_cast<const T*>(vpool),
+                                                        static_cast<const T*>(k_cur), static_cast<const T*>(v_cur),
+                                                        static_cast<T*>(out), lse, d_err);
+    } else {
+        using T = float;
+        attn_fwd_simt_kernel<T><<<blocks, 128, 0, st>>>(g, static_cast<const T*>(q), sel_off, sel_ids, d_kvslot_layer,
+                                                        static_cast<const T*>(kpool), static_cast<const T*>(vpool),
+                                                        static_cast<const T*>(k_cur), static_cast<const T*>(v_cur),
+                                                        static_cast<T*>(out), lse, d_err);
+    }
+    check_launch("attn_fwd_simt_kernel");
+}
+
+void launch_attn_bwd_simt(int dtype, const AttnGeom& g, const void* dout, const void* q, const int32_t* sel_off,
+                          const int32_t* sel_ids, const int32_t* d_kvslot_layer, const int32_t* d_gslot_layer,
+                          const void* kpool, const void* vpool, float* gkpool, float* gvpool, const void* k_cur,
+                          const void* v_cur, const void* out, const float* lse, float* dq, float* dk_cur,
+                          float* dv_cur, int* d_err, cudaStream_t st) {
+    const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
+    const unsigned blocks = static_cast<unsigned>((rows + 3) / 4);
+    if (dtype == OOMB_BF16) {
+        using T = __nv_bfloat16;
+        attn_bwd_simt_kernel<T><<<blocks, 128, 0, st>>>(
+            g, static_cast<const T*>(dout), static_cast<const T*>(q), sel_off, sel_ids, d_kvslot_layer, d_gslot_layer,
+            static_cast<const T*>(kpool), static_cast<const T*>(vpool), gkpool, gvpool, static_cast<const T*>(k_cur),
+            static_cast<const T*>(v_cur), static_cast<const T*>(out), lse, dq, dk_cur, dv_cur, d_err);
+    } else {
+        using T = float;
+        attn_bwd_simt_kernel<T><<<blocks, 128, 0, st>>>(
+            g, static_cast<const T*>(dout), static_cast<const T*>(q), sel_off, sel_ids, d_kvslot_layer, d_gslot_layer,
+            static_cast<const T*>(kpool), static_cast<const T*>(vpool), gkpool, gvpool, static_cast<const T*>(k_cur),
+            static_cast<const T*>(v_cur), static_cast<const T*>(out), lse, dq, dk_cur, dv_cur, d_err);
+    }
+    check_launch("attn_bwd_simt_kernel");
+}
+
+}  // namespace oomb

@@ -1,0 +1,899 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Host runtime behind include/oomb.h: the device page pool, the host mirror of
+// the reference page table (arena ids, LIFO free list, lazy gradient pages),
+// selections (device CSR + pinned host mirror), and dispatch to the sm_100a
+// kernels. Every entry point catches and converts exceptions to oomb_status.
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "oomb_internal.h"
+
+namespace oomb {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return OOMB_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return OOMB_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return OOMB_ERROR;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// cuTensorMapEncodeTiled through the runtime's driver entry point.
+// ---------------------------------------------------------------------------
+CUresult encode_tensor_map(CUtensorMap* map, CUtensorMapDataType dt, uint32_t rank, void* base, const uint64_t* dims,
+                           const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz) {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) throw Error(OOMB_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    uint32_t estr[5] = {1, 1, 1, 1, 1};
+    return fn(map, dt, rank, base, dims, strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
+// ---------------------------------------------------------------------------
+// Host mirror of PagedCache's page table (paged_kv.hpp:41-356): arena ids are
+// allocated exactly like the reference (LIFO free list; k then v per new page
+// at append; gk then gv lazily at first scatter; reset frees k, v, gk, gv per
+// page per layer) so page tables compare bit-exactly.
+// ---------------------------------------------------------------------------
+struct PageTable {
+    struct Entry {
+        int32_t k = -1, v = -1, gk = -1, gv = -1;
+        uint8_t tier = 0;  // 0 device, 1 host
+    };
+    int n_layers, P, kvh, hd, kv_elem, grad_elem;
+    std::vector<std::vector<Entry>> pages;
+    std::vector<int64_t> filled;
+    int64_t arena_n = 0;
+    std::vector<int32_t> free_list;
+
+    PageTable(int L, int P_, int kvh_, int hd_, int kve, int ge)
+        : n_layers(L), P(P_), kvh(kvh_), hd(hd_), kv_elem(kve), grad_elem(ge), pages(L), filled(L, 0) {}
+
+    void check_layer(int layer) const {
+        OOMB_REQUIRE(layer >= 0 && layer < n_layers, OOMB_SHAPE_ERROR, "cache: layer out of range");
+    }
+    int32_t alloc() {  // alloc_page_ paged_kv.hpp:280-288
+        if (!free_list.empty()) {
+            const int32_t id = free_list.back();
+            free_list.pop_back();
+            return id;
+        }
+        return static_cast<int32_t>(arena_n++);
+    }
+    // append_chunk's page bookkeeping (paged_kv.hpp:73-108). Returns [first_new, n_new).
+    void append(int layer, int64_t rows, int64_t* b, int64_t* e, int* first_new, int* n_new) {
+        check_layer(layer);
+        OOMB_REQUIRE(rows >= 0, OOMB_SHAPE_ERROR, "append_chunk: expected [rows x kvh x hd] K/V of equal shape");
+        auto& st = pages[layer];
+        *b = filled[layer];
+        *e = filled[layer] + rows;
+        *first_new = static_cast<int>(st.size());
+        *n_new = 0;
+        if (rows > 0) {
+            const int64_t last_page = (filled[layer] + rows - 1) / P;
+            while (static_cast<int64_t>(st.size()) <= last_page) {
+                Entry en;
+                en.k = alloc();
+                en.v = alloc();
+                st.push_back(en);
+                ++*n_new;
+            }
+        }
+        filled[layer] += rows;
+    }
+    void check_ids(int layer, const int32_t* ids, int n, bool enforce, const char* op) const {
+        check_layer(layer);
+        const auto& st = pages[layer];
+        for (int i = 0; i < n; ++i) {
+            OOMB_REQUIRE(ids[i] >= 0 && ids[i] < static_cast<int32_t>(st.size()), OOMB_SHAPE_ERROR,
+                         std::string(op) + ": page id out of range");
+            OOMB_REQUIRE(!enforce || st[ids[i]].tier == 0, OOMB_RESIDENCY_ERROR,
+                         std::string(op) + ": page " + std::to_string(ids[i]) + " of layer " + std::to_string(layer) +
+                             " is not device-resident");
+        }
+    }
+    // scatter_add_grads' lazy allocation (paged_kv.hpp:148-153), in call order.
+    std::vector<int32_t> scatter(int layer, const int32_t* ids, int n) {
+        std::vector<int32_t> fresh;
+        auto& st = pages[layer];
+        for (int i = 0; i < n; ++i) {
+            Entry& en = st[ids[i]];
+            if (en.gk < 0) {
+                en.gk = alloc();
+                en.gv = alloc();
+                fresh.push_back(ids[i]);
+            }
+        }
+        return fresh;
+    }
+    void reset() {  // paged_kv.hpp:227-242
+        for (int l = 0; l < n_layers; ++l) {
+            for (const auto& en : pages[l]) {
+                free_list.push_back(en.k);
+                free_list.push_back(en.v);
+                if (en.gk >= 0) {
+                    free_list.push_back(en.gk);
+                    free_list.push_back(en.gv);
+                }
+            }
+            pages[l].clear();
+            filled[l] = 0;
+        }
+    }
+    oomb_memory_report report() const {  // paged_kv.hpp:185-197
+        oomb_memory_report r{};
+        const uint64_t pe = static_cast<uint64_t>(P) * kvh * hd;
+        for (const auto& st : pages)
+            for (const auto& en : st) {
+                r.pages += 1;
+                if (en.tier == 0) r.device_bytes += 2 * pe * kv_elem;
+                else r.host_bytes += 2 * pe * kv_elem;
+                if (en.gk >= 0) r.grad_bytes += 2 * pe * grad_elem;
+            }
+        r.arena_blocks = arena_n;
+        r.free_list = static_cast<int64_t>(free_list.size());
+        return r;
+    }
+};
+
+}  // namespace oomb
+
+using namespace oomb;
+
+struct oomb_pagetable_s {
+    PageTable pt;
+};
+
+struct oomb_pool_s {
+    oomb_config cfg{};
+    int device = 0;
+    int64_t max_pages = 0;
+    int elem = 4;
+    int64_t page_elems = 0;
+    PageTable* pt = nullptr;
+    int64_t n_kv_slots = 0, n_g_slots = 0;
+    std::vector<int32_t> kv_free, g_free;
+    std::vector<std::vector<int32_t>> kvslot, gslot;
+    void* kpool = nullptr;
+    void* vpool = nullptr;
+    float* gkpool = nullptr;
+    float* gvpool = nullptr;
+    int32_t* d_kvslot = nullptr;
+    int32_t* d_gslot = nullptr;
+    float* d_kavg_sum = nullptr;
+    int32_t* d_kavg_cnt = nullptr;
+    int* d_err = nullptr;
+    bool enforce = false;
+    int policy = 0;
+    TcPoolMaps maps;
+    void* bwd_ws = nullptr;
+    size_t bwd_ws_bytes = 0;
+
+    int32_t* kvslot_layer(int l) { return d_kvslot + static_cast<int64_t>(l) * max_pages; }
+    int32_t* gslot_layer(int l) { return d_gslot + static_cast<int64_t>(l) * max_pages; }
+    float* kavg_sum_layer(int l) {
+        return d_kavg_sum + static_cast<int64_t>(l) * max_pages * cfg.n_kv_heads * cfg.head_dim;
+    }
+    int32_t* kavg_cnt_layer(int l) { return d_kavg_cnt + static_cast<int64_t>(l) * max_pages; }
+};
+
+struct oomb_selection_s {
+    oomb_pool_s* pool = nullptr;
+    int max_m = 0, max_ids = 0;
+    int32_t* d_off = nullptr;
+    int32_t* d_ids = nullptr;
+    int32_t* h_off = nullptr;  // pinned
+    int32_t* h_ids = nullptr;  // pinned
+    int m = 0, nnz = 0;
+    cudaEvent_t ev = nullptr;
+    bool host_pending = false;  // device -> host mirror copy in flight
+};
+
+namespace {
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+void validate_cfg(const oomb_config& c) {  // ModelConfig::validate (config.cpp:30-51), path subset
+    auto req = [](bool ok, const char* m) {
+        if (!ok) throw Error(OOMB_CONFIG_ERROR, std::string("config: ") + m);
+    };
+    req(c.n_layers >= 1, "n_layers must be >= 1");
+    req(c.n_q_heads >= 1 && c.n_kv_heads >= 1, "head counts must be >= 1");
+    req(c.n_q_heads % c.n_kv_heads == 0, "n_q_heads must be divisible by n_kv_heads");
+    req(c.head_dim >= 2 && c.head_dim % 2 == 0, "head_dim must be even (rotary pairs)");
+    req(c.page_size >= 1, "page_size must be >= 1");
+    req(c.chunk_size >= 1, "chunk_size must be >= 1");
+    req(c.chunk_size % c.page_size == 0, "chunk_size must be divisible by page_size");
+    req(c.retrieval_budget >= 0, "retrieval_budget must be >= 0");
+    req(c.retrieval_budget % c.page_size == 0, "retrieval_budget must be divisible by page_size");
+    req(c.local_window >= 0, "local_window must be >= 0");
+    req(c.dtype == OOMB_F32 || c.dtype == OOMB_BF16, "dtype must be OOMB_F32 or OOMB_BF16");
+    req(c.head_dim <= 256, "head_dim must be <= 256");
+    req(c.max_tokens >= 1, "max_tokens must be >= 1");
+}
+
+void set_dev(oomb_pool_s* p) { OOMB_CUDA(cudaSetDevice(p->device)); }
+
+int32_t pop_slot(std::vector<int32_t>& fl, const char* what) {
+    OOMB_REQUIRE(!fl.empty(), OOMB_CONFIG_ERROR,
+                 std::string("device ") + what + " capacity exhausted (raise device_capacity_pages or offload)");
+    const int32_t s = fl.back();
+    fl.pop_back();
+    return s;
+}
+
+// Copy a small host int32 array into a stream-ordered temporary device buffer.
+int32_t* upload_ids(const int32_t* host, int n, cudaStream_t st) {
+    int32_t* d = nullptr;
+    OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), std::max(n, 1) * sizeof(int32_t), st));
+    if (n > 0) OOMB_CUDA(cudaMemcpyAsync(d, host, n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    return d;
+}
+
+AttnGeom geom(oomb_pool_s* p, int64_t tokens, int layer) {
+    AttnGeom g{};
+    g.C = static_cast<int>(tokens);
+    g.Hq = p->cfg.n_q_heads;
+    g.Hkv = p->cfg.n_kv_heads;
+    g.hd = p->cfg.head_dim;
+    g.P = p->cfg.page_size;
+    g.group = g.Hq / g.Hkv;
+    g.m = static_cast<int>((tokens + g.P - 1) / g.P);
+    g.filled = p->pt->filled[layer];
+    g.scale = 1.0f / std::sqrt(static_cast<float>(g.hd));
+    g.max_pages = static_cast<int>(p->max_pages);
+    return g;
+}
+
+void sel_host_sync(oomb_selection_s* s) {
+    if (s->host_pending) {
+        OOMB_CUDA(cudaEventSynchronize(s->ev));
+        s->host_pending = false;
+    }
+}
+
+// Lazy grad pages for every list of the selection, reference order (qp asc, list order).
+void ensure_grad_pages(oomb_pool_s* p, int layer, const int32_t* h_off, const int32_t* h_ids, int m, cudaStream_t st) {
+    std::vector<int32_t> pages, slots;
+    for (int qp = 0; qp < m; ++qp) {
+        const int n = h_off[qp + 1] - h_off[qp];
+        if (n == 0) continue;
+        p->pt->check_ids(layer, h_ids + h_off[qp], n, p->enforce, "scatter_add_grads");
+        for (int32_t pid : p->pt->scatter(layer, h_ids + h_off[qp], n)) {
+            const int32_t gs = pop_slot(p->g_free, "gradient page");
+            p->gslot[layer][pid] = gs;
+            pages.push_back(pid);
+            slots.push_back(gs);
+        }
+    }
+    if (pages.empty()) return;
+    const int n = static_cast<int>(pages.size());
+    int32_t* d = nullptr;
+    OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), 2 * n * sizeof(int32_t), st));
+    std::vector<int32_t> both(pages);
+    both.insert(both.end(), slots.begin(), slots.end());
+    OOMB_CUDA(cudaMemcpyAsync(d, both.data(), 2 * n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    launch_grad_init(d, d + n, n, p->gslot_layer(layer), p->gkpool, p->gvpool, p->page_elems, st);
+    OOMB_CUDA(cudaFreeAsync(d, st));
+}
+
+bool use_tc(oomb_pool_s* p, const AttnGeom& g) {
+    if (p->policy == 1) return false;
+    const bool ok = tc_supported(g, p->cfg.dtype) && p->maps.valid;
+    OOMB_REQUIRE(p->policy != 2 || ok, OOMB_CONFIG_ERROR, "tcgen05 kernels do not support this shape/dtype");
+    return ok;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* oomb_last_error(void) { return g_last_error.c_str(); }
+int oomb_version(void) { return 1; }
+int64_t oomb_kernel_launches(void) { return g_kernel_launches.load(); }
+
+// ---------------------------------------------------------------------------
+// page table host logic
+// ---------------------------------------------------------------------------
+int oomb_pagetable_create(int n_layers, int page_size, int n_kv_heads, int head_dim, int kv_elem_bytes,
+                          int grad_elem_bytes, oomb_pagetable_t* out) {
+    return guard([&] {
+        OOMB_REQUIRE(n_layers >= 1 && page_size >= 1 && n_kv_heads >= 1 && head_dim >= 1, OOMB_CONFIG_ERROR,
+                     "pagetable: bad geometry");
+        *out = new oomb_pagetable_s{PageTable(n_layers, page_size, n_kv_heads, head_dim, kv_elem_bytes,
+                                              grad_elem_bytes)};
+    });
+}
+int oomb_pagetable_destroy(oomb_pagetable_t pt) {
+    delete pt;
+    return OOMB_OK;
+}
+int oomb_pagetable_append(oomb_pagetable_t pt, int layer, int64_t rows, int64_t* b, int64_t* e) {
+    return guard([&] {
+        int fn, nn;
+        pt->pt.append(layer, rows, b, e, &fn, &nn);
+    });
+}
+int oomb_pagetable_scatter(oomb_pagetable_t pt, int layer, const int32_t* ids, int n) {
+    return guard([&] {
+        pt->pt.check_ids(layer, ids, n, false, "scatter_add_grads");
+        pt->pt.scatter(layer, ids, n);
+    });
+}
+int oomb_pagetable_reset(oomb_pagetable_t pt) {
+    return guard([&] { pt->pt.reset(); });
+}
+int oomb_pagetable_n_pages(oomb_pagetable_t pt, int layer, int* n) {
+    return guard([&] {
+        pt->pt.check_layer(layer);
+        *n = static_cast<int>(pt->pt.pages[layer].size());
+    });
+}
+int oomb_pagetable_get(oomb_pagetable_t pt, int layer, int32_t* out) {
+    return guard([&] {
+        pt->pt.check_layer(layer);
+        const auto& st = pt->pt.pages[layer];
+        for (size_t i = 0; i < st.size(); ++i) {
+            out[4 * i + 0] = st[i].k;
+            out[4 * i + 1] = st[i].v;
+            out[4 * i + 2] = st[i].gk;
+            out[4 * i + 3] = st[i].gv;
+        }
+    });
+}
+int oomb_pagetable_set_tier(oomb_pagetable_t pt, int layer, int page, int tier) {
+    return guard([&] {
+        pt->pt.check_layer(layer);
+        OOMB_REQUIRE(page >= 0 && page < static_cast<int>(pt->pt.pages[layer].size()), OOMB_SHAPE_ERROR,
+                     "set_tier: page out of range");
+        pt->pt.pages[layer][page].tier = tier ? 1 : 0;
+    });
+}
+int oomb_pagetable_memory_report(oomb_pagetable_t pt, oomb_memory_report* out) {
+    return guard([&] { *out = pt->pt.report(); });
+}
+
+// ---------------------------------------------------------------------------
+// pool lifecycle
+// ---------------------------------------------------------------------------
+int oomb_pool_create(const oomb_config* cfg, int device, oomb_pool_t* out) {
+    return guard([&] {
+        validate_cfg(*cfg);
+        auto* p = new oomb_pool_s();
+        try {
+            p->cfg = *cfg;
+            p->device = device;
+            OOMB_CUDA(cudaSetDevice(device));
+            const auto& c = p->cfg;
+            p->max_pages = (c.max_tokens + c.page_size - 1) / c.page_size;
+            p->elem = c.dtype == OOMB_BF16 ? 2 : 4;
+            p->page_elems = static_cast<int64_t>(c.page_size) * c.n_kv_heads * c.head_dim;
+            p->pt = new PageTable(c.n_layers, c.page_size, c.n_kv_heads, c.head_dim, p->elem, 4);
+            p->n_kv_slots = c.device_capacity_pages > 0 ? c.device_capacity_pages : c.n_layers * p->max_pages;
+            p->n_g_slots = p->n_kv_slots;
+            p->kv_free.resize(p->n_kv_slots);
+            p->g_free.resize(p->n_g_slots);
+            // LIFO: slot 0 is handed out first.
+            for (int64_t i = 0; i < p->n_kv_slots; ++i) p->kv_free[i] = static_cast<int32_t>(p->n_kv_slots - 1 - i);
+            for (int64_t i = 0; i < p->n_g_slots; ++i) p->g_free[i] = static_cast<int32_t>(p->n_g_slots - 1 - i);
+            p->kvslot.assign(c.n_layers, std::vector<int32_t>(p->max_pages, -1));
+            p->gslot.assign(c.n_layers, std::vector<int32_t>(p->max_pages, -1));
+            const size_t kv_bytes = static_cast<size_t>(p->n_kv_slots) * p->page_elems * p->elem;
+            const size_t g_bytes = static_cast<size_t>(p->n_g_slots) * p->page_elems * sizeof(float);
+            OOMB_CUDA(cudaMalloc(&p->kpool, kv_bytes));
+            OOMB_CUDA(cudaMalloc(&p->vpool, kv_bytes));
+            OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->gkpool), g_bytes));
+            OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->gvpool), g_bytes));
+            const size_t tab = static_cast<size_t>(c.n_layers) * p->max_pages * sizeof(int32_t);
+            OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->d_kvslot), tab));
+            OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->d_gslot), tab));
+            OOMB_CUDA(cudaMemset(p->d_kvslot, 0xFF, tab));
+            OOMB_CUDA(cudaMemset(p->d_gslot, 0xFF, tab));
+            const size_t ks = static_cast<size_t>(c.n_layers) * p->max_pages * c.n_kv_heads * c.head_dim;
+            OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->d_kavg_sum), ks * sizeof(float)));
+            OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->d_kavg_cnt), tab));
+            OOMB_CUDA(cudaMemset(p->d_kavg_sum, 0, ks * sizeof(float)));
+            OOMB_CUDA(cudaMemset(p->d_kavg_cnt, 0, tab));
+            OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->d_err), sizeof(int)));
+            OOMB_CUDA(cudaMemset(p->d_err, 0, sizeof(int)));
+            if (c.dtype == OOMB_BF16 && c.head_dim == 128 && c.page_size % 128 == 0)
+                make_pool_maps(p->maps, p->kpool, p->vpool, p->n_kv_slots, c.n_kv_heads, c.page_size, c.head_dim);
+        } catch (...) {
+            oomb_pool_destroy(p);
+            throw;
+        }
+        *out = p;
+    });
+}
+
+int oomb_pool_destroy(oomb_pool_t p) {
+    if (!p) return OOMB_OK;
+    cudaSetDevice(p->device);
+    cudaDeviceSynchronize();
+    cudaFree(p->kpool);
+    cudaFree(p->vpool);
+    cudaFree(p->gkpool);
+    cudaFree(p->gvpool);
+    cudaFree(p->d_kvslot);
+    cudaFree(p->d_gslot);
+    cudaFree(p->d_kavg_sum);
+    cudaFree(p->d_kavg_cnt);
+    cudaFree(p->d_err);
+    cudaFree(p->bwd_ws);
+    delete p->pt;
+    delete p;
+    return OOMB_OK;
+}
+
+int oomb_pool_reset(oomb_pool_t p, void* stream) {
+    return guard([&] {
+        set_dev(p);
+        for (int l = 0; l < p->cfg.n_layers; ++l) {
+            for (int64_t pg = 0; pg < static_cast<int64_t>(p->pt->pages[l].size()); ++pg) {
+                if (p->kvslot[l][pg] >= 0) p->kv_free.push_back(p->kvslot[l][pg]);
+                if (p->gslot[l][pg] >= 0) p->g_free.push_back(p->gslot[l][pg]);
+                p->kvslot[l][pg] = -1;
+                p->gslot[l][pg] = -1;
+            }
+        }
+        p->pt->reset();
+        const size_t tab = static_cast<size_t>(p->cfg.n_layers) * p->max_pages * sizeof(int32_t);
+        OOMB_CUDA(cudaMemsetAsync(p->d_kvslot, 0xFF, tab, S(stream)));
+        OOMB_CUDA(cudaMemsetAsync(p->d_gslot, 0xFF, tab, S(stream)));
+        OOMB_CUDA(cudaMemsetAsync(p->d_kavg_cnt, 0, tab, S(stream)));
+    });
+}
+
+int oomb_zero_grad_pages(oomb_pool_t p, void* stream) {
+    return guard([&] {
+        set_dev(p);
+        std::vector<int32_t> slots;
+        for (int l = 0; l < p->cfg.n_layers; ++l)
+            for (size_t pg = 0; pg < p->pt->pages[l].size(); ++pg)
+                if (p->gslot[l][pg] >= 0) slots.push_back(p->gslot[l][pg]);
+        if (slots.empty()) return;
+        int32_t* d = upload_ids(slots.data(), static_cast<int>(slots.size()), S(stream));
+        launch_zero_slots(d, static_cast<int>(slots.size()), p->gkpool, p->gvpool, p->page_elems, S(stream));
+        OOMB_CUDA(cudaFreeAsync(d, S(stream)));
+    });
+}
+
+int oomb_memory_report_get(oomb_pool_t p, oomb_memory_report* out) {
+    return guard([&] { *out = p->pt->report(); });
+}
+
+int oomb_check_device_errors(oomb_pool_t p) {
+    return guard([&] {
+        set_dev(p);
+        int h = 0;
+        OOMB_CUDA(cudaDeviceSynchronize());
+        OOMB_CUDA(cudaMemcpy(&h, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+        OOMB_CUDA(cudaMemset(p->d_err, 0, sizeof(int)));
+        OOMB_REQUIRE(!(h & DERR_BAD_ID), OOMB_SHAPE_ERROR, "kernel read a page id out of range");
+        OOMB_REQUIRE(!(h & DERR_NOT_RESIDENT), OOMB_RESIDENCY_ERROR, "kernel read a page that is not device-resident");
+    });
+}
+
+int oomb_set_kernel_policy(oomb_pool_t p, int policy) {
+    return guard([&] {
+        OOMB_REQUIRE(policy >= 0 && policy <= 2, OOMB_CONFIG_ERROR, "policy must be 0, 1 or 2");
+        p->policy = policy;
+    });
+}
+
+// ---------------------------------------------------------------------------
+// page table ops
+// ---------------------------------------------------------------------------
+int oomb_append_chunk(oomb_pool_t p, int layer, const void* k, const void* v, int64_t rows, void* stream,
+                      int64_t* slot_begin, int64_t* slot_end) {
+    return guard([&] {
+        set_dev(p);
+        p->pt->check_layer(layer);
+        const int P = p->cfg.page_size;
+        OOMB_REQUIRE(p->pt->filled[layer] + rows <= p->max_pages * P, OOMB_CONFIG_ERROR,
+                     "append_chunk: layer capacity (max_tokens) exceeded");
+        int64_t b, e;
+        int first_new, n_new;
+        const int64_t filled0 = p->pt->filled[layer];
+        p->pt->append(layer, rows, &b, &e, &first_new, &n_new);
+        for (int i = 0; i < n_new; ++i) p->kvslot[layer][first_new + i] = pop_slot(p->kv_free, "KV page");
+        *slot_begin = b;
+        *slot_end = e;
+        // Launch in segments that create at most 100 new pages each.
+        const int64_t re = static_cast<int64_t>(p->cfg.n_kv_heads) * p->cfg.head_dim;
+        int64_t done = 0;
+        int published = first_new;  // first new page whose slot is not yet in d_kvslot
+        while (done < rows) {
+            const int64_t seg = std::min<int64_t>(rows - done, static_cast<int64_t>(100) * P);
+            const int64_t f = filled0 + done;
+            const int first_page = static_cast<int>(f / P);
+            const int last_page = static_cast<int>((f + seg - 1) / P);
+            NewSlots ns{};
+            ns.first_page = std::max(first_page, published);
+            ns.n = 0;
+            for (int pg = ns.first_page; pg <= last_page; ++pg) ns.slot[ns.n++] = p->kvslot[layer][pg];
+            const char* kb = static_cast<const char*>(k) + done * re * p->elem;
+            const char* vb = static_cast<const char*>(v) + done * re * p->elem;
+            launch_append(p->cfg.dtype, kb, vb, seg, f, P, p->cfg.n_kv_heads, p->cfg.head_dim, first_page,
+                          last_page - first_page + 1, ns, p->kvslot_layer(layer), p->kpool, p->vpool,
+                          p->kavg_sum_layer(layer), p->kavg_cnt_layer(layer), S(stream));
+            published = std::max(published, last_page + 1);
+            done += seg;
+        }
+    });
+}
+
+int oomb_n_pages(oomb_pool_t p, int layer, int* n) {
+    return guard([&] {
+        p->pt->check_layer(layer);
+        *n = static_cast<int>(p->pt->pages[layer].size());
+    });
+}
+int oomb_filled(oomb_pool_t p, int layer, int64_t* f) {
+    return guard([&] {
+        p->pt->check_layer(layer);
+        *f = p->pt->filled[layer];
+    });
+}
+int oomb_page_table_get(oomb_pool_t p, int layer, int32_t* out) {
+    return guard([&] {
+        p->pt->check_layer(layer);
+        const auto& st = p->pt->pages[layer];
+        for (size_t i = 0; i < st.size(); ++i) {
+            out[4 * i + 0] = st[i].k;
+            out[4 * i + 1] = st[i].v;
+            out[4 * i + 2] = st[i].gk;
+            out[4 * i + 3] = st[i].gv;
+        }
+    });
+}
+int oomb_device_slots_get(oomb_pool_t p, int layer, int32_t* out) {
+    return guard([&] {
+        p->pt->check_layer(layer);
+        for (size_t i = 0; i < p->pt->pages[layer].size(); ++i) {
+            out[2 * i + 0] = p->kvslot[layer][i];
+            out[2 * i + 1] = p->gslot[layer][i];
+        }
+    });
+}
+int oomb_page_mean_keys(oomb_pool_t p, int layer, int n_candidates, float* out, void* stream, int* n_out) {
+    return guard([&] {
+        set_dev(p);
+        p->pt->check_layer(layer);
+        const int np = static_cast<int>(p->pt->pages[layer].size());
+        const int n = n_candidates < 0 ? np : std::min(n_candidates, np);
+        launch_mean_keys(p->kavg_sum_layer(layer), p->kavg_cnt_layer(layer), n, p->cfg.n_kv_heads * p->cfg.head_dim,
+                         out, S(stream));
+        *n_out = n;
+    });
+}
+int oomb_kavg_raw(oomb_pool_t p, int layer, float* sum_out, int32_t* count_out, void* stream) {
+    return guard([&] {
+        set_dev(p);
+        p->pt->check_layer(layer);
+        const int64_t np = static_cast<int64_t>(p->pt->pages[layer].size());
+        const int64_t re = static_cast<int64_t>(p->cfg.n_kv_heads) * p->cfg.head_dim;
+        if (np == 0) return;
+        OOMB_CUDA(cudaMemcpyAsync(sum_out, p->kavg_sum_layer(layer), np * re * sizeof(float),
+                                  cudaMemcpyDeviceToDevice, S(stream)));
+        OOMB_CUDA(cudaMemcpyAsync(count_out, p->kavg_cnt_layer(layer), np * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                                  S(stream)));
+    });
+}
+int oomb_gather_pages(oomb_pool_t p, int layer, const int32_t* ids, int n, int grads, void* k_out, void* v_out,
+                      uint8_t* valid_out, void* stream) {
+    return guard([&] {
+        set_dev(p);
+        p->pt->check_ids(layer, ids, n, p->enforce, grads ? "gather_grad_pages" : "gather_pages");
+        if (n == 0) return;
+        int32_t* d = upload_ids(ids, n, S(stream));
+        launch_gather(p->cfg.dtype, grads, d, n, grads ? p->gslot_layer(layer) : p->kvslot_layer(layer),
+                      grads ? static_cast<const void*>(p->gkpool) : p->kpool,
+                      grads ? static_cast<const void*>(p->gvpool) : p->vpool, p->pt->filled[layer],
+                      p->cfg.page_size, p->cfg.n_kv_heads, p->cfg.head_dim, k_out, v_out, valid_out, p->d_err,
+                      S(stream));
+        OOMB_CUDA(cudaFreeAsync(d, S(stream)));
+    });
+}
+int oomb_scatter_add_grads(oomb_pool_t p, int layer, const int32_t* ids, int n, const float* dk, const float* dv,
+                           void* stream) {
+    return guard([&] {
+        set_dev(p);
+        p->pt->check_ids(layer, ids, n, p->enforce, "scatter_add_grads");
+        if (n == 0) return;
+        const int32_t off[2] = {0, n};
+        ensure_grad_pages(p, layer, off, ids, 1, S(stream));
+        int32_t* d = upload_ids(ids, n, S(stream));
+        launch_scatter(d, n, p->gslot_layer(layer), p->gkpool, p->gvpool, dk, dv, p->pt->filled[layer],
+                       p->cfg.page_size, p->cfg.n_kv_heads, p->cfg.head_dim, p->d_err, S(stream));
+        OOMB_CUDA(cudaFreeAsync(d, S(stream)));
+    });
+}
+int oomb_set_tier(oomb_pool_t p, int layer, int page, int tier) {
+    return guard([&] {
+        p->pt->check_layer(layer);
+        OOMB_REQUIRE(page >= 0 && page < static_cast<int>(p->pt->pages[layer].size()), OOMB_SHAPE_ERROR,
+                     "set_tier: page out of range");
+        p->pt->pages[layer][page].tier = tier ? 1 : 0;
+    });
+}
+int oomb_get_tier(oomb_pool_t p, int layer, int page, int* tier) {
+    return guard([&] {
+        p->pt->check_layer(layer);
+        OOMB_REQUIRE(page >= 0 && page < static_cast<int>(p->pt->pages[layer].size()), OOMB_SHAPE_ERROR,
+                     "tier: page out of range");
+        *tier = p->pt->pages[layer][page].tier;
+    });
+}
+int oomb_set_residency_enforced(oomb_pool_t p, int on) {
+    return guard([&] { p->enforce = on != 0; });
+}
+int oomb_grads_allocated(oomb_pool_t p, int layer, int page, int* a) {
+    return guard([&] {
+        p->pt->check_layer(layer);
+        OOMB_REQUIRE(page >= 0 && page < static_cast<int>(p->pt->pages[layer].size()), OOMB_SHAPE_ERROR,
+                     "grads_allocated: page out of range");
+        *a = p->pt->pages[layer][page].gk >= 0;
+    });
+}
+
+// ---------------------------------------------------------------------------
+// selections
+// ---------------------------------------------------------------------------
+int oomb_selection_create(oomb_pool_t p, int max_m, int max_ids, oomb_selection_t* out) {
+    return guard([&] {
+        set_dev(p);
+        OOMB_REQUIRE(max_m >= 1 && max_ids >= 0, OOMB_CONFIG_ERROR, "selection: bad capacity");
+        auto* s = new oomb_selection_s();
+        s->pool = p;
+        s->max_m = max_m;
+        s->max_ids = max_ids;
+        OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&s->d_off), (max_m + 1) * sizeof(int32_t)));
+        OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&s->d_ids), std::max(max_ids, 1) * sizeof(int32_t)));
+        OOMB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s->h_off), (max_m + 1) * sizeof(int32_t)));
+        OOMB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s->h_ids), std::max(max_ids, 1) * sizeof(int32_t)));
+        OOMB_CUDA(cudaEventCreateWithFlags(&s->ev, cudaEventDisableTiming));
+        s->h_off[0] = 0;
+        *out = s;
+    });
+}
+int oomb_selection_destroy(oomb_selection_t s) {
+    if (!s) return OOMB_OK;
+    cudaSetDevice(s->pool->device);
+    if (s->ev) cudaEventSynchronize(s->ev);
+    cudaFree(s->d_off);
+    cudaFree(s->d_ids);
+    cudaFreeHost(s->h_off);
+    cudaFreeHost(s->h_ids);
+    if (s->ev) cudaEventDestroy(s->ev);
+    delete s;
+    return OOMB_OK;
+}
+int oomb_selection_set_host(oomb_selection_t s, const int32_t* off, const int32_t* ids, int m, void* stream) {
+    return guard([&] {
+        set_dev(s->pool);
+        OOMB_REQUIRE(m >= 0 && m <= s->max_m, OOMB_SHAPE_ERROR, "selection: too many query pages");
+        const int nnz = m > 0 ? off[m] : 0;
+        OOMB_REQUIRE(nnz >= 0 && nnz <= s->max_ids, OOMB_SHAPE_ERROR, "selection: too many ids");
+        OOMB_CUDA(cudaEventSynchronize(s->ev));  // previous async copy out of the pinned mirror is done
+        s->host_pending = false;
+        std::memcpy(s->h_off, off, (m + 1) * sizeof(int32_t));
+        if (nnz) std::memcpy(s->h_ids, ids, nnz * sizeof(int32_t));
+        OOMB_CUDA(cudaMemcpyAsync(s->d_off, s->h_off, (m + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, S(stream)));
+        if (nnz)
+            OOMB_CUDA(cudaMemcpyAsync(s->d_ids, s->h_ids, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, S(stream)));
+        OOMB_CUDA(cudaEventRecord(s->ev, S(stream)));
+        s->m = m;
+        s->nnz = nnz;
+    });
+}
+int oomb_selection_get_host(oomb_selection_t s, int32_t* off, int32_t* ids, int* m, int* nnz) {
+    return guard([&] {
+        set_dev(s->pool);
+        sel_host_sync(s);
+        *m = s->m;
+        *nnz = s->nnz;
+        if (off) std::memcpy(off, s->h_off, (s->m + 1) * sizeof(int32_t));
+        if (ids && s->nnz) std::memcpy(ids, s->h_ids, s->nnz * sizeof(int32_t));
+    });
+}
+int oomb_selection_device(oomb_selection_t s, const int32_t** off, const int32_t** ids, int* m) {
+    return guard([&] {
+        *off = s->d_off;
+        *ids = s->d_ids;
+        *m = s->m;
+    });
+}
+static void select_range(oomb_selection_t s, int first, int count, int m, cudaStream_t st) {
+    OOMB_REQUIRE(m >= 0 && m <= s->max_m, OOMB_SHAPE_ERROR, "selection: too many query pages");
+    OOMB_REQUIRE(static_cast<int64_t>(m) * count <= s->max_ids, OOMB_SHAPE_ERROR, "selection: too many ids");
+    OOMB_CUDA(cudaEventSynchronize(s->ev));
+    s->host_pending = false;
+    for (int qp = 0; qp <= m; ++qp) s->h_off[qp] = qp * count;
+    for (int qp = 0; qp < m; ++qp)
+        for (int i = 0; i < count; ++i) s->h_ids[static_cast<int64_t>(qp) * count + i] = first + i;
+    s->m = m;
+    s->nnz = m * count;
+    launch_fill_csr_all(s->d_off, s->d_ids, m, first, count, st);
+}
+int oomb_select_all(oomb_selection_t s, int n_pages, int m, void* stream) {
+    return guard([&] {
+        set_dev(s->pool);
+        OOMB_REQUIRE(n_pages >= 0, OOMB_SHAPE_ERROR, "select_all: negative page count");
+        select_range(s, 0, n_pages, m, S(stream));
+    });
+}
+int oomb_select_recent(oomb_selection_t s, int n_pages, int window, int m, void* stream) {
+    return guard([&] {
+        set_dev(s->pool);
+        OOMB_REQUIRE(window >= 0, OOMB_SHAPE_ERROR, "select_recent: negative window");  // attention.hpp:100
+        const int take = std::min(n_pages, window);
+        select_range(s, n_pages - take, take, m, S(stream));
+    });
+}
+int oomb_select_topk(oomb_selection_t s, const float* vote, int m, int n, int k, void* stream) {
+    return guard([&] {
+        set_dev(s->pool);
+        OOMB_REQUIRE(k >= 0, OOMB_SHAPE_ERROR, "select_topk: negative budget");  // attention.hpp:73
+        OOMB_REQUIRE(m >= 0 && m <= s->max_m, OOMB_SHAPE_ERROR, "selection: too many query pages");
+        const int kk = std::min(k, n);
+        OOMB_REQUIRE(static_cast<int64_t>(m) * kk <= s->max_ids, OOMB_SHAPE_ERROR, "selection: too many ids");
+        OOMB_CUDA(cudaEventSynchronize(s->ev));
+        launch_topk(vote, m, n, k, s->d_off, s->d_ids, S(stream));
+        OOMB_CUDA(cudaMemcpyAsync(s->h_off, s->d_off, (m + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, S(stream)));
+        if (m * kk)
+            OOMB_CUDA(cudaMemcpyAsync(s->h_ids, s->d_ids, static_cast<size_t>(m) * kk * sizeof(int32_t),
+                                      cudaMemcpyDeviceToHost, S(stream)));
+        OOMB_CUDA(cudaEventRecord(s->ev, S(stream)));
+        s->host_pending = true;
+        s->m = m;
+        s->nnz = m * kk;
+    });
+}
+
+// ---------------------------------------------------------------------------
+// scoring
+// ---------------------------------------------------------------------------
+int oomb_score_pages(const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, int64_t n, int Hkv,
+                     int page_size, int score_scale, int dtype, float* vote, void* stream) {
+    return guard([&] {
+        OOMB_REQUIRE(n >= 1, OOMB_SHAPE_ERROR, "score_pages: needs at least one candidate page");
+        OOMB_REQUIRE(Hq >= 1 && Hkv >= 1 && Hq % Hkv == 0 && hd >= 1 && hd <= 256 && page_size >= 1,
+                     OOMB_SHAPE_ERROR, "score_pages: bad shape");
+        const float scale = score_scale ? 1.0f / std::sqrt(static_cast<float>(hd)) : 1.0f;
+        float* stats = nullptr;
+        OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&stats), std::max<int64_t>(tokens * Hq, 1) * 8, S(stream)));
+        launch_score_simt(dtype, q, tokens, Hq, hd, k_avg, n, Hkv, page_size, scale, vote, stats, S(stream));
+        OOMB_CUDA(cudaFreeAsync(stats, S(stream)));
+    });
+}
+
+int oomb_select_pages_topk(oomb_pool_t p, int layer, const void* q, int64_t tokens, int n_candidates,
+                           oomb_selection_t sel, float* vote_scratch, void* stream) {
+    return guard([&] {
+        set_dev(p);
+        p->pt->check_layer(layer);
+        const int np = static_cast<int>(p->pt->pages[layer].size());
+        const int n = std::min(n_candidates, np);
+        const int m = static_cast<int>((tokens + p->cfg.page_size - 1) / p->cfg.page_size);
+        if (n <= 0) {  // chunk_trainer.hpp:297: no candidates -> empty lists
+            select_range(sel, 0, 0, m, S(stream));
+            return;
+        }
+        const int64_t re = static_cast<int64_t>(p->cfg.n_kv_heads) * p->cfg.head_dim;
+        float* kavg = nullptr;
+        OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&kavg), n * re * sizeof(float), S(stream)));
+        launch_mean_keys(p->kavg_sum_layer(layer), p->kavg_cnt_layer(layer), n, static_cast<int>(re), kavg, S(stream));
+        const int rc = oomb_score_pages(q, tokens, p->cfg.n_q_heads, p->cfg.head_dim, kavg, n, p->cfg.n_kv_heads,
+                                        p->cfg.page_size, p->cfg.score_scale, p->cfg.dtype, vote_scratch, stream);
+        OOMB_CUDA(cudaFreeAsync(kavg, S(stream)));
+        if (rc) throw Error(rc, g_last_error);
+        const int rc2 = oomb_select_topk(sel, vote_scratch, m, n, p->cfg.retrieval_budget / p->cfg.page_size, stream);
+        if (rc2) throw Error(rc2, g_last_error);
+    });
+}
+
+// ---------------------------------------------------------------------------
+// attention
+// ---------------------------------------------------------------------------
+int oomb_attn_forward(oomb_pool_t p, int layer, const void* q, int64_t tokens, oomb_selection_t sel,
+                      const void* k_cur, const void* v_cur, void* out, float* lse, void* stream) {
+    return guard([&] {
+        set_dev(p);
+        p->pt->check_layer(layer);
+        OOMB_REQUIRE(tokens >= 1, OOMB_SHAPE_ERROR, "attn_forward: empty chunk");
+        AttnGeom g = geom(p, tokens, layer);
+        OOMB_REQUIRE(sel->m == g.m, OOMB_SHAPE_ERROR,
+                     "attn_forward: one selected-page list per query page required");  // attention.hpp:172-174
+        if (p->enforce) {  // gather_pages' residency check (paged_kv.hpp:118-122)
+            sel_host_sync(sel);
+            for (int qp = 0; qp < g.m; ++qp)
+                p->pt->check_ids(layer, sel->h_ids + sel->h_off[qp], sel->h_off[qp + 1] - sel->h_off[qp], true,
+                                 "gather_pages");
+        }
+        if (use_tc(p, g))
+            launch_attn_fwd_tc(g, p->maps, q, sel->d_off, sel->d_ids, p->kvslot_layer(layer), k_cur, v_cur, out, lse,
+                               p->d_err, S(stream));
+        else
+            launch_attn_fwd_simt(p->cfg.dtype, g, q, sel->d_off, sel->d_ids, p->kvslot_layer(layer), p->kpool, p->vpool,
+                                 k_cur, v_cur, out, lse, p->d_err, S(stream));
+    });
+}
+
+int oomb_attn_backward(oomb_pool_t p, int layer, const void* dout, const void* q, int64_t tokens,
+                       oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out, const float* lse,
+                       float* dq, float* dk_cur, float* dv_cur, void* stream) {
+    return guard([&] {
+        set_dev(p);
+        p->pt->check_layer(layer);
+        OOMB_REQUIRE(tokens >= 1, OOMB_SHAPE_ERROR, "attn_backward: empty chunk");
+        AttnGeom g = geom(p, tokens, layer);
+        OOMB_REQUIRE(sel->m == g.m, OOMB_SHAPE_ERROR, "attn_backward: one selected-page list per query page required");
+        sel_host_sync(sel);
+        for (int qp = 0; qp < g.m; ++qp)
+            p->pt->check_ids(layer, sel->h_ids + sel->h_off[qp], sel->h_off[qp + 1] - sel->h_off[qp], p->enforce,
+                             "gather_pages");
+        ensure_grad_pages(p, layer, sel->h_off, sel->h_ids, g.m, S(stream));
+        const size_t kvb = static_cast<size_t>(tokens) * g.Hkv * g.hd * sizeof(float);
+        const bool tc = p->policy != 1 && p->maps.valid && tc_supported(g, p->cfg.dtype) && tc_bwd_available();
+        if (tc) {
+            const size_t need = attn_bwd_tc_workspace(g, sel->nnz);
+            if (need > p->bwd_ws_bytes) {
+                OOMB_CUDA(cudaStreamSynchronize(S(stream)));
+                cudaFree(p->bwd_ws);
+                p->bwd_ws = nullptr;
+                OOMB_CUDA(cudaMalloc(&p->bwd_ws, need));
+                p->bwd_ws_bytes = need;
+            }
+            launch_attn_bwd_tc(g, p->maps, dout, q, sel->d_off, sel->d_ids, p->kvslot_layer(layer),
+                               p->gslot_layer(layer), p->gkpool, p->gvpool, k_cur, v_cur, out, lse, dq, dk_cur,
+                               dv_cur, p->d_err, p->bwd_ws, p->bwd_ws_bytes, S(stream));
+        } else {
+            OOMB_CUDA(cudaMemsetAsync(dk_cur, 0, kvb, S(stream)));
+            OOMB_CUDA(cudaMemsetAsync(dv_cur, 0, kvb, S(stream)));
+            launch_attn_bwd_simt(p->cfg.dtype, g, dout, q, sel->d_off, sel->d_ids, p->kvslot_layer(layer),
+                                 p->gslot_layer(layer), p->kpool, p->vpool, p->gkpool, p->gvpool, k_cur, v_cur, out,
+                                 lse, dq, dk_cur, dv_cur, p->d_err, S(stream));
+        }
+    });
+}
+
+int oomb_debug_tc_gemm(int mode, const void* a, const void* b, float* c, int m, int n, int k, void* stream) {
+    return guard([&] {
+        OOMB_REQUIRE(m == 128 && (n == 64 || n == 128 || n == 256) && k % 64 == 0 && k > 0, OOMB_SHAPE_ERROR,
+                     "debug_tc_gemm: M=128, N in {64,128,256}, K%64==0");
+        launch_debug_tc_gemm(mode, a, b, c, m, n, k, S(stream));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,125 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Internal declarations shared by the host runtime (oomb_api.cu) and the
+// kernel translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "oomb.h"
+
+namespace oomb {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define OOMB_REQUIRE(cond, code, msg)                     \
+    do {                                                  \
+        if (!(cond)) throw ::oomb::Error((code), (msg));  \
+    } while (0)
+
+#define OOMB_CUDA(call)                                                                          \
+    do {                                                                                         \
+        cudaError_t e_ = (call);                                                                 \
+        if (e_ != cudaSuccess)                                                                   \
+            throw ::oomb::Error(OOMB_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+extern std::atomic<int64_t> g_kernel_launches;
+inline void count_launch(int n = 1) { g_kernel_launches.fetch_add(n, std::memory_order_relaxed); }
+void check_launch(const char* what);
+
+// Device error flags (bitmask) written by kernels.
+enum : int { DERR_NOT_RESIDENT = 1, DERR_BAD_ID = 2 };
+
+// ---------------------------------------------------------------------------
+// Geometry passed to every attention kernel.
+// ---------------------------------------------------------------------------
+struct AttnGeom {
+    int C;         // query rows (tokens) in the chunk
+    int Hq, Hkv, hd, P;
+    int group;     // Hq / Hkv
+    int m;         // query pages = ceil(C / P)
+    int64_t filled;  // layer fill level (valid-slot mask of past pages)
+    float scale;   // 1/sqrt(hd)
+    int max_pages;
+};
+
+// ---------------------------------------------------------------------------
+// Kernel launchers (kernels_simt.cu)
+// ---------------------------------------------------------------------------
+struct NewSlots {
+    int32_t first_page;  // logical page id of slot[0]
+    int32_t n;
+    int32_t slot[120];
+};
+
+void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_t filled_before, int P, int Hkv,
+                   int hd, int first_page, int n_pages_touched, const NewSlots& ns, int32_t* d_kvslot_layer,
+                   void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, cudaStream_t st);
+void launch_mean_keys(const float* kavg_sum_layer, const int32_t* kavg_cnt_layer, int n, int row_elems,
+                      float* out, cudaStream_t st);
+void launch_gather(int dtype, int grads, const int32_t* d_ids, int n, const int32_t* d_slot_layer,
+                   const void* pk, const void* pv, int64_t filled, int P, int Hkv, int hd, void* k_out,
+                   void* v_out, uint8_t* valid_out, int* d_err, cudaStream_t st);
+void launch_scatter(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, float* gk, float* gv,
+                    const float* dk, const float* dv, int64_t filled, int P, int Hkv, int hd, int* d_err,
+                    cudaStream_t st);
+void launch_grad_init(const int32_t* d_pages, const int32_t* d_slots, int n, int32_t* d_gslot_layer, float* gk,
+                      float* gv, int64_t page_elems, cudaStream_t st);
+void launch_zero_slots(const int32_t* d_slots, int n, float* gk, float* gv, int64_t page_elems, cudaStream_t st);
+
+void launch_score_simt(int dtype, const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, int64_t n,
+                       int Hkv, int P, float scale, float* vote, float* stats_scratch, cudaStream_t st);
+void launch_topk(const float* vote, int m, int n, int k, int32_t* sel_off, int32_t* sel_ids, cudaStream_t st);
+void launch_fill_csr_all(int32_t* off, int32_t* ids, int m, int first, int count, cudaStream_t st);
+
+void launch_attn_fwd_simt(int dtype, const AttnGeom& g, const void* q, const int32_t* sel_off,
+                          const int32_t* sel_ids, const int32_t* d_kvslot_layer, const void* kpool,
+                          const void* vpool, const void* k_cur, const void* v_cur, void* out, float* lse, int* d_err,
+                          cudaStream_t st);
+void launch_attn_bwd_simt(int dtype, const AttnGeom& g, const void* dout, const void* q, const int32_t* sel_off,
+                          const int32_t* sel_ids, const int32_t* d_kvslot_layer, const int32_t* d_gslot_layer,
+                          const void* kpool, const void* vpool, float* gkpool, float* gvpool, const void* k_cur,
+                          const void* v_cur, const void* out, const float* lse, float* dq, float* dk_cur,
+                          float* dv_cur, int* d_err, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// tcgen05 / TMA kernels (attn_tc.cu)
+// ---------------------------------------------------------------------------
+struct TcPoolMaps {
+    CUtensorMap kpool;  // [n_slots*Hkv*P rows][hd] bf16, box 128 x 64, SW128
+    CUtensorMap vpool;
+    bool valid = false;
+};
+bool tc_supported(const AttnGeom& g, int dtype);
+bool tc_bwd_available();
+void make_pool_maps(TcPoolMaps& maps, const void* kpool, const void* vpool, int64_t n_slots, int Hkv, int P,
+                    int hd);
+void launch_attn_fwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* q, const int32_t* sel_off,
+                        const int32_t* sel_ids, const int32_t* d_kvslot_layer, const void* k_cur, const void* v_cur,
+                        void* out, float* lse, int* d_err, cudaStream_t st);
+void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* dout, const void* q,
+                        const int32_t* sel_off, const int32_t* sel_ids, const int32_t* d_kvslot_layer,
+                        const int32_t* d_gslot_layer, float* gkpool, float* gvpool, const void* k_cur,
+                        const void* v_cur, const void* out, const float* lse, float* dq, float* dk_cur,
+                        float* dv_cur, int* d_err, void* workspace, size_t workspace_bytes, cudaStream_t st);
+size_t attn_bwd_tc_workspace(const AttnGeom& g, int max_sel_ids);
+void launch_debug_tc_gemm(int mode, const void* a, const void* b, float* c, int m, int n, int k, cudaStream_t st);
+
+// Driver entry point for cuTensorMapEncodeTiled (no libcuda link dependency).
+CUresult encode_tensor_map(CUtensorMap* map, CUtensorMapDataType dt, uint32_t rank, void* base,
+                           const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box,
+                           CUtensorMapSwizzle swz);
+
+}  // namespace oomb
