@@ -173,6 +173,20 @@ OOMB_API int oomb_attn_backward(oomb_pool_t pool, int layer, const void* dout, c
  * 1 = force the SIMT kernels, 2 = force tcgen05 (error if the shape is unsupported). */
 OOMB_API int oomb_set_kernel_policy(oomb_pool_t pool, int policy);
 
+/* dM_i read-back (chunk_trainer.hpp:575-587): dk[i*P+s] += grad_k(ids[i], s) and the same for
+ * dv, reference layout [n*P][Hkv][hd] fp32 device; pages without gradients add 0. */
+OOMB_API int oomb_accumulate_grad_pages(oomb_pool_t pool, int layer, const int32_t* ids_host, int n, float* dk,
+                                        float* dv, void* stream);
+
+/* ---- kernel timing evidence ---------------------------------------------
+ * When enabled, every kernel the pool launches is bracketed by CUDA events on its
+ * stream; oomb_profile_collect synchronises and returns, per kernel kind, the number of
+ * launches and the summed device milliseconds, then clears the record.
+ * Kinds: 0 append, 1 score, 2 topk, 3 attn_fwd, 4 bwd_prep, 5 bwd_dq, 6 bwd_dkdv,
+ * 7 bwd_simt, 8 grad_init, 9 gather/scatter, 10 other. */
+OOMB_API int oomb_profile_enable(oomb_pool_t pool, int on);
+OOMB_API int oomb_profile_collect(oomb_pool_t pool, int64_t* counts, double* ms, int n_kinds);
+
 /* ---- page-table host logic (no device) -----------------------------------
  * The arena / LIFO free-list / lazy-gradient-page bookkeeping of PagedCache
  * (paged_kv.hpp:73-108,135-164,227-242,280-288), exposed on its own so that it is

@@ -83,6 +83,9 @@ _PROTOS = {
     "oomb_pagetable_set_tier": [VP, I, I, I],
     "oomb_pagetable_memory_report": [VP, C.POINTER(OombMemoryReport)],
     "oomb_debug_tc_gemm": [I, VP, VP, VP, I, I, I, VP],
+    "oomb_accumulate_grad_pages": [VP, I, VP, I, VP, VP, VP],
+    "oomb_profile_enable": [VP, I],
+    "oomb_profile_collect": [VP, VP, VP, I],
 }
 _RESTYPE = {"oomb_last_error": C.c_char_p, "oomb_kernel_launches": C.c_int64}
 

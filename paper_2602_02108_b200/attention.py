@@ -137,16 +137,20 @@ def _scratch_cache() -> PagedCache:
     return _SCRATCH[dev]
 
 
-def select_pages_topk(cache: PagedCache, layer: int, q: torch.Tensor, n_candidates: int, stream=None) -> Selection:
+def select_pages_topk(cache: PagedCache, layer: int, q: torch.Tensor, n_candidates: int, stream=None,
+                      out: Selection | None = None, vote: torch.Tensor | None = None) -> Selection:
     """chunk_trainer.hpp:305-311: K_avg (pinned metadata) -> score_pages -> select_topk_row
-    per query page, all on the device."""
+    per query page, all on the device. `out` / `vote` let a caller reuse buffers."""
     cfg = cache.cfg
     q = cache._dev(q)
     m = (q.shape[0] + cfg.page_size - 1) // cfg.page_size
     n = min(n_candidates, cache.n_pages(layer))
     k = min(cfg.budget_pages(), max(n, 0))
-    sel = Selection(cache, max(m, 1), m * k)
-    vote = torch.empty((m, max(n, 1)), dtype=torch.float32, device=cache.device)
+    sel = out if out is not None else Selection(cache, max(m, 1), m * k)
+    if vote is None or vote.numel() < m * max(n, 1):
+        vote = torch.empty((m, max(n, 1)), dtype=torch.float32, device=cache.device)
+    else:
+        vote = vote.reshape(-1)[: m * max(n, 1)].view(m, max(n, 1))
     call("oomb_select_pages_topk", cache.handle, layer, _ptr(q), q.shape[0], n_candidates, sel.handle, _ptr(vote),
          stream_handle(stream))
     sel.vote = vote[:, :max(n, 0)]
@@ -171,16 +175,18 @@ class AttnGrads:
 
 
 def attn_forward(cfg: ModelConfig, q, cache: PagedCache, layer: int, selected, k_cur, v_cur,
-                 stream=None) -> AttnSaved:
-    """attention.hpp:156-208."""
+                 stream=None, out: torch.Tensor | None = None, lse: torch.Tensor | None = None) -> AttnSaved:
+    """attention.hpp:156-208. `out` / `lse` may be preallocated by the caller."""
     q, k_cur, v_cur = cache._dev(q), cache._dev(k_cur), cache._dev(v_cur)
     c, qh, hd = q.shape
     if qh != cfg.n_q_heads or hd != cfg.head_dim or k_cur.shape != (c, cfg.n_kv_heads, hd) or \
             v_cur.shape != k_cur.shape:
         raise ShapeError("attn_forward: q / k_cur / v_cur shape mismatch")
     sel = as_selection(cache, selected, stream)
-    out = torch.empty_like(q)
-    lse = torch.empty((c, qh), dtype=torch.float32, device=q.device)
+    out = torch.empty_like(q) if out is None else out
+    lse = torch.empty((c, qh), dtype=torch.float32, device=q.device) if lse is None else lse
+    if out.shape != q.shape or out.dtype != q.dtype or lse.shape != (c, qh) or lse.dtype != torch.float32:
+        raise ShapeError("attn_forward: preallocated out / lse have the wrong shape or dtype")
     call("oomb_attn_forward", cache.handle, layer, _ptr(q), c, sel.handle, _ptr(k_cur), _ptr(v_cur), _ptr(out),
          _ptr(lse), stream_handle(stream))
     if cache.residency_enforced():
@@ -189,16 +195,23 @@ def attn_forward(cfg: ModelConfig, q, cache: PagedCache, layer: int, selected, k
 
 
 def attn_backward(cfg: ModelConfig, dout, q, cache: PagedCache, layer: int, k_cur, v_cur, saved: AttnSaved,
-                  stream=None) -> AttnGrads:
-    """attention.hpp:222-293 — past-page dK/dV go into the cache's gradient pages."""
+                  stream=None, grads: AttnGrads | None = None) -> AttnGrads:
+    """attention.hpp:222-293 — past-page dK/dV go into the cache's gradient pages.
+    `grads` may carry preallocated fp32 output buffers."""
     dout, q = cache._dev(dout), cache._dev(q)
     k_cur, v_cur = cache._dev(k_cur), cache._dev(v_cur)
     if dout.shape != saved.out.shape:
         raise ShapeError("attn_backward: dO shape mismatch")
     c = q.shape[0]
-    dq = torch.empty((c, cfg.n_q_heads, cfg.head_dim), dtype=torch.float32, device=q.device)
-    dk = torch.empty((c, cfg.n_kv_heads, cfg.head_dim), dtype=torch.float32, device=q.device)
-    dv = torch.empty_like(dk)
+    if grads is None:
+        dq = torch.empty((c, cfg.n_q_heads, cfg.head_dim), dtype=torch.float32, device=q.device)
+        dk = torch.empty((c, cfg.n_kv_heads, cfg.head_dim), dtype=torch.float32, device=q.device)
+        dv = torch.empty_like(dk)
+    else:
+        dq, dk, dv = grads.dq, grads.dk_cur, grads.dv_cur
+        if dq.shape != (c, cfg.n_q_heads, cfg.head_dim) or dk.shape != (c, cfg.n_kv_heads, cfg.head_dim) or \
+                dv.shape != dk.shape or {dq.dtype, dk.dtype, dv.dtype} != {torch.float32}:
+            raise ShapeError("attn_backward: preallocated gradients have the wrong shape or dtype")
     call("oomb_attn_backward", cache.handle, layer, _ptr(dout), _ptr(q), c, saved.selected.handle, _ptr(k_cur),
          _ptr(v_cur), _ptr(saved.out), _ptr(saved.lse), _ptr(dq), _ptr(dk), _ptr(dv), stream_handle(stream))
     if cache.residency_enforced():

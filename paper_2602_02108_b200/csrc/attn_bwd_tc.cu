@@ -1,0 +1,724 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// tcgen05 backward of the paged chunk attention (attention.hpp:222-293),
+// deterministic (no floating-point atomics):
+//
+//   bwd_prep      D[h][t] = sum_d dO*O (saved O, attention.hpp:253-256) and
+//                 L[h][t] = lse*log2(e), head-major for broadcast reads.
+//   bwd_mask      per past page: bitmask of the query pages that selected it.
+//   bwd_union     ascending union of selected pages (the backward's key blocks).
+//   attn_bwd_dq   query-major: S = Q K^T, dP = dO V^T, dS = P (dP - D),
+//                 dQ += dS K over the query page's selected pages then the
+//                 chunk's causal prefix; dQ written once (fp32).
+//   attn_bwd_dkdv key-major: one CTA owns one (key block, kv head) and loops over
+//                 every (64-row query tile, q-head of the group) that attends it:
+//                 S^T = K Q^T, dP^T = V dO^T, dV += P^T dO, dK += dS^T Q with
+//                 dK/dV accumulated in TMEM, then ONE read-modify-write into the
+//                 fp32 gradient pool (past pages) or a store to dk_cur/dv_cur
+//                 (the chunk's own keys). Pages never selected are not touched.
+
+#include <cub/block/block_scan.cuh>
+
+#include "tc_common.cuh"
+
+namespace oomb {
+
+using namespace tc;
+
+namespace {
+
+constexpr int kQ64 = 64;                        // query rows per dK/dV work item
+constexpr int kRegion64 = kQ64 * 128;           // [64 x 64] bf16 region = 8 KB
+constexpr int kTile64 = 2 * kRegion64;          // [64 x 128] tile = 16 KB
+constexpr int kPT = kTile * kQ64 * 2;           // P^T / dS^T [128 keys x 64 q] = 16 KB (one region)
+
+// ---------------------------------------------------------------- workspace
+struct BwdWs {
+    float* Dt;        // [Hq][C]
+    float* Lt;        // [Hq][C]
+    uint64_t* mask;   // [max_pages]
+    int32_t* uni;     // [max_pages]
+    int32_t* n_uni;   // [1]
+};
+
+BwdWs carve(const AttnGeom& g, void* ws) {
+    uint8_t* p = static_cast<uint8_t*>(ws);
+    BwdWs w;
+    const size_t hc = static_cast<size_t>(g.Hq) * g.C * sizeof(float);
+    w.Dt = reinterpret_cast<float*>(p);
+    w.Lt = reinterpret_cast<float*>(p + hc);
+    size_t off = (2 * hc + 255) & ~size_t(255);
+    w.mask = reinterpret_cast<uint64_t*>(p + off);
+    off += static_cast<size_t>(g.max_pages) * 8;
+    w.uni = reinterpret_cast<int32_t*>(p + off);
+    off += static_cast<size_t>(g.max_pages) * 4;
+    w.n_uni = reinterpret_cast<int32_t*>(p + off);
+    return w;
+}
+
+// ---------------------------------------------------------------- prep kernels
+__global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                                const float* __restrict__ lse, int C, int Hq, float* __restrict__ Dt,
+                                float* __restrict__ Lt) {
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= static_cast<int64_t>(C) * Hq) return;
+    const uint2 a = reinterpret_cast<const uint2*>(o + row * kHd)[lane];
+    const uint2 b = reinterpret_cast<const uint2*>(dout + row * kHd)[lane];
+    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const float2 fa = __bfloat1622float2(a2[i]);
+        const float2 fb = __bfloat1622float2(b2[i]);
+        s += fa.x * fb.x + fa.y * fb.y;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) {
+        const int t = static_cast<int>(row / Hq), h = static_cast<int>(row % Hq);
+        Dt[static_cast<int64_t>(h) * C + t] = s;
+        Lt[static_cast<int64_t>(h) * C + t] = lse[row] * kLog2e;
+    }
+}
+
+__global__ void bwd_mask_kernel(const int32_t* __restrict__ off, const int32_t* __restrict__ ids, int max_pages,
+                                uint64_t* __restrict__ mask, int* err) {
+    const int qp = blockIdx.x;
+    for (int i = off[qp] + threadIdx.x; i < off[qp + 1]; i += blockDim.x) {
+        const int pid = ids[i];
+        if (pid < 0 || pid >= max_pages) {
+            atomicOr(err, DERR_BAD_ID);
+            continue;
+        }
+        atomicOr(reinterpret_cast<unsigned long long*>(mask + pid), 1ull << qp);
+    }
+}
+
+__global__ void __launch_bounds__(1024) bwd_union_kernel(const uint64_t* __restrict__ mask, int n_pages,
+                                                         int32_t* __restrict__ uni, int32_t* __restrict__ n_uni) {
+    using Scan = cub::BlockScan<int, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n_pages; base += 1024) {
+        const int p = base + threadIdx.x;
+        const int f = (p < n_pages && mask[p] != 0ull) ? 1 : 0;
+        int pos, total;
+        Scan(tmp).ExclusiveSum(f, pos, total);
+        if (f) uni[carry + pos] = p;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *n_uni = carry;
+}
+
+// ===========================================================================
+// dQ kernel (query-major)
+// ===========================================================================
+constexpr int kDqQ = 0;
+constexpr int kDqDO = kDqQ + kTileBytes;
+constexpr int kDqK = kDqDO + kTileBytes;        // 2 stages
+constexpr int kDqV = kDqK + 2 * kTileBytes;     // 2 stages
+constexpr int kDqDS = kDqV + 2 * kTileBytes;    // 1 buffer
+constexpr int kDqBar = kDqDS + kTileBytes;
+constexpr int kDqSmem = kDqBar + 256 + 1024;
+
+struct DqBars {
+    uint64_t q_full;
+    uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
+    uint64_t s_full, s_free, dp_full, dp_free, ds_full, ds_empty, dq_done;
+    uint32_t tmem_base;
+};
+
+struct BwdParams {
+    AttnGeom g;
+    const int32_t* sel_off;
+    const int32_t* sel_ids;
+    const int32_t* kvslot;
+    const int32_t* gslot;
+    float* gk;
+    float* gv;
+    const float* Dt;
+    const float* Lt;
+    const uint64_t* mask;
+    const int32_t* uni;
+    const int32_t* n_uni;
+    float* dq;
+    float* dk_cur;
+    float* dv_cur;
+    int* err;
+};
+
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                       const __grid_constant__ CUtensorMap tm_kc, const __grid_constant__ CUtensorMap tm_vc,
+                       const __grid_constant__ CUtensorMap tm_kp, const __grid_constant__ CUtensorMap tm_vp,
+                       BwdParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    DqBars* bars = reinterpret_cast<DqBars*>(smem + kDqBar);
+    const AttnGeom& g = p.g;
+    const int h = blockIdx.x;
+    const int qt = (g.C / kTile) - 1 - blockIdx.y;  // longest causal prefixes first
+    const int kvh = h / g.group;
+    const int qp = (qt * kTile) / g.P;
+    const int sel_begin = p.sel_off[qp];
+    const int n_past = (p.sel_off[qp + 1] - sel_begin) * (g.P / kTile);
+    const int nb = n_past + qt + 1;
+    const int warp = warp_id(), lane = lane_id();
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars->q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bars->k_full[i], 1);
+            mbar_init(&bars->k_empty[i], 1);
+            mbar_init(&bars->v_full[i], 1);
+            mbar_init(&bars->v_empty[i], 1);
+        }
+        mbar_init(&bars->s_full, 1);
+        mbar_init(&bars->s_free, 128);
+        mbar_init(&bars->dp_full, 1);
+        mbar_init(&bars->dp_free, 128);
+        mbar_init(&bars->ds_full, 128);
+        mbar_init(&bars->ds_empty, 1);
+        mbar_init(&bars->dq_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 3) tmem_alloc<512>(&bars->tmem_base);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem_base;
+    const uint32_t tm_s = tmem, tm_dp = tmem + 128, tm_dq = tmem + 256;
+    uint8_t* sQ = smem + kDqQ;
+    uint8_t* sDO = smem + kDqDO;
+    uint8_t* sK = smem + kDqK;
+    uint8_t* sV = smem + kDqV;
+    uint8_t* sDS = smem + kDqDS;
+
+    if (warp == 0) {
+        if (lane == 0) {  // Q, dO, K producer
+            mbar_expect_tx(&bars->q_full, 2 * kTileBytes);
+            for (int r = 0; r < 2; ++r) {
+                tma_load_3d(sQ + r * kRegion, &tm_q, &bars->q_full, r * 64, h, qt * kTile);
+                tma_load_3d(sDO + r * kRegion, &tm_do, &bars->q_full, r * 64, h, qt * kTile);
+            }
+            for (int j = 0; j < nb; ++j) {
+                const int st = j & 1;
+                if (j >= 2) mbar_wait(&bars->k_empty[st], ((j - 2) >> 1) & 1);
+                mbar_expect_tx(&bars->k_full[st], kTileBytes);
+                uint8_t* dst = sK + st * kTileBytes;
+                if (j < n_past) {
+                    const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, j, kvh, p.err);
+                    for (int r = 0; r < 2; ++r) tma_load_2d(dst + r * kRegion, &tm_kp, &bars->k_full[st], r * 64, b.row);
+                } else {
+                    for (int r = 0; r < 2; ++r)
+                        tma_load_3d(dst + r * kRegion, &tm_kc, &bars->k_full[st], r * 64, kvh, (j - n_past) * kTile);
+                }
+            }
+        }
+    } else if (warp == 2) {
+        if (lane == 0) {  // V producer
+            for (int j = 0; j < nb; ++j) {
+                const int st = j & 1;
+                if (j >= 2) mbar_wait(&bars->v_empty[st], ((j - 2) >> 1) & 1);
+                mbar_expect_tx(&bars->v_full[st], kTileBytes);
+                uint8_t* dst = sV + st * kTileBytes;
+                if (j < n_past) {
+                    const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, j, kvh, nullptr);
+                    for (int r = 0; r < 2; ++r) tma_load_2d(dst + r * kRegion, &tm_vp, &bars->v_full[st], r * 64, b.row);
+                } else {
+                    for (int r = 0; r < 2; ++r)
+                        tma_load_3d(dst + r * kRegion, &tm_vc, &bars->v_full[st], r * 64, kvh, (j - n_past) * kTile);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kTile, 0, 0);
+        constexpr uint32_t idesc_dq = make_idesc_bf16(kTile, kHd, 0, 1);
+        const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO), ds_addr = smem_u32(sDS);
+        mbar_wait(&bars->q_full, 0);
+        for (int j = 0; j <= nb; ++j) {
+            if (j < nb) {
+                const int st = j & 1;
+                mbar_wait(&bars->k_full[st], (j >> 1) & 1);
+                if (j >= 1) mbar_wait(&bars->s_free, (j - 1) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t k_addr = smem_u32(sK + st * kTileBytes);
+                    for (int ks = 0; ks < kHd / 16; ++ks)
+                        umma_f16_ss(tm_s, desc_k(q_addr, ks, kRegion), desc_k(k_addr, ks, kRegion), idesc_s, ks > 0);
+                    umma_commit(&bars->s_full);
+                }
+                __syncwarp();
+                mbar_wait(&bars->v_full[st], (j >> 1) & 1);
+                if (j >= 1) mbar_wait(&bars->dp_free, (j - 1) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t v_addr = smem_u32(sV + st * kTileBytes);
+                    for (int ks = 0; ks < kHd / 16; ++ks)
+                        umma_f16_ss(tm_dp, desc_k(do_addr, ks, kRegion), desc_k(v_addr, ks, kRegion), idesc_s,
+                                    ks > 0);
+                    umma_commit(&bars->dp_full);
+                    umma_commit(&bars->v_empty[st]);
+                }
+                __syncwarp();
+            }
+            if (j >= 1) {
+                const int i = j - 1, st = i & 1;
+                mbar_wait(&bars->ds_full, i & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t k_addr = smem_u32(sK + st * kTileBytes);
+                    for (int ks = 0; ks < kTile / 16; ++ks)
+                        umma_f16_ss(tm_dq, desc_k(ds_addr, ks, kRegion), desc_mn(k_addr, ks, kRegion), idesc_dq,
+                                    (i > 0 || ks > 0) ? 1u : 0u);
+                    umma_commit(&bars->k_empty[st]);
+                    umma_commit(&bars->ds_empty);
+                    if (j == nb) umma_commit(&bars->dq_done);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp >= 4) {
+        const int quarter = warp & 3;
+        const int r = quarter * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        const int t = qt * kTile + r;
+        const float sl2 = g.scale * kLog2e;
+        const float L2 = p.Lt[static_cast<int64_t>(h) * g.C + t];
+        const float Dr = p.Dt[static_cast<int64_t>(h) * g.C + t];
+        for (int j = 0; j < nb; ++j) {
+            int lim;
+            if (j < n_past) {
+                const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, j, kvh, nullptr);
+                lim = b.n_valid - 1;
+            } else {
+                lim = (j - n_past == qt) ? r : kTile - 1;
+            }
+            mbar_wait(&bars->s_full, j & 1);
+            tc_fence_after();
+            float pr[kTile];
+#pragma unroll
+            for (int c = 0; c < kTile / 16; ++c)
+                tmem_ld16(tm_s + c * 16 + lane_off, *reinterpret_cast<uint32_t(*)[16]>(&pr[c * 16]));
+            tmem_wait_ld();
+            tc_fence_before();
+            mbar_arrive(&bars->s_free);
+#pragma unroll
+            for (int c = 0; c < kTile; ++c) {
+                const float e = ex2(pr[c] * sl2 - L2);
+                pr[c] = (c <= lim) ? e : 0.f;
+            }
+            mbar_wait(&bars->dp_full, j & 1);
+            if (j >= 1) mbar_wait(&bars->ds_empty, (j - 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < kTile / 16; ++c) {
+                uint32_t dp[16];
+                tmem_ld16(tm_dp + c * 16 + lane_off, dp);
+                tmem_wait_ld();
+                float ds[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) ds[u] = pr[c * 16 + u] * (__uint_as_float(dp[u]) - Dr);
+                st_sw128(sDS, kRegion, r, 2 * c, pack8(ds));
+                st_sw128(sDS, kRegion, r, 2 * c + 1, pack8(ds + 8));
+            }
+            tc_fence_before();
+            mbar_arrive(&bars->dp_free);
+            fence_proxy_async_smem();
+            mbar_arrive(&bars->ds_full);
+        }
+        mbar_wait(&bars->dq_done, 0);
+        tc_fence_after();
+        float* dqrow = p.dq + (static_cast<int64_t>(t) * g.Hq + h) * kHd;
+#pragma unroll 1
+        for (int c = 0; c < kHd / 16; ++c) {
+            uint32_t v[16];
+            tmem_ld16(tm_dq + c * 16 + lane_off, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 16; u += 4)
+                *reinterpret_cast<float4*>(dqrow + c * 16 + u) =
+                    make_float4(__uint_as_float(v[u]) * g.scale, __uint_as_float(v[u + 1]) * g.scale,
+                                __uint_as_float(v[u + 2]) * g.scale, __uint_as_float(v[u + 3]) * g.scale);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 3) tmem_dealloc<512>(tmem);
+}
+
+// ===========================================================================
+// dK/dV kernel (key-major, one CTA per (key block, kv head))
+// ===========================================================================
+constexpr int kKvK = 0;
+constexpr int kKvV = kKvK + kTileBytes;
+constexpr int kKvQ = kKvV + kTileBytes;          // 2 stages of [64 x 128]
+constexpr int kKvDO = kKvQ + 2 * kTile64;        // 2 stages
+constexpr int kKvP = kKvDO + 2 * kTile64;        // 2 buffers of P^T [128 x 64]
+constexpr int kKvDS = kKvP + 2 * kPT;            // 2 buffers of dS^T
+constexpr int kKvQps = kKvDS + 2 * kPT;          // query-page list (<= 64 ints)
+constexpr int kKvBar = kKvQps + 256;
+constexpr int kKvSmem = kKvBar + 256 + 1024;
+
+struct KvBars {
+    uint64_t kv_full;
+    uint64_t qdo_full[2], qdo_empty[2];
+    uint64_t sdp_full[2], sdp_free[2];
+    uint64_t pds_full[2], pds_empty[2];
+    uint64_t acc_done;
+    uint32_t tmem_base;
+};
+
+// Work unit of a dK/dV CTA: in-chunk key block b, or past page block (union index, sub).
+struct KvUnit {
+    bool valid;
+    bool past;
+    int key0;       // first key index of the block (chunk-relative for in-chunk, page-relative for past)
+    int pid;
+    int sub;
+    int n_items;
+    int n_qps;      // past: number of query pages in the list
+    int tiles_per_qp;
+};
+
+__device__ __forceinline__ void item_of(const BwdParams& p, const KvUnit& u, const int* qps, int i, int g_kv, int* h,
+                                        int* qt64, bool* diag) {
+    const int G = p.g.group;
+    if (!u.past) {
+        const int b = u.key0 / kTile;
+        *qt64 = 2 * b + i / G;
+        *h = g_kv * G + i % G;
+        *diag = *qt64 < 2 * b + 2;
+    } else {
+        const int per_qp = u.tiles_per_qp * G;
+        const int qp = qps[i / per_qp];
+        const int rem = i % per_qp;
+        *qt64 = qp * u.tiles_per_qp + rem / G;
+        *h = g_kv * G + rem % G;
+        *diag = false;
+    }
+}
+
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_constant__ CUtensorMap tm_do64,
+                         const __grid_constant__ CUtensorMap tm_kc, const __grid_constant__ CUtensorMap tm_vc,
+                         const __grid_constant__ CUtensorMap tm_kp, const __grid_constant__ CUtensorMap tm_vp,
+                         BwdParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    KvBars* bars = reinterpret_cast<KvBars*>(smem + kKvBar);
+    int* qps = reinterpret_cast<int*>(smem + kKvQps);
+    const AttnGeom& g = p.g;
+    const int g_kv = blockIdx.y;
+    const int n_chunk_blocks = g.C / kTile;
+    const int bpp = g.P / kTile;
+    const int warp = warp_id(), lane = lane_id();
+
+    // ---- decode the work unit (uniform across the CTA)
+    KvUnit u{};
+    u.tiles_per_qp = g.P / kQ64;
+    if (static_cast<int>(blockIdx.x) < n_chunk_blocks) {
+        const int b = blockIdx.x;
+        u.valid = true;
+        u.past = false;
+        u.key0 = b * kTile;
+        u.n_items = (g.C / kQ64 - 2 * b) * g.group;
+    } else {
+        const int pu = blockIdx.x - n_chunk_blocks;
+        const int idx = pu / bpp;
+        u.valid = idx < *p.n_uni;
+        if (u.valid) {
+            u.past = true;
+            u.pid = p.uni[idx];
+            u.sub = pu % bpp;
+            u.key0 = u.sub * kTile;
+            const uint64_t m = p.mask[u.pid];
+            u.n_qps = __popcll(m);
+            u.n_items = u.n_qps * u.tiles_per_qp * g.group;
+            if (threadIdx.x == 0) {
+                int k = 0;
+                for (int qp = 0; qp < 64; ++qp)
+                    if (m & (1ull << qp)) qps[k++] = qp;
+            }
+        }
+    }
+    if (!u.valid) return;
+
+    int kv_slot = 0, g_slot = -1, n_valid = kTile;
+    if (u.past) {
+        kv_slot = p.kvslot[u.pid];
+        g_slot = p.gslot[u.pid];
+        const int64_t nv = g.filled - static_cast<int64_t>(u.pid) * g.P - u.key0;
+        n_valid = static_cast<int>(nv < 0 ? 0 : (nv > kTile ? kTile : nv));
+        if (kv_slot < 0 || g_slot < 0) {
+            if (threadIdx.x == 0) atomicOr(p.err, DERR_NOT_RESIDENT);
+            return;
+        }
+    }
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars->kv_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bars->qdo_full[i], 1);
+            mbar_init(&bars->qdo_empty[i], 1);
+            mbar_init(&bars->sdp_full[i], 1);
+            mbar_init(&bars->sdp_free[i], 128);
+            mbar_init(&bars->pds_full[i], 128);
+            mbar_init(&bars->pds_empty[i], 1);
+        }
+        mbar_init(&bars->acc_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 3) tmem_alloc<512>(&bars->tmem_base);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem_base;
+    // TMEM: S^T [0,64) [64,128), dP^T [128,192) [192,256), dK [256,384), dV [384,512)
+    const uint32_t tm_s = tmem, tm_dp = tmem + 128, tm_dk = tmem + 256, tm_dv = tmem + 384;
+    uint8_t* sK = smem + kKvK;
+    uint8_t* sV = smem + kKvV;
+    uint8_t* sQ = smem + kKvQ;
+    uint8_t* sDO = smem + kKvDO;
+    uint8_t* sP = smem + kKvP;
+    uint8_t* sDS = smem + kKvDS;
+    const int n_items = u.n_items;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(&bars->kv_full, 2 * kTileBytes);
+            if (u.past) {
+                const int row = (kv_slot * g.Hkv + g_kv) * g.P + u.key0;
+                for (int r = 0; r < 2; ++r) {
+                    tma_load_2d(sK + r * kRegion, &tm_kp, &bars->kv_full, r * 64, row);
+                    tma_load_2d(sV + r * kRegion, &tm_vp, &bars->kv_full, r * 64, row);
+                }
+            } else {
+                for (int r = 0; r < 2; ++r) {
+                    tma_load_3d(sK + r * kRegion, &tm_kc, &bars->kv_full, r * 64, g_kv, u.key0);
+                    tma_load_3d(sV + r * kRegion, &tm_vc, &bars->kv_full, r * 64, g_kv, u.key0);
+                }
+            }
+            for (int i = 0; i < n_items; ++i) {
+                const int st = i & 1;
+                int h, qt64;
+                bool diag;
+                item_of(p, u, qps, i, g_kv, &h, &qt64, &diag);
+                if (i >= 2) mbar_wait(&bars->qdo_empty[st], ((i - 2) >> 1) & 1);
+                mbar_expect_tx(&bars->qdo_full[st], 2 * kTile64);
+                for (int r = 0; r < 2; ++r) {
+                    tma_load_3d(sQ + st * kTile64 + r * kRegion64, &tm_q64, &bars->qdo_full[st], r * 64, h,
+                                qt64 * kQ64);
+                    tma_load_3d(sDO + st * kTile64 + r * kRegion64, &tm_do64, &bars->qdo_full[st], r * 64, h,
+                                qt64 * kQ64);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kQ64, 0, 0);   // [128 keys] x [64 q], K = hd
+        constexpr uint32_t idesc_g = make_idesc_bf16(kTile, kHd, 0, 1);    // [128 keys] x [hd], K = 64 q
+        const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+        mbar_wait(&bars->kv_full, 0);
+        for (int i = 0; i <= n_items; ++i) {
+            if (i < n_items) {
+                const int st = i & 1;
+                mbar_wait(&bars->qdo_full[st], (i >> 1) & 1);
+                if (i >= 2) mbar_wait(&bars->sdp_free[st], ((i - 2) >> 1) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t q_addr = smem_u32(sQ + st * kTile64), do_addr = smem_u32(sDO + st * kTile64);
+                    for (int ks = 0; ks < kHd / 16; ++ks)
+                        umma_f16_ss(tm_s + st * kQ64, desc_k(k_addr, ks, kRegion), desc_k(q_addr, ks, kRegion64),
+                                    idesc_s, ks > 0);
+                    for (int ks = 0; ks < kHd / 16; ++ks)
+                        umma_f16_ss(tm_dp + st * kQ64, desc_k(v_addr, ks, kRegion), desc_k(do_addr, ks, kRegion64),
+                                    idesc_s, ks > 0);
+                    umma_commit(&bars->sdp_full[st]);
+                }
+                __syncwarp();
+            }
+            if (i >= 1) {
+                const int j = i - 1, st = j & 1;
+                mbar_wait(&bars->pds_full[st], (j >> 1) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t p_addr = smem_u32(sP + st * kPT), ds_addr = smem_u32(sDS + st * kPT);
+                    const uint32_t q_addr = smem_u32(sQ + st * kTile64), do_addr = smem_u32(sDO + st * kTile64);
+                    for (int ks = 0; ks < kQ64 / 16; ++ks)
+                        umma_f16_ss(tm_dv, desc_k(p_addr, ks, kPT), desc_mn(do_addr, ks, kRegion64), idesc_g,
+                                    (j > 0 || ks > 0) ? 1u : 0u);
+                    for (int ks = 0; ks < kQ64 / 16; ++ks)
+                        umma_f16_ss(tm_dk, desc_k(ds_addr, ks, kPT), desc_mn(q_addr, ks, kRegion64), idesc_g,
+                                    (j > 0 || ks > 0) ? 1u : 0u);
+                    umma_commit(&bars->qdo_empty[st]);
+                    umma_commit(&bars->pds_empty[st]);
+                    if (i == n_items) umma_commit(&bars->acc_done);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp >= 4) {
+        const int quarter = warp & 3;
+        const int kr = quarter * 32 + lane;  // key row of the block
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        const float sl2 = g.scale * kLog2e;
+        const bool key_ok = kr < n_valid;
+        const int key_abs = u.key0 + kr;  // chunk-relative key index (in-chunk blocks)
+        for (int i = 0; i < n_items; ++i) {
+            const int st = i & 1;
+            int h, qt64;
+            bool diag;
+            item_of(p, u, qps, i, g_kv, &h, &qt64, &diag);
+            const int q0 = qt64 * kQ64;
+            const float* Lrow = p.Lt + static_cast<int64_t>(h) * g.C + q0;
+            const float* Drow = p.Dt + static_cast<int64_t>(h) * g.C + q0;
+            mbar_wait(&bars->sdp_full[st], (i >> 1) & 1);
+            tc_fence_after();
+            float s[kQ64], dp[kQ64];
+#pragma unroll
+            for (int c = 0; c < kQ64 / 16; ++c) {
+                tmem_ld16(tm_s + st * kQ64 + c * 16 + lane_off, *reinterpret_cast<uint32_t(*)[16]>(&s[c * 16]));
+                tmem_ld16(tm_dp + st * kQ64 + c * 16 + lane_off, *reinterpret_cast<uint32_t(*)[16]>(&dp[c * 16]));
+            }
+            tmem_wait_ld();
+            tc_fence_before();
+            mbar_arrive(&bars->sdp_free[st]);
+            if (i >= 2) mbar_wait(&bars->pds_empty[st], ((i - 2) >> 1) & 1);
+            uint8_t* pb = sP + st * kPT;
+            uint8_t* db = sDS + st * kPT;
+#pragma unroll
+            for (int c8 = 0; c8 < kQ64 / 8; ++c8) {
+                const float4 l0 = *reinterpret_cast<const float4*>(Lrow + c8 * 8);
+                const float4 l1 = *reinterpret_cast<const float4*>(Lrow + c8 * 8 + 4);
+                const float4 d0 = *reinterpret_cast<const float4*>(Drow + c8 * 8);
+                const float4 d1 = *reinterpret_cast<const float4*>(Drow + c8 * 8 + 4);
+                const float lv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+                const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+                float pe[8], de[8];
+#pragma unroll
+                for (int u8 = 0; u8 < 8; ++u8) {
+                    const int c = c8 * 8 + u8;
+                    float e = ex2(s[c] * sl2 - lv[u8]);
+                    const bool vis = key_ok && (!diag || key_abs <= q0 + c);
+                    e = vis ? e : 0.f;
+                    pe[u8] = e;
+                    de[u8] = e * (dp[c] - dv[u8]);
+                }
+                st_sw128(pb, kPT, kr, c8, pack8(pe));
+                st_sw128(db, kPT, kr, c8, pack8(de));
+            }
+            fence_proxy_async_smem();
+            mbar_arrive(&bars->pds_full[st]);
+        }
+        // ---- epilogue: one RMW of the fp32 gradient page / store of dk_cur, dv_cur
+        mbar_wait(&bars->acc_done, 0);
+        tc_fence_after();
+        float *dkrow, *dvrow;
+        if (u.past) {
+            const int64_t base = ((static_cast<int64_t>(g_slot) * g.Hkv + g_kv) * g.P + u.key0 + kr) * kHd;
+            dkrow = p.gk + base;
+            dvrow = p.gv + base;
+        } else {
+            const int64_t base = (static_cast<int64_t>(key_abs) * g.Hkv + g_kv) * kHd;
+            dkrow = p.dk_cur + base;
+            dvrow = p.dv_cur + base;
+        }
+#pragma unroll 1
+        for (int c = 0; c < kHd / 16; ++c) {
+            uint32_t vk[16], vv[16];
+            tmem_ld16(tm_dk + c * 16 + lane_off, vk);
+            tmem_ld16(tm_dv + c * 16 + lane_off, vv);
+            tmem_wait_ld();
+            if (!key_ok) continue;
+#pragma unroll
+            for (int u4 = 0; u4 < 16; u4 += 4) {
+                float4 k4 = make_float4(__uint_as_float(vk[u4]) * g.scale, __uint_as_float(vk[u4 + 1]) * g.scale,
+                                        __uint_as_float(vk[u4 + 2]) * g.scale, __uint_as_float(vk[u4 + 3]) * g.scale);
+                float4 v4 = make_float4(__uint_as_float(vv[u4]), __uint_as_float(vv[u4 + 1]),
+                                        __uint_as_float(vv[u4 + 2]), __uint_as_float(vv[u4 + 3]));
+                float4* pk = reinterpret_cast<float4*>(dkrow + c * 16 + u4);
+                float4* pv = reinterpret_cast<float4*>(dvrow + c * 16 + u4);
+                if (u.past) {
+                    const float4 ok = *pk, ov = *pv;
+                    k4 = make_float4(ok.x + k4.x, ok.y + k4.y, ok.z + k4.z, ok.w + k4.w);
+                    v4 = make_float4(ov.x + v4.x, ov.y + v4.y, ov.z + v4.z, ov.w + v4.w);
+                }
+                *pk = k4;
+                *pv = v4;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 3) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace
+
+bool tc_bwd_available() { return true; }
+
+size_t attn_bwd_tc_workspace(const AttnGeom& g, int) {
+    const size_t hc = static_cast<size_t>(g.Hq) * g.C * sizeof(float);
+    return ((2 * hc + 255) & ~size_t(255)) + static_cast<size_t>(g.max_pages) * 12 + 256;
+}
+
+void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* dout, const void* q,
+                        const int32_t* sel_off, const int32_t* sel_ids, const int32_t* d_kvslot_layer,
+                        const int32_t* d_gslot_layer, float* gkpool, float* gvpool, const void* k_cur,
+                        const void* v_cur, const void* out, const float* lse, float* dq, float* dk_cur,
+                        float* dv_cur, int* d_err, void* workspace, size_t workspace_bytes, int nnz, int n_pages,
+                        cudaStream_t st) {
+    OOMB_REQUIRE(workspace_bytes >= attn_bwd_tc_workspace(g, nnz), OOMB_ERROR, "bwd workspace too small");
+    OOMB_REQUIRE(g.m <= 64, OOMB_CONFIG_ERROR, "tcgen05 backward supports at most 64 query pages per chunk");
+    static bool attr = false;
+    if (!attr) {
+        OOMB_CUDA(cudaFuncSetAttribute(attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDqSmem));
+        OOMB_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kKvSmem));
+        attr = true;
+    }
+    BwdWs w = carve(g, workspace);
+    ProfScope* prep_scope = new ProfScope(PK_BWD_PREP, st);
+    const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
+    bwd_prep_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), lse, g.C, g.Hq, w.Dt, w.Lt);
+    check_launch("bwd_prep_kernel");
+    if (n_pages > 0) OOMB_CUDA(cudaMemsetAsync(w.mask, 0, static_cast<size_t>(n_pages) * 8, st));
+    OOMB_CUDA(cudaMemsetAsync(w.n_uni, 0, sizeof(int32_t), st));
+    if (nnz > 0) {
+        bwd_mask_kernel<<<g.m, 128, 0, st>>>(sel_off, sel_ids, g.max_pages, w.mask, d_err);
+        check_launch("bwd_mask_kernel");
+        bwd_union_kernel<<<1, 1024, 0, st>>>(w.mask, n_pages, w.uni, w.n_uni);
+        check_launch("bwd_union_kernel");
+    }
+    const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, kHd);
+    const CUtensorMap tdo = map_rows_heads(dout, g.C, g.Hq, kHd);
+    const CUtensorMap tq64 = map_rows_heads(q, g.C, g.Hq, kHd, kQ64);
+    const CUtensorMap tdo64 = map_rows_heads(dout, g.C, g.Hq, kHd, kQ64);
+    const CUtensorMap tkc = map_rows_heads(k_cur, g.C, g.Hkv, kHd);
+    const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, kHd);
+    BwdParams p{g, sel_off, sel_ids, d_kvslot_layer, d_gslot_layer, gkpool, gvpool, w.Dt, w.Lt, w.mask, w.uni,
+                w.n_uni, dq, dk_cur, dv_cur, d_err};
+    delete prep_scope;
+    {
+        ProfScope s_(PK_BWD_DQ, st);
+        attn_bwd_dq_kernel<<<dim3(g.Hq, g.C / kTile), 256, kDqSmem, st>>>(tq, tdo, tkc, tvc, maps.kpool, maps.vpool,
+                                                                          p);
+        check_launch("attn_bwd_dq_kernel");
+    }
+    {
+        ProfScope s_(PK_BWD_DKDV, st);
+        const int max_union = std::min(nnz, n_pages);
+        const int units = g.C / kTile + max_union * (g.P / kTile);
+        attn_bwd_dkdv_kernel<<<dim3(units, g.Hkv), 256, kKvSmem, st>>>(tq64, tdo64, tkc, tvc, maps.kpool,
+                                                                       maps.vpool, p);
+        check_launch("attn_bwd_dkdv_kernel");
+    }
+}
+
+}  // namespace oomb

@@ -380,6 +380,7 @@ __global__ void __launch_bounds__(256, 1)
 void launch_attn_fwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* q, const int32_t* sel_off,
                         const int32_t* sel_ids, const int32_t* d_kvslot_layer, const void* k_cur, const void* v_cur,
                         void* out, float* lse, int* d_err, cudaStream_t st) {
+    ProfScope prof_(PK_FWD, st);
     static bool attr_set = false;
     if (!attr_set) {
         OOMB_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem));
@@ -392,17 +393,6 @@ void launch_attn_fwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* q
     dim3 grid(g.Hq, g.C / kTile);
     attn_fwd_tc_kernel<<<grid, 256, kFwdSmem, st>>>(tq, tkc, tvc, maps.kpool, maps.vpool, p);
     check_launch("attn_fwd_tc_kernel");
-}
-
-// ===========================================================================
-// Backward (tensor-core path not yet available: the host routes to SIMT)
-// ===========================================================================
-bool tc_bwd_available() { return false; }
-size_t attn_bwd_tc_workspace(const AttnGeom&, int) { return 0; }
-void launch_attn_bwd_tc(const AttnGeom&, const TcPoolMaps&, const void*, const void*, const int32_t*, const int32_t*,
-                        const int32_t*, const int32_t*, float*, float*, const void*, const void*, const void*,
-                        const float*, float*, float*, float*, int*, void*, size_t, cudaStream_t) {
-    throw Error(OOMB_CONFIG_ERROR, "tcgen05 backward not built");
 }
 
 // ===========================================================================

@@ -96,6 +96,7 @@ void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_
                    int hd, int first_page, int n_pages_touched, const NewSlots& ns, int32_t* d_kvslot_layer,
                    void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, cudaStream_t st) {
     if (rows <= 0 || n_pages_touched <= 0) return;
+    ProfScope prof_(PK_APPEND, st);
     const int re = Hkv * hd;
     dim3 grid((re + 127) / 128, n_pages_touched);
     if (dtype == OOMB_BF16)
@@ -126,6 +127,7 @@ __global__ void mean_keys_kernel(const float* __restrict__ sum, const int32_t* _
 void launch_mean_keys(const float* kavg_sum_layer, const int32_t* kavg_cnt_layer, int n, int row_elems, float* out,
                       cudaStream_t st) {
     if (n <= 0) return;
+    ProfScope prof_(PK_OTHER, st);
     const int64_t tot = static_cast<int64_t>(n) * row_elems;
     mean_keys_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(kavg_sum_layer, kavg_cnt_layer, n,
                                                                               row_elems, out);
@@ -170,6 +172,7 @@ void launch_gather(int dtype, int grads, const int32_t* d_ids, int n, const int3
                    const void* pv, int64_t filled, int P, int Hkv, int hd, void* k_out, void* v_out,
                    uint8_t* valid_out, int* d_err, cudaStream_t st) {
     if (n <= 0) return;
+    ProfScope prof_(PK_GATHER, st);
     const int64_t total = static_cast<int64_t>(n) * P * Hkv * hd;
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 32));
     if (grads) {
@@ -222,10 +225,43 @@ void launch_scatter(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, f
                     const float* dk, const float* dv, int64_t filled, int P, int Hkv, int hd, int* d_err,
                     cudaStream_t st) {
     if (n <= 0) return;
+    ProfScope prof_(PK_GATHER, st);
     const int64_t total = static_cast<int64_t>(n) * P * Hkv * hd;
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 32));
     scatter_kernel<<<blocks, 256, 0, st>>>(d_ids, n, d_gslot_layer, gk, gv, dk, dv, filled, P, Hkv, hd, d_err);
     check_launch("scatter_kernel");
+}
+
+// dM_i read-back (chunk_trainer.hpp:575-587): dk/dv (reference layout) += grad pages.
+__global__ void accumulate_grads_kernel(const int32_t* __restrict__ ids, int n, const int32_t* __restrict__ gslot,
+                                        const float* __restrict__ gk, const float* __restrict__ gv, int64_t filled,
+                                        int P, int Hkv, int hd, float* __restrict__ dk, float* __restrict__ dv) {
+    const int re = Hkv * hd;
+    const int64_t total = static_cast<int64_t>(n) * P * re;
+    for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(idx / (static_cast<int64_t>(P) * re));
+        const int rem = static_cast<int>(idx - static_cast<int64_t>(i) * P * re);
+        const int s = rem / re, e = rem - (rem / re) * re;
+        const int h = e / hd, d = e - (e / hd) * hd;
+        const int pid = ids[i];
+        const int g = gslot[pid];
+        if (g < 0 || s >= valid_in_page(filled, pid, P)) continue;
+        const size_t src = ((static_cast<size_t>(g) * Hkv + h) * P + s) * hd + d;
+        dk[idx] += gk[src];
+        dv[idx] += gv[src];
+    }
+}
+
+void launch_accumulate_grads(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, const float* gk,
+                             const float* gv, int64_t filled, int P, int Hkv, int hd, float* dk, float* dv,
+                             cudaStream_t st) {
+    if (n <= 0) return;
+    ProfScope prof_(PK_GATHER, st);
+    const int64_t total = static_cast<int64_t>(n) * P * Hkv * hd;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+    accumulate_grads_kernel<<<blocks, 256, 0, st>>>(d_ids, n, d_gslot_layer, gk, gv, filled, P, Hkv, hd, dk, dv);
+    check_launch("accumulate_grads_kernel");
 }
 
 // Lazy gradient pages: publish slot + zero (paged_kv.hpp:148-153).
@@ -249,6 +285,7 @@ __global__ void grad_init_kernel(const int32_t* __restrict__ pages, const int32_
 void launch_grad_init(const int32_t* d_pages, const int32_t* d_slots, int n, int32_t* d_gslot_layer, float* gk,
                       float* gv, int64_t page_elems, cudaStream_t st) {
     if (n <= 0) return;
+    ProfScope prof_(PK_GRAD_INIT, st);
     dim3 grid(static_cast<unsigned>(std::min<int64_t>((page_elems / 4 + 255) / 256, 16)), n);
     grad_init_kernel<<<grid, 256, 0, st>>>(d_pages, d_slots, n, d_gslot_layer, gk, gv, page_elems);
     check_launch("grad_init_kernel");
@@ -327,6 +364,7 @@ __global__ void score_vote_kernel(const T* __restrict__ q, int64_t tokens, int H
 
 void launch_score_simt(int dtype, const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, int64_t n,
                        int Hkv, int P, float scale, float* vote, float* stats_scratch, cudaStream_t st) {
+    ProfScope prof_(PK_SCORE, st);
     const int64_t rows = tokens * Hq;
     const int m = static_cast<int>((tokens + P - 1) / P);
     float2* stats = reinterpret_cast<float2*>(stats_scratch);
@@ -447,6 +485,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restr
 
 void launch_topk(const float* vote, int m, int n, int k, int32_t* sel_off, int32_t* sel_ids, cudaStream_t st) {
     if (m <= 0) return;
+    ProfScope prof_(PK_TOPK, st);
     topk_kernel<<<m, kTopkThreads, 0, st>>>(vote, m, n, k, sel_off, sel_ids);
     check_launch("topk_kernel");
 }
@@ -463,6 +502,7 @@ __global__ void fill_csr_kernel(int32_t* off, int32_t* ids, int m, int first, in
 
 void launch_fill_csr_all(int32_t* off, int32_t* ids, int m, int first, int count, cudaStream_t st) {
     if (m <= 0) return;
+    ProfScope prof_(PK_OTHER, st);
     fill_csr_kernel<<<m, 256, 0, st>>>(off, ids, m, first, count);
     check_launch("fill_csr_kernel");
 }
@@ -630,6 +670,7 @@ __global__ void attn_bwd_simt_kernel(AttnGeom g, const T* __restrict__ dout, con
 void launch_attn_fwd_simt(int dtype, const AttnGeom& g, const void* q, const int32_t* sel_off, const int32_t* sel_ids,
                           const int32_t* d_kvslot_layer, const void* kpool, const void* vpool, const void* k_cur,
                           const void* v_cur, void* out, float* lse, int* d_err, cudaStream_t st) {
+    ProfScope prof_(PK_FWD, st);
     const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
     const unsigned blocks = static_cast<unsigned>((rows + 3) / 4);
     if (dtype == OOMB_BF16) {
@@ -653,6 +694,7 @@ void launch_attn_bwd_simt(int dtype, const AttnGeom& g, const void* dout, const 
                           const void* kpool, const void* vpool, float* gkpool, float* gvpool, const void* k_cur,
                           const void* v_cur, const void* out, const float* lse, float* dq, float* dk_cur,
                           float* dv_cur, int* d_err, cudaStream_t st) {
+    ProfScope prof_(PK_BWD_SIMT, st);
     const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
     const unsigned blocks = static_cast<unsigned>((rows + 3) / 4);
     if (dtype == OOMB_BF16) {

@@ -21,9 +21,13 @@
 namespace oomb {
 
 thread_local std::string g_last_error;
+thread_local Profiler* g_prof = nullptr;
 
 template <class F>
 int guard(F&& f) {
+    struct Reset {
+        ~Reset() { g_prof = nullptr; }
+    } reset_prof;
     try {
         f();
         return OOMB_OK;
@@ -198,6 +202,8 @@ struct oomb_pool_s {
     TcPoolMaps maps;
     void* bwd_ws = nullptr;
     size_t bwd_ws_bytes = 0;
+    bool prof_on = false;
+    Profiler prof;
 
     int32_t* kvslot_layer(int l) { return d_kvslot + static_cast<int64_t>(l) * max_pages; }
     int32_t* gslot_layer(int l) { return d_gslot + static_cast<int64_t>(l) * max_pages; }
@@ -242,7 +248,10 @@ void validate_cfg(const oomb_config& c) {  // ModelConfig::validate (config.cpp:
     req(c.max_tokens >= 1, "max_tokens must be >= 1");
 }
 
-void set_dev(oomb_pool_s* p) { OOMB_CUDA(cudaSetDevice(p->device)); }
+void set_dev(oomb_pool_s* p) {
+    OOMB_CUDA(cudaSetDevice(p->device));
+    g_prof = p->prof_on ? &p->prof : nullptr;
+}
 
 int32_t pop_slot(std::vector<int32_t>& fl, const char* what) {
     OOMB_REQUIRE(!fl.empty(), OOMB_CONFIG_ERROR,
@@ -450,6 +459,11 @@ int oomb_pool_destroy(oomb_pool_t p) {
     cudaFree(p->d_kavg_cnt);
     cudaFree(p->d_err);
     cudaFree(p->bwd_ws);
+    for (auto& r : p->prof.recs) {
+        cudaEventDestroy(r.e0);
+        cudaEventDestroy(r.e1);
+    }
+    for (auto e : p->prof.spare) cudaEventDestroy(e);
     delete p->pt;
     delete p;
     return OOMB_OK;
@@ -877,7 +891,8 @@ int oomb_attn_backward(oomb_pool_t p, int layer, const void* dout, const void* q
             }
             launch_attn_bwd_tc(g, p->maps, dout, q, sel->d_off, sel->d_ids, p->kvslot_layer(layer),
                                p->gslot_layer(layer), p->gkpool, p->gvpool, k_cur, v_cur, out, lse, dq, dk_cur,
-                               dv_cur, p->d_err, p->bwd_ws, p->bwd_ws_bytes, S(stream));
+                               dv_cur, p->d_err, p->bwd_ws, p->bwd_ws_bytes, sel->nnz,
+                               static_cast<int>(p->pt->pages[layer].size()), S(stream));
         } else {
             OOMB_CUDA(cudaMemsetAsync(dk_cur, 0, kvb, S(stream)));
             OOMB_CUDA(cudaMemsetAsync(dv_cur, 0, kvb, S(stream)));
@@ -885,6 +900,45 @@ int oomb_attn_backward(oomb_pool_t p, int layer, const void* dout, const void* q
                                  p->gslot_layer(layer), p->kpool, p->vpool, p->gkpool, p->gvpool, k_cur, v_cur, out,
                                  lse, dq, dk_cur, dv_cur, p->d_err, S(stream));
         }
+    });
+}
+
+int oomb_accumulate_grad_pages(oomb_pool_t p, int layer, const int32_t* ids, int n, float* dk, float* dv,
+                               void* stream) {
+    return guard([&] {
+        set_dev(p);
+        p->pt->check_ids(layer, ids, n, p->enforce, "gather_grad_pages");
+        if (n == 0) return;
+        int32_t* d = upload_ids(ids, n, S(stream));
+        launch_accumulate_grads(d, n, p->gslot_layer(layer), p->gkpool, p->gvpool, p->pt->filled[layer],
+                                p->cfg.page_size, p->cfg.n_kv_heads, p->cfg.head_dim, dk, dv, S(stream));
+        OOMB_CUDA(cudaFreeAsync(d, S(stream)));
+    });
+}
+
+int oomb_profile_enable(oomb_pool_t p, int on) {
+    return guard([&] { p->prof_on = on != 0; });
+}
+
+int oomb_profile_collect(oomb_pool_t p, int64_t* counts, double* ms, int n_kinds) {
+    return guard([&] {
+        OOMB_CUDA(cudaSetDevice(p->device));
+        OOMB_CUDA(cudaDeviceSynchronize());
+        for (int k = 0; k < n_kinds; ++k) {
+            counts[k] = 0;
+            ms[k] = 0.0;
+        }
+        for (auto& r : p->prof.recs) {
+            float t = 0.f;
+            OOMB_CUDA(cudaEventElapsedTime(&t, r.e0, r.e1));
+            if (r.kind < n_kinds) {
+                counts[r.kind] += 1;
+                ms[r.kind] += t;
+            }
+            p->prof.spare.push_back(r.e0);
+            p->prof.spare.push_back(r.e1);
+        }
+        p->prof.recs.clear();
     });
 }
 

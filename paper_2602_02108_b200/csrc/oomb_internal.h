@@ -39,6 +39,53 @@ extern std::atomic<int64_t> g_kernel_launches;
 inline void count_launch(int n = 1) { g_kernel_launches.fetch_add(n, std::memory_order_relaxed); }
 void check_launch(const char* what);
 
+// ---------------------------------------------------------------------------
+// Per-kernel CUDA-event timing (oomb_profile_*). A launcher brackets its kernel
+// with a ProfScope; events are recorded only while a pool with profiling on is
+// the active pool of the calling thread.
+// ---------------------------------------------------------------------------
+enum ProfKind {
+    PK_APPEND = 0, PK_SCORE, PK_TOPK, PK_FWD, PK_BWD_PREP, PK_BWD_DQ, PK_BWD_DKDV, PK_BWD_SIMT, PK_GRAD_INIT,
+    PK_GATHER, PK_OTHER, PK_N
+};
+struct Profiler {
+    struct Rec {
+        int kind;
+        cudaEvent_t e0, e1;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> spare;
+    cudaEvent_t get() {
+        if (!spare.empty()) {
+            cudaEvent_t e = spare.back();
+            spare.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+};
+extern thread_local Profiler* g_prof;
+struct ProfScope {
+    int kind;
+    cudaStream_t st;
+    cudaEvent_t e0 = nullptr;
+    ProfScope(int k, cudaStream_t s) : kind(k), st(s) {
+        if (g_prof) {
+            e0 = g_prof->get();
+            cudaEventRecord(e0, st);
+        }
+    }
+    ~ProfScope() {
+        if (g_prof && e0) {
+            cudaEvent_t e1 = g_prof->get();
+            cudaEventRecord(e1, st);
+            g_prof->recs.push_back({kind, e0, e1});
+        }
+    }
+};
+
 // Device error flags (bitmask) written by kernels.
 enum : int { DERR_NOT_RESIDENT = 1, DERR_BAD_ID = 2 };
 
@@ -75,6 +122,9 @@ void launch_gather(int dtype, int grads, const int32_t* d_ids, int n, const int3
 void launch_scatter(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, float* gk, float* gv,
                     const float* dk, const float* dv, int64_t filled, int P, int Hkv, int hd, int* d_err,
                     cudaStream_t st);
+void launch_accumulate_grads(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, const float* gk,
+                             const float* gv, int64_t filled, int P, int Hkv, int hd, float* dk, float* dv,
+                             cudaStream_t st);
 void launch_grad_init(const int32_t* d_pages, const int32_t* d_slots, int n, int32_t* d_gslot_layer, float* gk,
                       float* gv, int64_t page_elems, cudaStream_t st);
 void launch_zero_slots(const int32_t* d_slots, int n, float* gk, float* gv, int64_t page_elems, cudaStream_t st);
@@ -113,7 +163,8 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
                         const int32_t* sel_off, const int32_t* sel_ids, const int32_t* d_kvslot_layer,
                         const int32_t* d_gslot_layer, float* gkpool, float* gvpool, const void* k_cur,
                         const void* v_cur, const void* out, const float* lse, float* dq, float* dk_cur,
-                        float* dv_cur, int* d_err, void* workspace, size_t workspace_bytes, cudaStream_t st);
+                        float* dv_cur, int* d_err, void* workspace, size_t workspace_bytes, int nnz, int n_pages,
+                        cudaStream_t st);
 size_t attn_bwd_tc_workspace(const AttnGeom& g, int max_sel_ids);
 void launch_debug_tc_gemm(int mode, const void* a, const void* b, float* c, int m, int n, int k, cudaStream_t st);
 

@@ -1,0 +1,89 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Shared pieces of the tcgen05 attention kernels: tile geometry, SW128 smem
+// layout helpers, UMMA descriptor shortcuts and TMA tensor-map builders.
+#pragma once
+
+#include "oomb_internal.h"
+#include "ptx.cuh"
+
+namespace oomb {
+namespace tc {
+
+constexpr int kTile = 128;               // query rows / keys per block
+constexpr int kHd = 128;                 // head dim of the tensor-core path
+constexpr int kRegion = kTile * 64 * 2;  // [128 x 64] bf16 SW128 region = 16 KB
+constexpr int kTileBytes = 2 * kRegion;  // [128 x 128] bf16 tile = 32 KB
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+// 16-byte chunk c (8 bf16) of row r in a K-major SW128 tile made of [rows x 64]
+// regions of `region_bytes` each (chunk c lives in region c/8).
+__device__ __forceinline__ void st_sw128(uint8_t* tile, int region_bytes, int r, int c, uint4 v) {
+    uint8_t* p = tile + (c >> 3) * region_bytes + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+    *reinterpret_cast<uint4*>(p) = v;
+}
+
+// K-major operand: K step of 16 elements = region kstep/4, +32 B inside the atom.
+__device__ __forceinline__ uint64_t desc_k(uint32_t tile, int kstep, int region_bytes) {
+    return make_sdesc_sw128(tile + (kstep >> 2) * region_bytes + (kstep & 3) * 32, 16, 1024);
+}
+// MN-major B operand stored as [K rows][N] in 64-wide N regions (LBO = region stride);
+// a K step of 16 rows advances 2048 B.
+__device__ __forceinline__ uint64_t desc_mn(uint32_t tile, int kstep, int region_bytes) {
+    return make_sdesc_sw128(tile + kstep * 2048, region_bytes, 1024);
+}
+
+__device__ __forceinline__ uint4 pack8(const float* e) {
+    uint4 pk;
+    pk.x = pack_bf16(e[0], e[1]);
+    pk.y = pack_bf16(e[2], e[3]);
+    pk.z = pack_bf16(e[4], e[5]);
+    pk.w = pack_bf16(e[6], e[7]);
+    return pk;
+}
+
+inline void encode_or_throw(CUtensorMap* m, uint32_t rank, const void* base, const uint64_t* dims,
+                            const uint64_t* strides, const uint32_t* box) {
+    CUresult r = encode_tensor_map(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides,
+                                   box, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (r != CUDA_SUCCESS) throw Error(OOMB_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+
+// [rows][heads][hd] bf16 tensor viewed as 3-D {hd, heads, rows}; box {64, 1, box_rows}.
+inline CUtensorMap map_rows_heads(const void* base, int64_t rows, int heads, int hd, int box_rows = kTile) {
+    CUtensorMap m;
+    const uint64_t dims[3] = {static_cast<uint64_t>(hd), static_cast<uint64_t>(heads), static_cast<uint64_t>(rows)};
+    const uint64_t strides[2] = {static_cast<uint64_t>(hd) * 2, static_cast<uint64_t>(heads) * hd * 2};
+    const uint32_t box[3] = {64, 1, static_cast<uint32_t>(box_rows)};
+    encode_or_throw(&m, 3, base, dims, strides, box);
+    return m;
+}
+
+// Past key block j of a query page: selected page j / bpp, sub-block j % bpp.
+struct PastBlock {
+    int row;      // pool tensor-map row
+    int n_valid;  // valid keys (partially filled pages are masked)
+    int pid;
+};
+__device__ __forceinline__ PastBlock past_block(const AttnGeom& g, const int32_t* sel_ids, const int32_t* kvslot,
+                                                int sel_begin, int j, int kvh, int* err) {
+    const int bpp = g.P / kTile;
+    PastBlock b;
+    b.pid = sel_ids[sel_begin + j / bpp];
+    const int sub = j % bpp;
+    const bool id_ok = b.pid >= 0 && b.pid < g.max_pages;
+    int slot = id_ok ? kvslot[b.pid] : -1;
+    const int64_t nv = g.filled - static_cast<int64_t>(b.pid) * g.P - static_cast<int64_t>(sub) * kTile;
+    b.n_valid = static_cast<int>(nv < 0 ? 0 : (nv > kTile ? kTile : nv));
+    if (slot < 0) {
+        if (err) atomicOr(err, id_ok ? DERR_NOT_RESIDENT : DERR_BAD_ID);
+        slot = 0;
+        b.n_valid = 0;
+    }
+    b.row = (slot * g.Hkv + kvh) * g.P + sub * kTile;
+    return b;
+}
+
+}  // namespace tc
+}  // namespace oomb

@@ -232,6 +232,28 @@ class PagedCache:
         call("oomb_device_slots_get", self.handle, layer, out.ctypes.data_as(C.c_void_p))
         return out[:n]
 
+    def accumulate_grad_pages(self, layer: int, page_ids, dk: torch.Tensor, dv: torch.Tensor, stream=None) -> None:
+        """dM_i read-back (chunk_trainer.hpp:575-587): dk += gather_grad_pages(ids).k, same for dv."""
+        ids = self._ids(page_ids)
+        if dk.dtype != torch.float32 or not dk.is_cuda or not dk.is_contiguous() or dk.shape != dv.shape:
+            raise ShapeError("accumulate_grad_pages: fp32 contiguous CUDA dk/dv of equal shape required")
+        call("oomb_accumulate_grad_pages", self.handle, layer, ids.ctypes.data_as(C.c_void_p), len(ids), _ptr(dk),
+             _ptr(dv), stream_handle(stream))
+
+    PROFILE_KINDS = ("append", "score", "topk", "attn_fwd", "bwd_prep", "bwd_dq", "bwd_dkdv", "bwd_simt",
+                     "grad_init", "gather_scatter", "other")
+
+    def profile_enable(self, on: bool = True) -> None:
+        call("oomb_profile_enable", self.handle, int(on))
+
+    def profile_collect(self) -> dict:
+        """Per kernel kind: (launches, device ms) since the last collect (synchronises)."""
+        n = len(self.PROFILE_KINDS)
+        counts = np.zeros(n, np.int64)
+        ms = np.zeros(n, np.float64)
+        call("oomb_profile_collect", self.handle, counts.ctypes.data_as(C.c_void_p), ms.ctypes.data_as(C.c_void_p), n)
+        return {k: (int(c), float(t)) for k, c, t in zip(self.PROFILE_KINDS, counts, ms) if c}
+
     def check_device_errors(self) -> None:
         call("oomb_check_device_errors", self.handle)
 
