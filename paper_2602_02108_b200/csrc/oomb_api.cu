@@ -775,42 +775,71 @@ int oomb_select_recent(oomb_selection_t s, int n_pages, int window, int m, void*
         select_range(s, n_pages - take, take, m, S(stream));
     });
 }
+static void select_topk_impl(oomb_selection_t s, const float* vote, int m, int n, int k, cudaStream_t st) {
+    OOMB_REQUIRE(k >= 0, OOMB_SHAPE_ERROR, "select_topk: negative budget");  // attention.hpp:73
+    OOMB_REQUIRE(m >= 0 && m <= s->max_m, OOMB_SHAPE_ERROR, "selection: too many query pages");
+    const int kk = std::min(k, n);
+    OOMB_REQUIRE(static_cast<int64_t>(m) * kk <= s->max_ids, OOMB_SHAPE_ERROR, "selection: too many ids");
+    OOMB_CUDA(cudaEventSynchronize(s->ev));
+    launch_topk(vote, m, n, k, s->d_off, s->d_ids, st);
+    OOMB_CUDA(cudaMemcpyAsync(s->h_off, s->d_off, (m + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    if (m * kk)
+        OOMB_CUDA(cudaMemcpyAsync(s->h_ids, s->d_ids, static_cast<size_t>(m) * kk * sizeof(int32_t),
+                                  cudaMemcpyDeviceToHost, st));
+    OOMB_CUDA(cudaEventRecord(s->ev, st));
+    s->host_pending = true;
+    s->m = m;
+    s->nnz = m * kk;
+}
+
 int oomb_select_topk(oomb_selection_t s, const float* vote, int m, int n, int k, void* stream) {
     return guard([&] {
         set_dev(s->pool);
-        OOMB_REQUIRE(k >= 0, OOMB_SHAPE_ERROR, "select_topk: negative budget");  // attention.hpp:73
-        OOMB_REQUIRE(m >= 0 && m <= s->max_m, OOMB_SHAPE_ERROR, "selection: too many query pages");
-        const int kk = std::min(k, n);
-        OOMB_REQUIRE(static_cast<int64_t>(m) * kk <= s->max_ids, OOMB_SHAPE_ERROR, "selection: too many ids");
-        OOMB_CUDA(cudaEventSynchronize(s->ev));
-        launch_topk(vote, m, n, k, s->d_off, s->d_ids, S(stream));
-        OOMB_CUDA(cudaMemcpyAsync(s->h_off, s->d_off, (m + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, S(stream)));
-        if (m * kk)
-            OOMB_CUDA(cudaMemcpyAsync(s->h_ids, s->d_ids, static_cast<size_t>(m) * kk * sizeof(int32_t),
-                                      cudaMemcpyDeviceToHost, S(stream)));
-        OOMB_CUDA(cudaEventRecord(s->ev, S(stream)));
-        s->host_pending = true;
-        s->m = m;
-        s->nnz = m * kk;
+        select_topk_impl(s, vote, m, n, k, S(stream));
     });
 }
 
 // ---------------------------------------------------------------------------
 // scoring
 // ---------------------------------------------------------------------------
+// score_pages on fp32 representatives (k_avg [n][Hkv][hd]) or, when kavg_sum/kavg_cnt are given,
+// on the pool's K_avg sums (mean formed on the fly, paged_kv.hpp:170-183). bf16 + hd 128 +
+// 128-aligned chunks use the tcgen05 scorer; everything else the exact SIMT scorer.
+static void score_impl(const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, const float* kavg_sum,
+                       const int32_t* kavg_cnt, int64_t n, int Hkv, int P, int score_scale, int dtype, bool allow_tc,
+                       float* vote, cudaStream_t st) {
+    OOMB_REQUIRE(n >= 1, OOMB_SHAPE_ERROR, "score_pages: needs at least one candidate page");
+    OOMB_REQUIRE(Hq >= 1 && Hkv >= 1 && Hq % Hkv == 0 && hd >= 1 && hd <= 256 && P >= 1, OOMB_SHAPE_ERROR,
+                 "score_pages: bad shape");
+    const float scale = score_scale ? 1.0f / std::sqrt(static_cast<float>(hd)) : 1.0f;
+    if (allow_tc && score_tc_supported(dtype, hd, P, tokens)) {
+        void* ws = nullptr;
+        OOMB_CUDA(cudaMallocAsync(&ws, score_tc_workspace(tokens, Hq, Hkv, n, P), st));
+        launch_score_tc(q, tokens, Hq, Hkv, P, kavg_sum, kavg_cnt, k_avg, n, scale, vote, ws, st);
+        OOMB_CUDA(cudaFreeAsync(ws, st));
+        return;
+    }
+    float* kavg = const_cast<float*>(k_avg);
+    if (!kavg) {
+        OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&kavg), n * Hkv * hd * sizeof(float), st));
+        launch_mean_keys(kavg_sum, kavg_cnt, static_cast<int>(n), Hkv * hd, kavg, st);
+    }
+    float* stats = nullptr;
+    OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&stats), std::max<int64_t>(tokens * Hq, 1) * 8, st));
+    launch_score_simt(dtype, q, tokens, Hq, hd, kavg, n, Hkv, P, scale, vote, stats, st);
+    OOMB_CUDA(cudaFreeAsync(stats, st));
+    if (!k_avg) OOMB_CUDA(cudaFreeAsync(kavg, st));
+}
+
 int oomb_score_pages(const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, int64_t n, int Hkv,
                      int page_size, int score_scale, int dtype, float* vote, void* stream) {
     return guard([&] {
-        OOMB_REQUIRE(n >= 1, OOMB_SHAPE_ERROR, "score_pages: needs at least one candidate page");
-        OOMB_REQUIRE(Hq >= 1 && Hkv >= 1 && Hq % Hkv == 0 && hd >= 1 && hd <= 256 && page_size >= 1,
-                     OOMB_SHAPE_ERROR, "score_pages: bad shape");
-        const float scale = score_scale ? 1.0f / std::sqrt(static_cast<float>(hd)) : 1.0f;
-        float* stats = nullptr;
-        OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&stats), std::max<int64_t>(tokens * Hq, 1) * 8, S(stream)));
-        launch_score_simt(dtype, q, tokens, Hq, hd, k_avg, n, Hkv, page_size, scale, vote, stats, S(stream));
-        OOMB_CUDA(cudaFreeAsync(stats, S(stream)));
+        score_impl(q, tokens, Hq, hd, k_avg, nullptr, nullptr, n, Hkv, page_size, score_scale, dtype, true, vote,
+                   S(stream));
     });
 }
+
+static void select_topk_impl(oomb_selection_t s, const float* vote, int m, int n, int k, cudaStream_t st);
 
 int oomb_select_pages_topk(oomb_pool_t p, int layer, const void* q, int64_t tokens, int n_candidates,
                            oomb_selection_t sel, float* vote_scratch, void* stream) {
@@ -824,16 +853,10 @@ int oomb_select_pages_topk(oomb_pool_t p, int layer, const void* q, int64_t toke
             select_range(sel, 0, 0, m, S(stream));
             return;
         }
-        const int64_t re = static_cast<int64_t>(p->cfg.n_kv_heads) * p->cfg.head_dim;
-        float* kavg = nullptr;
-        OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&kavg), n * re * sizeof(float), S(stream)));
-        launch_mean_keys(p->kavg_sum_layer(layer), p->kavg_cnt_layer(layer), n, static_cast<int>(re), kavg, S(stream));
-        const int rc = oomb_score_pages(q, tokens, p->cfg.n_q_heads, p->cfg.head_dim, kavg, n, p->cfg.n_kv_heads,
-                                        p->cfg.page_size, p->cfg.score_scale, p->cfg.dtype, vote_scratch, stream);
-        OOMB_CUDA(cudaFreeAsync(kavg, S(stream)));
-        if (rc) throw Error(rc, g_last_error);
-        const int rc2 = oomb_select_topk(sel, vote_scratch, m, n, p->cfg.retrieval_budget / p->cfg.page_size, stream);
-        if (rc2) throw Error(rc2, g_last_error);
+        score_impl(q, tokens, p->cfg.n_q_heads, p->cfg.head_dim, nullptr, p->kavg_sum_layer(layer),
+                   p->kavg_cnt_layer(layer), n, p->cfg.n_kv_heads, p->cfg.page_size, p->cfg.score_scale,
+                   p->cfg.dtype, p->policy != 1, vote_scratch, S(stream));
+        select_topk_impl(sel, vote_scratch, m, n, p->cfg.retrieval_budget / p->cfg.page_size, S(stream));
     });
 }
 

@@ -166,6 +166,11 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
                         float* dv_cur, int* d_err, void* workspace, size_t workspace_bytes, int nnz, int n_pages,
                         cudaStream_t st);
 size_t attn_bwd_tc_workspace(const AttnGeom& g, int max_sel_ids);
+bool score_tc_supported(int dtype, int hd, int P, int64_t tokens);
+size_t score_tc_workspace(int64_t tokens, int Hq, int Hkv, int64_t n, int P);
+void launch_score_tc(const void* q, int64_t tokens, int Hq, int Hkv, int P, const float* kavg_sum,
+                     const int32_t* kavg_cnt, const float* kavg_f32, int64_t n, float scale, float* vote, void* ws,
+                     cudaStream_t st);
 void launch_debug_tc_gemm(int mode, const void* a, const void* b, float* c, int m, int n, int k, cudaStream_t st);
 
 // Driver entry point for cuTensorMapEncodeTiled (no libcuda link dependency).

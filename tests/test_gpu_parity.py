@@ -223,14 +223,21 @@ def test_scoring_and_selection_parity(geom, dtype):
     want_vote = oracle.score_pages(q, oracle.mean_keys(0))
     sel = select_pages_topk(cache, 0, torch.from_numpy(q).to("cuda", tdt), npages)
     got_vote = T(sel.vote)
-    assert rel(got_vote, want_vote) < FP32_TOL
+    # fp32 mode (and shapes on the exact SIMT scorer) meet 1e-5; the bf16 tcgen05 scorer
+    # rounds K_avg to bf16 for the MMA, so its votes carry bf16 operand error.
+    tc = dtype == "bf16" and geom == "qwen"
+    tol = 5e-3 if tc else FP32_TOL
+    assert rel(got_vote, want_vote) < tol, rel(got_vote, want_vote)
     lists = sel.lists()
+    checked = 0
     for i in range(want_vote.shape[0]):
         want = Port.select_topk(want_vote[i].astype(np.float64), 3).tolist()
         row = np.sort(want_vote[i])[::-1]
         margin = (row[2] - row[3]) / max(abs(row[2]), 1e-30)
-        if margin > 1e-4:  # ids are defined bit-exactly only where the k-boundary margin exceeds score tolerance
+        if margin > 10 * tol:  # ids are defined bit-exactly only where the k-boundary margin exceeds score tolerance
             assert lists[i] == want
+            checked += 1
+    assert checked >= 1
 
 
 # ---------------------------------------------------------------------------
