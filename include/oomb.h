@@ -187,6 +187,55 @@ OOMB_API int oomb_accumulate_grad_pages(oomb_pool_t pool, int layer, const int32
 OOMB_API int oomb_profile_enable(oomb_pool_t pool, int on);
 OOMB_API int oomb_profile_collect(oomb_pool_t pool, int64_t* counts, double* ms, int n_kinds);
 
+/* ---- tiered residency / offload (TieredEngine, tiered_memory.hpp:99-432) ----
+ * The policy is the reference's, decision for decision: LRU eviction of unreserved pages
+ * (unpinned first), reserved / pinned states, all-or-nothing best-effort prefetch with
+ * append headroom, write-back of dirty K/V and gradient pages only, capacity errors.
+ * Created on a pool, pages really move: evictions D2H-copy dirty K/V (+dK/dV) into a
+ * pinned host pool on a D2H stream and free the device slot; fetches H2D-copy into a fresh
+ * slot on an H2D stream; wait() makes the compute stream wait on the copy and publishes
+ * the slot in the device page table. Log timestamps then come from CUDA events.
+ * Created on a bare page table (no device), the engine runs the reference's simulated
+ * clock (bandwidth + cost model) and its log matches the reference event for event. */
+typedef struct oomb_tier_s* oomb_tier_t;
+typedef struct {
+    int64_t device_capacity_pages; /* -1 = unlimited (TierConfig, tiered_memory.hpp:74-78) */
+    double bandwidth_bytes_per_s;  /* simulated link (simulation mode) */
+    double fixed_s_per_layer;      /* ComputeCostModel :58-72 */
+    double s_per_attended_token;
+} oomb_tier_config;
+typedef struct { /* ScheduleEvent tiered_memory.hpp:36-44 */
+    int32_t kind; /* 0 fetch_issued, 1 fetch_done, 2 evict, 3 compute_begin, 4 compute_end, 5 access */
+    int32_t layer;
+    int32_t page;
+    int32_t chunk;
+    int32_t phase; /* 0 forward, 1 backward */
+    int32_t pad;
+    uint64_t bytes;
+    double t;
+} oomb_event;
+OOMB_API int oomb_tier_create_sim(oomb_pagetable_t pt, const oomb_tier_config* cfg, oomb_tier_t* out);
+OOMB_API int oomb_tier_create(oomb_pool_t pool, const oomb_tier_config* cfg, void* compute_stream, oomb_tier_t* out);
+OOMB_API int oomb_tier_destroy(oomb_tier_t t);
+OOMB_API int oomb_tier_begin_phase(oomb_tier_t t, int phase);
+OOMB_API int oomb_tier_set_prefetch_headroom(oomb_tier_t t, int64_t pages);
+OOMB_API int oomb_tier_on_pages_appended(oomb_tier_t t, int layer, int64_t slot_begin, int64_t slot_end);
+OOMB_API int oomb_tier_on_grads_scattered(oomb_tier_t t, int layer, const int32_t* ids_host, int n);
+OOMB_API int oomb_tier_fetch_async(oomb_tier_t t, int layer, const int32_t* ids_host, int n, int chunk, int best_effort,
+                                   int64_t* handle);
+OOMB_API int oomb_tier_wait(oomb_tier_t t, int64_t handle);
+OOMB_API int oomb_tier_record_access(oomb_tier_t t, int layer, const int32_t* ids_host, int n, int chunk);
+OOMB_API int oomb_tier_advance_compute(oomb_tier_t t, double seconds, int chunk, int layer);
+OOMB_API int oomb_tier_end_layer_use(oomb_tier_t t, int layer, const int32_t* ids_host, int n);
+OOMB_API int oomb_tier_release_all(oomb_tier_t t);
+/* out[5] = {now, stall_seconds, h2d_bytes forward, h2d_bytes backward, d2h_bytes} */
+OOMB_API int oomb_tier_stats(oomb_tier_t t, double* out);
+OOMB_API int oomb_tier_log(oomb_tier_t t, oomb_event* out, int64_t cap, int64_t* n);
+/* validate_schedule (tiered_memory.cpp:47-138): out[6] = {stall_s, transfer_bytes, h2d_fwd, h2d_bwd,
+ * d2h, overlap_fraction}; n_violations = residency/order violations found. */
+OOMB_API int oomb_validate_schedule(const oomb_event* events, int64_t n, double bandwidth, double* out,
+                                    int* n_violations);
+
 /* ---- page-table host logic (no device) -----------------------------------
  * The arena / LIFO free-list / lazy-gradient-page bookkeeping of PagedCache
  * (paged_kv.hpp:73-108,135-164,227-242,280-288), exposed on its own so that it is

@@ -86,6 +86,22 @@ _PROTOS = {
     "oomb_accumulate_grad_pages": [VP, I, VP, I, VP, VP, VP],
     "oomb_profile_enable": [VP, I],
     "oomb_profile_collect": [VP, VP, VP, I],
+    "oomb_tier_create_sim": [VP, VP, C.POINTER(VP)],
+    "oomb_tier_create": [VP, VP, VP, C.POINTER(VP)],
+    "oomb_tier_destroy": [VP],
+    "oomb_tier_begin_phase": [VP, I],
+    "oomb_tier_set_prefetch_headroom": [VP, I64],
+    "oomb_tier_on_pages_appended": [VP, I, I64, I64],
+    "oomb_tier_on_grads_scattered": [VP, I, VP, I],
+    "oomb_tier_fetch_async": [VP, I, VP, I, I, I, C.POINTER(I64)],
+    "oomb_tier_wait": [VP, I64],
+    "oomb_tier_record_access": [VP, I, VP, I, I],
+    "oomb_tier_advance_compute": [VP, C.c_double, I, I],
+    "oomb_tier_end_layer_use": [VP, I, VP, I],
+    "oomb_tier_release_all": [VP],
+    "oomb_tier_stats": [VP, VP],
+    "oomb_tier_log": [VP, VP, I64, C.POINTER(I64)],
+    "oomb_validate_schedule": [VP, I64, C.c_double, VP, C.POINTER(I)],
 }
 _RESTYPE = {"oomb_last_error": C.c_char_p, "oomb_kernel_launches": C.c_int64}
 

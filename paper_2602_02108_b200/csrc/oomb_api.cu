@@ -16,32 +16,12 @@
 #include <string>
 #include <vector>
 
-#include "oomb_internal.h"
+#include "pool.h"
 
 namespace oomb {
 
 thread_local std::string g_last_error;
 thread_local Profiler* g_prof = nullptr;
-
-template <class F>
-int guard(F&& f) {
-    struct Reset {
-        ~Reset() { g_prof = nullptr; }
-    } reset_prof;
-    try {
-        f();
-        return OOMB_OK;
-    } catch (const Error& e) {
-        g_last_error = e.what();
-        return e.code;
-    } catch (const std::bad_alloc&) {
-        g_last_error = "out of host memory";
-        return OOMB_ERROR;
-    } catch (const std::exception& e) {
-        g_last_error = e.what();
-        return OOMB_ERROR;
-    }
-}
 
 // ---------------------------------------------------------------------------
 // cuTensorMapEncodeTiled through the runtime's driver entry point.
@@ -63,171 +43,7 @@ CUresult encode_tensor_map(CUtensorMap* map, CUtensorMapDataType dt, uint32_t ra
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
-// ---------------------------------------------------------------------------
-// Host mirror of PagedCache's page table (paged_kv.hpp:41-356): arena ids are
-// allocated exactly like the reference (LIFO free list; k then v per new page
-// at append; gk then gv lazily at first scatter; reset frees k, v, gk, gv per
-// page per layer) so page tables compare bit-exactly.
-// ---------------------------------------------------------------------------
-struct PageTable {
-    struct Entry {
-        int32_t k = -1, v = -1, gk = -1, gv = -1;
-        uint8_t tier = 0;  // 0 device, 1 host
-    };
-    int n_layers, P, kvh, hd, kv_elem, grad_elem;
-    std::vector<std::vector<Entry>> pages;
-    std::vector<int64_t> filled;
-    int64_t arena_n = 0;
-    std::vector<int32_t> free_list;
-
-    PageTable(int L, int P_, int kvh_, int hd_, int kve, int ge)
-        : n_layers(L), P(P_), kvh(kvh_), hd(hd_), kv_elem(kve), grad_elem(ge), pages(L), filled(L, 0) {}
-
-    void check_layer(int layer) const {
-        OOMB_REQUIRE(layer >= 0 && layer < n_layers, OOMB_SHAPE_ERROR, "cache: layer out of range");
-    }
-    int32_t alloc() {  // alloc_page_ paged_kv.hpp:280-288
-        if (!free_list.empty()) {
-            const int32_t id = free_list.back();
-            free_list.pop_back();
-            return id;
-        }
-        return static_cast<int32_t>(arena_n++);
-    }
-    // append_chunk's page bookkeeping (paged_kv.hpp:73-108). Returns [first_new, n_new).
-    void append(int layer, int64_t rows, int64_t* b, int64_t* e, int* first_new, int* n_new) {
-        check_layer(layer);
-        OOMB_REQUIRE(rows >= 0, OOMB_SHAPE_ERROR, "append_chunk: expected [rows x kvh x hd] K/V of equal shape");
-        auto& st = pages[layer];
-        *b = filled[layer];
-        *e = filled[layer] + rows;
-        *first_new = static_cast<int>(st.size());
-        *n_new = 0;
-        if (rows > 0) {
-            const int64_t last_page = (filled[layer] + rows - 1) / P;
-            while (static_cast<int64_t>(st.size()) <= last_page) {
-                Entry en;
-                en.k = alloc();
-                en.v = alloc();
-                st.push_back(en);
-                ++*n_new;
-            }
-        }
-        filled[layer] += rows;
-    }
-    void check_ids(int layer, const int32_t* ids, int n, bool enforce, const char* op) const {
-        check_layer(layer);
-        const auto& st = pages[layer];
-        for (int i = 0; i < n; ++i) {
-            OOMB_REQUIRE(ids[i] >= 0 && ids[i] < static_cast<int32_t>(st.size()), OOMB_SHAPE_ERROR,
-                         std::string(op) + ": page id out of range");
-            OOMB_REQUIRE(!enforce || st[ids[i]].tier == 0, OOMB_RESIDENCY_ERROR,
-                         std::string(op) + ": page " + std::to_string(ids[i]) + " of layer " + std::to_string(layer) +
-                             " is not device-resident");
-        }
-    }
-    // scatter_add_grads' lazy allocation (paged_kv.hpp:148-153), in call order.
-    std::vector<int32_t> scatter(int layer, const int32_t* ids, int n) {
-        std::vector<int32_t> fresh;
-        auto& st = pages[layer];
-        for (int i = 0; i < n; ++i) {
-            Entry& en = st[ids[i]];
-            if (en.gk < 0) {
-                en.gk = alloc();
-                en.gv = alloc();
-                fresh.push_back(ids[i]);
-            }
-        }
-        return fresh;
-    }
-    void reset() {  // paged_kv.hpp:227-242
-        for (int l = 0; l < n_layers; ++l) {
-            for (const auto& en : pages[l]) {
-                free_list.push_back(en.k);
-                free_list.push_back(en.v);
-                if (en.gk >= 0) {
-                    free_list.push_back(en.gk);
-                    free_list.push_back(en.gv);
-                }
-            }
-            pages[l].clear();
-            filled[l] = 0;
-        }
-    }
-    oomb_memory_report report() const {  // paged_kv.hpp:185-197
-        oomb_memory_report r{};
-        const uint64_t pe = static_cast<uint64_t>(P) * kvh * hd;
-        for (const auto& st : pages)
-            for (const auto& en : st) {
-                r.pages += 1;
-                if (en.tier == 0) r.device_bytes += 2 * pe * kv_elem;
-                else r.host_bytes += 2 * pe * kv_elem;
-                if (en.gk >= 0) r.grad_bytes += 2 * pe * grad_elem;
-            }
-        r.arena_blocks = arena_n;
-        r.free_list = static_cast<int64_t>(free_list.size());
-        return r;
-    }
-};
-
-}  // namespace oomb
-
-using namespace oomb;
-
-struct oomb_pagetable_s {
-    PageTable pt;
-};
-
-struct oomb_pool_s {
-    oomb_config cfg{};
-    int device = 0;
-    int64_t max_pages = 0;
-    int elem = 4;
-    int64_t page_elems = 0;
-    PageTable* pt = nullptr;
-    int64_t n_kv_slots = 0, n_g_slots = 0;
-    std::vector<int32_t> kv_free, g_free;
-    std::vector<std::vector<int32_t>> kvslot, gslot;
-    void* kpool = nullptr;
-    void* vpool = nullptr;
-    float* gkpool = nullptr;
-    float* gvpool = nullptr;
-    int32_t* d_kvslot = nullptr;
-    int32_t* d_gslot = nullptr;
-    float* d_kavg_sum = nullptr;
-    int32_t* d_kavg_cnt = nullptr;
-    int* d_err = nullptr;
-    bool enforce = false;
-    int policy = 0;
-    TcPoolMaps maps;
-    void* bwd_ws = nullptr;
-    size_t bwd_ws_bytes = 0;
-    bool prof_on = false;
-    Profiler prof;
-
-    int32_t* kvslot_layer(int l) { return d_kvslot + static_cast<int64_t>(l) * max_pages; }
-    int32_t* gslot_layer(int l) { return d_gslot + static_cast<int64_t>(l) * max_pages; }
-    float* kavg_sum_layer(int l) {
-        return d_kavg_sum + static_cast<int64_t>(l) * max_pages * cfg.n_kv_heads * cfg.head_dim;
-    }
-    int32_t* kavg_cnt_layer(int l) { return d_kavg_cnt + static_cast<int64_t>(l) * max_pages; }
-};
-
-struct oomb_selection_s {
-    oomb_pool_s* pool = nullptr;
-    int max_m = 0, max_ids = 0;
-    int32_t* d_off = nullptr;
-    int32_t* d_ids = nullptr;
-    int32_t* h_off = nullptr;  // pinned
-    int32_t* h_ids = nullptr;  // pinned
-    int m = 0, nnz = 0;
-    cudaEvent_t ev = nullptr;
-    bool host_pending = false;  // device -> host mirror copy in flight
-};
-
 namespace {
-
-cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
 void validate_cfg(const oomb_config& c) {  // ModelConfig::validate (config.cpp:30-51), path subset
     auto req = [](bool ok, const char* m) {
@@ -248,10 +64,6 @@ void validate_cfg(const oomb_config& c) {  // ModelConfig::validate (config.cpp:
     req(c.max_tokens >= 1, "max_tokens must be >= 1");
 }
 
-void set_dev(oomb_pool_s* p) {
-    OOMB_CUDA(cudaSetDevice(p->device));
-    g_prof = p->prof_on ? &p->prof : nullptr;
-}
 
 int32_t pop_slot(std::vector<int32_t>& fl, const char* what) {
     OOMB_REQUIRE(!fl.empty(), OOMB_CONFIG_ERROR,
@@ -300,6 +112,7 @@ void ensure_grad_pages(oomb_pool_s* p, int layer, const int32_t* h_off, const in
         p->pt->check_ids(layer, h_ids + h_off[qp], n, p->enforce, "scatter_add_grads");
         for (int32_t pid : p->pt->scatter(layer, h_ids + h_off[qp], n)) {
             const int32_t gs = pop_slot(p->g_free, "gradient page");
+            p->wait_slot(true, gs, st);
             p->gslot[layer][pid] = gs;
             pages.push_back(pid);
             slots.push_back(gs);
@@ -324,6 +137,9 @@ bool use_tc(oomb_pool_s* p, const AttnGeom& g) {
 }
 
 }  // namespace
+}  // namespace oomb
+
+using namespace oomb;
 
 extern "C" {
 
@@ -459,6 +275,10 @@ int oomb_pool_destroy(oomb_pool_t p) {
     cudaFree(p->d_kavg_cnt);
     cudaFree(p->d_err);
     cudaFree(p->bwd_ws);
+    for (auto e : p->kv_ev)
+        if (e) cudaEventDestroy(e);
+    for (auto e : p->g_ev)
+        if (e) cudaEventDestroy(e);
     for (auto& r : p->prof.recs) {
         cudaEventDestroy(r.e0);
         cudaEventDestroy(r.e1);
@@ -540,7 +360,11 @@ int oomb_append_chunk(oomb_pool_t p, int layer, const void* k, const void* v, in
         int first_new, n_new;
         const int64_t filled0 = p->pt->filled[layer];
         p->pt->append(layer, rows, &b, &e, &first_new, &n_new);
-        for (int i = 0; i < n_new; ++i) p->kvslot[layer][first_new + i] = pop_slot(p->kv_free, "KV page");
+        for (int i = 0; i < n_new; ++i) {
+            const int32_t s = pop_slot(p->kv_free, "KV page");
+            p->wait_slot(false, s, S(stream));  // a recycled slot may still be draining to the host
+            p->kvslot[layer][first_new + i] = s;
+        }
         *slot_begin = b;
         *slot_end = e;
         // Launch in segments that create at most 100 new pages each.

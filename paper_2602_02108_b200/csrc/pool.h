@@ -1,0 +1,220 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Host-side state shared by the C-ABI runtime (oomb_api.cu) and the offload
+// engine (tier.cu): the reference page-table mirror, the device pool and
+// selection handles, and the exception guard.
+#pragma once
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "oomb_internal.h"
+
+namespace oomb {
+
+extern thread_local std::string g_last_error;
+
+template <class F>
+int guard(F&& f) {
+    struct Reset {
+        ~Reset() { g_prof = nullptr; }
+    } reset_prof;
+    try {
+        f();
+        return OOMB_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return OOMB_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return OOMB_ERROR;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Host mirror of PagedCache's page table (paged_kv.hpp:41-356): arena ids are
+// allocated exactly like the reference (LIFO free list; k then v per new page
+// at append; gk then gv lazily at first scatter; reset frees k, v, gk, gv per
+// page per layer) so page tables compare bit-exactly.
+// ---------------------------------------------------------------------------
+struct PageTable {
+    struct Entry {
+        int32_t k = -1, v = -1, gk = -1, gv = -1;
+        uint8_t tier = 0;  // 0 device, 1 host
+    };
+    int n_layers, P, kvh, hd, kv_elem, grad_elem;
+    std::vector<std::vector<Entry>> pages;
+    std::vector<int64_t> filled;
+    int64_t arena_n = 0;
+    std::vector<int32_t> free_list;
+
+    PageTable(int L, int P_, int kvh_, int hd_, int kve, int ge)
+        : n_layers(L), P(P_), kvh(kvh_), hd(hd_), kv_elem(kve), grad_elem(ge), pages(L), filled(L, 0) {}
+
+    void check_layer(int layer) const {
+        OOMB_REQUIRE(layer >= 0 && layer < n_layers, OOMB_SHAPE_ERROR, "cache: layer out of range");
+    }
+    int32_t alloc() {  // alloc_page_ paged_kv.hpp:280-288
+        if (!free_list.empty()) {
+            const int32_t id = free_list.back();
+            free_list.pop_back();
+            return id;
+        }
+        return static_cast<int32_t>(arena_n++);
+    }
+    // append_chunk's page bookkeeping (paged_kv.hpp:73-108). Returns [first_new, n_new).
+    void append(int layer, int64_t rows, int64_t* b, int64_t* e, int* first_new, int* n_new) {
+        check_layer(layer);
+        OOMB_REQUIRE(rows >= 0, OOMB_SHAPE_ERROR, "append_chunk: expected [rows x kvh x hd] K/V of equal shape");
+        auto& st = pages[layer];
+        *b = filled[layer];
+        *e = filled[layer] + rows;
+        *first_new = static_cast<int>(st.size());
+        *n_new = 0;
+        if (rows > 0) {
+            const int64_t last_page = (filled[layer] + rows - 1) / P;
+            while (static_cast<int64_t>(st.size()) <= last_page) {
+                Entry en;
+                en.k = alloc();
+                en.v = alloc();
+                st.push_back(en);
+                ++*n_new;
+            }
+        }
+        filled[layer] += rows;
+    }
+    void check_ids(int layer, const int32_t* ids, int n, bool enforce, const char* op) const {
+        check_layer(layer);
+        const auto& st = pages[layer];
+        for (int i = 0; i < n; ++i) {
+            OOMB_REQUIRE(ids[i] >= 0 && ids[i] < static_cast<int32_t>(st.size()), OOMB_SHAPE_ERROR,
+                         std::string(op) + ": page id out of range");
+            OOMB_REQUIRE(!enforce || st[ids[i]].tier == 0, OOMB_RESIDENCY_ERROR,
+                         std::string(op) + ": page " + std::to_string(ids[i]) + " of layer " + std::to_string(layer) +
+                             " is not device-resident");
+        }
+    }
+    // scatter_add_grads' lazy allocation (paged_kv.hpp:148-153), in call order.
+    std::vector<int32_t> scatter(int layer, const int32_t* ids, int n) {
+        std::vector<int32_t> fresh;
+        auto& st = pages[layer];
+        for (int i = 0; i < n; ++i) {
+            Entry& en = st[ids[i]];
+            if (en.gk < 0) {
+                en.gk = alloc();
+                en.gv = alloc();
+                fresh.push_back(ids[i]);
+            }
+        }
+        return fresh;
+    }
+    void reset() {  // paged_kv.hpp:227-242
+        for (int l = 0; l < n_layers; ++l) {
+            for (const auto& en : pages[l]) {
+                free_list.push_back(en.k);
+                free_list.push_back(en.v);
+                if (en.gk >= 0) {
+                    free_list.push_back(en.gk);
+                    free_list.push_back(en.gv);
+                }
+            }
+            pages[l].clear();
+            filled[l] = 0;
+        }
+    }
+    oomb_memory_report report() const {  // paged_kv.hpp:185-197
+        oomb_memory_report r{};
+        const uint64_t pe = static_cast<uint64_t>(P) * kvh * hd;
+        for (const auto& st : pages)
+            for (const auto& en : st) {
+                r.pages += 1;
+                if (en.tier == 0) r.device_bytes += 2 * pe * kv_elem;
+                else r.host_bytes += 2 * pe * kv_elem;
+                if (en.gk >= 0) r.grad_bytes += 2 * pe * grad_elem;
+            }
+        r.arena_blocks = arena_n;
+        r.free_list = static_cast<int64_t>(free_list.size());
+        return r;
+    }
+};
+
+}  // namespace oomb
+
+using namespace oomb;
+
+struct oomb_pagetable_s {
+    PageTable pt;
+};
+
+struct oomb_pool_s {
+    oomb_config cfg{};
+    int device = 0;
+    int64_t max_pages = 0;
+    int elem = 4;
+    int64_t page_elems = 0;
+    PageTable* pt = nullptr;
+    int64_t n_kv_slots = 0, n_g_slots = 0;
+    std::vector<int32_t> kv_free, g_free;
+    std::vector<std::vector<int32_t>> kvslot, gslot;
+    void* kpool = nullptr;
+    void* vpool = nullptr;
+    float* gkpool = nullptr;
+    float* gvpool = nullptr;
+    int32_t* d_kvslot = nullptr;
+    int32_t* d_gslot = nullptr;
+    float* d_kavg_sum = nullptr;
+    int32_t* d_kavg_cnt = nullptr;
+    int* d_err = nullptr;
+    bool enforce = false;
+    int policy = 0;
+    TcPoolMaps maps;
+    void* bwd_ws = nullptr;
+    size_t bwd_ws_bytes = 0;
+    bool prof_on = false;
+    Profiler prof;
+    // Per-slot "last write-back out of this slot" events (offload engine). A stream that
+    // is about to write into a recycled slot waits on it first.
+    std::vector<cudaEvent_t> kv_ev, g_ev;
+
+    cudaEvent_t kv_slot_event(int32_t s) { return slot_event(kv_ev, s, n_kv_slots); }
+    cudaEvent_t g_slot_event(int32_t s) { return slot_event(g_ev, s, n_g_slots); }
+    cudaEvent_t slot_event(std::vector<cudaEvent_t>& v, int32_t s, int64_t n) {
+        if (v.empty()) v.assign(n, nullptr);
+        if (!v[s]) OOMB_CUDA(cudaEventCreateWithFlags(&v[s], cudaEventDisableTiming));
+        return v[s];
+    }
+    void wait_slot(bool grad, int32_t s, cudaStream_t st) {
+        auto& v = grad ? g_ev : kv_ev;
+        if (!v.empty() && v[s]) OOMB_CUDA(cudaStreamWaitEvent(st, v[s], 0));
+    }
+
+    int32_t* kvslot_layer(int l) { return d_kvslot + static_cast<int64_t>(l) * max_pages; }
+    int32_t* gslot_layer(int l) { return d_gslot + static_cast<int64_t>(l) * max_pages; }
+    float* kavg_sum_layer(int l) {
+        return d_kavg_sum + static_cast<int64_t>(l) * max_pages * cfg.n_kv_heads * cfg.head_dim;
+    }
+    int32_t* kavg_cnt_layer(int l) { return d_kavg_cnt + static_cast<int64_t>(l) * max_pages; }
+};
+
+struct oomb_selection_s {
+    oomb_pool_s* pool = nullptr;
+    int max_m = 0, max_ids = 0;
+    int32_t* d_off = nullptr;
+    int32_t* d_ids = nullptr;
+    int32_t* h_off = nullptr;  // pinned
+    int32_t* h_ids = nullptr;  // pinned
+    int m = 0, nnz = 0;
+    cudaEvent_t ev = nullptr;
+    bool host_pending = false;  // device -> host mirror copy in flight
+};
+
+
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+inline void set_dev(oomb_pool_s* p) {
+    OOMB_CUDA(cudaSetDevice(p->device));
+    g_prof = p->prof_on ? &p->prof : nullptr;
+}

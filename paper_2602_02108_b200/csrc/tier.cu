@@ -1,0 +1,649 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Tiered residency engine — TieredEngine (tiered_memory.hpp:99-432) for B200.
+//
+// The decision logic is the reference's, statement for statement: the same LRU
+// counter, reserved / pinned flags, best-effort all-or-nothing prefetch with append
+// headroom, write-back of dirty K/V and gradient pages only, the same capacity
+// error. On a bare page table it also runs the reference's simulated clock, so its
+// ScheduleLog equals the reference's event for event (tests/test_tier_cpu.py).
+//
+// On a pool the pages really move:
+//   evict  -> D2H stream waits for the compute stream's tail, copies the dirty K/V
+//             (and dK/dV) blocks of the page's device slots into its pinned host
+//             blocks, records an event; the device slots return to the free list
+//             tagged with that event; the device page-table entries are cleared on
+//             the compute stream.
+//   fetch  -> a device slot is taken (the H2D stream first waits for the slot's
+//             last write-back), K/V (+dK/dV) are copied H2D, an event is recorded.
+//   wait   -> the compute stream waits for the transfer's event, then the new
+//             slots are published in the device page table (one small kernel).
+// Log timestamps then come from CUDA events recorded at each point, so
+// validate_schedule checks residency-before-use on the real GPU timeline.
+
+#include <algorithm>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <set>
+#include <tuple>
+
+#include "pool.h"
+
+namespace oomb {
+
+enum EventKind { EV_FETCH_ISSUED = 0, EV_FETCH_DONE, EV_EVICT, EV_COMPUTE_BEGIN, EV_COMPUTE_END, EV_ACCESS };
+
+// Device page-table update list, applied by one kernel on the compute stream.
+struct TableUpdates {
+    int32_t n;
+    int32_t idx[480];  // (layer*max_pages + page) entries
+    int32_t kv[480];
+    int32_t g[480];
+};
+
+__global__ void table_update_kernel(TableUpdates u, int32_t* kvslot, int32_t* gslot) {
+    for (int i = threadIdx.x; i < u.n; i += blockDim.x) {
+        kvslot[u.idx[i]] = u.kv[i];
+        gslot[u.idx[i]] = u.g[i];
+    }
+}
+
+}  // namespace oomb
+
+using namespace oomb;
+
+struct oomb_tier_s {
+    struct PageState {
+        bool kv_host_valid = true;
+        bool grad_host_valid = true;
+        bool reserved = false;
+        bool pinned = false;
+        double in_flight_done = 0;
+        double writeback_done = 0;
+        uint64_t lru = 0;
+        bool host_has_kv = false;    // real mode: host block holds data
+        bool host_has_grad = false;
+    };
+    struct Transfer {
+        int layer = 0;
+        std::vector<int32_t> pages;
+        double ready = 0;
+        cudaEvent_t ev = nullptr;  // real mode: copies done
+    };
+    struct LogEv {
+        oomb_event e;
+        cudaEvent_t ev;  // real mode timestamp (nullptr: use e.t)
+    };
+
+    oomb_tier_config cfg{};
+    PageTable* pt = nullptr;
+    oomb_pool_s* pool = nullptr;  // nullptr = simulation mode
+    int phase = 0;
+    double clock = 0, h2d_free = 0, d2h_free = 0, stall_s = 0;
+    uint64_t h2d_fwd = 0, h2d_bwd = 0, d2h = 0, lru_counter = 0;
+    int64_t headroom = 0;
+    std::vector<std::vector<PageState>> pages;
+    std::vector<Transfer> transfers;
+    std::vector<LogEv> log;
+
+    // ---- real mode
+    cudaStream_t compute = nullptr, h2d_stream = nullptr, d2h_stream = nullptr;
+    cudaEvent_t t0 = nullptr;
+    std::vector<cudaEvent_t> spare_events;
+    uint8_t* host_kv = nullptr;    // pinned [layer][page] x (K, V) blocks
+    uint8_t* host_grad = nullptr;  // pinned [layer][page] x (dK, dV) blocks
+    size_t kv_block = 0, grad_block = 0;
+    TableUpdates pending{};
+
+    bool real() const { return pool != nullptr; }
+
+    cudaEvent_t new_event() {
+        if (!spare_events.empty()) {
+            cudaEvent_t e = spare_events.back();
+            spare_events.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        OOMB_CUDA(cudaEventCreate(&e));
+        return e;
+    }
+
+    void sync_pages() {
+        pages.resize(pt->n_layers);
+        for (int l = 0; l < pt->n_layers; ++l) pages[l].resize(pt->pages[l].size());
+    }
+    PageState& state(int layer, int page) {
+        sync_pages();
+        return pages.at(layer).at(page);
+    }
+    uint8_t tier(int layer, int page) const { return pt->pages[layer][page].tier; }
+    void set_tier(int layer, int page, uint8_t t) { pt->pages[layer][page].tier = t; }
+    int64_t device_page_count() const {  // tiered_memory.hpp:328-336
+        int64_t n = 0;
+        for (int l = 0; l < pt->n_layers; ++l)
+            for (const auto& e : pt->pages[l]) n += e.tier == 0;
+        return n;
+    }
+    bool grads_allocated(int layer, int page) const { return pt->pages[layer][page].gk >= 0; }
+    uint64_t kv_bytes() const {  // page_kv_bytes: K+V of one page, all kv heads
+        return 2ull * pt->P * pt->kvh * pt->hd * pt->kv_elem;
+    }
+    uint64_t grad_bytes() const { return 2ull * pt->P * pt->kvh * pt->hd * pt->grad_elem; }
+    uint64_t page_transfer_bytes(int layer, int page) const {  // tiered_memory.hpp:322-326
+        uint64_t b = kv_bytes();
+        if (grads_allocated(layer, page)) b += grad_bytes();
+        return b;
+    }
+
+    void push(int kind, double t, int layer, int32_t page, uint64_t bytes, int chunk, cudaStream_t st = nullptr) {
+        LogEv le{};
+        le.e.kind = kind;
+        le.e.t = t;
+        le.e.layer = layer;
+        le.e.page = page;
+        le.e.chunk = chunk;
+        le.e.bytes = bytes;
+        le.e.phase = phase;
+        le.ev = nullptr;
+        if (real() && st) {
+            le.ev = new_event();
+            OOMB_CUDA(cudaEventRecord(le.ev, st));
+        }
+        log.push_back(le);
+    }
+
+    // ---- device table publication (real mode)
+    void queue_table(int layer, int page) {
+        if (pending.n == 480) flush_table();
+        const int idx = static_cast<int>(layer * pool->max_pages + page);
+        pending.idx[pending.n] = idx;
+        pending.kv[pending.n] = pool->kvslot[layer][page];
+        pending.g[pending.n] = pool->gslot[layer][page];
+        ++pending.n;
+    }
+    void flush_table() {
+        if (!real() || pending.n == 0) return;
+        table_update_kernel<<<1, 256, 0, compute>>>(pending, pool->d_kvslot, pool->d_gslot);
+        check_launch("table_update_kernel");
+        pending.n = 0;
+    }
+
+    // ---- capacity (tiered_memory.hpp:341-384)
+    bool fits_after_eviction(int64_t incoming) {
+        if (cfg.device_capacity_pages < 0) return true;
+        sync_pages();
+        int64_t evictable = 0;
+        for (int l = 0; l < pt->n_layers; ++l)
+            for (size_t p = 0; p < pages[l].size(); ++p)
+                if (tier(l, static_cast<int>(p)) == 0 && !pages[l][p].reserved) ++evictable;
+        return device_page_count() - evictable + incoming <= cfg.device_capacity_pages;
+    }
+
+    void enforce_capacity(int64_t incoming) {
+        if (cfg.device_capacity_pages < 0) return;
+        sync_pages();
+        while (device_page_count() + incoming > cfg.device_capacity_pages) {
+            int best_l = -1, best_p = -1;
+            bool best_pinned = true;
+            uint64_t best_lru = std::numeric_limits<uint64_t>::max();
+            for (int l = 0; l < pt->n_layers; ++l) {
+                for (size_t p = 0; p < pages[l].size(); ++p) {
+                    const PageState& ps = pages[l][p];
+                    if (tier(l, static_cast<int>(p)) != 0 || ps.reserved) continue;
+                    if (std::make_pair(ps.pinned, ps.lru) < std::make_pair(best_pinned, best_lru)) {
+                        best_pinned = ps.pinned;
+                        best_lru = ps.lru;
+                        best_l = l;
+                        best_p = static_cast<int>(p);
+                    }
+                }
+            }
+            if (best_l < 0)
+                throw Error(OOMB_CONFIG_ERROR,
+                            "tiered_memory: device capacity smaller than the working set (capacity " +
+                                std::to_string(cfg.device_capacity_pages) + " pages)");
+            pages[best_l][best_p].pinned = false;
+            evict(best_l, best_p);
+        }
+    }
+
+    // ---- eviction (tiered_memory.hpp:386-403)
+    void evict(int layer, int page) {
+        PageState& ps = state(layer, page);
+        uint64_t bytes = 0;
+        const bool wb_kv = !ps.kv_host_valid;
+        const bool wb_grad = grads_allocated(layer, page) && !ps.grad_host_valid;
+        if (wb_kv) bytes += kv_bytes();
+        if (wb_grad) bytes += grad_bytes();
+        if (bytes > 0) {
+            const double start = std::max(d2h_free, clock);
+            ps.writeback_done = start + static_cast<double>(bytes) / cfg.bandwidth_bytes_per_s;
+            d2h_free = ps.writeback_done;
+            d2h += bytes;
+            ps.kv_host_valid = true;
+            ps.grad_host_valid = true;
+        }
+        if (real()) real_evict(layer, page, wb_kv, wb_grad);
+        set_tier(layer, page, 1);
+        push(EV_EVICT, clock, layer, page, bytes, -1, real() ? d2h_stream : nullptr);
+    }
+
+    void real_evict(int layer, int page, bool wb_kv, bool wb_grad) {
+        auto& p = *pool;
+        const int32_t ks = p.kvslot[layer][page], gs = p.gslot[layer][page];
+        // the copies must follow every kernel already enqueued on the compute stream
+        cudaEvent_t tail = new_event();
+        OOMB_CUDA(cudaEventRecord(tail, compute));
+        OOMB_CUDA(cudaStreamWaitEvent(d2h_stream, tail, 0));
+        spare_events.push_back(tail);
+        const size_t hidx = static_cast<size_t>(layer) * p.max_pages + page;
+        const size_t kvb = static_cast<size_t>(p.page_elems) * p.elem;
+        const size_t gb = static_cast<size_t>(p.page_elems) * sizeof(float);
+        PageState& ps = pages[layer][page];
+        if (wb_kv && ks >= 0) {
+            uint8_t* h = host_kv + hidx * kv_block;
+            OOMB_CUDA(cudaMemcpyAsync(h, static_cast<uint8_t*>(p.kpool) + ks * kvb, kvb, cudaMemcpyDeviceToHost,
+                                      d2h_stream));
+            OOMB_CUDA(cudaMemcpyAsync(h + kvb, static_cast<uint8_t*>(p.vpool) + ks * kvb, kvb, cudaMemcpyDeviceToHost,
+                                      d2h_stream));
+            ps.host_has_kv = true;
+        }
+        if (wb_grad && gs >= 0) {
+            uint8_t* h = host_grad + hidx * grad_block;
+            OOMB_CUDA(cudaMemcpyAsync(h, reinterpret_cast<uint8_t*>(p.gkpool) + gs * gb, gb, cudaMemcpyDeviceToHost,
+                                      d2h_stream));
+            OOMB_CUDA(cudaMemcpyAsync(h + gb, reinterpret_cast<uint8_t*>(p.gvpool) + gs * gb, gb,
+                                      cudaMemcpyDeviceToHost, d2h_stream));
+            ps.host_has_grad = true;
+        }
+        if (ks >= 0) {
+            OOMB_CUDA(cudaEventRecord(p.kv_slot_event(ks), d2h_stream));
+            p.kv_free.push_back(ks);
+        }
+        if (gs >= 0) {
+            OOMB_CUDA(cudaEventRecord(p.g_slot_event(gs), d2h_stream));
+            p.g_free.push_back(gs);
+        }
+        p.kvslot[layer][page] = -1;
+        p.gslot[layer][page] = -1;
+        queue_table(layer, page);
+    }
+
+    int32_t take_slot(bool grad, cudaStream_t st, const char* what) {
+        auto& fl = grad ? pool->g_free : pool->kv_free;
+        OOMB_REQUIRE(!fl.empty(), OOMB_CONFIG_ERROR,
+                     std::string("offload: no free device ") + what +
+                         " slot for an in-flight fetch (raise the pool's device_capacity_pages above the tier "
+                         "capacity)");
+        const int32_t s = fl.back();
+        fl.pop_back();
+        pool->wait_slot(grad, s, st);
+        return s;
+    }
+
+    // H2D of one page into fresh device slots (real mode).
+    void real_fetch(int layer, int page) {
+        auto& p = *pool;
+        const size_t hidx = static_cast<size_t>(layer) * p.max_pages + page;
+        const size_t kvb = static_cast<size_t>(p.page_elems) * p.elem;
+        const size_t gb = static_cast<size_t>(p.page_elems) * sizeof(float);
+        PageState& ps = pages[layer][page];
+        const int32_t ks = take_slot(false, h2d_stream, "KV");
+        p.kvslot[layer][page] = ks;
+        if (ps.host_has_kv) {
+            const uint8_t* h = host_kv + hidx * kv_block;
+            OOMB_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(p.kpool) + ks * kvb, h, kvb, cudaMemcpyHostToDevice,
+                                      h2d_stream));
+            OOMB_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(p.vpool) + ks * kvb, h + kvb, kvb, cudaMemcpyHostToDevice,
+                                      h2d_stream));
+        }
+        if (grads_allocated(layer, page)) {
+            const int32_t gs = take_slot(true, h2d_stream, "gradient");
+            p.gslot[layer][page] = gs;
+            if (ps.host_has_grad) {
+                const uint8_t* h = host_grad + hidx * grad_block;
+                OOMB_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(p.gkpool) + gs * gb, h, gb,
+                                          cudaMemcpyHostToDevice, h2d_stream));
+                OOMB_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(p.gvpool) + gs * gb, h + gb, gb,
+                                          cudaMemcpyHostToDevice, h2d_stream));
+            } else {
+                OOMB_CUDA(cudaMemsetAsync(reinterpret_cast<uint8_t*>(p.gkpool) + gs * gb, 0, gb, h2d_stream));
+                OOMB_CUDA(cudaMemsetAsync(reinterpret_cast<uint8_t*>(p.gvpool) + gs * gb, 0, gb, h2d_stream));
+            }
+        }
+    }
+
+    // ---- public operations
+    void on_pages_appended(int layer, int64_t b, int64_t e) {  // tiered_memory.hpp:131-145
+        sync_pages();
+        if (e <= b) return;
+        const int first = static_cast<int>(b / pt->P);
+        const int last = static_cast<int>((e - 1) / pt->P);
+        for (int p = first; p <= last; ++p) {
+            PageState& ps = state(layer, p);
+            ps.kv_host_valid = false;
+            ps.reserved = true;
+            ps.lru = ++lru_counter;
+            push(EV_FETCH_DONE, clock, layer, p, 0, -1, real() ? compute : nullptr);
+        }
+        enforce_capacity(0);
+    }
+
+    int64_t fetch_async(int layer, const int32_t* ids, int n, int chunk, bool best_effort) {  // :163-229
+        sync_pages();
+        Transfer tr;
+        tr.layer = layer;
+        std::vector<int32_t> to_transfer, to_pin;
+        double ready = clock;
+        for (int i = 0; i < n; ++i) {
+            const int32_t p = ids[i];
+            if (p < 0 || p >= static_cast<int32_t>(pt->pages[layer].size()))
+                throw Error(OOMB_STATE_ERROR, "fetch_pages: unknown page " + std::to_string(p));
+            PageState& ps = state(layer, p);
+            if (tier(layer, p) == 0) {
+                if (best_effort) {
+                    if (!ps.reserved && !ps.pinned) to_pin.push_back(p);
+                } else {
+                    ps.reserved = true;
+                    ps.pinned = false;
+                    ps.lru = ++lru_counter;
+                }
+                continue;
+            }
+            if (ps.in_flight_done > 0) {
+                tr.pages.push_back(p);
+                ready = std::max(ready, ps.in_flight_done);
+                continue;
+            }
+            to_transfer.push_back(p);
+        }
+        if (best_effort) {
+            const int64_t hr = phase == 0 ? headroom : 0;
+            const int64_t demand = static_cast<int64_t>(to_transfer.size()) + static_cast<int64_t>(to_pin.size()) + hr;
+            if (!fits_after_eviction(demand)) {
+                to_transfer.clear();
+            } else {
+                for (int32_t p : to_pin) {
+                    PageState& ps = state(layer, p);
+                    ps.pinned = true;
+                    ps.lru = ++lru_counter;
+                }
+            }
+        }
+        for (int32_t p : to_transfer) {
+            PageState& ps = state(layer, p);
+            const uint64_t bytes = page_transfer_bytes(layer, p);
+            push(EV_FETCH_ISSUED, clock, layer, p, 0, chunk, real() ? h2d_stream : nullptr);
+            const double start = std::max({h2d_free, clock, ps.writeback_done});
+            const double done = start + static_cast<double>(bytes) / cfg.bandwidth_bytes_per_s;
+            h2d_free = done;
+            ps.in_flight_done = done;
+            if (phase == 0) h2d_fwd += bytes;
+            else h2d_bwd += bytes;
+            if (real()) real_fetch(layer, p);
+            push(EV_FETCH_DONE, done, layer, p, bytes, chunk, real() ? h2d_stream : nullptr);
+            ready = std::max(ready, done);
+            tr.pages.push_back(p);
+        }
+        if (real()) {
+            tr.ev = new_event();
+            OOMB_CUDA(cudaEventRecord(tr.ev, h2d_stream));
+        }
+        tr.ready = ready;
+        transfers.push_back(std::move(tr));
+        return static_cast<int64_t>(transfers.size()) - 1;
+    }
+
+    void wait(int64_t h) {  // :234-254
+        if (h < 0 || h >= static_cast<int64_t>(transfers.size()))
+            throw Error(OOMB_STATE_ERROR, "wait: handle was never issued");
+        Transfer& tr = transfers[h];
+        if (tr.ready > clock) {
+            stall_s += tr.ready - clock;
+            clock = tr.ready;
+        }
+        if (real() && tr.ev) OOMB_CUDA(cudaStreamWaitEvent(compute, tr.ev, 0));
+        for (int32_t p : tr.pages) {
+            PageState& ps = state(tr.layer, p);
+            if (tier(tr.layer, p) == 0) continue;
+            enforce_capacity(1);
+            set_tier(tr.layer, p, 0);
+            ps.in_flight_done = 0;
+            ps.reserved = true;
+            ps.pinned = false;
+            ps.lru = ++lru_counter;
+            if (real()) queue_table(tr.layer, p);
+        }
+        tr.pages.clear();
+        flush_table();
+    }
+
+    void record_access(int layer, const int32_t* ids, int n, int chunk) {  // :256-264
+        flush_table();
+        for (int i = 0; i < n; ++i) {
+            const int32_t p = ids[i];
+            if (tier(layer, p) != 0) throw Error(OOMB_RESIDENCY_ERROR, "access to non-resident page " + std::to_string(p));
+            state(layer, p).lru = ++lru_counter;
+            push(EV_ACCESS, clock, layer, p, 0, chunk, real() ? compute : nullptr);
+        }
+    }
+
+    void advance_compute(double seconds, int chunk, int layer) {
+        push(EV_COMPUTE_BEGIN, clock, layer, -1, 0, chunk, real() ? compute : nullptr);
+        clock += seconds;
+        push(EV_COMPUTE_END, clock, layer, -1, 0, chunk, real() ? compute : nullptr);
+    }
+
+    void end_layer_use(int layer, const int32_t* ids, int n) {  // :274-280
+        for (int i = 0; i < n; ++i) {
+            state(layer, ids[i]).reserved = false;
+            state(layer, ids[i]).pinned = false;
+        }
+        enforce_capacity(0);
+        flush_table();
+    }
+
+    void release_all() {
+        for (auto& l : pages)
+            for (auto& ps : l) {
+                ps.reserved = false;
+                ps.pinned = false;
+            }
+        enforce_capacity(0);
+        flush_table();
+    }
+
+};
+
+extern "C" {
+
+int oomb_tier_create_sim(oomb_pagetable_t pt, const oomb_tier_config* cfg, oomb_tier_t* out) {
+    return guard([&] {
+        OOMB_REQUIRE(cfg->bandwidth_bytes_per_s > 0, OOMB_CONFIG_ERROR, "tiered_memory: bandwidth must be positive");
+        auto* t = new oomb_tier_s();
+        t->cfg = *cfg;
+        t->pt = &pt->pt;
+        t->sync_pages();
+        *out = t;
+    });
+}
+
+int oomb_tier_create(oomb_pool_t pool, const oomb_tier_config* cfg, void* compute_stream, oomb_tier_t* out) {
+    return guard([&] {
+        set_dev(pool);
+        OOMB_REQUIRE(cfg->bandwidth_bytes_per_s > 0, OOMB_CONFIG_ERROR, "tiered_memory: bandwidth must be positive");
+        auto* t = new oomb_tier_s();
+        try {
+            t->cfg = *cfg;
+            t->pt = pool->pt;
+            t->pool = pool;
+            t->compute = S(compute_stream);
+            OOMB_CUDA(cudaStreamCreateWithFlags(&t->h2d_stream, cudaStreamNonBlocking));
+            OOMB_CUDA(cudaStreamCreateWithFlags(&t->d2h_stream, cudaStreamNonBlocking));
+            t->kv_block = 2 * static_cast<size_t>(pool->page_elems) * pool->elem;
+            t->grad_block = 2 * static_cast<size_t>(pool->page_elems) * sizeof(float);
+            const size_t n_host = static_cast<size_t>(pool->cfg.n_layers) * pool->max_pages;
+            OOMB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&t->host_kv), n_host * t->kv_block, cudaHostAllocDefault));
+            OOMB_CUDA(
+                cudaHostAlloc(reinterpret_cast<void**>(&t->host_grad), n_host * t->grad_block, cudaHostAllocDefault));
+            OOMB_CUDA(cudaEventCreate(&t->t0));
+            OOMB_CUDA(cudaEventRecord(t->t0, t->compute));
+            pool->enforce = true;  // the engine turns residency enforcement on (tiered_memory.hpp:102-108)
+            t->sync_pages();
+        } catch (...) {
+            oomb_tier_destroy(t);
+            throw;
+        }
+        *out = t;
+    });
+}
+
+int oomb_tier_destroy(oomb_tier_t t) {
+    if (!t) return OOMB_OK;
+    if (t->real()) {
+        cudaSetDevice(t->pool->device);
+        cudaDeviceSynchronize();
+        t->pool->enforce = false;
+        for (auto& le : t->log)
+            if (le.ev) cudaEventDestroy(le.ev);
+        for (auto& tr : t->transfers)
+            if (tr.ev) cudaEventDestroy(tr.ev);
+        for (auto e : t->spare_events) cudaEventDestroy(e);
+        if (t->t0) cudaEventDestroy(t->t0);
+        if (t->h2d_stream) cudaStreamDestroy(t->h2d_stream);
+        if (t->d2h_stream) cudaStreamDestroy(t->d2h_stream);
+        cudaFreeHost(t->host_kv);
+        cudaFreeHost(t->host_grad);
+    }
+    delete t;
+    return OOMB_OK;
+}
+
+#define TIER_CALL(t, body)                     \
+    guard([&] {                                \
+        if ((t)->real()) set_dev((t)->pool);   \
+        body;                                  \
+    })
+
+int oomb_tier_begin_phase(oomb_tier_t t, int phase) { return TIER_CALL(t, t->phase = phase ? 1 : 0); }
+int oomb_tier_set_prefetch_headroom(oomb_tier_t t, int64_t pages) { return TIER_CALL(t, t->headroom = pages); }
+int oomb_tier_on_pages_appended(oomb_tier_t t, int layer, int64_t b, int64_t e) {
+    return TIER_CALL(t, t->on_pages_appended(layer, b, e));
+}
+int oomb_tier_on_grads_scattered(oomb_tier_t t, int layer, const int32_t* ids, int n) {
+    return TIER_CALL(t, for (int i = 0; i < n; ++i) t->state(layer, ids[i]).grad_host_valid = false);
+}
+int oomb_tier_fetch_async(oomb_tier_t t, int layer, const int32_t* ids, int n, int chunk, int best_effort,
+                          int64_t* handle) {
+    return TIER_CALL(t, *handle = t->fetch_async(layer, ids, n, chunk, best_effort != 0));
+}
+int oomb_tier_wait(oomb_tier_t t, int64_t handle) { return TIER_CALL(t, t->wait(handle)); }
+int oomb_tier_record_access(oomb_tier_t t, int layer, const int32_t* ids, int n, int chunk) {
+    return TIER_CALL(t, t->record_access(layer, ids, n, chunk));
+}
+int oomb_tier_advance_compute(oomb_tier_t t, double seconds, int chunk, int layer) {
+    return TIER_CALL(t, t->advance_compute(seconds, chunk, layer));
+}
+int oomb_tier_end_layer_use(oomb_tier_t t, int layer, const int32_t* ids, int n) {
+    return TIER_CALL(t, t->end_layer_use(layer, ids, n));
+}
+int oomb_tier_release_all(oomb_tier_t t) { return TIER_CALL(t, t->release_all()); }
+
+int oomb_tier_stats(oomb_tier_t t, double* out) {
+    return guard([&] {
+        out[0] = t->clock;
+        out[1] = t->stall_s;
+        out[2] = static_cast<double>(t->h2d_fwd);
+        out[3] = static_cast<double>(t->h2d_bwd);
+        out[4] = static_cast<double>(t->d2h);
+    });
+}
+
+int oomb_tier_log(oomb_tier_t t, oomb_event* out, int64_t cap, int64_t* n) {
+    return guard([&] {
+        *n = static_cast<int64_t>(t->log.size());
+        if (!out) return;
+        if (t->real()) {
+            set_dev(t->pool);
+            OOMB_CUDA(cudaDeviceSynchronize());
+        }
+        for (int64_t i = 0; i < std::min(cap, *n); ++i) {
+            out[i] = t->log[i].e;
+            if (t->real() && t->log[i].ev) {
+                float ms = 0.f;
+                OOMB_CUDA(cudaEventElapsedTime(&ms, t->t0, t->log[i].ev));
+                out[i].t = ms * 1e-3;
+            }
+        }
+    });
+}
+
+// validate_schedule (tiered_memory.cpp:47-138)
+int oomb_validate_schedule(const oomb_event* ev, int64_t n, double bw, double* out, int* n_viol) {
+    return guard([&] {
+        struct Track {
+            bool resident = false;
+            double since = 0;
+        };
+        std::map<std::pair<int, int32_t>, Track> track;
+        int viol = 0;
+        double last_compute_t = -1, prev_end = 0, begin_t = 0, busy = 0, stall = 0;
+        bool in_compute = false;
+        uint64_t transfer = 0, h2d_f = 0, h2d_b = 0, d2h_b = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            const oomb_event& e = ev[i];
+            const auto key = std::make_pair(e.layer, e.page);
+            switch (e.kind) {
+                case EV_FETCH_ISSUED: break;
+                case EV_FETCH_DONE:
+                    track[key].resident = true;
+                    track[key].since = e.t;
+                    transfer += e.bytes;
+                    if (e.phase == 0) h2d_f += e.bytes;
+                    else h2d_b += e.bytes;
+                    if (bw > 0) busy += static_cast<double>(e.bytes) / bw;
+                    break;
+                case EV_EVICT: {
+                    auto it = track.find(key);
+                    if (it == track.end() || !it->second.resident) ++viol;
+                    else it->second.resident = false;
+                    transfer += e.bytes;
+                    d2h_b += e.bytes;
+                    if (e.bytes > 0 && bw > 0) busy += static_cast<double>(e.bytes) / bw;
+                    break;
+                }
+                case EV_ACCESS: {
+                    auto it = track.find(key);
+                    if (it == track.end() || !it->second.resident || it->second.since > e.t) ++viol;
+                    break;
+                }
+                case EV_COMPUTE_BEGIN:
+                    if (e.t < last_compute_t) ++viol;
+                    last_compute_t = e.t;
+                    if (in_compute) ++viol;
+                    in_compute = true;
+                    begin_t = e.t;
+                    stall += std::max(0.0, e.t - prev_end);
+                    break;
+                case EV_COMPUTE_END:
+                    if (!in_compute) ++viol;
+                    if (e.t < begin_t) ++viol;
+                    in_compute = false;
+                    prev_end = e.t;
+                    last_compute_t = e.t;
+                    break;
+            }
+        }
+        if (in_compute) ++viol;
+        out[0] = stall;
+        out[1] = static_cast<double>(transfer);
+        out[2] = static_cast<double>(h2d_f);
+        out[3] = static_cast<double>(h2d_b);
+        out[4] = static_cast<double>(d2h_b);
+        out[5] = busy > 0 ? std::clamp(1.0 - stall / busy, 0.0, 1.0) : 1.0;
+        *n_viol = viol;
+    });
+}
+
+}  // extern "C"
