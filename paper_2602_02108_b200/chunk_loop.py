@@ -1,0 +1,106 @@
+"""The hot path's own call sequence for one attention layer over a sequence.
+
+This is the attention-only slice of ChunkTrainer::train_step
+(chunk_trainer.hpp:131-186): for every chunk in order, select pages (top-k on
+the device, or dense / local), append the chunk's K/V, run the forward; then for
+every chunk in reverse order run the backward (past-page dK/dV into the paged
+gradient pool) and the dM_i read-back (chunk_trainer.hpp:575-587). With a
+TieredEngine the residency protocol of run_chunk_ is followed: fetch right after
+selection (the q-projection point for top-k, :414-419), on_pages_appended,
+ensure_resident_ (wait + fill fetch + record_access, :356-363), end_layer_use
+after the layer (:455-462), and in the backward a one-step-ahead prefetch of the
+next (earlier) chunk's cached ids plus its own grad pages (:328-351, :531-541).
+Projections / MLP are not on the path; their inputs (q, k, v, dO per chunk) are
+supplied by the caller.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import attention as A
+from ._lib import call
+from .paged_kv import PagedCache, stream_handle
+
+
+class AttentionChunkLoop:
+    def __init__(self, cache: PagedCache, layer: int = 0, engine=None, max_chunks: int = 0):
+        self.cache = cache
+        self.cfg = cache.cfg
+        self.layer = layer
+        self.engine = engine
+        c = self.cfg
+        self.m = c.chunk_size // c.page_size
+        self.mode = c.mode_for_layer(layer)
+        self.sels: list[A.Selection] = []
+        self.saved: list[A.AttnSaved] = []
+        self.max_chunks = max_chunks
+
+    # ---- selection (chunk_trainer.hpp:292-316)
+    def _select(self, i: int, q: torch.Tensor, sel: A.Selection, stream=None) -> A.Selection:
+        n_cand = i * self.m
+        if self.mode == "topk" and n_cand > 0:
+            return A.select_pages_topk(self.cache, self.layer, q, n_cand, stream=stream, out=sel)
+        if self.mode == "local" and n_cand > 0:
+            call("oomb_select_recent", sel.handle, n_cand, self.cfg.local_window, self.m, stream_handle(stream))
+        else:
+            call("oomb_select_all", sel.handle, n_cand, self.m, stream_handle(stream))
+        return sel
+
+    def own_pages(self, i: int) -> list[int]:
+        return list(range(i * self.m, (i + 1) * self.m))
+
+    @staticmethod
+    def union(sel: A.Selection) -> list[int]:
+        return sorted(set(x for l in sel.lists() for x in l))
+
+    def forward_chunk(self, i: int, q, k, v, stream=None) -> A.AttnSaved:
+        if i >= len(self.sels):
+            kmax = self.m * (self.cfg.budget_pages() if self.mode == "topk" else
+                             (self.cfg.local_window if self.mode == "local" else self.cache.max_tokens //
+                              self.cfg.page_size))
+            self.sels.append(A.Selection(self.cache, self.m, max(kmax, 1)))
+        sel = self._select(i, q, self.sels[i], stream)
+        eng = self.engine
+        h = None
+        if eng is not None:
+            h = eng.fetch_async(self.layer, self.union(sel), i)
+        r = self.cache.append_chunk(self.layer, k, v, stream=stream)
+        if eng is not None:
+            eng.on_pages_appended(self.layer, r)
+            ids = self.union(sel)
+            eng.wait(h)
+            eng.wait(eng.fetch_async(self.layer, ids, i))
+            eng.record_access(self.layer, ids, i)
+        saved = A.attn_forward(self.cfg, q, self.cache, self.layer, sel, k, v, stream=stream)
+        if eng is not None:
+            eng.end_layer_use(self.layer, self.union(sel) + self.own_pages(i))
+        if i < len(self.saved):
+            self.saved[i] = saved
+        else:
+            self.saved.append(saved)
+        return saved
+
+    def backward_chunk(self, i: int, dout, q, k, v, stream=None, prefetch_next: bool = True) -> A.AttnGrads:
+        eng = self.engine
+        sel = self.sels[i]
+        ids = sorted(set(self.union(sel)) | set(self.own_pages(i)))
+        if eng is not None:
+            eng.wait(eng.fetch_async(self.layer, ids, i))
+            eng.record_access(self.layer, ids, i)
+            if prefetch_next and i > 0:  # step-ahead prefetch with cached ids + own grad pages
+                nxt = sorted(set(self.union(self.sels[i - 1])) | set(self.own_pages(i - 1)))
+                self._pending = eng.fetch_async(self.layer, nxt, i - 1, best_effort=True)
+        g = A.attn_backward(self.cfg, dout, q, self.cache, self.layer, k, v, self.saved[i], stream=stream)
+        if eng is not None:
+            eng.on_grads_scattered(self.layer, self.union(sel))
+        self.cache.accumulate_grad_pages(self.layer, self.own_pages(i), g.dk_cur, g.dv_cur, stream=stream)
+        if eng is not None:
+            eng.end_layer_use(self.layer, ids)
+        return g
+
+    def begin_backward(self):
+        if self.engine is not None:
+            from .tiered_memory import BACKWARD
+            self.engine.release_all_reservations()
+            self.engine.begin_phase(BACKWARD)

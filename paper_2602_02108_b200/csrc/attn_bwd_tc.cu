@@ -292,11 +292,15 @@ __global__ void __launch_bounds__(256, 1)
         const float sl2 = g.scale * kLog2e;
         const float L2 = p.Lt[static_cast<int64_t>(h) * g.C + t];
         const float Dr = p.Dt[static_cast<int64_t>(h) * g.C + t];
+        const int bpp = g.P / kTile;
+        int pid_next = n_past > 0 ? p.sel_ids[sel_begin] : 0;  // prefetched one block ahead
         for (int j = 0; j < nb; ++j) {
+            const int pid = pid_next;
+            if (j + 1 < n_past) pid_next = p.sel_ids[sel_begin + (j + 1) / bpp];
             int lim;
             if (j < n_past) {
-                const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, j, kvh, nullptr);
-                lim = b.n_valid - 1;
+                const int64_t nv = g.filled - static_cast<int64_t>(pid) * g.P - static_cast<int64_t>(j % bpp) * kTile;
+                lim = static_cast<int>(nv < 0 ? 0 : (nv > kTile ? kTile : nv)) - 1;
             } else {
                 lim = (j - n_past == qt) ? r : kTile - 1;
             }
@@ -363,7 +367,8 @@ constexpr int kKvDO = kKvQ + 2 * kTile64;        // 2 stages
 constexpr int kKvP = kKvDO + 2 * kTile64;        // 2 buffers of P^T [128 x 64]
 constexpr int kKvDS = kKvP + 2 * kPT;            // 2 buffers of dS^T
 constexpr int kKvQps = kKvDS + 2 * kPT;          // query-page list (<= 64 ints)
-constexpr int kKvBar = kKvQps + 256;
+constexpr int kKvLD = kKvQps + 256;              // 2 stages of {L[64], D[64]} fp32 (TMA bulk)
+constexpr int kKvBar = kKvLD + 1024;
 constexpr int kKvSmem = kKvBar + 256 + 1024;
 
 struct KvBars {
@@ -511,7 +516,10 @@ __global__ void __launch_bounds__(256, 1)
                 bool diag;
                 item_of(p, u, qps, i, g_kv, &h, &qt64, &diag);
                 if (i >= 2) mbar_wait(&bars->qdo_empty[st], ((i - 2) >> 1) & 1);
-                mbar_expect_tx(&bars->qdo_full[st], 2 * kTile64);
+                mbar_expect_tx(&bars->qdo_full[st], 2 * kTile64 + 512);
+                float* ld = reinterpret_cast<float*>(smem + kKvLD) + st * 128;
+                bulk_load(ld, p.Lt + static_cast<int64_t>(h) * g.C + qt64 * kQ64, 256, &bars->qdo_full[st]);
+                bulk_load(ld + 64, p.Dt + static_cast<int64_t>(h) * g.C + qt64 * kQ64, 256, &bars->qdo_full[st]);
                 for (int r = 0; r < 2; ++r) {
                     tma_load_3d(sQ + st * kTile64 + r * kRegion64, &tm_q64, &bars->qdo_full[st], r * 64, h,
                                 qt64 * kQ64);
@@ -576,8 +584,10 @@ __global__ void __launch_bounds__(256, 1)
             bool diag;
             item_of(p, u, qps, i, g_kv, &h, &qt64, &diag);
             const int q0 = qt64 * kQ64;
-            const float* Lrow = p.Lt + static_cast<int64_t>(h) * g.C + q0;
-            const float* Drow = p.Dt + static_cast<int64_t>(h) * g.C + q0;
+            // L, D of the item's 64 queries, staged into smem by the producer with Q / dO
+            const float* Lrow = reinterpret_cast<const float*>(smem + kKvLD) + st * 128;
+            const float* Drow = Lrow + 64;
+            mbar_wait(&bars->qdo_full[st], (i >> 1) & 1);  // makes the bulk-copied L / D visible
             mbar_wait(&bars->sdp_full[st], (i >> 1) & 1);
             tc_fence_after();
             float s[kQ64], dp[kQ64];

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(256, 1)
     FwdBars* bars = reinterpret_cast<FwdBars*>(smem + kSmemBar);
     const AttnGeom& g = p.g;
     const int h = blockIdx.x;
-    const int qt = blockIdx.y;
+    const int qt = (g.C / kTile) - 1 - static_cast<int>(blockIdx.y);  // longest causal prefix first (LPT)
     const int kvh = h / g.group;
     const int qp = (qt * kTile) / g.P;
     const int sel_begin = p.sel_off[qp];
@@ -277,9 +277,21 @@ __global__ void __launch_bounds__(256, 1)
         const float sl2 = g.scale * kLog2e;
         float m = -INFINITY;  // running max (log2 units) that O and l are relative to
         float l = 0.f;
+        const int bpp = g.P / kTile;
+        // the selection id of past block j is loaded one block ahead (off the critical path)
+        int pid_next = n_past_blocks > 0 ? p.sel_ids[sel_begin] : 0;
         for (int j = 0; j < nb; ++j) {
             const int b = j & 1;
-            const BlockInfo bi = block_info(p, qt, kvh, j, n_past_blocks, sel_begin, false);
+            const int pid = pid_next;
+            if (j + 1 < n_past_blocks) pid_next = p.sel_ids[sel_begin + (j + 1) / bpp];
+            int lim = kTile - 1;  // keep columns c <= lim
+            if (j < n_past_blocks) {
+                const int64_t nv = g.filled - static_cast<int64_t>(pid) * g.P - static_cast<int64_t>(j % bpp) * kTile;
+                lim = static_cast<int>(nv < 0 ? 0 : (nv > kTile ? kTile : nv)) - 1;
+            } else if (j - n_past_blocks == qt) {
+                lim = r;  // causal diagonal
+            }
+            const bool need_mask = (j >= n_past_blocks) ? (j - n_past_blocks == qt) : (lim < kTile - 1);
             mbar_wait(&bars->s_full[b], (j >> 1) & 1);
             tc_fence_after();
             uint32_t sr[kTile];
@@ -289,16 +301,19 @@ __global__ void __launch_bounds__(256, 1)
             tmem_wait_ld();
             tc_fence_before();
             mbar_arrive(&bars->s_free[b]);
-            // scale + mask, row max
-            const int lim = bi.diag ? r : (bi.n_valid - 1);  // keep columns c <= lim
-            float mx = -INFINITY;
+            if (need_mask) {
 #pragma unroll
-            for (int c = 0; c < kTile; ++c) {
-                float v = __uint_as_float(sr[c]) * sl2;
-                v = (c <= lim) ? v : -INFINITY;
-                sr[c] = __float_as_uint(v);
-                mx = fmaxf(mx, v);
+                for (int c = 0; c < kTile; ++c)
+                    if (c > lim) sr[c] = __float_as_uint(-INFINITY);
             }
+            // row max of the raw scores (8 independent chains), scaled once: sl2 > 0
+            float mx8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) mx8[u] = __uint_as_float(sr[u]);
+#pragma unroll
+            for (int c = 8; c < kTile; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
+            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
             const float m_new = fmaxf(m, mx);
             bool rescale = false;
             float alpha = 1.f;
@@ -311,14 +326,14 @@ __global__ void __launch_bounds__(256, 1)
             // P buffer b was read by PV_{j-2}
             if (j >= 2) mbar_wait(&bars->pv_done[b], ((j - 2) >> 1) & 1);
             uint8_t* pb = sP + b * kTileBytes;
-            float rs = 0.f;
+            float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int c = 0; c < kTile / 8; ++c) {
                 float e[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    e[u] = ex2(__uint_as_float(sr[c * 8 + u]) - m_use);
-                    rs += e[u];
+                    e[u] = ex2(fmaf(__uint_as_float(sr[c * 8 + u]), sl2, -m_use));
+                    rs8[u] += e[u];
                 }
                 uint4 pk;
                 pk.x = pack_bf16(e[0], e[1]);
@@ -342,6 +357,7 @@ __global__ void __launch_bounds__(256, 1)
                 }
                 tmem_wait_st();
             }
+            const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
             l = l * alpha + rs;
             fence_proxy_async_smem();
             tc_fence_before();

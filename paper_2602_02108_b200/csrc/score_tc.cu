@@ -143,16 +143,23 @@ __global__ void __launch_bounds__(192, 1)
             tc_fence_before();
             mbar_arrive(&bars->s_free[b]);
             const int valid = p.n - j * kTile;  // columns >= valid are padding
-            float mx = -INFINITY;
+            if (valid < kTile) {
 #pragma unroll
-            for (int c = 0; c < kTile; ++c) {
-                s[c] = (c < valid) ? s[c] * p.sl2 : -INFINITY;
-                mx = fmaxf(mx, s[c]);
+                for (int c = 0; c < kTile; ++c)
+                    if (c >= valid) s[c] = -INFINITY;
             }
-            const float m_new = fmaxf(m, mx);
-            float acc = 0.f;
+            float mx8[8];
 #pragma unroll
-            for (int c = 0; c < kTile; ++c) acc += ex2(s[c] - m_new);
+            for (int u = 0; u < 8; ++u) mx8[u] = s[u];
+#pragma unroll
+            for (int c = 8; c < kTile; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
+            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * p.sl2;
+            const float m_new = fmaxf(m, mx);
+            float a8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int c = 0; c < kTile; ++c) a8[c & 7] += ex2(fmaf(s[c], p.sl2, -m_new));
+            const float acc = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
             l = (m == -INFINITY ? 0.f : l * ex2(m - m_new)) + acc;
             m = m_new;
         }
@@ -168,7 +175,8 @@ __global__ void __launch_bounds__(192, 1)
 // ---------------------------------------------------------------- pass 2
 constexpr int kVoK = 0;
 constexpr int kVoQ = kVoK + kTileBytes;            // 3 stages
-constexpr int kVoBar = kVoQ + 3 * kTileBytes;
+constexpr int kVoST = kVoQ + 3 * kTileBytes;       // 3 stages of {m2[128], 1/l[128]} (TMA bulk)
+constexpr int kVoBar = kVoST + 3 * 1024;
 constexpr int kVoSmem = kVoBar + 256 + 1024;
 
 __global__ void __launch_bounds__(192, 1)
@@ -221,7 +229,10 @@ __global__ void __launch_bounds__(192, 1)
                 int qp, h, tile;
                 item(i, &qp, &h, &tile);
                 if (i >= 3) mbar_wait(&bars->k_empty[st], ((i - 3) / 3) & 1);
-                mbar_expect_tx(&bars->k_full[st], kTileBytes);
+                mbar_expect_tx(&bars->k_full[st], kTileBytes + 1024);
+                float* stt = reinterpret_cast<float*>(smem + kVoST) + st * 256;
+                bulk_load(stt, p.m2 + static_cast<int64_t>(h) * p.C + tile * kTile, 512, &bars->k_full[st]);
+                bulk_load(stt + 128, p.il + static_cast<int64_t>(h) * p.C + tile * kTile, 512, &bars->k_full[st]);
                 for (int r = 0; r < 2; ++r)
                     tma_load_3d(sQ + st * kTileBytes + r * kRegion, &tm_q, &bars->k_full[st], r * 64, h,
                                 tile * kTile);
@@ -251,11 +262,12 @@ __global__ void __launch_bounds__(192, 1)
         const int r = quarter * 32 + lane;  // page row of the block
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         const int page = pb * kTile + r;
-        float acc = 0.f;
+        float acc4[4] = {0.f, 0.f, 0.f, 0.f};
         for (int i = 0; i < n_items; ++i) {
-            const int b = i & 1;
+            const int b = i & 1, st = i % 3;
             int qp, h, tile;
             item(i, &qp, &h, &tile);
+            mbar_wait(&bars->k_full[st], (i / 3) & 1);  // makes the bulk-copied stats visible
             mbar_wait(&bars->s_full[b], (i >> 1) & 1);
             tc_fence_after();
             float s[kTile];
@@ -265,20 +277,21 @@ __global__ void __launch_bounds__(192, 1)
             tmem_wait_ld();
             tc_fence_before();
             mbar_arrive(&bars->s_free[b]);
-            const float* mrow = p.m2 + static_cast<int64_t>(h) * p.C + tile * kTile;
-            const float* lrow = p.il + static_cast<int64_t>(h) * p.C + tile * kTile;
+            const float* mrow = reinterpret_cast<const float*>(smem + kVoST) + st * 256;
+            const float* lrow = mrow + 128;
 #pragma unroll
             for (int c4 = 0; c4 < kTile / 4; ++c4) {
                 const float4 mm = *reinterpret_cast<const float4*>(mrow + c4 * 4);
                 const float4 ll = *reinterpret_cast<const float4*>(lrow + c4 * 4);
-                acc += ex2(s[c4 * 4 + 0] * p.sl2 - mm.x) * ll.x;
-                acc += ex2(s[c4 * 4 + 1] * p.sl2 - mm.y) * ll.y;
-                acc += ex2(s[c4 * 4 + 2] * p.sl2 - mm.z) * ll.z;
-                acc += ex2(s[c4 * 4 + 3] * p.sl2 - mm.w) * ll.w;
+                acc4[0] = fmaf(ex2(fmaf(s[c4 * 4 + 0], p.sl2, -mm.x)), ll.x, acc4[0]);
+                acc4[1] = fmaf(ex2(fmaf(s[c4 * 4 + 1], p.sl2, -mm.y)), ll.y, acc4[1]);
+                acc4[2] = fmaf(ex2(fmaf(s[c4 * 4 + 2], p.sl2, -mm.z)), ll.z, acc4[2]);
+                acc4[3] = fmaf(ex2(fmaf(s[c4 * 4 + 3], p.sl2, -mm.w)), ll.w, acc4[3]);
             }
             if ((i + 1) % per_qp == 0) {  // finished every (head, tile) of this query page
+                const float acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
                 if (page < p.n) p.vote_part[(static_cast<int64_t>(kvh) * p.m + qp) * p.n + page] = acc;
-                acc = 0.f;
+                acc4[0] = acc4[1] = acc4[2] = acc4[3] = 0.f;
             }
         }
     }

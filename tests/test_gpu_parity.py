@@ -240,6 +240,34 @@ def test_scoring_and_selection_parity(geom, dtype):
     assert checked >= 1
 
 
+@pytest.mark.parametrize("n_pages,tokens", [(300, 512), (1000, 1024), (40, 256)])
+def test_tc_scorer_matches_exact_scorer(n_pages, tokens):
+    """The tcgen05 two-pass scorer against the exact SIMT scorer on the same pool:
+    votes within the bf16-operand tolerance, and identical top-k where margins allow."""
+    from paper_2602_02108_b200.attention import select_pages_topk
+    c = Cfg(n_layers=1, n_q_heads=28, n_kv_heads=4, head_dim=128, chunk_size=tokens, page_size=128,
+            retrieval_budget=8 * 128)
+    cache = cache_for(c, "bf16", max_tokens=(n_pages + 8) * 128)
+    g = torch.Generator(device="cuda").manual_seed(n_pages)
+    k = torch.randn(n_pages * 128, 4, 128, device="cuda", generator=g)
+    k += 1.5 * torch.randn(n_pages, 1, 4, 128, device="cuda", generator=g).repeat_interleave(128, 0)[:, 0]
+    cache.append_chunk(0, k.bfloat16(), torch.randn_like(k).bfloat16())
+    q = torch.randn(tokens, 28, 128, device="cuda", generator=g).bfloat16()
+    tc = select_pages_topk(cache, 0, q, n_pages)
+    v_tc = tc.vote.clone()
+    cache.set_kernel_policy("simt")
+    ex = select_pages_topk(cache, 0, q, n_pages)
+    v_ex = ex.vote.clone()
+    torch.cuda.synchronize()
+    assert rel(T(v_tc), T(v_ex)) < 5e-3
+    a, b = tc.lists(), ex.lists()
+    vv = T(v_ex)
+    for i in range(len(a)):
+        row = np.sort(vv[i])[::-1]
+        if (row[7] - row[8]) / row[7] > 5e-2:
+            assert a[i] == b[i]
+
+
 # ---------------------------------------------------------------------------
 # attention forward / backward
 # ---------------------------------------------------------------------------
