@@ -158,6 +158,14 @@ OOMB_API int oomb_score_pages(const void* q, int64_t tokens, int n_q_heads, int 
 OOMB_API int oomb_select_pages_topk(oomb_pool_t pool, int layer, const void* q, int64_t tokens, int n_candidates,
                            oomb_selection_t sel, float* vote_scratch, void* stream);
 
+/* KV-group sharding support: the vote of score_pages sums over ALL q-heads
+ * (attention.hpp:44-64). A rank holding a subset of KV groups computes per-group partial votes
+ * [Hkv_local][m][n] fp32; after an all-gather in global group order, oomb_vote_reduce sums them in
+ * that fixed order, so every rank (and the single-GPU path) selects identically. */
+OOMB_API int oomb_score_pages_partial(oomb_pool_t pool, int layer, const void* q, int64_t tokens, int n_candidates,
+                                      float* partials, void* stream);
+OOMB_API int oomb_vote_reduce(const float* partials, int groups, int64_t m, int64_t n, float* vote, void* stream);
+
 /* ---- attention ---------------------------------------------------------- */
 /* attn_forward  attention.hpp:156-208: q [C][Hq][hd], k_cur/v_cur [C][Hkv][hd] (pool dtype) ->
  * out [C][Hq][hd] (pool dtype), lse [C][Hq] fp32 (natural log). */

@@ -337,7 +337,7 @@ __global__ void score_stats_kernel(const T* __restrict__ q, int64_t tokens, int 
 template <typename T>
 __global__ void score_vote_kernel(const T* __restrict__ q, int64_t tokens, int Hq, int hd,
                                   const float* __restrict__ kavg, int64_t n, int Hkv, int P, float scale,
-                                  const float2* __restrict__ stats, float* __restrict__ vote) {
+                                  const float2* __restrict__ stats, float* __restrict__ vote, int h0, int h1) {
     extern __shared__ float qs[];  // [hd]
     const int qp = blockIdx.y;
     const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -346,7 +346,7 @@ __global__ void score_vote_kernel(const T* __restrict__ q, int64_t tokens, int H
     const int64_t t0 = static_cast<int64_t>(qp) * P;
     const int64_t t1 = min(tokens, t0 + P);
     for (int64_t t = t0; t < t1; ++t) {
-        for (int h = 0; h < Hq; ++h) {
+        for (int h = h0; h < h1; ++h) {
             __syncthreads();
             for (int j = threadIdx.x; j < hd; j += blockDim.x) qs[j] = to_f(q[(t * Hq + h) * hd + j]);
             __syncthreads();
@@ -363,7 +363,8 @@ __global__ void score_vote_kernel(const T* __restrict__ q, int64_t tokens, int H
 }
 
 void launch_score_simt(int dtype, const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, int64_t n,
-                       int Hkv, int P, float scale, float* vote, float* stats_scratch, cudaStream_t st) {
+                       int Hkv, int P, float scale, float* vote, float* stats_scratch, cudaStream_t st,
+                       bool partial_only) {
     ProfScope prof_(PK_SCORE, st);
     const int64_t rows = tokens * Hq;
     const int m = static_cast<int>((tokens + P - 1) / P);
@@ -374,14 +375,18 @@ void launch_score_simt(int dtype, const void* q, int64_t tokens, int Hq, int hd,
         auto qq = static_cast<const __nv_bfloat16*>(q);
         score_stats_kernel<<<g1, 256, 0, st>>>(qq, tokens, Hq, hd, k_avg, n, Hkv, scale, stats);
         check_launch("score_stats_kernel");
-        score_vote_kernel<<<g2, 128, hd * sizeof(float), st>>>(qq, tokens, Hq, hd, k_avg, n, Hkv, P, scale, stats,
-                                                               vote);
+        for (int g = 0; g < (partial_only ? Hkv : 1); ++g)
+            score_vote_kernel<<<g2, 128, hd * sizeof(float), st>>>(
+                qq, tokens, Hq, hd, k_avg, n, Hkv, P, scale, stats, vote + (partial_only ? g * m * n : 0),
+                partial_only ? g * (Hq / Hkv) : 0, partial_only ? (g + 1) * (Hq / Hkv) : Hq);
     } else {
         auto qq = static_cast<const float*>(q);
         score_stats_kernel<<<g1, 256, 0, st>>>(qq, tokens, Hq, hd, k_avg, n, Hkv, scale, stats);
         check_launch("score_stats_kernel");
-        score_vote_kernel<<<g2, 128, hd * sizeof(float), st>>>(qq, tokens, Hq, hd, k_avg, n, Hkv, P, scale, stats,
-                                                               vote);
+        for (int g = 0; g < (partial_only ? Hkv : 1); ++g)
+            score_vote_kernel<<<g2, 128, hd * sizeof(float), st>>>(
+                qq, tokens, Hq, hd, k_avg, n, Hkv, P, scale, stats, vote + (partial_only ? g * m * n : 0),
+                partial_only ? g * (Hq / Hkv) : 0, partial_only ? (g + 1) * (Hq / Hkv) : Hq);
     }
     check_launch("score_vote_kernel");
 }

@@ -631,7 +631,7 @@ int oomb_select_topk(oomb_selection_t s, const float* vote, int m, int n, int k,
 // 128-aligned chunks use the tcgen05 scorer; everything else the exact SIMT scorer.
 static void score_impl(const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, const float* kavg_sum,
                        const int32_t* kavg_cnt, int64_t n, int Hkv, int P, int score_scale, int dtype, bool allow_tc,
-                       float* vote, cudaStream_t st) {
+                       float* vote, cudaStream_t st, bool partial_only = false) {
     OOMB_REQUIRE(n >= 1, OOMB_SHAPE_ERROR, "score_pages: needs at least one candidate page");
     OOMB_REQUIRE(Hq >= 1 && Hkv >= 1 && Hq % Hkv == 0 && hd >= 1 && hd <= 256 && P >= 1, OOMB_SHAPE_ERROR,
                  "score_pages: bad shape");
@@ -639,7 +639,7 @@ static void score_impl(const void* q, int64_t tokens, int Hq, int hd, const floa
     if (allow_tc && score_tc_supported(dtype, hd, P, tokens)) {
         void* ws = nullptr;
         OOMB_CUDA(cudaMallocAsync(&ws, score_tc_workspace(tokens, Hq, Hkv, n, P), st));
-        launch_score_tc(q, tokens, Hq, Hkv, P, kavg_sum, kavg_cnt, k_avg, n, scale, vote, ws, st);
+        launch_score_tc(q, tokens, Hq, Hkv, P, kavg_sum, kavg_cnt, k_avg, n, scale, vote, ws, st, partial_only);
         OOMB_CUDA(cudaFreeAsync(ws, st));
         return;
     }
@@ -650,7 +650,7 @@ static void score_impl(const void* q, int64_t tokens, int Hq, int hd, const floa
     }
     float* stats = nullptr;
     OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&stats), std::max<int64_t>(tokens * Hq, 1) * 8, st));
-    launch_score_simt(dtype, q, tokens, Hq, hd, kavg, n, Hkv, P, scale, vote, stats, st);
+    launch_score_simt(dtype, q, tokens, Hq, hd, kavg, n, Hkv, P, scale, vote, stats, st, partial_only);
     OOMB_CUDA(cudaFreeAsync(stats, st));
     if (!k_avg) OOMB_CUDA(cudaFreeAsync(kavg, st));
 }
@@ -664,6 +664,26 @@ int oomb_score_pages(const void* q, int64_t tokens, int Hq, int hd, const float*
 }
 
 static void select_topk_impl(oomb_selection_t s, const float* vote, int m, int n, int k, cudaStream_t st);
+
+int oomb_score_pages_partial(oomb_pool_t p, int layer, const void* q, int64_t tokens, int n_candidates,
+                             float* partials, void* stream) {
+    return guard([&] {
+        set_dev(p);
+        p->pt->check_layer(layer);
+        const int n = std::min(n_candidates, static_cast<int>(p->pt->pages[layer].size()));
+        OOMB_REQUIRE(n >= 1, OOMB_SHAPE_ERROR, "score_pages: needs at least one candidate page");
+        score_impl(q, tokens, p->cfg.n_q_heads, p->cfg.head_dim, nullptr, p->kavg_sum_layer(layer),
+                   p->kavg_cnt_layer(layer), n, p->cfg.n_kv_heads, p->cfg.page_size, p->cfg.score_scale,
+                   p->cfg.dtype, p->policy != 1, partials, S(stream), /*partial_only=*/true);
+    });
+}
+
+int oomb_vote_reduce(const float* partials, int groups, int64_t m, int64_t n, float* vote, void* stream) {
+    return guard([&] {
+        OOMB_REQUIRE(groups >= 1 && m >= 0 && n >= 0, OOMB_SHAPE_ERROR, "vote_reduce: bad shape");
+        if (m * n > 0) launch_vote_reduce(partials, groups, m * n, vote, S(stream));
+    });
+}
 
 int oomb_select_pages_topk(oomb_pool_t p, int layer, const void* q, int64_t tokens, int n_candidates,
                            oomb_selection_t sel, float* vote_scratch, void* stream) {

@@ -130,7 +130,8 @@ void launch_grad_init(const int32_t* d_pages, const int32_t* d_slots, int n, int
 void launch_zero_slots(const int32_t* d_slots, int n, float* gk, float* gv, int64_t page_elems, cudaStream_t st);
 
 void launch_score_simt(int dtype, const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, int64_t n,
-                       int Hkv, int P, float scale, float* vote, float* stats_scratch, cudaStream_t st);
+                       int Hkv, int P, float scale, float* vote, float* stats_scratch, cudaStream_t st,
+                       bool partial_only = false);
 void launch_topk(const float* vote, int m, int n, int k, int32_t* sel_off, int32_t* sel_ids, cudaStream_t st);
 void launch_fill_csr_all(int32_t* off, int32_t* ids, int m, int first, int count, cudaStream_t st);
 
@@ -170,7 +171,8 @@ bool score_tc_supported(int dtype, int hd, int P, int64_t tokens);
 size_t score_tc_workspace(int64_t tokens, int Hq, int Hkv, int64_t n, int P);
 void launch_score_tc(const void* q, int64_t tokens, int Hq, int Hkv, int P, const float* kavg_sum,
                      const int32_t* kavg_cnt, const float* kavg_f32, int64_t n, float scale, float* vote, void* ws,
-                     cudaStream_t st);
+                     cudaStream_t st, bool partial_only = false);
+void launch_vote_reduce(const float* part, int groups, int64_t mn, float* vote, cudaStream_t st);
 void launch_debug_tc_gemm(int mode, const void* a, const void* b, float* c, int m, int n, int k, cudaStream_t st);
 
 // Driver entry point for cuTensorMapEncodeTiled (no libcuda link dependency).

@@ -322,9 +322,15 @@ size_t score_tc_workspace(int64_t tokens, int Hq, int Hkv, int64_t n, int P) {
            static_cast<size_t>(Hkv * m * n * 4) + 4 * 256;
 }
 
+void launch_vote_reduce(const float* part, int groups, int64_t mn, float* vote, cudaStream_t st) {
+    vote_reduce_kernel<<<static_cast<unsigned>(std::min<int64_t>((mn + 255) / 256, 2048)), 256, 0, st>>>(
+        part, groups, mn, vote);
+    check_launch("vote_reduce_kernel");
+}
+
 void launch_score_tc(const void* q, int64_t tokens, int Hq, int Hkv, int P, const float* kavg_sum,
                      const int32_t* kavg_cnt, const float* kavg_f32, int64_t n, float scale, float* vote,
-                     void* ws, cudaStream_t st) {
+                     void* ws, cudaStream_t st, bool partial_only) {
     static bool attr = false;
     if (!attr) {
         OOMB_CUDA(cudaFuncSetAttribute(score_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStSmem));
@@ -342,7 +348,7 @@ void launch_score_tc(const void* q, int64_t tokens, int Hq, int Hkv, int P, cons
     off += align(static_cast<size_t>(Hq) * tokens * 4);
     float* il = reinterpret_cast<float*>(w + off);
     off += align(static_cast<size_t>(Hq) * tokens * 4);
-    float* part = reinterpret_cast<float*>(w + off);
+    float* part = partial_only ? vote : reinterpret_cast<float*>(w + off);  // [Hkv][m][n]
 
     const int64_t tot = static_cast<int64_t>(Hkv) * n_pad * kHd;
     kavg_prep_kernel<<<static_cast<unsigned>(std::min<int64_t>((tot + 255) / 256, 4096)), 256, 0, st>>>(
@@ -362,10 +368,7 @@ void launch_score_tc(const void* q, int64_t tokens, int Hq, int Hkv, int P, cons
     check_launch("score_stats_kernel");
     score_vote_kernel<<<dim3(n_pad / kTile, Hkv, (m + kQpGroup - 1) / kQpGroup), 192, kVoSmem, st>>>(tq, tka, p);
     check_launch("score_vote_kernel");
-    const int64_t mn = static_cast<int64_t>(m) * n;
-    vote_reduce_kernel<<<static_cast<unsigned>(std::min<int64_t>((mn + 255) / 256, 2048)), 256, 0, st>>>(
-        part, Hkv, mn, vote);
-    check_launch("vote_reduce_kernel");
+    if (!partial_only) launch_vote_reduce(part, Hkv, static_cast<int64_t>(m) * n, vote, st);
 }
 
 }  // namespace oomb
