@@ -47,7 +47,14 @@ struct FwdBars {
     uint32_t tmem_base;
 };
 
-__device__ __forceinline__ void make_maps_dummy() {}
+__device__ __forceinline__ uint4 tc_pack8(const float* e) {
+    uint4 pk;
+    pk.x = pack_bf16(e[0], e[1]);
+    pk.y = pack_bf16(e[2], e[3]);
+    pk.z = pack_bf16(e[4], e[5]);
+    pk.w = pack_bf16(e[6], e[7]);
+    return pk;
+}
 
 // Write 8 consecutive bf16 (packed in 4 u32) of row r, 16-byte chunk c (0..15) of a
 // K-major SW128 [128 x 128] tile made of two [128 x 64] regions.
@@ -393,6 +400,222 @@ __global__ void __launch_bounds__(256, 1)
     if (warp == 3) tmem_dealloc<512>(tmem);
 }
 
+// ===========================================================================
+// Forward, variant 2: two CTAs per SM. Each CTA keeps S and O in 256 TMEM
+// columns and writes P (bf16) back into the S columns, so PV runs as a TS-MMA
+// (A = P from TMEM, B = V from smem) and smem holds only Q, K and V (96 KB).
+// A CTA's own S -> softmax -> PV chain is serial; the co-resident CTA fills the
+// tensor pipe while this one runs its softmax.
+// ===========================================================================
+constexpr int kF2Q = 0;
+constexpr int kF2K = kF2Q + kTileBytes;
+constexpr int kF2V = kF2K + kTileBytes;
+constexpr int kF2Bar = kF2V + kTileBytes;
+constexpr int kF2Smem = kF2Bar + 128 + 1024;
+
+struct F2Bars {
+    uint64_t q_full, k_full, k_empty, v_full, v_empty, s_full, p_full, pv_done;
+    uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(192, 2)
+    attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kc,
+                        const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kp,
+                        const __grid_constant__ CUtensorMap tm_vp, FwdParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    F2Bars* bars = reinterpret_cast<F2Bars*>(smem + kF2Bar);
+    const AttnGeom& g = p.g;
+    const int h = blockIdx.x;
+    const int qt = (g.C / kTile) - 1 - static_cast<int>(blockIdx.y);
+    const int kvh = h / g.group;
+    const int qp = (qt * kTile) / g.P;
+    const int sel_begin = p.sel_off[qp];
+    const int n_past_blocks = (p.sel_off[qp + 1] - sel_begin) * (g.P / kTile);
+    const int nb = n_past_blocks + qt + 1;
+    const int warp = warp_id(), lane = lane_id();
+    if (threadIdx.x == 0) {
+        mbar_init(&bars->q_full, 1);
+        mbar_init(&bars->k_full, 1);
+        mbar_init(&bars->k_empty, 1);
+        mbar_init(&bars->v_full, 1);
+        mbar_init(&bars->v_empty, 1);
+        mbar_init(&bars->s_full, 1);
+        mbar_init(&bars->p_full, 128);
+        mbar_init(&bars->pv_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<256>(&bars->tmem_base);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem_base;
+    const uint32_t tm_s = tmem, tm_o = tmem + 128;  // P (bf16x2) overwrites S columns [0, 64)
+    uint8_t* sQ = smem + kF2Q;
+    uint8_t* sK = smem + kF2K;
+    uint8_t* sV = smem + kF2V;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(&bars->q_full, kTileBytes);
+            for (int r = 0; r < 2; ++r) tma_load_3d(sQ + r * kRegion, &tm_q, &bars->q_full, r * 64, h, qt * kTile);
+            for (int j = 0; j < nb; ++j) {
+                const BlockInfo b = block_info(p, qt, kvh, j, n_past_blocks, sel_begin, true);
+                if (j >= 1) mbar_wait(&bars->k_empty, (j - 1) & 1);
+                mbar_expect_tx(&bars->k_full, kTileBytes);
+                for (int r = 0; r < 2; ++r) {
+                    if (b.past) tma_load_2d(sK + r * kRegion, &tm_kp, &bars->k_full, r * 64, b.row);
+                    else tma_load_3d(sK + r * kRegion, &tm_kc, &bars->k_full, r * 64, kvh, b.row);
+                }
+                if (j >= 1) mbar_wait(&bars->v_empty, (j - 1) & 1);
+                mbar_expect_tx(&bars->v_full, kTileBytes);
+                for (int r = 0; r < 2; ++r) {
+                    if (b.past) tma_load_2d(sV + r * kRegion, &tm_vp, &bars->v_full, r * 64, b.row);
+                    else tma_load_3d(sV + r * kRegion, &tm_vc, &bars->v_full, r * 64, kvh, b.row);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kTile, 0, 0);
+        constexpr uint32_t idesc_o = make_idesc_bf16(kTile, kHd, 0, 1);
+        const uint32_t q_addr = smem_u32(sQ), k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+        mbar_wait(&bars->q_full, 0);
+        for (int j = 0; j < nb; ++j) {
+            mbar_wait(&bars->k_full, j & 1);
+            if (j >= 1) mbar_wait(&bars->pv_done, (j - 1) & 1);  // PV_{j-1} has read P out of the S columns
+            tc_fence_after();
+            if (lane == 0) {
+                for (int ks = 0; ks < kHd / 16; ++ks)
+                    umma_f16_ss(tm_s, desc_kmajor(q_addr, ks), desc_kmajor(k_addr, ks), idesc_s, ks > 0);
+                umma_commit(&bars->s_full);
+                umma_commit(&bars->k_empty);
+            }
+            __syncwarp();
+            mbar_wait(&bars->p_full, j & 1);
+            mbar_wait(&bars->v_full, j & 1);
+            tc_fence_after();
+            if (lane == 0) {
+                for (int ks = 0; ks < kTile / 16; ++ks)
+                    umma_f16_ts(tm_o, tm_s + ks * 8, desc_mnmajor(v_addr, ks), idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
+                umma_commit(&bars->pv_done);
+                umma_commit(&bars->v_empty);
+            }
+            __syncwarp();
+        }
+    } else {
+        const int quarter = warp & 3;  // warps 2..5 -> lane quarters 2,3,0,1
+        const int r = quarter * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        const float sl2 = g.scale * kLog2e;
+        const int bpp = g.P / kTile;
+        float m = -INFINITY, l = 0.f;
+        int pid_next = n_past_blocks > 0 ? p.sel_ids[sel_begin] : 0;
+        for (int j = 0; j < nb; ++j) {
+            const int pid = pid_next;
+            if (j + 1 < n_past_blocks) pid_next = p.sel_ids[sel_begin + (j + 1) / bpp];
+            int lim = kTile - 1;
+            if (j < n_past_blocks) {
+                const int64_t nv = g.filled - static_cast<int64_t>(pid) * g.P - static_cast<int64_t>(j % bpp) * kTile;
+                lim = static_cast<int>(nv < 0 ? 0 : (nv > kTile ? kTile : nv)) - 1;
+            } else if (j - n_past_blocks == qt) {
+                lim = r;
+            }
+            mbar_wait(&bars->s_full, j & 1);
+            tc_fence_after();
+            // pass 1: row max of the raw scores
+            float mx8[8] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int c = 0; c < kTile / 32; ++c) {
+                uint32_t a[32];
+                tmem_ld32(tm_s + c * 32 + lane_off, a);
+                tmem_wait_ld();
+#pragma unroll
+                for (int u = 0; u < 32; ++u) {
+                    const float v = (c * 32 + u <= lim) ? __uint_as_float(a[u]) : -INFINITY;
+                    mx8[u & 7] = fmaxf(mx8[u & 7], v);
+                }
+            }
+            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
+            const float m_new = fmaxf(m, mx);
+            float alpha = 1.f;
+            bool rescale = false;
+            if (m == -INFINITY || m_new > m + kRescaleThreshold) {
+                alpha = (m == -INFINITY) ? 0.f : ex2(m - m_new);
+                rescale = j > 0 && m != -INFINITY;
+                m = m_new;
+            }
+            const float m_use = (m == -INFINITY) ? 0.f : m;
+            // O rescale: PV_{j-1} is complete (S_j was issued after it)
+            if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll 1
+                for (int c = 0; c < kHd / 16; ++c) {
+                    uint32_t o[16];
+                    tmem_ld16(tm_o + c * 16 + lane_off, o);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * alpha);
+                    tmem_st16(tm_o + c * 16 + lane_off, o);
+                }
+            }
+            // pass 2: P = exp2(s*sl2 - m) packed bf16x2 into S columns [0, 64)
+            float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int c = 0; c < kTile / 32; ++c) {
+                uint32_t a[32];
+                tmem_ld32(tm_s + c * 32 + lane_off, a);
+                tmem_wait_ld();
+                uint32_t pk[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int c0 = c * 32 + 2 * u;
+                    float e0 = ex2(fmaf(__uint_as_float(a[2 * u]), sl2, -m_use));
+                    float e1 = ex2(fmaf(__uint_as_float(a[2 * u + 1]), sl2, -m_use));
+                    e0 = (c0 <= lim) ? e0 : 0.f;
+                    e1 = (c0 + 1 <= lim) ? e1 : 0.f;
+                    rs8[(2 * u) & 7] += e0;
+                    rs8[(2 * u + 1) & 7] += e1;
+                    pk[u] = pack_bf16(e0, e1);
+                }
+                tmem_st16(tm_s + c * 16 + lane_off, pk);  // P cols [16c, 16c+16) — below S cols still unread
+            }
+            tmem_wait_st();
+            const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+            l = l * alpha + rs;
+            tc_fence_before();
+            mbar_arrive(&bars->p_full);
+        }
+        mbar_wait(&bars->pv_done, (nb - 1) & 1);
+        tc_fence_after();
+        const int t = qt * kTile + r;
+        const float inv = 1.f / l;
+        __nv_bfloat16* orow = p.out + (static_cast<int64_t>(t) * g.Hq + h) * kHd;
+#pragma unroll 1
+        for (int c = 0; c < kHd / 16; ++c) {
+            uint32_t o[16];
+            tmem_ld16(tm_o + c * 16 + lane_off, o);
+            tmem_wait_ld();
+            float f[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) f[u] = __uint_as_float(o[u]) * inv;
+            *reinterpret_cast<uint4*>(orow + c * 16) = tc_pack8(f);
+            *reinterpret_cast<uint4*>(orow + c * 16 + 8) = tc_pack8(f + 8);
+        }
+        p.lse[static_cast<int64_t>(t) * g.Hq + h] = (m + __log2f(l)) * kLn2;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<256>(tmem);
+}
+
+static int fwd_variant() {
+    static int v = [] {
+        const char* e = getenv("OOMB_FWD_KERNEL");
+        return e ? atoi(e) : 2;
+    }();
+    return v;
+}
+
 void launch_attn_fwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* q, const int32_t* sel_off,
                         const int32_t* sel_ids, const int32_t* d_kvslot_layer, const void* k_cur, const void* v_cur,
                         void* out, float* lse, int* d_err, cudaStream_t st) {
@@ -400,6 +623,7 @@ void launch_attn_fwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* q
     static bool attr_set = false;
     if (!attr_set) {
         OOMB_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem));
+        OOMB_CUDA(cudaFuncSetAttribute(attn_fwd_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kF2Smem));
         attr_set = true;
     }
     const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, kHd);
@@ -407,8 +631,13 @@ void launch_attn_fwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* q
     const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, kHd);
     FwdParams p{g, sel_off, sel_ids, d_kvslot_layer, static_cast<__nv_bfloat16*>(out), lse, d_err};
     dim3 grid(g.Hq, g.C / kTile);
-    attn_fwd_tc_kernel<<<grid, 256, kFwdSmem, st>>>(tq, tkc, tvc, maps.kpool, maps.vpool, p);
-    check_launch("attn_fwd_tc_kernel");
+    if (fwd_variant() == 2) {
+        attn_fwd_tc2_kernel<<<grid, 192, kF2Smem, st>>>(tq, tkc, tvc, maps.kpool, maps.vpool, p);
+        check_launch("attn_fwd_tc2_kernel");
+    } else {
+        attn_fwd_tc_kernel<<<grid, 256, kFwdSmem, st>>>(tq, tkc, tvc, maps.kpool, maps.vpool, p);
+        check_launch("attn_fwd_tc_kernel");
+    }
 }
 
 // ===========================================================================
@@ -435,17 +664,18 @@ __global__ void __launch_bounds__(128, 1)
         mbar_init(mma_bar, 1);
         fence_barrier_init();
     }
-    if (warp == 0) tmem_alloc<256>(tslot);
+    if (warp == 0) tmem_alloc<512>(tslot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
+    const bool a_tmem = mode >= 3;  // A operand staged in TMEM columns [256, 256 + K/2)
     if (threadIdx.x == 0) {
-        const int a_bytes = (mode == 2) ? 0 : 128 * k * 2;
+        const int a_bytes = (mode == 2 || a_tmem) ? 0 : 128 * k * 2;
         mbar_expect_tx(bar, a_bytes + n * k * 2);
-        if (mode != 2)
+        if (mode != 2 && !a_tmem)
             for (int kb = 0; kb < k / 64; ++kb) tma_load_2d(sA + kb * kRegion, &ta, bar, kb * 64, 0);
-        if (mode == 0)
+        if (mode == 0 || mode == 4)
             for (int kb = 0; kb < k / 64; ++kb) tma_load_2d(sB + kb * n * 128, &tb, bar, kb * 64, 0);
         else
             for (int nb = 0; nb < n / 64; ++nb) tma_load_2d(sB + nb * k * 128, &tb, bar, nb * 64, 0);
@@ -459,18 +689,31 @@ __global__ void __launch_bounds__(128, 1)
         }
         fence_proxy_async_smem();
     }
+    if (a_tmem) {  // row r -> TMEM lane r, bf16 pairs packed per 32-bit column
+        const int r = threadIdx.x;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(a_raw + static_cast<int64_t>(r) * k);
+        for (int c = 0; c < k / 32; ++c) {
+            uint32_t v[16];
+            for (int u = 0; u < 16; ++u) v[u] = src[c * 16 + u];
+            tmem_st16(tmem + 256 + c * 16 + (static_cast<uint32_t>(warp * 32) << 16), v);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+    }
     __syncthreads();
     mbar_wait(bar, 0);
     tc_fence_after();
     if (threadIdx.x == 0) {
-        const uint32_t idesc = make_idesc_bf16(128, n, 0, mode == 0 ? 0 : 1);
+        const bool b_kmajor = mode == 0 || mode == 4;
+        const uint32_t idesc = make_idesc_bf16(128, n, 0, b_kmajor ? 0 : 1);
         const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
         for (int ks = 0; ks < k / 16; ++ks) {
             const uint64_t ad = make_sdesc_sw128(a0 + (ks >> 2) * kRegion + (ks & 3) * 32, 16, 1024);
             uint64_t bd;
-            if (mode == 0) bd = make_sdesc_sw128(b0 + (ks >> 2) * n * 128 + (ks & 3) * 32, 16, 1024);
+            if (b_kmajor) bd = make_sdesc_sw128(b0 + (ks >> 2) * n * 128 + (ks & 3) * 32, 16, 1024);
             else bd = make_sdesc_sw128(b0 + ks * 2048, k * 128, 1024);
-            umma_f16_ss(tmem, ad, bd, idesc, ks > 0);
+            if (a_tmem) umma_f16_ts(tmem, tmem + 256 + ks * 8, bd, idesc, ks > 0);
+            else umma_f16_ss(tmem, ad, bd, idesc, ks > 0);
         }
         umma_commit(mma_bar);
     }
@@ -486,11 +729,11 @@ __global__ void __launch_bounds__(128, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc<256>(tmem);
+    if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
 void launch_debug_tc_gemm(int mode, const void* a, const void* b, float* c, int m, int n, int k, cudaStream_t st) {
-    OOMB_REQUIRE(k <= 128 && (mode != 0 || n <= 256), OOMB_SHAPE_ERROR, "debug gemm: K <= 128");
+    OOMB_REQUIRE(k <= 128 && mode >= 0 && mode <= 4, OOMB_SHAPE_ERROR, "debug gemm: K <= 128, mode 0..4");
     static bool attr_set = false;
     if (!attr_set) {
         OOMB_CUDA(cudaFuncSetAttribute(debug_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDbgSmem));
@@ -503,7 +746,7 @@ void launch_debug_tc_gemm(int mode, const void* a, const void* b, float* c, int 
         const uint32_t box[2] = {64, 128};
         encode_or_throw(&ta, 2, a, dims, strides, box);
     }
-    if (mode == 0) {
+    if (mode == 0 || mode == 4) {
         const uint64_t dims[2] = {static_cast<uint64_t>(k), static_cast<uint64_t>(n)};
         const uint64_t strides[1] = {static_cast<uint64_t>(k) * 2};
         const uint32_t box[2] = {64, static_cast<uint32_t>(n)};

@@ -79,12 +79,13 @@ def bf16_case(case):
 # tcgen05 / TMA building blocks
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("mode,n,k", [(0, 128, 128), (0, 256, 64), (0, 64, 128), (1, 128, 128), (1, 256, 64),
-                                      (2, 128, 128), (2, 64, 64)])
+                                      (2, 128, 128), (2, 64, 64), (3, 128, 128), (3, 64, 64), (4, 128, 128),
+                                      (4, 64, 128)])
 def test_tc_gemm_descriptors(mode, n, k):
     from paper_2602_02108_b200.attention import debug_tc_gemm
     g = torch.Generator(device="cuda").manual_seed(mode * 1000 + n + k)
     a = torch.randn(128, k, device="cuda", generator=g).bfloat16()
-    if mode == 0:
+    if mode in (0, 4):
         b = torch.randn(n, k, device="cuda", generator=g).bfloat16()
         want = a.float() @ b.float().T
     else:
