@@ -53,6 +53,7 @@ constexpr int kStSmem = kStBar + 256 + 1024;
 struct StatsBars {
     uint64_t q_full;
     uint64_t k_full[3], k_empty[3];
+    uint64_t st_empty[3];  // vote kernel: the compute warps finished reading a stage's stats
     uint64_t s_full[2], s_free[2];
     uint32_t tmem_base;
 };
@@ -198,6 +199,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int i = 0; i < 3; ++i) {
             mbar_init(&bars->k_full[i], 1);
             mbar_init(&bars->k_empty[i], 1);
+            mbar_init(&bars->st_empty[i], 128);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bars->s_full[i], 1);
@@ -228,7 +230,12 @@ __global__ void __launch_bounds__(192, 1)
                 const int st = i % 3;
                 int qp, h, tile;
                 item(i, &qp, &h, &tile);
-                if (i >= 3) mbar_wait(&bars->k_empty[st], ((i - 3) / 3) & 1);
+                if (i >= 3) {
+                    mbar_wait(&bars->k_empty[st], ((i - 3) / 3) & 1);
+                    // the compute warps read this stage's stats and waited on its k_full phase:
+                    // only then may the phase advance again (no parity aliasing)
+                    mbar_wait(&bars->st_empty[st], ((i - 3) / 3) & 1);
+                }
                 mbar_expect_tx(&bars->k_full[st], kTileBytes + 1024);
                 float* stt = reinterpret_cast<float*>(smem + kVoST) + st * 256;
                 bulk_load(stt, p.m2 + static_cast<int64_t>(h) * p.C + tile * kTile, 512, &bars->k_full[st]);
@@ -288,6 +295,7 @@ __global__ void __launch_bounds__(192, 1)
                 acc4[2] = fmaf(ex2(fmaf(s[c4 * 4 + 2], p.sl2, -mm.z)), ll.z, acc4[2]);
                 acc4[3] = fmaf(ex2(fmaf(s[c4 * 4 + 3], p.sl2, -mm.w)), ll.w, acc4[3]);
             }
+            mbar_arrive(&bars->st_empty[st]);
             if ((i + 1) % per_qp == 0) {  // finished every (head, tile) of this query page
                 const float acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
                 if (page < p.n) p.vote_part[(static_cast<int64_t>(kvh) * p.m + qp) * p.n + page] = acc;
