@@ -240,9 +240,13 @@ OOMB_API int oomb_tier_release_all(oomb_tier_t t);
 OOMB_API int oomb_tier_stats(oomb_tier_t t, double* out);
 OOMB_API int oomb_tier_log(oomb_tier_t t, oomb_event* out, int64_t cap, int64_t* n);
 /* validate_schedule (tiered_memory.cpp:47-138): out[6] = {stall_s, transfer_bytes, h2d_fwd, h2d_bwd,
- * d2h, overlap_fraction}; n_violations = residency/order violations found. */
+ * d2h, overlap_fraction}; n_violations = residency/order violations found. When viol_event / viol_code
+ * are non-null, the first viol_cap violations are described by the index of the offending event (-1 for
+ * the end-of-log check) and a code: 1 evict of non-resident page, 2 access before fetch_done (or after
+ * evict), 3 compute timestamps decrease, 4 nested compute_begin, 5 compute_end without begin, 6 compute
+ * segment ends before it begins, 7 unterminated compute segment — the reference's message list. */
 OOMB_API int oomb_validate_schedule(const oomb_event* events, int64_t n, double bandwidth, double* out,
-                                    int* n_violations);
+                                    int* n_violations, int64_t* viol_event, int32_t* viol_code, int64_t viol_cap);
 
 /* ---- page-table host logic (no device) -----------------------------------
  * The arena / LIFO free-list / lazy-gradient-page bookkeeping of PagedCache

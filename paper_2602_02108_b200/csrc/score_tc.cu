@@ -2,8 +2,12 @@
 //
 // tcgen05 page scorer — score_pages (attention.hpp:32-67) for bf16 mode:
 //
-//   kavg_prep     K_avg = sum * (1/count) (paged_kv.hpp:170-183, fp32 exact), rounded
-//                 to bf16 into a head-major, 128-padded [Hkv][n_pad][hd] operand.
+//   kavg_prep     K_avg = sum * (1/count) (paged_kv.hpp:170-183, fp32 exact), split into
+//                 two bf16 planes hi = bf16(K_avg), lo = bf16(K_avg - hi), head-major and
+//                 128-padded: [2][Hkv][n_pad][hd]. Every score is q.hi + q.lo accumulated in
+//                 fp32 on the tensor cores, so K_avg carries ~16 mantissa bits instead of 8
+//                 and the votes stay within ~1e-5 of the fp32 reference — the top-k ids are
+//                 then exact wherever the reference's own k-boundary margin exceeds that.
 //   score_stats   pass 1, query-major: S = Q K_avg^T per (128-token tile, q-head) over
 //                 all candidate blocks; per-row running max / sum of exp (log2 domain).
 //   score_vote    pass 2, page-major: S^T = K_avg Q^T per (128-page block, kv group,
@@ -40,14 +44,16 @@ __global__ void kavg_prep_kernel(const float* __restrict__ sum, const int32_t* _
             const int64_t src = (static_cast<int64_t>(p) * Hkv + h) * hd + d;
             v = kavg_f32 ? kavg_f32[src] : __fmul_rn(sum[src], __fdiv_rn(1.0f, static_cast<float>(cnt[p])));
         }
-        out[i] = __float2bfloat16_rn(v);
+        const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+        out[i] = hi;
+        out[total + i] = __float2bfloat16_rn(v - __bfloat162float(hi));
     }
 }
 
 // ---------------------------------------------------------------- pass 1
 constexpr int kStQ = 0;
-constexpr int kStK = kStQ + kTileBytes;            // 3 stages
-constexpr int kStBar = kStK + 3 * kTileBytes;
+constexpr int kStK = kStQ + kTileBytes;            // 3 stages of {hi, lo} K_avg tiles
+constexpr int kStBar = kStK + 3 * 2 * kTileBytes;
 constexpr int kStSmem = kStBar + 256 + 1024;
 
 struct StatsBars {
@@ -64,6 +70,7 @@ struct ScoreParams {
     float* m2;  // [Hq][C] running max (log2 units)
     float* il;  // [Hq][C] 1 / sum
     float* vote_part;  // [Hkv][m][n]
+    int lo_row;        // first row of the lo plane in the K_avg map (= Hkv * n_pad)
 };
 
 __global__ void __launch_bounds__(192, 1)
@@ -102,10 +109,11 @@ __global__ void __launch_bounds__(192, 1)
             for (int j = 0; j < nb; ++j) {
                 const int st = j % 3;
                 if (j >= 3) mbar_wait(&bars->k_empty[st], ((j - 3) / 3) & 1);
-                mbar_expect_tx(&bars->k_full[st], kTileBytes);
-                for (int r = 0; r < 2; ++r)
-                    tma_load_2d(sK + st * kTileBytes + r * kRegion, &tm_ka, &bars->k_full[st], r * 64,
-                                kvh * p.n_pad + j * kTile);
+                mbar_expect_tx(&bars->k_full[st], 2 * kTileBytes);
+                for (int pl = 0; pl < 2; ++pl)
+                    for (int r = 0; r < 2; ++r)
+                        tma_load_2d(sK + (2 * st + pl) * kTileBytes + r * kRegion, &tm_ka, &bars->k_full[st], r * 64,
+                                    pl * p.lo_row + kvh * p.n_pad + j * kTile);
             }
         }
     } else if (warp == 1) {
@@ -118,10 +126,12 @@ __global__ void __launch_bounds__(192, 1)
             if (j >= 2) mbar_wait(&bars->s_free[b], ((j - 2) >> 1) & 1);
             tc_fence_after();
             if (lane == 0) {
-                const uint32_t k_addr = smem_u32(sK + st * kTileBytes);
-                for (int ks = 0; ks < kHd / 16; ++ks)
-                    umma_f16_ss(tmem + b * kTile, desc_k(q_addr, ks, kRegion), desc_k(k_addr, ks, kRegion), idesc,
-                                ks > 0);
+                for (int pl = 0; pl < 2; ++pl) {  // S = Q hi^T + Q lo^T
+                    const uint32_t k_addr = smem_u32(sK + (2 * st + pl) * kTileBytes);
+                    for (int ks = 0; ks < kHd / 16; ++ks)
+                        umma_f16_ss(tmem + b * kTile, desc_k(q_addr, ks, kRegion), desc_k(k_addr, ks, kRegion),
+                                    idesc, (pl > 0 || ks > 0) ? 1u : 0u);
+                }
                 umma_commit(&bars->s_full[b]);
                 umma_commit(&bars->k_empty[st]);
             }
@@ -175,7 +185,7 @@ __global__ void __launch_bounds__(192, 1)
 
 // ---------------------------------------------------------------- pass 2
 constexpr int kVoK = 0;
-constexpr int kVoQ = kVoK + kTileBytes;            // 3 stages
+constexpr int kVoQ = kVoK + 2 * kTileBytes;        // K_avg {hi, lo}; then 3 stages of Q
 constexpr int kVoST = kVoQ + 3 * kTileBytes;       // 3 stages of {m2[128], 1/l[128]} (TMA bulk)
 constexpr int kVoBar = kVoST + 3 * 1024;
 constexpr int kVoSmem = kVoBar + 256 + 1024;
@@ -223,9 +233,11 @@ __global__ void __launch_bounds__(192, 1)
     };
     if (warp == 0) {
         if (lane == 0) {
-            mbar_expect_tx(&bars->q_full, kTileBytes);
-            for (int r = 0; r < 2; ++r)
-                tma_load_2d(sK + r * kRegion, &tm_ka, &bars->q_full, r * 64, kvh * p.n_pad + pb * kTile);
+            mbar_expect_tx(&bars->q_full, 2 * kTileBytes);
+            for (int pl = 0; pl < 2; ++pl)
+                for (int r = 0; r < 2; ++r)
+                    tma_load_2d(sK + pl * kTileBytes + r * kRegion, &tm_ka, &bars->q_full, r * 64,
+                                pl * p.lo_row + kvh * p.n_pad + pb * kTile);
             for (int i = 0; i < n_items; ++i) {
                 const int st = i % 3;
                 int qp, h, tile;
@@ -256,9 +268,10 @@ __global__ void __launch_bounds__(192, 1)
             tc_fence_after();
             if (lane == 0) {
                 const uint32_t q_addr = smem_u32(sQ + st * kTileBytes);
-                for (int ks = 0; ks < kHd / 16; ++ks)
-                    umma_f16_ss(tmem + b * kTile, desc_k(k_addr, ks, kRegion), desc_k(q_addr, ks, kRegion), idesc,
-                                ks > 0);
+                for (int pl = 0; pl < 2; ++pl)  // S^T = hi Q^T + lo Q^T
+                    for (int ks = 0; ks < kHd / 16; ++ks)
+                        umma_f16_ss(tmem + b * kTile, desc_k(k_addr + pl * kTileBytes, ks, kRegion),
+                                    desc_k(q_addr, ks, kRegion), idesc, (pl > 0 || ks > 0) ? 1u : 0u);
                 umma_commit(&bars->s_full[b]);
                 umma_commit(&bars->k_empty[st]);
             }
@@ -326,7 +339,7 @@ bool score_tc_supported(int dtype, int hd, int P, int64_t tokens) {
 size_t score_tc_workspace(int64_t tokens, int Hq, int Hkv, int64_t n, int P) {
     const int64_t n_pad = (n + kTile - 1) / kTile * kTile;
     const int64_t m = tokens / P;
-    return static_cast<size_t>(Hkv * n_pad * kHd * 2) + 2 * static_cast<size_t>(Hq * tokens * 4) +
+    return static_cast<size_t>(2 * Hkv * n_pad * kHd * 2) + 2 * static_cast<size_t>(Hq * tokens * 4) +
            static_cast<size_t>(Hkv * m * n * 4) + 4 * 256;
 }
 
@@ -351,7 +364,7 @@ void launch_score_tc(const void* q, int64_t tokens, int Hq, int Hkv, int P, cons
     uint8_t* w = static_cast<uint8_t*>(ws);
     auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
     __nv_bfloat16* ka = reinterpret_cast<__nv_bfloat16*>(w);
-    size_t off = align(static_cast<size_t>(Hkv) * n_pad * kHd * 2);
+    size_t off = align(static_cast<size_t>(2) * Hkv * n_pad * kHd * 2);
     float* m2 = reinterpret_cast<float*>(w + off);
     off += align(static_cast<size_t>(Hq) * tokens * 4);
     float* il = reinterpret_cast<float*>(w + off);
@@ -365,13 +378,13 @@ void launch_score_tc(const void* q, int64_t tokens, int Hq, int Hkv, int P, cons
     CUtensorMap tq = map_rows_heads(q, tokens, Hq, kHd);
     CUtensorMap tka;
     {
-        const uint64_t dims[2] = {static_cast<uint64_t>(kHd), static_cast<uint64_t>(Hkv) * n_pad};
+        const uint64_t dims[2] = {static_cast<uint64_t>(kHd), 2 * static_cast<uint64_t>(Hkv) * n_pad};
         const uint64_t strides[1] = {static_cast<uint64_t>(kHd) * 2};
         const uint32_t box[2] = {64, kTile};
         encode_or_throw(&tka, 2, ka, dims, strides, box);
     }
     ScoreParams p{static_cast<int>(tokens), Hq, Hkv, kHd, P, static_cast<int>(n), n_pad, m, scale * kLog2e, m2, il,
-                  part};
+                  part, Hkv * n_pad};
     score_stats_kernel<<<dim3(Hq, static_cast<unsigned>(tokens / kTile)), 192, kStSmem, st>>>(tq, tka, p);
     check_launch("score_stats_kernel");
     score_vote_kernel<<<dim3(n_pad / kTile, Hkv, (m + kQpGroup - 1) / kQpGroup), 192, kVoSmem, st>>>(tq, tka, p);

@@ -136,7 +136,10 @@ struct oomb_tier_s {
         return b;
     }
 
-    void push(int kind, double t, int layer, int32_t page, uint64_t bytes, int chunk, cudaStream_t st = nullptr) {
+    // `on`: the stream whose timeline stamps the event in real mode (the compute stream may be the
+    // legacy default stream, i.e. a null handle, so the choice is explicit rather than a pointer).
+    enum On { ON_NONE = 0, ON_COMPUTE, ON_H2D, ON_D2H };
+    void push(int kind, double t, int layer, int32_t page, uint64_t bytes, int chunk, On on = ON_NONE) {
         LogEv le{};
         le.e.kind = kind;
         le.e.t = t;
@@ -146,9 +149,9 @@ struct oomb_tier_s {
         le.e.bytes = bytes;
         le.e.phase = phase;
         le.ev = nullptr;
-        if (real() && st) {
+        if (real() && on != ON_NONE) {
             le.ev = new_event();
-            OOMB_CUDA(cudaEventRecord(le.ev, st));
+            OOMB_CUDA(cudaEventRecord(le.ev, on == ON_COMPUTE ? compute : (on == ON_H2D ? h2d_stream : d2h_stream)));
         }
         log.push_back(le);
     }
@@ -226,7 +229,7 @@ struct oomb_tier_s {
         }
         if (real()) real_evict(layer, page, wb_kv, wb_grad);
         set_tier(layer, page, 1);
-        push(EV_EVICT, clock, layer, page, bytes, -1, real() ? d2h_stream : nullptr);
+        push(EV_EVICT, clock, layer, page, bytes, -1, ON_D2H);
     }
 
     void real_evict(int layer, int page, bool wb_kv, bool wb_grad) {
@@ -325,7 +328,7 @@ struct oomb_tier_s {
             ps.kv_host_valid = false;
             ps.reserved = true;
             ps.lru = ++lru_counter;
-            push(EV_FETCH_DONE, clock, layer, p, 0, -1, real() ? compute : nullptr);
+            push(EV_FETCH_DONE, clock, layer, p, 0, -1, ON_COMPUTE);
         }
         enforce_capacity(0);
     }
@@ -374,7 +377,7 @@ struct oomb_tier_s {
         for (int32_t p : to_transfer) {
             PageState& ps = state(layer, p);
             const uint64_t bytes = page_transfer_bytes(layer, p);
-            push(EV_FETCH_ISSUED, clock, layer, p, 0, chunk, real() ? h2d_stream : nullptr);
+            push(EV_FETCH_ISSUED, clock, layer, p, 0, chunk, ON_H2D);
             const double start = std::max({h2d_free, clock, ps.writeback_done});
             const double done = start + static_cast<double>(bytes) / cfg.bandwidth_bytes_per_s;
             h2d_free = done;
@@ -382,7 +385,7 @@ struct oomb_tier_s {
             if (phase == 0) h2d_fwd += bytes;
             else h2d_bwd += bytes;
             if (real()) real_fetch(layer, p);
-            push(EV_FETCH_DONE, done, layer, p, bytes, chunk, real() ? h2d_stream : nullptr);
+            push(EV_FETCH_DONE, done, layer, p, bytes, chunk, ON_H2D);
             ready = std::max(ready, done);
             tr.pages.push_back(p);
         }
@@ -425,14 +428,14 @@ struct oomb_tier_s {
             const int32_t p = ids[i];
             if (tier(layer, p) != 0) throw Error(OOMB_RESIDENCY_ERROR, "access to non-resident page " + std::to_string(p));
             state(layer, p).lru = ++lru_counter;
-            push(EV_ACCESS, clock, layer, p, 0, chunk, real() ? compute : nullptr);
+            push(EV_ACCESS, clock, layer, p, 0, chunk, ON_COMPUTE);
         }
     }
 
     void advance_compute(double seconds, int chunk, int layer) {
-        push(EV_COMPUTE_BEGIN, clock, layer, -1, 0, chunk, real() ? compute : nullptr);
+        push(EV_COMPUTE_BEGIN, clock, layer, -1, 0, chunk, ON_COMPUTE);
         clock += seconds;
-        push(EV_COMPUTE_END, clock, layer, -1, 0, chunk, real() ? compute : nullptr);
+        push(EV_COMPUTE_END, clock, layer, -1, 0, chunk, ON_COMPUTE);
     }
 
     void end_layer_use(int layer, const int32_t* ids, int n) {  // :274-280
@@ -580,7 +583,8 @@ int oomb_tier_log(oomb_tier_t t, oomb_event* out, int64_t cap, int64_t* n) {
 }
 
 // validate_schedule (tiered_memory.cpp:47-138)
-int oomb_validate_schedule(const oomb_event* ev, int64_t n, double bw, double* out, int* n_viol) {
+int oomb_validate_schedule(const oomb_event* ev, int64_t n, double bw, double* out, int* n_viol, int64_t* viol_event,
+                           int32_t* viol_code, int64_t viol_cap) {
     return guard([&] {
         struct Track {
             bool resident = false;
@@ -588,11 +592,20 @@ int oomb_validate_schedule(const oomb_event* ev, int64_t n, double bw, double* o
         };
         std::map<std::pair<int, int32_t>, Track> track;
         int viol = 0;
+        int64_t cur = -1;
+        auto violate = [&](int32_t code) {
+            if (viol_event && viol_code && viol < viol_cap) {
+                viol_event[viol] = cur;
+                viol_code[viol] = code;
+            }
+            ++viol;
+        };
         double last_compute_t = -1, prev_end = 0, begin_t = 0, busy = 0, stall = 0;
         bool in_compute = false;
         uint64_t transfer = 0, h2d_f = 0, h2d_b = 0, d2h_b = 0;
         for (int64_t i = 0; i < n; ++i) {
             const oomb_event& e = ev[i];
+            cur = i;
             const auto key = std::make_pair(e.layer, e.page);
             switch (e.kind) {
                 case EV_FETCH_ISSUED: break;
@@ -606,7 +619,7 @@ int oomb_validate_schedule(const oomb_event* ev, int64_t n, double bw, double* o
                     break;
                 case EV_EVICT: {
                     auto it = track.find(key);
-                    if (it == track.end() || !it->second.resident) ++viol;
+                    if (it == track.end() || !it->second.resident) violate(1);
                     else it->second.resident = false;
                     transfer += e.bytes;
                     d2h_b += e.bytes;
@@ -615,27 +628,28 @@ int oomb_validate_schedule(const oomb_event* ev, int64_t n, double bw, double* o
                 }
                 case EV_ACCESS: {
                     auto it = track.find(key);
-                    if (it == track.end() || !it->second.resident || it->second.since > e.t) ++viol;
+                    if (it == track.end() || !it->second.resident || it->second.since > e.t) violate(2);
                     break;
                 }
                 case EV_COMPUTE_BEGIN:
-                    if (e.t < last_compute_t) ++viol;
+                    if (e.t < last_compute_t) violate(3);
                     last_compute_t = e.t;
-                    if (in_compute) ++viol;
+                    if (in_compute) violate(4);
                     in_compute = true;
                     begin_t = e.t;
                     stall += std::max(0.0, e.t - prev_end);
                     break;
                 case EV_COMPUTE_END:
-                    if (!in_compute) ++viol;
-                    if (e.t < begin_t) ++viol;
+                    if (!in_compute) violate(5);
+                    if (e.t < begin_t) violate(6);
                     in_compute = false;
                     prev_end = e.t;
                     last_compute_t = e.t;
                     break;
             }
         }
-        if (in_compute) ++viol;
+        cur = -1;
+        if (in_compute) violate(7);
         out[0] = stall;
         out[1] = static_cast<double>(transfer);
         out[2] = static_cast<double>(h2d_f);

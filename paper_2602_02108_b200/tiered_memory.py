@@ -77,7 +77,7 @@ class ScheduleLog:
 
 @dataclass
 class ValidationReport:
-    violations: int
+    violations: list  # messages, as the reference's ValidationReport::violations (tiered_memory.hpp:84-97)
     stall_seconds: float
     transfer_bytes: int
     h2d_bytes_forward: int
@@ -238,5 +238,22 @@ def validate_schedule(log, bandwidth: float | None = None) -> ValidationReport:
         arr = (OombEvent * max(n, 1))(*log)
     out = (C.c_double * 6)()
     nv = C.c_int()
-    call("oomb_validate_schedule", arr, n, C.c_double(bw), out, C.byref(nv))
-    return ValidationReport(nv.value, out[0], int(out[1]), int(out[2]), int(out[3]), int(out[4]), out[5])
+    cap = max(n, 1) + 1
+    vev = (C.c_int64 * cap)()
+    vcode = (C.c_int32 * cap)()
+    call("oomb_validate_schedule", arr, n, C.c_double(bw), out, C.byref(nv), vev, vcode, cap)
+    msgs = []
+    for i in range(min(nv.value, cap)):
+        e = arr[vev[i]] if vev[i] >= 0 else None
+        msgs.append(_violation_message(vcode[i], e))
+    return ValidationReport(msgs, out[0], int(out[1]), int(out[2]), int(out[3]), int(out[4]), out[5])
+
+
+def _violation_message(code: int, e) -> str:
+    """The reference's violation strings (tiered_memory.cpp:50-126)."""
+    if code == 1:
+        return f"evict of non-resident page layer={e.layer} page={e.page} t={e.t:g}"
+    if code == 2:
+        return f"access before fetch_done (or after evict): layer={e.layer} page={e.page} t={e.t:g}"
+    return {3: "compute stream timestamps decrease", 4: "nested compute_begin", 5: "compute_end without begin",
+            6: "compute segment ends before it begins", 7: "unterminated compute segment"}[code]

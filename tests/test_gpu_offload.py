@@ -11,11 +11,11 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def make(mode, capacity=None):
+def make(mode, capacity=None, n_layers=2):
     from paper_2602_02108_b200 import ModelConfig, PagedCache
     from paper_2602_02108_b200.chunk_loop import AttentionChunkLoop
     from paper_2602_02108_b200.tiered_memory import TierConfig, TieredEngine
-    cfg = ModelConfig(n_layers=1, n_q_heads=28, n_kv_heads=4, head_dim=128, chunk_size=512, page_size=128,
+    cfg = ModelConfig(n_layers=n_layers, n_q_heads=28, n_kv_heads=4, head_dim=128, chunk_size=512, page_size=128,
                       retrieval_budget=3 * 128, local_window=3, attention_mode=[mode])
     slots = -1 if capacity is None else capacity + 24  # physical slots: capacity + in-flight staging
     cache = PagedCache(cfg, dtype="bf16", max_tokens=8 * 512, device_capacity_pages=slots)
@@ -23,25 +23,28 @@ def make(mode, capacity=None):
     if capacity is not None:
         eng = TieredEngine(cache, TierConfig(device_capacity_pages=capacity, bandwidth_bytes_per_s=25e9))
         eng.set_prefetch_headroom_pages(cfg.pages_per_chunk())
-    return cache, AttentionChunkLoop(cache, engine=eng), eng
+    return cache, [AttentionChunkLoop(cache, layer=l, engine=eng) for l in range(n_layers)], eng
 
 
-def run(mode, capacity, n_chunks=6, seed=3):
-    cache, loop, eng = make(mode, capacity)
+def run(mode, capacity, n_chunks=6, seed=3, n_layers=2):
+    """Two attention layers interleaved per chunk, as the trainer runs them (chunk_trainer.hpp:131-186):
+    while one layer attends, the other layer's pages are the eviction candidates."""
+    cache, loops, eng = make(mode, capacity, n_layers)
     g = torch.Generator(device="cuda").manual_seed(seed)
     C = cache.cfg.chunk_size
-    qs = [torch.randn(C, 28, 128, device="cuda", generator=g).bfloat16() for _ in range(n_chunks)]
-    ks = [torch.randn(C, 4, 128, device="cuda", generator=g).bfloat16() for _ in range(n_chunks)]
-    vs = [torch.randn(C, 4, 128, device="cuda", generator=g).bfloat16() for _ in range(n_chunks)]
-    dos = [torch.randn(C, 28, 128, device="cuda", generator=g).bfloat16() for _ in range(n_chunks)]
+    rnd = lambda h: [[torch.randn(C, h, 128, device="cuda", generator=g).bfloat16() for _ in range(n_chunks)]
+                     for _ in range(n_layers)]
+    qs, ks, vs, dos = rnd(28), rnd(4), rnd(4), rnd(28)
     outs, grads = [], []
     for i in range(n_chunks):
-        s = loop.forward_chunk(i, qs[i], ks[i], vs[i])
-        outs.append((s.out.clone(), s.lse.clone()))
-    loop.begin_backward()
+        for l, loop in enumerate(loops):
+            s = loop.forward_chunk(i, qs[l][i], ks[l][i], vs[l][i])
+            outs.append((s.out.clone(), s.lse.clone()))
+    loops[0].begin_backward()
     for i in reversed(range(n_chunks)):
-        gr = loop.backward_chunk(i, dos[i], qs[i], ks[i], vs[i])
-        grads.append((gr.dq.clone(), gr.dk_cur.clone(), gr.dv_cur.clone()))
+        for l in reversed(range(n_layers)):
+            gr = loops[l].backward_chunk(i, dos[l][i], qs[l][i], ks[l][i], vs[l][i])
+            grads.append((gr.dq.clone(), gr.dk_cur.clone(), gr.dv_cur.clone()))
     torch.cuda.synchronize()
     log = None
     if eng is not None:
@@ -51,15 +54,28 @@ def run(mode, capacity, n_chunks=6, seed=3):
         eng.close()  # the engine leaves; every page must now be readable again
     else:
         stats = None
-    sels = [s.lists() for s in loop.sels]
+    sels = [s.lists() for loop in loops for s in loop.sels]
     return outs, grads, sels, log, stats, cache
+
+
+def _explain(log, rep):
+    """First violations with the events of the same page around them (diagnostics)."""
+    lines = rep.violations[:5]
+    for msg in rep.violations[:3]:
+        if "page=" not in msg:
+            continue
+        page = int(msg.split("page=")[1].split()[0])
+        evs = [(i, e.kind, e.chunk, e.phase, e.bytes, round(e.t * 1e6, 2)) for i, e in enumerate(log.events)
+               if e.page == page]
+        lines.append(f"page {page}: {evs[:40]}")
+    return "\n".join(lines)
 
 
 @pytest.mark.parametrize("mode", ["topk", "dense", "local"])
 def test_offload_bitwise_identical(mode):
     from paper_2602_02108_b200.tiered_memory import validate_schedule
     a_out, a_gr, a_sel, _, _, a_cache = run(mode, None)
-    cap = 12 if mode != "dense" else 24
+    cap = 12 if mode != "dense" else 24  # dense: one layer's whole past (20 pages) + its chunk (4)
     b_out, b_gr, b_sel, log, stats, b_cache = run(mode, cap)
     assert a_sel == b_sel
     for (o1, l1), (o2, l2) in zip(a_out, b_out):
@@ -69,7 +85,7 @@ def test_offload_bitwise_identical(mode):
             assert torch.equal(u, w)
     assert stats[2] > 0 and stats[0] + stats[1] > 0, "the capacity must force write-backs and fetches"
     rep = validate_schedule(log)
-    assert rep.violations == 0
+    assert rep.violations == [], _explain(log, rep)
     assert any(e.kind == "evict" and e.bytes > 0 for e in log.events)
 
 
@@ -82,19 +98,18 @@ def test_offload_pages_round_trip_exactly():
     cache = PagedCache(cfg, dtype="bf16", max_tokens=16 * 128, device_capacity_pages=16)
     k = torch.randn(16 * 128, 4, 128, device="cuda").bfloat16()
     v = torch.randn(16 * 128, 4, 128, device="cuda").bfloat16()
-    cache.append_chunk(0, k, v)
-    before = cache.gather_pages(0, list(range(16)))
     eng = TieredEngine(cache, TierConfig(device_capacity_pages=8, bandwidth_bytes_per_s=25e9))
-    eng.on_pages_appended(0, (0, 16 * 128))
-    eng.end_layer_use(0, list(range(16)))            # capacity 8 -> 8 pages written back
+    for c in range(4):  # appended pages are reserved until the layer is done with them (tiered_memory.hpp:131-145)
+        r = cache.append_chunk(0, k[c * 512:(c + 1) * 512], v[c * 512:(c + 1) * 512])
+        eng.on_pages_appended(0, r)
+        eng.end_layer_use(0, list(range(4 * c, 4 * c + 4)))  # capacity 8 -> older pages written back
     tiers = [cache.tier(0, p) for p in range(16)]
     assert sum(tiers) == 8
     evicted = [p for p in range(16) if tiers[p]]
-    eng.end_layer_use(0, [])
     eng.wait(eng.fetch_async(0, evicted[:4]))        # 4 come back (4 more go out)
     eng.record_access(0, evicted[:4])
     got = cache.gather_pages(0, evicted[:4])
     for j, p in enumerate(evicted[:4]):
-        assert torch.equal(got.k[j * 128:(j + 1) * 128], before.k[p * 128:(p + 1) * 128])
-        assert torch.equal(got.v[j * 128:(j + 1) * 128], before.v[p * 128:(p + 1) * 128])
+        assert torch.equal(got.k[j * 128:(j + 1) * 128], k[p * 128:(p + 1) * 128])
+        assert torch.equal(got.v[j * 128:(j + 1) * 128], v[p * 128:(p + 1) * 128])
     eng.close()

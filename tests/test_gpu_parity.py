@@ -208,6 +208,10 @@ def test_score_pages_known_answer():
     assert torch.allclose(u.cpu(), torch.full((2, 3), 4 * 2 / 3.0), atol=1e-5)
 
 
+# relative L2 of the tcgen05 scorer's votes vs the fp32 reference (hi/lo bf16 split of K_avg)
+TC_VOTE_TOL = 1e-4
+
+
 @pytest.mark.parametrize("geom,dtype", [("c1", "fp32"), ("qwen", "fp32"), ("c1", "bf16"), ("qwen", "bf16")])
 def test_scoring_and_selection_parity(geom, dtype):
     from paper_2602_02108_b200.attention import select_pages_topk
@@ -225,9 +229,9 @@ def test_scoring_and_selection_parity(geom, dtype):
     sel = select_pages_topk(cache, 0, torch.from_numpy(q).to("cuda", tdt), npages)
     got_vote = T(sel.vote)
     # fp32 mode (and shapes on the exact SIMT scorer) meet 1e-5; the bf16 tcgen05 scorer
-    # rounds K_avg to bf16 for the MMA, so its votes carry bf16 operand error.
+    # multiplies by K_avg split into hi + lo bf16 planes (~16 mantissa bits), fp32 accumulate.
     tc = dtype == "bf16" and geom == "qwen"
-    tol = 5e-3 if tc else FP32_TOL
+    tol = TC_VOTE_TOL if tc else FP32_TOL
     assert rel(got_vote, want_vote) < tol, rel(got_vote, want_vote)
     lists = sel.lists()
     checked = 0
@@ -260,13 +264,17 @@ def test_tc_scorer_matches_exact_scorer(n_pages, tokens):
     ex = select_pages_topk(cache, 0, q, n_pages)
     v_ex = ex.vote.clone()
     torch.cuda.synchronize()
-    assert rel(T(v_tc), T(v_ex)) < 5e-3
+    err = rel(T(v_tc), T(v_ex))
+    assert err < TC_VOTE_TOL, err
     a, b = tc.lists(), ex.lists()
     vv = T(v_ex)
+    checked = 0
     for i in range(len(a)):
         row = np.sort(vv[i])[::-1]
-        if (row[7] - row[8]) / row[7] > 5e-2:
+        if (row[7] - row[8]) / row[7] > 10 * TC_VOTE_TOL:
             assert a[i] == b[i]
+            checked += 1
+    assert checked >= len(a) // 2, (checked, len(a))
 
 
 # ---------------------------------------------------------------------------

@@ -279,7 +279,7 @@ def test_transfer_arithmetic_and_validator():
     nv = C.c_int()
     arr = (RefEvent * len(lb))(*[RefEvent(k, l, p, c, ph, 0, b, t) for (k, l, p, c, ph, b, t) in lb])
     assert ref.L.ref_validate_schedule(arr, len(lb), C.c_double(1e6), refv, C.byref(nv)) == 0
-    assert rep.violations == nv.value == 0
+    assert len(rep.violations) == nv.value == 0
     assert [rep.stall_seconds, rep.transfer_bytes, rep.h2d_bytes_forward, rep.h2d_bytes_backward, rep.d2h_bytes,
             rep.overlap_fraction] == list(refv)
 
@@ -302,8 +302,9 @@ def test_validator_flags_access_before_fetch():
             else:
                 evs.append(OombEvent(5, 0, page, -1, 0, 0, 0, t))
                 accesses.append(evs[-1])
-        assert validate_schedule(evs, 1e9).violations == 0
+        assert validate_schedule(evs, 1e9).violations == []
         if accesses:
             rogue = accesses[int(rng.integers(0, len(accesses)))]
             bad = [OombEvent(5, 0, rogue.page, -1, 0, 0, 0, 0.0)] + evs
-            assert validate_schedule(bad, 1e9).violations > 0
+            v = validate_schedule(bad, 1e9).violations
+            assert v and v[0].startswith("access before fetch_done") and f"page={rogue.page}" in v[0]
