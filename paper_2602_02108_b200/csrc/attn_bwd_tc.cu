@@ -30,7 +30,6 @@ namespace {
 constexpr int kQ64 = 64;                        // query rows per dK/dV work item
 constexpr int kRegion64 = kQ64 * 128;           // [64 x 64] bf16 region = 8 KB
 constexpr int kTile64 = 2 * kRegion64;          // [64 x 128] tile = 16 KB
-constexpr int kPT = kTile * kQ64 * 2;           // P^T / dS^T [128 keys x 64 q] = 16 KB (one region)
 
 // ---------------------------------------------------------------- workspace
 struct BwdWs {
@@ -157,7 +156,7 @@ __global__ void __launch_bounds__(256, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_kc, const __grid_constant__ CUtensorMap tm_vc,
                        const __grid_constant__ CUtensorMap tm_kp, const __grid_constant__ CUtensorMap tm_vp,
-                       BwdParams p) {
+                       const __grid_constant__ CUtensorMap tmap_dq, BwdParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     DqBars* bars = reinterpret_cast<DqBars*>(smem + kDqBar);
@@ -337,19 +336,19 @@ __global__ void __launch_bounds__(256, 1)
             fence_proxy_async_smem();
             mbar_arrive(&bars->ds_full);
         }
+        // dQ (scaled) leaves TMEM as four [128 x 32] fp32 slices staged in the idle K / V buffers,
+        // then one TMA tile store each into dq [C][Hq][hd].
         mbar_wait(&bars->dq_done, 0);
         tc_fence_after();
-        float* dqrow = p.dq + (static_cast<int64_t>(t) * g.Hq + h) * kHd;
+        uint8_t* stage = sK;
 #pragma unroll 1
-        for (int c = 0; c < kHd / 16; ++c) {
-            uint32_t v[16];
-            tmem_ld16(tm_dq + c * 16 + lane_off, v);
-            tmem_wait_ld();
-#pragma unroll
-            for (int u = 0; u < 16; u += 4)
-                *reinterpret_cast<float4*>(dqrow + c * 16 + u) =
-                    make_float4(__uint_as_float(v[u]) * g.scale, __uint_as_float(v[u + 1]) * g.scale,
-                                __uint_as_float(v[u + 2]) * g.scale, __uint_as_float(v[u + 3]) * g.scale);
+        for (int c = 0; c < kHd / 32; ++c) stage_slice(tm_dq + c * 32 + lane_off, stage + c * kSliceBytes, r, g.scale);
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (warp == 4 && lane == 0) {
+            for (int c = 0; c < kHd / 32; ++c) tma_store_3d(&tmap_dq, stage + c * kSliceBytes, c * 32, h, qt * kTile);
+            bulk_commit();
+            bulk_wait_read0();
         }
     }
     tc_fence_before();
@@ -359,23 +358,31 @@ __global__ void __launch_bounds__(256, 1)
 
 // ===========================================================================
 // dK/dV kernel (key-major, one CTA per (key block, kv head))
+//
+// Per work item (64 query rows of one q-head): S^T = K Q^T and dP^T = V dO^T land in
+// TMEM (double buffered); the softmax warps turn them into P^T and dS^T = P^T (dP^T - D)
+// and write them back as packed bf16 IN PLACE of S^T / dP^T, so dV += P^T dO and
+// dK += dS^T Q run as TS-MMAs (A operand from TMEM). The TMEM buffer of item i is
+// rewritten by S/dP of item i+2 only after dV/dK(i) were issued, and tcgen05.mma
+// operations of one thread execute in issue order. Shared memory then holds only K, V
+// and a 4-deep ring of Q / dO / {L, D} stages.
 // ===========================================================================
+constexpr int kKvStages = 4;
 constexpr int kKvK = 0;
 constexpr int kKvV = kKvK + kTileBytes;
-constexpr int kKvQ = kKvV + kTileBytes;          // 2 stages of [64 x 128]
-constexpr int kKvDO = kKvQ + 2 * kTile64;        // 2 stages
-constexpr int kKvP = kKvDO + 2 * kTile64;        // 2 buffers of P^T [128 x 64]
-constexpr int kKvDS = kKvP + 2 * kPT;            // 2 buffers of dS^T
-constexpr int kKvQps = kKvDS + 2 * kPT;          // query-page list (<= 64 ints)
-constexpr int kKvLD = kKvQps + 256;              // 2 stages of {L[64], D[64]} fp32 (TMA bulk)
-constexpr int kKvBar = kKvLD + 1024;
+constexpr int kKvQ = kKvV + kTileBytes;                  // kKvStages stages of [64 x 128]
+constexpr int kKvDO = kKvQ + kKvStages * kTile64;        // kKvStages stages
+constexpr int kKvQps = kKvDO + kKvStages * kTile64;      // query-page list (<= 64 ints)
+constexpr int kKvLD = kKvQps + 256;                      // kKvStages stages of {L[64], D[64]} fp32 (TMA bulk)
+constexpr int kKvBar = kKvLD + kKvStages * 512;
 constexpr int kKvSmem = kKvBar + 256 + 1024;
+static_assert(kKvStages * 2 * kTile64 >= 8 * kSliceBytes, "epilogue staging reuses the Q / dO ring");
 
 struct KvBars {
     uint64_t kv_full;
-    uint64_t qdo_full[2], qdo_empty[2];
-    uint64_t sdp_full[2], sdp_free[2];
-    uint64_t pds_full[2], pds_empty[2];
+    uint64_t qdo_full[kKvStages], qdo_empty[kKvStages];
+    uint64_t sdp_full[2];
+    uint64_t pds_full[2];
     uint64_t acc_done;
     uint32_t tmem_base;
 };
@@ -414,6 +421,8 @@ __global__ void __launch_bounds__(256, 1)
     attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_constant__ CUtensorMap tm_do64,
                          const __grid_constant__ CUtensorMap tm_kc, const __grid_constant__ CUtensorMap tm_vc,
                          const __grid_constant__ CUtensorMap tm_kp, const __grid_constant__ CUtensorMap tm_vp,
+                         const __grid_constant__ CUtensorMap tm_gk, const __grid_constant__ CUtensorMap tm_gv,
+                         const __grid_constant__ CUtensorMap tm_dkc, const __grid_constant__ CUtensorMap tm_dvc,
                          BwdParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -469,13 +478,13 @@ __global__ void __launch_bounds__(256, 1)
 
     if (threadIdx.x == 0) {
         mbar_init(&bars->kv_full, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kKvStages; ++i) {
             mbar_init(&bars->qdo_full[i], 1);
             mbar_init(&bars->qdo_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&bars->sdp_full[i], 1);
-            mbar_init(&bars->sdp_free[i], 128);
             mbar_init(&bars->pds_full[i], 128);
-            mbar_init(&bars->pds_empty[i], 1);
         }
         mbar_init(&bars->acc_done, 1);
         fence_barrier_init();
@@ -485,14 +494,13 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
-    // TMEM: S^T [0,64) [64,128), dP^T [128,192) [192,256), dK [256,384), dV [384,512)
+    // TMEM: S^T [0,64) [64,128), dP^T [128,192) [192,256) (P^T / dS^T overwrite their first
+    // 32 columns as packed bf16), dK [256,384), dV [384,512)
     const uint32_t tm_s = tmem, tm_dp = tmem + 128, tm_dk = tmem + 256, tm_dv = tmem + 384;
     uint8_t* sK = smem + kKvK;
     uint8_t* sV = smem + kKvV;
     uint8_t* sQ = smem + kKvQ;
     uint8_t* sDO = smem + kKvDO;
-    uint8_t* sP = smem + kKvP;
-    uint8_t* sDS = smem + kKvDS;
     const int n_items = u.n_items;
 
     if (warp == 0) {
@@ -511,11 +519,11 @@ __global__ void __launch_bounds__(256, 1)
                 }
             }
             for (int i = 0; i < n_items; ++i) {
-                const int st = i & 1;
+                const int st = i % kKvStages;
                 int h, qt64;
                 bool diag;
                 item_of(p, u, qps, i, g_kv, &h, &qt64, &diag);
-                if (i >= 2) mbar_wait(&bars->qdo_empty[st], ((i - 2) >> 1) & 1);
+                if (i >= kKvStages) mbar_wait(&bars->qdo_empty[st], ((i / kKvStages) - 1) & 1);
                 mbar_expect_tx(&bars->qdo_full[st], 2 * kTile64 + 512);
                 float* ld = reinterpret_cast<float*>(smem + kKvLD) + st * 128;
                 bulk_load(ld, p.Lt + static_cast<int64_t>(h) * g.C + qt64 * kQ64, 256, &bars->qdo_full[st]);
@@ -535,37 +543,34 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(&bars->kv_full, 0);
         for (int i = 0; i <= n_items; ++i) {
             if (i < n_items) {
-                const int st = i & 1;
-                mbar_wait(&bars->qdo_full[st], (i >> 1) & 1);
-                if (i >= 2) mbar_wait(&bars->sdp_free[st], ((i - 2) >> 1) & 1);
+                const int st = i % kKvStages, b = i & 1;
+                mbar_wait(&bars->qdo_full[st], (i / kKvStages) & 1);
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t q_addr = smem_u32(sQ + st * kTile64), do_addr = smem_u32(sDO + st * kTile64);
                     for (int ks = 0; ks < kHd / 16; ++ks)
-                        umma_f16_ss(tm_s + st * kQ64, desc_k(k_addr, ks, kRegion), desc_k(q_addr, ks, kRegion64),
+                        umma_f16_ss(tm_s + b * kQ64, desc_k(k_addr, ks, kRegion), desc_k(q_addr, ks, kRegion64),
                                     idesc_s, ks > 0);
                     for (int ks = 0; ks < kHd / 16; ++ks)
-                        umma_f16_ss(tm_dp + st * kQ64, desc_k(v_addr, ks, kRegion), desc_k(do_addr, ks, kRegion64),
+                        umma_f16_ss(tm_dp + b * kQ64, desc_k(v_addr, ks, kRegion), desc_k(do_addr, ks, kRegion64),
                                     idesc_s, ks > 0);
-                    umma_commit(&bars->sdp_full[st]);
+                    umma_commit(&bars->sdp_full[b]);
                 }
                 __syncwarp();
             }
             if (i >= 1) {
-                const int j = i - 1, st = j & 1;
-                mbar_wait(&bars->pds_full[st], (j >> 1) & 1);
+                const int j = i - 1, st = j % kKvStages, b = j & 1;
+                mbar_wait(&bars->pds_full[b], (j >> 1) & 1);
                 tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t p_addr = smem_u32(sP + st * kPT), ds_addr = smem_u32(sDS + st * kPT);
                     const uint32_t q_addr = smem_u32(sQ + st * kTile64), do_addr = smem_u32(sDO + st * kTile64);
                     for (int ks = 0; ks < kQ64 / 16; ++ks)
-                        umma_f16_ss(tm_dv, desc_k(p_addr, ks, kPT), desc_mn(do_addr, ks, kRegion64), idesc_g,
+                        umma_f16_ts(tm_dv, tm_s + b * kQ64 + ks * 8, desc_mn(do_addr, ks, kRegion64), idesc_g,
                                     (j > 0 || ks > 0) ? 1u : 0u);
                     for (int ks = 0; ks < kQ64 / 16; ++ks)
-                        umma_f16_ss(tm_dk, desc_k(ds_addr, ks, kPT), desc_mn(q_addr, ks, kRegion64), idesc_g,
+                        umma_f16_ts(tm_dk, tm_dp + b * kQ64 + ks * 8, desc_mn(q_addr, ks, kRegion64), idesc_g,
                                     (j > 0 || ks > 0) ? 1u : 0u);
                     umma_commit(&bars->qdo_empty[st]);
-                    umma_commit(&bars->pds_empty[st]);
                     if (i == n_items) umma_commit(&bars->acc_done);
                 }
                 __syncwarp();
@@ -579,7 +584,7 @@ __global__ void __launch_bounds__(256, 1)
         const bool key_ok = kr < n_valid;
         const int key_abs = u.key0 + kr;  // chunk-relative key index (in-chunk blocks)
         for (int i = 0; i < n_items; ++i) {
-            const int st = i & 1;
+            const int st = i % kKvStages, b = i & 1;
             int h, qt64;
             bool diag;
             item_of(p, u, qps, i, g_kv, &h, &qt64, &diag);
@@ -587,81 +592,78 @@ __global__ void __launch_bounds__(256, 1)
             // L, D of the item's 64 queries, staged into smem by the producer with Q / dO
             const float* Lrow = reinterpret_cast<const float*>(smem + kKvLD) + st * 128;
             const float* Drow = Lrow + 64;
-            mbar_wait(&bars->qdo_full[st], (i >> 1) & 1);  // makes the bulk-copied L / D visible
-            mbar_wait(&bars->sdp_full[st], (i >> 1) & 1);
+            mbar_wait(&bars->qdo_full[st], (i / kKvStages) & 1);  // makes the bulk-copied L / D visible
+            mbar_wait(&bars->sdp_full[b], (i >> 1) & 1);
             tc_fence_after();
             float s[kQ64], dp[kQ64];
 #pragma unroll
-            for (int c = 0; c < kQ64 / 16; ++c) {
-                tmem_ld16(tm_s + st * kQ64 + c * 16 + lane_off, *reinterpret_cast<uint32_t(*)[16]>(&s[c * 16]));
-                tmem_ld16(tm_dp + st * kQ64 + c * 16 + lane_off, *reinterpret_cast<uint32_t(*)[16]>(&dp[c * 16]));
+            for (int c = 0; c < kQ64 / 32; ++c) {
+                tmem_ld32(tm_s + b * kQ64 + c * 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
+                tmem_ld32(tm_dp + b * kQ64 + c * 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(&dp[c * 32]));
             }
             tmem_wait_ld();
-            tc_fence_before();
-            mbar_arrive(&bars->sdp_free[st]);
-            if (i >= 2) mbar_wait(&bars->pds_empty[st], ((i - 2) >> 1) & 1);
-            uint8_t* pb = sP + st * kPT;
-            uint8_t* db = sDS + st * kPT;
 #pragma unroll
-            for (int c8 = 0; c8 < kQ64 / 8; ++c8) {
-                const float4 l0 = *reinterpret_cast<const float4*>(Lrow + c8 * 8);
-                const float4 l1 = *reinterpret_cast<const float4*>(Lrow + c8 * 8 + 4);
-                const float4 d0 = *reinterpret_cast<const float4*>(Drow + c8 * 8);
-                const float4 d1 = *reinterpret_cast<const float4*>(Drow + c8 * 8 + 4);
-                const float lv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
-                const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-                float pe[8], de[8];
+            for (int c16 = 0; c16 < kQ64 / 32; ++c16) {  // 32 queries -> 16 packed columns of P^T and dS^T
+                uint32_t pp[16], dd[16];
 #pragma unroll
-                for (int u8 = 0; u8 < 8; ++u8) {
-                    const int c = c8 * 8 + u8;
-                    float e = ex2(s[c] * sl2 - lv[u8]);
-                    const bool vis = key_ok && (!diag || key_abs <= q0 + c);
-                    e = vis ? e : 0.f;
-                    pe[u8] = e;
-                    de[u8] = e * (dp[c] - dv[u8]);
+                for (int c4 = 0; c4 < 8; ++c4) {
+                    const int c0 = c16 * 32 + c4 * 4;
+                    const float4 l4 = *reinterpret_cast<const float4*>(Lrow + c0);
+                    const float4 d4 = *reinterpret_cast<const float4*>(Drow + c0);
+                    const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+                    const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+                    float pe[4], de[4];
+#pragma unroll
+                    for (int u4 = 0; u4 < 4; ++u4) {
+                        const int c = c0 + u4;
+                        float e = ex2(s[c] * sl2 - lv[u4]);
+                        const bool vis = key_ok && (!diag || key_abs <= q0 + c);
+                        e = vis ? e : 0.f;
+                        pe[u4] = e;
+                        de[u4] = e * (dp[c] - dv[u4]);
+                    }
+                    pp[c4 * 2] = pack_bf16(pe[0], pe[1]);
+                    pp[c4 * 2 + 1] = pack_bf16(pe[2], pe[3]);
+                    dd[c4 * 2] = pack_bf16(de[0], de[1]);
+                    dd[c4 * 2 + 1] = pack_bf16(de[2], de[3]);
                 }
-                st_sw128(pb, kPT, kr, c8, pack8(pe));
-                st_sw128(db, kPT, kr, c8, pack8(de));
+                tmem_st16(tm_s + b * kQ64 + c16 * 16 + lane_off, pp);
+                tmem_st16(tm_dp + b * kQ64 + c16 * 16 + lane_off, dd);
             }
-            fence_proxy_async_smem();
-            mbar_arrive(&bars->pds_full[st]);
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&bars->pds_full[b]);
         }
-        // ---- epilogue: one RMW of the fp32 gradient page / store of dk_cur, dv_cur
+        // ---- epilogue: dK (scaled) and dV leave TMEM as eight [128 x 32] fp32 slices staged in
+        // the now idle Q / dO ring (128 KB); the TMA unit then adds them into the fp32 gradient
+        // page in L2 (past pages: one owner per (page, kv head, block) in this launch, so the
+        // result is deterministic) or stores them to dk_cur / dv_cur (the chunk's own keys).
+        // Rows beyond the page's fill level carry zeros (the reference leaves those slots at 0).
         mbar_wait(&bars->acc_done, 0);
         tc_fence_after();
-        float *dkrow, *dvrow;
-        if (u.past) {
-            const int64_t base = ((static_cast<int64_t>(g_slot) * g.Hkv + g_kv) * g.P + u.key0 + kr) * kHd;
-            dkrow = p.gk + base;
-            dvrow = p.gv + base;
-        } else {
-            const int64_t base = (static_cast<int64_t>(key_abs) * g.Hkv + g_kv) * kHd;
-            dkrow = p.dk_cur + base;
-            dvrow = p.dv_cur + base;
-        }
+        uint8_t* stage = smem + kKvQ;
 #pragma unroll 1
-        for (int c = 0; c < kHd / 16; ++c) {
-            uint32_t vk[16], vv[16];
-            tmem_ld16(tm_dk + c * 16 + lane_off, vk);
-            tmem_ld16(tm_dv + c * 16 + lane_off, vv);
-            tmem_wait_ld();
-            if (!key_ok) continue;
-#pragma unroll
-            for (int u4 = 0; u4 < 16; u4 += 4) {
-                float4 k4 = make_float4(__uint_as_float(vk[u4]) * g.scale, __uint_as_float(vk[u4 + 1]) * g.scale,
-                                        __uint_as_float(vk[u4 + 2]) * g.scale, __uint_as_float(vk[u4 + 3]) * g.scale);
-                float4 v4 = make_float4(__uint_as_float(vv[u4]), __uint_as_float(vv[u4 + 1]),
-                                        __uint_as_float(vv[u4 + 2]), __uint_as_float(vv[u4 + 3]));
-                float4* pk = reinterpret_cast<float4*>(dkrow + c * 16 + u4);
-                float4* pv = reinterpret_cast<float4*>(dvrow + c * 16 + u4);
-                if (u.past) {
-                    const float4 ok = *pk, ov = *pv;
-                    k4 = make_float4(ok.x + k4.x, ok.y + k4.y, ok.z + k4.z, ok.w + k4.w);
-                    v4 = make_float4(ov.x + v4.x, ov.y + v4.y, ov.z + v4.z, ov.w + v4.w);
+        for (int c = 0; c < kHd / 32; ++c) {
+            stage_slice(tm_dk + c * 32 + lane_off, stage + c * kSliceBytes, kr, key_ok ? g.scale : 0.f);
+            stage_slice(tm_dv + c * 32 + lane_off, stage + (4 + c) * kSliceBytes, kr, key_ok ? 1.f : 0.f);
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (warp == 4 && lane == 0) {
+            if (u.past) {
+                const int row = (g_slot * g.Hkv + g_kv) * g.P + u.key0;
+                for (int c = 0; c < kHd / 32; ++c) {
+                    tma_reduce_add_2d(&tm_gk, stage + c * kSliceBytes, c * 32, row);
+                    tma_reduce_add_2d(&tm_gv, stage + (4 + c) * kSliceBytes, c * 32, row);
                 }
-                *pk = k4;
-                *pv = v4;
+            } else {
+                for (int c = 0; c < kHd / 32; ++c) {
+                    tma_store_3d(&tm_dkc, stage + c * kSliceBytes, c * 32, g_kv, u.key0);
+                    tma_store_3d(&tm_dvc, stage + (4 + c) * kSliceBytes, c * 32, g_kv, u.key0);
+                }
             }
+            bulk_commit();
+            bulk_wait_read0();
         }
     }
     tc_fence_before();
@@ -717,16 +719,19 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     delete prep_scope;
     {
         ProfScope s_(PK_BWD_DQ, st);
+        const CUtensorMap tdq = map_rows_heads_f32(dq, g.C, g.Hq, kHd);
         attn_bwd_dq_kernel<<<dim3(g.Hq, g.C / kTile), 256, kDqSmem, st>>>(tq, tdo, tkc, tvc, maps.kpool, maps.vpool,
-                                                                          p);
+                                                                          tdq, p);
         check_launch("attn_bwd_dq_kernel");
     }
     {
         ProfScope s_(PK_BWD_DKDV, st);
         const int max_union = std::min(nnz, n_pages);
         const int units = g.C / kTile + max_union * (g.P / kTile);
-        attn_bwd_dkdv_kernel<<<dim3(units, g.Hkv), 256, kKvSmem, st>>>(tq64, tdo64, tkc, tvc, maps.kpool,
-                                                                       maps.vpool, p);
+        const CUtensorMap tdkc = map_rows_heads_f32(dk_cur, g.C, g.Hkv, kHd);
+        const CUtensorMap tdvc = map_rows_heads_f32(dv_cur, g.C, g.Hkv, kHd);
+        attn_bwd_dkdv_kernel<<<dim3(units, g.Hkv), 256, kKvSmem, st>>>(
+            tq64, tdo64, tkc, tvc, maps.kpool, maps.vpool, maps.gkpool, maps.gvpool, tdkc, tdvc, p);
         check_launch("attn_bwd_dkdv_kernel");
     }
 }

@@ -88,13 +88,23 @@ static void encode_or_throw(CUtensorMap* m, uint32_t rank, const void* base, con
     if (r != CUDA_SUCCESS) throw Error(OOMB_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
-void make_pool_maps(TcPoolMaps& maps, const void* kpool, const void* vpool, int64_t n_slots, int Hkv, int P,
-                    int hd) {
+void make_pool_maps(TcPoolMaps& maps, const void* kpool, const void* vpool, int64_t n_slots, const float* gkpool,
+                    const float* gvpool, int64_t n_g_slots, int Hkv, int P, int hd) {
     const uint64_t dims[2] = {static_cast<uint64_t>(hd), static_cast<uint64_t>(n_slots) * Hkv * P};
     const uint64_t strides[1] = {static_cast<uint64_t>(hd) * 2};
     const uint32_t box[2] = {64, kTile};
     encode_or_throw(&maps.kpool, 2, kpool, dims, strides, box);
     encode_or_throw(&maps.vpool, 2, vpool, dims, strides, box);
+    // fp32 gradient pools: 32-column boxes (128 B rows) for the dK/dV TMA reduce-add epilogue
+    const uint64_t gdims[2] = {static_cast<uint64_t>(hd), static_cast<uint64_t>(n_g_slots) * Hkv * P};
+    const uint64_t gstrides[1] = {static_cast<uint64_t>(hd) * 4};
+    const uint32_t gbox[2] = {32, kTile};
+    CUresult r = encode_tensor_map(&maps.gkpool, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(gkpool), gdims,
+                                   gstrides, gbox, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (r == CUDA_SUCCESS)
+        r = encode_tensor_map(&maps.gvpool, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(gvpool), gdims,
+                              gstrides, gbox, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (r != CUDA_SUCCESS) throw Error(OOMB_CUDA_ERROR, "cuTensorMapEncodeTiled (grad pool) failed: " + std::to_string(r));
     maps.valid = true;
 }
 

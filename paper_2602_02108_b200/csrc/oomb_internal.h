@@ -151,12 +151,14 @@ void launch_attn_bwd_simt(int dtype, const AttnGeom& g, const void* dout, const 
 struct TcPoolMaps {
     CUtensorMap kpool;  // [n_slots*Hkv*P rows][hd] bf16, box 128 x 64, SW128
     CUtensorMap vpool;
+    CUtensorMap gkpool;  // [n_g_slots*Hkv*P rows][hd] fp32, box 128 x 32, SW128 (TMA reduce-add target)
+    CUtensorMap gvpool;
     bool valid = false;
 };
 bool tc_supported(const AttnGeom& g, int dtype);
 bool tc_bwd_available();
-void make_pool_maps(TcPoolMaps& maps, const void* kpool, const void* vpool, int64_t n_slots, int Hkv, int P,
-                    int hd);
+void make_pool_maps(TcPoolMaps& maps, const void* kpool, const void* vpool, int64_t n_slots, const float* gkpool,
+                    const float* gvpool, int64_t n_g_slots, int Hkv, int P, int hd);
 void launch_attn_fwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* q, const int32_t* sel_off,
                         const int32_t* sel_ids, const int32_t* d_kvslot_layer, const void* k_cur, const void* v_cur,
                         void* out, float* lse, int* d_err, cudaStream_t st);

@@ -44,10 +44,40 @@ __device__ __forceinline__ uint4 pack8(const float* e) {
 }
 
 inline void encode_or_throw(CUtensorMap* m, uint32_t rank, const void* base, const uint64_t* dims,
-                            const uint64_t* strides, const uint32_t* box) {
-    CUresult r = encode_tensor_map(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides,
-                                   box, CU_TENSOR_MAP_SWIZZLE_128B);
+                            const uint64_t* strides, const uint32_t* box,
+                            CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
+    CUresult r = encode_tensor_map(m, dt, rank, const_cast<void*>(base), dims, strides, box,
+                                   CU_TENSOR_MAP_SWIZZLE_128B);
     if (r != CUDA_SUCCESS) throw Error(OOMB_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+
+// fp32 [rows][heads][hd] tensor viewed as 3-D {hd, heads, rows}; box {32, 1, 128}: the
+// 128-B swizzled staging box of the TMA-store epilogues (one 32-column slice of a tile).
+inline CUtensorMap map_rows_heads_f32(const void* base, int64_t rows, int heads, int hd) {
+    CUtensorMap m;
+    const uint64_t dims[3] = {static_cast<uint64_t>(hd), static_cast<uint64_t>(heads), static_cast<uint64_t>(rows)};
+    const uint64_t strides[2] = {static_cast<uint64_t>(hd) * 4, static_cast<uint64_t>(heads) * hd * 4};
+    const uint32_t box[3] = {32, 1, static_cast<uint32_t>(kTile)};
+    encode_or_throw(&m, 3, base, dims, strides, box, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+    return m;
+}
+
+// Epilogue staging of fp32 accumulator slices: slice s ([128 rows x 32 fp32] = 16 KB) in the
+// TMA SWIZZLE_128B layout, 16-byte unit u (0..7) of row r at r*128 + ((u ^ (r & 7)) << 4).
+constexpr int kSliceBytes = kTile * 128;
+__device__ __forceinline__ void st_slice_f32(uint8_t* slice, int r, int u, float4 v) {
+    *reinterpret_cast<float4*>(slice + r * 128 + ((u ^ (r & 7)) << 4)) = v;
+}
+// Load 32 accumulator columns of this thread's TMEM lane, scale, and stage them as one slice.
+__device__ __forceinline__ void stage_slice(uint32_t taddr, uint8_t* slice, int r, float scale) {
+    uint32_t v[32];
+    tmem_ld32(taddr, v);
+    tmem_wait_ld();
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+        st_slice_f32(slice, r, u,
+                     make_float4(__uint_as_float(v[4 * u]) * scale, __uint_as_float(v[4 * u + 1]) * scale,
+                                 __uint_as_float(v[4 * u + 2]) * scale, __uint_as_float(v[4 * u + 3]) * scale));
 }
 
 // [rows][heads][hd] bf16 tensor viewed as 3-D {hd, heads, rows}; box {64, 1, box_rows}.
