@@ -150,6 +150,7 @@ struct BwdParams {
     float* dk_cur;
     float* dv_cur;
     int* err;
+    CtaTrace tr;  // debug CTA timeline (OOMB_CTA_TRACE)
 };
 
 __global__ void __launch_bounds__(256, 1)
@@ -399,25 +400,48 @@ struct KvUnit {
     int tiles_per_qp;
 };
 
-__device__ __forceinline__ void item_of(const BwdParams& p, const KvUnit& u, const int* qps, int i, int g_kv, int* h,
-                                        int* qt64, bool* diag) {
-    const int G = p.g.group;
-    if (!u.past) {
-        const int b = u.key0 / kTile;
-        *qt64 = 2 * b + i / G;
-        *h = g_kv * G + i % G;
-        *diag = *qt64 < 2 * b + 2;
-    } else {
-        const int per_qp = u.tiles_per_qp * G;
-        const int qp = qps[i / per_qp];
-        const int rem = i % per_qp;
-        *qt64 = qp * u.tiles_per_qp + rem / G;
-        *h = g_kv * G + rem % G;
-        *diag = false;
-    }
-}
+// TMEM column of K step ks (16 queries = 8 packed columns) of P^T / dS^T inside an item's
+// 64-column S^T / dP^T buffer: each softmax half packs its 32 queries at the start of its own
+// 32 columns.
+__host__ __device__ constexpr uint32_t pt_col(int ks) { return (ks >> 1) * 32 + (ks & 1) * 8; }
 
-__global__ void __launch_bounds__(256, 1)
+// Items of a unit in order: past units walk (query page of the list, 64-row tile, q-head of
+// the group) head-fastest; in-chunk units walk (64-row tile from the key block's diagonal on,
+// q-head). Advanced incrementally (no integer division on the per-item path).
+struct ItemIter {
+    int h, qt64, qpi, tile;  // q-head, 64-row query tile, index in the query-page list, tile in the page
+    bool diag;
+    __device__ __forceinline__ void init(const KvUnit& u, const int* qps, int g_kv, int G) {
+        h = g_kv * G;
+        qpi = 0;
+        tile = 0;
+        if (u.past) {
+            qt64 = qps[0] * u.tiles_per_qp;
+            diag = false;
+        } else {
+            qt64 = 2 * (u.key0 / kTile);
+            diag = true;
+        }
+    }
+    __device__ __forceinline__ void next(const KvUnit& u, const int* qps, int g_kv, int G) {
+        if (++h < (g_kv + 1) * G) return;
+        h = g_kv * G;
+        if (!u.past) {
+            ++qt64;
+            diag = qt64 < 2 * (u.key0 / kTile) + 2;
+            return;
+        }
+        if (++tile == u.tiles_per_qp) {
+            tile = 0;
+            ++qpi;
+            if (qpi < u.n_qps) qt64 = qps[qpi] * u.tiles_per_qp;
+        } else {
+            ++qt64;
+        }
+    }
+};
+
+__global__ void __launch_bounds__(384, 1)
     attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_constant__ CUtensorMap tm_do64,
                          const __grid_constant__ CUtensorMap tm_kc, const __grid_constant__ CUtensorMap tm_vc,
                          const __grid_constant__ CUtensorMap tm_kp, const __grid_constant__ CUtensorMap tm_vp,
@@ -463,6 +487,11 @@ __global__ void __launch_bounds__(256, 1)
         }
     }
     if (!u.valid) return;
+    if (threadIdx.x == 0) {
+        trace_value(p.tr, 0, smid());
+        trace_mark(p.tr, 1);
+        trace_value(p.tr, 7, u.n_items);
+    }
 
     int kv_slot = 0, g_slot = -1, n_valid = kTile;
     if (u.past) {
@@ -484,7 +513,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bars->sdp_full[i], 1);
-            mbar_init(&bars->pds_full[i], 128);
+            mbar_init(&bars->pds_full[i], 256);
         }
         mbar_init(&bars->acc_done, 1);
         fence_barrier_init();
@@ -518,11 +547,11 @@ __global__ void __launch_bounds__(256, 1)
                     tma_load_3d(sV + r * kRegion, &tm_vc, &bars->kv_full, r * 64, g_kv, u.key0);
                 }
             }
-            for (int i = 0; i < n_items; ++i) {
+            ItemIter it;
+            it.init(u, qps, g_kv, g.group);
+            for (int i = 0; i < n_items; ++i, it.next(u, qps, g_kv, g.group)) {
                 const int st = i % kKvStages;
-                int h, qt64;
-                bool diag;
-                item_of(p, u, qps, i, g_kv, &h, &qt64, &diag);
+                const int h = it.h, qt64 = it.qt64;
                 if (i >= kKvStages) mbar_wait(&bars->qdo_empty[st], ((i / kKvStages) - 1) & 1);
                 mbar_expect_tx(&bars->qdo_full[st], 2 * kTile64 + 512);
                 float* ld = reinterpret_cast<float*>(smem + kKvLD) + st * 128;
@@ -537,99 +566,97 @@ __global__ void __launch_bounds__(256, 1)
             }
         }
     } else if (warp == 1) {
+        // MMA warp, converged: descriptors advance by constant offsets from uniform bases.
         constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kQ64, 0, 0);   // [128 keys] x [64 q], K = hd
         constexpr uint32_t idesc_g = make_idesc_bf16(kTile, kHd, 0, 1);    // [128 keys] x [hd], K = 64 q
-        const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+        const uint64_t dK = sdesc_k(smem_u32(sK)), dV = sdesc_k(smem_u32(sV));
+        const uint64_t dQ = sdesc_k(smem_u32(sQ)), dDO = sdesc_k(smem_u32(sDO));
+        const uint64_t dQmn = sdesc_mn(smem_u32(sQ), kRegion64), dDOmn = sdesc_mn(smem_u32(sDO), kRegion64);
         mbar_wait(&bars->kv_full, 0);
+        if (lane == 0) trace_mark(p.tr, 2);
+        __syncwarp();
         for (int i = 0; i <= n_items; ++i) {
             if (i < n_items) {
                 const int st = i % kKvStages, b = i & 1;
+                const uint64_t so = boff(st * kTile64);
                 mbar_wait(&bars->qdo_full[st], (i / kKvStages) & 1);
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t q_addr = smem_u32(sQ + st * kTile64), do_addr = smem_u32(sDO + st * kTile64);
-                    for (int ks = 0; ks < kHd / 16; ++ks)
-                        umma_f16_ss(tm_s + b * kQ64, desc_k(k_addr, ks, kRegion), desc_k(q_addr, ks, kRegion64),
-                                    idesc_s, ks > 0);
-                    for (int ks = 0; ks < kHd / 16; ++ks)
-                        umma_f16_ss(tm_dp + b * kQ64, desc_k(v_addr, ks, kRegion), desc_k(do_addr, ks, kRegion64),
-                                    idesc_s, ks > 0);
-                    umma_commit(&bars->sdp_full[b]);
-                }
-                __syncwarp();
+#pragma unroll
+                for (int ks = 0; ks < kHd / 16; ++ks)
+                    umma_ss_w(tm_s + b * kQ64, dK + koff(ks, kRegion), dQ + so + koff(ks, kRegion64), idesc_s, ks);
+#pragma unroll
+                for (int ks = 0; ks < kHd / 16; ++ks)
+                    umma_ss_w(tm_dp + b * kQ64, dV + koff(ks, kRegion), dDO + so + koff(ks, kRegion64), idesc_s, ks);
+                umma_commit_w(&bars->sdp_full[b]);
             }
             if (i >= 1) {
                 const int j = i - 1, st = j % kKvStages, b = j & 1;
+                const uint64_t so = boff(st * kTile64);
                 mbar_wait(&bars->pds_full[b], (j >> 1) & 1);
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t q_addr = smem_u32(sQ + st * kTile64), do_addr = smem_u32(sDO + st * kTile64);
-                    for (int ks = 0; ks < kQ64 / 16; ++ks)
-                        umma_f16_ts(tm_dv, tm_s + b * kQ64 + ks * 8, desc_mn(do_addr, ks, kRegion64), idesc_g,
-                                    (j > 0 || ks > 0) ? 1u : 0u);
-                    for (int ks = 0; ks < kQ64 / 16; ++ks)
-                        umma_f16_ts(tm_dk, tm_dp + b * kQ64 + ks * 8, desc_mn(q_addr, ks, kRegion64), idesc_g,
-                                    (j > 0 || ks > 0) ? 1u : 0u);
-                    umma_commit(&bars->qdo_empty[st]);
-                    if (i == n_items) umma_commit(&bars->acc_done);
-                }
-                __syncwarp();
+#pragma unroll
+                for (int ks = 0; ks < kQ64 / 16; ++ks)
+                    umma_ts_w(tm_dv, tm_s + b * kQ64 + pt_col(ks), dDOmn + so + mnoff(ks), idesc_g, j | ks);
+#pragma unroll
+                for (int ks = 0; ks < kQ64 / 16; ++ks)
+                    umma_ts_w(tm_dk, tm_dp + b * kQ64 + pt_col(ks), dQmn + so + mnoff(ks), idesc_g, j | ks);
+                umma_commit_w(&bars->qdo_empty[st]);
+                if (i == n_items) umma_commit_w(&bars->acc_done);
             }
         }
     } else if (warp >= 4) {
-        const int quarter = warp & 3;
+        // Two warpgroups: warps 4..7 take query columns [0, 32) of each item, warps 8..11
+        // columns [32, 64); warp w reads TMEM lanes 32*(w%4).. (its key rows).
+        const int quarter = warp & 3, half = (warp - 4) >> 2;
         const int kr = quarter * 32 + lane;  // key row of the block
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         const float sl2 = g.scale * kLog2e;
         const bool key_ok = kr < n_valid;
+        const bool page_full = n_valid == kTile;
         const int key_abs = u.key0 + kr;  // chunk-relative key index (in-chunk blocks)
-        for (int i = 0; i < n_items; ++i) {
+        const uint32_t ld_base = smem_u32(smem + kKvLD) + half * 128;
+        ItemIter it;
+        it.init(u, qps, g_kv, g.group);
+        for (int i = 0; i < n_items; ++i, it.next(u, qps, g_kv, g.group)) {
             const int st = i % kKvStages, b = i & 1;
-            int h, qt64;
-            bool diag;
-            item_of(p, u, qps, i, g_kv, &h, &qt64, &diag);
-            const int q0 = qt64 * kQ64;
-            // L, D of the item's 64 queries, staged into smem by the producer with Q / dO
-            const float* Lrow = reinterpret_cast<const float*>(smem + kKvLD) + st * 128;
-            const float* Drow = Lrow + 64;
+            const int q0 = it.qt64 * kQ64 + half * 32;
+            const uint32_t lrow = ld_base + st * 512, drow = lrow + 256;
             mbar_wait(&bars->qdo_full[st], (i / kKvStages) & 1);  // makes the bulk-copied L / D visible
             mbar_wait(&bars->sdp_full[b], (i >> 1) & 1);
+            if (i == 0 && threadIdx.x == 128) trace_mark(p.tr, 3);
             tc_fence_after();
-            float s[kQ64], dp[kQ64];
-#pragma unroll
-            for (int c = 0; c < kQ64 / 32; ++c) {
-                tmem_ld32(tm_s + b * kQ64 + c * 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
-                tmem_ld32(tm_dp + b * kQ64 + c * 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(&dp[c * 32]));
-            }
+            uint32_t s[32], dp[32];
+            tmem_ld32(tm_s + b * kQ64 + half * 32 + lane_off, s);
+            tmem_ld32(tm_dp + b * kQ64 + half * 32 + lane_off, dp);
             tmem_wait_ld();
+            const bool masked = it.diag || !page_full;
+            uint32_t pp[16], dd[16];
 #pragma unroll
-            for (int c16 = 0; c16 < kQ64 / 32; ++c16) {  // 32 queries -> 16 packed columns of P^T and dS^T
-                uint32_t pp[16], dd[16];
-#pragma unroll
-                for (int c4 = 0; c4 < 8; ++c4) {
-                    const int c0 = c16 * 32 + c4 * 4;
-                    const float4 l4 = *reinterpret_cast<const float4*>(Lrow + c0);
-                    const float4 d4 = *reinterpret_cast<const float4*>(Drow + c0);
-                    const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-                    const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
-                    float pe[4], de[4];
-#pragma unroll
-                    for (int u4 = 0; u4 < 4; ++u4) {
-                        const int c = c0 + u4;
-                        float e = ex2(s[c] * sl2 - lv[u4]);
-                        const bool vis = key_ok && (!diag || key_abs <= q0 + c);
-                        e = vis ? e : 0.f;
-                        pe[u4] = e;
-                        de[u4] = e * (dp[c] - dv[u4]);
-                    }
-                    pp[c4 * 2] = pack_bf16(pe[0], pe[1]);
-                    pp[c4 * 2 + 1] = pack_bf16(pe[2], pe[3]);
-                    dd[c4 * 2] = pack_bf16(de[0], de[1]);
-                    dd[c4 * 2 + 1] = pack_bf16(de[2], de[3]);
+            for (int c4 = 0; c4 < 8; ++c4) {
+                const float4 l4 = lds128(lrow + c4 * 16);
+                const float4 d4 = lds128(drow + c4 * 16);
+                float e0 = ex2(fmaf(__uint_as_float(s[4 * c4 + 0]), sl2, -l4.x));
+                float e1 = ex2(fmaf(__uint_as_float(s[4 * c4 + 1]), sl2, -l4.y));
+                float e2 = ex2(fmaf(__uint_as_float(s[4 * c4 + 2]), sl2, -l4.z));
+                float e3 = ex2(fmaf(__uint_as_float(s[4 * c4 + 3]), sl2, -l4.w));
+                if (masked) {
+                    const int qc = q0 + 4 * c4;
+                    e0 = (key_ok && (!it.diag || key_abs <= qc + 0)) ? e0 : 0.f;
+                    e1 = (key_ok && (!it.diag || key_abs <= qc + 1)) ? e1 : 0.f;
+                    e2 = (key_ok && (!it.diag || key_abs <= qc + 2)) ? e2 : 0.f;
+                    e3 = (key_ok && (!it.diag || key_abs <= qc + 3)) ? e3 : 0.f;
                 }
-                tmem_st16(tm_s + b * kQ64 + c16 * 16 + lane_off, pp);
-                tmem_st16(tm_dp + b * kQ64 + c16 * 16 + lane_off, dd);
+                pp[2 * c4] = pack_bf16(e0, e1);
+                pp[2 * c4 + 1] = pack_bf16(e2, e3);
+                dd[2 * c4] = pack_bf16(e0 * (__uint_as_float(dp[4 * c4 + 0]) - d4.x),
+                                       e1 * (__uint_as_float(dp[4 * c4 + 1]) - d4.y));
+                dd[2 * c4 + 1] = pack_bf16(e2 * (__uint_as_float(dp[4 * c4 + 2]) - d4.z),
+                                           e3 * (__uint_as_float(dp[4 * c4 + 3]) - d4.w));
             }
+            // packed into the first 16 of this half's own 32 S / dP columns (the other half may
+            // still be reading its S columns): K steps 0,1 at cols 0..15, K steps 2,3 at 32..47
+            tmem_st16(tm_s + b * kQ64 + half * 32 + lane_off, pp);
+            tmem_st16(tm_dp + b * kQ64 + half * 32 + lane_off, dd);
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive(&bars->pds_full[b]);
@@ -639,17 +666,25 @@ __global__ void __launch_bounds__(256, 1)
         // page in L2 (past pages: one owner per (page, kv head, block) in this launch, so the
         // result is deterministic) or stores them to dk_cur / dv_cur (the chunk's own keys).
         // Rows beyond the page's fill level carry zeros (the reference leaves those slots at 0).
+        if (threadIdx.x == 128) trace_mark(p.tr, 4);
         mbar_wait(&bars->acc_done, 0);
+        if (threadIdx.x == 128) trace_mark(p.tr, 5);
         tc_fence_after();
-        uint8_t* stage = smem + kKvQ;
+        // ---- epilogue: dK (scaled; warpgroup 0) and dV (warpgroup 1) leave TMEM as [128 x 32]
+        // fp32 slices staged in the now idle Q / dO ring (128 KB); the TMA unit then adds them
+        // into the fp32 gradient page in L2 (past pages: one owner per (page, kv head, block)
+        // in this launch, so the result is deterministic) or stores them to dk_cur / dv_cur (the
+        // chunk's own keys). Rows beyond the page's fill level carry zeros (the reference leaves
+        // those slots at 0).
+        uint8_t* stage = smem + kKvQ + half * 4 * kSliceBytes;
+        const uint32_t acc = half ? tm_dv : tm_dk;
+        const float sc = key_ok ? (half ? 1.f : g.scale) : 0.f;
 #pragma unroll 1
-        for (int c = 0; c < kHd / 32; ++c) {
-            stage_slice(tm_dk + c * 32 + lane_off, stage + c * kSliceBytes, kr, key_ok ? g.scale : 0.f);
-            stage_slice(tm_dv + c * 32 + lane_off, stage + (4 + c) * kSliceBytes, kr, key_ok ? 1.f : 0.f);
-        }
+        for (int c = 0; c < kHd / 32; ++c) stage_slice(acc + c * 32 + lane_off, stage + c * kSliceBytes, kr, sc);
         fence_proxy_async_smem();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, 256);
         if (warp == 4 && lane == 0) {
+            stage = smem + kKvQ;
             if (u.past) {
                 const int row = (g_slot * g.Hkv + g_kv) * g.P + u.key0;
                 for (int c = 0; c < kHd / 32; ++c) {
@@ -664,6 +699,7 @@ __global__ void __launch_bounds__(256, 1)
             }
             bulk_commit();
             bulk_wait_read0();
+            trace_mark(p.tr, 6);
         }
     }
     tc_fence_before();
@@ -715,7 +751,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     const CUtensorMap tkc = map_rows_heads(k_cur, g.C, g.Hkv, kHd);
     const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, kHd);
     BwdParams p{g, sel_off, sel_ids, d_kvslot_layer, d_gslot_layer, gkpool, gvpool, w.Dt, w.Lt, w.mask, w.uni,
-                w.n_uni, dq, dk_cur, dv_cur, d_err};
+                w.n_uni, dq, dk_cur, dv_cur, d_err, CtaTrace{}};
     delete prep_scope;
     {
         ProfScope s_(PK_BWD_DQ, st);
@@ -728,11 +764,14 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         ProfScope s_(PK_BWD_DKDV, st);
         const int max_union = std::min(nnz, n_pages);
         const int units = g.C / kTile + max_union * (g.P / kTile);
+        const size_t n_ctas = static_cast<size_t>(units) * g.Hkv;
+        p.tr = trace_begin("dkdv", n_ctas, 8);
         const CUtensorMap tdkc = map_rows_heads_f32(dk_cur, g.C, g.Hkv, kHd);
         const CUtensorMap tdvc = map_rows_heads_f32(dv_cur, g.C, g.Hkv, kHd);
-        attn_bwd_dkdv_kernel<<<dim3(units, g.Hkv), 256, kKvSmem, st>>>(
+        attn_bwd_dkdv_kernel<<<dim3(units, g.Hkv), 384, kKvSmem, st>>>(
             tq64, tdo64, tkc, tvc, maps.kpool, maps.vpool, maps.gkpool, maps.gvpool, tdkc, tdvc, p);
         check_launch("attn_bwd_dkdv_kernel");
+        trace_end(p.tr, n_ctas, st);
     }
 }
 

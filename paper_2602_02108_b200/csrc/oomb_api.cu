@@ -5,6 +5,7 @@
 // selections (device CSR + pinned host mirror), and dispatch to the sm_100a
 // kernels. Every entry point catches and converts exceptions to oomb_status.
 
+#include <map>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -22,6 +23,57 @@ namespace oomb {
 
 thread_local std::string g_last_error;
 thread_local Profiler* g_prof = nullptr;
+
+namespace {
+struct TraceReq {
+    std::string tag, path;
+    long index = -1;
+    std::map<std::string, long> counts;
+    std::string pending_path;
+};
+TraceReq& trace_req() {
+    static TraceReq r = [] {
+        TraceReq t;
+        if (const char* e = getenv("OOMB_CTA_TRACE")) {
+            std::string v(e);
+            const size_t a = v.find(':'), b = v.find(':', a + 1);
+            if (a != std::string::npos && b != std::string::npos) {
+                t.tag = v.substr(0, a);
+                t.index = std::stol(v.substr(a + 1, b - a - 1));
+                t.path = v.substr(b + 1);
+            }
+        }
+        return t;
+    }();
+    return r;
+}
+}  // namespace
+
+CtaTrace trace_begin(const char* tag, size_t n_ctas, int slots) {
+    TraceReq& r = trace_req();
+    CtaTrace t;
+    if (r.index < 0 || r.tag != tag) return t;
+    if (r.counts[tag]++ != r.index) return t;
+    OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&t.buf), n_ctas * slots * sizeof(unsigned long long)));
+    OOMB_CUDA(cudaMemset(t.buf, 0, n_ctas * slots * sizeof(unsigned long long)));
+    t.slots = slots;
+    return t;
+}
+
+void trace_end(CtaTrace& t, size_t n_ctas, cudaStream_t st) {
+    if (!t.buf) return;
+    OOMB_CUDA(cudaStreamSynchronize(st));
+    std::vector<unsigned long long> h(n_ctas * t.slots);
+    OOMB_CUDA(cudaMemcpy(h.data(), t.buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    if (FILE* f = fopen(trace_req().path.c_str(), "wb")) {
+        const int64_t hdr[2] = {static_cast<int64_t>(n_ctas), t.slots};
+        fwrite(hdr, sizeof(hdr), 1, f);
+        fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+        fclose(f);
+    }
+    cudaFree(t.buf);
+    t.buf = nullptr;
+}
 
 // ---------------------------------------------------------------------------
 // cuTensorMapEncodeTiled through the runtime's driver entry point.

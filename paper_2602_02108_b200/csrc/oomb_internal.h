@@ -86,6 +86,41 @@ struct ProfScope {
     }
 };
 
+// ---------------------------------------------------------------------------
+// Debug CTA timeline. OOMB_CTA_TRACE="<tag>:<launch index>:<file>" makes the chosen
+// launch of kernel <tag> write, per CTA, its SM id (slot 0) and %globaltimer stamps
+// (slots 1..) into a device buffer that is dumped to <file> after the launch
+// (int64 header {n_ctas, slots}, then n_ctas x slots uint64). Off by default; a null
+// buffer makes every mark a predicated-off branch.
+// ---------------------------------------------------------------------------
+struct CtaTrace {
+    unsigned long long* buf = nullptr;
+    int slots = 0;
+};
+#ifdef __CUDACC__
+__device__ __forceinline__ void trace_mark(const CtaTrace& t, int slot) {
+    if (t.buf) {
+        unsigned long long ts;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+        const size_t cta = blockIdx.x + static_cast<size_t>(gridDim.x) * (blockIdx.y + gridDim.y * blockIdx.z);
+        t.buf[cta * t.slots + slot] = ts;
+    }
+}
+__device__ __forceinline__ void trace_value(const CtaTrace& t, int slot, unsigned long long v) {
+    if (t.buf) {
+        const size_t cta = blockIdx.x + static_cast<size_t>(gridDim.x) * (blockIdx.y + gridDim.y * blockIdx.z);
+        t.buf[cta * t.slots + slot] = v;
+    }
+}
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+#endif
+CtaTrace trace_begin(const char* tag, size_t n_ctas, int slots);
+void trace_end(CtaTrace& t, size_t n_ctas, cudaStream_t st);
+
 // Device error flags (bitmask) written by kernels.
 enum : int { DERR_NOT_RESIDENT = 1, DERR_BAD_ID = 2 };
 

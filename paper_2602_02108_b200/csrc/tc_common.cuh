@@ -34,6 +34,19 @@ __device__ __forceinline__ uint64_t desc_mn(uint32_t tile, int kstep, int region
     return make_sdesc_sw128(tile + kstep * 2048, region_bytes, 1024);
 }
 
+// Descriptor arithmetic on a precomputed base: the start-address field is the low 14 bits
+// (address >> 4) and never carries for shared-memory addresses, so advancing a descriptor
+// is one 64-bit add of (byte offset >> 4) — a compile-time constant inside unrolled K loops.
+__device__ __forceinline__ uint64_t sdesc_k(uint32_t tile) { return make_sdesc_sw128(tile, 16, 1024); }
+__device__ __forceinline__ uint64_t sdesc_mn(uint32_t tile, int region_bytes) {
+    return make_sdesc_sw128(tile, region_bytes, 1024);
+}
+__host__ __device__ constexpr uint64_t koff(int kstep, int region_bytes) {  // K-major K step of 16 elements
+    return static_cast<uint64_t>(((kstep >> 2) * region_bytes + (kstep & 3) * 32) >> 4);
+}
+__host__ __device__ constexpr uint64_t mnoff(int kstep) { return static_cast<uint64_t>((kstep * 2048) >> 4); }
+__host__ __device__ constexpr uint64_t boff(int bytes) { return static_cast<uint64_t>(bytes >> 4); }
+
 __device__ __forceinline__ uint4 pack8(const float* e) {
     uint4 pk;
     pk.x = pack_bf16(e[0], e[1]);

@@ -1,6 +1,6 @@
 import json, sys
 l = [x for x in open(sys.argv[1]) if x.startswith('{')]
 d = json.loads(l[-1])
-print(round(d['value']), round(d['ms_per_step'], 1), round(d['pct_bf16_peak'], 4), 'e2e', d.get('e2e', {}).get('value'))
+print(round(d['value']), round(d['ms_per_step'], 1), round(d['pct_bf16_peak'], 4), 'e2e', (d.get("e2e") or {}).get("value"))
 for k, v in d['kernels'].items():
     print(' ', k, {a: round(b, 3) for a, b in v.items()})
