@@ -271,6 +271,13 @@ int oomb_pool_create(const oomb_config* cfg, int device, oomb_pool_t* out) {
             p->cfg = *cfg;
             p->device = device;
             OOMB_CUDA(cudaSetDevice(device));
+            {  // stream-ordered scratch (scoring workspace, id lists) is reused chunk after chunk: keep
+               // freed blocks in the device's default pool instead of unmapping them at every sync
+                cudaMemPool_t mp;
+                OOMB_CUDA(cudaDeviceGetDefaultMemPool(&mp, device));
+                uint64_t keep = UINT64_MAX;
+                OOMB_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep));
+            }
             const auto& c = p->cfg;
             p->max_pages = (c.max_tokens + c.page_size - 1) / c.page_size;
             p->elem = c.dtype == OOMB_BF16 ? 2 : 4;

@@ -1,0 +1,64 @@
+// Microbenchmark: tcgen05.mma issue/throughput for the operand shapes the attention
+// kernels use (SS vs TS, N = 32/64/128/256), one CTA per SM, back-to-back MMAs.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../../paper_2602_02108_b200/csrc mma_rate.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "ptx.cuh"
+using namespace oomb;
+
+template <int N, bool TS>
+__global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+    if (warp == 0) tmem_alloc<512>(&tbase);
+    tc_fence_before(); __syncthreads(); tc_fence_after();
+    const uint32_t tmem = tbase;
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 65536);
+    const uint64_t da = make_sdesc_sw128(a, 16, 1024), db = make_sdesc_sw128(b, 16, 1024);
+    constexpr uint32_t idesc = make_idesc_bf16(128, N, 0, 0);
+    unsigned long long t0 = clock64();
+    if (warp == 0) {
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                if (TS) umma_ts_w(tmem + 256, tmem + ks * 8, db + ks * 2, idesc, 1);
+                else umma_ss_w(tmem + 256, da + ks * 2, db + ks * 2, idesc, 1);
+            }
+        }
+        umma_commit_w(&bar);
+        mbar_wait(&bar, 0);
+    }
+    __syncthreads();
+    unsigned long long t1 = clock64();
+    if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+    tc_fence_before(); __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+template <int N, bool TS>
+void run(int sms) {
+    unsigned long long* d; cudaMalloc(&d, sms * 8);
+    auto k = k_mma<N, TS>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    const int iters = 2000;
+    k<<<sms, 128, 160 * 1024>>>(10, d);
+    k<<<sms, 128, 160 * 1024>>>(iters, d);
+    cudaDeviceSynchronize();
+    unsigned long long h[256]; cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
+    double mx = 0; for (int i = 0; i < sms; ++i) mx = mx > h[i] ? mx : h[i];
+    const double fma = 128.0 * N * 16;
+    const double clk = mx / (iters * 8.0);
+    printf("%s N=%3d: %6.1f clk/MMA  -> %6.0f FMA/clk/SM (%.0f%% of 4096)  err=%s\n", TS ? "TS" : "SS", N, clk, fma / clk,
+           fma / clk / 4096 * 100, cudaGetErrorString(cudaGetLastError()));
+    cudaFree(d);
+}
+
+int main() {
+    int sms = 148;
+    run<32, false>(sms); run<64, false>(sms); run<128, false>(sms); run<256, false>(sms);
+    run<32, true>(sms); run<64, true>(sms); run<128, true>(sms); run<256, true>(sms);
+    return 0;
+}
