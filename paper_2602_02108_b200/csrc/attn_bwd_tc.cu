@@ -360,18 +360,13 @@ __global__ void __launch_bounds__(256, 1)
 // ===========================================================================
 // dK/dV kernel (key-major, one CTA per (key block, kv head))
 //
-// Every MMA reads its A operand from TMEM (a TS-MMA): shared memory then supplies only
-// the B operand, which keeps the 128 B/clk smem operand port below the tensor rate
-// (measured: an SS-MMA with N = 64 runs at 67% of peak, a TS-MMA at 97-100%).
-//   * K and V of the block are staged into TMEM once per CTA (bf16 packed, 64 columns each).
-//   * Per work item (64 query rows of one q-head), split into two 32-query halves that the two
-//     softmax warpgroups own: S^T_h = K Q_h^T and dP^T_h = V dO_h^T land in the half's TMEM
-//     columns, the warpgroup writes P^T_h and dS^T_h = P^T_h (dP^T_h - D) back IN PLACE as
-//     packed bf16, and dV += P^T_h dO_h, dK += dS^T_h Q_h accumulate in TMEM. While one half
-//     is in the softmax the tensor pipe runs the other half's MMAs. A half's columns are
-//     rewritten (next item) only by MMAs issued after the dV/dK that read them, and the
-//     tcgen05.mma operations of one thread execute in issue order.
-// TMEM: K [0,64) V [64,128) S^T [128,192) dP^T [192,256) dK [256,384) dV [384,512).
+// Per work item (64 query rows of one q-head): S^T = K Q^T and dP^T = V dO^T land in
+// TMEM (double buffered); the softmax warps turn them into P^T and dS^T = P^T (dP^T - D)
+// and write them back as packed bf16 IN PLACE of S^T / dP^T, so dV += P^T dO and
+// dK += dS^T Q run as TS-MMAs (A operand from TMEM). The TMEM buffer of item i is
+// rewritten by S/dP of item i+2 only after dV/dK(i) were issued, and tcgen05.mma
+// operations of one thread execute in issue order. Shared memory then holds only K, V
+// and a 4-deep ring of Q / dO / {L, D} stages.
 // ===========================================================================
 constexpr int kKvStages = 4;
 constexpr int kKvK = 0;
@@ -385,11 +380,10 @@ constexpr int kKvSmem = kKvBar + 256 + 1024;
 static_assert(kKvStages * 2 * kTile64 >= 8 * kSliceBytes, "epilogue staging reuses the Q / dO ring");
 
 struct KvBars {
-    uint64_t kv_full;    // K, V tiles in smem (TMA)
-    uint64_t kv_tmem;    // K, V staged into TMEM by the softmax warps
+    uint64_t kv_full;
     uint64_t qdo_full[kKvStages], qdo_empty[kKvStages];
-    uint64_t sdp_full[2];  // per half
-    uint64_t pds_full[2];  // per half
+    uint64_t sdp_full[2];
+    uint64_t pds_full[2];
     uint64_t acc_done;
     uint32_t tmem_base;
 };
@@ -405,6 +399,11 @@ struct KvUnit {
     int n_qps;      // past: number of query pages in the list
     int tiles_per_qp;
 };
+
+// TMEM column of K step ks (16 queries = 8 packed columns) of P^T / dS^T inside an item's
+// 64-column S^T / dP^T buffer: each softmax half packs its 32 queries at the start of its own
+// 32 columns.
+__host__ __device__ constexpr uint32_t pt_col(int ks) { return (ks >> 1) * 32 + (ks & 1) * 8; }
 
 // Items of a unit in order: past units walk (query page of the list, 64-row tile, q-head of
 // the group) head-fastest; in-chunk units walk (64-row tile from the key block's diagonal on,
@@ -539,14 +538,13 @@ __global__ void __launch_bounds__(384, 1)
 
     if (threadIdx.x == 0) {
         mbar_init(&bars->kv_full, 1);
-        mbar_init(&bars->kv_tmem, 256);
         for (int i = 0; i < kKvStages; ++i) {
             mbar_init(&bars->qdo_full[i], 1);
             mbar_init(&bars->qdo_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bars->sdp_full[i], 1);
-            mbar_init(&bars->pds_full[i], 128);
+            mbar_init(&bars->pds_full[i], 256);
         }
         mbar_init(&bars->acc_done, 1);
         fence_barrier_init();
@@ -556,8 +554,9 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
-    const uint32_t tm_k = tmem, tm_v = tmem + 64, tm_s = tmem + 128, tm_dp = tmem + 192, tm_dk = tmem + 256,
-                   tm_dv = tmem + 384;
+    // TMEM: S^T [0,64) [64,128), dP^T [128,192) [192,256) (P^T / dS^T overwrite their first
+    // 32 columns as packed bf16), dK [256,384), dV [384,512)
+    const uint32_t tm_s = tmem, tm_dp = tmem + 128, tm_dk = tmem + 256, tm_dv = tmem + 384;
     uint8_t* sK = smem + kKvK;
     uint8_t* sV = smem + kKvV;
     uint8_t* sQ = smem + kKvQ;
@@ -599,59 +598,46 @@ __global__ void __launch_bounds__(384, 1)
         }
     } else if (warp == 1) {
         // MMA warp, converged: descriptors advance by constant offsets from uniform bases.
-        constexpr uint32_t idesc_s = make_idesc_bf16(kTile, 32, 0, 0);    // [128 keys] x [32 q], K = hd
-        constexpr uint32_t idesc_g = make_idesc_bf16(kTile, kHd, 0, 1);    // [128 keys] x [hd], K = 32 q
+        constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kQ64, 0, 0);   // [128 keys] x [64 q], K = hd
+        constexpr uint32_t idesc_g = make_idesc_bf16(kTile, kHd, 0, 1);    // [128 keys] x [hd], K = 64 q
+        const uint64_t dK = sdesc_k(smem_u32(sK)), dV = sdesc_k(smem_u32(sV));
         const uint64_t dQ = sdesc_k(smem_u32(sQ)), dDO = sdesc_k(smem_u32(sDO));
         const uint64_t dQmn = sdesc_mn(smem_u32(sQ), kRegion64), dDOmn = sdesc_mn(smem_u32(sDO), kRegion64);
-        mbar_wait(&bars->kv_tmem, 0);
-        tc_fence_after();
+        mbar_wait(&bars->kv_full, 0);
         if (lane == 0) trace_mark(p.tr, 2);
         __syncwarp();
-        // issue order: SdP_0(0) SdP_1(0) | dVdK_0(0) SdP_0(1) | dVdK_1(0) SdP_1(1) | dVdK_0(1) ...
-        auto sdp = [&](int i, int h) {
-            const int st = i % kKvStages;
-            const uint64_t so = boff(st * kTile64 + h * 32 * 128);  // rows [32h, 32h+32) of the stage
-            if (h == 0) {
+        for (int i = 0; i <= n_items; ++i) {
+            if (i < n_items) {
+                const int st = i % kKvStages, b = i & 1;
+                const uint64_t so = boff(st * kTile64);
                 mbar_wait(&bars->qdo_full[st], (i / kKvStages) & 1);
                 tc_fence_after();
+#pragma unroll
+                for (int ks = 0; ks < kHd / 16; ++ks)
+                    umma_ss_w(tm_s + b * kQ64, dK + koff(ks, kRegion), dQ + so + koff(ks, kRegion64), idesc_s, ks);
+#pragma unroll
+                for (int ks = 0; ks < kHd / 16; ++ks)
+                    umma_ss_w(tm_dp + b * kQ64, dV + koff(ks, kRegion), dDO + so + koff(ks, kRegion64), idesc_s, ks);
+                umma_commit_w(&bars->sdp_full[b]);
             }
+            if (i >= 1) {
+                const int j = i - 1, st = j % kKvStages, b = j & 1;
+                const uint64_t so = boff(st * kTile64);
+                mbar_wait(&bars->pds_full[b], (j >> 1) & 1);
+                tc_fence_after();
 #pragma unroll
-            for (int ks = 0; ks < kHd / 16; ++ks)
-                umma_ts_w(tm_s + h * 32, tm_k + ks * 8, dQ + so + koff(ks, kRegion64), idesc_s, ks);
+                for (int ks = 0; ks < kQ64 / 16; ++ks)
+                    umma_ts_w(tm_dv, tm_s + b * kQ64 + pt_col(ks), dDOmn + so + mnoff(ks), idesc_g, j | ks);
 #pragma unroll
-            for (int ks = 0; ks < kHd / 16; ++ks)
-                umma_ts_w(tm_dp + h * 32, tm_v + ks * 8, dDO + so + koff(ks, kRegion64), idesc_s, ks);
-            umma_commit_w(&bars->sdp_full[h]);
-        };
-        auto dvdk = [&](int i, int h) {
-            const int st = i % kKvStages;
-            const uint64_t so = boff(st * kTile64);
-            mbar_wait(&bars->pds_full[h], i & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks)
-                umma_ts_w(tm_dv, tm_s + h * 32 + ks * 8, dDOmn + so + mnoff(2 * h + ks), idesc_g, i | h | ks);
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks)
-                umma_ts_w(tm_dk, tm_dp + h * 32 + ks * 8, dQmn + so + mnoff(2 * h + ks), idesc_g, i | h | ks);
-            if (h == 1) umma_commit_w(&bars->qdo_empty[st]);
-        };
-        if (n_items > 0) {
-            sdp(0, 0);
-            sdp(0, 1);
+                for (int ks = 0; ks < kQ64 / 16; ++ks)
+                    umma_ts_w(tm_dk, tm_dp + b * kQ64 + pt_col(ks), dQmn + so + mnoff(ks), idesc_g, j | ks);
+                umma_commit_w(&bars->qdo_empty[st]);
+                if (i == n_items) umma_commit_w(&bars->acc_done);
+            }
         }
-        for (int i = 0; i < n_items; ++i) {
-            dvdk(i, 0);
-            if (i == 8 && lane == 0) trace_mark(p.tr, 10);
-            if (i + 1 < n_items) sdp(i + 1, 0);
-            if (i == 8 && lane == 0) trace_mark(p.tr, 11);
-            dvdk(i, 1);
-            if (i + 1 < n_items) sdp(i + 1, 1);
-        }
-        umma_commit_w(&bars->acc_done);
     } else if (warp >= 4) {
-        // Two warpgroups: warps 4..7 own query columns [0, 32) of each item (half 0), warps
-        // 8..11 columns [32, 64) (half 1); warp w reads TMEM lanes 32*(w%4).. (its key rows).
+        // Two warpgroups: warps 4..7 take query columns [0, 32) of each item, warps 8..11
+        // columns [32, 64); warp w reads TMEM lanes 32*(w%4).. (its key rows).
         const int quarter = warp & 3, half = (warp - 4) >> 2;
         const int kr = quarter * 32 + lane;  // key row of the block
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
@@ -659,46 +645,20 @@ __global__ void __launch_bounds__(384, 1)
         const bool key_ok = kr < n_valid;
         const bool page_full = n_valid == kTile;
         const int key_abs = u.key0 + kr;  // chunk-relative key index (in-chunk blocks)
-        // ---- stage this thread's key row of K (half 0) or V (half 1) into TMEM as packed bf16
-        {
-            mbar_wait(&bars->kv_full, 0);
-            const uint8_t* src = half ? sV : sK;
-            const uint32_t dst = (half ? tm_v : tm_k) + lane_off;
-#pragma unroll
-            for (int c16 = 0; c16 < 4; ++c16) {  // 4 x 16 columns = 4 x 32 elements
-                uint32_t v[16];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int c = c16 * 4 + q;  // 16-byte chunk (8 elements) of the row
-                    const uint4 x = *reinterpret_cast<const uint4*>(src + (c >> 3) * kRegion + kr * 128 +
-                                                                     (((c & 7) ^ (kr & 7)) << 4));
-                    v[4 * q] = x.x;
-                    v[4 * q + 1] = x.y;
-                    v[4 * q + 2] = x.z;
-                    v[4 * q + 3] = x.w;
-                }
-                tmem_st16(dst + c16 * 16, v);
-            }
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&bars->kv_tmem);
-        }
         const uint32_t ld_base = smem_u32(smem + kKvLD) + half * 128;
-        const uint32_t tm_sh = tm_s + half * 32 + lane_off, tm_dph = tm_dp + half * 32 + lane_off;
         ItemIter it;
         it.init(u, qps, g_kv, g.group);
         for (int i = 0; i < n_items; ++i, it.next(u, qps, g_kv, g.group)) {
-            const int st = i % kKvStages;
+            const int st = i % kKvStages, b = i & 1;
             const int q0 = it.qt64 * kQ64 + half * 32;
             const uint32_t lrow = ld_base + st * 512, drow = lrow + 256;
             mbar_wait(&bars->qdo_full[st], (i / kKvStages) & 1);  // makes the bulk-copied L / D visible
-            mbar_wait(&bars->sdp_full[half], i & 1);
+            mbar_wait(&bars->sdp_full[b], (i >> 1) & 1);
             if (i == 0 && threadIdx.x == 128) trace_mark(p.tr, 3);
-            if (kr == 0 && (i == 8 || i == 9)) trace_mark(p.tr, half ? 13 + (i - 8) * 2 : 8 + (i - 8) * 4);
             tc_fence_after();
             uint32_t s[32], dp[32];
-            tmem_ld32(tm_sh, s);
-            tmem_ld32(tm_dph, dp);
+            tmem_ld32(tm_s + b * kQ64 + half * 32 + lane_off, s);
+            tmem_ld32(tm_dp + b * kQ64 + half * 32 + lane_off, dp);
             tmem_wait_ld();
             uint32_t pp[16], dd[16];
             if (it.diag || !page_full) {  // causal diagonal / partially filled page: per-element mask
@@ -707,13 +667,19 @@ __global__ void __launch_bounds__(384, 1)
             } else {
                 pds_half<false>(s, dp, lrow, drow, sl2, 0, pp, dd);
             }
-            tmem_st16(tm_sh, pp);   // P^T_h: 32 queries packed into the half's first 16 columns
-            tmem_st16(tm_dph, dd);  // dS^T_h
+            // packed into the first 16 of this half's own 32 S / dP columns (the other half may
+            // still be reading its S columns): K steps 0,1 at cols 0..15, K steps 2,3 at 32..47
+            tmem_st16(tm_s + b * kQ64 + half * 32 + lane_off, pp);
+            tmem_st16(tm_dp + b * kQ64 + half * 32 + lane_off, dd);
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&bars->pds_full[half]);
-            if (kr == 0 && i == 8) trace_mark(p.tr, half ? 14 : 9);
+            mbar_arrive(&bars->pds_full[b]);
         }
+        // ---- epilogue: dK (scaled) and dV leave TMEM as eight [128 x 32] fp32 slices staged in
+        // the now idle Q / dO ring (128 KB); the TMA unit then adds them into the fp32 gradient
+        // page in L2 (past pages: one owner per (page, kv head, block) in this launch, so the
+        // result is deterministic) or stores them to dk_cur / dv_cur (the chunk's own keys).
+        // Rows beyond the page's fill level carry zeros (the reference leaves those slots at 0).
         if (threadIdx.x == 128) trace_mark(p.tr, 4);
         mbar_wait(&bars->acc_done, 0);
         if (threadIdx.x == 128) trace_mark(p.tr, 5);
@@ -813,7 +779,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         const int max_union = std::min(nnz, n_pages);
         const int units = g.C / kTile + max_union * (g.P / kTile);
         const size_t n_ctas = static_cast<size_t>(units) * g.Hkv;
-        p.tr = trace_begin("dkdv", n_ctas, 16);
+        p.tr = trace_begin("dkdv", n_ctas, 8);
         const CUtensorMap tdkc = map_rows_heads_f32(dk_cur, g.C, g.Hkv, kHd);
         const CUtensorMap tdvc = map_rows_heads_f32(dv_cur, g.C, g.Hkv, kHd);
         attn_bwd_dkdv_kernel<<<dim3(units, g.Hkv), 384, kKvSmem, st>>>(

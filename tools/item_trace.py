@@ -16,3 +16,7 @@ d(8, 12, "h0 item period")
 d(13, 14, "softmax h1 item8")
 d(13, 15, "h1 item period")
 d(8, 13, "h0 start -> h1 start")
+if slots > 17:
+    d(10, 16, "MMA: dvdk0 issued -> qdo_full(9) passed")
+    d(16, 17, "MMA: S^T_0(9) 8 MMAs issued")
+    d(17, 11, "MMA: dP^T_0(9) 8 MMAs issued + commit")

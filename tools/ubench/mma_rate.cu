@@ -6,8 +6,8 @@
 #include "ptx.cuh"
 using namespace oomb;
 
-template <int N, bool TS>
-__global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* out) {
+template <int N, bool TS, int LDST = 0>
+__global__ void __launch_bounds__(256, 1) k_mma(int iters, unsigned long long* out) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bar;
     __shared__ uint32_t tbase;
@@ -30,6 +30,18 @@ __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* o
         }
         umma_commit_w(&bar);
         mbar_wait(&bar, 0);
+    } else if (LDST && warp >= 4) {
+        // interference: tcgen05.ld / st of 32 columns in a loop on this warp's lane quarter
+        const uint32_t lo = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        uint32_t v[32];
+        for (int it = 0; it < iters * (LDST == 2 ? 4 : 1); ++it) {
+            tmem_ld32(tmem + 64 + lo, v);
+            tmem_wait_ld();
+            uint32_t w[16];
+            for (int u = 0; u < 16; ++u) w[u] = v[u] + v[u + 16];
+            tmem_st16(tmem + 64 + lo, w);
+            tmem_wait_st();
+        }
     }
     __syncthreads();
     unsigned long long t1 = clock64();
@@ -38,27 +50,87 @@ __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* o
     if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
-template <int N, bool TS>
+template <int N, bool TS, int LDST = 0>
 void run(int sms) {
     unsigned long long* d; cudaMalloc(&d, sms * 8);
-    auto k = k_mma<N, TS>;
+    auto k = k_mma<N, TS, LDST>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     const int iters = 2000;
-    k<<<sms, 128, 160 * 1024>>>(10, d);
-    k<<<sms, 128, 160 * 1024>>>(iters, d);
+    k<<<sms, 256, 160 * 1024>>>(10, d);
+    k<<<sms, 256, 160 * 1024>>>(iters, d);
     cudaDeviceSynchronize();
     unsigned long long h[256]; cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
     double mx = 0; for (int i = 0; i < sms; ++i) mx = mx > h[i] ? mx : h[i];
     const double fma = 128.0 * N * 16;
     const double clk = mx / (iters * 8.0);
-    printf("%s N=%3d: %6.1f clk/MMA  -> %6.0f FMA/clk/SM (%.0f%% of 4096)  err=%s\n", TS ? "TS" : "SS", N, clk, fma / clk,
+    printf("ldst=%d %s N=%3d:", LDST, TS ? "TS" : "SS", N); printf(" %6.1f clk/MMA  -> %6.0f FMA/clk/SM (%.0f%% of 4096)  err=%s\n", TS ? "TS" : "SS", N, clk, fma / clk,
            fma / clk / 4096 * 100, cudaGetErrorString(cudaGetLastError()));
+    cudaFree(d);
+}
+
+
+// The dK/dV kernel's per-half MMA mix: 8 x (N=32) into S, 8 x (N=32) into dP, 2 x (N=128) into
+// dV, 2 x (N=128) into dK, repeated; expected 16*16.5 + 4*64 = 520 clk per group without bubbles.
+template <int MODE>
+__global__ void __launch_bounds__(128, 1) k_mix(int iters, unsigned long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+    if (warp == 0) tmem_alloc<512>(&tbase);
+    tc_fence_before(); __syncthreads(); tc_fence_after();
+    const uint32_t tmem = tbase;
+    const uint32_t b = smem_u32(smem + 65536);
+    const uint64_t db = make_sdesc_sw128(b, 16, 1024);
+    const uint64_t dbmn = make_sdesc_sw128(b, 8192, 1024);
+    constexpr uint32_t id32 = make_idesc_bf16(128, 32, 0, 0);
+    constexpr uint32_t id128 = make_idesc_bf16(128, 128, 0, 1);
+    unsigned long long t0 = clock64();
+    if (warp == 0) {
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) umma_ts_w(tmem + 128, tmem + ks * 8, db + ks * 2, id32, ks);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) umma_ts_w(tmem + 192, tmem + 64 + ks * 8, db + ks * 2, id32, ks);
+            if (MODE >= 1) {
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) umma_ts_w(tmem + 256, tmem + 128 + ks * 8, dbmn + ks * 128, id128, 1);
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) umma_ts_w(tmem + 384, tmem + 192 + ks * 8, dbmn + ks * 128, id128, 1);
+            }
+            if (MODE == 2) umma_commit_w(&bar);  // a commit per group (as the kernel does)
+        }
+        umma_commit_w(&bar);
+        mbar_wait(&bar, MODE == 2 ? (iters & 1) : 0);
+    }
+    __syncthreads();
+    unsigned long long t1 = clock64();
+    if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+    tc_fence_before(); __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tmem);
+}
+template <int MODE>
+void run_mix(int sms) {
+    unsigned long long* d; cudaMalloc(&d, sms * 8);
+    auto k = k_mix<MODE>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    const int iters = 1000;
+    k<<<sms, 128, 160 * 1024>>>(10, d);
+    k<<<sms, 128, 160 * 1024>>>(iters, d);
+    cudaDeviceSynchronize();
+    unsigned long long h[256]; cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
+    double mx = 0; for (int i = 0; i < sms; ++i) mx = mx > h[i] ? mx : h[i];
+    printf("mix mode %d: %.1f clk per group (ideal %d)  err=%s\n", MODE, mx / iters, MODE ? 520 : 264,
+           cudaGetErrorString(cudaGetLastError()));
     cudaFree(d);
 }
 
 int main() {
     int sms = 148;
-    run<32, false>(sms); run<64, false>(sms); run<128, false>(sms); run<256, false>(sms);
-    run<32, true>(sms); run<64, true>(sms); run<128, true>(sms); run<256, true>(sms);
+    run<32, false>(sms); run<64, false>(sms); run<128, false>(sms);
+    run<32, true>(sms); run<64, true>(sms); run<128, true>(sms);
+    run<32, true, 1>(sms); run<128, true, 1>(sms); run<32, true, 2>(sms); run<128, true, 2>(sms);
+    run_mix<0>(sms); run_mix<1>(sms); run_mix<2>(sms);
     return 0;
 }
