@@ -116,20 +116,33 @@ __global__ void __launch_bounds__(1024) bwd_union_kernel(const uint64_t* __restr
 }
 
 // ===========================================================================
-// dQ kernel (query-major)
+// dQ kernel (query-major): one CTA per (128-row query tile, q-head), looping over the key
+// blocks the tile attends (its query page's selected pages, then the chunk's causal prefix).
+//
+// Every MMA is a TS-MMA (A from TMEM), so shared memory supplies only B operands:
+//   Q and dO are staged into TMEM once (bf16 packed, 64 columns each);
+//   S = Q K^T and dP = dO V^T land in TMEM; the softmax warpgroups turn S into P as soon as
+//   S is ready (the exp work, overlapping dQ of the previous block and dP of this one), then
+//   dS = P (dP - D) is written back IN PLACE of dP as packed bf16 and dQ += dS K runs with
+//   dS as the TMEM A operand. dQ is scaled and stored once, by TMA, at the end.
+// TMEM (the CTA owns all 512 columns, base 0): Q [0,64) dO [64,128) S [128,256) dP [256,384)
+// dQ [384,512). Warpgroup w owns key columns [64w, 64w+64) of every block; its packed dS
+// goes to dP columns [256+64w, 256+64w+32) (its own region: the other group may still be
+// reading its dP columns).
 // ===========================================================================
+constexpr int kDqKSt = 3, kDqVSt = 2;
 constexpr int kDqQ = 0;
 constexpr int kDqDO = kDqQ + kTileBytes;
-constexpr int kDqK = kDqDO + kTileBytes;        // 2 stages
-constexpr int kDqV = kDqK + 2 * kTileBytes;     // 2 stages
-constexpr int kDqDS = kDqV + 2 * kTileBytes;    // 1 buffer
-constexpr int kDqBar = kDqDS + kTileBytes;
+constexpr int kDqK = kDqDO + kTileBytes;            // kDqKSt stages
+constexpr int kDqV = kDqK + kDqKSt * kTileBytes;    // kDqVSt stages
+constexpr int kDqBar = kDqV + kDqVSt * kTileBytes;
 constexpr int kDqSmem = kDqBar + 256 + 1024;
+constexpr uint32_t kDqTmQ = 0, kDqTmDO = 64, kDqTmS = 128, kDqTmDP = 256, kDqTmDQ = 384;
 
 struct DqBars {
-    uint64_t q_full;
-    uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-    uint64_t s_full, s_free, dp_full, dp_free, ds_full, ds_empty, dq_done;
+    uint64_t qdo_full, qdo_tmem;
+    uint64_t k_full[kDqKSt], k_empty[kDqKSt], v_full[kDqVSt], v_empty[kDqVSt];
+    uint64_t s_full, s_free, dp_full, ds_full, dq_done;
     uint32_t tmem_base;
 };
 
@@ -153,7 +166,31 @@ struct BwdParams {
     CtaTrace tr;  // debug CTA timeline (OOMB_CTA_TRACE)
 };
 
-__global__ void __launch_bounds__(256, 1)
+// dQ-kernel K step ks (16 keys) of the packed dS operand: keys [64w, 64w+64) of warpgroup w
+// sit in dP columns [64w, 64w+32).
+__host__ __device__ constexpr uint32_t ds_col(int ks) { return (ks >> 2) * 64 + (ks & 3) * 8; }
+
+// Stage one 128 x 128 bf16 row of a K-major SW128 tile (two [128 x 64] regions) into 64 TMEM
+// columns of this thread's lane (bf16 pairs packed per 32-bit column).
+__device__ __forceinline__ void stage_row_tmem(const uint8_t* tile, int region_bytes, int r, uint32_t taddr) {
+#pragma unroll
+    for (int c16 = 0; c16 < 4; ++c16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = c16 * 4 + q;
+            const uint4 x = *reinterpret_cast<const uint4*>(tile + (c >> 3) * region_bytes + r * 128 +
+                                                             (((c & 7) ^ (r & 7)) << 4));
+            v[4 * q] = x.x;
+            v[4 * q + 1] = x.y;
+            v[4 * q + 2] = x.z;
+            v[4 * q + 3] = x.w;
+        }
+        tmem_st16(taddr + c16 * 16, v);
+    }
+}
+
+__global__ void __launch_bounds__(384, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_kc, const __grid_constant__ CUtensorMap tm_vc,
                        const __grid_constant__ CUtensorMap tm_kp, const __grid_constant__ CUtensorMap tm_vp,
@@ -172,19 +209,20 @@ __global__ void __launch_bounds__(256, 1)
     const int warp = warp_id(), lane = lane_id();
 
     if (threadIdx.x == 0) {
-        mbar_init(&bars->q_full, 1);
-        for (int i = 0; i < 2; ++i) {
+        mbar_init(&bars->qdo_full, 1);
+        mbar_init(&bars->qdo_tmem, 256);
+        for (int i = 0; i < kDqKSt; ++i) {
             mbar_init(&bars->k_full[i], 1);
             mbar_init(&bars->k_empty[i], 1);
+        }
+        for (int i = 0; i < kDqVSt; ++i) {
             mbar_init(&bars->v_full[i], 1);
             mbar_init(&bars->v_empty[i], 1);
         }
         mbar_init(&bars->s_full, 1);
-        mbar_init(&bars->s_free, 128);
+        mbar_init(&bars->s_free, 256);
         mbar_init(&bars->dp_full, 1);
-        mbar_init(&bars->dp_free, 128);
-        mbar_init(&bars->ds_full, 128);
-        mbar_init(&bars->ds_empty, 1);
+        mbar_init(&bars->ds_full, 256);
         mbar_init(&bars->dq_done, 1);
         fence_barrier_init();
     }
@@ -192,24 +230,22 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = bars->tmem_base;
-    const uint32_t tm_s = tmem, tm_dp = tmem + 128, tm_dq = tmem + 256;
+    if (bars->tmem_base != 0) __trap();  // all 512 columns: base column 0 (the constants rely on it)
     uint8_t* sQ = smem + kDqQ;
     uint8_t* sDO = smem + kDqDO;
     uint8_t* sK = smem + kDqK;
     uint8_t* sV = smem + kDqV;
-    uint8_t* sDS = smem + kDqDS;
 
     if (warp == 0) {
         if (lane == 0) {  // Q, dO, K producer
-            mbar_expect_tx(&bars->q_full, 2 * kTileBytes);
+            mbar_expect_tx(&bars->qdo_full, 2 * kTileBytes);
             for (int r = 0; r < 2; ++r) {
-                tma_load_3d(sQ + r * kRegion, &tm_q, &bars->q_full, r * 64, h, qt * kTile);
-                tma_load_3d(sDO + r * kRegion, &tm_do, &bars->q_full, r * 64, h, qt * kTile);
+                tma_load_3d(sQ + r * kRegion, &tm_q, &bars->qdo_full, r * 64, h, qt * kTile);
+                tma_load_3d(sDO + r * kRegion, &tm_do, &bars->qdo_full, r * 64, h, qt * kTile);
             }
             for (int j = 0; j < nb; ++j) {
-                const int st = j & 1;
-                if (j >= 2) mbar_wait(&bars->k_empty[st], ((j - 2) >> 1) & 1);
+                const int st = j % kDqKSt;
+                if (j >= kDqKSt) mbar_wait(&bars->k_empty[st], ((j / kDqKSt) - 1) & 1);
                 mbar_expect_tx(&bars->k_full[st], kTileBytes);
                 uint8_t* dst = sK + st * kTileBytes;
                 if (j < n_past) {
@@ -224,8 +260,8 @@ __global__ void __launch_bounds__(256, 1)
     } else if (warp == 2) {
         if (lane == 0) {  // V producer
             for (int j = 0; j < nb; ++j) {
-                const int st = j & 1;
-                if (j >= 2) mbar_wait(&bars->v_empty[st], ((j - 2) >> 1) & 1);
+                const int st = j % kDqVSt;
+                if (j >= kDqVSt) mbar_wait(&bars->v_empty[st], ((j / kDqVSt) - 1) & 1);
                 mbar_expect_tx(&bars->v_full[st], kTileBytes);
                 uint8_t* dst = sV + st * kTileBytes;
                 if (j < n_past) {
@@ -238,114 +274,131 @@ __global__ void __launch_bounds__(256, 1)
             }
         }
     } else if (warp == 1) {
-        constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kTile, 0, 0);
-        constexpr uint32_t idesc_dq = make_idesc_bf16(kTile, kHd, 0, 1);
-        const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO), ds_addr = smem_u32(sDS);
-        mbar_wait(&bars->q_full, 0);
-        for (int j = 0; j <= nb; ++j) {
-            if (j < nb) {
-                const int st = j & 1;
-                mbar_wait(&bars->k_full[st], (j >> 1) & 1);
-                if (j >= 1) mbar_wait(&bars->s_free, (j - 1) & 1);
-                tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t k_addr = smem_u32(sK + st * kTileBytes);
-                    for (int ks = 0; ks < kHd / 16; ++ks)
-                        umma_f16_ss(tm_s, desc_k(q_addr, ks, kRegion), desc_k(k_addr, ks, kRegion), idesc_s, ks > 0);
-                    umma_commit(&bars->s_full);
-                }
-                __syncwarp();
-                mbar_wait(&bars->v_full[st], (j >> 1) & 1);
-                if (j >= 1) mbar_wait(&bars->dp_free, (j - 1) & 1);
-                tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t v_addr = smem_u32(sV + st * kTileBytes);
-                    for (int ks = 0; ks < kHd / 16; ++ks)
-                        umma_f16_ss(tm_dp, desc_k(do_addr, ks, kRegion), desc_k(v_addr, ks, kRegion), idesc_s,
-                                    ks > 0);
-                    umma_commit(&bars->dp_full);
-                    umma_commit(&bars->v_empty[st]);
-                }
-                __syncwarp();
-            }
-            if (j >= 1) {
-                const int i = j - 1, st = i & 1;
-                mbar_wait(&bars->ds_full, i & 1);
-                tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t k_addr = smem_u32(sK + st * kTileBytes);
-                    for (int ks = 0; ks < kTile / 16; ++ks)
-                        umma_f16_ss(tm_dq, desc_k(ds_addr, ks, kRegion), desc_mn(k_addr, ks, kRegion), idesc_dq,
-                                    (i > 0 || ks > 0) ? 1u : 0u);
-                    umma_commit(&bars->k_empty[st]);
-                    umma_commit(&bars->ds_empty);
-                    if (j == nb) umma_commit(&bars->dq_done);
-                }
-                __syncwarp();
-            }
+        // MMA warp (converged). Order: S(0) dP(0) | S(1) dQ(0) dP(1) | S(2) dQ(1) dP(2) | ... dQ(nb-1).
+        constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kTile, 0, 0);  // [128 q] x [128 keys], K = hd
+        constexpr uint32_t idesc_q = make_idesc_bf16(kTile, kHd, 0, 1);    // [128 q] x [hd], K = keys
+        const uint64_t dK = sdesc_k(smem_u32(sK)), dV = sdesc_k(smem_u32(sV));
+        const uint64_t dKmn = sdesc_mn(smem_u32(sK), kRegion);
+        mbar_wait(&bars->qdo_tmem, 0);
+        tc_fence_after();
+        auto mma_s = [&](int j) {
+            const int st = j % kDqKSt;
+            mbar_wait(&bars->k_full[st], (j / kDqKSt) & 1);
+            if (j >= 1) mbar_wait(&bars->s_free, (j - 1) & 1);  // softmax read S(j-1) into registers
+            tc_fence_after();
+            const uint64_t so = boff(st * kTileBytes);
+#pragma unroll
+            for (int ks = 0; ks < kHd / 16; ++ks)
+                umma_ts_w(kDqTmS, kDqTmQ + ks * 8, dK + so + koff(ks, kRegion), idesc_s, ks);
+            umma_commit_w(&bars->s_full);
+        };
+        auto mma_dp = [&](int j) {
+            const int st = j % kDqVSt;
+            mbar_wait(&bars->v_full[st], (j / kDqVSt) & 1);
+            tc_fence_after();
+            const uint64_t so = boff(st * kTileBytes);
+#pragma unroll
+            for (int ks = 0; ks < kHd / 16; ++ks)
+                umma_ts_w(kDqTmDP, kDqTmDO + ks * 8, dV + so + koff(ks, kRegion), idesc_s, ks);
+            umma_commit_w(&bars->dp_full);
+            umma_commit_w(&bars->v_empty[st]);
+        };
+        auto mma_dq = [&](int j) {
+            const int st = j % kDqKSt;
+            mbar_wait(&bars->ds_full, j & 1);
+            tc_fence_after();
+            const uint64_t so = boff(st * kTileBytes);
+            const uint32_t first = j == 0 ? 0u : 1u;
+#pragma unroll
+            for (int ks = 0; ks < kTile / 16; ++ks)
+                umma_ts_w(kDqTmDQ, kDqTmDP + ds_col(ks), dKmn + so + mnoff(ks), idesc_q, first | ks);
+            umma_commit_w(&bars->k_empty[st]);
+        };
+        mma_s(0);
+        mma_dp(0);
+        for (int j = 1; j < nb; ++j) {
+            mma_s(j);
+            mma_dq(j - 1);  // dS(j-1) lives in the dP columns: dP(j) is issued after it
+            mma_dp(j);
         }
+        mma_dq(nb - 1);
+        umma_commit_w(&bars->dq_done);
     } else if (warp >= 4) {
-        const int quarter = warp & 3;
-        const int r = quarter * 32 + lane;
+        const int quarter = warp & 3, wg = (warp - 4) >> 2;
+        const int r = quarter * 32 + lane;  // query row of the tile = TMEM lane
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        // ---- stage Q (group 0) / dO (group 1) rows into TMEM
+        mbar_wait(&bars->qdo_full, 0);
+        stage_row_tmem(wg ? sDO : sQ, kRegion, r, (wg ? kDqTmDO : kDqTmQ) + lane_off);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bars->qdo_tmem);
         const int t = qt * kTile + r;
         const float sl2 = g.scale * kLog2e;
         const float L2 = p.Lt[static_cast<int64_t>(h) * g.C + t];
         const float Dr = p.Dt[static_cast<int64_t>(h) * g.C + t];
         const int bpp = g.P / kTile;
+        const uint32_t tS = kDqTmS + wg * 64 + lane_off, tDP = kDqTmDP + wg * 64 + lane_off;
         int pid_next = n_past > 0 ? p.sel_ids[sel_begin] : 0;  // prefetched one block ahead
         for (int j = 0; j < nb; ++j) {
             const int pid = pid_next;
             if (j + 1 < n_past) pid_next = p.sel_ids[sel_begin + (j + 1) / bpp];
-            int lim;
+            int lim;  // keep key columns c <= lim (of this group's 64)
             if (j < n_past) {
                 const int64_t nv = g.filled - static_cast<int64_t>(pid) * g.P - static_cast<int64_t>(j % bpp) * kTile;
-                lim = static_cast<int>(nv < 0 ? 0 : (nv > kTile ? kTile : nv)) - 1;
+                lim = static_cast<int>(nv < 0 ? 0 : (nv > kTile ? kTile : nv)) - 1 - wg * 64;
             } else {
-                lim = (j - n_past == qt) ? r : kTile - 1;
+                lim = ((j - n_past == qt) ? r : kTile - 1) - wg * 64;
             }
+            // ---- P = exp2(S * scale * log2e - L) for this group's 64 key columns
             mbar_wait(&bars->s_full, j & 1);
             tc_fence_after();
-            float pr[kTile];
+            float pr[64];
+            {
+                uint32_t a[32], b2[32];
+                tmem_ld32(tS, a);
+                tmem_ld32(tS + 32, b2);
+                tmem_wait_ld();
+                tc_fence_before();
+                mbar_arrive(&bars->s_free);
 #pragma unroll
-            for (int c = 0; c < kTile / 16; ++c)
-                tmem_ld16(tm_s + c * 16 + lane_off, *reinterpret_cast<uint32_t(*)[16]>(&pr[c * 16]));
-            tmem_wait_ld();
-            tc_fence_before();
-            mbar_arrive(&bars->s_free);
+                for (int c = 0; c < 32; ++c) pr[c] = ex2(fmaf(__uint_as_float(a[c]), sl2, -L2));
 #pragma unroll
-            for (int c = 0; c < kTile; ++c) {
-                const float e = ex2(pr[c] * sl2 - L2);
-                pr[c] = (c <= lim) ? e : 0.f;
+                for (int c = 0; c < 32; ++c) pr[32 + c] = ex2(fmaf(__uint_as_float(b2[c]), sl2, -L2));
             }
+            if (lim < 63) {
+#pragma unroll
+                for (int c = 0; c < 64; ++c) pr[c] = (c <= lim) ? pr[c] : 0.f;
+            }
+            // ---- dS = P (dP - D), packed bf16 into this group's first 32 dP columns
             mbar_wait(&bars->dp_full, j & 1);
-            if (j >= 1) mbar_wait(&bars->ds_empty, (j - 1) & 1);
             tc_fence_after();
 #pragma unroll
-            for (int c = 0; c < kTile / 16; ++c) {
-                uint32_t dp[16];
-                tmem_ld16(tm_dp + c * 16 + lane_off, dp);
+            for (int c2 = 0; c2 < 2; ++c2) {
+                uint32_t d[32];
+                tmem_ld32(tDP + c2 * 32, d);
                 tmem_wait_ld();
-                float ds[16];
+                uint32_t pk[16];
 #pragma unroll
-                for (int u = 0; u < 16; ++u) ds[u] = pr[c * 16 + u] * (__uint_as_float(dp[u]) - Dr);
-                st_sw128(sDS, kRegion, r, 2 * c, pack8(ds));
-                st_sw128(sDS, kRegion, r, 2 * c + 1, pack8(ds + 8));
+                for (int u = 0; u < 16; ++u)
+                    pk[u] = pack_bf16(pr[c2 * 32 + 2 * u] * (__uint_as_float(d[2 * u]) - Dr),
+                                      pr[c2 * 32 + 2 * u + 1] * (__uint_as_float(d[2 * u + 1]) - Dr));
+                tmem_st16(tDP + c2 * 16, pk);  // below the columns still to be read
             }
+            tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&bars->dp_free);
-            fence_proxy_async_smem();
             mbar_arrive(&bars->ds_full);
         }
-        // dQ (scaled) leaves TMEM as four [128 x 32] fp32 slices staged in the idle K / V buffers,
-        // then one TMA tile store each into dq [C][Hq][hd].
+        // ---- dQ (scaled) leaves TMEM as four [128 x 32] fp32 slices staged in the idle K / V
+        // stages (group w: slices 2w, 2w+1), then one TMA tile store each into dq [C][Hq][hd].
         mbar_wait(&bars->dq_done, 0);
         tc_fence_after();
         uint8_t* stage = sK;
 #pragma unroll 1
-        for (int c = 0; c < kHd / 32; ++c) stage_slice(tm_dq + c * 32 + lane_off, stage + c * kSliceBytes, r, g.scale);
+        for (int c = 2 * wg; c < 2 * wg + 2; ++c)
+            stage_slice(kDqTmDQ + c * 32 + lane_off, stage + c * kSliceBytes, r, g.scale);
         fence_proxy_async_smem();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, 256);
         if (warp == 4 && lane == 0) {
             for (int c = 0; c < kHd / 32; ++c) tma_store_3d(&tmap_dq, stage + c * kSliceBytes, c * 32, h, qt * kTile);
             bulk_commit();
@@ -354,7 +407,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 3) tmem_dealloc<512>(tmem);
+    if (warp == 3) tmem_dealloc<512>(0);
 }
 
 // ===========================================================================
@@ -770,7 +823,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     {
         ProfScope s_(PK_BWD_DQ, st);
         const CUtensorMap tdq = map_rows_heads_f32(dq, g.C, g.Hq, kHd);
-        attn_bwd_dq_kernel<<<dim3(g.Hq, g.C / kTile), 256, kDqSmem, st>>>(tq, tdo, tkc, tvc, maps.kpool, maps.vpool,
+        attn_bwd_dq_kernel<<<dim3(g.Hq, g.C / kTile), 384, kDqSmem, st>>>(tq, tdo, tkc, tvc, maps.kpool, maps.vpool,
                                                                           tdq, p);
         check_launch("attn_bwd_dq_kernel");
     }
