@@ -27,9 +27,6 @@ using namespace tc;
 
 namespace {
 
-constexpr int kQ64 = 64;                        // query rows per dK/dV work item
-constexpr int kRegion64 = kQ64 * 128;           // [64 x 64] bf16 region = 8 KB
-constexpr int kTile64 = 2 * kRegion64;          // [64 x 128] tile = 16 KB
 
 // ---------------------------------------------------------------- workspace
 struct BwdWs {
@@ -136,7 +133,10 @@ constexpr int kDqDO = kDqQ + kTileBytes;
 constexpr int kDqK = kDqDO + kTileBytes;            // kDqKSt stages
 constexpr int kDqV = kDqK + kDqKSt * kTileBytes;    // kDqVSt stages
 constexpr int kDqBar = kDqV + kDqVSt * kTileBytes;
-constexpr int kDqSmem = kDqBar + 256 + 1024;
+constexpr int kDqNv = kDqBar + 256;                 // uint8 valid-key counts of the past blocks
+constexpr int kDqNvCap = 1024;
+constexpr int kDqSmem = kDqNv + kDqNvCap + 1024;
+static_assert(kDqSmem <= 232448, "dynamic shared memory above the 227 KB opt-in limit");
 constexpr uint32_t kDqTmQ = 0, kDqTmDO = 64, kDqTmS = 128, kDqTmDP = 256, kDqTmDQ = 384;
 
 struct DqBars {
@@ -337,16 +337,14 @@ __global__ void __launch_bounds__(384, 1)
         const float sl2 = g.scale * kLog2e;
         const float L2 = p.Lt[static_cast<int64_t>(h) * g.C + t];
         const float Dr = p.Dt[static_cast<int64_t>(h) * g.C + t];
-        const int bpp = g.P / kTile;
         const uint32_t tS = kDqTmS + wg * 64 + lane_off, tDP = kDqTmDP + wg * 64 + lane_off;
-        int pid_next = n_past > 0 ? p.sel_ids[sel_begin] : 0;  // prefetched one block ahead
+        uint8_t* nvt = smem + kDqNv;
+        stage_past_valid(g, p.sel_ids, sel_begin, n_past, nvt, kDqNvCap, threadIdx.x - 128, 256);
+        named_bar_sync(3, 256);
         for (int j = 0; j < nb; ++j) {
-            const int pid = pid_next;
-            if (j + 1 < n_past) pid_next = p.sel_ids[sel_begin + (j + 1) / bpp];
             int lim;  // keep key columns c <= lim (of this group's 64)
             if (j < n_past) {
-                const int64_t nv = g.filled - static_cast<int64_t>(pid) * g.P - static_cast<int64_t>(j % bpp) * kTile;
-                lim = static_cast<int>(nv < 0 ? 0 : (nv > kTile ? kTile : nv)) - 1 - wg * 64;
+                lim = past_valid(g, p.sel_ids, sel_begin, nvt, kDqNvCap, j) - 1 - wg * 64;
             } else {
                 lim = ((j - n_past == qt) ? r : kTile - 1) - wg * 64;
             }
@@ -413,30 +411,40 @@ __global__ void __launch_bounds__(384, 1)
 // ===========================================================================
 // dK/dV kernel (key-major, one CTA per (key block, kv head))
 //
-// Per work item (64 query rows of one q-head): S^T = K Q^T and dP^T = V dO^T land in
-// TMEM (double buffered); the softmax warps turn them into P^T and dS^T = P^T (dP^T - D)
-// and write them back as packed bf16 IN PLACE of S^T / dP^T, so dV += P^T dO and
-// dK += dS^T Q run as TS-MMAs (A operand from TMEM). The TMEM buffer of item i is
-// rewritten by S/dP of item i+2 only after dV/dK(i) were issued, and tcgen05.mma
-// operations of one thread execute in issue order. Shared memory then holds only K, V
-// and a 4-deep ring of Q / dO / {L, D} stages.
+// A CTA owns one 128-key block (a past page, or a block of the chunk's own keys) of one kv
+// head and loops over the work items that attend it: (128-row query tile, q-head of the
+// group) — the query pages that selected the page, or the chunk's tiles from the diagonal on.
+// Per item:
+//   S^T = K Q^T, dP^T = V dO^T   SS-MMAs with N = 128 queries (full rate: the smem operand
+//                                port carries 8 KB per 64 clk);
+//   P^T = exp2(S^T scale log2e - L)  written back IN PLACE of S^T as packed bf16 as soon as
+//                                S^T lands (the exp work overlaps dK of the previous item and
+//                                dP^T of this one), kept in registers for
+//   dS^T = P^T (dP^T - D)        written back in place of dP^T;
+//   dV += P^T dO, dK += dS^T Q   TS-MMAs (A from TMEM), accumulated over all items in TMEM.
+// Issue order: S(0) dP(0) | dV(0) S(1) dK(0) dP(1) | dV(1) S(2) dK(1) dP(2) | ... — each MMA
+// that rewrites S^T / dP^T columns is issued after the MMA that read them, and tcgen05.mma
+// operations of one thread execute in issue order.
+// TMEM (all 512 columns, base 0): S^T [0,128) dP^T [128,256) dK [256,384) dV [384,512);
+// softmax warpgroup w owns query columns [64w, 64w+64) and packs into its own first 32.
 // ===========================================================================
-constexpr int kKvStages = 4;
+constexpr int kKvStages = 2;
 constexpr int kKvK = 0;
 constexpr int kKvV = kKvK + kTileBytes;
-constexpr int kKvQ = kKvV + kTileBytes;                  // kKvStages stages of [64 x 128]
-constexpr int kKvDO = kKvQ + kKvStages * kTile64;        // kKvStages stages
-constexpr int kKvQps = kKvDO + kKvStages * kTile64;      // query-page list (<= 64 ints)
-constexpr int kKvLD = kKvQps + 256;                      // kKvStages stages of {L[64], D[64]} fp32 (TMA bulk)
-constexpr int kKvBar = kKvLD + kKvStages * 512;
+constexpr int kKvQ = kKvV + kTileBytes;                  // kKvStages stages of [128 x 128]
+constexpr int kKvDO = kKvQ + kKvStages * kTileBytes;     // kKvStages stages
+constexpr int kKvQps = kKvDO + kKvStages * kTileBytes;   // query-page list (<= 64 ints)
+constexpr int kKvLD = kKvQps + 256;                      // kKvStages stages of {L[128], D[128]} fp32 (TMA bulk)
+constexpr int kKvBar = kKvLD + kKvStages * 1024;
 constexpr int kKvSmem = kKvBar + 256 + 1024;
-static_assert(kKvStages * 2 * kTile64 >= 8 * kSliceBytes, "epilogue staging reuses the Q / dO ring");
+static_assert(kKvSmem <= 232448, "dynamic shared memory above the 227 KB opt-in limit");
+static_assert(kKvStages * 2 * kTileBytes >= 8 * kSliceBytes, "epilogue staging reuses the Q / dO ring");
+constexpr uint32_t kTmS = 0, kTmDP = 128, kTmDK = 256, kTmDV = 384;
 
 struct KvBars {
     uint64_t kv_full;
     uint64_t qdo_full[kKvStages], qdo_empty[kKvStages];
-    uint64_t sdp_full[2];
-    uint64_t pds_full[2];
+    uint64_t s_full, dp_full, p_full, ds_full;
     uint64_t acc_done;
     uint32_t tmem_base;
 };
@@ -453,26 +461,25 @@ struct KvUnit {
     int tiles_per_qp;
 };
 
-// TMEM column of K step ks (16 queries = 8 packed columns) of P^T / dS^T inside an item's
-// 64-column S^T / dP^T buffer: each softmax half packs its 32 queries at the start of its own
-// 32 columns.
-__host__ __device__ constexpr uint32_t pt_col(int ks) { return (ks >> 1) * 32 + (ks & 1) * 8; }
+// K step ks (16 queries) of a packed P^T / dS^T operand: queries [64w, 64w+64) of warpgroup w
+// sit in the first 32 of its own 64 columns.
+__host__ __device__ constexpr uint32_t pk_col(int ks) { return (ks >> 2) * 64 + (ks & 3) * 8; }
 
-// Items of a unit in order: past units walk (query page of the list, 64-row tile, q-head of
-// the group) head-fastest; in-chunk units walk (64-row tile from the key block's diagonal on,
-// q-head). Advanced incrementally (no integer division on the per-item path).
+// Items of a unit in order: past units walk (query page of the list, 128-row tile of the page,
+// q-head of the group) head-fastest; in-chunk units walk (128-row tile from the key block's
+// diagonal on, q-head). Advanced incrementally (no integer division on the per-item path).
 struct ItemIter {
-    int h, qt64, qpi, tile;  // q-head, 64-row query tile, index in the query-page list, tile in the page
+    int h, qt, qpi, tile;  // q-head, 128-row query tile, index in the query-page list, tile in the page
     bool diag;
     __device__ __forceinline__ void init(const KvUnit& u, const int* qps, int g_kv, int G) {
         h = g_kv * G;
         qpi = 0;
         tile = 0;
         if (u.past) {
-            qt64 = qps[0] * u.tiles_per_qp;
+            qt = qps[0] * u.tiles_per_qp;
             diag = false;
         } else {
-            qt64 = 2 * (u.key0 / kTile);
+            qt = u.key0 / kTile;
             diag = true;
         }
     }
@@ -480,53 +487,22 @@ struct ItemIter {
         if (++h < (g_kv + 1) * G) return;
         h = g_kv * G;
         if (!u.past) {
-            ++qt64;
-            diag = qt64 < 2 * (u.key0 / kTile) + 2;
+            ++qt;
+            diag = false;
             return;
         }
         if (++tile == u.tiles_per_qp) {
             tile = 0;
             ++qpi;
-            if (qpi < u.n_qps) qt64 = qps[qpi] * u.tiles_per_qp;
+            if (qpi < u.n_qps) qt = qps[qpi] * u.tiles_per_qp;
         } else {
-            ++qt64;
+            ++qt;
         }
     }
 };
 
-// P^T and dS^T of one 32-query half of an item for this thread's key row, packed bf16.
-// kMasked: columns c < lim are zeroed (causal diagonal / unfilled page slots).
-template <bool kMasked>
-__device__ __forceinline__ void pds_half(const uint32_t (&s)[32], const uint32_t (&dp)[32], uint32_t lrow,
-                                         uint32_t drow, float sl2, int lim, uint32_t (&pp)[16],
-                                         uint32_t (&dd)[16]) {
-    float e[32];
-#pragma unroll
-    for (int c4 = 0; c4 < 8; ++c4) {
-        const float4 l4 = lds128(lrow + c4 * 16);
-        e[4 * c4 + 0] = ex2(fmaf(__uint_as_float(s[4 * c4 + 0]), sl2, -l4.x));
-        e[4 * c4 + 1] = ex2(fmaf(__uint_as_float(s[4 * c4 + 1]), sl2, -l4.y));
-        e[4 * c4 + 2] = ex2(fmaf(__uint_as_float(s[4 * c4 + 2]), sl2, -l4.z));
-        e[4 * c4 + 3] = ex2(fmaf(__uint_as_float(s[4 * c4 + 3]), sl2, -l4.w));
-    }
-    if (kMasked) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) e[c] = (c >= lim) ? e[c] : 0.f;
-    }
-#pragma unroll
-    for (int c4 = 0; c4 < 8; ++c4) {
-        const float4 d4 = lds128(drow + c4 * 16);
-        pp[2 * c4] = pack_bf16(e[4 * c4 + 0], e[4 * c4 + 1]);
-        pp[2 * c4 + 1] = pack_bf16(e[4 * c4 + 2], e[4 * c4 + 3]);
-        dd[2 * c4] = pack_bf16(e[4 * c4 + 0] * (__uint_as_float(dp[4 * c4 + 0]) - d4.x),
-                               e[4 * c4 + 1] * (__uint_as_float(dp[4 * c4 + 1]) - d4.y));
-        dd[2 * c4 + 1] = pack_bf16(e[4 * c4 + 2] * (__uint_as_float(dp[4 * c4 + 2]) - d4.z),
-                                   e[4 * c4 + 3] * (__uint_as_float(dp[4 * c4 + 3]) - d4.w));
-    }
-}
-
 __global__ void __launch_bounds__(384, 1)
-    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_constant__ CUtensorMap tm_do64,
+    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                          const __grid_constant__ CUtensorMap tm_kc, const __grid_constant__ CUtensorMap tm_vc,
                          const __grid_constant__ CUtensorMap tm_kp, const __grid_constant__ CUtensorMap tm_vp,
                          const __grid_constant__ CUtensorMap tm_gk, const __grid_constant__ CUtensorMap tm_gv,
@@ -544,13 +520,13 @@ __global__ void __launch_bounds__(384, 1)
 
     // ---- decode the work unit (uniform across the CTA)
     KvUnit u{};
-    u.tiles_per_qp = g.P / kQ64;
+    u.tiles_per_qp = g.P / kTile;
     if (static_cast<int>(blockIdx.x) < n_chunk_blocks) {
         const int b = blockIdx.x;
         u.valid = true;
         u.past = false;
         u.key0 = b * kTile;
-        u.n_items = (g.C / kQ64 - 2 * b) * g.group;
+        u.n_items = (n_chunk_blocks - b) * g.group;
     } else {
         const int pu = blockIdx.x - n_chunk_blocks;
         const int idx = pu / bpp;
@@ -595,10 +571,10 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(&bars->qdo_full[i], 1);
             mbar_init(&bars->qdo_empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&bars->sdp_full[i], 1);
-            mbar_init(&bars->pds_full[i], 256);
-        }
+        mbar_init(&bars->s_full, 1);
+        mbar_init(&bars->dp_full, 1);
+        mbar_init(&bars->p_full, 256);
+        mbar_init(&bars->ds_full, 256);
         mbar_init(&bars->acc_done, 1);
         fence_barrier_init();
     }
@@ -606,10 +582,7 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = bars->tmem_base;
-    // TMEM: S^T [0,64) [64,128), dP^T [128,192) [192,256) (P^T / dS^T overwrite their first
-    // 32 columns as packed bf16), dK [256,384), dV [384,512)
-    const uint32_t tm_s = tmem, tm_dp = tmem + 128, tm_dk = tmem + 256, tm_dv = tmem + 384;
+    if (bars->tmem_base != 0) __trap();  // all 512 columns: base column 0 (the constants rely on it)
     uint8_t* sK = smem + kKvK;
     uint8_t* sV = smem + kKvV;
     uint8_t* sQ = smem + kKvQ;
@@ -635,104 +608,165 @@ __global__ void __launch_bounds__(384, 1)
             it.init(u, qps, g_kv, g.group);
             for (int i = 0; i < n_items; ++i, it.next(u, qps, g_kv, g.group)) {
                 const int st = i % kKvStages;
-                const int h = it.h, qt64 = it.qt64;
                 if (i >= kKvStages) mbar_wait(&bars->qdo_empty[st], ((i / kKvStages) - 1) & 1);
-                mbar_expect_tx(&bars->qdo_full[st], 2 * kTile64 + 512);
-                float* ld = reinterpret_cast<float*>(smem + kKvLD) + st * 128;
-                bulk_load(ld, p.Lt + static_cast<int64_t>(h) * g.C + qt64 * kQ64, 256, &bars->qdo_full[st]);
-                bulk_load(ld + 64, p.Dt + static_cast<int64_t>(h) * g.C + qt64 * kQ64, 256, &bars->qdo_full[st]);
+                mbar_expect_tx(&bars->qdo_full[st], 2 * kTileBytes + 1024);
+                float* ld = reinterpret_cast<float*>(smem + kKvLD) + st * 256;
+                bulk_load(ld, p.Lt + static_cast<int64_t>(it.h) * g.C + it.qt * kTile, 512, &bars->qdo_full[st]);
+                bulk_load(ld + 128, p.Dt + static_cast<int64_t>(it.h) * g.C + it.qt * kTile, 512,
+                          &bars->qdo_full[st]);
                 for (int r = 0; r < 2; ++r) {
-                    tma_load_3d(sQ + st * kTile64 + r * kRegion64, &tm_q64, &bars->qdo_full[st], r * 64, h,
-                                qt64 * kQ64);
-                    tma_load_3d(sDO + st * kTile64 + r * kRegion64, &tm_do64, &bars->qdo_full[st], r * 64, h,
-                                qt64 * kQ64);
+                    tma_load_3d(sQ + st * kTileBytes + r * kRegion, &tm_q, &bars->qdo_full[st], r * 64, it.h,
+                                it.qt * kTile);
+                    tma_load_3d(sDO + st * kTileBytes + r * kRegion, &tm_do, &bars->qdo_full[st], r * 64, it.h,
+                                it.qt * kTile);
                 }
             }
         }
     } else if (warp == 1) {
-        // MMA warp, converged: descriptors advance by constant offsets from uniform bases.
-        constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kQ64, 0, 0);   // [128 keys] x [64 q], K = hd
-        constexpr uint32_t idesc_g = make_idesc_bf16(kTile, kHd, 0, 1);    // [128 keys] x [hd], K = 64 q
+        // MMA warp (converged): S(0) dP(0) | dV(0) S(1) dK(0) dP(1) | dV(1) S(2) dK(1) dP(2) | ...
+        constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kTile, 0, 0);  // [128 keys] x [128 q], K = hd
+        constexpr uint32_t idesc_g = make_idesc_bf16(kTile, kHd, 0, 1);    // [128 keys] x [hd], K = q
         const uint64_t dK = sdesc_k(smem_u32(sK)), dV = sdesc_k(smem_u32(sV));
         const uint64_t dQ = sdesc_k(smem_u32(sQ)), dDO = sdesc_k(smem_u32(sDO));
-        const uint64_t dQmn = sdesc_mn(smem_u32(sQ), kRegion64), dDOmn = sdesc_mn(smem_u32(sDO), kRegion64);
+        const uint64_t dQmn = sdesc_mn(smem_u32(sQ), kRegion), dDOmn = sdesc_mn(smem_u32(sDO), kRegion);
         mbar_wait(&bars->kv_full, 0);
         if (lane == 0) trace_mark(p.tr, 2);
         __syncwarp();
-        for (int i = 0; i <= n_items; ++i) {
-            if (i < n_items) {
-                const int st = i % kKvStages, b = i & 1;
-                const uint64_t so = boff(st * kTile64);
-                mbar_wait(&bars->qdo_full[st], (i / kKvStages) & 1);
-                tc_fence_after();
+        auto mma_s = [&](int i) {
+            const int st = i % kKvStages;
+            mbar_wait(&bars->qdo_full[st], (i / kKvStages) & 1);
+            tc_fence_after();
+            const uint64_t so = boff(st * kTileBytes);
 #pragma unroll
-                for (int ks = 0; ks < kHd / 16; ++ks)
-                    umma_ss_w(tm_s + b * kQ64, dK + koff(ks, kRegion), dQ + so + koff(ks, kRegion64), idesc_s, ks);
+            for (int ks = 0; ks < kHd / 16; ++ks)
+                umma_ss_w(kTmS, dK + koff(ks, kRegion), dQ + so + koff(ks, kRegion), idesc_s, ks);
+            umma_commit_w(&bars->s_full);
+        };
+        auto mma_dp = [&](int i) {
+            const int st = i % kKvStages;
+            const uint64_t so = boff(st * kTileBytes);
 #pragma unroll
-                for (int ks = 0; ks < kHd / 16; ++ks)
-                    umma_ss_w(tm_dp + b * kQ64, dV + koff(ks, kRegion), dDO + so + koff(ks, kRegion64), idesc_s, ks);
-                umma_commit_w(&bars->sdp_full[b]);
-            }
-            if (i >= 1) {
-                const int j = i - 1, st = j % kKvStages, b = j & 1;
-                const uint64_t so = boff(st * kTile64);
-                mbar_wait(&bars->pds_full[b], (j >> 1) & 1);
-                tc_fence_after();
+            for (int ks = 0; ks < kHd / 16; ++ks)
+                umma_ss_w(kTmDP, dV + koff(ks, kRegion), dDO + so + koff(ks, kRegion), idesc_s, ks);
+            umma_commit_w(&bars->dp_full);
+        };
+        auto mma_dv = [&](int i) {
+            const int st = i % kKvStages;
+            mbar_wait(&bars->p_full, i & 1);
+            tc_fence_after();
+            const uint64_t so = boff(st * kTileBytes);
+            const uint32_t first = i == 0 ? 0u : 1u;
 #pragma unroll
-                for (int ks = 0; ks < kQ64 / 16; ++ks)
-                    umma_ts_w(tm_dv, tm_s + b * kQ64 + pt_col(ks), dDOmn + so + mnoff(ks), idesc_g, j | ks);
+            for (int ks = 0; ks < kTile / 16; ++ks)
+                umma_ts_w(kTmDV, kTmS + pk_col(ks), dDOmn + so + mnoff(ks), idesc_g, first | ks);
+        };
+        auto mma_dk = [&](int i) {
+            const int st = i % kKvStages;
+            mbar_wait(&bars->ds_full, i & 1);
+            tc_fence_after();
+            const uint64_t so = boff(st * kTileBytes);
+            const uint32_t first = i == 0 ? 0u : 1u;
 #pragma unroll
-                for (int ks = 0; ks < kQ64 / 16; ++ks)
-                    umma_ts_w(tm_dk, tm_dp + b * kQ64 + pt_col(ks), dQmn + so + mnoff(ks), idesc_g, j | ks);
-                umma_commit_w(&bars->qdo_empty[st]);
-                if (i == n_items) umma_commit_w(&bars->acc_done);
-            }
+            for (int ks = 0; ks < kTile / 16; ++ks)
+                umma_ts_w(kTmDK, kTmDP + pk_col(ks), dQmn + so + mnoff(ks), idesc_g, first | ks);
+            umma_commit_w(&bars->qdo_empty[st]);
+        };
+        mma_s(0);
+        mma_dp(0);
+        for (int i = 0; i < n_items; ++i) {
+            const bool tr8 = i == 8 && lane == 0;
+            if (tr8) trace_mark(p.tr, 12);
+            mma_dv(i);
+            if (tr8) trace_mark(p.tr, 13);
+            if (i + 1 < n_items) mma_s(i + 1);   // rewrites S^T after dV(i) read P^T(i)
+            if (tr8) trace_mark(p.tr, 14);
+            mma_dk(i);
+            if (tr8) trace_mark(p.tr, 15);
+            if (i + 1 < n_items) mma_dp(i + 1);  // rewrites dP^T after dK(i) read dS^T(i)
+            if (tr8) trace_mark(p.tr, 16);
         }
+        umma_commit_w(&bars->acc_done);
     } else if (warp >= 4) {
-        // Two warpgroups: warps 4..7 take query columns [0, 32) of each item, warps 8..11
-        // columns [32, 64); warp w reads TMEM lanes 32*(w%4).. (its key rows).
-        const int quarter = warp & 3, half = (warp - 4) >> 2;
+        // Warpgroup w: query columns [64w, 64w+64) of every item; thread = key row (TMEM lane).
+        const int quarter = warp & 3, wg = (warp - 4) >> 2;
         const int kr = quarter * 32 + lane;  // key row of the block
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         const float sl2 = g.scale * kLog2e;
         const bool key_ok = kr < n_valid;
         const bool page_full = n_valid == kTile;
-        const int key_abs = u.key0 + kr;  // chunk-relative key index (in-chunk blocks)
-        const uint32_t ld_base = smem_u32(smem + kKvLD) + half * 128;
+        const uint32_t ld_base = smem_u32(smem + kKvLD) + wg * 256;
+        const uint32_t tS = kTmS + wg * 64 + lane_off, tDP = kTmDP + wg * 64 + lane_off;
         ItemIter it;
         it.init(u, qps, g_kv, g.group);
         for (int i = 0; i < n_items; ++i, it.next(u, qps, g_kv, g.group)) {
-            const int st = i % kKvStages, b = i & 1;
-            const int q0 = it.qt64 * kQ64 + half * 32;
-            const uint32_t lrow = ld_base + st * 512, drow = lrow + 256;
+            const int st = i % kKvStages;
+            const uint32_t lrow = ld_base + st * 1024, drow = lrow + 512;
+            // visible iff query column c >= lim (causal diagonal: key row <= query row)
+            const int lim = key_ok ? (it.diag ? kr - wg * 64 : 0) : 1 << 20;
+            const bool masked = it.diag || !page_full;
             mbar_wait(&bars->qdo_full[st], (i / kKvStages) & 1);  // makes the bulk-copied L / D visible
-            mbar_wait(&bars->sdp_full[b], (i >> 1) & 1);
+            // ---- P^T = exp2(S^T sl2 - L): computed as soon as S^T lands, packed in place
+            const bool tr = (i == 8 || i == 9) && threadIdx.x == 128;
+            mbar_wait(&bars->s_full, i & 1);
             if (i == 0 && threadIdx.x == 128) trace_mark(p.tr, 3);
+            if (tr) trace_mark(p.tr, i == 8 ? 8 : 17);
             tc_fence_after();
-            uint32_t s[32], dp[32];
-            tmem_ld32(tm_s + b * kQ64 + half * 32 + lane_off, s);
-            tmem_ld32(tm_dp + b * kQ64 + half * 32 + lane_off, dp);
-            tmem_wait_ld();
-            uint32_t pp[16], dd[16];
-            if (it.diag || !page_full) {  // causal diagonal / partially filled page: per-element mask
-                const int lim = key_ok ? (it.diag ? key_abs - q0 : 0) : 1 << 20;  // visible iff column >= lim
-                pds_half<true>(s, dp, lrow, drow, sl2, lim, pp, dd);
-            } else {
-                pds_half<false>(s, dp, lrow, drow, sl2, 0, pp, dd);
+            float pr[64];
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2) {
+                uint32_t sv[32];
+                tmem_ld32(tS + c2 * 32, sv);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c4 = 0; c4 < 8; ++c4) {
+                    const float4 l4 = lds128(lrow + (c2 * 32 + c4 * 4) * 4);
+                    pr[c2 * 32 + 4 * c4 + 0] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 0]), sl2, -l4.x));
+                    pr[c2 * 32 + 4 * c4 + 1] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 1]), sl2, -l4.y));
+                    pr[c2 * 32 + 4 * c4 + 2] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 2]), sl2, -l4.z));
+                    pr[c2 * 32 + 4 * c4 + 3] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 3]), sl2, -l4.w));
+                }
             }
-            // packed into the first 16 of this half's own 32 S / dP columns (the other half may
-            // still be reading its S columns): K steps 0,1 at cols 0..15, K steps 2,3 at 32..47
-            tmem_st16(tm_s + b * kQ64 + half * 32 + lane_off, pp);
-            tmem_st16(tm_dp + b * kQ64 + half * 32 + lane_off, dd);
+            if (masked) {
+#pragma unroll
+                for (int c = 0; c < 64; ++c) pr[c] = (c >= lim) ? pr[c] : 0.f;
+            }
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int u2 = 0; u2 < 16; ++u2) pk[u2] = pack_bf16(pr[c2 * 32 + 2 * u2], pr[c2 * 32 + 2 * u2 + 1]);
+                tmem_st16(tS + c2 * 16, pk);  // below the columns still to be read
+            }
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&bars->pds_full[b]);
+            mbar_arrive(&bars->p_full);
+            if (tr && i == 8) trace_mark(p.tr, 9);
+            // ---- dS^T = P^T (dP^T - D), packed in place of dP^T
+            mbar_wait(&bars->dp_full, i & 1);
+            if (tr && i == 8) trace_mark(p.tr, 10);
+            tc_fence_after();
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2) {
+                uint32_t dv[32];
+                tmem_ld32(tDP + c2 * 32, dv);
+                tmem_wait_ld();
+                uint32_t pk[16];
+#pragma unroll
+                for (int c4 = 0; c4 < 8; ++c4) {
+                    const float4 d4 = lds128(drow + (c2 * 32 + c4 * 4) * 4);
+                    const int c = c2 * 32 + 4 * c4;
+                    pk[2 * c4] = pack_bf16(pr[c] * (__uint_as_float(dv[4 * c4]) - d4.x),
+                                           pr[c + 1] * (__uint_as_float(dv[4 * c4 + 1]) - d4.y));
+                    pk[2 * c4 + 1] = pack_bf16(pr[c + 2] * (__uint_as_float(dv[4 * c4 + 2]) - d4.z),
+                                               pr[c + 3] * (__uint_as_float(dv[4 * c4 + 3]) - d4.w));
+                }
+                tmem_st16(tDP + c2 * 16, pk);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&bars->ds_full);
+            if (tr && i == 8) trace_mark(p.tr, 11);
         }
-        // ---- epilogue: dK (scaled) and dV leave TMEM as eight [128 x 32] fp32 slices staged in
-        // the now idle Q / dO ring (128 KB); the TMA unit then adds them into the fp32 gradient
-        // page in L2 (past pages: one owner per (page, kv head, block) in this launch, so the
-        // result is deterministic) or stores them to dk_cur / dv_cur (the chunk's own keys).
-        // Rows beyond the page's fill level carry zeros (the reference leaves those slots at 0).
         if (threadIdx.x == 128) trace_mark(p.tr, 4);
         mbar_wait(&bars->acc_done, 0);
         if (threadIdx.x == 128) trace_mark(p.tr, 5);
@@ -743,9 +777,9 @@ __global__ void __launch_bounds__(384, 1)
         // in this launch, so the result is deterministic) or stores them to dk_cur / dv_cur (the
         // chunk's own keys). Rows beyond the page's fill level carry zeros (the reference leaves
         // those slots at 0).
-        uint8_t* stage = smem + kKvQ + half * 4 * kSliceBytes;
-        const uint32_t acc = half ? tm_dv : tm_dk;
-        const float sc = key_ok ? (half ? 1.f : g.scale) : 0.f;
+        uint8_t* stage = smem + kKvQ + wg * 4 * kSliceBytes;
+        const uint32_t acc = wg ? kTmDV : kTmDK;
+        const float sc = key_ok ? (wg ? 1.f : g.scale) : 0.f;
 #pragma unroll 1
         for (int c = 0; c < kHd / 32; ++c) stage_slice(acc + c * 32 + lane_off, stage + c * kSliceBytes, kr, sc);
         fence_proxy_async_smem();
@@ -771,7 +805,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 3) tmem_dealloc<512>(tmem);
+    if (warp == 3) tmem_dealloc<512>(0);
 }
 
 }  // namespace
@@ -813,8 +847,6 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     }
     const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, kHd);
     const CUtensorMap tdo = map_rows_heads(dout, g.C, g.Hq, kHd);
-    const CUtensorMap tq64 = map_rows_heads(q, g.C, g.Hq, kHd, kQ64);
-    const CUtensorMap tdo64 = map_rows_heads(dout, g.C, g.Hq, kHd, kQ64);
     const CUtensorMap tkc = map_rows_heads(k_cur, g.C, g.Hkv, kHd);
     const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, kHd);
     BwdParams p{g, sel_off, sel_ids, d_kvslot_layer, d_gslot_layer, gkpool, gvpool, w.Dt, w.Lt, w.mask, w.uni,
@@ -832,11 +864,11 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         const int max_union = std::min(nnz, n_pages);
         const int units = g.C / kTile + max_union * (g.P / kTile);
         const size_t n_ctas = static_cast<size_t>(units) * g.Hkv;
-        p.tr = trace_begin("dkdv", n_ctas, 8);
+        p.tr = trace_begin("dkdv", n_ctas, 20);
         const CUtensorMap tdkc = map_rows_heads_f32(dk_cur, g.C, g.Hkv, kHd);
         const CUtensorMap tdvc = map_rows_heads_f32(dv_cur, g.C, g.Hkv, kHd);
         attn_bwd_dkdv_kernel<<<dim3(units, g.Hkv), 384, kKvSmem, st>>>(
-            tq64, tdo64, tkc, tvc, maps.kpool, maps.vpool, maps.gkpool, maps.gvpool, tdkc, tdvc, p);
+            tq, tdo, tkc, tvc, maps.kpool, maps.vpool, maps.gkpool, maps.gvpool, tdkc, tdvc, p);
         check_launch("attn_bwd_dkdv_kernel");
         trace_end(p.tr, n_ctas, st);
     }

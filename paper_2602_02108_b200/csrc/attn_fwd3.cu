@@ -26,16 +26,22 @@ using namespace tc;
 
 namespace {
 
-constexpr int kKSt = 3, kVSt = 2;
+constexpr int kKSt = 3, kVSt = 3;  // V stage 2 aliases the Q staging tile (free once Q is in TMEM)
 constexpr int kF3Q = 0;
 constexpr int kF3K = kF3Q + kTileBytes;
-constexpr int kF3V = kF3K + kKSt * kTileBytes;
-constexpr int kF3Red = kF3V + kVSt * kTileBytes;   // [3][2 groups][128 rows] fp32: maxima by block parity, sums
-constexpr int kF3Bar = kF3Red + 3 * 2 * 128 * 4;
+constexpr int kF3V = kF3K + kKSt * kTileBytes;     // V stages 0, 1 (stage 2 = kF3Q)
+constexpr int kF3Red = kF3V + 2 * kTileBytes;   // [3][2 groups][128 rows] fp32: maxima by block parity, sums
+constexpr int kF3Nv = kF3Red + 3 * 2 * 128 * 4;   // uint8 valid-key counts of the past blocks
+constexpr int kF3NvCap = 8192;
+constexpr int kF3Bar = kF3Nv + kF3NvCap;
 constexpr int kF3Smem = kF3Bar + 256 + 1024;
 static_assert(kF3Smem <= 232448, "dynamic shared memory above the 227 KB opt-in limit");
 constexpr uint32_t kTmQ = 0, kTmS = 64, kTmO = 320;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef OOMB_FWD_POLY_EVERY
+#define OOMB_FWD_POLY_EVERY 0  // measured: the forward is not MUFU-bound; keep every exp2 on MUFU
+#endif
+constexpr int kPolyEvery = OOMB_FWD_POLY_EVERY;  // 1 in kPolyEvery element pairs use ex2_poly
 
 struct F3Bars {
     uint64_t q_full, q_tmem;
@@ -52,6 +58,7 @@ struct F3Params {
     __nv_bfloat16* out;
     float* lse;
     int* err;
+    CtaTrace tr;
 };
 
 // K step ks (16 keys) of the packed P operand: keys [64w, 64w+64) of group w sit in the first
@@ -121,6 +128,10 @@ __global__ void __launch_bounds__(384, 1)
     uint8_t* sK = smem + kF3K;
     uint8_t* sV = smem + kF3V;
 
+    if (warp == 3 && lane == 0 && p.tr.buf && nb > 10) {  // observer: when does s_full of block 9 complete?
+        for (int j = 1; j <= 9; j += 2) mbar_wait(&bars->s_full[1], (j >> 1) & 1);
+        trace_mark(p.tr, 6);
+    }
     if (warp == 0 || warp == 2) {
         if (lane == 0) {  // w0: Q + K, w2: V
             const bool is_k = warp == 0;
@@ -137,8 +148,9 @@ __global__ void __launch_bounds__(384, 1)
             for (int j = 0; j < nb; ++j) {
                 const int st = j % nst;
                 if (j >= nst) mbar_wait(&empty[st], ((j / nst) - 1) & 1);
+                if (!is_k && j == 2) mbar_wait(&bars->q_tmem, 0);  // V stage 2 reuses the Q staging tile
                 mbar_expect_tx(&full[st], kTileBytes);
-                uint8_t* dst = base + st * kTileBytes;
+                uint8_t* dst = (!is_k && st == 2) ? sQ : base + st * kTileBytes;
                 if (j < n_past) {
                     const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, j, kvh, is_k ? p.err : nullptr);
                     for (int r = 0; r < 2; ++r) tma_load_2d(dst + r * kRegion, mp, &full[st], r * 64, b.row);
@@ -153,11 +165,13 @@ __global__ void __launch_bounds__(384, 1)
         constexpr uint32_t idesc_o = make_idesc_bf16(kTile, kHd, 0, 1);    // [128 q] x [hd], K = keys
         const uint64_t dK = sdesc_k(smem_u32(sK));
         const uint64_t dVmn = sdesc_mn(smem_u32(sV), kRegion);
+        const uint64_t dV2mn = sdesc_mn(smem_u32(sQ), kRegion);  // V stage 2 (the Q staging tile)
         mbar_wait(&bars->q_tmem, 0);
         tc_fence_after();
         auto mma_s = [&](int j) {
             const int st = j % kKSt, b = j & 1;
             mbar_wait(&bars->k_full[st], (j / kKSt) & 1);
+            if (j == 9 && lane == 0) trace_mark(p.tr, 13);
             tc_fence_after();
             const uint64_t so = boff(st * kTileBytes);
 #pragma unroll
@@ -169,20 +183,26 @@ __global__ void __launch_bounds__(384, 1)
         auto mma_pv = [&](int j) {
             const int st = j % kVSt, b = j & 1;
             mbar_wait(&bars->p_full[b], (j >> 1) & 1);
+            if (j == 8 && lane == 0) trace_mark(p.tr, 14);
             mbar_wait(&bars->v_full[st], (j / kVSt) & 1);
+            if (j == 8 && lane == 0) trace_mark(p.tr, 15);
             tc_fence_after();
-            const uint64_t so = boff(st * kTileBytes);
+            const uint64_t vbase = st == 2 ? dV2mn : dVmn + boff(st * kTileBytes);
             const uint32_t first = j == 0 ? 0u : 1u;
 #pragma unroll
             for (int ks = 0; ks < kTile / 16; ++ks)
-                umma_ts_w(kTmO, kTmS + b * 128 + p_col(ks), dVmn + so + mnoff(ks), idesc_o, first | ks);
+                umma_ts_w(kTmO, kTmS + b * 128 + p_col(ks), vbase + mnoff(ks), idesc_o, first | ks);
             umma_commit_w(&bars->pv_done);
             umma_commit_w(&bars->v_empty[st]);
         };
         mma_s(0);
         for (int j = 0; j < nb; ++j) {
+            const bool tr = j == 8 && lane == 0;
+            if (tr) trace_mark(p.tr, 10);
             if (j + 1 < nb) mma_s(j + 1);  // S(j+1) rewrites the buffer PV(j-1) read: issued after it
+            if (tr) trace_mark(p.tr, 11);
             mma_pv(j);
+            if (tr) trace_mark(p.tr, 12);
         }
     } else if (warp >= 4) {
         const int quarter = warp & 3, wg = (warp - 4) >> 2;
@@ -195,23 +215,24 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_before();
         mbar_arrive(&bars->q_tmem);
         const float sl2 = g.scale * kLog2e;
-        const int bpp = g.P / kTile;
+        uint8_t* nvt = smem + kF3Nv;
+        stage_past_valid(g, p.sel_ids, sel_begin, n_past, nvt, kF3NvCap, threadIdx.x - 128, 256);
+        named_bar_sync(3, 256);
         float m = -INFINITY;  // running row max (log2 units) that O and l are relative to
         float l = 0.f;        // this group's partial row sum
-        int pid_next = n_past > 0 ? p.sel_ids[sel_begin] : 0;
         for (int j = 0; j < nb; ++j) {
             const int b = j & 1;
-            const int pid = pid_next;
-            if (j + 1 < n_past) pid_next = p.sel_ids[sel_begin + (j + 1) / bpp];
             int lim;  // keep key columns c <= lim of this group's 64
             if (j < n_past) {
-                const int64_t nv = g.filled - static_cast<int64_t>(pid) * g.P - static_cast<int64_t>(j % bpp) * kTile;
-                lim = static_cast<int>(nv < 0 ? 0 : (nv > kTile ? kTile : nv)) - 1 - wg * 64;
+                lim = past_valid(g, p.sel_ids, sel_begin, nvt, kF3NvCap, j) - 1 - wg * 64;
             } else {
                 lim = ((j - n_past == qt) ? r : kTile - 1) - wg * 64;
             }
             const uint32_t tS = kTmS + b * 128 + wg * 64 + lane_off;
+            if (j == 9 && threadIdx.x == 128) trace_mark(p.tr, 7);
             mbar_wait(&bars->s_full[b], (j >> 1) & 1);
+            const bool tr = (j == 8 || j == 9) && threadIdx.x == 128;
+            if (tr) trace_mark(p.tr, j == 8 ? 1 : 5);
             tc_fence_after();
             uint32_t sr[64];
             tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
@@ -231,7 +252,9 @@ __global__ void __launch_bounds__(384, 1)
                                     fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
             // exchange the partial maxima of the two groups (double-buffered by block parity)
             red[(b * 2 + wg) * 128 + r] = mxg;
+            if (tr && j == 8) trace_mark(p.tr, 2);
             named_bar_sync(2, 256);
+            if (tr && j == 8) trace_mark(p.tr, 3);
             const float mx = fmaxf(mxg, red[(b * 2 + (wg ^ 1)) * 128 + r]) * sl2;
             const float m_new = fmaxf(m, mx);
             bool rescale = false;
@@ -243,13 +266,25 @@ __global__ void __launch_bounds__(384, 1)
             }
             const float m_use = (m == -INFINITY) ? 0.f : m;
             float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#ifdef OOMB_EXP_NOSOFTMAX
+            if (true) {
+                uint32_t pk[16];
+                for (int u = 0; u < 16; ++u) pk[u] = sr[2 * u];
+                tmem_st16(tS, pk);
+                tmem_st16(tS + 16, pk);
+            } else
+#endif
 #pragma unroll
             for (int c2 = 0; c2 < 2; ++c2) {
                 uint32_t pk[16];
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
-                    const float e0 = ex2(fmaf(__uint_as_float(sr[c2 * 32 + 2 * u]), sl2, -m_use));
-                    const float e1 = ex2(fmaf(__uint_as_float(sr[c2 * 32 + 2 * u + 1]), sl2, -m_use));
+                    // a share of the exponentials runs on the FMA pipe (MUFU is as busy as the tensor core)
+                    const float x0 = fmaf(__uint_as_float(sr[c2 * 32 + 2 * u]), sl2, -m_use);
+                    const float x1 = fmaf(__uint_as_float(sr[c2 * 32 + 2 * u + 1]), sl2, -m_use);
+                    const bool poly = kPolyEvery > 0 && (u % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1;
+                    const float e0 = poly ? ex2_poly(x0) : ex2(x0);
+                    const float e1 = poly ? ex2_poly(x1) : ex2(x1);
                     rs8[(2 * u) & 7] += e0;
                     rs8[(2 * u + 1) & 7] += e1;
                     pk[u] = pack_bf16(e0, e1);
@@ -277,6 +312,7 @@ __global__ void __launch_bounds__(384, 1)
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive(&bars->p_full[b]);
+            if (tr && j == 8) trace_mark(p.tr, 4);
         }
         // ---- epilogue: l = l_0 + l_1, O / l -> bf16 (this group's 64 columns), lse (natural log)
         red[(4 + wg) * 128 + r] = l;  // own buffer: the other group may still read its last maxima
@@ -318,9 +354,12 @@ void launch_attn_fwd_tc3(const AttnGeom& g, const TcPoolMaps& maps, const void* 
     const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, kHd);
     const CUtensorMap tkc = map_rows_heads(k_cur, g.C, g.Hkv, kHd);
     const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, kHd);
-    F3Params p{g, sel_off, sel_ids, d_kvslot_layer, static_cast<__nv_bfloat16*>(out), lse, d_err};
+    F3Params p{g, sel_off, sel_ids, d_kvslot_layer, static_cast<__nv_bfloat16*>(out), lse, d_err, CtaTrace{}};
+    const size_t n_ctas = static_cast<size_t>(g.Hq) * (g.C / kTile);
+    p.tr = trace_begin("fwd", n_ctas, 16);
     attn_fwd_tc3_kernel<<<dim3(g.Hq, g.C / kTile), 384, kF3Smem, st>>>(tq, tkc, tvc, maps.kpool, maps.vpool, p);
     check_launch("attn_fwd_tc3_kernel");
+    trace_end(p.tr, n_ctas, st);
 }
 
 }  // namespace oomb

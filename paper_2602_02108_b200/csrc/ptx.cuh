@@ -277,6 +277,21 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// exp2 on the FMA pipe (x <= 0 or -inf): round-to-nearest split x = i + f, f in [-1/2, 1/2],
+// degree-3 minimax polynomial for 2^f (max relative error 8.4e-5, below bf16 rounding), and
+// 2^i added into the exponent field. Used for a fraction of the softmax elements so the MUFU
+// unit (16 exp2 / clk / SM) is not the only exponential pipe (the tensor core needs one exp2
+// per 8 FMA of S = Q K^T at head_dim 128).
+__device__ __forceinline__ float ex2_poly(float x) {
+    const float xc = fmaxf(x, -126.0f);
+    const float t = xc + 12582912.0f;  // 1.5 * 2^23: integer part lands in the low mantissa bits
+    const float f = xc - (t - 12582912.0f);
+    float p = fmaf(0.0553458875f, f, 0.24260599f);
+    p = fmaf(p, f, 0.69322751f);
+    p = fmaf(p, f, 0.999927776f);
+    const float r = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+    return x > -126.0f ? r : 0.0f;  // masked (-inf) and underflowing inputs give exactly 0
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);

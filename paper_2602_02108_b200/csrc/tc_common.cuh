@@ -128,5 +128,23 @@ __device__ __forceinline__ PastBlock past_block(const AttnGeom& g, const int32_t
     return b;
 }
 
+// Valid keys (0..128) of past key block j of a query page: partially filled pages are masked
+// (paged_kv.hpp:295-299). The softmax warps stage these counts into shared memory once per CTA
+// so the per-block path never waits on a global load of the selection ids.
+__device__ __forceinline__ int past_valid_global(const AttnGeom& g, const int32_t* sel_ids, int sel_begin, int j) {
+    const int bpp = g.P / kTile;
+    const int pid = sel_ids[sel_begin + j / bpp];
+    const int64_t nv = g.filled - static_cast<int64_t>(pid) * g.P - static_cast<int64_t>(j % bpp) * kTile;
+    return static_cast<int>(nv < 0 ? 0 : (nv > kTile ? kTile : nv));
+}
+__device__ __forceinline__ void stage_past_valid(const AttnGeom& g, const int32_t* sel_ids, int sel_begin,
+                                                 int n_past, uint8_t* tab, int cap, int tid, int nthr) {
+    for (int j = tid; j < n_past && j < cap; j += nthr) tab[j] = static_cast<uint8_t>(past_valid_global(g, sel_ids, sel_begin, j));
+}
+__device__ __forceinline__ int past_valid(const AttnGeom& g, const int32_t* sel_ids, int sel_begin, const uint8_t* tab,
+                                          int cap, int j) {
+    return j < cap ? tab[j] : past_valid_global(g, sel_ids, sel_begin, j);
+}
+
 }  // namespace tc
 }  // namespace oomb
