@@ -409,22 +409,27 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 // ===========================================================================
-// dK/dV kernel (key-major, one CTA per (key block, kv head))
+// dK/dV kernel (key-major, persistent)
 //
-// A CTA owns one 128-key block (a past page, or a block of the chunk's own keys) of one kv
-// head and loops over the work items that attend it: (128-row query tile, q-head of the
-// group) — the query pages that selected the page, or the chunk's tiles from the diagonal on.
+// A work unit is one 128-key block (a past page, or a block of the chunk's own keys) of one kv
+// head; its items are the (128-row query tile, q-head of the group) pairs that attend it — the
+// query pages that selected the page, or the chunk's tiles from the diagonal on. One CTA per SM
+// takes units from an atomic counter (the chunk's own blocks, the longest, first) and overlaps
+// consecutive units: the next unit's K/V and first Q/dO tiles load, and its first S^T/dP^T MMAs
+// run, while the previous unit finishes and drains its accumulators.
 // Per item:
-//   S^T = K Q^T, dP^T = V dO^T   SS-MMAs with N = 128 queries (full rate: the smem operand
-//                                port carries 8 KB per 64 clk);
+//   S^T = K Q^T, dP^T = V dO^T   SS-MMAs with N = 128 queries (full rate);
 //   P^T = exp2(S^T scale log2e - L)  written back IN PLACE of S^T as packed bf16 as soon as
-//                                S^T lands (the exp work overlaps dK of the previous item and
-//                                dP^T of this one), kept in registers for
+//                                S^T lands, kept in registers for
 //   dS^T = P^T (dP^T - D)        written back in place of dP^T;
-//   dV += P^T dO, dK += dS^T Q   TS-MMAs (A from TMEM), accumulated over all items in TMEM.
+//   dV += P^T dO, dK += dS^T Q   TS-MMAs (A from TMEM), accumulated over the unit's items.
 // Issue order: S(0) dP(0) | dV(0) S(1) dK(0) dP(1) | dV(1) S(2) dK(1) dP(2) | ... — each MMA
 // that rewrites S^T / dP^T columns is issued after the MMA that read them, and tcgen05.mma
 // operations of one thread execute in issue order.
+// Epilogue of a unit: the softmax warps pull dK (scaled) / dV out of TMEM into registers, free
+// the accumulators, then stage [128 x 32] fp32 slices in smem for the TMA unit to ADD into the
+// fp32 gradient page in L2 (past pages: one owner per (page, kv head, block) per launch, so the
+// result is deterministic) or STORE into dk_cur / dv_cur (the chunk's own keys).
 // TMEM (all 512 columns, base 0): S^T [0,128) dP^T [128,256) dK [256,384) dV [384,512);
 // softmax warpgroup w owns query columns [64w, 64w+64) and packs into its own first 32.
 // ===========================================================================
@@ -433,33 +438,38 @@ constexpr int kKvK = 0;
 constexpr int kKvV = kKvK + kTileBytes;
 constexpr int kKvQ = kKvV + kTileBytes;                  // kKvStages stages of [128 x 128]
 constexpr int kKvDO = kKvQ + kKvStages * kTileBytes;     // kKvStages stages
-constexpr int kKvQps = kKvDO + kKvStages * kTileBytes;   // query-page list (<= 64 ints)
-constexpr int kKvLD = kKvQps + 256;                      // kKvStages stages of {L[128], D[128]} fp32 (TMA bulk)
-constexpr int kKvBar = kKvLD + kKvStages * 1024;
-constexpr int kKvSmem = kKvBar + 256 + 1024;
+constexpr int kKvStage = kKvDO + kKvStages * kTileBytes; // epilogue: one [128 x 32] fp32 slice per warpgroup
+constexpr int kKvLD = kKvStage + 2 * kSliceBytes;        // kKvStages stages of {L[128], D[128]} fp32 (TMA bulk)
+constexpr int kKvDesc = kKvLD + kKvStages * 1024;        // 2 unit descriptors
+constexpr int kKvBar = kKvDesc + 256;
+constexpr int kKvSmem = kKvBar + 256;                    // the dynamic smem base is 1024-aligned (checked)
 static_assert(kKvSmem <= 232448, "dynamic shared memory above the 227 KB opt-in limit");
-static_assert(kKvStages * 2 * kTileBytes >= 8 * kSliceBytes, "epilogue staging reuses the Q / dO ring");
 constexpr uint32_t kTmS = 0, kTmDP = 128, kTmDK = 256, kTmDV = 384;
 
 struct KvBars {
-    uint64_t kv_full;
+    uint64_t unit_full[2], unit_empty[2];
+    uint64_t kv_full, kv_empty;
     uint64_t qdo_full[kKvStages], qdo_empty[kKvStages];
     uint64_t s_full, dp_full, p_full, ds_full;
-    uint64_t acc_done;
+    uint64_t acc_done, acc_free;
     uint32_t tmem_base;
 };
 
-// Work unit of a dK/dV CTA: in-chunk key block b, or past page block (union index, sub).
+// A work unit as the scheduler publishes it to the MMA and softmax warps.
 struct KvUnit {
-    bool valid;
-    bool past;
-    int key0;       // first key index of the block (chunk-relative for in-chunk, page-relative for past)
-    int pid;
-    int sub;
+    int valid;
+    int past;
+    int key0;      // first key of the block (chunk-relative for in-chunk, page-relative for past)
     int n_items;
-    int n_qps;      // past: number of query pages in the list
-    int tiles_per_qp;
+    int n_qps;     // past: number of query pages in the list
+    int g_kv;
+    int kv_row;    // pool tensor-map row of the K/V block (past)
+    int g_row;     // grad-pool tensor-map row (past)
+    int n_valid;   // valid keys of the block
+    int pad;
+    uint8_t qps[64];  // past: the query pages that selected the page, ascending
 };
+static_assert(sizeof(KvUnit) <= 128, "unit descriptor");
 
 // K step ks (16 queries) of a packed P^T / dS^T operand: queries [64w, 64w+64) of warpgroup w
 // sit in the first 32 of its own 64 columns.
@@ -471,35 +481,77 @@ __host__ __device__ constexpr uint32_t pk_col(int ks) { return (ks >> 2) * 64 + 
 struct ItemIter {
     int h, qt, qpi, tile;  // q-head, 128-row query tile, index in the query-page list, tile in the page
     bool diag;
-    __device__ __forceinline__ void init(const KvUnit& u, const int* qps, int g_kv, int G) {
-        h = g_kv * G;
+    __device__ __forceinline__ void init(const KvUnit& u, int G, int tpq) {
+        h = u.g_kv * G;
         qpi = 0;
         tile = 0;
         if (u.past) {
-            qt = qps[0] * u.tiles_per_qp;
+            qt = u.qps[0] * tpq;
             diag = false;
         } else {
             qt = u.key0 / kTile;
             diag = true;
         }
     }
-    __device__ __forceinline__ void next(const KvUnit& u, const int* qps, int g_kv, int G) {
-        if (++h < (g_kv + 1) * G) return;
-        h = g_kv * G;
+    __device__ __forceinline__ void next(const KvUnit& u, int G, int tpq) {
+        if (++h < (u.g_kv + 1) * G) return;
+        h = u.g_kv * G;
         if (!u.past) {
             ++qt;
             diag = false;
             return;
         }
-        if (++tile == u.tiles_per_qp) {
+        if (++tile == tpq) {
             tile = 0;
             ++qpi;
-            if (qpi < u.n_qps) qt = qps[qpi] * u.tiles_per_qp;
+            if (qpi < u.n_qps) qt = u.qps[qpi] * tpq;
         } else {
             ++qt;
         }
     }
 };
+
+// Decode work index w (units of the chunk's own blocks first, then past page blocks; kv head
+// fastest) into a unit descriptor.
+__device__ void decode_unit(const BwdParams& p, int w, KvUnit& u) {
+    const AttnGeom& g = p.g;
+    const int n_chunk_blocks = g.C / kTile, bpp = g.P / kTile;
+    const int n_units = (n_chunk_blocks + *p.n_uni * bpp) * g.Hkv;
+    u.valid = w < n_units;
+    if (!u.valid) return;
+    const int unit = w / g.Hkv;
+    u.g_kv = w % g.Hkv;
+    u.n_valid = kTile;
+    if (unit < n_chunk_blocks) {
+        u.past = 0;
+        u.key0 = unit * kTile;
+        u.n_items = (n_chunk_blocks - unit) * g.group;
+        u.n_qps = 0;
+        return;
+    }
+    const int pu = unit - n_chunk_blocks;
+    const int pid = p.uni[pu / bpp];
+    const int sub = pu % bpp;
+    u.past = 1;
+    u.key0 = sub * kTile;
+    const uint64_t m = p.mask[pid];
+    int k = 0;
+    for (int qp = 0; qp < 64; ++qp)
+        if (m & (1ull << qp)) u.qps[k++] = static_cast<uint8_t>(qp);
+    u.n_qps = k;
+    u.n_items = k * bpp * g.group;
+    const int kv_slot = p.kvslot[pid], g_slot = p.gslot[pid];
+    const int64_t nv = g.filled - static_cast<int64_t>(pid) * g.P - u.key0;
+    u.n_valid = static_cast<int>(nv < 0 ? 0 : (nv > kTile ? kTile : nv));
+    if (kv_slot < 0 || g_slot < 0) {  // not resident: report, and do no work for it
+        atomicOr(p.err, DERR_NOT_RESIDENT);
+        u.n_items = 0;
+        u.kv_row = u.g_row = 0;
+        return;
+    }
+    u.kv_row = (kv_slot * g.Hkv + u.g_kv) * g.P + u.key0;
+    u.g_row = (g_slot * g.Hkv + u.g_kv) * g.P + u.key0;
+}
 
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
@@ -507,66 +559,21 @@ __global__ void __launch_bounds__(384, 1)
                          const __grid_constant__ CUtensorMap tm_kp, const __grid_constant__ CUtensorMap tm_vp,
                          const __grid_constant__ CUtensorMap tm_gk, const __grid_constant__ CUtensorMap tm_gv,
                          const __grid_constant__ CUtensorMap tm_dkc, const __grid_constant__ CUtensorMap tm_dvc,
-                         BwdParams p) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+                         BwdParams p, int* work_counter) {
+    extern __shared__ __align__(1024) uint8_t smem[];
     KvBars* bars = reinterpret_cast<KvBars*>(smem + kKvBar);
-    int* qps = reinterpret_cast<int*>(smem + kKvQps);
+    KvUnit* desc = reinterpret_cast<KvUnit*>(smem + kKvDesc);
     const AttnGeom& g = p.g;
-    const int g_kv = blockIdx.y;
-    const int n_chunk_blocks = g.C / kTile;
-    const int bpp = g.P / kTile;
+    const int tpq = g.P / kTile;
     const int warp = warp_id(), lane = lane_id();
-
-    // ---- decode the work unit (uniform across the CTA)
-    KvUnit u{};
-    u.tiles_per_qp = g.P / kTile;
-    if (static_cast<int>(blockIdx.x) < n_chunk_blocks) {
-        const int b = blockIdx.x;
-        u.valid = true;
-        u.past = false;
-        u.key0 = b * kTile;
-        u.n_items = (n_chunk_blocks - b) * g.group;
-    } else {
-        const int pu = blockIdx.x - n_chunk_blocks;
-        const int idx = pu / bpp;
-        u.valid = idx < *p.n_uni;
-        if (u.valid) {
-            u.past = true;
-            u.pid = p.uni[idx];
-            u.sub = pu % bpp;
-            u.key0 = u.sub * kTile;
-            const uint64_t m = p.mask[u.pid];
-            u.n_qps = __popcll(m);
-            u.n_items = u.n_qps * u.tiles_per_qp * g.group;
-            if (threadIdx.x == 0) {
-                int k = 0;
-                for (int qp = 0; qp < 64; ++qp)
-                    if (m & (1ull << qp)) qps[k++] = qp;
-            }
-        }
-    }
-    if (!u.valid) return;
     if (threadIdx.x == 0) {
-        trace_value(p.tr, 0, smid());
-        trace_mark(p.tr, 1);
-        trace_value(p.tr, 7, u.n_items);
-    }
-
-    int kv_slot = 0, g_slot = -1, n_valid = kTile;
-    if (u.past) {
-        kv_slot = p.kvslot[u.pid];
-        g_slot = p.gslot[u.pid];
-        const int64_t nv = g.filled - static_cast<int64_t>(u.pid) * g.P - u.key0;
-        n_valid = static_cast<int>(nv < 0 ? 0 : (nv > kTile ? kTile : nv));
-        if (kv_slot < 0 || g_slot < 0) {
-            if (threadIdx.x == 0) atomicOr(p.err, DERR_NOT_RESIDENT);
-            return;
+        if (smem_u32(smem) & 1023) __trap();  // SW128 operands and the smem budget need a 1 KB-aligned base
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bars->unit_full[i], 1);
+            mbar_init(&bars->unit_empty[i], 1 + 256);
         }
-    }
-
-    if (threadIdx.x == 0) {
         mbar_init(&bars->kv_full, 1);
+        mbar_init(&bars->kv_empty, 1);
         for (int i = 0; i < kKvStages; ++i) {
             mbar_init(&bars->qdo_full[i], 1);
             mbar_init(&bars->qdo_empty[i], 1);
@@ -576,6 +583,7 @@ __global__ void __launch_bounds__(384, 1)
         mbar_init(&bars->p_full, 256);
         mbar_init(&bars->ds_full, 256);
         mbar_init(&bars->acc_done, 1);
+        mbar_init(&bars->acc_free, 256);
         fence_barrier_init();
     }
     if (warp == 3) tmem_alloc<512>(&bars->tmem_base);
@@ -587,54 +595,57 @@ __global__ void __launch_bounds__(384, 1)
     uint8_t* sV = smem + kKvV;
     uint8_t* sQ = smem + kKvQ;
     uint8_t* sDO = smem + kKvDO;
-    const int n_items = u.n_items;
 
     if (warp == 0) {
-        if (lane == 0) {
-            mbar_expect_tx(&bars->kv_full, 2 * kTileBytes);
-            if (u.past) {
-                const int row = (kv_slot * g.Hkv + g_kv) * g.P + u.key0;
+        if (lane == 0) {  // scheduler + TMA producer
+            int gi = 0;
+            for (int un = 0;; ++un) {
+                const int k = un & 1;
+                if (un >= 2) mbar_wait(&bars->unit_empty[k], ((un >> 1) - 1) & 1);
+                KvUnit& u = desc[k];
+                decode_unit(p, atomicAdd(work_counter, 1), u);
+                mbar_arrive(&bars->unit_full[k]);  // release: the descriptor is visible to the waiters
+                if (!u.valid) break;
+                if (un >= 1) mbar_wait(&bars->kv_empty, (un - 1) & 1);  // the previous unit's last S / dP
+                mbar_expect_tx(&bars->kv_full, 2 * kTileBytes);
                 for (int r = 0; r < 2; ++r) {
-                    tma_load_2d(sK + r * kRegion, &tm_kp, &bars->kv_full, r * 64, row);
-                    tma_load_2d(sV + r * kRegion, &tm_vp, &bars->kv_full, r * 64, row);
+                    if (u.past) {
+                        tma_load_2d(sK + r * kRegion, &tm_kp, &bars->kv_full, r * 64, u.kv_row);
+                        tma_load_2d(sV + r * kRegion, &tm_vp, &bars->kv_full, r * 64, u.kv_row);
+                    } else {
+                        tma_load_3d(sK + r * kRegion, &tm_kc, &bars->kv_full, r * 64, u.g_kv, u.key0);
+                        tma_load_3d(sV + r * kRegion, &tm_vc, &bars->kv_full, r * 64, u.g_kv, u.key0);
+                    }
                 }
-            } else {
-                for (int r = 0; r < 2; ++r) {
-                    tma_load_3d(sK + r * kRegion, &tm_kc, &bars->kv_full, r * 64, g_kv, u.key0);
-                    tma_load_3d(sV + r * kRegion, &tm_vc, &bars->kv_full, r * 64, g_kv, u.key0);
-                }
-            }
-            ItemIter it;
-            it.init(u, qps, g_kv, g.group);
-            for (int i = 0; i < n_items; ++i, it.next(u, qps, g_kv, g.group)) {
-                const int st = i % kKvStages;
-                if (i >= kKvStages) mbar_wait(&bars->qdo_empty[st], ((i / kKvStages) - 1) & 1);
-                mbar_expect_tx(&bars->qdo_full[st], 2 * kTileBytes + 1024);
-                float* ld = reinterpret_cast<float*>(smem + kKvLD) + st * 256;
-                bulk_load(ld, p.Lt + static_cast<int64_t>(it.h) * g.C + it.qt * kTile, 512, &bars->qdo_full[st]);
-                bulk_load(ld + 128, p.Dt + static_cast<int64_t>(it.h) * g.C + it.qt * kTile, 512,
-                          &bars->qdo_full[st]);
-                for (int r = 0; r < 2; ++r) {
-                    tma_load_3d(sQ + st * kTileBytes + r * kRegion, &tm_q, &bars->qdo_full[st], r * 64, it.h,
-                                it.qt * kTile);
-                    tma_load_3d(sDO + st * kTileBytes + r * kRegion, &tm_do, &bars->qdo_full[st], r * 64, it.h,
-                                it.qt * kTile);
+                ItemIter it;
+                it.init(u, g.group, tpq);
+                for (int i = 0; i < u.n_items; ++i, ++gi, it.next(u, g.group, tpq)) {
+                    const int st = gi % kKvStages;
+                    if (gi >= kKvStages) mbar_wait(&bars->qdo_empty[st], ((gi / kKvStages) - 1) & 1);
+                    mbar_expect_tx(&bars->qdo_full[st], 2 * kTileBytes + 1024);
+                    float* ld = reinterpret_cast<float*>(smem + kKvLD) + st * 256;
+                    bulk_load(ld, p.Lt + static_cast<int64_t>(it.h) * g.C + it.qt * kTile, 512, &bars->qdo_full[st]);
+                    bulk_load(ld + 128, p.Dt + static_cast<int64_t>(it.h) * g.C + it.qt * kTile, 512,
+                              &bars->qdo_full[st]);
+                    for (int r = 0; r < 2; ++r) {
+                        tma_load_3d(sQ + st * kTileBytes + r * kRegion, &tm_q, &bars->qdo_full[st], r * 64, it.h,
+                                    it.qt * kTile);
+                        tma_load_3d(sDO + st * kTileBytes + r * kRegion, &tm_do, &bars->qdo_full[st], r * 64, it.h,
+                                    it.qt * kTile);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
-        // MMA warp (converged): S(0) dP(0) | dV(0) S(1) dK(0) dP(1) | dV(1) S(2) dK(1) dP(2) | ...
+        // MMA warp (converged).
         constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kTile, 0, 0);  // [128 keys] x [128 q], K = hd
         constexpr uint32_t idesc_g = make_idesc_bf16(kTile, kHd, 0, 1);    // [128 keys] x [hd], K = q
         const uint64_t dK = sdesc_k(smem_u32(sK)), dV = sdesc_k(smem_u32(sV));
         const uint64_t dQ = sdesc_k(smem_u32(sQ)), dDO = sdesc_k(smem_u32(sDO));
         const uint64_t dQmn = sdesc_mn(smem_u32(sQ), kRegion), dDOmn = sdesc_mn(smem_u32(sDO), kRegion);
-        mbar_wait(&bars->kv_full, 0);
-        if (lane == 0) trace_mark(p.tr, 2);
-        __syncwarp();
-        auto mma_s = [&](int i) {
-            const int st = i % kKvStages;
-            mbar_wait(&bars->qdo_full[st], (i / kKvStages) & 1);
+        auto mma_s = [&](int gi) {
+            const int st = gi % kKvStages;
+            mbar_wait(&bars->qdo_full[st], (gi / kKvStages) & 1);
             tc_fence_after();
             const uint64_t so = boff(st * kTileBytes);
 #pragma unroll
@@ -642,166 +653,188 @@ __global__ void __launch_bounds__(384, 1)
                 umma_ss_w(kTmS, dK + koff(ks, kRegion), dQ + so + koff(ks, kRegion), idesc_s, ks);
             umma_commit_w(&bars->s_full);
         };
-        auto mma_dp = [&](int i) {
-            const int st = i % kKvStages;
-            const uint64_t so = boff(st * kTileBytes);
+        auto mma_dp = [&](int gi) {
+            const uint64_t so = boff((gi % kKvStages) * kTileBytes);
 #pragma unroll
             for (int ks = 0; ks < kHd / 16; ++ks)
                 umma_ss_w(kTmDP, dV + koff(ks, kRegion), dDO + so + koff(ks, kRegion), idesc_s, ks);
             umma_commit_w(&bars->dp_full);
         };
-        auto mma_dv = [&](int i) {
-            const int st = i % kKvStages;
-            mbar_wait(&bars->p_full, i & 1);
+        auto mma_dv = [&](int gi, uint32_t first) {
+            mbar_wait(&bars->p_full, gi & 1);
             tc_fence_after();
-            const uint64_t so = boff(st * kTileBytes);
-            const uint32_t first = i == 0 ? 0u : 1u;
+            const uint64_t so = boff((gi % kKvStages) * kTileBytes);
 #pragma unroll
             for (int ks = 0; ks < kTile / 16; ++ks)
                 umma_ts_w(kTmDV, kTmS + pk_col(ks), dDOmn + so + mnoff(ks), idesc_g, first | ks);
         };
-        auto mma_dk = [&](int i) {
-            const int st = i % kKvStages;
-            mbar_wait(&bars->ds_full, i & 1);
+        auto mma_dk = [&](int gi, uint32_t first) {
+            const int st = gi % kKvStages;
+            mbar_wait(&bars->ds_full, gi & 1);
             tc_fence_after();
             const uint64_t so = boff(st * kTileBytes);
-            const uint32_t first = i == 0 ? 0u : 1u;
 #pragma unroll
             for (int ks = 0; ks < kTile / 16; ++ks)
                 umma_ts_w(kTmDK, kTmDP + pk_col(ks), dQmn + so + mnoff(ks), idesc_g, first | ks);
             umma_commit_w(&bars->qdo_empty[st]);
         };
-        mma_s(0);
-        mma_dp(0);
-        for (int i = 0; i < n_items; ++i) {
-            const bool tr8 = i == 8 && lane == 0;
-            if (tr8) trace_mark(p.tr, 12);
-            mma_dv(i);
-            if (tr8) trace_mark(p.tr, 13);
-            if (i + 1 < n_items) mma_s(i + 1);   // rewrites S^T after dV(i) read P^T(i)
-            if (tr8) trace_mark(p.tr, 14);
-            mma_dk(i);
-            if (tr8) trace_mark(p.tr, 15);
-            if (i + 1 < n_items) mma_dp(i + 1);  // rewrites dP^T after dK(i) read dS^T(i)
-            if (tr8) trace_mark(p.tr, 16);
+        int gi = 0;
+        for (int un = 0;; ++un) {
+            const int k = un & 1;
+            mbar_wait(&bars->unit_full[k], (un >> 1) & 1);
+            const KvUnit& u = desc[k];
+            if (!u.valid) break;
+            const int n = u.n_items;
+            mbar_wait(&bars->kv_full, un & 1);
+            if (n > 0) {
+                mma_s(gi);
+                mma_dp(gi);
+                if (n == 1) umma_commit_w(&bars->kv_empty);
+                for (int i = 0; i < n; ++i) {
+                    const uint32_t first = i == 0 ? 0u : 1u;
+                    if (i == 0 && un > 0) {  // the previous unit's dK / dV have left TMEM
+                        mbar_wait(&bars->acc_free, (un - 1) & 1);
+                        tc_fence_after();
+                    }
+                    mma_dv(gi + i, first);
+                    if (i + 1 < n) mma_s(gi + i + 1);   // rewrites S^T after dV(i) read P^T(i)
+                    mma_dk(gi + i, first);
+                    if (i + 1 < n) {
+                        mma_dp(gi + i + 1);  // rewrites dP^T after dK(i) read dS^T(i)
+                        if (i + 2 == n) umma_commit_w(&bars->kv_empty);  // last reader of K / V issued
+                    }
+                }
+            } else {
+                umma_commit_w(&bars->kv_empty);
+            }
+            umma_commit_w(&bars->acc_done);
+            gi += n;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->unit_empty[k]);
         }
-        umma_commit_w(&bars->acc_done);
     } else if (warp >= 4) {
         // Warpgroup w: query columns [64w, 64w+64) of every item; thread = key row (TMEM lane).
         const int quarter = warp & 3, wg = (warp - 4) >> 2;
         const int kr = quarter * 32 + lane;  // key row of the block
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         const float sl2 = g.scale * kLog2e;
-        const bool key_ok = kr < n_valid;
-        const bool page_full = n_valid == kTile;
-        const uint32_t ld_base = smem_u32(smem + kKvLD) + wg * 256;
         const uint32_t tS = kTmS + wg * 64 + lane_off, tDP = kTmDP + wg * 64 + lane_off;
-        ItemIter it;
-        it.init(u, qps, g_kv, g.group);
-        for (int i = 0; i < n_items; ++i, it.next(u, qps, g_kv, g.group)) {
-            const int st = i % kKvStages;
-            const uint32_t lrow = ld_base + st * 1024, drow = lrow + 512;
-            // visible iff query column c >= lim (causal diagonal: key row <= query row)
-            const int lim = key_ok ? (it.diag ? kr - wg * 64 : 0) : 1 << 20;
-            const bool masked = it.diag || !page_full;
-            mbar_wait(&bars->qdo_full[st], (i / kKvStages) & 1);  // makes the bulk-copied L / D visible
-            // ---- P^T = exp2(S^T sl2 - L): computed as soon as S^T lands, packed in place
-            const bool tr = (i == 8 || i == 9) && threadIdx.x == 128;
-            mbar_wait(&bars->s_full, i & 1);
-            if (i == 0 && threadIdx.x == 128) trace_mark(p.tr, 3);
-            if (tr) trace_mark(p.tr, i == 8 ? 8 : 17);
+        uint8_t* stage = smem + kKvStage + wg * kSliceBytes;
+        const bool issuer = (threadIdx.x & 127) == 0;  // first thread of the warpgroup issues its TMA
+        int gi = 0;
+        for (int un = 0;; ++un) {
+            const int k = un & 1;
+            mbar_wait(&bars->unit_full[k], (un >> 1) & 1);
+            const KvUnit& u = desc[k];
+            if (!u.valid) break;
+            const int n = u.n_items;
+            const bool past = u.past;
+            const int key0 = u.key0, g_row = u.g_row, g_kv = u.g_kv;
+            const bool key_ok = kr < u.n_valid;
+            const bool page_full = u.n_valid == kTile;
+            ItemIter it;
+            it.init(u, g.group, tpq);
+            for (int i = 0; i < n; ++i, it.next(u, g.group, tpq)) {
+                const int gj = gi + i;
+                const int st = gj % kKvStages;
+                const uint32_t lrow = smem_u32(smem + kKvLD) + st * 1024 + wg * 256, drow = lrow + 512;
+                // visible iff query column c >= lim (causal diagonal: key row <= query row)
+                const int lim = key_ok ? (it.diag ? kr - wg * 64 : 0) : 1 << 20;
+                const bool masked = it.diag || !page_full;
+                mbar_wait(&bars->qdo_full[st], (gj / kKvStages) & 1);  // makes the bulk-copied L / D visible
+                // ---- P^T = exp2(S^T sl2 - L): computed as soon as S^T lands, packed in place
+                mbar_wait(&bars->s_full, gj & 1);
+                tc_fence_after();
+                float pr[64];
+#pragma unroll
+                for (int c2 = 0; c2 < 2; ++c2) {
+                    uint32_t sv[32];
+                    tmem_ld32(tS + c2 * 32, sv);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c4 = 0; c4 < 8; ++c4) {
+                        const float4 l4 = lds128(lrow + (c2 * 32 + c4 * 4) * 4);
+                        pr[c2 * 32 + 4 * c4 + 0] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 0]), sl2, -l4.x));
+                        pr[c2 * 32 + 4 * c4 + 1] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 1]), sl2, -l4.y));
+                        pr[c2 * 32 + 4 * c4 + 2] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 2]), sl2, -l4.z));
+                        pr[c2 * 32 + 4 * c4 + 3] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 3]), sl2, -l4.w));
+                    }
+                }
+                if (masked) {
+#pragma unroll
+                    for (int c = 0; c < 64; ++c) pr[c] = (c >= lim) ? pr[c] : 0.f;
+                }
+#pragma unroll
+                for (int c2 = 0; c2 < 2; ++c2) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int u2 = 0; u2 < 16; ++u2) pk[u2] = pack_bf16(pr[c2 * 32 + 2 * u2], pr[c2 * 32 + 2 * u2 + 1]);
+                    tmem_st16(tS + c2 * 16, pk);  // below the columns still to be read
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(&bars->p_full);
+                // ---- dS^T = P^T (dP^T - D), packed in place of dP^T
+                mbar_wait(&bars->dp_full, gj & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int c2 = 0; c2 < 2; ++c2) {
+                    uint32_t dv[32];
+                    tmem_ld32(tDP + c2 * 32, dv);
+                    tmem_wait_ld();
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int c4 = 0; c4 < 8; ++c4) {
+                        const float4 d4 = lds128(drow + (c2 * 32 + c4 * 4) * 4);
+                        const int c = c2 * 32 + 4 * c4;
+                        pk[2 * c4] = pack_bf16(pr[c] * (__uint_as_float(dv[4 * c4]) - d4.x),
+                                               pr[c + 1] * (__uint_as_float(dv[4 * c4 + 1]) - d4.y));
+                        pk[2 * c4 + 1] = pack_bf16(pr[c + 2] * (__uint_as_float(dv[4 * c4 + 2]) - d4.z),
+                                                   pr[c + 3] * (__uint_as_float(dv[4 * c4 + 3]) - d4.w));
+                    }
+                    tmem_st16(tDP + c2 * 16, pk);
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(&bars->ds_full);
+            }
+            gi += n;
+            // ---- epilogue: pull this group's accumulator (dK scaled / dV) into registers, free TMEM
+            mbar_wait(&bars->acc_done, un & 1);
             tc_fence_after();
-            float pr[64];
+            const uint32_t acc = (wg ? kTmDV : kTmDK) + lane_off;
+            const float sc = key_ok ? (wg ? 1.f : g.scale) : 0.f;
+            uint32_t va[4][32];
 #pragma unroll
-            for (int c2 = 0; c2 < 2; ++c2) {
-                uint32_t sv[32];
-                tmem_ld32(tS + c2 * 32, sv);
-                tmem_wait_ld();
-#pragma unroll
-                for (int c4 = 0; c4 < 8; ++c4) {
-                    const float4 l4 = lds128(lrow + (c2 * 32 + c4 * 4) * 4);
-                    pr[c2 * 32 + 4 * c4 + 0] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 0]), sl2, -l4.x));
-                    pr[c2 * 32 + 4 * c4 + 1] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 1]), sl2, -l4.y));
-                    pr[c2 * 32 + 4 * c4 + 2] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 2]), sl2, -l4.z));
-                    pr[c2 * 32 + 4 * c4 + 3] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 3]), sl2, -l4.w));
-                }
-            }
-            if (masked) {
-#pragma unroll
-                for (int c = 0; c < 64; ++c) pr[c] = (c >= lim) ? pr[c] : 0.f;
-            }
-#pragma unroll
-            for (int c2 = 0; c2 < 2; ++c2) {
-                uint32_t pk[16];
-#pragma unroll
-                for (int u2 = 0; u2 < 16; ++u2) pk[u2] = pack_bf16(pr[c2 * 32 + 2 * u2], pr[c2 * 32 + 2 * u2 + 1]);
-                tmem_st16(tS + c2 * 16, pk);  // below the columns still to be read
-            }
-            tmem_wait_st();
+            for (int c = 0; c < 4; ++c) tmem_ld32(acc + c * 32, va[c]);
+            tmem_wait_ld();
             tc_fence_before();
-            mbar_arrive(&bars->p_full);
-            if (tr && i == 8) trace_mark(p.tr, 9);
-            // ---- dS^T = P^T (dP^T - D), packed in place of dP^T
-            mbar_wait(&bars->dp_full, i & 1);
-            if (tr && i == 8) trace_mark(p.tr, 10);
-            tc_fence_after();
+            mbar_arrive(&bars->acc_free);
+            mbar_arrive(&bars->unit_empty[k]);  // descriptor fields are in registers
+            if (n > 0) {
+                // ---- four [128 x 32] slices through this group's staging buffer into L2 / dk_cur / dv_cur
 #pragma unroll
-            for (int c2 = 0; c2 < 2; ++c2) {
-                uint32_t dv[32];
-                tmem_ld32(tDP + c2 * 32, dv);
-                tmem_wait_ld();
-                uint32_t pk[16];
+                for (int c = 0; c < 4; ++c) {
+                    if (issuer) bulk_wait_read0();     // the previous slice has left the staging buffer
+                    named_bar_sync(4 + wg, 128);
 #pragma unroll
-                for (int c4 = 0; c4 < 8; ++c4) {
-                    const float4 d4 = lds128(drow + (c2 * 32 + c4 * 4) * 4);
-                    const int c = c2 * 32 + 4 * c4;
-                    pk[2 * c4] = pack_bf16(pr[c] * (__uint_as_float(dv[4 * c4]) - d4.x),
-                                           pr[c + 1] * (__uint_as_float(dv[4 * c4 + 1]) - d4.y));
-                    pk[2 * c4 + 1] = pack_bf16(pr[c + 2] * (__uint_as_float(dv[4 * c4 + 2]) - d4.z),
-                                               pr[c + 3] * (__uint_as_float(dv[4 * c4 + 3]) - d4.w));
-                }
-                tmem_st16(tDP + c2 * 16, pk);
-            }
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&bars->ds_full);
-            if (tr && i == 8) trace_mark(p.tr, 11);
-        }
-        if (threadIdx.x == 128) trace_mark(p.tr, 4);
-        mbar_wait(&bars->acc_done, 0);
-        if (threadIdx.x == 128) trace_mark(p.tr, 5);
-        tc_fence_after();
-        // ---- epilogue: dK (scaled; warpgroup 0) and dV (warpgroup 1) leave TMEM as [128 x 32]
-        // fp32 slices staged in the now idle Q / dO ring (128 KB); the TMA unit then adds them
-        // into the fp32 gradient page in L2 (past pages: one owner per (page, kv head, block)
-        // in this launch, so the result is deterministic) or stores them to dk_cur / dv_cur (the
-        // chunk's own keys). Rows beyond the page's fill level carry zeros (the reference leaves
-        // those slots at 0).
-        uint8_t* stage = smem + kKvQ + wg * 4 * kSliceBytes;
-        const uint32_t acc = wg ? kTmDV : kTmDK;
-        const float sc = key_ok ? (wg ? 1.f : g.scale) : 0.f;
-#pragma unroll 1
-        for (int c = 0; c < kHd / 32; ++c) stage_slice(acc + c * 32 + lane_off, stage + c * kSliceBytes, kr, sc);
-        fence_proxy_async_smem();
-        named_bar_sync(1, 256);
-        if (warp == 4 && lane == 0) {
-            stage = smem + kKvQ;
-            if (u.past) {
-                const int row = (g_slot * g.Hkv + g_kv) * g.P + u.key0;
-                for (int c = 0; c < kHd / 32; ++c) {
-                    tma_reduce_add_2d(&tm_gk, stage + c * kSliceBytes, c * 32, row);
-                    tma_reduce_add_2d(&tm_gv, stage + (4 + c) * kSliceBytes, c * 32, row);
-                }
-            } else {
-                for (int c = 0; c < kHd / 32; ++c) {
-                    tma_store_3d(&tm_dkc, stage + c * kSliceBytes, c * 32, g_kv, u.key0);
-                    tma_store_3d(&tm_dvc, stage + (4 + c) * kSliceBytes, c * 32, g_kv, u.key0);
+                    for (int u8 = 0; u8 < 8; ++u8)
+                        st_slice_f32(stage, kr, u8,
+                                     make_float4(__uint_as_float(va[c][4 * u8]) * sc,
+                                                 __uint_as_float(va[c][4 * u8 + 1]) * sc,
+                                                 __uint_as_float(va[c][4 * u8 + 2]) * sc,
+                                                 __uint_as_float(va[c][4 * u8 + 3]) * sc));
+                    fence_proxy_async_smem();
+                    named_bar_sync(4 + wg, 128);
+                    if (issuer) {
+                        if (past) tma_reduce_add_2d(wg ? &tm_gv : &tm_gk, stage, c * 32, g_row);
+                        else tma_store_3d(wg ? &tm_dvc : &tm_dkc, stage, c * 32, g_kv, key0);
+                        bulk_commit();
+                    }
                 }
             }
-            bulk_commit();
-            bulk_wait_read0();
-            trace_mark(p.tr, 6);
         }
+        if (issuer) bulk_wait_read0();
     }
     tc_fence_before();
     __syncthreads();
@@ -809,6 +842,8 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 }  // namespace
+
+int g_num_sms = 148;
 
 bool tc_bwd_available() { return true; }
 
@@ -829,6 +864,9 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     if (!attr) {
         OOMB_CUDA(cudaFuncSetAttribute(attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDqSmem));
         OOMB_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kKvSmem));
+        int dev = 0;
+        OOMB_CUDA(cudaGetDevice(&dev));
+        OOMB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
         attr = true;
     }
     BwdWs w = carve(g, workspace);
@@ -838,7 +876,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), lse, g.C, g.Hq, w.Dt, w.Lt);
     check_launch("bwd_prep_kernel");
     if (n_pages > 0) OOMB_CUDA(cudaMemsetAsync(w.mask, 0, static_cast<size_t>(n_pages) * 8, st));
-    OOMB_CUDA(cudaMemsetAsync(w.n_uni, 0, sizeof(int32_t), st));
+    OOMB_CUDA(cudaMemsetAsync(w.n_uni, 0, 2 * sizeof(int32_t), st));  // union count + dK/dV work counter
     if (nnz > 0) {
         bwd_mask_kernel<<<g.m, 128, 0, st>>>(sel_off, sel_ids, g.max_pages, w.mask, d_err);
         check_launch("bwd_mask_kernel");
@@ -862,15 +900,14 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     {
         ProfScope s_(PK_BWD_DKDV, st);
         const int max_union = std::min(nnz, n_pages);
-        const int units = g.C / kTile + max_union * (g.P / kTile);
-        const size_t n_ctas = static_cast<size_t>(units) * g.Hkv;
-        p.tr = trace_begin("dkdv", n_ctas, 20);
+        const int units = (g.C / kTile + max_union * (g.P / kTile)) * g.Hkv;
+        const int n_ctas = std::max(1, std::min(units, g_num_sms));
         const CUtensorMap tdkc = map_rows_heads_f32(dk_cur, g.C, g.Hkv, kHd);
         const CUtensorMap tdvc = map_rows_heads_f32(dv_cur, g.C, g.Hkv, kHd);
-        attn_bwd_dkdv_kernel<<<dim3(units, g.Hkv), 384, kKvSmem, st>>>(
-            tq, tdo, tkc, tvc, maps.kpool, maps.vpool, maps.gkpool, maps.gvpool, tdkc, tdvc, p);
+        attn_bwd_dkdv_kernel<<<n_ctas, 384, kKvSmem, st>>>(tq, tdo, tkc, tvc, maps.kpool, maps.vpool, maps.gkpool,
+                                                            maps.gvpool, tdkc, tdvc, p, w.n_uni + 1);
         check_launch("attn_bwd_dkdv_kernel");
-        trace_end(p.tr, n_ctas, st);
+
     }
 }
 
