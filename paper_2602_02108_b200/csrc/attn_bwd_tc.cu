@@ -170,26 +170,6 @@ struct BwdParams {
 // sit in dP columns [64w, 64w+32).
 __host__ __device__ constexpr uint32_t ds_col(int ks) { return (ks >> 2) * 64 + (ks & 3) * 8; }
 
-// Stage one 128 x 128 bf16 row of a K-major SW128 tile (two [128 x 64] regions) into 64 TMEM
-// columns of this thread's lane (bf16 pairs packed per 32-bit column).
-__device__ __forceinline__ void stage_row_tmem(const uint8_t* tile, int region_bytes, int r, uint32_t taddr) {
-#pragma unroll
-    for (int c16 = 0; c16 < 4; ++c16) {
-        uint32_t v[16];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int c = c16 * 4 + q;
-            const uint4 x = *reinterpret_cast<const uint4*>(tile + (c >> 3) * region_bytes + r * 128 +
-                                                             (((c & 7) ^ (r & 7)) << 4));
-            v[4 * q] = x.x;
-            v[4 * q + 1] = x.y;
-            v[4 * q + 2] = x.z;
-            v[4 * q + 3] = x.w;
-        }
-        tmem_st16(taddr + c16 * 16, v);
-    }
-}
-
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_kc, const __grid_constant__ CUtensorMap tm_vc,

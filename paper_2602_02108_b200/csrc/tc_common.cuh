@@ -128,6 +128,26 @@ __device__ __forceinline__ PastBlock past_block(const AttnGeom& g, const int32_t
     return b;
 }
 
+// Stage one 128 x 128 bf16 row of a K-major SW128 tile (two [128 x 64] regions) into 64 TMEM
+// columns of this thread's lane (bf16 pairs packed per 32-bit column).
+__device__ __forceinline__ void stage_row_tmem(const uint8_t* tile, int region_bytes, int r, uint32_t taddr) {
+#pragma unroll
+    for (int c16 = 0; c16 < 4; ++c16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = c16 * 4 + q;
+            const uint4 x = *reinterpret_cast<const uint4*>(tile + (c >> 3) * region_bytes + r * 128 +
+                                                             (((c & 7) ^ (r & 7)) << 4));
+            v[4 * q] = x.x;
+            v[4 * q + 1] = x.y;
+            v[4 * q + 2] = x.z;
+            v[4 * q + 3] = x.w;
+        }
+        tmem_st16(taddr + c16 * 16, v);
+    }
+}
+
 // Valid keys (0..128) of past key block j of a query page: partially filled pages are masked
 // (paged_kv.hpp:295-299). The softmax warps stage these counts into shared memory once per CTA
 // so the per-block path never waits on a global load of the selection ids.
