@@ -56,23 +56,27 @@ BwdWs carve(const AttnGeom& g, void* ws) {
 __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                                 const float* __restrict__ lse, int C, int Hq, float* __restrict__ Dt,
                                 float* __restrict__ Lt) {
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (row >= static_cast<int64_t>(C) * Hq) return;
-    const uint2 a = reinterpret_cast<const uint2*>(o + row * kHd)[lane];
-    const uint2 b = reinterpret_cast<const uint2*>(dout + row * kHd)[lane];
-    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
-    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+    // two (token, head) rows per warp: 16 lanes x 16 B of O and dO each
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * 2 +
+                        ((threadIdx.x >> 4) & 1);
+    const int l16 = threadIdx.x & 15;
+    const bool ok = row < static_cast<int64_t>(C) * Hq;
     float s = 0.f;
+    if (ok) {
+        const uint4 a = reinterpret_cast<const uint4*>(o + row * kHd)[l16];
+        const uint4 b = reinterpret_cast<const uint4*>(dout + row * kHd)[l16];
+        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const float2 fa = __bfloat1622float2(a2[i]);
-        const float2 fb = __bfloat1622float2(b2[i]);
-        s += fa.x * fb.x + fa.y * fb.y;
+        for (int i = 0; i < 4; ++i) {
+            const float2 fa = __bfloat1622float2(a2[i]);
+            const float2 fb = __bfloat1622float2(b2[i]);
+            s += fa.x * fb.x + fa.y * fb.y;
+        }
     }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) {
+    for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (ok && l16 == 0) {
         const int t = static_cast<int>(row / Hq), h = static_cast<int>(row % Hq);
         Dt[static_cast<int64_t>(h) * C + t] = s;
         Lt[static_cast<int64_t>(h) * C + t] = lse[row] * kLog2e;
@@ -94,22 +98,19 @@ __global__ void bwd_mask_kernel(const int32_t* __restrict__ off, const int32_t* 
 
 __global__ void __launch_bounds__(1024) bwd_union_kernel(const uint64_t* __restrict__ mask, int n_pages,
                                                          int32_t* __restrict__ uni, int32_t* __restrict__ n_uni) {
+    // ascending list of the pages any query page selected: each thread counts a contiguous
+    // range, one block scan places the ranges, then each thread writes its pages in order
     using Scan = cub::BlockScan<int, 1024>;
     __shared__ typename Scan::TempStorage tmp;
-    __shared__ int carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < n_pages; base += 1024) {
-        const int p = base + threadIdx.x;
-        const int f = (p < n_pages && mask[p] != 0ull) ? 1 : 0;
-        int pos, total;
-        Scan(tmp).ExclusiveSum(f, pos, total);
-        if (f) uni[carry + pos] = p;
-        __syncthreads();
-        if (threadIdx.x == 0) carry += total;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *n_uni = carry;
+    const int per = (n_pages + 1023) / 1024;
+    const int p0 = min(n_pages, static_cast<int>(threadIdx.x) * per), p1 = min(n_pages, p0 + per);
+    int cnt = 0;
+    for (int p = p0; p < p1; ++p) cnt += mask[p] != 0ull;
+    int pos, total;
+    Scan(tmp).ExclusiveSum(cnt, pos, total);
+    for (int p = p0; p < p1; ++p)
+        if (mask[p] != 0ull) uni[pos++] = p;
+    if (threadIdx.x == 0) *n_uni = total;
 }
 
 // ===========================================================================
@@ -852,7 +853,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     BwdWs w = carve(g, workspace);
     ProfScope* prep_scope = new ProfScope(PK_BWD_PREP, st);
     const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
-    bwd_prep_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(
+    bwd_prep_kernel<<<static_cast<unsigned>((rows + 15) / 16), 256, 0, st>>>(
         static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), lse, g.C, g.Hq, w.Dt, w.Lt);
     check_launch("bwd_prep_kernel");
     if (n_pages > 0) OOMB_CUDA(cudaMemsetAsync(w.mask, 0, static_cast<size_t>(n_pages) * 8, st));

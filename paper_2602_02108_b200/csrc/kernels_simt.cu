@@ -78,15 +78,29 @@ __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, 
     const int64_t s0 = max(filled, static_cast<int64_t>(pg) * P);
     const int64_t s1 = min(filled + rows, static_cast<int64_t>(pg + 1) * P);
     float sum = is_new ? 0.f : ksum[static_cast<int64_t>(pg) * re + e];
-    for (int64_t s = s0; s < s1; ++s) {
-        const int64_t r = s - filled;
-        const int off = static_cast<int>(s - static_cast<int64_t>(pg) * P);
-        const T kv = k[r * re + e];
-        const T vv = v[r * re + e];
-        const size_t dst = ((static_cast<size_t>(slot) * Hkv + h) * P + off) * hd + d;
-        kpool[dst] = kv;
-        vpool[dst] = vv;
-        sum = __fadd_rn(sum, to_f(kv));
+    // rows in batches of 16: all loads of a batch are issued before its stores and the
+    // in-order (append order, paged_kv.hpp:98-104) fp32 sum, so 32 loads are in flight per thread
+    constexpr int kB = 16;
+    const size_t dst0 = ((static_cast<size_t>(slot) * Hkv + h) * P) * hd + d;
+    for (int64_t sb = s0; sb < s1; sb += kB) {
+        T kb[kB], vb[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            if (sb + u < s1) {
+                const int64_t r = sb + u - filled;
+                kb[u] = k[r * re + e];
+                vb[u] = v[r * re + e];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            if (sb + u < s1) {
+                const int off = static_cast<int>(sb + u - static_cast<int64_t>(pg) * P);
+                kpool[dst0 + static_cast<size_t>(off) * hd] = kb[u];
+                vpool[dst0 + static_cast<size_t>(off) * hd] = vb[u];
+                sum = __fadd_rn(sum, to_f(kb[u]));
+            }
+        }
     }
     ksum[static_cast<int64_t>(pg) * re + e] = sum;
     if (e == 0) kcnt[pg] = (is_new ? 0 : kcnt[pg]) + static_cast<int>(s1 - s0);
