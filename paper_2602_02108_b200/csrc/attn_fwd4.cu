@@ -1,0 +1,297 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Paged flash forward, variant 4 — attention.hpp:156-208 on tcgen05 with the key blocks of a
+// query tile split between two softmax warpgroups.
+//
+// One CTA per (128-row query tile, q-head), one CTA per SM, looping over the tile's key blocks
+// (its query page's selected pages in list order, then the chunk's causal prefix). Warpgroup w
+// owns the blocks j with j % 2 == w: it keeps its own running max m_w, row sum l_w and output
+// accumulator O_w (a split-K flash attention), so the two groups' exp work, the S MMAs of one
+// group's blocks and the PV MMAs of the other's overlap instead of forming one serial chain.
+// At the end O = (O_0 2^(m_0-m) + O_1 2^(m_1-m)) / (l_0 2^(m_0-m) + l_1 2^(m_1-m)), exact.
+// The online softmax of each group rescales O_w only when m_w grows by more than 2^8.
+//
+// S = Q K^T is an SS-MMA with N = 128 (full rate); P is written back into its S buffer as packed
+// bf16 and O_w += P V is a TS-MMA. A group's O_w rescale needs PV of its previous block to have
+// landed: the commit of S(j) covers every MMA issued before it, PV(j-2) included.
+// TMEM (all 512 columns, base 0): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).
+// Warp roles (384 threads): w0 Q + K producer, w1 MMA, w2 V producer, w3 TMEM allocator,
+// w4..w7 softmax group 0 (even blocks), w8..w11 group 1 (odd blocks); thread = query row.
+
+#include "tc_common.cuh"
+
+namespace oomb {
+
+using namespace tc;
+
+namespace {
+
+constexpr int kKSt = 3, kVSt = 2;
+constexpr int kF4Q = 0;
+constexpr int kF4K = kF4Q + kTileBytes;
+constexpr int kF4V = kF4K + kKSt * kTileBytes;
+constexpr int kF4Red = kF4V + kVSt * kTileBytes;  // [2 groups][128 rows] {m, l}
+constexpr int kF4Nv = kF4Red + 2 * 128 * 8;       // uint8 valid-key counts of the past blocks
+constexpr int kF4NvCap = 8192;
+constexpr int kF4Bar = kF4Nv + kF4NvCap;
+constexpr int kF4Smem = kF4Bar + 256;
+static_assert(kF4Smem <= 232448, "dynamic shared memory above the 227 KB opt-in limit");
+constexpr uint32_t kTmS = 0, kTmO = 256;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+struct F4Bars {
+    uint64_t q_full;
+    uint64_t k_full[kKSt], k_empty[kKSt], v_full[kVSt], v_empty[kVSt];
+    uint64_t s_full[2], p_full[2], o_done;
+    uint32_t tmem_base;
+};
+
+struct F4Params {
+    AttnGeom g;
+    const int32_t* sel_off;
+    const int32_t* sel_ids;
+    const int32_t* kvslot;
+    __nv_bfloat16* out;
+    float* lse;
+    int* err;
+};
+
+__global__ void __launch_bounds__(384, 1)
+    attn_fwd_tc4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kc,
+                        const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kp,
+                        const __grid_constant__ CUtensorMap tm_vp, F4Params p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    F4Bars* bars = reinterpret_cast<F4Bars*>(smem + kF4Bar);
+    const AttnGeom& g = p.g;
+    const int h = blockIdx.x;
+    const int qt = (g.C / kTile) - 1 - static_cast<int>(blockIdx.y);  // longest causal prefix first (LPT)
+    const int kvh = h / g.group;
+    const int qp = (qt * kTile) / g.P;
+    const int sel_begin = p.sel_off[qp];
+    const int n_past = (p.sel_off[qp + 1] - sel_begin) * (g.P / kTile);
+    const int nb = n_past + qt + 1;
+    const int warp = warp_id(), lane = lane_id();
+
+    if (threadIdx.x == 0) {
+        if (smem_u32(smem) & 1023) __trap();  // SW128 operands need a 1 KB-aligned base
+        mbar_init(&bars->q_full, 1);
+        for (int i = 0; i < kKSt; ++i) {
+            mbar_init(&bars->k_full[i], 1);
+            mbar_init(&bars->k_empty[i], 1);
+        }
+        for (int i = 0; i < kVSt; ++i) {
+            mbar_init(&bars->v_full[i], 1);
+            mbar_init(&bars->v_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bars->s_full[i], 1);
+            mbar_init(&bars->p_full[i], 128);
+        }
+        mbar_init(&bars->o_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 3) tmem_alloc<512>(&bars->tmem_base);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (bars->tmem_base != 0) __trap();  // all 512 columns: base column 0 (the constants rely on it)
+    uint8_t* sQ = smem + kF4Q;
+    uint8_t* sK = smem + kF4K;
+    uint8_t* sV = smem + kF4V;
+
+    if (warp == 0 || warp == 2) {
+        if (lane == 0) {  // w0: Q + K, w2: V
+            const bool is_k = warp == 0;
+            const int nst = is_k ? kKSt : kVSt;
+            uint8_t* base = is_k ? sK : sV;
+            uint64_t* full = is_k ? bars->k_full : bars->v_full;
+            uint64_t* empty = is_k ? bars->k_empty : bars->v_empty;
+            const CUtensorMap* mp = is_k ? &tm_kp : &tm_vp;
+            const CUtensorMap* mc = is_k ? &tm_kc : &tm_vc;
+            if (is_k) {
+                mbar_expect_tx(&bars->q_full, kTileBytes);
+                for (int r = 0; r < 2; ++r) tma_load_3d(sQ + r * kRegion, &tm_q, &bars->q_full, r * 64, h, qt * kTile);
+            }
+            for (int j = 0; j < nb; ++j) {
+                const int st = j % nst;
+                if (j >= nst) mbar_wait(&empty[st], ((j / nst) - 1) & 1);
+                mbar_expect_tx(&full[st], kTileBytes);
+                uint8_t* dst = base + st * kTileBytes;
+                if (j < n_past) {
+                    const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, j, kvh, is_k ? p.err : nullptr);
+                    for (int r = 0; r < 2; ++r) tma_load_2d(dst + r * kRegion, mp, &full[st], r * 64, b.row);
+                } else {
+                    for (int r = 0; r < 2; ++r)
+                        tma_load_3d(dst + r * kRegion, mc, &full[st], r * 64, kvh, (j - n_past) * kTile);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // MMA warp (converged): S(0) S(1) | PV(0) S(2) | PV(1) S(3) | ... | PV(nb-1)
+        constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kTile, 0, 0);  // [128 q] x [128 keys], K = hd
+        constexpr uint32_t idesc_o = make_idesc_bf16(kTile, kHd, 0, 1);    // [128 q] x [hd], K = keys
+        const uint64_t dQ = sdesc_k(smem_u32(sQ));
+        const uint64_t dK = sdesc_k(smem_u32(sK));
+        const uint64_t dVmn = sdesc_mn(smem_u32(sV), kRegion);
+        mbar_wait(&bars->q_full, 0);
+        auto mma_s = [&](int j) {
+            const int st = j % kKSt, b = j & 1;
+            mbar_wait(&bars->k_full[st], (j / kKSt) & 1);
+            tc_fence_after();
+            const uint64_t so = boff(st * kTileBytes);
+#pragma unroll
+            for (int ks = 0; ks < kHd / 16; ++ks)
+                umma_ss_w(kTmS + b * 128, dQ + koff(ks, kRegion), dK + so + koff(ks, kRegion), idesc_s, ks);
+            umma_commit_w(&bars->s_full[b]);
+            umma_commit_w(&bars->k_empty[st]);
+        };
+        auto mma_pv = [&](int j) {
+            const int st = j % kVSt, b = j & 1;
+            mbar_wait(&bars->p_full[b], (j >> 1) & 1);
+            mbar_wait(&bars->v_full[st], (j / kVSt) & 1);
+            tc_fence_after();
+            const uint64_t so = boff(st * kTileBytes);
+            const uint32_t first = j < 2 ? 0u : 1u;  // the first block of each group overwrites O_w
+#pragma unroll
+            for (int ks = 0; ks < kTile / 16; ++ks)
+                umma_ts_w(kTmO + b * 128, kTmS + b * 128 + ks * 8, dVmn + so + mnoff(ks), idesc_o, first | ks);
+            umma_commit_w(&bars->v_empty[st]);
+        };
+        mma_s(0);
+        if (nb > 1) mma_s(1);
+        for (int j = 0; j < nb; ++j) {
+            mma_pv(j);
+            if (j + 2 < nb) mma_s(j + 2);  // S(j+2) rewrites the buffer PV(j) read: issued after it
+        }
+        umma_commit_w(&bars->o_done);
+    } else if (warp >= 4) {
+        const int quarter = warp & 3, wg = (warp - 4) >> 2;
+        const int r = quarter * 32 + lane;  // query row = TMEM lane
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        uint8_t* nvt = smem + kF4Nv;
+        stage_past_valid(g, p.sel_ids, sel_begin, n_past, nvt, kF4NvCap, threadIdx.x - 128, 256);
+        named_bar_sync(3, 256);
+        const float sl2 = g.scale * kLog2e;
+        const uint32_t tS = kTmS + wg * 128 + lane_off, tO = kTmO + wg * 128 + lane_off;
+        float m = -INFINITY;  // this group's running row max (log2 units) that O_w and l are relative to
+        float l = 0.f;
+        for (int j = wg; j < nb; j += 2) {
+            int lim;  // keep key columns c <= lim
+            if (j < n_past) lim = past_valid(g, p.sel_ids, sel_begin, nvt, kF4NvCap, j) - 1;
+            else lim = (j - n_past == qt) ? r : kTile - 1;
+            mbar_wait(&bars->s_full[wg], (j >> 1) & 1);
+            tc_fence_after();
+            uint32_t sr[128];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+            tmem_wait_ld();
+            if (lim < kTile - 1) {
+#pragma unroll
+                for (int c = 0; c < kTile; ++c)
+                    if (c > lim) sr[c] = __float_as_uint(-INFINITY);
+            }
+            float mx8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) mx8[u] = __uint_as_float(sr[u]);
+#pragma unroll
+            for (int c = 8; c < kTile; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
+            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
+            const float m_new = fmaxf(m, mx);
+            bool rescale = false;
+            float alpha = 1.f;
+            if (m == -INFINITY || m_new > m + kRescaleThreshold) {
+                alpha = (m == -INFINITY) ? 0.f : ex2(m - m_new);
+                rescale = j >= 2 && m != -INFINITY;
+                m = m_new;
+            }
+            const float m_use = (m == -INFINITY) ? 0.f : m;
+            // O_w rescale: PV(j-2) has landed (the commit of S(j) covers it)
+            if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll 1
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t o[16];
+                    tmem_ld16(tO + c * 16, o);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * alpha);
+                    tmem_st16(tO + c * 16, o);
+                }
+            }
+            float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const float e0 = ex2(fmaf(__uint_as_float(sr[c4 * 32 + 2 * u]), sl2, -m_use));
+                    const float e1 = ex2(fmaf(__uint_as_float(sr[c4 * 32 + 2 * u + 1]), sl2, -m_use));
+                    rs8[(2 * u) & 7] += e0;
+                    rs8[(2 * u + 1) & 7] += e1;
+                    pk[u] = pack_bf16(e0, e1);
+                }
+                tmem_st16(tS + c4 * 16, pk);  // P cols [16 c4, 16 c4 + 16): below the S columns still unread
+            }
+            const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+            l = l * alpha + rs;
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&bars->p_full[wg]);
+        }
+        // ---- merge the two groups: O = (O_0 a_0 + O_1 a_1) / (l_0 a_0 + l_1 a_1), a_w = 2^(m_w - m)
+        float2* red = reinterpret_cast<float2*>(smem + kF4Red);
+        red[wg * 128 + r] = make_float2(m, l);
+        named_bar_sync(2, 256);
+        const float2 o = red[(wg ^ 1) * 128 + r];
+        const float m0 = wg ? o.x : m, l0 = wg ? o.y : l, m1 = wg ? m : o.x, l1 = wg ? l : o.y;
+        const float mt = fmaxf(m0, m1);
+        const float a0 = (l0 > 0.f) ? ex2(m0 - mt) : 0.f, a1 = (l1 > 0.f) ? ex2(m1 - mt) : 0.f;
+        const float lt = l0 * a0 + l1 * a1;
+        const float s0 = a0 / lt, s1 = a1 / lt;
+        mbar_wait(&bars->o_done, 0);
+        tc_fence_after();
+        const int t = qt * kTile + r;
+        // group w writes output columns [64w, 64w + 64)
+        __nv_bfloat16* orow = p.out + (static_cast<int64_t>(t) * g.Hq + h) * kHd + wg * 64;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+            uint32_t x0[16], x1[16];
+            tmem_ld16(kTmO + wg * 64 + c * 16 + lane_off, x0);
+            tmem_ld16(kTmO + 128 + wg * 64 + c * 16 + lane_off, x1);
+            tmem_wait_ld();
+            float f[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const float v0 = s0 != 0.f ? __uint_as_float(x0[u]) * s0 : 0.f;  // an O_w never written holds
+                const float v1 = s1 != 0.f ? __uint_as_float(x1[u]) * s1 : 0.f;  // garbage: never multiply it
+                f[u] = v0 + v1;
+            }
+            *reinterpret_cast<uint4*>(orow + c * 16) = pack8(f);
+            *reinterpret_cast<uint4*>(orow + c * 16 + 8) = pack8(f + 8);
+        }
+        if (wg == 0) p.lse[static_cast<int64_t>(t) * g.Hq + h] = (mt + __log2f(lt)) * kLn2;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 3) tmem_dealloc<512>(0);
+}
+
+}  // namespace
+
+void launch_attn_fwd_tc4(const AttnGeom& g, const TcPoolMaps& maps, const void* q, const int32_t* sel_off,
+                         const int32_t* sel_ids, const int32_t* d_kvslot_layer, const void* k_cur, const void* v_cur,
+                         void* out, float* lse, int* d_err, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        OOMB_CUDA(cudaFuncSetAttribute(attn_fwd_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kF4Smem));
+        attr = true;
+    }
+    const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, kHd);
+    const CUtensorMap tkc = map_rows_heads(k_cur, g.C, g.Hkv, kHd);
+    const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, kHd);
+    F4Params p{g, sel_off, sel_ids, d_kvslot_layer, static_cast<__nv_bfloat16*>(out), lse, d_err};
+    attn_fwd_tc4_kernel<<<dim3(g.Hq, g.C / kTile), 384, kF4Smem, st>>>(tq, tkc, tvc, maps.kpool, maps.vpool, p);
+    check_launch("attn_fwd_tc4_kernel");
+}
+
+}  // namespace oomb
