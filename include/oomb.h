@@ -177,6 +177,26 @@ OOMB_API int oomb_attn_forward(oomb_pool_t pool, int layer, const void* q, int64
 OOMB_API int oomb_attn_backward(oomb_pool_t pool, int layer, const void* dout, const void* q, int64_t tokens,
                        oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out,
                        const float* lse, float* dq, float* dk_cur, float* dv_cur, void* stream);
+/* Page-range split: a shard attends only its share of every query page's
+ * selected pages. flags = OOMB_ATTN_PAST_ONLY drops the chunk's own causal keys (the shard that
+ * owns them passes 0). The forward then writes that shard's partial (out, lse) — lse = -inf and
+ * out = 0 for rows that attended no key; the backward, given the MERGED out / lse, writes the
+ * shard's partial dq (summed over shards afterwards), its pages' dK/dV, and zeros in
+ * dk_cur / dv_cur when the chunk's keys are not its own. Replaces the reference call sites
+ * chunk_trainer.hpp:437 / :565 on a page-range shard. */
+#define OOMB_ATTN_PAST_ONLY 1
+OOMB_API int oomb_attn_forward_ex(oomb_pool_t pool, int layer, const void* q, int64_t tokens, oomb_selection_t sel,
+                                  const void* k_cur, const void* v_cur, void* out, float* lse, int flags,
+                                  void* stream);
+OOMB_API int oomb_attn_backward_ex(oomb_pool_t pool, int layer, const void* dout, const void* q, int64_t tokens,
+                                   oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out,
+                                   const float* lse, float* dq, float* dk_cur, float* dv_cur, int flags,
+                                   void* stream);
+/* Exact merge of page-range shards' partial attention outputs, shards in rank order:
+ * o_parts [parts][rows][hd] (dtype), lse_parts [parts][rows] fp32 natural log ->
+ * lse = ln sum_r e^{lse_r}, out = sum_r e^{lse_r - lse} o_r. rows = tokens * n_q_heads. */
+OOMB_API int oomb_lse_merge(const void* o_parts, const float* lse_parts, int parts, int64_t rows, int hd, int dtype,
+                            void* out, float* lse, void* stream);
 /* Kernel family selection: 0 = auto (tcgen05 when dtype bf16, hd 128, P % 128 == 0),
  * 1 = force the SIMT kernels, 2 = force tcgen05 (error if the shape is unsupported). */
 OOMB_API int oomb_set_kernel_policy(oomb_pool_t pool, int policy);

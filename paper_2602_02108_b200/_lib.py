@@ -72,6 +72,9 @@ _PROTOS = {
     "oomb_select_pages_topk": [VP, I, VP, I64, I, VP, VP, VP],
     "oomb_attn_forward": [VP, I, VP, I64, VP, VP, VP, VP, VP, VP],
     "oomb_attn_backward": [VP, I, VP, VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP],
+    "oomb_attn_forward_ex": [VP, I, VP, I64, VP, VP, VP, VP, VP, I, VP],
+    "oomb_attn_backward_ex": [VP, I, VP, VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, I, VP],
+    "oomb_lse_merge": [VP, VP, I, I64, I, I, VP, VP, VP],
     "oomb_set_kernel_policy": [VP, I],
     "oomb_pagetable_create": [I, I, I, I, I, I, C.POINTER(VP)],
     "oomb_pagetable_destroy": [VP],

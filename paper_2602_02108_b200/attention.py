@@ -174,9 +174,14 @@ class AttnGrads:
     dv_cur: torch.Tensor
 
 
+PAST_ONLY = 1  # OOMB_ATTN_PAST_ONLY: a page-range shard that does not own the chunk's own keys
+
+
 def attn_forward(cfg: ModelConfig, q, cache: PagedCache, layer: int, selected, k_cur, v_cur,
-                 stream=None, out: torch.Tensor | None = None, lse: torch.Tensor | None = None) -> AttnSaved:
-    """attention.hpp:156-208. `out` / `lse` may be preallocated by the caller."""
+                 stream=None, out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
+                 past_only: bool = False) -> AttnSaved:
+    """attention.hpp:156-208. `out` / `lse` may be preallocated by the caller.
+    past_only: page-range shard mode (selected pages only, no chunk keys; see sharding.PageRangeShard)."""
     q, k_cur, v_cur = cache._dev(q), cache._dev(k_cur), cache._dev(v_cur)
     c, qh, hd = q.shape
     if qh != cfg.n_q_heads or hd != cfg.head_dim or k_cur.shape != (c, cfg.n_kv_heads, hd) or \
@@ -187,15 +192,16 @@ def attn_forward(cfg: ModelConfig, q, cache: PagedCache, layer: int, selected, k
     lse = torch.empty((c, qh), dtype=torch.float32, device=q.device) if lse is None else lse
     if out.shape != q.shape or out.dtype != q.dtype or lse.shape != (c, qh) or lse.dtype != torch.float32:
         raise ShapeError("attn_forward: preallocated out / lse have the wrong shape or dtype")
-    call("oomb_attn_forward", cache.handle, layer, _ptr(q), c, sel.handle, _ptr(k_cur), _ptr(v_cur), _ptr(out),
-         _ptr(lse), stream_handle(stream))
+    call("oomb_attn_forward_ex", cache.handle, layer, _ptr(q), c, sel.handle, _ptr(k_cur), _ptr(v_cur), _ptr(out),
+         _ptr(lse), PAST_ONLY if past_only else 0, stream_handle(stream))
     if cache.residency_enforced():
         cache.check_device_errors()
     return AttnSaved(out, lse, sel)
 
 
 def attn_backward(cfg: ModelConfig, dout, q, cache: PagedCache, layer: int, k_cur, v_cur, saved: AttnSaved,
-                  stream=None, grads: AttnGrads | None = None) -> AttnGrads:
+                  stream=None, grads: AttnGrads | None = None, past_only: bool = False,
+                  selected=None) -> AttnGrads:
     """attention.hpp:222-293 — past-page dK/dV go into the cache's gradient pages.
     `grads` may carry preallocated fp32 output buffers."""
     dout, q = cache._dev(dout), cache._dev(q)
@@ -212,8 +218,10 @@ def attn_backward(cfg: ModelConfig, dout, q, cache: PagedCache, layer: int, k_cu
         if dq.shape != (c, cfg.n_q_heads, cfg.head_dim) or dk.shape != (c, cfg.n_kv_heads, cfg.head_dim) or \
                 dv.shape != dk.shape or {dq.dtype, dk.dtype, dv.dtype} != {torch.float32}:
             raise ShapeError("attn_backward: preallocated gradients have the wrong shape or dtype")
-    call("oomb_attn_backward", cache.handle, layer, _ptr(dout), _ptr(q), c, saved.selected.handle, _ptr(k_cur),
-         _ptr(v_cur), _ptr(saved.out), _ptr(saved.lse), _ptr(dq), _ptr(dk), _ptr(dv), stream_handle(stream))
+    sel = saved.selected if selected is None else as_selection(cache, selected, stream)
+    call("oomb_attn_backward_ex", cache.handle, layer, _ptr(dout), _ptr(q), c, sel.handle, _ptr(k_cur),
+         _ptr(v_cur), _ptr(saved.out), _ptr(saved.lse), _ptr(dq), _ptr(dk), _ptr(dv), PAST_ONLY if past_only else 0,
+         stream_handle(stream))
     if cache.residency_enforced():
         cache.check_device_errors()
     return AttnGrads(dq, dk, dv)

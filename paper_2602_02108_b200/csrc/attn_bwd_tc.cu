@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(384, 1)
     const int qp = (qt * kTile) / g.P;
     const int sel_begin = p.sel_off[qp];
     const int n_past = (p.sel_off[qp + 1] - sel_begin) * (g.P / kTile);
-    const int nb = n_past + qt + 1;
+    const int nb = n_past + (g.chunk_keys ? qt + 1 : 0);
     const int warp = warp_id(), lane = lane_id();
 
     if (threadIdx.x == 0) {
@@ -295,14 +295,16 @@ __global__ void __launch_bounds__(384, 1)
                 umma_ts_w(kDqTmDQ, kDqTmDP + ds_col(ks), dKmn + so + mnoff(ks), idesc_q, first | ks);
             umma_commit_w(&bars->k_empty[st]);
         };
-        mma_s(0);
-        mma_dp(0);
-        for (int j = 1; j < nb; ++j) {
-            mma_s(j);
-            mma_dq(j - 1);  // dS(j-1) lives in the dP columns: dP(j) is issued after it
-            mma_dp(j);
+        if (nb > 0) {
+            mma_s(0);
+            mma_dp(0);
+            for (int j = 1; j < nb; ++j) {
+                mma_s(j);
+                mma_dq(j - 1);  // dS(j-1) lives in the dP columns: dP(j) is issued after it
+                mma_dp(j);
+            }
+            mma_dq(nb - 1);
         }
-        mma_dq(nb - 1);
         umma_commit_w(&bars->dq_done);
     } else if (warp >= 4) {
         const int quarter = warp & 3, wg = (warp - 4) >> 2;
@@ -374,8 +376,14 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         uint8_t* stage = sK;
 #pragma unroll 1
-        for (int c = 2 * wg; c < 2 * wg + 2; ++c)
-            stage_slice(kDqTmDQ + c * 32 + lane_off, stage + c * kSliceBytes, r, g.scale);
+        for (int c = 2 * wg; c < 2 * wg + 2; ++c) {
+            if (nb > 0) {
+                stage_slice(kDqTmDQ + c * 32 + lane_off, stage + c * kSliceBytes, r, g.scale);
+            } else {  // a page-range shard with no key for this tile: dQ = 0 (TMEM was never written)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) st_slice_f32(stage + c * kSliceBytes, r, u, make_float4(0.f, 0.f, 0.f, 0.f));
+            }
+        }
         fence_proxy_async_smem();
         named_bar_sync(1, 256);
         if (warp == 4 && lane == 0) {
@@ -496,7 +504,7 @@ struct ItemIter {
 // fastest) into a unit descriptor.
 __device__ void decode_unit(const BwdParams& p, int w, KvUnit& u) {
     const AttnGeom& g = p.g;
-    const int n_chunk_blocks = g.C / kTile, bpp = g.P / kTile;
+    const int n_chunk_blocks = g.chunk_keys ? g.C / kTile : 0, bpp = g.P / kTile;
     const int n_units = (n_chunk_blocks + *p.n_uni * bpp) * g.Hkv;
     u.valid = w < n_units;
     if (!u.valid) return;
@@ -881,7 +889,11 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     {
         ProfScope s_(PK_BWD_DKDV, st);
         const int max_union = std::min(nnz, n_pages);
-        const int units = (g.C / kTile + max_union * (g.P / kTile)) * g.Hkv;
+        if (!g.chunk_keys) {  // past-only shard: the chunk's own keys are another shard's
+            OOMB_CUDA(cudaMemsetAsync(dk_cur, 0, static_cast<size_t>(g.C) * g.Hkv * kHd * sizeof(float), st));
+            OOMB_CUDA(cudaMemsetAsync(dv_cur, 0, static_cast<size_t>(g.C) * g.Hkv * kHd * sizeof(float), st));
+        }
+        const int units = ((g.chunk_keys ? g.C / kTile : 0) + max_union * (g.P / kTile)) * g.Hkv;
         const int n_ctas = std::max(1, std::min(units, g_num_sms));
         const CUtensorMap tdkc = map_rows_heads_f32(dk_cur, g.C, g.Hkv, kHd);
         const CUtensorMap tdvc = map_rows_heads_f32(dv_cur, g.C, g.Hkv, kHd);

@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(384, 1)
     const int qp = (qt * kTile) / g.P;
     const int sel_begin = p.sel_off[qp];
     const int n_past = (p.sel_off[qp + 1] - sel_begin) * (g.P / kTile);
-    const int nb = n_past + qt + 1;
+    const int nb = n_past + (g.chunk_keys ? qt + 1 : 0);
     const int warp = warp_id(), lane = lane_id();
 
     if (threadIdx.x == 0) {
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(384, 1)
                 umma_ts_w(kTmO + b * 128, kTmS + b * 128 + ks * 8, dVmn + so + mnoff(ks), idesc_o, first | ks);
             umma_commit_w(&bars->v_empty[st]);
         };
-        mma_s(0);
+        if (nb > 0) mma_s(0);
         if (nb > 1) mma_s(1);
         for (int j = 0; j < nb; ++j) {
             mma_pv(j);
@@ -246,8 +246,8 @@ __global__ void __launch_bounds__(384, 1)
         const float m0 = wg ? o.x : m, l0 = wg ? o.y : l, m1 = wg ? m : o.x, l1 = wg ? l : o.y;
         const float mt = fmaxf(m0, m1);
         const float a0 = (l0 > 0.f) ? ex2(m0 - mt) : 0.f, a1 = (l1 > 0.f) ? ex2(m1 - mt) : 0.f;
-        const float lt = l0 * a0 + l1 * a1;
-        const float s0 = a0 / lt, s1 = a1 / lt;
+        const float lt = l0 * a0 + l1 * a1;  // 0 only for a page-range shard that attended no key
+        const float s0 = lt > 0.f ? a0 / lt : 0.f, s1 = lt > 0.f ? a1 / lt : 0.f;
         mbar_wait(&bars->o_done, 0);
         tc_fence_after();
         const int t = qt * kTile + r;
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(384, 1)
             *reinterpret_cast<uint4*>(orow + c * 16) = pack8(f);
             *reinterpret_cast<uint4*>(orow + c * 16 + 8) = pack8(f + 8);
         }
-        if (wg == 0) p.lse[static_cast<int64_t>(t) * g.Hq + h] = (mt + __log2f(lt)) * kLn2;
+        if (wg == 0) p.lse[static_cast<int64_t>(t) * g.Hq + h] = lt > 0.f ? (mt + __log2f(lt)) * kLn2 : -INFINITY;
     }
     tc_fence_before();
     __syncthreads();

@@ -630,7 +630,7 @@ void launch_attn_fwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* q
                         const int32_t* sel_ids, const int32_t* d_kvslot_layer, const void* k_cur, const void* v_cur,
                         void* out, float* lse, int* d_err, cudaStream_t st) {
     ProfScope prof_(PK_FWD, st);
-    if (fwd_variant() == 4) {
+    if (fwd_variant() == 4 || !g.chunk_keys) {  // only variant 4 implements the past-only (range shard) mode
         launch_attn_fwd_tc4(g, maps, q, sel_off, sel_ids, d_kvslot_layer, k_cur, v_cur, out, lse, d_err, st);
         return;
     }

@@ -592,17 +592,19 @@ __global__ void attn_fwd_simt_kernel(AttnGeom g, const T* __restrict__ q, const 
         const size_t base = (static_cast<size_t>(slot) * g.Hkv + kvh) * g.P * hd;
         for (int s = 0; s < vs; ++s) visit(kpool + base + static_cast<size_t>(s) * hd, vpool + base + static_cast<size_t>(s) * hd);
     }
-    for (int s = 0; s <= t; ++s) {
-        const size_t o = (static_cast<size_t>(s) * g.Hkv + kvh) * hd;
-        visit(k_cur + o, v_cur + o);
+    if (g.chunk_keys) {
+        for (int s = 0; s <= t; ++s) {
+            const size_t o = (static_cast<size_t>(s) * g.Hkv + kvh) * hd;
+            visit(k_cur + o, v_cur + o);
+        }
     }
-    const float inv = 1.f / l;
+    const float inv = l > 0.f ? 1.f / l : 0.f;  // a shard that attended no key: O = 0, lse = -inf
 #pragma unroll
     for (int i = 0; i < kMaxLaneElems; ++i) {
         const int d = lane + 32 * i;
         if (i < nd && d < hd) out[row * hd + d] = from_f<T>(acc[i] * inv);
     }
-    if (lane == 0) lse[row] = m + logf(l);
+    if (lane == 0) lse[row] = l > 0.f ? m + logf(l) : -INFINITY;
 }
 
 template <typename T>
@@ -675,9 +677,11 @@ __global__ void attn_bwd_simt_kernel(AttnGeom g, const T* __restrict__ dout, con
             visit(kpool + base + so, vpool + base + so, gk + gbase + so, gv + gbase + so);
         }
     }
-    for (int s = 0; s <= t; ++s) {
-        const size_t so = (static_cast<size_t>(s) * g.Hkv + kvh) * hd;
-        visit(k_cur + so, v_cur + so, dk_cur + so, dv_cur + so);
+    if (g.chunk_keys) {
+        for (int s = 0; s <= t; ++s) {
+            const size_t so = (static_cast<size_t>(s) * g.Hkv + kvh) * hd;
+            visit(k_cur + so, v_cur + so, dk_cur + so, dv_cur + so);
+        }
     }
 #pragma unroll
     for (int i = 0; i < kMaxLaneElems; ++i) {
@@ -730,6 +734,53 @@ void launch_attn_bwd_simt(int dtype, const AttnGeom& g, const void* dout, const 
             static_cast<const T*>(v_cur), static_cast<const T*>(out), lse, dq, dk_cur, dv_cur, d_err);
     }
     check_launch("attn_bwd_simt_kernel");
+}
+
+// ===========================================================================
+// Page-range split merge: rank r attended a disjoint subset of every query page's
+// selected pages and produced (O_r, LSE_r), O_r normalised by its own row sum, LSE natural log
+// (-inf: the rank attended no key for that row). Exact combination, parts in rank order:
+//   LSE = m + ln sum_r exp(LSE_r - m),  O = sum_r exp(LSE_r - LSE) O_r.
+// One warp per (token, head) row.
+// ===========================================================================
+template <typename T>
+__global__ void lse_merge_kernel(const T* __restrict__ o_parts, const float* __restrict__ lse_parts, int parts,
+                                 int64_t rows, int hd, T* __restrict__ out, float* __restrict__ lse) {
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    float m = -INFINITY;
+    for (int r = 0; r < parts; ++r) m = fmaxf(m, lse_parts[static_cast<int64_t>(r) * rows + row]);
+    float l = 0.f;
+    for (int r = 0; r < parts; ++r) {
+        const float x = lse_parts[static_cast<int64_t>(r) * rows + row];
+        if (x != -INFINITY) l += expf(x - m);
+    }
+    const float L = (m == -INFINITY) ? -INFINITY : m + logf(l);
+    for (int d = lane; d < hd; d += 32) {
+        float acc = 0.f;
+        for (int r = 0; r < parts; ++r) {
+            const float x = lse_parts[static_cast<int64_t>(r) * rows + row];
+            if (x == -INFINITY) continue;
+            acc += expf(x - L) * to_f(o_parts[(static_cast<int64_t>(r) * rows + row) * hd + d]);
+        }
+        out[row * hd + d] = from_f<T>(acc);
+    }
+    if (lane == 0) lse[row] = L;
+}
+
+void launch_lse_merge(const void* o_parts, const float* lse_parts, int parts, int64_t rows, int hd, int dtype,
+                      void* out, float* lse, cudaStream_t st) {
+    if (rows <= 0) return;
+    ProfScope prof_(PK_OTHER, st);
+    const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
+    if (dtype == OOMB_BF16)
+        lse_merge_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o_parts), lse_parts,
+                                                              parts, rows, hd, static_cast<__nv_bfloat16*>(out), lse);
+    else
+        lse_merge_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(o_parts), lse_parts, parts, rows, hd,
+                                                      static_cast<float*>(out), lse);
+    check_launch("lse_merge_kernel");
 }
 
 }  // namespace oomb

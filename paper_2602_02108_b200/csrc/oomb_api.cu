@@ -145,6 +145,7 @@ AttnGeom geom(oomb_pool_s* p, int64_t tokens, int layer) {
     g.filled = p->pt->filled[layer];
     g.scale = 1.0f / std::sqrt(static_cast<float>(g.hd));
     g.max_pages = static_cast<int>(p->max_pages);
+    g.chunk_keys = 1;
     return g;
 }
 
@@ -738,6 +739,15 @@ int oomb_score_pages_partial(oomb_pool_t p, int layer, const void* q, int64_t to
     });
 }
 
+int oomb_lse_merge(const void* o_parts, const float* lse_parts, int parts, int64_t rows, int hd, int dtype,
+                   void* out, float* lse, void* stream) {
+    return guard([&] {
+        OOMB_REQUIRE(parts >= 1 && rows >= 0 && hd >= 1 && hd <= 256, OOMB_SHAPE_ERROR, "lse_merge: bad shape");
+        OOMB_REQUIRE(dtype == OOMB_BF16 || dtype == OOMB_F32, OOMB_CONFIG_ERROR, "lse_merge: dtype");
+        launch_lse_merge(o_parts, lse_parts, parts, rows, hd, dtype, out, lse, S(stream));
+    });
+}
+
 int oomb_vote_reduce(const float* partials, int groups, int64_t m, int64_t n, float* vote, void* stream) {
     return guard([&] {
         OOMB_REQUIRE(groups >= 1 && m >= 0 && n >= 0, OOMB_SHAPE_ERROR, "vote_reduce: bad shape");
@@ -767,13 +777,14 @@ int oomb_select_pages_topk(oomb_pool_t p, int layer, const void* q, int64_t toke
 // ---------------------------------------------------------------------------
 // attention
 // ---------------------------------------------------------------------------
-int oomb_attn_forward(oomb_pool_t p, int layer, const void* q, int64_t tokens, oomb_selection_t sel,
-                      const void* k_cur, const void* v_cur, void* out, float* lse, void* stream) {
+int oomb_attn_forward_ex(oomb_pool_t p, int layer, const void* q, int64_t tokens, oomb_selection_t sel,
+                         const void* k_cur, const void* v_cur, void* out, float* lse, int flags, void* stream) {
     return guard([&] {
         set_dev(p);
         p->pt->check_layer(layer);
         OOMB_REQUIRE(tokens >= 1, OOMB_SHAPE_ERROR, "attn_forward: empty chunk");
         AttnGeom g = geom(p, tokens, layer);
+        if (flags & OOMB_ATTN_PAST_ONLY) g.chunk_keys = 0;
         OOMB_REQUIRE(sel->m == g.m, OOMB_SHAPE_ERROR,
                      "attn_forward: one selected-page list per query page required");  // attention.hpp:172-174
         if (p->enforce) {  // gather_pages' residency check (paged_kv.hpp:118-122)
@@ -791,14 +802,20 @@ int oomb_attn_forward(oomb_pool_t p, int layer, const void* q, int64_t tokens, o
     });
 }
 
-int oomb_attn_backward(oomb_pool_t p, int layer, const void* dout, const void* q, int64_t tokens,
+int oomb_attn_forward(oomb_pool_t p, int layer, const void* q, int64_t tokens, oomb_selection_t sel,
+                      const void* k_cur, const void* v_cur, void* out, float* lse, void* stream) {
+    return oomb_attn_forward_ex(p, layer, q, tokens, sel, k_cur, v_cur, out, lse, 0, stream);
+}
+
+int oomb_attn_backward_ex(oomb_pool_t p, int layer, const void* dout, const void* q, int64_t tokens,
                        oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out, const float* lse,
-                       float* dq, float* dk_cur, float* dv_cur, void* stream) {
+                       float* dq, float* dk_cur, float* dv_cur, int flags, void* stream) {
     return guard([&] {
         set_dev(p);
         p->pt->check_layer(layer);
         OOMB_REQUIRE(tokens >= 1, OOMB_SHAPE_ERROR, "attn_backward: empty chunk");
         AttnGeom g = geom(p, tokens, layer);
+        if (flags & OOMB_ATTN_PAST_ONLY) g.chunk_keys = 0;
         OOMB_REQUIRE(sel->m == g.m, OOMB_SHAPE_ERROR, "attn_backward: one selected-page list per query page required");
         sel_host_sync(sel);
         for (int qp = 0; qp < g.m; ++qp)
@@ -828,6 +845,12 @@ int oomb_attn_backward(oomb_pool_t p, int layer, const void* dout, const void* q
                                  lse, dq, dk_cur, dv_cur, p->d_err, S(stream));
         }
     });
+}
+
+int oomb_attn_backward(oomb_pool_t p, int layer, const void* dout, const void* q, int64_t tokens,
+                       oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out, const float* lse,
+                       float* dq, float* dk_cur, float* dv_cur, void* stream) {
+    return oomb_attn_backward_ex(p, layer, dout, q, tokens, sel, k_cur, v_cur, out, lse, dq, dk_cur, dv_cur, 0, stream);
 }
 
 int oomb_accumulate_grad_pages(oomb_pool_t p, int layer, const int32_t* ids, int n, float* dk, float* dv,

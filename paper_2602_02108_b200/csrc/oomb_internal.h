@@ -135,6 +135,8 @@ struct AttnGeom {
     int64_t filled;  // layer fill level (valid-slot mask of past pages)
     float scale;   // 1/sqrt(hd)
     int max_pages;
+    int chunk_keys;  // 1: attend the chunk's causal prefix after the selected pages (attention.hpp:187-199);
+                     // 0: selected pages only (a page-range shard other than the one owning the chunk's keys)
 };
 
 // ---------------------------------------------------------------------------
@@ -167,6 +169,8 @@ void launch_zero_slots(const int32_t* d_slots, int n, float* gk, float* gv, int6
 void launch_score_simt(int dtype, const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, int64_t n,
                        int Hkv, int P, float scale, float* vote, float* stats_scratch, cudaStream_t st,
                        bool partial_only = false);
+void launch_lse_merge(const void* o_parts, const float* lse_parts, int parts, int64_t rows, int hd, int dtype,
+                      void* out, float* lse, cudaStream_t st);
 void launch_topk(const float* vote, int m, int n, int k, int32_t* sel_off, int32_t* sel_ids, cudaStream_t st);
 void launch_fill_csr_all(int32_t* off, int32_t* ids, int m, int first, int count, cudaStream_t st);
 

@@ -1,4 +1,8 @@
-"""KV-head-group sharding of the hot path across the GPUs of one node.
+"""Sharding of the hot path across the GPUs of one node.
+
+KV-head-group sharding (KVGroupShard) and, when groups run out (Qwen2.5-7B has 4 groups
+for 8 GPUs; c5 splits page ranges across 2/4/8 GPUs), the page-range split
+(PageRangeShard) with an exact LSE / output merge.
 
 Attention forward / backward and the gradient pool of different KV groups touch
 disjoint K/V/dK/dV head slices and disjoint q-heads, so a rank that owns a
@@ -116,3 +120,76 @@ def select_pages_topk_sharded(cache, layer: int, q_local: torch.Tensor, n_candid
              stream_handle(None))
     sel.vote = vote
     return sel
+
+
+# ---------------------------------------------------------------------------
+# Page-range split (SURVEY §8e "page-range split", c5)
+# ---------------------------------------------------------------------------
+@dataclass
+class PageRangeShard:
+    """Rank r of R owns the pages with id % R == r (interleaved ranges keep every rank's share
+    of a growing sequence balanced at every chunk) and attends, for every query page, the
+    selected pages it owns, in list order. Rank 0 also owns the chunk's own causal keys.
+
+    forward : partial (O_r, LSE_r) -> all-gather in rank order -> exact merge
+              LSE = ln sum_r e^{LSE_r}, O = sum_r e^{LSE_r - LSE} O_r   (oomb_lse_merge)
+    backward: with the merged (O, LSE) every rank's dK/dV for its own pages are exact and local;
+              the partial dQ are all-gathered and summed in rank order (deterministic, equal on
+              every rank); dk_cur / dv_cur come from rank 0 (the other ranks' are zero).
+    """
+    rank: int
+    world: int
+
+    def owns(self, page: int) -> bool:
+        return page % self.world == self.rank
+
+    def split_lists(self, lists) -> list[list[int]]:
+        return [[p for p in l if self.owns(p)] for l in lists]
+
+    @property
+    def past_only(self) -> bool:
+        return self.rank != 0
+
+
+def lse_merge(o_parts: torch.Tensor, lse_parts: torch.Tensor):
+    """o_parts [R, C, H, hd] (bf16 or fp32), lse_parts [R, C, H] fp32 -> (O [C, H, hd], LSE [C, H])."""
+    from .paged_kv import stream_handle
+    r, c, h, hd = o_parts.shape
+    out = torch.empty((c, h, hd), dtype=o_parts.dtype, device=o_parts.device)
+    lse = torch.empty((c, h), dtype=torch.float32, device=o_parts.device)
+    dtype = 1 if o_parts.dtype == torch.bfloat16 else 0
+    call("oomb_lse_merge", C.c_void_p(o_parts.contiguous().data_ptr()), C.c_void_p(lse_parts.contiguous().data_ptr()),
+         r, c * h, hd, dtype, C.c_void_p(out.data_ptr()), C.c_void_p(lse.data_ptr()), stream_handle(None))
+    return out, lse
+
+
+def _gather(x: torch.Tensor, group=None) -> torch.Tensor:
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return x.unsqueeze(0)
+    out = torch.empty((world,) + tuple(x.shape), dtype=x.dtype, device=x.device)
+    dist.all_gather_into_tensor(out, x.contiguous(), group=group)
+    return out
+
+
+def range_forward(shard: PageRangeShard, cfg, q, cache, layer, selected_lists, k_cur, v_cur, group=None):
+    """attn_forward on a page-range shard + the collective merge; returns the merged AttnSaved
+    (out, lse) and this rank's sub-selection (for the backward)."""
+    from . import attention as A
+    sub = A.Selection.from_lists(cache, shard.split_lists(selected_lists))
+    part = A.attn_forward(cfg, q, cache, layer, sub, k_cur, v_cur, past_only=shard.past_only)
+    out, lse = lse_merge(_gather(part.out, group), _gather(part.lse, group))
+    return A.AttnSaved(out, lse, sub), sub
+
+
+def range_backward(shard: PageRangeShard, cfg, dout, q, cache, layer, k_cur, v_cur, saved, group=None):
+    """attn_backward on a page-range shard with the merged (O, LSE); dQ summed over ranks in rank
+    order, dk_cur / dv_cur from rank 0. The rank's own pages' dK/dV land in its gradient pool."""
+    from . import attention as A
+    g = A.attn_backward(cfg, dout, q, cache, layer, k_cur, v_cur, saved, past_only=shard.past_only)
+    dq_parts = _gather(g.dq, group)
+    dq = fixed_order_sum(dq_parts.reshape(dq_parts.shape[0], 1, -1)).reshape(g.dq.shape)
+    dk = _gather(g.dk_cur, group)[0].clone()
+    dv = _gather(g.dv_cur, group)[0].clone()
+    return A.AttnGrads(dq, dk, dv)

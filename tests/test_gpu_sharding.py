@@ -57,3 +57,83 @@ def test_sharded_equals_unsharded_bitwise():
         assert torch.equal(gr.dq, g_full.dq[:, a:b])
         assert torch.equal(gr.dk_cur, g_full.dk_cur[:, ka:kb]) and torch.equal(gr.dv_cur, g_full.dv_cur[:, ka:kb])
         assert torch.equal(gp.k, gp_full.k[:, ka:kb]) and torch.equal(gp.v, gp_full.v[:, ka:kb])
+
+
+def _rel(a, b):
+    a, b = a.double(), b.double()
+    return float((a - b).norm() / max(b.norm(), 1e-30))
+
+
+@pytest.mark.parametrize("dtype,world", [("bf16", 2), ("bf16", 3), ("fp32", 2)])
+def test_page_range_split_matches_unsplit(dtype, world):
+    """Page-range split simulated on one GPU: R shards attend the pages they own
+    (id % R), shard 0 also the chunk's keys; the exact LSE merge of their partial outputs and the
+    rank-ordered sum of their partial dQ reproduce the unsplit layer, and the gradient pages of
+    every shard's own pages equal the unsplit ones (tolerances of BASELINE north_star)."""
+    from paper_2602_02108_b200 import ModelConfig, PagedCache
+    from paper_2602_02108_b200 import attention as A
+    from paper_2602_02108_b200.sharding import PageRangeShard, fixed_order_sum, lse_merge
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    tol = 2e-2 if dtype == "bf16" else 1e-5
+    cfg = ModelConfig(n_layers=1, n_q_heads=28, n_kv_heads=4, head_dim=128, chunk_size=512, page_size=128,
+                      retrieval_budget=5 * 128, attention_mode=["topk"])
+    g = torch.Generator(device="cuda").manual_seed(21 + world)
+    n_past = 14
+    past = torch.randn(n_past * 128, 4, 128, device="cuda", generator=g).to(tdt)
+    pv = torch.randn(n_past * 128, 4, 128, device="cuda", generator=g).to(tdt)
+    q = torch.randn(512, 28, 128, device="cuda", generator=g).to(tdt)
+    k = torch.randn(512, 4, 128, device="cuda", generator=g).to(tdt)
+    v = torch.randn(512, 4, 128, device="cuda", generator=g).to(tdt)
+    do = torch.randn(512, 28, 128, device="cuda", generator=g).to(tdt)
+    lists = [[0, 3, 5, 8, 13], [1, 2, 9, 11, 12], [4, 6, 7, 10, 0], [13, 12, 5]]
+
+    def layer():
+        c = PagedCache(cfg, dtype=dtype, max_tokens=8192)
+        c.append_chunk(0, past, pv)
+        c.append_chunk(0, k, v)
+        return c
+
+    full = layer()
+    s_full = A.attn_forward(cfg, q, full, 0, lists, k, v)
+    g_full = A.attn_backward(cfg, do, q, full, 0, k, v, s_full)
+    gp_full = full.gather_grad_pages(0, list(range(n_past)))
+
+    cache = layer()  # one pool stands in for the shards' pools: their pages are disjoint
+    shards = [PageRangeShard(r, world) for r in range(world)]
+    parts = []
+    subs = []
+    for sh in shards:
+        sub = A.Selection.from_lists(cache, sh.split_lists(lists))
+        subs.append(sub)
+        parts.append(A.attn_forward(cfg, q, cache, 0, sub, k, v, past_only=sh.past_only))
+    out, lse = lse_merge(torch.stack([p.out for p in parts]), torch.stack([p.lse for p in parts]))
+    assert _rel(out.float(), s_full.out.float()) < tol
+    assert _rel(lse, s_full.lse) < tol
+    dqs, dk0, dv0 = [], None, None
+    for sh, sub in zip(shards, subs):
+        saved = A.AttnSaved(out, lse, sub)
+        gr = A.attn_backward(cfg, do, q, cache, 0, k, v, saved, past_only=sh.past_only)
+        dqs.append(gr.dq.clone())
+        if sh.rank == 0:
+            dk0, dv0 = gr.dk_cur.clone(), gr.dv_cur.clone()
+        else:
+            assert torch.count_nonzero(gr.dk_cur) == 0 and torch.count_nonzero(gr.dv_cur) == 0
+    dq = fixed_order_sum(torch.stack(dqs).reshape(world, 1, -1)).reshape(g_full.dq.shape)
+    assert _rel(dq, g_full.dq) < tol
+    assert _rel(dk0, g_full.dk_cur) < tol and _rel(dv0, g_full.dv_cur) < tol
+    gp = cache.gather_grad_pages(0, list(range(n_past)))
+    assert _rel(gp.k, gp_full.k) < tol and _rel(gp.v, gp_full.v) < tol
+
+
+def test_lse_merge_single_part_is_identity_and_empty_parts_vanish():
+    from paper_2602_02108_b200.sharding import lse_merge
+    g = torch.Generator(device="cuda").manual_seed(3)
+    o = torch.randn(1, 64, 4, 128, device="cuda", generator=g)
+    l = torch.randn(1, 64, 4, device="cuda", generator=g)
+    out, lse = lse_merge(o, l)
+    assert torch.allclose(out, o[0], rtol=1e-6, atol=1e-6) and torch.allclose(lse, l[0], rtol=1e-6, atol=1e-6)
+    # a shard that attended nothing contributes lse = -inf, out = 0
+    o2 = torch.stack([o[0], torch.zeros_like(o[0])])
+    l2 = torch.stack([l[0], torch.full_like(l[0], float("-inf"))])
+    out2, lse2 = lse_merge(o2, l2)
+    assert torch.allclose(out2, o[0], rtol=1e-6, atol=1e-6) and torch.allclose(lse2, l[0], rtol=1e-6, atol=1e-6)

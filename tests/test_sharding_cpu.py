@@ -83,3 +83,65 @@ def test_shard_geometry():
         KVGroupShard(0, 8, 4, 28)
     x = torch.arange(2 * 28 * 3).reshape(2, 28, 3)
     assert torch.equal(sh.shard_q(x), x[:, 14:28])
+
+
+# ---------------------------------------------------------------------------
+# page-range split: ownership partition and the exact LSE merge (host math, gloo world 2)
+# ---------------------------------------------------------------------------
+def test_page_range_partition_is_exact():
+    from paper_2602_02108_b200.sharding import PageRangeShard
+    lists = [[0, 3, 5, 8, 13], [], [4, 6, 7, 10, 1], [13, 12]]
+    for world in (1, 2, 3, 8):
+        shards = [PageRangeShard(r, world) for r in range(world)]
+        for i, l in enumerate(lists):
+            parts = [sh.split_lists(lists)[i] for sh in shards]
+            assert sorted(x for p in parts for x in p) == sorted(l)          # every page exactly once
+            for p in parts:                                                   # list order kept
+                assert p == [x for x in l if x in p]
+        assert [sh.past_only for sh in shards] == [False] + [True] * (world - 1)
+
+
+def _merge_np(o_parts, lse_parts):
+    m = np.max(lse_parts, axis=0)
+    w = np.where(np.isneginf(lse_parts), 0.0, np.exp(lse_parts - m))
+    L = m + np.log(w.sum(axis=0))
+    return (np.exp(lse_parts - L)[..., None] * o_parts).sum(axis=0), L
+
+
+def _range_worker(rank, world, port, logits, vals, result):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2602_02108_b200.sharding import PageRangeShard
+        sh = PageRangeShard(rank, world)
+        keys = [k for k in range(logits.shape[1]) if sh.owns(k // 4)]  # 4 keys per "page"
+        s = logits[:, keys]
+        mx = s.max(axis=1)
+        p = np.exp(s - mx[:, None])
+        o = (p @ vals[keys]) / p.sum(axis=1)[:, None]
+        lse = mx + np.log(p.sum(axis=1))
+        go = [torch.zeros(o.shape, dtype=torch.float64) for _ in range(world)]
+        gl = [torch.zeros(lse.shape, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(go, torch.from_numpy(o))
+        dist.all_gather(gl, torch.from_numpy(lse))
+        out, L = _merge_np(np.stack([x.numpy() for x in go]), np.stack([x.numpy() for x in gl]))
+        result[rank] = (out, L)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_page_range_merge_over_gloo_equals_full_softmax():
+    rng = np.random.default_rng(0)
+    logits = rng.standard_normal((16, 40)) * 3
+    vals = rng.standard_normal((40, 8))
+    full_p = np.exp(logits - logits.max(axis=1, keepdims=True))
+    full_o = (full_p @ vals) / full_p.sum(axis=1)[:, None]
+    full_l = logits.max(axis=1) + np.log(full_p.sum(axis=1))
+    mgr = mp.Manager()
+    result = mgr.dict()
+    mp.spawn(_range_worker, args=(2, _free_port(), logits, vals, result), nprocs=2, join=True)
+    for r in range(2):
+        out, L = result[r]
+        assert np.allclose(out, full_o, rtol=1e-12, atol=1e-12) and np.allclose(L, full_l, rtol=1e-12, atol=1e-12)
+    assert np.array_equal(result[0][0], result[1][0])
