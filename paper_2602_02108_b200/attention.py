@@ -50,14 +50,23 @@ class Selection:
         s._keep = (off, ids)
         return s
 
-    def lists(self) -> list[list[int]]:
+    def csr(self) -> tuple[np.ndarray, np.ndarray]:
+        """(offsets [m+1], ids [nnz]) int32 from the host mirror (waits for the selection's D2H)."""
         m, nnz = C.c_int(), C.c_int()
         call("oomb_selection_get_host", self.handle, None, None, C.byref(m), C.byref(nnz))
         off = np.zeros(m.value + 1, np.int32)
         ids = np.zeros(max(nnz.value, 1), np.int32)
         call("oomb_selection_get_host", self.handle, off.ctypes.data_as(C.c_void_p), ids.ctypes.data_as(C.c_void_p),
              C.byref(m), C.byref(nnz))
-        return [ids[off[i]:off[i + 1]].tolist() for i in range(m.value)]
+        return off, ids[:nnz.value]
+
+    def union(self) -> np.ndarray:
+        """Ascending distinct selected page ids (the residency working set of the selection)."""
+        return np.unique(self.csr()[1])
+
+    def lists(self) -> list[list[int]]:
+        off, ids = self.csr()
+        return [ids[off[i]:off[i + 1]].tolist() for i in range(len(off) - 1)]
 
     def __len__(self) -> int:
         off, ids, m = C.c_void_p(), C.c_void_p(), C.c_int()

@@ -47,12 +47,12 @@ class AttentionChunkLoop:
             call("oomb_select_all", sel.handle, n_cand, self.m, stream_handle(stream))
         return sel
 
-    def own_pages(self, i: int) -> list[int]:
-        return list(range(i * self.m, (i + 1) * self.m))
+    def own_pages(self, i: int) -> np.ndarray:
+        return np.arange(i * self.m, (i + 1) * self.m, dtype=np.int32)
 
     @staticmethod
-    def union(sel: A.Selection) -> list[int]:
-        return sorted(set(x for l in sel.lists() for x in l))
+    def union(sel: A.Selection) -> np.ndarray:
+        return sel.union()
 
     def forward_chunk(self, i: int, q, k, v, stream=None) -> A.AttnSaved:
         if i >= len(self.sels):
@@ -74,7 +74,7 @@ class AttentionChunkLoop:
             eng.record_access(self.layer, ids, i)
         saved = A.attn_forward(self.cfg, q, self.cache, self.layer, sel, k, v, stream=stream)
         if eng is not None:
-            eng.end_layer_use(self.layer, self.union(sel) + self.own_pages(i))
+            eng.end_layer_use(self.layer, np.concatenate([ids, self.own_pages(i)]))
         if i < len(self.saved):
             self.saved[i] = saved
         else:
@@ -84,12 +84,12 @@ class AttentionChunkLoop:
     def backward_chunk(self, i: int, dout, q, k, v, stream=None, prefetch_next: bool = True) -> A.AttnGrads:
         eng = self.engine
         sel = self.sels[i]
-        ids = sorted(set(self.union(sel)) | set(self.own_pages(i)))
         if eng is not None:
+            ids = np.union1d(self.union(sel), self.own_pages(i)).astype(np.int32)
             eng.wait(eng.fetch_async(self.layer, ids, i))
             eng.record_access(self.layer, ids, i)
             if prefetch_next and i > 0:  # step-ahead prefetch with cached ids + own grad pages
-                nxt = sorted(set(self.union(self.sels[i - 1])) | set(self.own_pages(i - 1)))
+                nxt = np.union1d(self.union(self.sels[i - 1]), self.own_pages(i - 1)).astype(np.int32)
                 self._pending = eng.fetch_async(self.layer, nxt, i - 1, best_effort=True)
         g = A.attn_backward(self.cfg, dout, q, self.cache, self.layer, k, v, self.saved[i], stream=stream)
         if eng is not None:

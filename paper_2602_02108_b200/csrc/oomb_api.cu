@@ -336,10 +336,7 @@ int oomb_pool_destroy(oomb_pool_t p) {
     cudaFree(p->d_kavg_cnt);
     cudaFree(p->d_err);
     cudaFree(p->bwd_ws);
-    for (auto e : p->kv_ev)
-        if (e) cudaEventDestroy(e);
-    for (auto e : p->g_ev)
-        if (e) cudaEventDestroy(e);
+    if (p->wb_done) cudaEventDestroy(p->wb_done);
     for (auto& r : p->prof.recs) {
         cudaEventDestroy(r.e0);
         cudaEventDestroy(r.e1);

@@ -176,20 +176,32 @@ struct oomb_pool_s {
     size_t bwd_ws_bytes = 0;
     bool prof_on = false;
     Profiler prof;
-    // Per-slot "last write-back out of this slot" events (offload engine). A stream that
-    // is about to write into a recycled slot waits on it first.
-    std::vector<cudaEvent_t> kv_ev, g_ev;
+    // Write-back tickets (offload engine): a slot freed by an eviction carries the number of
+    // the D2H batch that reads it out; `wb_done` is recorded on the (in-order) D2H stream after
+    // the newest batch, so waiting on it covers every older ticket. A stream about to write into
+    // a recycled slot waits once per newer ticket, not once per slot.
+    std::vector<uint64_t> kv_ticket, g_ticket;
+    uint64_t wb_ticket = 0;            // newest write-back batch
+    cudaEvent_t wb_done = nullptr;     // recorded after batch wb_ticket
+    std::vector<std::pair<cudaStream_t, uint64_t>> waited;  // newest ticket each stream has waited for
 
-    cudaEvent_t kv_slot_event(int32_t s) { return slot_event(kv_ev, s, n_kv_slots); }
-    cudaEvent_t g_slot_event(int32_t s) { return slot_event(g_ev, s, n_g_slots); }
-    cudaEvent_t slot_event(std::vector<cudaEvent_t>& v, int32_t s, int64_t n) {
-        if (v.empty()) v.assign(n, nullptr);
-        if (!v[s]) OOMB_CUDA(cudaEventCreateWithFlags(&v[s], cudaEventDisableTiming));
-        return v[s];
+    void free_slot_after_writeback(bool grad, int32_t s) {
+        auto& v = grad ? g_ticket : kv_ticket;
+        if (v.empty()) v.assign(grad ? n_g_slots : n_kv_slots, 0);
+        v[s] = wb_ticket;
     }
     void wait_slot(bool grad, int32_t s, cudaStream_t st) {
-        auto& v = grad ? g_ev : kv_ev;
-        if (!v.empty() && v[s]) OOMB_CUDA(cudaStreamWaitEvent(st, v[s], 0));
+        const auto& v = grad ? g_ticket : kv_ticket;
+        if (v.empty() || v[s] == 0 || !wb_done) return;
+        for (auto& w : waited)
+            if (w.first == st) {
+                if (w.second >= v[s]) return;
+                OOMB_CUDA(cudaStreamWaitEvent(st, wb_done, 0));
+                w.second = wb_ticket;
+                return;
+            }
+        OOMB_CUDA(cudaStreamWaitEvent(st, wb_done, 0));
+        waited.emplace_back(st, wb_ticket);
     }
 
     int32_t* kvslot_layer(int l) { return d_kvslot + static_cast<int64_t>(l) * max_pages; }

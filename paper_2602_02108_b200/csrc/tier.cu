@@ -139,7 +139,24 @@ struct oomb_tier_s {
     // `on`: the stream whose timeline stamps the event in real mode (the compute stream may be the
     // legacy default stream, i.e. a null handle, so the choice is explicit rather than a pointer).
     enum On { ON_NONE = 0, ON_COMPUTE, ON_H2D, ON_D2H };
-    void push(int kind, double t, int layer, int32_t page, uint64_t bytes, int chunk, On on = ON_NONE) {
+    // Real-mode log timestamps: one CUDA event per engine operation and stream, shared by every
+    // log entry it stamps (one event per page would be one API call per page). `stamp` records
+    // now; `later` creates an event that the caller records once the batch it stamps is enqueued.
+    std::vector<cudaEvent_t> log_events;  // owned, destroyed with the engine
+    cudaStream_t stream_of(On on) const { return on == ON_COMPUTE ? compute : (on == ON_H2D ? h2d_stream : d2h_stream); }
+    cudaEvent_t later() {
+        if (!real()) return nullptr;
+        cudaEvent_t e;
+        OOMB_CUDA(cudaEventCreate(&e));
+        log_events.push_back(e);
+        return e;
+    }
+    cudaEvent_t stamp(On on) {
+        cudaEvent_t e = later();
+        if (e) OOMB_CUDA(cudaEventRecord(e, stream_of(on)));
+        return e;
+    }
+    void push(int kind, double t, int layer, int32_t page, uint64_t bytes, int chunk, cudaEvent_t ev = nullptr) {
         LogEv le{};
         le.e.kind = kind;
         le.e.t = t;
@@ -148,12 +165,50 @@ struct oomb_tier_s {
         le.e.chunk = chunk;
         le.e.bytes = bytes;
         le.e.phase = phase;
-        le.ev = nullptr;
-        if (real() && on != ON_NONE) {
-            le.ev = new_event();
-            OOMB_CUDA(cudaEventRecord(le.ev, on == ON_COMPUTE ? compute : (on == ON_H2D ? h2d_stream : d2h_stream)));
-        }
+        le.ev = ev;
         log.push_back(le);
+    }
+
+    // ---- batched page copies (real mode): one cudaMemcpyBatchAsync per direction and operation
+    std::vector<void*> cp_dst[2], cp_src[2];
+    std::vector<size_t> cp_size[2];
+    cudaEvent_t d2h_batch_ev = nullptr;  // the current write-back batch's completion stamp
+    void queue_copy(int dir, void* dst, const void* src, size_t n) {  // dir 0: H2D, 1: D2H
+        cp_dst[dir].push_back(dst);
+        cp_src[dir].push_back(const_cast<void*>(src));
+        cp_size[dir].push_back(n);
+    }
+    void flush_copies(int dir) {
+        if (cp_dst[dir].empty()) return;
+        cudaMemcpyAttributes attr{};
+        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+        size_t idx0 = 0, fail = 0;
+        OOMB_CUDA(cudaMemcpyBatchAsync(cp_dst[dir].data(), cp_src[dir].data(), cp_size[dir].data(), cp_dst[dir].size(),
+                                       &attr, &idx0, 1, &fail, dir ? d2h_stream : h2d_stream));
+        cp_dst[dir].clear();
+        cp_src[dir].clear();
+        cp_size[dir].clear();
+    }
+    // A write-back batch: the D2H stream follows everything enqueued on the compute stream so
+    // far, then copies every evicted page, then stamps the batch; slots freed by it carry its
+    // ticket (pool.h) so a later write into a recycled slot waits for the read-out.
+    void begin_writeback() {
+        if (!real()) return;
+        cudaEvent_t tail = new_event();
+        OOMB_CUDA(cudaEventRecord(tail, compute));
+        OOMB_CUDA(cudaStreamWaitEvent(d2h_stream, tail, 0));
+        spare_events.push_back(tail);
+        ++pool->wb_ticket;
+        d2h_batch_ev = later();
+    }
+    void end_writeback() {
+        if (!real()) return;
+        flush_copies(1);
+        if (!pool->wb_done) OOMB_CUDA(cudaEventCreateWithFlags(&pool->wb_done, cudaEventDisableTiming));
+        OOMB_CUDA(cudaEventRecord(pool->wb_done, d2h_stream));
+        OOMB_CUDA(cudaEventRecord(d2h_batch_ev, d2h_stream));
+        d2h_batch_ev = nullptr;
     }
 
     // ---- device table publication (real mode)
@@ -184,31 +239,40 @@ struct oomb_tier_s {
     }
 
     void enforce_capacity(int64_t incoming) {
+        // The reference evicts one page at a time, each time the non-reserved resident page with
+        // the smallest (pinned, lru) key (tiered_memory.hpp:341-384). Evicting a page changes no
+        // other page's key, so the victims are exactly the `need` smallest keys in ascending order:
+        // one scan + partial sort gives the same evictions and log, O(n + k log k) instead of O(n k).
         if (cfg.device_capacity_pages < 0) return;
         sync_pages();
-        while (device_page_count() + incoming > cfg.device_capacity_pages) {
-            int best_l = -1, best_p = -1;
-            bool best_pinned = true;
-            uint64_t best_lru = std::numeric_limits<uint64_t>::max();
-            for (int l = 0; l < pt->n_layers; ++l) {
-                for (size_t p = 0; p < pages[l].size(); ++p) {
-                    const PageState& ps = pages[l][p];
-                    if (tier(l, static_cast<int>(p)) != 0 || ps.reserved) continue;
-                    if (std::make_pair(ps.pinned, ps.lru) < std::make_pair(best_pinned, best_lru)) {
-                        best_pinned = ps.pinned;
-                        best_lru = ps.lru;
-                        best_l = l;
-                        best_p = static_cast<int>(p);
-                    }
-                }
+        const int64_t need = device_page_count() + incoming - cfg.device_capacity_pages;
+        if (need <= 0) return;
+        struct Cand {
+            bool pinned;
+            uint64_t lru;
+            int l, p;
+        };
+        std::vector<Cand> cand;
+        for (int l = 0; l < pt->n_layers; ++l)
+            for (size_t p = 0; p < pages[l].size(); ++p) {
+                const PageState& ps = pages[l][p];
+                if (tier(l, static_cast<int>(p)) != 0 || ps.reserved) continue;
+                cand.push_back({ps.pinned, ps.lru, l, static_cast<int>(p)});
             }
-            if (best_l < 0)
-                throw Error(OOMB_CONFIG_ERROR,
-                            "tiered_memory: device capacity smaller than the working set (capacity " +
-                                std::to_string(cfg.device_capacity_pages) + " pages)");
-            pages[best_l][best_p].pinned = false;
-            evict(best_l, best_p);
+        const size_t k = std::min<size_t>(cand.size(), static_cast<size_t>(need));
+        auto key_less = [](const Cand& a, const Cand& b) {
+            return std::make_pair(a.pinned, a.lru) < std::make_pair(b.pinned, b.lru);
+        };
+        std::partial_sort(cand.begin(), cand.begin() + k, cand.end(), key_less);
+        begin_writeback();
+        for (size_t i = 0; i < k; ++i) {
+            pages[cand[i].l][cand[i].p].pinned = false;
+            evict(cand[i].l, cand[i].p);
         }
+        end_writeback();
+        if (static_cast<int64_t>(k) < need)
+            throw Error(OOMB_CONFIG_ERROR, "tiered_memory: device capacity smaller than the working set (capacity " +
+                                               std::to_string(cfg.device_capacity_pages) + " pages)");
     }
 
     // ---- eviction (tiered_memory.hpp:386-403)
@@ -229,43 +293,34 @@ struct oomb_tier_s {
         }
         if (real()) real_evict(layer, page, wb_kv, wb_grad);
         set_tier(layer, page, 1);
-        push(EV_EVICT, clock, layer, page, bytes, -1, ON_D2H);
+        push(EV_EVICT, clock, layer, page, bytes, -1, d2h_batch_ev);
     }
 
     void real_evict(int layer, int page, bool wb_kv, bool wb_grad) {
         auto& p = *pool;
         const int32_t ks = p.kvslot[layer][page], gs = p.gslot[layer][page];
-        // the copies must follow every kernel already enqueued on the compute stream
-        cudaEvent_t tail = new_event();
-        OOMB_CUDA(cudaEventRecord(tail, compute));
-        OOMB_CUDA(cudaStreamWaitEvent(d2h_stream, tail, 0));
-        spare_events.push_back(tail);
         const size_t hidx = static_cast<size_t>(layer) * p.max_pages + page;
         const size_t kvb = static_cast<size_t>(p.page_elems) * p.elem;
         const size_t gb = static_cast<size_t>(p.page_elems) * sizeof(float);
         PageState& ps = pages[layer][page];
         if (wb_kv && ks >= 0) {
             uint8_t* h = host_kv + hidx * kv_block;
-            OOMB_CUDA(cudaMemcpyAsync(h, static_cast<uint8_t*>(p.kpool) + ks * kvb, kvb, cudaMemcpyDeviceToHost,
-                                      d2h_stream));
-            OOMB_CUDA(cudaMemcpyAsync(h + kvb, static_cast<uint8_t*>(p.vpool) + ks * kvb, kvb, cudaMemcpyDeviceToHost,
-                                      d2h_stream));
+            queue_copy(1, h, static_cast<uint8_t*>(p.kpool) + ks * kvb, kvb);
+            queue_copy(1, h + kvb, static_cast<uint8_t*>(p.vpool) + ks * kvb, kvb);
             ps.host_has_kv = true;
         }
         if (wb_grad && gs >= 0) {
             uint8_t* h = host_grad + hidx * grad_block;
-            OOMB_CUDA(cudaMemcpyAsync(h, reinterpret_cast<uint8_t*>(p.gkpool) + gs * gb, gb, cudaMemcpyDeviceToHost,
-                                      d2h_stream));
-            OOMB_CUDA(cudaMemcpyAsync(h + gb, reinterpret_cast<uint8_t*>(p.gvpool) + gs * gb, gb,
-                                      cudaMemcpyDeviceToHost, d2h_stream));
+            queue_copy(1, h, reinterpret_cast<uint8_t*>(p.gkpool) + gs * gb, gb);
+            queue_copy(1, h + gb, reinterpret_cast<uint8_t*>(p.gvpool) + gs * gb, gb);
             ps.host_has_grad = true;
         }
         if (ks >= 0) {
-            OOMB_CUDA(cudaEventRecord(p.kv_slot_event(ks), d2h_stream));
+            p.free_slot_after_writeback(false, ks);
             p.kv_free.push_back(ks);
         }
         if (gs >= 0) {
-            OOMB_CUDA(cudaEventRecord(p.g_slot_event(gs), d2h_stream));
+            p.free_slot_after_writeback(true, gs);
             p.g_free.push_back(gs);
         }
         p.kvslot[layer][page] = -1;
@@ -296,20 +351,16 @@ struct oomb_tier_s {
         p.kvslot[layer][page] = ks;
         if (ps.host_has_kv) {
             const uint8_t* h = host_kv + hidx * kv_block;
-            OOMB_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(p.kpool) + ks * kvb, h, kvb, cudaMemcpyHostToDevice,
-                                      h2d_stream));
-            OOMB_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(p.vpool) + ks * kvb, h + kvb, kvb, cudaMemcpyHostToDevice,
-                                      h2d_stream));
+            queue_copy(0, static_cast<uint8_t*>(p.kpool) + ks * kvb, h, kvb);
+            queue_copy(0, static_cast<uint8_t*>(p.vpool) + ks * kvb, h + kvb, kvb);
         }
         if (grads_allocated(layer, page)) {
             const int32_t gs = take_slot(true, h2d_stream, "gradient");
             p.gslot[layer][page] = gs;
             if (ps.host_has_grad) {
                 const uint8_t* h = host_grad + hidx * grad_block;
-                OOMB_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(p.gkpool) + gs * gb, h, gb,
-                                          cudaMemcpyHostToDevice, h2d_stream));
-                OOMB_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(p.gvpool) + gs * gb, h + gb, gb,
-                                          cudaMemcpyHostToDevice, h2d_stream));
+                queue_copy(0, reinterpret_cast<uint8_t*>(p.gkpool) + gs * gb, h, gb);
+                queue_copy(0, reinterpret_cast<uint8_t*>(p.gvpool) + gs * gb, h + gb, gb);
             } else {
                 OOMB_CUDA(cudaMemsetAsync(reinterpret_cast<uint8_t*>(p.gkpool) + gs * gb, 0, gb, h2d_stream));
                 OOMB_CUDA(cudaMemsetAsync(reinterpret_cast<uint8_t*>(p.gvpool) + gs * gb, 0, gb, h2d_stream));
@@ -323,12 +374,13 @@ struct oomb_tier_s {
         if (e <= b) return;
         const int first = static_cast<int>(b / pt->P);
         const int last = static_cast<int>((e - 1) / pt->P);
+        cudaEvent_t ev = stamp(ON_COMPUTE);
         for (int p = first; p <= last; ++p) {
             PageState& ps = state(layer, p);
             ps.kv_host_valid = false;
             ps.reserved = true;
             ps.lru = ++lru_counter;
-            push(EV_FETCH_DONE, clock, layer, p, 0, -1, ON_COMPUTE);
+            push(EV_FETCH_DONE, clock, layer, p, 0, -1, ev);
         }
         enforce_capacity(0);
     }
@@ -374,10 +426,12 @@ struct oomb_tier_s {
                 }
             }
         }
+        cudaEvent_t ev_issue = to_transfer.empty() ? nullptr : stamp(ON_H2D);
+        cudaEvent_t ev_done = to_transfer.empty() ? nullptr : later();
         for (int32_t p : to_transfer) {
             PageState& ps = state(layer, p);
             const uint64_t bytes = page_transfer_bytes(layer, p);
-            push(EV_FETCH_ISSUED, clock, layer, p, 0, chunk, ON_H2D);
+            push(EV_FETCH_ISSUED, clock, layer, p, 0, chunk, ev_issue);
             const double start = std::max({h2d_free, clock, ps.writeback_done});
             const double done = start + static_cast<double>(bytes) / cfg.bandwidth_bytes_per_s;
             h2d_free = done;
@@ -385,11 +439,13 @@ struct oomb_tier_s {
             if (phase == 0) h2d_fwd += bytes;
             else h2d_bwd += bytes;
             if (real()) real_fetch(layer, p);
-            push(EV_FETCH_DONE, done, layer, p, bytes, chunk, ON_H2D);
+            push(EV_FETCH_DONE, done, layer, p, bytes, chunk, ev_done);
             ready = std::max(ready, done);
             tr.pages.push_back(p);
         }
         if (real()) {
+            flush_copies(0);
+            if (ev_done) OOMB_CUDA(cudaEventRecord(ev_done, h2d_stream));
             tr.ev = new_event();
             OOMB_CUDA(cudaEventRecord(tr.ev, h2d_stream));
         }
@@ -407,10 +463,18 @@ struct oomb_tier_s {
             clock = tr.ready;
         }
         if (real() && tr.ev) OOMB_CUDA(cudaStreamWaitEvent(compute, tr.ev, 0));
+        // The reference enforces capacity for one incoming page before each page turns resident;
+        // the pages of this transfer are not eviction candidates either way (still host-tier, or
+        // already resident and reserved), so one enforcement for all of them evicts the same pages
+        // in the same order.
+        std::set<int32_t> coming;
+        for (int32_t p : tr.pages)
+            if (tier(tr.layer, p) != 0) coming.insert(p);
+        const int64_t incoming = static_cast<int64_t>(coming.size());
+        if (incoming > 0) enforce_capacity(incoming);
         for (int32_t p : tr.pages) {
             PageState& ps = state(tr.layer, p);
             if (tier(tr.layer, p) == 0) continue;
-            enforce_capacity(1);
             set_tier(tr.layer, p, 0);
             ps.in_flight_done = 0;
             ps.reserved = true;
@@ -424,18 +488,19 @@ struct oomb_tier_s {
 
     void record_access(int layer, const int32_t* ids, int n, int chunk) {  // :256-264
         flush_table();
+        cudaEvent_t ev = n > 0 ? stamp(ON_COMPUTE) : nullptr;
         for (int i = 0; i < n; ++i) {
             const int32_t p = ids[i];
             if (tier(layer, p) != 0) throw Error(OOMB_RESIDENCY_ERROR, "access to non-resident page " + std::to_string(p));
             state(layer, p).lru = ++lru_counter;
-            push(EV_ACCESS, clock, layer, p, 0, chunk, ON_COMPUTE);
+            push(EV_ACCESS, clock, layer, p, 0, chunk, ev);
         }
     }
 
     void advance_compute(double seconds, int chunk, int layer) {
-        push(EV_COMPUTE_BEGIN, clock, layer, -1, 0, chunk, ON_COMPUTE);
+        push(EV_COMPUTE_BEGIN, clock, layer, -1, 0, chunk, stamp(ON_COMPUTE));
         clock += seconds;
-        push(EV_COMPUTE_END, clock, layer, -1, 0, chunk, ON_COMPUTE);
+        push(EV_COMPUTE_END, clock, layer, -1, 0, chunk, stamp(ON_COMPUTE));
     }
 
     void end_layer_use(int layer, const int32_t* ids, int n) {  // :274-280
@@ -508,8 +573,7 @@ int oomb_tier_destroy(oomb_tier_t t) {
         cudaSetDevice(t->pool->device);
         cudaDeviceSynchronize();
         t->pool->enforce = false;
-        for (auto& le : t->log)
-            if (le.ev) cudaEventDestroy(le.ev);
+        for (auto e : t->log_events) cudaEventDestroy(e);
         for (auto& tr : t->transfers)
             if (tr.ev) cudaEventDestroy(tr.ev);
         for (auto e : t->spare_events) cudaEventDestroy(e);
