@@ -29,6 +29,10 @@ using namespace tc;
 namespace {
 
 constexpr int kQpGroup = 8;  // query pages per vote CTA
+#ifndef OOMB_SCORE_POLY
+#define OOMB_SCORE_POLY 4
+#endif
+constexpr int kScPoly = OOMB_SCORE_POLY;  // 0: every exp2 on MUFU
 
 __global__ void kavg_prep_kernel(const float* __restrict__ sum, const int32_t* __restrict__ cnt,
                                  const float* __restrict__ kavg_f32, int n, int n_pad, int Hkv, int hd,
@@ -182,7 +186,10 @@ __global__ void __launch_bounds__(384, 1)
             if (m_new == -INFINITY) continue;  // every column so far is padding
             float a8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int c = 0; c < 64; ++c) a8[c & 7] += ex2(fmaf(__uint_as_float(sv[c]), p.sl2, -m_new));
+            for (int c = 0; c < 64; ++c) {  // 1 in kScPoly exponentials on the FMA pipe (MUFU-bound pass)
+                const float x = fmaf(__uint_as_float(sv[c]), p.sl2, -m_new);
+                a8[c & 7] += (kScPoly > 0 && c % kScPoly == kScPoly - 1) ? ex2_poly4(x) : ex2(x);
+            }
             const float acc = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
             l = (m == -INFINITY ? 0.f : l * ex2(m - m_new)) + acc;
             m = m_new;
@@ -343,7 +350,10 @@ __global__ void __launch_bounds__(384, 1)
                 acc4[0] = fmaf(ex2(fmaf(__uint_as_float(sv[c4 * 4 + 0]), p.sl2, -mm.x)), ll.x, acc4[0]);
                 acc4[1] = fmaf(ex2(fmaf(__uint_as_float(sv[c4 * 4 + 1]), p.sl2, -mm.y)), ll.y, acc4[1]);
                 acc4[2] = fmaf(ex2(fmaf(__uint_as_float(sv[c4 * 4 + 2]), p.sl2, -mm.z)), ll.z, acc4[2]);
-                acc4[3] = fmaf(ex2(fmaf(__uint_as_float(sv[c4 * 4 + 3]), p.sl2, -mm.w)), ll.w, acc4[3]);
+                {
+                    const float x3 = fmaf(__uint_as_float(sv[c4 * 4 + 3]), p.sl2, -mm.w);
+                    acc4[3] = fmaf((kScPoly > 0 && (c4 % (kScPoly > 0 ? kScPoly / 4 + (kScPoly < 4) : 1)) == 0) ? ex2_poly4(x3) : ex2(x3), ll.w, acc4[3]);
+                }
             }
             mbar_arrive(&bars->q_empty[st]);  // this stage's stats are consumed (no reuse / parity aliasing)
             if (++cnt == per_qp) {  // every (head, tile) of this query page: add the two groups' partials
