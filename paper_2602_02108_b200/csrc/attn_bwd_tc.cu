@@ -27,6 +27,11 @@ using namespace tc;
 
 namespace {
 
+#ifndef OOMB_BWD_POLY
+#define OOMB_BWD_POLY 0  // measured: no gain (the P phase is latency-, not MUFU-bound)
+#endif
+constexpr bool kBwdPoly = OOMB_BWD_POLY != 0;  // one in four exp2 of P on the FMA pipe (ex2_poly)
+
 
 // ---------------------------------------------------------------- workspace
 struct BwdWs {
@@ -343,9 +348,15 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_before();
                 mbar_arrive(&bars->s_free);
 #pragma unroll
-                for (int c = 0; c < 32; ++c) pr[c] = ex2(fmaf(__uint_as_float(a[c]), sl2, -L2));
+                for (int c = 0; c < 32; ++c) {
+                    const float x = fmaf(__uint_as_float(a[c]), sl2, -L2);
+                    pr[c] = (kBwdPoly && (c & 3) == 3) ? ex2_poly(x) : ex2(x);
+                }
 #pragma unroll
-                for (int c = 0; c < 32; ++c) pr[32 + c] = ex2(fmaf(__uint_as_float(b2[c]), sl2, -L2));
+                for (int c = 0; c < 32; ++c) {
+                    const float x = fmaf(__uint_as_float(b2[c]), sl2, -L2);
+                    pr[32 + c] = (kBwdPoly && (c & 3) == 3) ? ex2_poly(x) : ex2(x);
+                }
             }
             if (lim < 63) {
 #pragma unroll
@@ -746,7 +757,10 @@ __global__ void __launch_bounds__(384, 1)
                         pr[c2 * 32 + 4 * c4 + 0] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 0]), sl2, -l4.x));
                         pr[c2 * 32 + 4 * c4 + 1] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 1]), sl2, -l4.y));
                         pr[c2 * 32 + 4 * c4 + 2] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 2]), sl2, -l4.z));
-                        pr[c2 * 32 + 4 * c4 + 3] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 3]), sl2, -l4.w));
+                        {  // one in four exponentials on the FMA pipe (P is rounded to bf16)
+                            const float x3 = fmaf(__uint_as_float(sv[4 * c4 + 3]), sl2, -l4.w);
+                            pr[c2 * 32 + 4 * c4 + 3] = kBwdPoly ? ex2_poly(x3) : ex2(x3);
+                        }
                     }
                 }
                 if (masked) {
