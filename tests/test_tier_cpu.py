@@ -308,3 +308,21 @@ def test_validator_flags_access_before_fetch():
             bad = [OombEvent(5, 0, rogue.page, -1, 0, 0, 0, 0.0)] + evs
             v = validate_schedule(bad, 1e9).violations
             assert v and v[0].startswith("access before fetch_done") and f"page={rogue.page}" in v[0]
+
+
+def test_reports_in_reference_formats():
+    """memory_report_to_json (paged_kv.cpp:13-22) and the CLI's retrieval.csv (chunktrain.cpp:115-130)."""
+    import io
+    from paper_2602_02108_b200.reports import emit_retrieval_csv, memory_report_to_json
+    from paper_2602_02108_b200.tiered_memory import HostPageTable
+    pt = HostPageTable(n_layers=2, page_size=4, n_kv_heads=1, head_dim=2)
+    pt.append_chunk(0, 8)
+    pt.scatter_add_grads(0, [1])
+    rep = pt.memory_report()
+    s = memory_report_to_json(rep)
+    assert s == ('{"copied_bytes":0,"device_bytes":%d,"grad_bytes":%d,"host_bytes":0,"pages":2,"reallocs":0}'
+                 % (rep.device_bytes, rep.grad_bytes))
+    assert rep.device_bytes == 2 * pt.page_kv_bytes() and rep.grad_bytes > 0
+    buf = io.StringIO()
+    emit_retrieval_csv(buf, 7, [(0, [[[], []], [[], []]]), (1, [[[0, 1], [1]], [[0], []]])])
+    assert buf.getvalue() == "7,1,0,2,0\n7,1,0,2,1\n7,1,0,3,1\n7,1,1,2,0\n"
