@@ -106,6 +106,17 @@ OOMB_API int oomb_check_device_errors(oomb_pool_t pool);
  * Writes tail slots in place and updates the K_avg fp32 sums in append order. */
 OOMB_API int oomb_append_chunk(oomb_pool_t pool, int layer, const void* k, const void* v, int64_t rows, void* stream,
                       int64_t* slot_begin, int64_t* slot_end);
+/* Fused projection epilogue (chunk_trainer.hpp:424-432): k_raw is the PRE-RoPE
+ * key projection; every row is rotated at its absolute position (ops.hpp:192-225, angles and trig
+ * in double) on its way into the page, and K_avg accumulates the rotated keys — the rotated K is
+ * never written back to HBM separately. Same slot semantics as oomb_append_chunk. */
+OOMB_API int oomb_append_chunk_rope(oomb_pool_t pool, int layer, const void* k_raw, const void* v, int64_t rows,
+                                    float rope_base, void* stream, int64_t* slot_begin, int64_t* slot_end);
+/* rope / rope_backward (ops.hpp:192-230) over [rows][heads][hd]: row r at position pos_offset + r,
+ * sign +1 forward, -1 backward (the inverse rotation). dtypes OOMB_F32 / OOMB_BF16; out may
+ * alias x. */
+OOMB_API int oomb_rope(const void* x, int64_t rows, int heads, int hd, int64_t pos_offset, float base, int sign,
+                       int in_dtype, int out_dtype, void* out, void* stream);
 OOMB_API int oomb_n_pages(oomb_pool_t pool, int layer, int* n_pages);   /* paged_kv.hpp:62 */
 OOMB_API int oomb_filled(oomb_pool_t pool, int layer, int64_t* filled); /* paged_kv.hpp:61 */
 /* Reference arena ids {k_phys, v_phys, gk_phys, gv_phys} per logical page (PageEntry paged_kv.hpp:256-262). */

@@ -48,6 +48,8 @@ _PROTOS = {
     "oomb_memory_report_get": [VP, C.POINTER(OombMemoryReport)],
     "oomb_check_device_errors": [VP],
     "oomb_append_chunk": [VP, I, VP, VP, I64, VP, C.POINTER(I64), C.POINTER(I64)],
+    "oomb_append_chunk_rope": [VP, I, VP, VP, I64, C.c_float, VP, C.POINTER(I64), C.POINTER(I64)],
+    "oomb_rope": [VP, I64, I, I, I64, C.c_float, I, I, I, VP, VP],
     "oomb_n_pages": [VP, I, C.POINTER(I)],
     "oomb_filled": [VP, I, C.POINTER(I64)],
     "oomb_page_table_get": [VP, I, VP],

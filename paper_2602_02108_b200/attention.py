@@ -236,6 +236,20 @@ def attn_backward(cfg: ModelConfig, dout, q, cache: PagedCache, layer: int, k_cu
     return AttnGrads(dq, dk, dv)
 
 
+def rope(x: torch.Tensor, pos_offset: int, base: float = 10000.0, sign: int = 1, out=None,
+         out_dtype=None) -> torch.Tensor:
+    """ops.hpp:192-225 (sign -1: rope_backward, ops.hpp:227-230) on the device, [rows, heads, hd]."""
+    if x.dim() != 3:
+        raise ShapeError("rope: expected [t x h x d]")
+    x = x.contiguous() if x.is_cuda else x.cuda().contiguous()
+    odt = out_dtype or x.dtype
+    out = torch.empty(x.shape, dtype=odt, device=x.device) if out is None else out
+    code = {torch.float32: 0, torch.bfloat16: 1}
+    call("oomb_rope", _ptr(x), x.shape[0], x.shape[1], x.shape[2], int(pos_offset), C.c_float(base), int(sign),
+         code[x.dtype], code[odt], _ptr(out), stream_handle(None))
+    return out
+
+
 def debug_tc_gemm(mode: int, a: torch.Tensor, b: torch.Tensor, n: int) -> torch.Tensor:
     """Validation hook for the tcgen05/TMA descriptor builders (tests only)."""
     m, k = a.shape

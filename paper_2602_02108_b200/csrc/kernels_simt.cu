@@ -60,11 +60,23 @@ __device__ __forceinline__ int valid_in_page(int64_t filled, int pid, int P) {
 // One thread per (page touched, h, d): copies the page's new rows in order and
 // accumulates kavg_sum in append order -> bit-identical fp32 sums.
 // ===========================================================================
+// RoPE of one element (ops.hpp:192-225): row at absolute position pos, element d of a head;
+// angle = pos * base^(-2i/d) in double (inv_freq precomputed on the host with the reference's
+// std::pow), cos / sin in double rounded to Real, then the rotation in Real with no contraction.
+template <typename T>
+__device__ __forceinline__ float rope_elem(const T* __restrict__ row, int d, double pos, const double* inv_freq) {
+    const int i = d >> 1;
+    const double ang = pos * inv_freq[i];
+    const float c = static_cast<float>(cos(ang)), s = static_cast<float>(sin(ang));
+    const float x0 = to_f(row[2 * i]), x1 = to_f(row[2 * i + 1]);
+    return (d & 1) ? __fadd_rn(__fmul_rn(x0, s), __fmul_rn(x1, c)) : __fsub_rn(__fmul_rn(x0, c), __fmul_rn(x1, s));
+}
+
 template <typename T>
 __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, int64_t rows, int64_t filled,
                               int P, int Hkv, int hd, int first_page, NewSlots ns, int32_t* __restrict__ kvslot,
                               T* __restrict__ kpool, T* __restrict__ vpool, float* __restrict__ ksum,
-                              int32_t* __restrict__ kcnt) {
+                              int32_t* __restrict__ kcnt, const double* __restrict__ rope_inv_freq) {
     const int re = Hkv * hd;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     const int pg = first_page + blockIdx.y;
@@ -88,7 +100,11 @@ __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, 
         for (int u = 0; u < kB; ++u) {
             if (sb + u < s1) {
                 const int64_t r = sb + u - filled;
-                kb[u] = k[r * re + e];
+                // fused RoPE (chunk_trainer.hpp:424-432): K is rotated at its absolute position
+                // on the way into the page, never written back un-rotated
+                kb[u] = rope_inv_freq ? from_f<T>(rope_elem(k + r * re + h * hd, d, static_cast<double>(sb + u),
+                                                            rope_inv_freq))
+                                      : k[r * re + e];
                 vb[u] = v[r * re + e];
             }
         }
@@ -108,7 +124,8 @@ __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, 
 
 void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_t filled_before, int P, int Hkv,
                    int hd, int first_page, int n_pages_touched, const NewSlots& ns, int32_t* d_kvslot_layer,
-                   void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, cudaStream_t st) {
+                   void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, cudaStream_t st,
+                   const double* rope_inv_freq) {
     if (rows <= 0 || n_pages_touched <= 0) return;
     ProfScope prof_(PK_APPEND, st);
     const int re = Hkv * hd;
@@ -117,12 +134,12 @@ void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_
         append_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(
             static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), rows, filled_before, P, Hkv,
             hd, first_page, ns, d_kvslot_layer, static_cast<__nv_bfloat16*>(kpool), static_cast<__nv_bfloat16*>(vpool),
-            kavg_sum_layer, kavg_cnt_layer);
+            kavg_sum_layer, kavg_cnt_layer, rope_inv_freq);
     else
         append_kernel<float><<<grid, 128, 0, st>>>(static_cast<const float*>(k), static_cast<const float*>(v), rows,
                                                    filled_before, P, Hkv, hd, first_page, ns, d_kvslot_layer,
                                                    static_cast<float*>(kpool), static_cast<float*>(vpool),
-                                                   kavg_sum_layer, kavg_cnt_layer);
+                                                   kavg_sum_layer, kavg_cnt_layer, rope_inv_freq);
     check_launch("append_kernel");
 }
 
@@ -781,6 +798,50 @@ void launch_lse_merge(const void* o_parts, const float* lse_parts, int parts, in
         lse_merge_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(o_parts), lse_parts, parts, rows, hd,
                                                       static_cast<float*>(out), lse);
     check_launch("lse_merge_kernel");
+}
+
+// ===========================================================================
+// RoPE / inverse RoPE (ops.hpp:192-230) over [rows][heads][hd]: q before attention,
+// dq / dk_cur after it (rope_backward = sign -1). out may alias x.
+// ===========================================================================
+template <typename Tin, typename Tout>
+__global__ void rope_kernel(const Tin* x, int64_t rows, int heads, int hd, int64_t pos0, int sign,
+                            const double* __restrict__ inv_freq, Tout* out) {
+    const int64_t pairs = rows * heads * hd / 2;
+    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < pairs;
+         q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        // one rotation pair per thread, so an in-place rotation reads both elements before writing
+        const int64_t e0 = q * 2;
+        const int64_t r = e0 / (static_cast<int64_t>(heads) * hd);
+        const int d = static_cast<int>(e0 % hd);
+        const Tin* row = x + (e0 - d);
+        const double pos = static_cast<double>(sign) * static_cast<double>(pos0 + r);
+        const float y0 = rope_elem(row, d, pos, inv_freq);
+        const float y1 = rope_elem(row, d + 1, pos, inv_freq);
+        out[e0] = from_f<Tout>(y0);
+        out[e0 + 1] = from_f<Tout>(y1);
+    }
+}
+
+void launch_rope(int in_dtype, int out_dtype, const void* x, int64_t rows, int heads, int hd, int64_t pos0, int sign,
+                 const double* inv_freq, void* out, cudaStream_t st) {
+    const int64_t pairs = rows * heads * hd / 2;
+    if (pairs <= 0) return;
+    ProfScope prof_(PK_OTHER, st);
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((pairs + 255) / 256, 4096));
+    if (in_dtype == OOMB_BF16 && out_dtype == OOMB_BF16)
+        rope_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(x), rows, heads, hd, pos0, sign, inv_freq, static_cast<__nv_bfloat16*>(out));
+    else if (in_dtype == OOMB_BF16)
+        rope_kernel<__nv_bfloat16, float><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), rows, heads, hd,
+                                                                 pos0, sign, inv_freq, static_cast<float*>(out));
+    else if (out_dtype == OOMB_BF16)
+        rope_kernel<float, __nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const float*>(x), rows, heads, hd, pos0,
+                                                                 sign, inv_freq, static_cast<__nv_bfloat16*>(out));
+    else
+        rope_kernel<float, float><<<grid, 256, 0, st>>>(static_cast<const float*>(x), rows, heads, hd, pos0, sign,
+                                                        inv_freq, static_cast<float*>(out));
+    check_launch("rope_kernel");
 }
 
 }  // namespace oomb

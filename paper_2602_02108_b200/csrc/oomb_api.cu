@@ -6,6 +6,7 @@
 // kernels. Every entry point catches and converts exceptions to oomb_status.
 
 #include <map>
+#include <tuple>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -23,6 +24,25 @@ namespace oomb {
 
 thread_local std::string g_last_error;
 thread_local Profiler* g_prof = nullptr;
+
+const double* rope_inv_freq_table(float base, int hd) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, float, int>, double*> tables;
+    int dev = 0;
+    OOMB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_tuple(dev, base, hd);
+    auto it = tables.find(key);
+    if (it != tables.end()) return it->second;
+    std::vector<double> h(static_cast<size_t>(hd / 2));
+    for (int i = 0; i < hd / 2; ++i)
+        h[static_cast<size_t>(i)] = std::pow(static_cast<double>(base), -2.0 * static_cast<double>(i) / static_cast<double>(hd));
+    double* d = nullptr;
+    OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&d), h.size() * sizeof(double)));
+    OOMB_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+    tables[key] = d;
+    return d;
+}
 
 namespace {
 struct TraceReq {
@@ -406,14 +426,15 @@ int oomb_set_kernel_policy(oomb_pool_t p, int policy) {
 // ---------------------------------------------------------------------------
 // page table ops
 // ---------------------------------------------------------------------------
-int oomb_append_chunk(oomb_pool_t p, int layer, const void* k, const void* v, int64_t rows, void* stream,
-                      int64_t* slot_begin, int64_t* slot_end) {
+static int append_impl(oomb_pool_t p, int layer, const void* k, const void* v, int64_t rows, void* stream,
+                       int64_t* slot_begin, int64_t* slot_end, float rope_base) {
     return guard([&] {
         set_dev(p);
         p->pt->check_layer(layer);
         const int P = p->cfg.page_size;
         OOMB_REQUIRE(p->pt->filled[layer] + rows <= p->max_pages * P, OOMB_CONFIG_ERROR,
                      "append_chunk: layer capacity (max_tokens) exceeded");
+        const double* inv_freq = rope_base > 0.f ? rope_inv_freq_table(rope_base, p->cfg.head_dim) : nullptr;
         int64_t b, e;
         int first_new, n_new;
         const int64_t filled0 = p->pt->filled[layer];
@@ -442,10 +463,33 @@ int oomb_append_chunk(oomb_pool_t p, int layer, const void* k, const void* v, in
             const char* vb = static_cast<const char*>(v) + done * re * p->elem;
             launch_append(p->cfg.dtype, kb, vb, seg, f, P, p->cfg.n_kv_heads, p->cfg.head_dim, first_page,
                           last_page - first_page + 1, ns, p->kvslot_layer(layer), p->kpool, p->vpool,
-                          p->kavg_sum_layer(layer), p->kavg_cnt_layer(layer), S(stream));
+                          p->kavg_sum_layer(layer), p->kavg_cnt_layer(layer), S(stream), inv_freq);
             published = std::max(published, last_page + 1);
             done += seg;
         }
+    });
+}
+
+int oomb_append_chunk(oomb_pool_t p, int layer, const void* k, const void* v, int64_t rows, void* stream,
+                      int64_t* slot_begin, int64_t* slot_end) {
+    return append_impl(p, layer, k, v, rows, stream, slot_begin, slot_end, 0.f);
+}
+int oomb_append_chunk_rope(oomb_pool_t p, int layer, const void* k_raw, const void* v, int64_t rows, float rope_base,
+                           void* stream, int64_t* slot_begin, int64_t* slot_end) {
+    const int rc = guard([&] {
+        OOMB_REQUIRE(rope_base > 0.f, OOMB_CONFIG_ERROR, "append_chunk_rope: rope base must be positive");
+    });
+    if (rc != OOMB_OK) return rc;
+    return append_impl(p, layer, k_raw, v, rows, stream, slot_begin, slot_end, rope_base);
+}
+int oomb_rope(const void* x, int64_t rows, int heads, int hd, int64_t pos_offset, float base, int sign, int in_dtype,
+              int out_dtype, void* out, void* stream) {
+    return guard([&] {
+        OOMB_REQUIRE(rows >= 0 && heads >= 1 && hd >= 2 && hd % 2 == 0, OOMB_SHAPE_ERROR,
+                     "rope: head dimension must be even");  // ops.hpp:194-196
+        OOMB_REQUIRE(base > 0.f && (sign == 1 || sign == -1), OOMB_CONFIG_ERROR, "rope: base > 0, sign +-1");
+        launch_rope(in_dtype, out_dtype, x, rows, heads, hd, pos_offset, sign, rope_inv_freq_table(base, hd), out,
+                    S(stream));
     });
 }
 

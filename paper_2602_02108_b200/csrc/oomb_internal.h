@@ -150,7 +150,13 @@ struct NewSlots {
 
 void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_t filled_before, int P, int Hkv,
                    int hd, int first_page, int n_pages_touched, const NewSlots& ns, int32_t* d_kvslot_layer,
-                   void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, cudaStream_t st);
+                   void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, cudaStream_t st,
+                   const double* rope_inv_freq = nullptr);
+void launch_rope(int in_dtype, int out_dtype, const void* x, int64_t rows, int heads, int hd, int64_t pos0, int sign,
+                 const double* inv_freq, void* out, cudaStream_t st);
+// Device table inv_freq[i] = base^(-2i/hd) computed on the host with the reference's std::pow
+// (ops.hpp:198-201); cached per (device, base, hd) for the life of the library.
+const double* rope_inv_freq_table(float base, int hd);
 void launch_mean_keys(const float* kavg_sum_layer, const int32_t* kavg_cnt_layer, int n, int row_elems,
                       float* out, cudaStream_t st);
 void launch_gather(int dtype, int grads, const int32_t* d_ids, int n, const int32_t* d_slot_layer,

@@ -132,15 +132,21 @@ class PagedCache:
     def full_pages_before(tokens: int, page_size: int) -> int:
         return tokens // page_size
 
-    def append_chunk(self, layer: int, k, v, stream=None) -> SlotRange:
-        """paged_kv.hpp:73-108 — write rows into tail-page slots, update K_avg sums."""
+    def append_chunk(self, layer: int, k, v, stream=None, rope_base: float | None = None) -> SlotRange:
+        """paged_kv.hpp:73-108 — write rows into tail-page slots, update K_avg sums.
+        rope_base: k is the PRE-RoPE projection; it is rotated at its absolute positions on the
+        way into the page (the fused epilogue of chunk_trainer.hpp:424-432)."""
         k, v = self._dev(k), self._dev(v)
         cfg = self.cfg
         if k.dim() != 3 or k.shape[1] != cfg.n_kv_heads or k.shape[2] != cfg.head_dim or k.shape != v.shape:
             raise ShapeError("append_chunk: expected [rows x kvh x hd] K/V of equal shape")
         b, e = C.c_int64(), C.c_int64()
-        call("oomb_append_chunk", self.handle, layer, _ptr(k), _ptr(v), k.shape[0], stream_handle(stream),
-             C.byref(b), C.byref(e))
+        if rope_base is None:
+            call("oomb_append_chunk", self.handle, layer, _ptr(k), _ptr(v), k.shape[0], stream_handle(stream),
+                 C.byref(b), C.byref(e))
+        else:
+            call("oomb_append_chunk_rope", self.handle, layer, _ptr(k), _ptr(v), k.shape[0], C.c_float(rope_base),
+                 stream_handle(stream), C.byref(b), C.byref(e))
         return SlotRange(b.value, e.value)
 
     def gather_pages(self, layer: int, page_ids, stream=None) -> Gathered:
