@@ -38,6 +38,10 @@ constexpr int kF4Smem = kF4Bar + 256;
 static_assert(kF4Smem <= 232448, "dynamic shared memory above the 227 KB opt-in limit");
 constexpr uint32_t kTmS = 0, kTmO = 256;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef OOMB_FWD4_POLY
+#define OOMB_FWD4_POLY 0  // measured: no gain (the softmax phase is latency-bound, not MUFU-bound)
+#endif
+constexpr bool kF4Poly = OOMB_FWD4_POLY != 0;
 
 struct F4Bars {
     uint64_t q_full;
@@ -224,8 +228,10 @@ __global__ void __launch_bounds__(384, 1)
                 uint32_t pk[16];
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
-                    const float e0 = ex2(fmaf(__uint_as_float(sr[c4 * 32 + 2 * u]), sl2, -m_use));
-                    const float e1 = ex2(fmaf(__uint_as_float(sr[c4 * 32 + 2 * u + 1]), sl2, -m_use));
+                    const float x0 = fmaf(__uint_as_float(sr[c4 * 32 + 2 * u]), sl2, -m_use);
+                    const float x1 = fmaf(__uint_as_float(sr[c4 * 32 + 2 * u + 1]), sl2, -m_use);
+                    const float e0 = ex2(x0);
+                    const float e1 = (kF4Poly && (u & 1)) ? ex2_poly(x1) : ex2(x1);  // 1 in 4 on the FMA pipe
                     rs8[(2 * u) & 7] += e0;
                     rs8[(2 * u + 1) & 7] += e1;
                     pk[u] = pack_bf16(e0, e1);
