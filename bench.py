@@ -547,11 +547,20 @@ def main():
             kernels[name]["achieved_tflops"] = fl / (t / 1e3) / 1e12
             kernels[name]["frac_of_peak"] = fl / (t / 1e3) / 1e12 / peak
     achieved = bwd_fl / (t_bwd / 1e3) / 1e12 if t_bwd > 0 else None
+    traffic = None
+    try:  # DRAM bytes of the dominant kernel pair from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            tr = json.load(f)
+        traffic = {"bytes_per_launch": sum(tr[k]["dram_read_bytes"] + tr[k]["dram_write_bytes"]
+                                           for k in ("attn_bwd_dq", "attn_bwd_dkdv")),
+                   "source": tr["source"]}
+    except Exception:
+        pass
     roofline = {"bound": "tensor", "kernel": "attn_bwd_dq + attn_bwd_dkdv (tcgen05), per chunk",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if achieved else None, "peak_source": peak_src,
                 "algorithmic": "10*hd*Hq*pairs per chunk, pairs = P*P*sum|sel| + C(C+1)/2 (SURVEY 8d)",
-                "traffic": None}
+                "traffic": traffic}
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
