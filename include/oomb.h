@@ -222,7 +222,8 @@ OOMB_API int oomb_accumulate_grad_pages(oomb_pool_t pool, int layer, const int32
  * stream; oomb_profile_collect synchronises and returns, per kernel kind, the number of
  * launches and the summed device milliseconds, then clears the record.
  * Kinds: 0 append, 1 score, 2 topk, 3 attn_fwd, 4 bwd_prep, 5 bwd_dq, 6 bwd_dkdv,
- * 7 bwd_simt, 8 grad_init, 9 gather/scatter, 10 other. */
+ * 7 bwd_simt, 8 grad_init, 9 gather/scatter, 10 other, 11 bwd_pair (the span of the dq and dkdv
+ * kernels, which run concurrently: dq on a library side stream). */
 OOMB_API int oomb_profile_enable(oomb_pool_t pool, int on);
 OOMB_API int oomb_profile_collect(oomb_pool_t pool, int64_t* counts, double* ms, int n_kinds);
 

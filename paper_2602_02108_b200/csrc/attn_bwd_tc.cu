@@ -18,6 +18,8 @@
 //                 (the chunk's own keys). Pages never selected are not touched.
 
 #include <cub/block/block_scan.cuh>
+#include <map>
+#include <tuple>
 
 #include "tc_common.cuh"
 
@@ -893,13 +895,36 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     BwdParams p{g, sel_off, sel_ids, d_kvslot_layer, d_gslot_layer, gkpool, gvpool, w.Dt, w.Lt, w.mask, w.uni,
                 w.n_uni, dq, dk_cur, dv_cur, d_err, CtaTrace{}};
     delete prep_scope;
+    // dQ and dK/dV only read the chunk's inputs and the prep outputs: dQ runs on a side stream,
+    // launched first, and the persistent dK/dV CTAs pick up SMs as dQ's last wave drains (and
+    // vice versa), so neither kernel's tail leaves SMs idle. The caller's stream waits for both.
+    static std::map<int, std::tuple<cudaStream_t, cudaEvent_t, cudaEvent_t>> side_by_dev;
+    int dev = 0;
+    OOMB_CUDA(cudaGetDevice(&dev));
+    auto it = side_by_dev.find(dev);
+    if (it == side_by_dev.end()) {
+        cudaStream_t s2;
+        cudaEvent_t e1, e2;
+        OOMB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        OOMB_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+        OOMB_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+        it = side_by_dev.emplace(dev, std::make_tuple(s2, e1, e2)).first;
+    }
+    cudaStream_t side = std::get<0>(it->second);
+    cudaEvent_t ev_prep = std::get<1>(it->second), ev_dq = std::get<2>(it->second);
+    // the dQ + dK/dV pair as one span on the caller's stream (the two kernels overlap, so their
+    // own spans each include time spent sharing the GPU with the other)
+    ProfScope* pair_scope = new ProfScope(PK_BWD_PAIR, st);
+    OOMB_CUDA(cudaEventRecord(ev_prep, st));
+    OOMB_CUDA(cudaStreamWaitEvent(side, ev_prep, 0));
     {
-        ProfScope s_(PK_BWD_DQ, st);
+        ProfScope s_(PK_BWD_DQ, side);
         const CUtensorMap tdq = map_rows_heads_f32(dq, g.C, g.Hq, kHd);
-        attn_bwd_dq_kernel<<<dim3(g.Hq, g.C / kTile), 384, kDqSmem, st>>>(tq, tdo, tkc, tvc, maps.kpool, maps.vpool,
-                                                                          tdq, p);
+        attn_bwd_dq_kernel<<<dim3(g.Hq, g.C / kTile), 384, kDqSmem, side>>>(tq, tdo, tkc, tvc, maps.kpool,
+                                                                            maps.vpool, tdq, p);
         check_launch("attn_bwd_dq_kernel");
     }
+    OOMB_CUDA(cudaEventRecord(ev_dq, side));
     {
         ProfScope s_(PK_BWD_DKDV, st);
         const int max_union = std::min(nnz, n_pages);
@@ -914,6 +939,8 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         attn_bwd_dkdv_kernel<<<n_ctas, 384, kKvSmem, st>>>(tq, tdo, tkc, tvc, maps.kpool, maps.vpool, maps.gkpool,
                                                             maps.gvpool, tdkc, tdvc, p, w.n_uni + 1);
         check_launch("attn_bwd_dkdv_kernel");
+        OOMB_CUDA(cudaStreamWaitEvent(st, ev_dq, 0));
+        delete pair_scope;
 
     }
 }

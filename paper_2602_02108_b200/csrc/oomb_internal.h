@@ -46,7 +46,7 @@ void check_launch(const char* what);
 // ---------------------------------------------------------------------------
 enum ProfKind {
     PK_APPEND = 0, PK_SCORE, PK_TOPK, PK_FWD, PK_BWD_PREP, PK_BWD_DQ, PK_BWD_DKDV, PK_BWD_SIMT, PK_GRAD_INIT,
-    PK_GATHER, PK_OTHER, PK_N
+    PK_GATHER, PK_OTHER, PK_BWD_PAIR, PK_N
 };
 struct Profiler {
     struct Rec {

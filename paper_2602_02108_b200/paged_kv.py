@@ -247,7 +247,7 @@ class PagedCache:
              _ptr(dv), stream_handle(stream))
 
     PROFILE_KINDS = ("append", "score", "topk", "attn_fwd", "bwd_prep", "bwd_dq", "bwd_dkdv", "bwd_simt",
-                     "grad_init", "gather_scatter", "other")
+                     "grad_init", "gather_scatter", "other", "bwd_pair")
 
     def profile_enable(self, on: bool = True) -> None:
         call("oomb_profile_enable", self.handle, int(on))
