@@ -21,7 +21,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "liboomb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["oomb_api.cu", "kernels_simt.cu", "attn_tc.cu", "attn_fwd3.cu", "attn_fwd4.cu", "attn_fwd5.cu", "attn_bwd_tc.cu", "score_tc.cu", "tier.cu"]
+SOURCES = ["oomb_api.cu", "kernels_simt.cu", "attn_tc.cu", "attn_fwd4.cu", "attn_bwd_tc.cu", "score_tc.cu", "tier.cu"]
 HEADERS = ["oomb_internal.h", "ptx.cuh", "tc_common.cuh", "pool.h"]
 
 FLAGS = [

@@ -207,13 +207,7 @@ void make_pool_maps(TcPoolMaps& maps, const void* kpool, const void* vpool, int6
 void launch_attn_fwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* q, const int32_t* sel_off,
                         const int32_t* sel_ids, const int32_t* d_kvslot_layer, const void* k_cur, const void* v_cur,
                         void* out, float* lse, int* d_err, cudaStream_t st);
-void launch_attn_fwd_tc3(const AttnGeom& g, const TcPoolMaps& maps, const void* q, const int32_t* sel_off,
-                         const int32_t* sel_ids, const int32_t* d_kvslot_layer, const void* k_cur, const void* v_cur,
-                         void* out, float* lse, int* d_err, cudaStream_t st);
 void launch_attn_fwd_tc4(const AttnGeom& g, const TcPoolMaps& maps, const void* q, const int32_t* sel_off,
-                         const int32_t* sel_ids, const int32_t* d_kvslot_layer, const void* k_cur, const void* v_cur,
-                         void* out, float* lse, int* d_err, cudaStream_t st);
-void launch_attn_fwd_tc5(const AttnGeom& g, const TcPoolMaps& maps, const void* q, const int32_t* sel_off,
                          const int32_t* sel_ids, const int32_t* d_kvslot_layer, const void* k_cur, const void* v_cur,
                          void* out, float* lse, int* d_err, cudaStream_t st);
 void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* dout, const void* q,
