@@ -323,13 +323,29 @@ class E2E:
             h2d_b += 2 * (self.qd[b].numel() + 2 * self.kd[b].numel())
 
         load_fwd(0)
+        # as Run.forward_pass: chunk i+1's selection on a second stream overlaps chunk i's attention
+        if not hasattr(self, "ss"):
+            self.ss = torch.cuda.Stream(device=r.dev)
+        ss = self.ss
+        ev_app = [torch.cuda.Event() for _ in range(2)]
+        ev_sel = [torch.cuda.Event() for _ in range(2)]
+        ss.wait_stream(comp)
         for i in range(S):
             b = i & 1
             if i + 1 < S:
                 load_fwd(i + 1)
+            ss.wait_event(ev_in[b])
+            if i > 0:
+                ss.wait_event(ev_app[(i - 1) & 1])  # K_avg of every earlier chunk is in
+            r._select(i, self.qd[b], stream=ss)
+            ev_sel[b].record(ss)
             comp.wait_event(ev_in[b])
             comp.wait_event(ev_out[b])  # the D2H that last read out slot b finished
-            r.fwd_chunk(i, self.qd[b], self.kd[b], self.vd[b])
+            r.cache.append_chunk(0, self.kd[b], self.vd[b], stream=comp)
+            ev_app[b].record(comp)
+            comp.wait_event(ev_sel[b])  # (the selection read qd[b] too: ev_used below covers it)
+            r.A.attn_forward(r.mc, self.qd[b], r.cache, 0, r.sels[i], self.kd[b], self.vd[b], stream=comp,
+                             out=r.o_all[i], lse=r.lse_all[i])
             ev_used[b].record(comp)
             with torch.cuda.stream(self.d2h):
                 self.d2h.wait_event(ev_used[b])
