@@ -42,6 +42,12 @@ CONFIGS = {
                mode="topk", budget=8192),
     "c2": dict(desc="BASELINE configs[1]: Qwen2.5-7B attention, page 128, chunk 4096, 128K context, dense",
                Hq=28, Hkv=4, hd=128, P=128, C=4096, T=1 << 17, mode="dense", budget=0),
+    "c4": dict(desc="BASELINE configs[3] on one GPU: Qwen2.5-7B attention, page 128, chunk 4096, 4M context, "
+                    "top-k 64 pages per query page (the 8-GPU KV-group split is weak-scaled by --gpus)",
+               Hq=28, Hkv=4, hd=128, P=128, C=4096, T=1 << 22, mode="topk", budget=8192),
+    "c5": dict(desc="BASELINE configs[4] on one GPU: Llama-3-8B attention (32Q/8KV, hd 128), page 256, "
+                    "chunk 4096, 512K context, dense", Hq=32, Hkv=8, hd=128, P=256, C=4096, T=1 << 19,
+               mode="dense", budget=0),
     "c1": dict(desc="BASELINE configs[0]: tiny 4Q/1KV, hd 64, page 64, chunk 256, 8K context, dense",
                Hq=4, Hkv=1, hd=64, P=64, C=256, T=8192, mode="dense", budget=0),
 }
@@ -623,7 +629,7 @@ def main():
                                   "capped-capacity regime separately; e2e moves chunk inputs/outputs over the host link"},
             "pct_bf16_peak": tflops / peak, "pct_bf16_peak_sustained": tflops / peak_sus,
             "algorithmic_tflops": tflops,
-            "model_equiv_tokens_per_s": value / 28,
+            "model_equiv_tokens_per_s": value / (32 if cfg["Hq"] == 32 else 28),
             "roofline": roofline, "kernels": kernels, "gpu_launches": launches // args.steps,
             "gpu_launches_timed_region": launches, "clocks": clk, "e2e": e2e, "offload": offload,
             "train_step_variant": {

@@ -129,6 +129,12 @@ def qwen_slice_cfg() -> Cfg:
                retrieval_budget=512, local_window=4)
 
 
+def llama_slice_cfg() -> Cfg:
+    """Llama-3-8B attention shape (32Q/8KV, hd 128) with page 256 (BASELINE config 5) on a 512-token chunk."""
+    return Cfg(n_layers=1, n_q_heads=32, n_kv_heads=8, head_dim=128, chunk_size=512, page_size=256,
+               retrieval_budget=512, local_window=4)
+
+
 def small_cfg() -> Cfg:
     """test_attention.cpp:19-31 attn_config()."""
     return Cfg(n_layers=1, n_q_heads=4, n_kv_heads=2, head_dim=8, chunk_size=16, page_size=8,

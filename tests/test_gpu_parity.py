@@ -10,7 +10,7 @@ import pytest
 import torch
 
 from oracle.oracle import Cfg, Port, det_normal, to_bf16
-from tests.golden.make_golden import attn_case, c1_cfg, qwen_slice_cfg, small_cfg, topk_case
+from tests.golden.make_golden import attn_case, c1_cfg, llama_slice_cfg, qwen_slice_cfg, small_cfg, topk_case
 
 pytestmark = pytest.mark.gpu
 
@@ -287,6 +287,8 @@ ATTN_CASES = {
     "c1_dense": (c1_cfg, 4 * 64, 31, None),
     "qwen_sparse": (qwen_slice_cfg, 8 * 128, 41, [[0, 3, 5], [1, 2], [7], [0, 4, 6, 7]]),
     "qwen_nopast": (qwen_slice_cfg, 0, 42, [[], [], [], []]),
+    "qwen_partial": (qwen_slice_cfg, 8 * 128 - 37, 44, [[0, 3, 7], [1, 7], [7], [0, 4, 6]]),  # last past page partial
+    "llama_sparse": (llama_slice_cfg, 6 * 256, 51, [[0, 3, 5], [1, 2, 4, 0]]),               # P 256, GQA 4
 }
 
 
@@ -302,7 +304,8 @@ def test_attention_fp32_parity(name):
         assert rel(got[k], want[k]) < FP32_TOL, (name, k, rel(got[k], want[k]))
 
 
-@pytest.mark.parametrize("name", ["c1_dense", "qwen_sparse", "qwen_nopast", "small_sparse"])
+@pytest.mark.parametrize("name", ["c1_dense", "qwen_sparse", "qwen_nopast", "small_sparse", "qwen_partial",
+                                  "llama_sparse"])
 @pytest.mark.parametrize("policy", ["auto", "simt"])
 def test_attention_bf16_parity(name, policy):
     mk, past, seed, sel = ATTN_CASES[name]
