@@ -587,10 +587,11 @@ def main():
     for k in ("bwd_dq", "bwd_dkdv"):
         if k in kernels and "bwd_pair" in kernels:
             kernels[k]["note"] = "overlaps the other backward kernel; see bwd_pair for their joint span"
-    for k in ("score", "topk", "attn_fwd"):
+    for k in ("score", "topk", "other", "append", "attn_fwd"):
         if k in kernels:
-            kernels[k]["note"] = ("chunk i+1's selection (score, topk) runs on a second stream while chunk i "
-                                  "attends: these spans overlap each other")
+            kernels[k]["note"] = ("chunk i+1's selection (score, topk; the dense CSR fill is 'other') runs on "
+                                  "a second stream while chunk i appends and attends: these spans overlap "
+                                  "each other, so they are not additive")
 
     # dominant kernel pair: the tcgen05 backward (dq + dkdv launches per chunk)
     # the dq and dkdv kernels run concurrently (dq on a side stream): their pair is timed as one span
