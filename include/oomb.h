@@ -6,9 +6,10 @@
  * template surface of paged_kv.hpp / attention.hpp / tiered_memory.hpp. Each
  * entry point below replaces one of those calls; the citation next to it is
  * the reference interface it stands in for (paths relative to
- * /root/reference/proj/core/include/chunktrain/). The host-side mirror of that
- * API lives in paper_2602_02108_b200/ (Python, ctypes); INTEGRATION.md shows
- * the binding a maintainer of the reference would add.
+ * /root/reference/proj/core/include/chunktrain/). The host side of that API is
+ * the C++ facade include/oomb.hpp (reference names and exceptions), mirrored in
+ * Python (paper_2602_02108_b200/, ctypes); INTEGRATION.md shows the binding a
+ * maintainer of the reference would add.
  *
  * Conventions
  *  - Every function returns an oomb_status; OOMB_OK == 0. The codes map 1:1
