@@ -12,6 +12,7 @@ from .errors import raise_for_status
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "liboomb.so")
+COMM_LIB_PATH = os.path.join(PKG, "liboomb_comm.so")
 
 I32P = C.POINTER(C.c_int32)
 
@@ -145,3 +146,44 @@ def kernel_launches() -> int:
 
 def exported_symbols() -> list[str]:
     return list(_PROTOS)
+
+
+# liboomb_comm.so (include/oomb_comm.h): NCCL exchange steps of the sharded path
+_COMM_PROTOS = {
+    "oomb_comm_last_error": [],
+    "oomb_comm_get_unique_id": [VP],
+    "oomb_comm_init": [VP, I, I, I, VP],
+    "oomb_comm_destroy": [VP],
+    "oomb_comm_rank": [VP, VP, VP],
+    "oomb_vote_allgather": [VP, VP, I, I64, I64, VP, VP],
+    "oomb_lse_merge_allgather": [VP, VP, VP, I64, I, I, VP, VP, VP],
+    "oomb_dq_reduce": [VP, VP, I64, VP, VP],
+}
+_comm = None
+
+
+def comm_lib() -> C.CDLL:
+    """Load liboomb_comm.so once (it pulls in liboomb.so and NCCL); raise loudly when absent."""
+    global _comm
+    if _comm is None:
+        lib()
+        if not os.path.exists(COMM_LIB_PATH):
+            raise ImportError(f"{COMM_LIB_PATH} not found: build it with `python -m paper_2602_02108_b200.build`")
+        L = C.CDLL(COMM_LIB_PATH)
+        for name, args in _COMM_PROTOS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_char_p if name == "oomb_comm_last_error" else C.c_int
+        _comm = L
+    return _comm
+
+
+def comm_call(name: str, *args) -> None:
+    L = comm_lib()
+    rc = getattr(L, name)(*args)
+    if rc != 0:
+        raise_for_status(rc, L.oomb_comm_last_error().decode(errors="replace"))
+
+
+def comm_exported_symbols() -> list[str]:
+    return list(_COMM_PROTOS)

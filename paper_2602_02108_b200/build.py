@@ -19,6 +19,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "liboomb.so")
+COMM_LIB = os.path.join(PKG, "liboomb_comm.so")  # NCCL exchange steps (include/oomb_comm.h)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["oomb_api.cu", "kernels_simt.cu", "attn_tc.cu", "attn_fwd4.cu", "attn_bwd_tc.cu", "score_tc.cu", "tier.cu"]
@@ -41,8 +42,9 @@ def _digest() -> str:
     for f in SOURCES + HEADERS:
         with open(os.path.join(CSRC, f), "rb") as fh:
             h.update(fh.read())
-    with open(os.path.join(INCLUDE, "oomb.h"), "rb") as fh:
-        h.update(fh.read())
+    for f in (os.path.join(INCLUDE, "oomb.h"), os.path.join(INCLUDE, "oomb_comm.h"), os.path.join(CSRC, "comm.cu")):
+        with open(f, "rb") as fh:
+            h.update(fh.read())
     h.update(" ".join(FLAGS).encode())
     return h.hexdigest()
 
@@ -50,7 +52,7 @@ def _digest() -> str:
 def build(force: bool = False, verbose: bool = False) -> str:
     stamp = LIB + ".sha256"
     dig = _digest()
-    if not force and os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read() == dig:
+    if not force and os.path.exists(LIB) and os.path.exists(COMM_LIB) and os.path.exists(stamp) and open(stamp).read() == dig:
         return LIB
     objdir = os.path.join(PKG, "_build")
     os.makedirs(objdir, exist_ok=True)
@@ -73,6 +75,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
+    # liboomb_comm.so: host code over NCCL and liboomb.so's public combine entry points
+    comm_obj = os.path.join(objdir, "comm.o")
+    for cmd in ([NVCC, *FLAGS, "-c", os.path.join(CSRC, "comm.cu"), "-o", comm_obj],
+                [NVCC, "-shared", "-cudart", "static", "-o", COMM_LIB, comm_obj, f"-L{PKG}", "-loomb", "-lnccl",
+                 "-Xlinker", "-rpath,$ORIGIN"]):
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("liboomb_comm.so build failed")
     with open(os.path.join(objdir, "ptxas.log"), "w") as fh:
         fh.write("\n".join(logs))
     if verbose:

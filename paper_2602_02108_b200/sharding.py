@@ -64,6 +64,74 @@ class KVGroupShard:
         return x[:, a:b].contiguous()
 
 
+class OombComm:
+    """liboomb_comm.so: an NCCL communicator with the path's deterministic exchange steps
+    (include/oomb_comm.h). Rank 0 creates the NCCL id; the process group broadcasts it."""
+
+    def __init__(self, rank: int, world: int, device: int, uid: bytes):
+        from ._lib import comm_call
+        h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        comm_call("oomb_comm_init", buf, rank, world, device, C.byref(h))
+        self.handle, self.rank, self.world = h, rank, world
+
+    @staticmethod
+    def unique_id() -> bytes:
+        from ._lib import comm_call
+        buf = (C.c_uint8 * 128)()
+        comm_call("oomb_comm_get_unique_id", buf)
+        return bytes(buf)
+
+    @classmethod
+    def from_process_group(cls, group=None, device: int | None = None) -> "OombComm":
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        return cls(rank, world, torch.cuda.current_device() if device is None else device, obj[0])
+
+    def close(self):
+        if getattr(self, "handle", None):
+            from ._lib import comm_lib
+            comm_lib().oomb_comm_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+    def vote_allgather(self, partials_local: torch.Tensor, stream=None) -> torch.Tensor:
+        """[G_local, m, n] partial votes -> [m, n] summed over all ranks' groups in global order."""
+        from ._lib import comm_call
+        from .paged_kv import stream_handle
+        g, m, n = partials_local.shape
+        p = partials_local.contiguous()
+        vote = torch.empty((m, n), dtype=torch.float32, device=p.device)
+        comm_call("oomb_vote_allgather", self.handle, C.c_void_p(p.data_ptr()), g, m, n, C.c_void_p(vote.data_ptr()),
+                  stream_handle(stream))
+        return vote
+
+    def lse_merge_allgather(self, o_part: torch.Tensor, lse_part: torch.Tensor, stream=None):
+        """partial (O [C, H, hd], LSE [C, H]) of this rank -> the exact merge over all ranks."""
+        from ._lib import comm_call
+        from .paged_kv import stream_handle
+        c, h, hd = o_part.shape
+        o, l = o_part.contiguous(), lse_part.contiguous()
+        out, lse = torch.empty_like(o), torch.empty_like(l)
+        comm_call("oomb_lse_merge_allgather", self.handle, C.c_void_p(o.data_ptr()), C.c_void_p(l.data_ptr()), c * h,
+                  hd, 1 if o.dtype == torch.bfloat16 else 0, C.c_void_p(out.data_ptr()), C.c_void_p(lse.data_ptr()),
+                  stream_handle(stream))
+        return out, lse
+
+    def dq_reduce(self, dq_part: torch.Tensor, stream=None) -> torch.Tensor:
+        """sum of every rank's partial dQ in rank order (fp32)."""
+        from ._lib import comm_call
+        from .paged_kv import stream_handle
+        p = dq_part.contiguous()
+        out = torch.empty_like(p)
+        comm_call("oomb_dq_reduce", self.handle, C.c_void_p(p.data_ptr()), p.numel(), C.c_void_p(out.data_ptr()),
+                  stream_handle(stream))
+        return out
+
+
 def fixed_order_sum(parts: torch.Tensor) -> torch.Tensor:
     """vote = ((p_0 + p_1) + p_2) + ... over the group axis: on CUDA the library's
     vote_reduce kernel, elsewhere the same fp32 additions in the same order."""
@@ -80,9 +148,12 @@ def fixed_order_sum(parts: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def combine_votes(partials_local: torch.Tensor, group=None) -> torch.Tensor:
+def combine_votes(partials_local: torch.Tensor, group=None, comm: OombComm | None = None) -> torch.Tensor:
     """All-gather [G_local, m, n] partial votes over the process group (global group
-    order = rank order) and reduce them in that fixed order -> [m, n] vote."""
+    order = rank order) and reduce them in that fixed order -> [m, n] vote.
+    With `comm` the exchange runs in liboomb_comm.so (NCCL) instead of torch.distributed."""
+    if comm is not None:
+        return comm.vote_allgather(partials_local)
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
@@ -107,12 +178,12 @@ def score_pages_partial(cache, layer: int, q_local: torch.Tensor, n_candidates: 
 
 
 def select_pages_topk_sharded(cache, layer: int, q_local: torch.Tensor, n_candidates: int, group=None,
-                              out=None):
+                              out=None, comm: OombComm | None = None):
     """chunk_trainer.hpp:305-311 on a KV-group shard: partial votes -> all-gather ->
     fixed-order sum -> top-k per query page. Identical ids on every rank."""
     from . import attention as A
     parts = score_pages_partial(cache, layer, q_local, n_candidates)
-    vote = combine_votes(parts.contiguous(), group)
+    vote = combine_votes(parts.contiguous(), group, comm)
     sel = A.select_topk_rows(cache, vote, cache.cfg.budget_pages()) if out is None else out
     if out is not None:
         from .paged_kv import _ptr, stream_handle
@@ -173,23 +244,31 @@ def _gather(x: torch.Tensor, group=None) -> torch.Tensor:
     return out
 
 
-def range_forward(shard: PageRangeShard, cfg, q, cache, layer, selected_lists, k_cur, v_cur, group=None):
+def range_forward(shard: PageRangeShard, cfg, q, cache, layer, selected_lists, k_cur, v_cur, group=None,
+                  comm: OombComm | None = None):
     """attn_forward on a page-range shard + the collective merge; returns the merged AttnSaved
     (out, lse) and this rank's sub-selection (for the backward)."""
     from . import attention as A
     sub = A.Selection.from_lists(cache, shard.split_lists(selected_lists))
     part = A.attn_forward(cfg, q, cache, layer, sub, k_cur, v_cur, past_only=shard.past_only)
-    out, lse = lse_merge(_gather(part.out, group), _gather(part.lse, group))
+    if comm is not None:
+        out, lse = comm.lse_merge_allgather(part.out, part.lse)
+    else:
+        out, lse = lse_merge(_gather(part.out, group), _gather(part.lse, group))
     return A.AttnSaved(out, lse, sub), sub
 
 
-def range_backward(shard: PageRangeShard, cfg, dout, q, cache, layer, k_cur, v_cur, saved, group=None):
+def range_backward(shard: PageRangeShard, cfg, dout, q, cache, layer, k_cur, v_cur, saved, group=None,
+                   comm: OombComm | None = None):
     """attn_backward on a page-range shard with the merged (O, LSE); dQ summed over ranks in rank
     order, dk_cur / dv_cur from rank 0. The rank's own pages' dK/dV land in its gradient pool."""
     from . import attention as A
     g = A.attn_backward(cfg, dout, q, cache, layer, k_cur, v_cur, saved, past_only=shard.past_only)
-    dq_parts = _gather(g.dq, group)
-    dq = fixed_order_sum(dq_parts.reshape(dq_parts.shape[0], 1, -1)).reshape(g.dq.shape)
+    if comm is not None:
+        dq = comm.dq_reduce(g.dq)
+    else:
+        dq_parts = _gather(g.dq, group)
+        dq = fixed_order_sum(dq_parts.reshape(dq_parts.shape[0], 1, -1)).reshape(g.dq.shape)
     dk = _gather(g.dk_cur, group)[0].clone()
     dv = _gather(g.dv_cur, group)[0].clone()
     return A.AttnGrads(dq, dk, dv)

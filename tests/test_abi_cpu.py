@@ -32,6 +32,23 @@ def test_library_exports_every_header_symbol():
     assert L.oomb_version() == 1
 
 
+def test_comm_library_exports_every_header_symbol():
+    """liboomb_comm.so (NCCL exchange steps) loads without a GPU and exports include/oomb_comm.h."""
+    src = open(os.path.join(ROOT, "include", "oomb_comm.h")).read()
+    syms = sorted(set(re.findall(r"^OOMB_API\s+[\w\s\*]+?\b(oomb_\w+)\s*\(", src, flags=re.M)))
+    assert len(syms) == 8
+    L = _lib.comm_lib()
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(_lib.comm_exported_symbols())
+    # argument checks happen before any NCCL / CUDA call
+    from paper_2602_02108_b200 import errors
+    with pytest.raises(errors.ConfigError):
+        _lib.comm_call("oomb_comm_init", (C.c_uint8 * 128)(), 3, 2, 0, C.byref(C.c_void_p()))
+    with pytest.raises(errors.StateError):
+        _lib.comm_call("oomb_dq_reduce", None, None, 4, None, None)
+
+
 def test_library_carries_sm100a_tensor_core_code():
     import subprocess
     so = _lib.LIB_PATH

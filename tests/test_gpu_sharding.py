@@ -137,3 +137,21 @@ def test_lse_merge_single_part_is_identity_and_empty_parts_vanish():
     l2 = torch.stack([l[0], torch.full_like(l[0], float("-inf"))])
     out2, lse2 = lse_merge(o2, l2)
     assert torch.allclose(out2, o[0], rtol=1e-6, atol=1e-6) and torch.allclose(lse2, l[0], rtol=1e-6, atol=1e-6)
+
+
+def test_nccl_comm_world1_exchanges_are_exact():
+    """liboomb_comm.so over a real NCCL communicator (world 1 — one GPU per rank, one GPU here):
+    the vote all-gather equals the fixed-order reduction bitwise, and the LSE merge and dQ reduce
+    of a single rank are the identity. The same calls run unchanged at world 2..8."""
+    from paper_2602_02108_b200.sharding import OombComm, fixed_order_sum
+    comm = OombComm(0, 1, torch.cuda.current_device(), OombComm.unique_id())
+    g = torch.Generator(device="cuda").manual_seed(21)
+    parts = torch.rand(4, 32, 1000, device="cuda", generator=g)
+    assert torch.equal(comm.vote_allgather(parts), fixed_order_sum(parts))
+    o = torch.randn(256, 28, 128, device="cuda", generator=g).bfloat16()
+    lse = torch.randn(256, 28, device="cuda", generator=g)
+    out, lse2 = comm.lse_merge_allgather(o, lse)
+    assert torch.equal(out, o) and torch.equal(lse2, lse)
+    dq = torch.randn(256, 28, 128, device="cuda", generator=g)
+    assert torch.equal(comm.dq_reduce(dq), dq)
+    comm.close()
