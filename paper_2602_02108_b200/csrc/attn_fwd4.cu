@@ -37,6 +37,13 @@ constexpr int kF4Bar = kF4Nv + kF4NvCap;
 constexpr int kF4Smem = kF4Bar + 256;
 static_assert(kF4Smem <= 232448, "dynamic shared memory above the 227 KB opt-in limit");
 constexpr uint32_t kTmS = 0, kTmO = 256;
+#ifndef OOMB_FWD4_PCHUNKS
+#define OOMB_FWD4_PCHUNKS 2
+#endif
+// P is published to the MMA warp in kPChunks key chunks: PV starts on the first keys of a block
+// while the softmax group is still exponentiating the last ones.
+constexpr int kPChunks = OOMB_FWD4_PCHUNKS;
+static_assert(kPChunks == 1 || kPChunks == 2 || kPChunks == 4, "P chunks");
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef OOMB_FWD4_POLY
 #define OOMB_FWD4_POLY 0  // measured: no gain (the softmax phase is latency-bound, not MUFU-bound)
@@ -46,7 +53,7 @@ constexpr bool kF4Poly = OOMB_FWD4_POLY != 0;
 struct F4Bars {
     uint64_t q_full;
     uint64_t k_full[kKSt], k_empty[kKSt], v_full[kVSt], v_empty[kVSt];
-    uint64_t s_full[2], p_full[2], o_done;
+    uint64_t s_full[2], p_full[2][kPChunks], o_done;
     uint32_t tmem_base;
 };
 
@@ -89,7 +96,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bars->s_full[i], 1);
-            mbar_init(&bars->p_full[i], 128);
+            for (int c = 0; c < kPChunks; ++c) mbar_init(&bars->p_full[i][c], 128);
         }
         mbar_init(&bars->o_done, 1);
         fence_barrier_init();
@@ -151,14 +158,20 @@ __global__ void __launch_bounds__(384, 1)
         };
         auto mma_pv = [&](int j) {
             const int st = j % kVSt, b = j & 1;
-            mbar_wait(&bars->p_full[b], (j >> 1) & 1);
             mbar_wait(&bars->v_full[st], (j / kVSt) & 1);
-            tc_fence_after();
             const uint64_t so = boff(st * kTileBytes);
             const uint32_t first = j < 2 ? 0u : 1u;  // the first block of each group overwrites O_w
+            constexpr int kStepsPerChunk = kTile / 16 / kPChunks;
 #pragma unroll
-            for (int ks = 0; ks < kTile / 16; ++ks)
-                umma_ts_w(kTmO + b * 128, kTmS + b * 128 + ks * 8, dVmn + so + mnoff(ks), idesc_o, first | ks);
+            for (int c = 0; c < kPChunks; ++c) {
+                mbar_wait(&bars->p_full[b][c], (j >> 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int i = 0; i < kStepsPerChunk; ++i) {
+                    const int ks = c * kStepsPerChunk + i;
+                    umma_ts_w(kTmO + b * 128, kTmS + b * 128 + ks * 8, dVmn + so + mnoff(ks), idesc_o, first | ks);
+                }
+            }
             umma_commit_w(&bars->v_empty[st]);
         };
         if (nb > 0) mma_s(0);
@@ -237,12 +250,14 @@ __global__ void __launch_bounds__(384, 1)
                     pk[u] = pack_bf16(e0, e1);
                 }
                 tmem_st16(tS + c4 * 16, pk);  // P cols [16 c4, 16 c4 + 16): below the S columns still unread
+                if ((c4 + 1) % (4 / kPChunks) == 0) {  // publish this chunk of P (and, with chunk 0, the O_w rescale)
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(&bars->p_full[wg][c4 / (4 / kPChunks)]);
+                }
             }
             const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
             l = l * alpha + rs;
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&bars->p_full[wg]);
         }
         // ---- merge the two groups: O = (O_0 a_0 + O_1 a_1) / (l_0 a_0 + l_1 a_1), a_w = 2^(m_w - m)
         float2* red = reinterpret_cast<float2*>(smem + kF4Red);
