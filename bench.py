@@ -154,11 +154,13 @@ def offload_measure(run, cap_frac: float):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for i in range(run.S):
-            loop.forward_chunk(i, run.q[i % run.RQ], run.k_all[i * C:(i + 1) * C], run.v_all[i * C:(i + 1) * C])
+            nq = run.q[(i + 1) % run.RQ] if i + 1 < run.S else None  # selection one chunk ahead
+            loop.forward_chunk(i, run.q[i % run.RQ], run.k_all[i * C:(i + 1) * C], run.v_all[i * C:(i + 1) * C],
+                               next_q=nq, out=run.o_all[i], lse=run.lse_all[i])
         loop.begin_backward()
         for i in reversed(range(run.S)):
             loop.backward_chunk(i, run.do[i % run.RQ], run.q[i % run.RQ], run.k_all[i * C:(i + 1) * C],
-                                run.v_all[i * C:(i + 1) * C])
+                                run.v_all[i * C:(i + 1) * C], grads=run.grads)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         out = {"wall_s": wall}
@@ -177,13 +179,17 @@ def offload_measure(run, cap_frac: float):
             "wall_s_capped": off["wall_s"], "wall_s_resident": res["wall_s"],
             "exposed_pct": 100.0 * (off["wall_s"] - res["wall_s"]) / off["wall_s"],
             "h2d_bytes": off["h2d_bytes"], "d2h_bytes": off["d2h_bytes"],
-            "note": "pinned-host page moves on side streams (one batched copy per engine operation); the "
-                    "remaining exposure is the protocol's per-chunk host synchronisation on the selected ids"}
+            "note": "pinned-host page moves on side streams (one batched copy per engine operation); each "
+                    "chunk's selection is issued one chunk ahead, so the host's wait for the selected ids (the "
+                    "fetch decision) does not drain the compute stream"}
 
 
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+SEL_PRIORITY = os.environ.get("OOMB_SEL_PRIORITY", "1") != "0"
+
+
 class Run:
     RQ = 16  # distinct q / dO chunk buffers (K/V are distinct for every chunk)
 
@@ -243,7 +249,9 @@ class Run:
         torch, C = self.torch, self.cfg["C"]
         comp = torch.cuda.current_stream()
         if not hasattr(self, "sel_stream"):
-            self.sel_stream = torch.cuda.Stream()
+            # high priority: the selection's CTAs are scheduled ahead of the running attention's
+            # remaining ones, so chunk i+1's ids are ready before chunk i's attention drains
+            self.sel_stream = torch.cuda.Stream(priority=-1 if SEL_PRIORITY else 0)
             self.ev_app = [torch.cuda.Event() for _ in range(2)]
             self.ev_sel = [torch.cuda.Event() for _ in range(2)]
         ss = self.sel_stream

@@ -618,7 +618,9 @@ inline void check_qkv(const ModelConfig& cfg, const DeviceTensor& q, const Devic
 }
 }  // namespace detail
 
-// attention.hpp:156-208 on the device.
+// attention.hpp:156-208 on the device. Under residency enforcement the library checks the selected
+// pages on the host before the launch (ResidencyError); the kernels' device-side flag is read by
+// PagedCache::check_device_errors() (it synchronises, so it is not done per call).
 inline DeviceAttnSaved attn_forward(const ModelConfig& cfg, const DeviceTensor& q, PagedCache& cache, int layer,
                                     Selection selected, const DeviceTensor& k_cur, const DeviceTensor& v_cur,
                                     cudaStream_t st = nullptr) {
@@ -627,7 +629,6 @@ inline DeviceAttnSaved attn_forward(const ModelConfig& cfg, const DeviceTensor& 
                       std::move(selected)};
     check(oomb_attn_forward(cache.handle(), layer, q.data(), q.dim(0), s.selected.handle(), k_cur.data(),
                             v_cur.data(), s.out.data(), s.lse.as<float>(), sv(st)));
-    if (cache.residency_enforced()) cache.check_device_errors();
     return s;
 }
 // attention.hpp:222-293 on the device: past-page dK/dV go into the cache's fp32 gradient pages.
@@ -642,7 +643,6 @@ inline DeviceAttnGrads attn_backward(const ModelConfig& cfg, const DeviceTensor&
     check(oomb_attn_backward(cache.handle(), layer, dout.data(), q.data(), q.dim(0), saved.selected.handle(),
                              k_cur.data(), v_cur.data(), saved.out.data(), saved.lse.as<float>(), g.dq.as<float>(),
                              g.dk_cur.as<float>(), g.dv_cur.as<float>(), sv(st)));
-    if (cache.residency_enforced()) cache.check_device_errors();
     return g;
 }
 

@@ -201,10 +201,11 @@ def attn_forward(cfg: ModelConfig, q, cache: PagedCache, layer: int, selected, k
     lse = torch.empty((c, qh), dtype=torch.float32, device=q.device) if lse is None else lse
     if out.shape != q.shape or out.dtype != q.dtype or lse.shape != (c, qh) or lse.dtype != torch.float32:
         raise ShapeError("attn_forward: preallocated out / lse have the wrong shape or dtype")
+    # under residency enforcement the library checks the selected pages on the host before the
+    # launch (ResidencyError, paged_kv.hpp:301-312); the kernels' device flag is read by
+    # cache.check_device_errors() without draining the stream on every chunk
     call("oomb_attn_forward_ex", cache.handle, layer, _ptr(q), c, sel.handle, _ptr(k_cur), _ptr(v_cur), _ptr(out),
          _ptr(lse), PAST_ONLY if past_only else 0, stream_handle(stream))
-    if cache.residency_enforced():
-        cache.check_device_errors()
     return AttnSaved(out, lse, sel)
 
 
@@ -231,8 +232,6 @@ def attn_backward(cfg: ModelConfig, dout, q, cache: PagedCache, layer: int, k_cu
     call("oomb_attn_backward_ex", cache.handle, layer, _ptr(dout), _ptr(q), c, sel.handle, _ptr(k_cur),
          _ptr(v_cur), _ptr(saved.out), _ptr(saved.lse), _ptr(dq), _ptr(dk), _ptr(dv), PAST_ONLY if past_only else 0,
          stream_handle(stream))
-    if cache.residency_enforced():
-        cache.check_device_errors()
     return AttnGrads(dq, dk, dv)
 
 

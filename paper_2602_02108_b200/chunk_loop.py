@@ -35,6 +35,9 @@ class AttentionChunkLoop:
         self.sels: list[A.Selection] = []
         self.saved: list[A.AttnSaved] = []
         self.max_chunks = max_chunks
+        self._presel: dict[int, A.Selection] = {}  # selections issued one chunk ahead (forward_chunk next_q)
+        self._sel_stream = None
+        self._votes = None
 
     # ---- selection (chunk_trainer.hpp:292-316)
     def _select(self, i: int, q: torch.Tensor, sel: A.Selection, stream=None) -> A.Selection:
@@ -54,25 +57,56 @@ class AttentionChunkLoop:
     def union(sel: A.Selection) -> np.ndarray:
         return sel.union()
 
-    def forward_chunk(self, i: int, q, k, v, stream=None) -> A.AttnSaved:
-        if i >= len(self.sels):
+    def _selection(self, i: int) -> A.Selection:
+        while i >= len(self.sels):
             kmax = self.m * (self.cfg.budget_pages() if self.mode == "topk" else
                              (self.cfg.local_window if self.mode == "local" else self.cache.max_tokens //
                               self.cfg.page_size))
             self.sels.append(A.Selection(self.cache, self.m, max(kmax, 1)))
-        sel = self._select(i, q, self.sels[i], stream)
+        return self.sels[i]
+
+    def _preselect(self, i: int, q, stream) -> None:
+        """Issue chunk i's page selection on a side stream right after chunk i-1's append (it reads
+        only K_avg of chunks < i, chunk_trainer.hpp:297-311), so it runs under chunk i-1's attention
+        and the host's wait for the ids (the fetch decision) does not drain the compute stream."""
+        if self._sel_stream is None:
+            # high priority: the selection's CTAs go ahead of the running attention's remaining ones
+            self._sel_stream = torch.cuda.Stream(device=self.cache.device, priority=-1)
+            n = self.m * max(self.cache.max_tokens // self.cfg.page_size, 1)
+            self._votes = [torch.empty(n, dtype=torch.float32, device=self.cache.device) for _ in range(2)]
+        ss = self._sel_stream
+        ss.wait_stream(torch.cuda.current_stream() if stream is None else stream)
+        sel = self._selection(i)
+        n_cand = i * self.m
+        if self.mode == "topk" and n_cand > 0:
+            A.select_pages_topk(self.cache, self.layer, q, n_cand, stream=ss, out=sel, vote=self._votes[i & 1])
+        else:
+            self._select(i, q, sel, ss)
+        self._presel[i] = sel
+
+    def forward_chunk(self, i: int, q, k, v, stream=None, next_q=None, out=None, lse=None) -> A.AttnSaved:
+        """One chunk of the forward. next_q: the next chunk's queries; its selection is then issued
+        on a side stream as soon as this chunk's pages are appended (same engine call order).
+        out / lse: caller-owned output buffers (the saved activations of the chunk)."""
+        sel = self._presel.pop(i, None)
+        if sel is None:
+            sel = self._select(i, q, self._selection(i), stream)
+        else:  # the compute stream must not read the selection before the side stream wrote it
+            (torch.cuda.current_stream() if stream is None else stream).wait_stream(self._sel_stream)
         eng = self.engine
         h = None
         if eng is not None:
             h = eng.fetch_async(self.layer, self.union(sel), i)
         r = self.cache.append_chunk(self.layer, k, v, stream=stream)
+        if next_q is not None:
+            self._preselect(i + 1, next_q, stream)
         if eng is not None:
             eng.on_pages_appended(self.layer, r)
             ids = self.union(sel)
             eng.wait(h)
             eng.wait(eng.fetch_async(self.layer, ids, i))
             eng.record_access(self.layer, ids, i)
-        saved = A.attn_forward(self.cfg, q, self.cache, self.layer, sel, k, v, stream=stream)
+        saved = A.attn_forward(self.cfg, q, self.cache, self.layer, sel, k, v, stream=stream, out=out, lse=lse)
         if eng is not None:
             eng.end_layer_use(self.layer, np.concatenate([ids, self.own_pages(i)]))
         if i < len(self.saved):
@@ -81,7 +115,8 @@ class AttentionChunkLoop:
             self.saved.append(saved)
         return saved
 
-    def backward_chunk(self, i: int, dout, q, k, v, stream=None, prefetch_next: bool = True) -> A.AttnGrads:
+    def backward_chunk(self, i: int, dout, q, k, v, stream=None, prefetch_next: bool = True,
+                       grads: A.AttnGrads | None = None) -> A.AttnGrads:
         eng = self.engine
         sel = self.sels[i]
         if eng is not None:
@@ -91,7 +126,7 @@ class AttentionChunkLoop:
             if prefetch_next and i > 0:  # step-ahead prefetch with cached ids + own grad pages
                 nxt = np.union1d(self.union(self.sels[i - 1]), self.own_pages(i - 1)).astype(np.int32)
                 self._pending = eng.fetch_async(self.layer, nxt, i - 1, best_effort=True)
-        g = A.attn_backward(self.cfg, dout, q, self.cache, self.layer, k, v, self.saved[i], stream=stream)
+        g = A.attn_backward(self.cfg, dout, q, self.cache, self.layer, k, v, self.saved[i], stream=stream, grads=grads)
         if eng is not None:
             eng.on_grads_scattered(self.layer, self.union(sel))
         self.cache.accumulate_grad_pages(self.layer, self.own_pages(i), g.dk_cur, g.dv_cur, stream=stream)
@@ -99,8 +134,14 @@ class AttentionChunkLoop:
             eng.end_layer_use(self.layer, ids)
         return g
 
+    def check_device_errors(self) -> None:
+        """The kernels' device-side residency / page-id flags (the host check in front of every
+        launch raises ResidencyError first; this confirms no kernel saw a non-resident slot)."""
+        self.cache.check_device_errors()
+
     def begin_backward(self):
         if self.engine is not None:
+            self.check_device_errors()
             from .tiered_memory import BACKWARD
             self.engine.release_all_reservations()
             self.engine.begin_phase(BACKWARD)

@@ -137,11 +137,11 @@ void validate_cfg(const oomb_config& c) {  // ModelConfig::validate (config.cpp:
 }
 
 
-int32_t pop_slot(std::vector<int32_t>& fl, const char* what) {
+int32_t pop_slot(std::deque<int32_t>& fl, const char* what) {
     OOMB_REQUIRE(!fl.empty(), OOMB_CONFIG_ERROR,
                  std::string("device ") + what + " capacity exhausted (raise device_capacity_pages or offload)");
-    const int32_t s = fl.back();
-    fl.pop_back();
+    const int32_t s = fl.front();
+    fl.pop_front();
     return s;
 }
 
@@ -306,11 +306,9 @@ int oomb_pool_create(const oomb_config* cfg, int device, oomb_pool_t* out) {
             p->pt = new PageTable(c.n_layers, c.page_size, c.n_kv_heads, c.head_dim, p->elem, 4);
             p->n_kv_slots = c.device_capacity_pages > 0 ? c.device_capacity_pages : c.n_layers * p->max_pages;
             p->n_g_slots = p->n_kv_slots;
-            p->kv_free.resize(p->n_kv_slots);
-            p->g_free.resize(p->n_g_slots);
-            // LIFO: slot 0 is handed out first.
-            for (int64_t i = 0; i < p->n_kv_slots; ++i) p->kv_free[i] = static_cast<int32_t>(p->n_kv_slots - 1 - i);
-            for (int64_t i = 0; i < p->n_g_slots; ++i) p->g_free[i] = static_cast<int32_t>(p->n_g_slots - 1 - i);
+            // FIFO (pool.h): slot 0 is handed out first.
+            for (int64_t i = 0; i < p->n_kv_slots; ++i) p->kv_free.push_back(static_cast<int32_t>(i));
+            for (int64_t i = 0; i < p->n_g_slots; ++i) p->g_free.push_back(static_cast<int32_t>(i));
             p->kvslot.assign(c.n_layers, std::vector<int32_t>(p->max_pages, -1));
             p->gslot.assign(c.n_layers, std::vector<int32_t>(p->max_pages, -1));
             const size_t kv_bytes = static_cast<size_t>(p->n_kv_slots) * p->page_elems * p->elem;
@@ -356,7 +354,7 @@ int oomb_pool_destroy(oomb_pool_t p) {
     cudaFree(p->d_kavg_cnt);
     cudaFree(p->d_err);
     cudaFree(p->bwd_ws);
-    if (p->wb_done) cudaEventDestroy(p->wb_done);
+    p->destroy_writeback_events();
     for (auto& r : p->prof.recs) {
         cudaEventDestroy(r.e0);
         cudaEventDestroy(r.e1);

@@ -6,6 +6,7 @@
 #pragma once
 
 #include <algorithm>
+#include <deque>
 #include <string>
 #include <vector>
 
@@ -158,7 +159,9 @@ struct oomb_pool_s {
     int64_t page_elems = 0;
     PageTable* pt = nullptr;
     int64_t n_kv_slots = 0, n_g_slots = 0;
-    std::vector<int32_t> kv_free, g_free;
+    // Free device slots, FIFO: a slot freed by an eviction goes to the back, so the slot handed out
+    // next is the one freed longest ago, whose write-back has most likely drained already.
+    std::deque<int32_t> kv_free, g_free;
     std::vector<std::vector<int32_t>> kvslot, gslot;
     void* kpool = nullptr;
     void* vpool = nullptr;
@@ -177,31 +180,68 @@ struct oomb_pool_s {
     bool prof_on = false;
     Profiler prof;
     // Write-back tickets (offload engine): a slot freed by an eviction carries the number of
-    // the D2H batch that reads it out; `wb_done` is recorded on the (in-order) D2H stream after
-    // the newest batch, so waiting on it covers every older ticket. A stream about to write into
-    // a recycled slot waits once per newer ticket, not once per slot.
+    // the D2H batch that reads it out, and so does the page's host block it was written to. Each
+    // batch records an event on the (in-order) D2H stream; a stream about to write into a recycled
+    // slot, or to read a host block back, waits for that batch only if it has not completed yet
+    // (and at most once per newer batch).
     std::vector<uint64_t> kv_ticket, g_ticket;
-    uint64_t wb_ticket = 0;            // newest write-back batch
-    cudaEvent_t wb_done = nullptr;     // recorded after batch wb_ticket
-    std::vector<std::pair<cudaStream_t, uint64_t>> waited;  // newest ticket each stream has waited for
+    uint64_t wb_ticket = 0;                                    // newest write-back batch
+    uint64_t wb_completed = 0;                                 // every batch <= this has drained
+    std::deque<std::pair<uint64_t, cudaEvent_t>> wb_events;    // batches not yet seen complete
+    std::vector<cudaEvent_t> wb_spare;
+    std::vector<std::pair<cudaStream_t, uint64_t>> waited;     // newest batch each stream has waited for
 
     void free_slot_after_writeback(bool grad, int32_t s) {
         auto& v = grad ? g_ticket : kv_ticket;
         if (v.empty()) v.assign(grad ? n_g_slots : n_kv_slots, 0);
         v[s] = wb_ticket;
     }
+    void record_writeback(cudaStream_t d2h) {  // after the copies of batch wb_ticket
+        cudaEvent_t e;
+        if (wb_spare.empty()) {
+            OOMB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        } else {
+            e = wb_spare.back();
+            wb_spare.pop_back();
+        }
+        OOMB_CUDA(cudaEventRecord(e, d2h));
+        wb_events.emplace_back(wb_ticket, e);
+    }
+    void retire_writebacks() {
+        while (!wb_events.empty()) {
+            const cudaError_t q = cudaEventQuery(wb_events.front().second);
+            if (q == cudaErrorNotReady) return;
+            OOMB_CUDA(q);
+            wb_completed = wb_events.front().first;
+            wb_spare.push_back(wb_events.front().second);
+            wb_events.pop_front();
+        }
+    }
     void wait_slot(bool grad, int32_t s, cudaStream_t st) {
         const auto& v = grad ? g_ticket : kv_ticket;
-        if (v.empty() || v[s] == 0 || !wb_done) return;
-        for (auto& w : waited)
-            if (w.first == st) {
-                if (w.second >= v[s]) return;
-                OOMB_CUDA(cudaStreamWaitEvent(st, wb_done, 0));
-                w.second = wb_ticket;
+        if (!v.empty()) wait_ticket(v[s], st);
+    }
+    // Make stream st wait until write-back batch t has drained (no-op when it has, or when st
+    // already waited for a batch >= t).
+    void wait_ticket(uint64_t t, cudaStream_t st) {
+        if (t <= wb_completed) return;
+        retire_writebacks();
+        if (t <= wb_completed) return;
+        auto it = std::find_if(waited.begin(), waited.end(), [&](const auto& w) { return w.first == st; });
+        if (it != waited.end() && it->second >= t) return;
+        for (const auto& b : wb_events)
+            if (b.first >= t) {  // the first pending batch at or after the slot's: covers it (in-order stream)
+                OOMB_CUDA(cudaStreamWaitEvent(st, b.second, 0));
+                if (it != waited.end()) it->second = b.first;
+                else waited.emplace_back(st, b.first);
                 return;
             }
-        OOMB_CUDA(cudaStreamWaitEvent(st, wb_done, 0));
-        waited.emplace_back(st, wb_ticket);
+    }
+    void destroy_writeback_events() {
+        for (auto& b : wb_events) cudaEventDestroy(b.second);
+        for (auto e : wb_spare) cudaEventDestroy(e);
+        wb_events.clear();
+        wb_spare.clear();
     }
 
     int32_t* kvslot_layer(int l) { return d_kvslot + static_cast<int64_t>(l) * max_pages; }

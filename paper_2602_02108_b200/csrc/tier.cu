@@ -64,6 +64,7 @@ struct oomb_tier_s {
         uint64_t lru = 0;
         bool host_has_kv = false;    // real mode: host block holds data
         bool host_has_grad = false;
+        uint64_t wb_batch = 0;       // real mode: the write-back batch that last filled the host block
     };
     struct Transfer {
         int layer = 0;
@@ -205,8 +206,7 @@ struct oomb_tier_s {
     void end_writeback() {
         if (!real()) return;
         flush_copies(1);
-        if (!pool->wb_done) OOMB_CUDA(cudaEventCreateWithFlags(&pool->wb_done, cudaEventDisableTiming));
-        OOMB_CUDA(cudaEventRecord(pool->wb_done, d2h_stream));
+        pool->record_writeback(d2h_stream);
         OOMB_CUDA(cudaEventRecord(d2h_batch_ev, d2h_stream));
         d2h_batch_ev = nullptr;
     }
@@ -308,12 +308,14 @@ struct oomb_tier_s {
             queue_copy(1, h, static_cast<uint8_t*>(p.kpool) + ks * kvb, kvb);
             queue_copy(1, h + kvb, static_cast<uint8_t*>(p.vpool) + ks * kvb, kvb);
             ps.host_has_kv = true;
+            ps.wb_batch = p.wb_ticket;
         }
         if (wb_grad && gs >= 0) {
             uint8_t* h = host_grad + hidx * grad_block;
             queue_copy(1, h, reinterpret_cast<uint8_t*>(p.gkpool) + gs * gb, gb);
             queue_copy(1, h + gb, reinterpret_cast<uint8_t*>(p.gvpool) + gs * gb, gb);
             ps.host_has_grad = true;
+            ps.wb_batch = p.wb_ticket;
         }
         if (ks >= 0) {
             p.free_slot_after_writeback(false, ks);
@@ -334,8 +336,8 @@ struct oomb_tier_s {
                      std::string("offload: no free device ") + what +
                          " slot for an in-flight fetch (raise the pool's device_capacity_pages above the tier "
                          "capacity)");
-        const int32_t s = fl.back();
-        fl.pop_back();
+        const int32_t s = fl.front();
+        fl.pop_front();
         pool->wait_slot(grad, s, st);
         return s;
     }
@@ -347,6 +349,9 @@ struct oomb_tier_s {
         const size_t kvb = static_cast<size_t>(p.page_elems) * p.elem;
         const size_t gb = static_cast<size_t>(p.page_elems) * sizeof(float);
         PageState& ps = pages[layer][page];
+        // the host block is read only after the write-back that filled it has landed (a page evicted
+        // and fetched back soon after); the destination slots wait for their own read-outs in take_slot
+        p.wait_ticket(ps.wb_batch, h2d_stream);
         const int32_t ks = take_slot(false, h2d_stream, "KV");
         p.kvslot[layer][page] = ks;
         if (ps.host_has_kv) {

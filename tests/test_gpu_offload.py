@@ -26,9 +26,11 @@ def make(mode, capacity=None, n_layers=2):
     return cache, [AttentionChunkLoop(cache, layer=l, engine=eng) for l in range(n_layers)], eng
 
 
-def run(mode, capacity, n_chunks=6, seed=3, n_layers=2):
+def run(mode, capacity, n_chunks=6, seed=3, n_layers=2, pipelined=None):
     """Two attention layers interleaved per chunk, as the trainer runs them (chunk_trainer.hpp:131-186):
-    while one layer attends, the other layer's pages are the eviction candidates."""
+    while one layer attends, the other layer's pages are the eviction candidates. pipelined (default:
+    with an engine): every chunk's selection is issued one chunk ahead on a side stream."""
+    pipelined = capacity is not None if pipelined is None else pipelined
     cache, loops, eng = make(mode, capacity, n_layers)
     g = torch.Generator(device="cuda").manual_seed(seed)
     C = cache.cfg.chunk_size
@@ -38,7 +40,8 @@ def run(mode, capacity, n_chunks=6, seed=3, n_layers=2):
     outs, grads = [], []
     for i in range(n_chunks):
         for l, loop in enumerate(loops):
-            s = loop.forward_chunk(i, qs[l][i], ks[l][i], vs[l][i])
+            nq = qs[l][i + 1] if pipelined and i + 1 < n_chunks else None
+            s = loop.forward_chunk(i, qs[l][i], ks[l][i], vs[l][i], next_q=nq)
             outs.append((s.out.clone(), s.lse.clone()))
     loops[0].begin_backward()
     for i in reversed(range(n_chunks)):
@@ -46,6 +49,7 @@ def run(mode, capacity, n_chunks=6, seed=3, n_layers=2):
             gr = loops[l].backward_chunk(i, dos[l][i], qs[l][i], ks[l][i], vs[l][i])
             grads.append((gr.dq.clone(), gr.dk_cur.clone(), gr.dv_cur.clone()))
     torch.cuda.synchronize()
+    cache.check_device_errors()  # no kernel read a slot that was not resident
     log = None
     if eng is not None:
         eng.release_all_reservations()
