@@ -188,6 +188,10 @@ def offload_measure(run, cap_frac: float):
 # our arm
 # ---------------------------------------------------------------------------
 SEL_PRIORITY = os.environ.get("OOMB_SEL_PRIORITY", "1") != "0"
+# consecutive chunks' attention forwards on two streams (they are independent: see forward_pass)
+FWD_STREAMS = int(os.environ.get("OOMB_FWD_STREAMS", "2"))
+# backward with deferred dQ joins: chunk i-1's dK/dV overlaps chunk i's dQ (OOMB_ATTN_DEFER_DQ)
+BWD_DEFER = os.environ.get("OOMB_BWD_DEFER", "1") != "0"
 
 
 class Run:
@@ -219,6 +223,7 @@ class Run:
         self.grads = A.AttnGrads(torch.empty(C, Hq, hd, device=device), torch.empty(C, Hkv, hd, device=device),
                                  torch.empty(C, Hkv, hd, device=device))
         self.own = [np.arange(i * self.m, (i + 1) * self.m, dtype=np.int32) for i in range(self.S)]
+        self.bwd_phase = []  # (start, end) CUDA events of every step's backward pass
 
     def _select(self, i, q, stream=None):
         from paper_2602_02108_b200._lib import call
@@ -235,10 +240,10 @@ class Run:
         return self.A.attn_forward(self.mc, q, self.cache, 0, self.sels[i], k, v, stream=stream,
                                    out=self.o_all[i] if out is None else out, lse=self.lse_all[i])
 
-    def bwd_chunk(self, i, do, q, k, v, grads=None, stream=None):
+    def bwd_chunk(self, i, do, q, k, v, grads=None, stream=None, defer_dq=False):
         g = self.grads if grads is None else grads
         saved = self.A.AttnSaved(self.o_all[i], self.lse_all[i], self.sels[i])
-        self.A.attn_backward(self.mc, do, q, self.cache, 0, k, v, saved, stream=stream, grads=g)
+        self.A.attn_backward(self.mc, do, q, self.cache, 0, k, v, saved, stream=stream, grads=g, defer_dq=defer_dq)
         self.cache.accumulate_grad_pages(0, self.own[i], g.dk_cur, g.dv_cur, stream=stream)
         return g
 
@@ -256,6 +261,11 @@ class Run:
             self.ev_sel = [torch.cuda.Event() for _ in range(2)]
         ss = self.sel_stream
         ss.wait_stream(comp)  # the cache reset / previous work precede this step's selections
+        if FWD_STREAMS > 1 and not hasattr(self, "att_streams"):
+            self.att_streams = [torch.cuda.Stream() for _ in range(FWD_STREAMS)]
+            self.ev_att = [torch.cuda.Event() for _ in range(FWD_STREAMS)]
+        for st in getattr(self, "att_streams", []):
+            st.wait_stream(comp)
         for i in range(self.S):
             q, k, v = self.q[i % self.RQ], self.k_all[i * C:(i + 1) * C], self.v_all[i * C:(i + 1) * C]
             if i > 0:
@@ -264,18 +274,36 @@ class Run:
             self.ev_sel[i & 1].record(ss)
             self.cache.append_chunk(0, k, v, stream=comp)
             self.ev_app[i & 1].record(comp)
-            comp.wait_event(self.ev_sel[i & 1])
-            self.A.attn_forward(self.mc, q, self.cache, 0, self.sels[i], k, v, stream=comp, out=self.o_all[i],
+            # chunk i's attention reads pages of chunks < i (appended above, before the selection
+            # that chose them) and its own k/v: it does not depend on chunk i-1's attention, so with
+            # FWD_STREAMS > 1 consecutive chunks attend concurrently and fill each other's tail wave
+            ast = comp if FWD_STREAMS <= 1 else self.att_streams[i % FWD_STREAMS]
+            if ast is not comp:
+                ast.wait_event(self.ev_app[i & 1])
+            ast.wait_event(self.ev_sel[i & 1])
+            self.A.attn_forward(self.mc, q, self.cache, 0, self.sels[i], k, v, stream=ast, out=self.o_all[i],
                                 lse=self.lse_all[i])
+        for st in getattr(self, "att_streams", []):
+            comp.wait_stream(st)
         comp.wait_stream(ss)
 
     def step(self):
-        C = self.cfg["C"]
+        torch, C = self.torch, self.cfg["C"]
         self.cache.reset()
         self.forward_pass()
+        comp = torch.cuda.current_stream()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(comp)
         for i in reversed(range(self.S)):
+            # with BWD_DEFER the stream does not wait for chunk i's dQ (it runs on the library's
+            # side stream): chunk i-1's prep and dK/dV start under it; the grads buffers are
+            # reused, so only the last chunk's dQ survives the step (it is not read here)
             self.bwd_chunk(i, self.do[i % self.RQ], self.q[i % self.RQ], self.k_all[i * C:(i + 1) * C],
-                           self.v_all[i * C:(i + 1) * C])
+                           self.v_all[i * C:(i + 1) * C], defer_dq=BWD_DEFER)
+        if BWD_DEFER:
+            self.A.join_dq(self.cache, comp)
+        b1.record(comp)
+        self.bwd_phase.append((b0, b1))
 
 
 class E2E:
@@ -339,8 +367,11 @@ class E2E:
         load_fwd(0)
         # as Run.forward_pass: chunk i+1's selection on a second stream overlaps chunk i's attention
         if not hasattr(self, "ss"):
-            self.ss = torch.cuda.Stream(device=r.dev)
+            self.ss = torch.cuda.Stream(device=r.dev, priority=-1 if SEL_PRIORITY else 0)
+            self.att = [torch.cuda.Stream(device=r.dev) for _ in range(max(FWD_STREAMS, 1))]
         ss = self.ss
+        for st in self.att:
+            st.wait_stream(comp)
         ev_app = [torch.cuda.Event() for _ in range(2)]
         ev_sel = [torch.cuda.Event() for _ in range(2)]
         ss.wait_stream(comp)
@@ -357,21 +388,28 @@ class E2E:
             comp.wait_event(ev_out[b])  # the D2H that last read out slot b finished
             r.cache.append_chunk(0, self.kd[b], self.vd[b], stream=comp)
             ev_app[b].record(comp)
-            comp.wait_event(ev_sel[b])  # (the selection read qd[b] too: ev_used below covers it)
-            r.A.attn_forward(r.mc, self.qd[b], r.cache, 0, r.sels[i], self.kd[b], self.vd[b], stream=comp,
+            # as Run.forward_pass: consecutive chunks attend on alternating streams
+            ast = self.att[i % len(self.att)]
+            ast.wait_event(ev_app[b])
+            ast.wait_event(ev_sel[b])  # (the selection read qd[b] too: ev_used below covers it)
+            r.A.attn_forward(r.mc, self.qd[b], r.cache, 0, r.sels[i], self.kd[b], self.vd[b], stream=ast,
                              out=r.o_all[i], lse=r.lse_all[i])
-            ev_used[b].record(comp)
+            ev_used[b].record(ast)
             with torch.cuda.stream(self.d2h):
                 self.d2h.wait_event(ev_used[b])
                 self.out_h[b].copy_(r.o_all[i], non_blocking=True)
                 ev_out[b].record(self.d2h)
             d2h_b += 2 * r.o_all[i].numel()
+        for st in self.att:
+            comp.wait_stream(st)
 
         def load_bwd(i):
             nonlocal h2d_b
             b = i & 1
             with torch.cuda.stream(self.h2d):
                 self.h2d.wait_event(ev_used[b])
+                if BWD_DEFER:  # the deferred dQ of the chunk that last used slot b read its inputs too
+                    r.A.join_dq(r.cache, self.h2d)
                 self.dod[b].copy_(self.do_h[i % r.RQ], non_blocking=True)
                 self.qd[b].copy_(self.q_h[i % r.RQ], non_blocking=True)
                 self.kd[b].copy_(self.k_h[i * C:(i + 1) * C], non_blocking=True)
@@ -387,15 +425,19 @@ class E2E:
                 load_bwd(order[n + 1])
             comp.wait_event(ev_in[b])
             comp.wait_event(ev_out[b])
-            g = r.bwd_chunk(i, self.dod[b], self.qd[b], self.kd[b], self.vd[b], grads=self.gd[b])
+            g = r.bwd_chunk(i, self.dod[b], self.qd[b], self.kd[b], self.vd[b], grads=self.gd[b], defer_dq=BWD_DEFER)
             ev_used[b].record(comp)
             with torch.cuda.stream(self.d2h):
                 self.d2h.wait_event(ev_used[b])
+                if BWD_DEFER:
+                    r.A.join_dq(r.cache, self.d2h)  # dq(i) ran on the library's side stream
                 self.dq_h[b].copy_(g.dq, non_blocking=True)
                 self.dk_h[b].copy_(g.dk_cur, non_blocking=True)
                 self.dv_h[b].copy_(g.dv_cur, non_blocking=True)
                 ev_out[b].record(self.d2h)
             d2h_b += 4 * (g.dq.numel() + 2 * g.dk_cur.numel())
+        if BWD_DEFER:
+            r.A.join_dq(r.cache, comp)
         comp.wait_stream(self.d2h)
         self.h2d_bytes, self.d2h_bytes = h2d_b, d2h_b
 
@@ -546,11 +588,13 @@ def main():
     clocks.start()
     launches0 = _lib.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    run.bwd_phase.clear()
     e0.record()
     for _ in range(args.steps):
         run.step()
     e1.record()
     torch.cuda.synchronize()
+    bwd_phase_ms = sum(a.elapsed_time(b) for a, b in run.bwd_phase) / args.steps
     launches = _lib.kernel_launches() - launches0
     barrier()
     clk = clocks.stop()
@@ -603,7 +647,12 @@ def main():
 
     # dominant kernel pair: the tcgen05 backward (dq + dkdv launches per chunk)
     # the dq and dkdv kernels run concurrently (dq on a side stream): their pair is timed as one span
-    if "bwd_pair" in prof:
+    if BWD_DEFER:  # chunks chain through the dQ side stream: the backward pass is the span
+        t_bwd = bwd_phase_ms
+        kernels["bwd_phase"] = {"ms_per_step": bwd_phase_ms,
+                                "note": "CUDA events around the whole backward pass (dq + dkdv of every chunk, "
+                                        "chained; also bwd_prep, grad_init, the dM read-back)"}
+    elif "bwd_pair" in prof:
         t_bwd = prof["bwd_pair"][1] / args.steps
     else:
         t_bwd = (prof.get("bwd_dq", (0, 0.0))[1] + prof.get("bwd_dkdv", (0, 0.0))[1]) / args.steps
@@ -623,7 +672,11 @@ def main():
                    "source": tr["source"]}
     except Exception:
         pass
-    roofline = {"bound": "tensor", "kernel": "attn_bwd_dq + attn_bwd_dkdv (tcgen05, run concurrently), per chunk",
+    roofline = {"bound": "tensor",
+                "kernel": ("attn_bwd_dq + attn_bwd_dkdv (tcgen05), every chunk's pair chained through the dQ side "
+                           "stream: achieved = backward FLOPs / backward-pass span (CUDA events on the launching "
+                           "stream)") if BWD_DEFER else
+                          "attn_bwd_dq + attn_bwd_dkdv (tcgen05, run concurrently), per chunk",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if achieved else None, "peak_source": peak_src,
                 "algorithmic": "10*hd*Hq*pairs per chunk, pairs = P*P*sum|sel| + C(C+1)/2 (SURVEY 8d)",

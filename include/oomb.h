@@ -197,6 +197,11 @@ OOMB_API int oomb_attn_backward(oomb_pool_t pool, int layer, const void* dout, c
  * dk_cur / dv_cur when the chunk's keys are not its own. Replaces the reference call sites
  * chunk_trainer.hpp:437 / :565 on a page-range shard. */
 #define OOMB_ATTN_PAST_ONLY 1
+/* Backward only: do not make `stream` wait for dq. The dQ kernel runs on the pool's side stream
+ * concurrently with dK/dV and keeps running under the caller's next work (the next chunk's
+ * backward); oomb_attn_join_dq makes a stream wait for every deferred dq. q, dout, k_cur, v_cur,
+ * the selection and dq must stay untouched until then. */
+#define OOMB_ATTN_DEFER_DQ 2
 OOMB_API int oomb_attn_forward_ex(oomb_pool_t pool, int layer, const void* q, int64_t tokens, oomb_selection_t sel,
                                   const void* k_cur, const void* v_cur, void* out, float* lse, int flags,
                                   void* stream);
@@ -207,6 +212,8 @@ OOMB_API int oomb_attn_backward_ex(oomb_pool_t pool, int layer, const void* dout
 /* Exact merge of page-range shards' partial attention outputs, shards in rank order:
  * o_parts [parts][rows][hd] (dtype), lse_parts [parts][rows] fp32 natural log ->
  * lse = ln sum_r e^{lse_r}, out = sum_r e^{lse_r - lse} o_r. rows = tokens * n_q_heads. */
+/* Make `stream` wait for the dq of every earlier oomb_attn_backward_ex(..., OOMB_ATTN_DEFER_DQ). */
+OOMB_API int oomb_attn_join_dq(oomb_pool_t pool, void* stream);
 OOMB_API int oomb_lse_merge(const void* o_parts, const float* lse_parts, int parts, int64_t rows, int hd, int dtype,
                             void* out, float* lse, void* stream);
 /* Kernel family selection: 0 = auto (tcgen05 when dtype bf16, hd 128, P % 128 == 0),

@@ -184,6 +184,7 @@ class AttnGrads:
 
 
 PAST_ONLY = 1  # OOMB_ATTN_PAST_ONLY: a page-range shard that does not own the chunk's own keys
+DEFER_DQ = 2   # OOMB_ATTN_DEFER_DQ: dq keeps running on the library's side stream (join_dq)
 
 
 def attn_forward(cfg: ModelConfig, q, cache: PagedCache, layer: int, selected, k_cur, v_cur,
@@ -211,9 +212,10 @@ def attn_forward(cfg: ModelConfig, q, cache: PagedCache, layer: int, selected, k
 
 def attn_backward(cfg: ModelConfig, dout, q, cache: PagedCache, layer: int, k_cur, v_cur, saved: AttnSaved,
                   stream=None, grads: AttnGrads | None = None, past_only: bool = False,
-                  selected=None) -> AttnGrads:
+                  selected=None, defer_dq: bool = False) -> AttnGrads:
     """attention.hpp:222-293 — past-page dK/dV go into the cache's gradient pages.
-    `grads` may carry preallocated fp32 output buffers."""
+    `grads` may carry preallocated fp32 output buffers. defer_dq: the stream does not wait for dq
+    (it overlaps the caller's next backward); join_dq(cache, stream) before reading it."""
     dout, q = cache._dev(dout), cache._dev(q)
     k_cur, v_cur = cache._dev(k_cur), cache._dev(v_cur)
     if dout.shape != saved.out.shape:
@@ -230,9 +232,14 @@ def attn_backward(cfg: ModelConfig, dout, q, cache: PagedCache, layer: int, k_cu
             raise ShapeError("attn_backward: preallocated gradients have the wrong shape or dtype")
     sel = saved.selected if selected is None else as_selection(cache, selected, stream)
     call("oomb_attn_backward_ex", cache.handle, layer, _ptr(dout), _ptr(q), c, sel.handle, _ptr(k_cur),
-         _ptr(v_cur), _ptr(saved.out), _ptr(saved.lse), _ptr(dq), _ptr(dk), _ptr(dv), PAST_ONLY if past_only else 0,
-         stream_handle(stream))
+         _ptr(v_cur), _ptr(saved.out), _ptr(saved.lse), _ptr(dq), _ptr(dk), _ptr(dv),
+         (PAST_ONLY if past_only else 0) | (DEFER_DQ if defer_dq else 0), stream_handle(stream))
     return AttnGrads(dq, dk, dv)
+
+
+def join_dq(cache: PagedCache, stream=None) -> None:
+    """Make `stream` wait for every dq deferred by attn_backward(..., defer_dq=True)."""
+    call("oomb_attn_join_dq", cache.handle, stream_handle(stream))
 
 
 def rope(x: torch.Tensor, pos_offset: int, base: float = 10000.0, sign: int = 1, out=None,

@@ -18,8 +18,6 @@
 //                 (the chunk's own keys). Pages never selected are not touched.
 
 #include <cub/block/block_scan.cuh>
-#include <map>
-#include <tuple>
 
 #include "tc_common.cuh"
 
@@ -862,7 +860,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
                         const int32_t* d_gslot_layer, float* gkpool, float* gvpool, const void* k_cur,
                         const void* v_cur, const void* out, const float* lse, float* dq, float* dk_cur,
                         float* dv_cur, int* d_err, void* workspace, size_t workspace_bytes, int nnz, int n_pages,
-                        cudaStream_t st) {
+                        cudaStream_t st, cudaStream_t side, cudaEvent_t ev_prep, cudaEvent_t ev_dq, bool join_dq) {
     OOMB_REQUIRE(workspace_bytes >= attn_bwd_tc_workspace(g, nnz), OOMB_ERROR, "bwd workspace too small");
     OOMB_REQUIRE(g.m <= 64, OOMB_CONFIG_ERROR, "tcgen05 backward supports at most 64 query pages per chunk");
     static bool attr = false;
@@ -895,26 +893,14 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     BwdParams p{g, sel_off, sel_ids, d_kvslot_layer, d_gslot_layer, gkpool, gvpool, w.Dt, w.Lt, w.mask, w.uni,
                 w.n_uni, dq, dk_cur, dv_cur, d_err, CtaTrace{}};
     delete prep_scope;
-    // dQ and dK/dV only read the chunk's inputs and the prep outputs: dQ runs on a side stream,
-    // launched first, and the persistent dK/dV CTAs pick up SMs as dQ's last wave drains (and
-    // vice versa), so neither kernel's tail leaves SMs idle. The caller's stream waits for both.
-    static std::map<int, std::tuple<cudaStream_t, cudaEvent_t, cudaEvent_t>> side_by_dev;
-    int dev = 0;
-    OOMB_CUDA(cudaGetDevice(&dev));
-    auto it = side_by_dev.find(dev);
-    if (it == side_by_dev.end()) {
-        cudaStream_t s2;
-        cudaEvent_t e1, e2;
-        OOMB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
-        OOMB_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
-        OOMB_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
-        it = side_by_dev.emplace(dev, std::make_tuple(s2, e1, e2)).first;
-    }
-    cudaStream_t side = std::get<0>(it->second);
-    cudaEvent_t ev_prep = std::get<1>(it->second), ev_dq = std::get<2>(it->second);
-    // the dQ + dK/dV pair as one span on the caller's stream (the two kernels overlap, so their
-    // own spans each include time spent sharing the GPU with the other)
-    ProfScope* pair_scope = new ProfScope(PK_BWD_PAIR, st);
+    // dQ and dK/dV only read the chunk's inputs and the prep outputs: dQ runs on the pool's side
+    // stream, launched first, and the persistent dK/dV CTAs pick up SMs as dQ's last wave drains
+    // (and vice versa), so neither kernel's tail leaves SMs idle. join_dq: the caller's stream
+    // waits for both; otherwise (OOMB_ATTN_DEFER_DQ) only ev_dq marks dQ's end, and the next
+    // chunk's dK/dV may start under this chunk's dQ.
+    // The dQ + dK/dV pair as one span on the caller's stream (the two kernels overlap, so their
+    // own spans each include time spent sharing the GPU with the other).
+    ProfScope* pair_scope = join_dq ? new ProfScope(PK_BWD_PAIR, st) : nullptr;
     OOMB_CUDA(cudaEventRecord(ev_prep, st));
     OOMB_CUDA(cudaStreamWaitEvent(side, ev_prep, 0));
     {
@@ -939,7 +925,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         attn_bwd_dkdv_kernel<<<n_ctas, 384, kKvSmem, st>>>(tq, tdo, tkc, tvc, maps.kpool, maps.vpool, maps.gkpool,
                                                             maps.gvpool, tdkc, tdvc, p, w.n_uni + 1);
         check_launch("attn_bwd_dkdv_kernel");
-        OOMB_CUDA(cudaStreamWaitEvent(st, ev_dq, 0));
+        if (join_dq) OOMB_CUDA(cudaStreamWaitEvent(st, ev_dq, 0));
         delete pair_scope;
 
     }

@@ -353,7 +353,12 @@ int oomb_pool_destroy(oomb_pool_t p) {
     cudaFree(p->d_kavg_sum);
     cudaFree(p->d_kavg_cnt);
     cudaFree(p->d_err);
-    cudaFree(p->bwd_ws);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(p->bwd_ws[b]);
+        if (p->bwd_ev_dq[b]) cudaEventDestroy(p->bwd_ev_dq[b]);
+    }
+    if (p->bwd_ev_prep) cudaEventDestroy(p->bwd_ev_prep);
+    if (p->bwd_side) cudaStreamDestroy(p->bwd_side);
     p->destroy_writeback_events();
     for (auto& r : p->prof.recs) {
         cudaEventDestroy(r.e0);
@@ -864,18 +869,31 @@ int oomb_attn_backward_ex(oomb_pool_t p, int layer, const void* dout, const void
         const size_t kvb = static_cast<size_t>(tokens) * g.Hkv * g.hd * sizeof(float);
         const bool tc = p->policy != 1 && p->maps.valid && tc_supported(g, p->cfg.dtype) && tc_bwd_available();
         if (tc) {
-            const size_t need = attn_bwd_tc_workspace(g, sel->nnz);
-            if (need > p->bwd_ws_bytes) {
-                OOMB_CUDA(cudaStreamSynchronize(S(stream)));
-                cudaFree(p->bwd_ws);
-                p->bwd_ws = nullptr;
-                OOMB_CUDA(cudaMalloc(&p->bwd_ws, need));
-                p->bwd_ws_bytes = need;
+            if (!p->bwd_side) {
+                OOMB_CUDA(cudaStreamCreateWithFlags(&p->bwd_side, cudaStreamNonBlocking));
+                OOMB_CUDA(cudaEventCreateWithFlags(&p->bwd_ev_prep, cudaEventDisableTiming));
+                for (int b = 0; b < 2; ++b) OOMB_CUDA(cudaEventCreateWithFlags(&p->bwd_ev_dq[b], cudaEventDisableTiming));
             }
+            const bool defer = (flags & OOMB_ATTN_DEFER_DQ) != 0;
+            const int b = p->bwd_parity;
+            p->bwd_parity ^= 1;
+            const size_t need = attn_bwd_tc_workspace(g, sel->nnz);
+            if (need > p->bwd_ws_bytes[b]) {
+                OOMB_CUDA(cudaDeviceSynchronize());  // a deferred dQ may still read the old workspace
+                cudaFree(p->bwd_ws[b]);
+                p->bwd_ws[b] = nullptr;
+                OOMB_CUDA(cudaMalloc(&p->bwd_ws[b], need));
+                p->bwd_ws_bytes[b] = need;
+            }
+            // the dQ that last used this workspace has finished reading it
+            if (p->bwd_ws_used[b]) OOMB_CUDA(cudaStreamWaitEvent(S(stream), p->bwd_ev_dq[b], 0));
             launch_attn_bwd_tc(g, p->maps, dout, q, sel->d_off, sel->d_ids, p->kvslot_layer(layer),
                                p->gslot_layer(layer), p->gkpool, p->gvpool, k_cur, v_cur, out, lse, dq, dk_cur,
-                               dv_cur, p->d_err, p->bwd_ws, p->bwd_ws_bytes, sel->nnz,
-                               static_cast<int>(p->pt->pages[layer].size()), S(stream));
+                               dv_cur, p->d_err, p->bwd_ws[b], p->bwd_ws_bytes[b], sel->nnz,
+                               static_cast<int>(p->pt->pages[layer].size()), S(stream), p->bwd_side,
+                               p->bwd_ev_prep, p->bwd_ev_dq[b], !defer);
+            p->bwd_ws_used[b] = true;
+            p->bwd_last_dq = p->bwd_ev_dq[b];
         } else {
             OOMB_CUDA(cudaMemsetAsync(dk_cur, 0, kvb, S(stream)));
             OOMB_CUDA(cudaMemsetAsync(dv_cur, 0, kvb, S(stream)));
@@ -890,6 +908,13 @@ int oomb_attn_backward(oomb_pool_t p, int layer, const void* dout, const void* q
                        oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out, const float* lse,
                        float* dq, float* dk_cur, float* dv_cur, void* stream) {
     return oomb_attn_backward_ex(p, layer, dout, q, tokens, sel, k_cur, v_cur, out, lse, dq, dk_cur, dv_cur, 0, stream);
+}
+
+int oomb_attn_join_dq(oomb_pool_t p, void* stream) {
+    return guard([&] {
+        set_dev(p);
+        if (p->bwd_last_dq) OOMB_CUDA(cudaStreamWaitEvent(S(stream), p->bwd_last_dq, 0));
+    });
 }
 
 int oomb_accumulate_grad_pages(oomb_pool_t p, int layer, const int32_t* ids, int n, float* dk, float* dv,

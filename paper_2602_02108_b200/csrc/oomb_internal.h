@@ -215,7 +215,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
                         const int32_t* d_gslot_layer, float* gkpool, float* gvpool, const void* k_cur,
                         const void* v_cur, const void* out, const float* lse, float* dq, float* dk_cur,
                         float* dv_cur, int* d_err, void* workspace, size_t workspace_bytes, int nnz, int n_pages,
-                        cudaStream_t st);
+                        cudaStream_t st, cudaStream_t side, cudaEvent_t ev_prep, cudaEvent_t ev_dq, bool join_dq);
 size_t attn_bwd_tc_workspace(const AttnGeom& g, int max_sel_ids);
 bool score_tc_supported(int dtype, int hd, int P, int64_t tokens);
 size_t score_tc_workspace(int64_t tokens, int Hq, int Hkv, int64_t n, int P);

@@ -175,8 +175,17 @@ struct oomb_pool_s {
     bool enforce = false;
     int policy = 0;
     TcPoolMaps maps;
-    void* bwd_ws = nullptr;
-    size_t bwd_ws_bytes = 0;
+    // tcgen05 backward: dQ runs on bwd_side concurrently with dK/dV on the caller's stream. Two
+    // workspaces alternate between calls so that, with OOMB_ATTN_DEFER_DQ, chunk i-1's prep and
+    // dK/dV can start while chunk i's dQ still reads its workspace (bwd_ev_dq[b] marks its end).
+    void* bwd_ws[2] = {nullptr, nullptr};
+    size_t bwd_ws_bytes[2] = {0, 0};
+    bool bwd_ws_used[2] = {false, false};
+    int bwd_parity = 0;
+    cudaStream_t bwd_side = nullptr;
+    cudaEvent_t bwd_ev_prep = nullptr;
+    cudaEvent_t bwd_ev_dq[2] = {nullptr, nullptr};
+    cudaEvent_t bwd_last_dq = nullptr;
     bool prof_on = false;
     Profiler prof;
     // Write-back tickets (offload engine): a slot freed by an eviction carries the number of
