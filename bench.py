@@ -223,7 +223,8 @@ class Run:
         self.grads = A.AttnGrads(torch.empty(C, Hq, hd, device=device), torch.empty(C, Hkv, hd, device=device),
                                  torch.empty(C, Hkv, hd, device=device))
         self.own = [np.arange(i * self.m, (i + 1) * self.m, dtype=np.int32) for i in range(self.S)]
-        self.bwd_phase = []  # (start, end) CUDA events of every step's backward pass
+        self.fwd_phase = []  # (start, end) CUDA events of every step's forward pass
+        self.bwd_phase = []  # and of its backward pass
 
     def _select(self, i, q, stream=None):
         from paper_2602_02108_b200._lib import call
@@ -290,9 +291,10 @@ class Run:
     def step(self):
         torch, C = self.torch, self.cfg["C"]
         self.cache.reset()
-        self.forward_pass()
         comp = torch.cuda.current_stream()
-        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0, b0, b1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        f0.record(comp)
+        self.forward_pass()
         b0.record(comp)
         for i in reversed(range(self.S)):
             # with BWD_DEFER the stream does not wait for chunk i's dQ (it runs on the library's
@@ -303,6 +305,7 @@ class Run:
         if BWD_DEFER:
             self.A.join_dq(self.cache, comp)
         b1.record(comp)
+        self.fwd_phase.append((f0, b0))
         self.bwd_phase.append((b0, b1))
 
 
@@ -588,6 +591,7 @@ def main():
     clocks.start()
     launches0 = _lib.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    run.fwd_phase.clear()
     run.bwd_phase.clear()
     e0.record()
     for _ in range(args.steps):
@@ -595,6 +599,7 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     bwd_phase_ms = sum(a.elapsed_time(b) for a, b in run.bwd_phase) / args.steps
+    fwd_phase_ms = sum(a.elapsed_time(b) for a, b in run.fwd_phase) / args.steps
     launches = _lib.kernel_launches() - launches0
     barrier()
     clk = clocks.stop()
@@ -639,6 +644,10 @@ def main():
     for k in ("bwd_dq", "bwd_dkdv"):
         if k in kernels and "bwd_pair" in kernels:
             kernels[k]["note"] = "overlaps the other backward kernel; see bwd_pair for their joint span"
+    for k in ("bwd_dq", "bwd_dkdv", "bwd_prep", "gather_scatter", "grad_init"):
+        if k in kernels and BWD_DEFER:
+            kernels[k]["note"] = ("chunk i's dQ runs on the library's side stream under chunk i-1's prep, dK/dV and "
+                                  "dM read-back: these spans overlap each other; see bwd_phase")
     for k in ("score", "topk", "other", "append", "attn_fwd"):
         if k in kernels:
             kernels[k]["note"] = ("chunk i+1's selection (score, topk; the dense CSR fill is 'other') runs on "
@@ -656,7 +665,11 @@ def main():
         t_bwd = prof["bwd_pair"][1] / args.steps
     else:
         t_bwd = (prof.get("bwd_dq", (0, 0.0))[1] + prof.get("bwd_dkdv", (0, 0.0))[1]) / args.steps
-    t_fwd = prof.get("attn_fwd", (0, 0.0))[1] / args.steps
+    kernels["fwd_phase"] = {"ms_per_step": fwd_phase_ms,
+                            "note": "CUDA events around the whole forward pass (selection, append and attention of "
+                                    "every chunk)"}
+    # with two attention streams the per-launch spans overlap: the forward pass span is the honest time
+    t_fwd = fwd_phase_ms if FWD_STREAMS > 1 else prof.get("attn_fwd", (0, 0.0))[1] / args.steps
     for name, fl, t in (("attn_fwd", fwd_fl, t_fwd), ("attn_bwd(dq+dkdv)", bwd_fl, t_bwd)):
         if t > 0:
             kernels.setdefault(name, {})
@@ -696,6 +709,9 @@ def main():
             "gpu_launches_timed_region": launches, "clocks": clk, "e2e": e2e, "offload": offload,
             "train_step_variant": {
                 "what": "full train step of SURVEY 3.2: 2 forwards (phase A + recompute) + 1 backward per chunk; "
+                        "the recompute forward is charged as a whole forward pass (fwd_phase, selection and append "
+                        "included: an upper bound)" if FWD_STREAMS > 1 else
+                        "full train step of SURVEY 3.2: 2 forwards (phase A + recompute) + 1 backward per chunk; "
                         "the recompute forward is the same forward kernel, timed above",
                 "tokens_per_s": world * cfg["T"] / ((ms_step + t_fwd) / 1e3),
                 "ms_per_step": ms_step + t_fwd}}
