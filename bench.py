@@ -309,11 +309,15 @@ class Run:
         self.bwd_phase.append((b0, b1))
 
 
+NB = 3  # e2e staging depth
+
+
 class E2E:
     """Same step through the public API, inputs from pinned host memory: per chunk
     H2D(q, k, v) before the forward, D2H(out) after it; H2D(dO, q, k, v) before the
     backward, D2H(dq, dk_cur, dv_cur) after it. Copies run on side streams one chunk
-    ahead (double-buffered device staging) so they overlap the kernels."""
+    ahead (NB-deep device staging, so a slow read-out of chunk i-NB is the only thing chunk i's
+    kernels can wait for) so they overlap the kernels."""
 
     def __init__(self, run: Run):
         torch = run.torch
@@ -327,17 +331,17 @@ class E2E:
         self.q_h = [x.cpu().pin_memory() for x in run.q]
         self.do_h = [x.cpu().pin_memory() for x in run.do]
         bf = torch.bfloat16
-        self.out_h = [torch.empty(C, Hq, hd, dtype=bf, **pin) for _ in range(2)]
-        self.dq_h = [torch.empty(C, Hq, hd, **pin) for _ in range(2)]
-        self.dk_h = [torch.empty(C, Hkv, hd, **pin) for _ in range(2)]
-        self.dv_h = [torch.empty(C, Hkv, hd, **pin) for _ in range(2)]
+        self.out_h = [torch.empty(C, Hq, hd, dtype=bf, **pin) for _ in range(NB)]
+        self.dq_h = [torch.empty(C, Hq, hd, **pin) for _ in range(NB)]
+        self.dk_h = [torch.empty(C, Hkv, hd, **pin) for _ in range(NB)]
+        self.dv_h = [torch.empty(C, Hkv, hd, **pin) for _ in range(NB)]
         d = run.dev
-        self.qd = [torch.empty(C, Hq, hd, dtype=bf, device=d) for _ in range(2)]
-        self.dod = [torch.empty(C, Hq, hd, dtype=bf, device=d) for _ in range(2)]
-        self.kd = [torch.empty(C, Hkv, hd, dtype=bf, device=d) for _ in range(2)]
-        self.vd = [torch.empty(C, Hkv, hd, dtype=bf, device=d) for _ in range(2)]
+        self.qd = [torch.empty(C, Hq, hd, dtype=bf, device=d) for _ in range(NB)]
+        self.dod = [torch.empty(C, Hq, hd, dtype=bf, device=d) for _ in range(NB)]
+        self.kd = [torch.empty(C, Hkv, hd, dtype=bf, device=d) for _ in range(NB)]
+        self.vd = [torch.empty(C, Hkv, hd, dtype=bf, device=d) for _ in range(NB)]
         self.gd = [run.A.AttnGrads(torch.empty(C, Hq, hd, device=d), torch.empty(C, Hkv, hd, device=d),
-                                   torch.empty(C, Hkv, hd, device=d)) for _ in range(2)]
+                                   torch.empty(C, Hkv, hd, device=d)) for _ in range(NB)]
         self.h2d = torch.cuda.Stream(device=d)
         self.d2h = torch.cuda.Stream(device=d)
         self.h2d_bytes = 0
@@ -350,15 +354,15 @@ class E2E:
         S = r.S
         r.cache.reset()
         h2d_b = d2h_b = 0
-        ev_in = [torch.cuda.Event() for _ in range(2)]
-        ev_used = [torch.cuda.Event() for _ in range(2)]
-        ev_out = [torch.cuda.Event() for _ in range(2)]
+        ev_in = [torch.cuda.Event() for _ in range(NB)]
+        ev_used = [torch.cuda.Event() for _ in range(NB)]
+        ev_out = [torch.cuda.Event() for _ in range(NB)]
         for e in ev_used + ev_out:
             e.record(comp)
 
         def load_fwd(i):
             nonlocal h2d_b
-            b = i & 1
+            b = i % NB
             with torch.cuda.stream(self.h2d):
                 self.h2d.wait_event(ev_used[b])
                 self.qd[b].copy_(self.q_h[i % r.RQ], non_blocking=True)
@@ -375,16 +379,16 @@ class E2E:
         ss = self.ss
         for st in self.att:
             st.wait_stream(comp)
-        ev_app = [torch.cuda.Event() for _ in range(2)]
-        ev_sel = [torch.cuda.Event() for _ in range(2)]
+        ev_app = [torch.cuda.Event() for _ in range(NB)]
+        ev_sel = [torch.cuda.Event() for _ in range(NB)]
         ss.wait_stream(comp)
         for i in range(S):
-            b = i & 1
+            b = i % NB
             if i + 1 < S:
                 load_fwd(i + 1)
             ss.wait_event(ev_in[b])
             if i > 0:
-                ss.wait_event(ev_app[(i - 1) & 1])  # K_avg of every earlier chunk is in
+                ss.wait_event(ev_app[(i - 1) % NB])  # K_avg of every earlier chunk is in
             r._select(i, self.qd[b], stream=ss)
             ev_sel[b].record(ss)
             comp.wait_event(ev_in[b])
@@ -408,7 +412,7 @@ class E2E:
 
         def load_bwd(i):
             nonlocal h2d_b
-            b = i & 1
+            b = i % NB
             with torch.cuda.stream(self.h2d):
                 self.h2d.wait_event(ev_used[b])
                 if BWD_DEFER:  # the deferred dQ of the chunk that last used slot b read its inputs too
@@ -423,7 +427,7 @@ class E2E:
         order = list(reversed(range(S)))
         load_bwd(order[0])
         for n, i in enumerate(order):
-            b = i & 1
+            b = i % NB
             if n + 1 < S:
                 load_bwd(order[n + 1])
             comp.wait_event(ev_in[b])
