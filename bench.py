@@ -173,9 +173,11 @@ def offload_measure(run, cap_frac: float):
         return out
 
     step(1.0)  # warm-up of the loop path
-    res = step(1.0)
-    off = step(cap_frac)
+    runs = [(step(1.0), step(cap_frac)) for _ in range(2)]  # alternate; wall clock: keep the best of two
+    res = min((r for r, _ in runs), key=lambda x: x["wall_s"])
+    off = min((o for _, o in runs), key=lambda x: x["wall_s"])
     return {"capacity_frac": cap_frac, "capacity_pages": off["cap_pages"], "layer_pages": n_pages,
+            "wall_s_capped_runs": [o["wall_s"] for _, o in runs], "wall_s_resident_runs": [r["wall_s"] for r, _ in runs],
             "wall_s_capped": off["wall_s"], "wall_s_resident": res["wall_s"],
             "exposed_pct": 100.0 * (off["wall_s"] - res["wall_s"]) / off["wall_s"],
             "h2d_bytes": off["h2d_bytes"], "d2h_bytes": off["d2h_bytes"],
