@@ -199,7 +199,7 @@ BWD_DEFER = os.environ.get("OOMB_BWD_DEFER", "1") != "0"
 class Run:
     RQ = 16  # distinct q / dO chunk buffers (K/V are distinct for every chunk)
 
-    def __init__(self, cfg, seed: int, device):
+    def __init__(self, cfg, seed: int, device, comm=None):
         import torch
         from paper_2602_02108_b200 import ModelConfig, PagedCache
         from paper_2602_02108_b200 import attention as A
@@ -225,6 +225,11 @@ class Run:
         self.grads = A.AttnGrads(torch.empty(C, Hq, hd, device=device), torch.empty(C, Hkv, hd, device=device),
                                  torch.empty(C, Hkv, hd, device=device))
         self.own = [np.arange(i * self.m, (i + 1) * self.m, dtype=np.int32) for i in range(self.S)]
+        # KV-group sharding (--shard kv): this rank holds Hkv of the model's KV groups; the page vote
+        # sums over every rank's groups (per-group partial votes, NCCL all-gather in group order)
+        self.comm = comm
+        if comm is not None:
+            self.parts = torch.empty(Hkv * self.m * max(T // P, 1), device=device, dtype=torch.float32)
         self.fwd_phase = []  # (start, end) CUDA events of every step's forward pass
         self.bwd_phase = []  # and of its backward pass
 
@@ -232,7 +237,16 @@ class Run:
         from paper_2602_02108_b200._lib import call
         from paper_2602_02108_b200.paged_kv import stream_handle
         n_cand = i * self.m
-        if self.cfg["mode"] == "topk" and n_cand > 0:
+        if self.cfg["mode"] == "topk" and n_cand > 0 and self.comm is not None:
+            from paper_2602_02108_b200.paged_kv import _ptr
+            n, g = min(n_cand, self.cache.n_pages(0)), self.cfg["Hkv"]
+            parts = self.parts[: g * self.m * n].view(g, self.m, n)
+            call("oomb_score_pages_partial", self.cache.handle, 0, _ptr(q), q.shape[0], n, _ptr(parts),
+                 stream_handle(stream))
+            vote = self.comm.vote_allgather(parts, stream=stream, out=self.vote[: self.m * n].view(self.m, n))
+            call("oomb_select_topk", self.sels[i].handle, _ptr(vote), self.m, n, self.cfg["budget"] // self.cfg["P"],
+                 stream_handle(stream))
+        elif self.cfg["mode"] == "topk" and n_cand > 0:
             self.A.select_pages_topk(self.cache, 0, q, n_cand, stream=stream, out=self.sels[i], vote=self.vote)
         else:  # dense (select_all) or no candidates yet (chunk_trainer.hpp:297-304)
             call("oomb_select_all", self.sels[i].handle, n_cand, self.m, stream_handle(stream))
@@ -528,6 +542,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-workers", type=int, default=None)
     ap.add_argument("--tokens", type=int, default=None, help="override the context length (debug)")
+    ap.add_argument("--shard", default="replica", choices=["replica", "kv"],
+                    help="replica: every rank runs its own sequence (weak scaling, the default); kv: one sequence "
+                         "split across the ranks by KV-head group, page votes all-gathered over NCCL (strong scaling)")
     ap.add_argument("--offload-cap", type=float, default=0.75,
                     help="device capacity (fraction of the layer's pages) of the offload measurement; 0 = skip")
     args = ap.parse_args()
@@ -541,7 +558,9 @@ def main():
                    "chunk": cfg["C"], "page": cfg["P"], "q_heads": cfg["Hq"], "kv_heads": cfg["Hkv"],
                    "head_dim": cfg["hd"], "selection": cfg["mode"],
                    "pages_per_query_page": cfg["budget"] // cfg["P"] if cfg["mode"] == "topk" else "all",
-                   "layers_per_step": 1}
+                   "layers_per_step": 1,
+                   "parallelism": (f"one sequence split by KV-head group over {world} GPU(s)" if args.shard == "kv"
+                                   else f"{world} independent replica(s), one sequence each")}
 
     if args.impl == "reference":
         if rank != 0:
@@ -583,7 +602,16 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
-    run = Run(cfg, seed=1234 + rank, device=dev)
+    comm = None
+    run_cfg = cfg
+    if args.shard == "kv":
+        from paper_2602_02108_b200.sharding import KVGroupShard, OombComm
+        sh = KVGroupShard(rank, world, cfg["Hkv"], cfg["Hq"])  # raises when the groups do not divide
+        comm = (OombComm.from_process_group() if world > 1
+                else OombComm(0, 1, dev.index, OombComm.unique_id()))
+        run_cfg = dict(cfg, Hq=cfg["Hq"] // world, Hkv=sh.kv_local)
+        args.no_e2e, args.no_cpu, args.offload_cap = True, True, 0.0  # the sharded line is throughput only
+    run = Run(run_cfg, seed=1234 + rank, device=dev, comm=comm)
     for _ in range(args.warmup):
         run.step()
     torch.cuda.synchronize()
@@ -612,7 +640,8 @@ def main():
     prof = run.cache.profile_collect()
     run.cache.profile_enable(False)
     ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    value = world * cfg["T"] / (ms_step / 1e3)
+    seqs = 1 if args.shard == "kv" else world  # sequences processed by the whole job per step
+    value = seqs * cfg["T"] / (ms_step / 1e3)
 
     # ---- e2e: same API from pinned host buffers
     e2e = None
@@ -643,7 +672,10 @@ def main():
     peak, peak_sus, hbm, peak_src = peaks()
     fwd_fl = sum(c["fwd"] for c in chunks)
     bwd_fl = sum(c["bwd"] for c in chunks)
-    tflops = (fwd_fl + bwd_fl) / (ms_step / 1e3) / 1e12
+    # per-GPU algorithmic TFLOP/s: a kv shard does 1/world of the sequence's heads
+    tflops = (fwd_fl + bwd_fl) / (ms_step / 1e3) / 1e12 / (world if args.shard == "kv" else 1)
+    if args.shard == "kv":
+        fwd_fl, bwd_fl = fwd_fl / world, bwd_fl / world
     kernels = {}
     for k, (n, ms) in prof.items():
         kernels[k] = {"launches_per_step": n / args.steps, "ms_per_step": ms / args.steps}
@@ -701,7 +733,8 @@ def main():
                 "algorithmic": "10*hd*Hq*pairs per chunk, pairs = P*P*sum|sel| + C(C+1)/2 (SURVEY 8d)",
                 "traffic": traffic}
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if args.shard == "kv" else "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic N(0,1) bf16 q/k/v/dO generated on device (1M-token K/V distinct per chunk; "
                     "16 distinct q/dO chunks cycled); random-init, no checkpoint",

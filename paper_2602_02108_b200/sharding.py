@@ -98,13 +98,13 @@ class OombComm:
 
     __del__ = close
 
-    def vote_allgather(self, partials_local: torch.Tensor, stream=None) -> torch.Tensor:
+    def vote_allgather(self, partials_local: torch.Tensor, stream=None, out: torch.Tensor | None = None) -> torch.Tensor:
         """[G_local, m, n] partial votes -> [m, n] summed over all ranks' groups in global order."""
         from ._lib import comm_call
         from .paged_kv import stream_handle
         g, m, n = partials_local.shape
         p = partials_local.contiguous()
-        vote = torch.empty((m, n), dtype=torch.float32, device=p.device)
+        vote = torch.empty((m, n), dtype=torch.float32, device=p.device) if out is None else out
         comm_call("oomb_vote_allgather", self.handle, C.c_void_p(p.data_ptr()), g, m, n, C.c_void_p(vote.data_ptr()),
                   stream_handle(stream))
         return vote

@@ -155,3 +155,20 @@ def test_nccl_comm_world1_exchanges_are_exact():
     dq = torch.randn(256, 28, 128, device="cuda", generator=g)
     assert torch.equal(comm.dq_reduce(dq), dq)
     comm.close()
+
+
+def test_bench_kv_shard_mode_world1():
+    """bench.py --shard kv (one sequence split by KV-head group, votes all-gathered over NCCL)
+    runs end to end and reports strong scaling; world 1 here, the same code at world 2 / 4."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--shard", "kv", "--config", "c3",
+                        "--tokens", str(16 * 4096), "--steps", "1", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["scaling"] == "strong" and line["value"] > 0 and line["gpu_launches"] > 0
+    assert "KV-head group" in line["config"]["parallelism"]

@@ -16,7 +16,7 @@ try:
     d = json.loads(open(f"gpurun_out/ab_{v}_{rep}.json").read().strip().splitlines()[-1])
     k = d.get("kernels", {})
     print(f"{v:10s} rep{rep} ms/step {d['ms_per_step']:.1f}  frac {d['roofline']['frac']:.3f}  clocks {d['clocks']['sm_mhz']}  " +
-          "  ".join(f"{n}={k[n]['ms_per_step']:.1f}" for n in ("score", "attn_fwd", "bwd_pair", "bwd_dq", "bwd_dkdv") if n in k))
+          "  ".join(f"{n}={k[n]['ms_per_step']:.1f}" for n in ("fwd_phase", "bwd_phase", "score") if n in k))
 except Exception as e:
     print(v, rep, "failed", e, open(f"gpurun_out/ab_{v}_{rep}.err").read()[-800:])
 PY
