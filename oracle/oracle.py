@@ -553,3 +553,61 @@ def to_bf16(x: np.ndarray) -> np.ndarray:
     a = np.ascontiguousarray(np.asarray(x, dtype=np.float32)).view(np.uint32).astype(np.uint64)
     rounded = (a + np.uint64(0x7FFF) + ((a >> np.uint64(16)) & np.uint64(1))) & np.uint64(0xFFFF0000)
     return rounded.astype(np.uint32).view(np.float32).reshape(np.shape(x))
+
+
+# ---------------------------------------------------------------------------
+# Whole-model chunked training step: the reference's
+# ChunkTrainer::train_step through the shim. TEST INFRASTRUCTURE.
+# ---------------------------------------------------------------------------
+class RefModelCfg(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("n_layers", "d_model", "n_q_heads", "n_kv_heads", "head_dim", "d_ff",
+                                       "vocab_size", "chunk_size", "page_size", "retrieval_budget", "local_window",
+                                       "score_scale", "mode")] + [("rope_base", C.c_double), ("seed", C.c_uint64)]
+
+
+MODES = {"dense": 0, "topk": 1, "local": 2}
+
+
+def ref_model_cfg(mc, mode: str) -> RefModelCfg:
+    """chunktrain::ModelConfig fields from a paper_2602_02108_b200 ModelConfig (one mode for all layers)."""
+    return RefModelCfg(mc.n_layers, mc.d_model, mc.n_q_heads, mc.n_kv_heads, mc.head_dim, mc.d_ff, mc.vocab_size,
+                       mc.chunk_size, mc.page_size, mc.retrieval_budget, mc.local_window, int(mc.score_scale),
+                       MODES[mode], mc.rope_base, mc.seed)
+
+
+def _ref_model_lib():
+    L = C.CDLL(build_ref())
+    L.ref_model_numel.restype = C.c_int64
+    L.ref_last_error.restype = C.c_char_p
+    return L
+
+
+def ref_init_params(mc, mode: str, seed: int, real_bytes: int = 4) -> np.ndarray:
+    """init_params (model.hpp:127-145), flattened in ModelParams::visit order."""
+    L = _ref_model_lib()
+    c = ref_model_cfg(mc, mode)
+    n = L.ref_model_numel(C.byref(c))
+    out = np.zeros(n, np.float32 if real_bytes == 4 else np.float64)
+    if L.ref_init_params(real_bytes, C.byref(c), C.c_uint64(seed), out.ctypes.data_as(C.c_void_p)):
+        raise OracleError(9, L.ref_last_error().decode())
+    return out
+
+
+def ref_train_step(mc, mode: str, params: np.ndarray, tokens: np.ndarray):
+    """ChunkTrainer<Real>::train_step (chunk_trainer.hpp:131-186) -> (loss, flat grads, selected-id counts
+    per (chunk, layer, query page)). Real follows params.dtype."""
+    L = _ref_model_lib()
+    c = ref_model_cfg(mc, mode)
+    rb = params.dtype.itemsize
+    params = np.ascontiguousarray(params)
+    toks = np.ascontiguousarray(tokens, dtype=np.int32)
+    grads = np.zeros_like(params)
+    loss = C.c_double()
+    n_chunks = (len(toks) + mc.chunk_size - 1) // mc.chunk_size
+    counts = np.zeros(n_chunks * mc.n_layers * (mc.chunk_size // mc.page_size), np.int32)
+    rc = L.ref_train_step(rb, C.byref(c), params.ctypes.data_as(C.c_void_p), toks.ctypes.data_as(C.c_void_p),
+                          C.c_int64(len(toks)), grads.ctypes.data_as(C.c_void_p), C.byref(loss),
+                          counts.ctypes.data_as(C.c_void_p))
+    if rc:
+        raise OracleError(rc, L.ref_last_error().decode())
+    return loss.value, grads, counts

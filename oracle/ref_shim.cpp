@@ -33,6 +33,8 @@
 
 #define private public
 #include "chunktrain/attention.hpp"
+#include "chunktrain/chunk_trainer.hpp"
+#include "chunktrain/model.hpp"
 #include "chunktrain/oracle.hpp"
 #include "chunktrain/paged_kv.hpp"
 #include "chunktrain/tiered_memory.hpp"
@@ -568,6 +570,100 @@ int ref_validate_schedule(const RefEvent* ev, int64_t n, double bandwidth, doubl
         out[4] = static_cast<double>(rep.d2h_bytes);
         out[5] = rep.overlap_fraction;
         *n_violations = static_cast<int>(rep.violations.size());
+    });
+}
+
+// ---- whole-model chunked training step: ChunkTrainer::train_step
+// (chunk_trainer.hpp:131-186) on caller-provided parameters, flattened in ModelParams::visit
+// order (model.hpp:66-81). Test infrastructure: the GPU chunk loop is compared against it.
+struct RefModelCfg {
+    int n_layers, d_model, n_q_heads, n_kv_heads, head_dim, d_ff, vocab_size, chunk_size, page_size;
+    int retrieval_budget, local_window, score_scale;
+    int mode;  // 0 dense, 1 topk, 2 local (one mode for every layer)
+    double rope_base;
+    uint64_t seed;
+};
+
+}  // extern "C"
+
+namespace {
+ModelConfig to_model_cfg(const RefModelCfg& c) {
+    ModelConfig m;
+    m.n_layers = c.n_layers;
+    m.d_model = c.d_model;
+    m.n_q_heads = c.n_q_heads;
+    m.n_kv_heads = c.n_kv_heads;
+    m.head_dim = c.head_dim;
+    m.d_ff = c.d_ff;
+    m.vocab_size = c.vocab_size;
+    m.chunk_size = c.chunk_size;
+    m.page_size = c.page_size;
+    m.retrieval_budget = c.retrieval_budget;
+    m.local_window = c.local_window;
+    m.score_scale = c.score_scale != 0;
+    m.attention_mode = {c.mode == 0 ? AttentionMode::dense
+                                    : (c.mode == 1 ? AttentionMode::topk_sparse : AttentionMode::local)};
+    m.rope_base = c.rope_base;
+    m.seed = c.seed;
+    return m;
+}
+template <class Real>
+void flat_in(ModelParams<Real>& p, const void* src) {
+    const Real* s = static_cast<const Real*>(src);
+    p.visit([&](const char*, int, Tensor<Real>& t) {
+        std::memcpy(t.ptr(), s, t.bytes());
+        s += t.numel();
+    });
+}
+template <class Real>
+void flat_out(const ModelParams<Real>& p, void* dst) {
+    Real* d = static_cast<Real*>(dst);
+    p.visit([&](const char*, int, const Tensor<Real>& t) {
+        std::memcpy(d, t.ptr(), t.bytes());
+        d += t.numel();
+    });
+}
+template <class Real>
+void train_step_impl(const RefModelCfg* c, const void* params, const int32_t* tokens, int64_t n, void* grads,
+                     double* loss, int32_t* sel_counts) {
+    const ModelConfig cfg = to_model_cfg(*c);
+    ModelParams<Real> p = ModelParams<Real>::zeros_like_config(cfg);
+    flat_in(p, params);
+    ParamGrads<Real> g = ParamGrads<Real>::zeros_like_config(cfg);
+    ChunkTrainer<Real> tr(cfg);
+    const StepMetrics m = tr.train_step(p, std::span<const int32_t>(tokens, static_cast<size_t>(n)), g);
+    flat_out(g, grads);
+    *loss = m.loss;
+    if (sel_counts) {  // number of selected ids per (chunk, layer, query page), for the caller's checks
+        int64_t k = 0;
+        for (const auto& ch : tr.last_chunks())
+            for (const auto& per_layer : ch.selected)
+                for (const auto& ids : per_layer) sel_counts[k++] = static_cast<int32_t>(ids.size());
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int64_t ref_model_numel(const RefModelCfg* c) {
+    int64_t n = 0;
+    guarded([&] { n = ModelParams<double>::zeros_like_config(to_model_cfg(*c)).param_count(); });
+    return n;
+}
+
+// init_params (model.hpp:127-145) flattened in visit order.
+int ref_init_params(int real_bytes, const RefModelCfg* c, uint64_t seed, void* out) {
+    return guarded([&] {
+        if (real_bytes == 4) flat_out(init_params<float>(to_model_cfg(*c), seed), out);
+        else flat_out(init_params<double>(to_model_cfg(*c), seed), out);
+    });
+}
+
+int ref_train_step(int real_bytes, const RefModelCfg* c, const void* params, const int32_t* tokens, int64_t n,
+                   void* grads, double* loss, int32_t* sel_counts) {
+    return guarded([&] {
+        if (real_bytes == 4) train_step_impl<float>(c, params, tokens, n, grads, loss, sel_counts);
+        else train_step_impl<double>(c, params, tokens, n, grads, loss, sel_counts);
     });
 }
 

@@ -34,7 +34,10 @@ class Selection:
     def __del__(self):
         h = getattr(self, "handle", None)
         if h:
-            _lib.lib().oomb_selection_destroy(h)
+            try:
+                _lib.lib().oomb_selection_destroy(h)
+            except Exception:  # interpreter shutdown: module globals may be gone already
+                pass
             self.handle = None
 
     @classmethod

@@ -88,7 +88,10 @@ class PagedCache:
     def __del__(self):
         h = getattr(self, "handle", None)
         if h:
-            _lib.lib().oomb_pool_destroy(h)
+            try:
+                _lib.lib().oomb_pool_destroy(h)
+            except Exception:  # interpreter shutdown: module globals may be gone already
+                pass
             self.handle = None
 
     # ------------------------------------------------------------------ helpers
