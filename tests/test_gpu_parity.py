@@ -245,7 +245,7 @@ def test_scoring_and_selection_parity(geom, dtype):
     assert checked >= 1
 
 
-@pytest.mark.parametrize("n_pages,tokens", [(300, 512), (1000, 1024), (40, 256)])
+@pytest.mark.parametrize("n_pages,tokens", [(300, 512), (1000, 1024), (40, 256), (8300, 256)])  # 8300: long rows (65 candidate blocks)
 def test_tc_scorer_matches_exact_scorer(n_pages, tokens):
     """The tcgen05 two-pass scorer against the exact SIMT scorer on the same pool:
     votes within the bf16-operand tolerance, and identical top-k where margins allow."""
