@@ -611,3 +611,19 @@ def ref_train_step(mc, mode: str, params: np.ndarray, tokens: np.ndarray):
     if rc:
         raise OracleError(rc, L.ref_last_error().decode())
     return loss.value, grads, counts
+
+
+def ref_full_forward_backward(mc, params: np.ndarray, tokens: np.ndarray):
+    """full_forward_backward (oracle.hpp:89-276): the non-chunked ground truth -> (loss, flat grads)."""
+    L = _ref_model_lib()
+    c = ref_model_cfg(mc, "dense")
+    params = np.ascontiguousarray(params)
+    toks = np.ascontiguousarray(tokens, dtype=np.int32)
+    grads = np.zeros_like(params)
+    loss = C.c_double()
+    rc = L.ref_full_forward_backward(params.dtype.itemsize, C.byref(c), params.ctypes.data_as(C.c_void_p),
+                                     toks.ctypes.data_as(C.c_void_p), C.c_int64(len(toks)),
+                                     grads.ctypes.data_as(C.c_void_p), C.byref(loss))
+    if rc:
+        raise OracleError(rc, L.ref_last_error().decode())
+    return loss.value, grads

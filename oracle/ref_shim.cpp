@@ -659,6 +659,25 @@ int ref_init_params(int real_bytes, const RefModelCfg* c, uint64_t seed, void* o
     });
 }
 
+// full_forward_backward (oracle.hpp:89-276): the exact non-chunked model pass (monolithic causal
+// softmax), the reference's ground truth for the chunked trainer.
+int ref_full_forward_backward(int real_bytes, const RefModelCfg* c, const void* params, const int32_t* tokens,
+                              int64_t n, void* grads, double* loss) {
+    return guarded([&] {
+        const ModelConfig cfg = to_model_cfg(*c);
+        auto run = [&](auto zero) {
+            using Real = decltype(zero);
+            ModelParams<Real> p = ModelParams<Real>::zeros_like_config(cfg);
+            flat_in(p, params);
+            const auto r = full_forward_backward(cfg, p, std::span<const int32_t>(tokens, static_cast<size_t>(n)));
+            flat_out(r.grads, grads);
+            *loss = r.loss;
+        };
+        if (real_bytes == 4) run(float{});
+        else run(double{});
+    });
+}
+
 int ref_train_step(int real_bytes, const RefModelCfg* c, const void* params, const int32_t* tokens, int64_t n,
                    void* grads, double* loss, int32_t* sel_counts) {
     return guarded([&] {

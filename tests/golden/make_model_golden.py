@@ -6,7 +6,8 @@ unmodified reference headers compiled in place).
 
 Writes model_step.npz: the configuration, init_params(seed) flattened in ModelParams::visit
 order, a token window, and per attention mode (dense / topk / local) the f32 and f64 loss and
-parameter gradients plus the selected-page counts.
+parameter gradients plus the selected-page counts, and full_forward_backward (oracle.hpp:89-276,
+the exact non-chunked pass) in f64 as the ground truth of the dense step.
 """
 from __future__ import annotations
 
@@ -18,7 +19,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
-from oracle.oracle import ref_init_params, ref_train_step  # noqa: E402
+from oracle.oracle import ref_full_forward_backward, ref_init_params, ref_train_step  # noqa: E402
 from paper_2602_02108_b200.config import ModelConfig  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
@@ -47,6 +48,12 @@ def main():
         out[f"{mode}_sel_counts"] = cnt
         print(mode, "loss f32", l32, "f64", l64, "grad rel (f32 vs f64)",
               float(np.linalg.norm(g32 - g64) / np.linalg.norm(g64)))
+    # the exact non-chunked pass in f64: ground truth for the dense chunked step (acceptance criterion 1)
+    lf, gf = ref_full_forward_backward(model_cfg("dense"), params.astype(np.float64), tokens)
+    out["full_loss_f64"] = np.float64(lf)
+    out["full_grads_f64"] = gf.astype(np.float32)
+    print("full f64 loss", lf, "dense chunked f64 vs full f64 grad rel",
+          float(np.linalg.norm(out["dense_grads_f64"] - gf) / np.linalg.norm(gf)))
     np.savez_compressed(os.path.join(OUT, "model_step.npz"), **out)
 
 

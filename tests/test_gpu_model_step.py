@@ -36,6 +36,10 @@ def test_device_train_step_matches_reference(mode):
         n = int(np.prod(shape))
         assert rel(gflat[o:o + n], ref[o:o + n]) < 1e-4, (name, layer, rel(gflat[o:o + n], ref[o:o + n]))
         o += n
+    if mode == "dense":  # acceptance criterion 1: the chunked step equals the exact non-chunked pass
+        full = z["full_grads_f64"]  # full_forward_backward (oracle.hpp:89-276) in f64
+        assert rel(gflat, full) < 1e-5, rel(gflat, full)
+        assert abs(m.loss - float(z["full_loss_f64"])) < 1e-5 * float(z["full_loss_f64"])
     # same selections as the reference (selected-page counts per chunk / layer / query page)
     if mode == "topk":
         got = np.array([len(l) for ch in tr.chunks for s in ch.selected for l in s.lists()], np.int32)

@@ -22,6 +22,8 @@ def test_fixture_layout_matches_visit_order():
         # f32 reference vs f64 reference: the fixture's own precision floor
         g64 = z[f"{mode}_grads_f64"]
         assert np.linalg.norm(g - g64) / np.linalg.norm(g64) < 1e-5
+    # the reference's own chunked f64 step equals its exact non-chunked pass (test_chunk_trainer.cpp:54-90)
+    assert np.linalg.norm(z["dense_grads_f64"] - z["full_grads_f64"]) / np.linalg.norm(z["full_grads_f64"]) < 1e-6
     cnt = z["topk_sel_counts"].reshape(5, 2, 4)  # chunks x layers x query pages
     assert (cnt[0] == 0).all() and (cnt[1] == 2).all() and (cnt[4] == 2).all()  # k = 16 / 8 = 2 pages
 
