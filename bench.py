@@ -731,7 +731,8 @@ def main():
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if achieved else None, "peak_source": peak_src,
                 "algorithmic": "10*hd*Hq*pairs per chunk, pairs = P*P*sum|sel| + C(C+1)/2 (SURVEY 8d)",
-                "traffic": traffic}
+                "traffic": traffic["bytes_per_launch"] if traffic else None,
+                "traffic_source": traffic["source"] if traffic else None}
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if args.shard == "kv" else "weak",
@@ -744,8 +745,8 @@ def main():
             "pct_bf16_peak": tflops / peak, "pct_bf16_peak_sustained": tflops / peak_sus,
             "algorithmic_tflops": tflops,
             "model_equiv_tokens_per_s": value / (32 if cfg["Hq"] == 32 else 28),
-            "roofline": roofline, "kernels": kernels, "gpu_launches": launches // args.steps,
-            "gpu_launches_timed_region": launches, "clocks": clk, "e2e": e2e, "offload": offload,
+            "roofline": roofline, "kernels": kernels, "gpu_launches": launches,
+            "gpu_launches_per_step": launches // args.steps, "clocks": clk, "e2e": e2e, "offload": offload,
             "train_step_variant": {
                 "what": "full train step of SURVEY 3.2: 2 forwards (phase A + recompute) + 1 backward per chunk; "
                         "the recompute forward is charged as a whole forward pass (fwd_phase, selection and append "
