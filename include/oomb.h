@@ -224,6 +224,12 @@ OOMB_API int oomb_set_kernel_policy(oomb_pool_t pool, int policy);
  * dv, reference layout [n*P][Hkv][hd] fp32 device; pages without gradients add 0. */
 OOMB_API int oomb_accumulate_grad_pages(oomb_pool_t pool, int layer, const int32_t* ids_host, int n, float* dk,
                                         float* dv, void* stream);
+/* The reverse projection epilogue (chunk_trainer.hpp:575-592): the dM_i read-back
+ * followed by rope_backward of dK (ops.hpp:227-230) in one pass: dk <- rope^-1(dk + grad_k),
+ * dv <- dv + grad_v, row r at absolute position pos_offset + r. Bitwise equal to
+ * oomb_accumulate_grad_pages followed by oomb_rope(sign -1) on dk. */
+OOMB_API int oomb_accumulate_grad_pages_rope(oomb_pool_t pool, int layer, const int32_t* ids_host, int n, float* dk,
+                                             float* dv, int64_t pos_offset, float rope_base, void* stream);
 
 /* ---- kernel timing evidence ---------------------------------------------
  * When enabled, every kernel the pool launches is bracketed by CUDA events on its

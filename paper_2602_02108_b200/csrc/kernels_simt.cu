@@ -284,13 +284,54 @@ __global__ void accumulate_grads_kernel(const int32_t* __restrict__ ids, int n, 
     }
 }
 
+// The reverse projection epilogue (chunk_trainer.hpp:575-592): dM_i read-back
+// then rope_backward of dK in one pass: dk <- rope^-1(dk + grad_k(own pages)), dv += grad_v. One
+// rotation pair per thread, the same fp32 operations in the same order as the two separate steps.
+__global__ void accumulate_grads_rope_kernel(const int32_t* __restrict__ ids, int n, const int32_t* __restrict__ gslot,
+                                             const float* __restrict__ gk, const float* __restrict__ gv,
+                                             int64_t filled, int P, int Hkv, int hd, int64_t pos0,
+                                             const double* __restrict__ inv_freq, float* __restrict__ dk,
+                                             float* __restrict__ dv) {
+    const int re = Hkv * hd;
+    const int64_t pairs = static_cast<int64_t>(n) * P * re / 2;
+    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < pairs;
+         q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t idx = q * 2;
+        const int i = static_cast<int>(idx / (static_cast<int64_t>(P) * re));
+        const int rem = static_cast<int>(idx - static_cast<int64_t>(i) * P * re);
+        const int s = rem / re, e = rem - (rem / re) * re;
+        const int h = e / hd, d = e - (e / hd) * hd;
+        const int pid = ids[i];
+        const int g = gslot[pid];
+        float k2[2] = {dk[idx], dk[idx + 1]};
+        if (g >= 0 && s < valid_in_page(filled, pid, P)) {
+            const size_t src = ((static_cast<size_t>(g) * Hkv + h) * P + s) * hd + d;
+            k2[0] += gk[src];
+            k2[1] += gk[src + 1];
+            dv[idx] += gv[src];
+            dv[idx + 1] += gv[src + 1];
+        }
+        // rope_elem (ops.hpp:192-225) at position -(pos0 + row): angle and trig in double, rotation in fp32
+        const double ang = -static_cast<double>(pos0 + static_cast<int64_t>(i) * P + s) * inv_freq[d >> 1];
+        const float c = static_cast<float>(cos(ang)), sn = static_cast<float>(sin(ang));
+        dk[idx] = __fsub_rn(__fmul_rn(k2[0], c), __fmul_rn(k2[1], sn));
+        dk[idx + 1] = __fadd_rn(__fmul_rn(k2[0], sn), __fmul_rn(k2[1], c));
+    }
+}
+
 void launch_accumulate_grads(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, const float* gk,
                              const float* gv, int64_t filled, int P, int Hkv, int hd, float* dk, float* dv,
-                             cudaStream_t st) {
+                             cudaStream_t st, int64_t rope_pos0, const double* rope_inv_freq) {
     if (n <= 0) return;
     ProfScope prof_(PK_GATHER, st);
     const int64_t total = static_cast<int64_t>(n) * P * Hkv * hd;
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+    if (rope_inv_freq) {
+        accumulate_grads_rope_kernel<<<blocks, 256, 0, st>>>(d_ids, n, d_gslot_layer, gk, gv, filled, P, Hkv, hd,
+                                                             rope_pos0, rope_inv_freq, dk, dv);
+        check_launch("accumulate_grads_rope_kernel");
+        return;
+    }
     accumulate_grads_kernel<<<blocks, 256, 0, st>>>(d_ids, n, d_gslot_layer, gk, gv, filled, P, Hkv, hd, dk, dv);
     check_launch("accumulate_grads_kernel");
 }

@@ -930,6 +930,21 @@ int oomb_accumulate_grad_pages(oomb_pool_t p, int layer, const int32_t* ids, int
     });
 }
 
+int oomb_accumulate_grad_pages_rope(oomb_pool_t p, int layer, const int32_t* ids, int n, float* dk, float* dv,
+                                    int64_t pos_offset, float rope_base, void* stream) {
+    return guard([&] {
+        set_dev(p);
+        p->pt->check_ids(layer, ids, n, p->enforce, "gather_grad_pages");
+        OOMB_REQUIRE(rope_base > 1.f, OOMB_CONFIG_ERROR, "rope_base must be > 1");
+        if (n == 0) return;
+        int32_t* d = upload_ids(ids, n, S(stream));
+        launch_accumulate_grads(d, n, p->gslot_layer(layer), p->gkpool, p->gvpool, p->pt->filled[layer],
+                                p->cfg.page_size, p->cfg.n_kv_heads, p->cfg.head_dim, dk, dv, S(stream), pos_offset,
+                                rope_inv_freq_table(rope_base, p->cfg.head_dim));
+        OOMB_CUDA(cudaFreeAsync(d, S(stream)));
+    });
+}
+
 int oomb_profile_enable(oomb_pool_t p, int on) {
     return guard([&] { p->prof_on = on != 0; });
 }

@@ -167,7 +167,8 @@ void launch_scatter(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, f
                     cudaStream_t st);
 void launch_accumulate_grads(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, const float* gk,
                              const float* gv, int64_t filled, int P, int Hkv, int hd, float* dk, float* dv,
-                             cudaStream_t st);
+                             cudaStream_t st, int64_t rope_pos0 = 0,
+                             const double* rope_inv_freq = nullptr);
 void launch_grad_init(const int32_t* d_pages, const int32_t* d_slots, int n, int32_t* d_gslot_layer, float* gk,
                       float* gv, int64_t page_elems, cudaStream_t st);
 void launch_zero_slots(const int32_t* d_slots, int n, float* gk, float* gv, int64_t page_elems, cudaStream_t st);

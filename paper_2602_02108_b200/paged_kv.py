@@ -249,6 +249,16 @@ class PagedCache:
         call("oomb_accumulate_grad_pages", self.handle, layer, ids.ctypes.data_as(C.c_void_p), len(ids), _ptr(dk),
              _ptr(dv), stream_handle(stream))
 
+    def accumulate_grad_pages_rope(self, layer: int, page_ids, dk: torch.Tensor, dv: torch.Tensor, pos_offset: int,
+                                   rope_base: float = 10000.0, stream=None) -> None:
+        """The dM_i read-back fused with rope_backward of dK (chunk_trainer.hpp:575-592):
+        dk <- rope^-1(dk + grad_k(ids)), dv += grad_v(ids); row r at position pos_offset + r."""
+        ids = self._ids(page_ids)
+        if dk.dtype != torch.float32 or not dk.is_cuda or not dk.is_contiguous() or dk.shape != dv.shape:
+            raise ShapeError("accumulate_grad_pages_rope: fp32 contiguous CUDA dk/dv of equal shape required")
+        call("oomb_accumulate_grad_pages_rope", self.handle, layer, ids.ctypes.data_as(C.c_void_p), len(ids),
+             _ptr(dk), _ptr(dv), int(pos_offset), C.c_float(rope_base), stream_handle(stream))
+
     PROFILE_KINDS = ("append", "score", "topk", "attn_fwd", "bwd_prep", "bwd_dq", "bwd_dkdv", "bwd_simt",
                      "grad_init", "gather_scatter", "other", "bwd_pair")
 

@@ -216,10 +216,11 @@ class ChunkTrainer:
             dattn = linear_backward(la["attn_flat"], lp["wo"], dh2, lg["wo"])
             dout = dattn.view(C, hq, hd).to(self.dtype).contiguous()
             ag = A.attn_backward(cfg, dout, la["q"], self.cache, l, la["k"], la["v"], la["saved"])
-            # dM_i: what later chunks deposited into this chunk's own pages joins dK / dV
-            self.cache.accumulate_grad_pages(l, own, ag.dk_cur, ag.dv_cur)
+            # dM_i: what later chunks deposited into this chunk's own pages joins dK / dV, and dK is
+            # rotated back in the same pass (the reverse projection epilogue)
+            self.cache.accumulate_grad_pages_rope(l, own, ag.dk_cur, ag.dv_cur, chunk.pos_offset, cfg.rope_base)
             dq_pre = A.rope(ag.dq, chunk.pos_offset, cfg.rope_base, sign=-1).view(C, hq * hd)
-            dk_pre = A.rope(ag.dk_cur, chunk.pos_offset, cfg.rope_base, sign=-1).view(C, hk * hd)
+            dk_pre = ag.dk_cur.view(C, hk * hd)
             da = linear_backward(la["a"], lp["wq"], dq_pre, lg["wq"])
             da = da + linear_backward(la["a"], lp["wk"], dk_pre, lg["wk"])
             da = da + linear_backward(la["a"], lp["wv"], ag.dv_cur.view(C, hk * hd), lg["wv"])

@@ -58,7 +58,9 @@ def test_gradient_pages_carry_the_cross_chunk_gradient():
     p = unflatten(z["params"], cfg, tr.dev)
     _, g_full = tr.train_step(p, z["tokens"])
     full = flatten(g_full, cfg).cpu().numpy()
-    tr.cache.accumulate_grad_pages = lambda *a, **k: None  # sever dM_i
+    from paper_2602_02108_b200.attention import rope
+    tr.cache.accumulate_grad_pages_rope = (  # sever dM_i: only the inverse rotation of dK is left
+        lambda layer, ids, dk, dv, pos, base: dk.copy_(rope(dk, pos, base, sign=-1)))
     _, g_cut = tr.train_step(p, z["tokens"])
     cut = flatten(g_cut, cfg).cpu().numpy()
     assert rel(cut, full) > 1e-3

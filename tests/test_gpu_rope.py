@@ -58,3 +58,30 @@ def test_fused_rope_append_equals_rope_then_append(dtype):
     a, b = fused.gather_pages(0, ids), split.gather_pages(0, ids)
     assert torch.equal(a.k, b.k) and torch.equal(a.v, b.v)
     assert torch.equal(fused.page_mean_keys(0), split.page_mean_keys(0))
+
+
+@pytest.mark.parametrize("pos", [4096, 1 << 20])
+def test_reverse_epilogue_equals_readback_then_rope_backward(pos):
+    """oomb_accumulate_grad_pages_rope == accumulate_grad_pages followed by rope(sign -1) on dK,
+    bitwise (chunk_trainer.hpp:575-592 in one pass)."""
+    from paper_2602_02108_b200 import ModelConfig, PagedCache
+    from paper_2602_02108_b200.attention import rope
+    cfg = ModelConfig(n_layers=1, n_q_heads=8, n_kv_heads=2, head_dim=128, chunk_size=256, page_size=128,
+                      retrieval_budget=256)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    cache = PagedCache(cfg, dtype="bf16", max_tokens=1024)
+    kv = torch.randn(512, 2, 128, device="cuda", generator=g).bfloat16()
+    cache.append_chunk(0, kv, kv)
+    n = 512 // 128
+    dk_pages = torch.randn(n * 128, 2, 128, device="cuda", generator=g)
+    cache.scatter_add_grads(0, list(range(n)), dk_pages, 2 * dk_pages)  # grads of the "own" pages
+    own = [2, 3]
+    dk = torch.randn(256, 2, 128, device="cuda", generator=g)
+    dv = torch.randn(256, 2, 128, device="cuda", generator=g)
+    a_k, a_v = dk.clone(), dv.clone()
+    cache.accumulate_grad_pages(0, own, a_k, a_v)
+    a_k = rope(a_k, pos, 10000.0, sign=-1)
+    b_k, b_v = dk.clone(), dv.clone()
+    cache.accumulate_grad_pages_rope(0, own, b_k, b_v, pos, 10000.0)
+    torch.cuda.synchronize()
+    assert torch.equal(a_k, b_k) and torch.equal(a_v, b_v)
