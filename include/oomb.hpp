@@ -395,6 +395,13 @@ public:
         check(oomb_accumulate_grad_pages(pool_, layer, ids.data(), static_cast<int>(ids.size()), dk.as<float>(),
                                          dv.as<float>(), sv(st)));
     }
+    // The same read-back fused with rope_backward of dK (chunk_trainer.hpp:575-592): row r of dk is
+    // rotated back from absolute position pos_offset + r.
+    void accumulate_grad_pages_rope(int layer, std::span<const int32_t> ids, DeviceTensor& dk, DeviceTensor& dv,
+                                    int64_t pos_offset, float rope_base, cudaStream_t st = nullptr) {
+        check(oomb_accumulate_grad_pages_rope(pool_, layer, ids.data(), static_cast<int>(ids.size()), dk.as<float>(),
+                                              dv.as<float>(), pos_offset, rope_base, sv(st)));
+    }
     // paged_kv.hpp:170-183: [n][Hkv][hd] fp32.
     DeviceTensor page_mean_keys(int layer, int n_candidates = -1, cudaStream_t st = nullptr) const {
         const int n = n_candidates < 0 ? n_pages(layer) : std::min(n_candidates, n_pages(layer));
