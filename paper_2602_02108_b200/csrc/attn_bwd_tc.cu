@@ -846,7 +846,6 @@ __global__ void __launch_bounds__(384, 1)
 
 }  // namespace
 
-int g_num_sms = 148;
 
 bool tc_bwd_available() { return true; }
 
@@ -863,15 +862,13 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
                         cudaStream_t st, cudaStream_t side, cudaEvent_t ev_prep, cudaEvent_t ev_dq, bool join_dq) {
     OOMB_REQUIRE(workspace_bytes >= attn_bwd_tc_workspace(g, nnz), OOMB_ERROR, "bwd workspace too small");
     OOMB_REQUIRE(g.m <= 64, OOMB_CONFIG_ERROR, "tcgen05 backward supports at most 64 query pages per chunk");
-    static bool attr = false;
-    if (!attr) {
+    if (first_use_on_device(2)) {
         OOMB_CUDA(cudaFuncSetAttribute(attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDqSmem));
         OOMB_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kKvSmem));
-        int dev = 0;
-        OOMB_CUDA(cudaGetDevice(&dev));
-        OOMB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-        attr = true;
     }
+    int dev = 0, num_sms = 148;
+    OOMB_CUDA(cudaGetDevice(&dev));
+    OOMB_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
     BwdWs w = carve(g, workspace);
     ProfScope* prep_scope = new ProfScope(PK_BWD_PREP, st);
     const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
@@ -919,7 +916,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
             OOMB_CUDA(cudaMemsetAsync(dv_cur, 0, static_cast<size_t>(g.C) * g.Hkv * kHd * sizeof(float), st));
         }
         const int units = ((g.chunk_keys ? g.C / kTile : 0) + max_union * (g.P / kTile)) * g.Hkv;
-        const int n_ctas = std::max(1, std::min(units, g_num_sms));
+        const int n_ctas = std::max(1, std::min(units, num_sms));
         const CUtensorMap tdkc = map_rows_heads_f32(dk_cur, g.C, g.Hkv, kHd);
         const CUtensorMap tdvc = map_rows_heads_f32(dv_cur, g.C, g.Hkv, kHd);
         attn_bwd_dkdv_kernel<<<n_ctas, 384, kKvSmem, st>>>(tq, tdo, tkc, tvc, maps.kpool, maps.vpool, maps.gkpool,

@@ -302,11 +302,8 @@ __global__ void __launch_bounds__(384, 1)
 void launch_attn_fwd_tc4(const AttnGeom& g, const TcPoolMaps& maps, const void* q, const int32_t* sel_off,
                          const int32_t* sel_ids, const int32_t* d_kvslot_layer, const void* k_cur, const void* v_cur,
                          void* out, float* lse, int* d_err, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    if (first_use_on_device(1))
         OOMB_CUDA(cudaFuncSetAttribute(attn_fwd_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kF4Smem));
-        attr = true;
-    }
     const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, kHd);
     const CUtensorMap tkc = map_rows_heads(k_cur, g.C, g.Hkv, kHd);
     const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, kHd);

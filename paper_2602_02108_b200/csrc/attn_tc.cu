@@ -155,11 +155,8 @@ __global__ void __launch_bounds__(128, 1)
 
 void launch_debug_tc_gemm(int mode, const void* a, const void* b, float* c, int m, int n, int k, cudaStream_t st) {
     OOMB_REQUIRE(k <= 128 && mode >= 0 && mode <= 4, OOMB_SHAPE_ERROR, "debug gemm: K <= 128, mode 0..4");
-    static bool attr_set = false;
-    if (!attr_set) {
+    if (first_use_on_device(4))
         OOMB_CUDA(cudaFuncSetAttribute(debug_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDbgSmem));
-        attr_set = true;
-    }
     CUtensorMap ta, tb;
     {
         const uint64_t dims[2] = {static_cast<uint64_t>(k), static_cast<uint64_t>(m)};

@@ -10,6 +10,9 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -17,6 +20,17 @@
 #include "oomb.h"
 
 namespace oomb {
+
+// Per-device one-time setup (kernel attributes apply to the current device's context): true the
+// first time `key` is seen on the current device.
+inline bool first_use_on_device(int key) {
+    static std::mutex mu;
+    static std::set<std::pair<int, int>> seen;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return true;
+    std::lock_guard<std::mutex> lock(mu);
+    return seen.insert({dev, key}).second;
+}
 
 struct Error : std::runtime_error {
     int code;

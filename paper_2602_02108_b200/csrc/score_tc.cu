@@ -404,11 +404,9 @@ void launch_vote_reduce(const float* part, int groups, int64_t mn, float* vote, 
 void launch_score_tc(const void* q, int64_t tokens, int Hq, int Hkv, int P, const float* kavg_sum,
                      const int32_t* kavg_cnt, const float* kavg_f32, int64_t n, float scale, float* vote,
                      void* ws, cudaStream_t st, bool partial_only) {
-    static bool attr = false;
-    if (!attr) {
+    if (first_use_on_device(3)) {
         OOMB_CUDA(cudaFuncSetAttribute(score_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStSmem));
         OOMB_CUDA(cudaFuncSetAttribute(score_vote_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kVoSmem));
-        attr = true;
     }
     ProfScope prof_(PK_SCORE, st);
     const int n_pad = static_cast<int>((n + kTile - 1) / kTile * kTile);
