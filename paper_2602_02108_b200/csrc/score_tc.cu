@@ -28,7 +28,10 @@ using namespace tc;
 
 namespace {
 
-constexpr int kQpGroup = 8;  // query pages per vote CTA
+#ifndef OOMB_VOTE_QPG
+#define OOMB_VOTE_QPG 8
+#endif
+constexpr int kQpGroup = OOMB_VOTE_QPG;  // query pages per vote CTA (4 / 16 measured no better at c3)
 #ifndef OOMB_SCORE_POLY
 #define OOMB_SCORE_POLY 4
 #endif
