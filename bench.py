@@ -662,7 +662,8 @@ def main():
                "h2d_bytes_per_step": ee.h2d_bytes, "d2h_bytes_per_step": ee.d2h_bytes}
 
     offload = None
-    if args.offload_cap and 0 < args.offload_cap < 1 and cfg["mode"] == "topk":
+    # the offload regime is a one-GPU measurement (wall clock, pinned host tier per process)
+    if args.offload_cap and 0 < args.offload_cap < 1 and cfg["mode"] == "topk" and world == 1:
         try:
             offload = offload_measure(run, args.offload_cap)
         except Exception as ex:  # the offload measurement never blocks the line
@@ -756,7 +757,7 @@ def main():
                         "the recompute forward is the same forward kernel, timed above",
                 "tokens_per_s": world * cfg["T"] / ((ms_step + t_fwd) / 1e3),
                 "ms_per_step": ms_step + t_fwd}}
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:  # rank 0 at N = 1 only (the reference arm covers every N)
         try:
             line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_workers)
         except Exception as ex:  # the baseline never blocks the measurement line
