@@ -547,6 +547,30 @@ int ref_tier_log(void* h, RefEvent* out) {
 }
 
 // validate_schedule  tiered_memory.cpp:47-138 over an externally built log
+// dump_schedule_jsonl (tiered_memory.cpp:28-45) of an event list into a caller buffer.
+int ref_dump_schedule_jsonl(const RefEvent* ev, int64_t n, double bandwidth, char* out, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        ScheduleLog log;
+        log.bandwidth_bytes_per_s = bandwidth;
+        for (int64_t i = 0; i < n; ++i) {
+            ScheduleEvent e;
+            e.kind = static_cast<EventKind>(ev[i].kind);
+            e.t = ev[i].t;
+            e.layer = ev[i].layer;
+            e.page = ev[i].page;
+            e.chunk = ev[i].chunk;
+            e.bytes = ev[i].bytes;
+            e.phase = static_cast<Phase>(ev[i].phase);
+            log.events.push_back(e);
+        }
+        std::ostringstream os;
+        dump_schedule_jsonl(log, os);
+        const std::string str = os.str();
+        *len = static_cast<int64_t>(str.size());
+        if (out && cap > 0) std::memcpy(out, str.data(), static_cast<size_t>(std::min<int64_t>(cap, *len)));
+    });
+}
+
 int ref_validate_schedule(const RefEvent* ev, int64_t n, double bandwidth, double* out, int* n_violations) {
     return guarded([&] {
         ScheduleLog log;

@@ -326,3 +326,40 @@ def test_reports_in_reference_formats():
     buf = io.StringIO()
     emit_retrieval_csv(buf, 7, [(0, [[[], []], [[], []]]), (1, [[[0, 1], [1]], [[0], []]])])
     assert buf.getvalue() == "7,1,0,2,0\n7,1,0,2,1\n7,1,0,3,1\n7,1,1,2,0\n"
+
+
+def test_schedule_jsonl_matches_reference_dump():
+    """dump_schedule_jsonl (tiered_memory.cpp:28-45) of a simulated engine log, byte for byte the
+    reference's own dump of the same events (when the reference shim is built)."""
+    import ctypes as C
+    import io
+    from oracle.oracle import Ref, build_ref
+    from paper_2602_02108_b200.reports import dump_schedule_jsonl
+    from paper_2602_02108_b200.tiered_memory import HostPageTable, TierConfig, TieredEngine
+    pt = HostPageTable(n_layers=1, page_size=4, n_kv_heads=1, head_dim=2)
+    eng = TieredEngine(pt, TierConfig(device_capacity_pages=5, bandwidth_bytes_per_s=1e6))
+    for chunk in range(4):
+        b, e = pt.append_chunk(0, 8)
+        eng.on_pages_appended(0, (b, e))
+        ids = list(range(max(0, pt.n_pages(0) - 4), pt.n_pages(0) - 2))
+        if ids:
+            eng.wait(eng.fetch_async(0, ids, chunk))
+            eng.record_access(0, ids, chunk)
+        eng.advance_compute(1e-4, chunk, 0)
+        eng.end_layer_use(0, list(range(pt.n_pages(0))))
+    buf = io.StringIO()
+    dump_schedule_jsonl(eng.log(), buf)
+    lines = buf.getvalue().splitlines()
+    assert lines[0] == '{"bandwidth_bytes_per_s":1000000.0}' and len(lines) == len(eng.raw_log()) + 1
+    if not Ref.available():
+        pytest.skip("reference shim not built (oracle/_ref)")
+    raw = eng.raw_log()
+    L = C.CDLL(build_ref())
+    arr = (type(raw[0]) * len(raw))(*raw)
+    n = C.c_int64()
+    assert L.ref_dump_schedule_jsonl(arr, len(raw), C.c_double(1e6), None, 0, C.byref(n)) == 0
+    out = C.create_string_buffer(n.value)
+    assert L.ref_dump_schedule_jsonl(arr, len(raw), C.c_double(1e6), out, n.value, C.byref(n)) == 0
+    ref = out.raw[: n.value].decode()
+    # nlohmann writes the header's double as 1000000.0 too; compare every line exactly
+    assert buf.getvalue() == ref, (buf.getvalue()[:300], ref[:300])
