@@ -23,6 +23,10 @@
 
 namespace oomb {
 
+#ifndef OOMB_BWD_KV_FIRST
+#define OOMB_BWD_KV_FIRST 0  // launch order of the pair (both orders measured equal at c3)
+#endif
+
 using namespace tc;
 
 namespace {
@@ -900,15 +904,15 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     ProfScope* pair_scope = join_dq ? new ProfScope(PK_BWD_PAIR, st) : nullptr;
     OOMB_CUDA(cudaEventRecord(ev_prep, st));
     OOMB_CUDA(cudaStreamWaitEvent(side, ev_prep, 0));
-    {
+    auto launch_dq = [&] {
         ProfScope s_(PK_BWD_DQ, side);
         const CUtensorMap tdq = map_rows_heads_f32(dq, g.C, g.Hq, kHd);
         attn_bwd_dq_kernel<<<dim3(g.Hq, g.C / kTile), 384, kDqSmem, side>>>(tq, tdo, tkc, tvc, maps.kpool,
                                                                             maps.vpool, tdq, p);
         check_launch("attn_bwd_dq_kernel");
-    }
-    OOMB_CUDA(cudaEventRecord(ev_dq, side));
-    {
+        OOMB_CUDA(cudaEventRecord(ev_dq, side));
+    };
+    auto launch_dkdv = [&] {
         ProfScope s_(PK_BWD_DKDV, st);
         const int max_union = std::min(nnz, n_pages);
         if (!g.chunk_keys) {  // past-only shard: the chunk's own keys are another shard's
@@ -922,6 +926,15 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         attn_bwd_dkdv_kernel<<<n_ctas, 384, kKvSmem, st>>>(tq, tdo, tkc, tvc, maps.kpool, maps.vpool, maps.gkpool,
                                                             maps.gvpool, tdkc, tdvc, p, w.n_uni + 1);
         check_launch("attn_bwd_dkdv_kernel");
+    };
+    if (OOMB_BWD_KV_FIRST) {
+        launch_dkdv();
+        launch_dq();
+    } else {
+        launch_dq();
+        launch_dkdv();
+    }
+    {
         if (join_dq) OOMB_CUDA(cudaStreamWaitEvent(st, ev_dq, 0));
         delete pair_scope;
 
