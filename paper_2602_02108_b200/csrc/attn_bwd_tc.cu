@@ -137,7 +137,10 @@ __global__ void __launch_bounds__(1024) bwd_union_kernel(const uint64_t* __restr
 // goes to dP columns [256+64w, 256+64w+32) (its own region: the other group may still be
 // reading its dP columns).
 // ===========================================================================
-constexpr int kDqKSt = 3, kDqVSt = 2;
+#ifndef OOMB_DQ_KST
+#define OOMB_DQ_KST 3
+#endif
+constexpr int kDqKSt = OOMB_DQ_KST, kDqVSt = 5 - OOMB_DQ_KST;  // K / V stages (3 / 2 kept: 2 / 3 measured 6 % slower)
 constexpr int kDqQ = 0;
 constexpr int kDqDO = kDqQ + kTileBytes;
 constexpr int kDqK = kDqDO + kTileBytes;            // kDqKSt stages

@@ -26,7 +26,10 @@ using namespace tc;
 
 namespace {
 
-constexpr int kKSt = 3, kVSt = 2;
+#ifndef OOMB_FWD4_KST
+#define OOMB_FWD4_KST 3
+#endif
+constexpr int kKSt = OOMB_FWD4_KST, kVSt = 5 - OOMB_FWD4_KST;  // K / V stages (3 / 2 and 2 / 3 measured equal)
 constexpr int kF4Q = 0;
 constexpr int kF4K = kF4Q + kTileBytes;
 constexpr int kF4V = kF4K + kKSt * kTileBytes;
