@@ -627,3 +627,32 @@ def ref_full_forward_backward(mc, params: np.ndarray, tokens: np.ndarray):
     if rc:
         raise OracleError(rc, L.ref_last_error().decode())
     return loss.value, grads
+
+
+class RefTierCfgC(C.Structure):
+    _fields_ = [("device_capacity_pages", C.c_int64), ("bandwidth_bytes_per_s", C.c_double),
+                ("fixed_s_per_layer", C.c_double), ("s_per_attended_token", C.c_double)]
+
+
+def ref_train_step_offload(mc, mode: str, params: np.ndarray, tokens: np.ndarray, capacity: int,
+                           bandwidth: float = 16e9, fixed_s: float = 1e-3, s_per_token: float = 1e-6):
+    """ChunkTrainer::train_step with enable_offload (chunk_trainer.hpp:118-186) -> (loss, flat grads,
+    ScheduleLog events as an int64 array [n, 6] of (kind, layer, page, chunk, phase, bytes) plus times)."""
+    L = _ref_model_lib()
+    c = ref_model_cfg(mc, mode)
+    tc = RefTierCfgC(capacity, bandwidth, fixed_s, s_per_token)
+    params = np.ascontiguousarray(params)
+    toks = np.ascontiguousarray(tokens, dtype=np.int32)
+    grads = np.zeros_like(params)
+    loss = C.c_double()
+    cap = 1 << 16
+    evs = (RefEvent * cap)()
+    n = C.c_int64()
+    rc = L.ref_train_step_offload(params.dtype.itemsize, C.byref(c), params.ctypes.data_as(C.c_void_p),
+                                  toks.ctypes.data_as(C.c_void_p), C.c_int64(len(toks)), C.byref(tc),
+                                  grads.ctypes.data_as(C.c_void_p), C.byref(loss), evs, C.c_int64(cap), C.byref(n))
+    if rc:
+        raise OracleError(rc, L.ref_last_error().decode())
+    ev = np.array([(e.kind, e.layer, e.page, e.chunk, e.phase, e.bytes) for e in evs[: n.value]], np.int64)
+    t = np.array([e.t for e in evs[: n.value]])
+    return loss.value, grads, ev, t

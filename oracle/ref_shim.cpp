@@ -702,6 +702,41 @@ int ref_full_forward_backward(int real_bytes, const RefModelCfg* c, const void* 
     });
 }
 
+// ChunkTrainer::train_step with enable_offload(tier) (chunk_trainer.hpp:118-186): gradients, loss and
+// the step's ScheduleLog (last_schedule()) as RefEvent records; *n_events = log size.
+int ref_train_step_offload(int real_bytes, const RefModelCfg* c, const void* params, const int32_t* tokens, int64_t n,
+                           const RefTierCfg* tc, void* grads, double* loss, RefEvent* events, int64_t cap,
+                           int64_t* n_events) {
+    return guarded([&] {
+        const ModelConfig cfg = to_model_cfg(*c);
+        TierConfig tier;
+        tier.device_capacity_pages = tc->device_capacity_pages;
+        tier.bandwidth_bytes_per_s = tc->bandwidth_bytes_per_s;
+        tier.compute.fixed_s_per_layer = tc->fixed_s_per_layer;
+        tier.compute.s_per_attended_token = tc->s_per_attended_token;
+        auto run = [&](auto zero) {
+            using Real = decltype(zero);
+            ModelParams<Real> p = ModelParams<Real>::zeros_like_config(cfg);
+            flat_in(p, params);
+            ParamGrads<Real> g = ParamGrads<Real>::zeros_like_config(cfg);
+            ChunkTrainer<Real> tr(cfg);
+            tr.enable_offload(tier);
+            const StepMetrics m = tr.train_step(p, std::span<const int32_t>(tokens, static_cast<size_t>(n)), g);
+            flat_out(g, grads);
+            *loss = m.loss;
+            const ScheduleLog* log = tr.last_schedule();
+            *n_events = log ? static_cast<int64_t>(log->events.size()) : 0;
+            for (int64_t i = 0; log && i < std::min(cap, *n_events); ++i) {
+                const auto& e = log->events[static_cast<size_t>(i)];
+                events[i] = RefEvent{static_cast<int32_t>(e.kind), e.layer, e.page, e.chunk,
+                                     static_cast<int32_t>(e.phase), 0, e.bytes, e.t};
+            }
+        };
+        if (real_bytes == 4) run(float{});
+        else run(double{});
+    });
+}
+
 int ref_train_step(int real_bytes, const RefModelCfg* c, const void* params, const int32_t* tokens, int64_t n,
                    void* grads, double* loss, int32_t* sel_counts) {
     return guarded([&] {

@@ -472,6 +472,9 @@ struct oomb_tier_s {
         // the pages of this transfer are not eviction candidates either way (still host-tier, or
         // already resident and reserved), so one enforcement for all of them evicts the same pages
         // in the same order.
+        // Only the pages still host-tier at entry land here: a page of this transfer that is already
+        // resident (it landed via another handle) is skipped, as in the reference, even if the
+        // enforcement below evicts it (the reference checks it before any of its evictions).
         std::set<int32_t> coming;
         for (int32_t p : tr.pages)
             if (tier(tr.layer, p) != 0) coming.insert(p);
@@ -479,7 +482,7 @@ struct oomb_tier_s {
         if (incoming > 0) enforce_capacity(incoming);
         for (int32_t p : tr.pages) {
             PageState& ps = state(tr.layer, p);
-            if (tier(tr.layer, p) == 0) continue;
+            if (!coming.erase(p)) continue;
             set_tier(tr.layer, p, 0);
             ps.in_flight_done = 0;
             ps.reserved = true;

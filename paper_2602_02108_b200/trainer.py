@@ -24,6 +24,7 @@ from . import attention as A
 from .config import ModelConfig
 from .errors import StateError
 from .paged_kv import PagedCache
+from .tiered_memory import BACKWARD, FORWARD, ComputeCostModel, TierConfig, TieredEngine
 
 RMS_EPS = 1e-6        # kRmsNormEps, chunk_trainer.hpp:31
 IGNORE_TARGET = -1    # kIgnoreTarget, ops.hpp:268
@@ -123,15 +124,66 @@ class StepMetrics:
 
 
 class ChunkTrainer:
-    """Device counterpart of chunktrain::ChunkTrainer<float> for one sequence (no offload)."""
+    """Device counterpart of chunktrain::ChunkTrainer<float> for one sequence. With a TierConfig
+    (enable_offload, chunk_trainer.hpp:118-124) every step runs the reference's residency protocol
+    on a TieredEngine: lookahead prefetch, ensure_resident_, end_layer_use, grads-scattered marks and
+    the cost-model clock (chunk_trainer.hpp:318-363, 388-462, 531-541), with real page moves."""
 
-    def __init__(self, cfg: ModelConfig, max_tokens: int, dtype: str = "fp32"):
+    def __init__(self, cfg: ModelConfig, max_tokens: int, dtype: str = "fp32", tier: TierConfig | None = None):
         cfg.validate()
         self.cfg = cfg
         self.cache = PagedCache(cfg, dtype=dtype, max_tokens=max_tokens)
         self.dev = self.cache.device
         self.dtype = self.cache.dtype
         self.chunks: list[ChunkState] = []
+        self.tier = tier
+        self.engine: TieredEngine | None = None
+        self.pending = None
+        self.last_log = None  # raw ScheduleLog events of the last offloaded step
+
+    def enable_offload(self, tier: TierConfig) -> None:
+        self.tier = tier
+
+    def disable_offload(self) -> None:
+        self.tier = None
+
+    # ---- residency protocol (chunk_trainer.hpp:318-363)
+    @staticmethod
+    def _union(sel) -> list[int]:
+        return sorted({int(p) for l in sel.lists() for p in l})
+
+    def _attended(self, sel) -> int:  # attended_tokens_ (chunk_trainer.hpp:318-322)
+        return self.cfg.chunk_size + sum(len(l) for l in sel.lists()) * self.cfg.page_size
+
+    def _lookahead(self, nxt: ChunkState, layer: int, cached: bool, backward_part: bool) -> None:
+        eng, cfg = self.engine, self.cfg
+        if eng is None:
+            return
+        if cached:
+            pages = self._union(nxt.selected[layer])
+            if backward_part:
+                pages = sorted(set(pages) | set(self._own_pages(nxt).tolist()))
+        else:
+            mode = cfg.mode_for_layer(layer)
+            if mode == "topk":
+                return  # sparse ids appear only after that layer's q projection
+            n_cand = nxt.pos_offset // cfg.page_size
+            pages = A.select_all(n_cand) if mode == "dense" else A.select_recent(n_cand, cfg.local_window)
+            existing = self.cache.n_pages(layer)
+            pages = [p for p in pages if p < existing]  # pages appended later are device-born
+        self.pending = eng.fetch_async(layer, pages, nxt.index, best_effort=True)
+
+    def _ensure_resident(self, layer: int, ids, chunk_idx: int, h_cur) -> None:
+        eng = self.engine
+        if eng is None:
+            return
+        if h_cur is not None:
+            eng.wait(h_cur)
+        eng.wait(eng.fetch_async(layer, ids, chunk_idx))
+        eng.record_access(layer, ids, chunk_idx)
+
+    def _cost(self) -> ComputeCostModel:
+        return self.tier.compute
 
     def make_chunk_states(self, tokens) -> list[ChunkState]:  # chunk_trainer.hpp:225-251
         toks = np.asarray(tokens, dtype=np.int64)
@@ -170,25 +222,52 @@ class ChunkTrainer:
         """chunk_trainer.hpp:388-501: the shared chunk pass; append=True is phase A."""
         cfg, C = self.cfg, self.cfg.chunk_size
         hq, hk, hd = cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim
+        eng = self.engine
         h = p["emb"][chunk.tokens]
         for l in range(cfg.n_layers):
             lp = p["layers"][l]
+            h_cur = None
+            if eng is not None:  # prefetch for the step that follows this one
+                h_cur, self.pending = self.pending, None
+                if l + 1 < cfg.n_layers:
+                    self._lookahead(chunk, l + 1, cached=not append, backward_part=False)
+                elif append:
+                    if chunk.index + 1 < len(self.chunks):
+                        self._lookahead(self.chunks[chunk.index + 1], 0, cached=False, backward_part=False)
+                else:  # last recompute layer: this chunk's backward of the same layer comes next
+                    self._lookahead(chunk, l, cached=True, backward_part=True)
             a = rmsnorm(h, lp["attn_norm"])
             q = A.rope((a @ lp["wq"]).view(C, hq, hd), chunk.pos_offset, cfg.rope_base, out_dtype=self.dtype)
+            if eng is not None:
+                eng.advance_compute(self._cost().q_time(), chunk.index, l)
             if append:
                 chunk.selected.append(self._select(chunk, l, q))
+                if eng is not None and cfg.mode_for_layer(l) == "topk":
+                    h_cur = eng.fetch_async(l, self._union(chunk.selected[l]), chunk.index)
             sel = chunk.selected[l]
+            sel_union = self._union(sel) if eng is not None else None
             k = A.rope((a @ lp["wk"]).view(C, hk, hd), chunk.pos_offset, cfg.rope_base, out_dtype=self.dtype)
             v = (a @ lp["wv"]).view(C, hk, hd).to(self.dtype).contiguous()
+            if eng is not None:
+                eng.advance_compute(self._cost().kv_time(), chunk.index, l)
             if append:
-                self.cache.append_chunk(l, k, v)
+                r = self.cache.append_chunk(l, k, v)
+                if eng is not None:
+                    eng.on_pages_appended(l, r)
+            self._ensure_resident(l, sel_union, chunk.index, h_cur)
             saved = A.attn_forward(cfg, q, self.cache, l, sel, k, v)
+            if eng is not None:
+                eng.advance_compute(self._cost().attn_time(self._attended(sel)), chunk.index, l)
             attn_flat = saved.out.view(C, hq * hd).float()
             h2 = h + attn_flat @ lp["wo"]
             b = rmsnorm(h2, lp["mlp_norm"])
             u = b @ lp["w_up"]
             s = silu(u)
             h_next = h2 + s @ lp["w_down"]
+            if eng is not None:
+                eng.advance_compute(self._cost().post_time(), chunk.index, l)
+                used = sel_union + (self._own_pages(chunk).tolist() if append else [])
+                eng.end_layer_use(l, used)
             if tape is not None:
                 tape.append(dict(attn_norm_in=h, a=a, q=q, k=k, v=v, saved=saved, attn_flat=attn_flat, h2=h2, b=b,
                                  u=u, s=s))
@@ -207,15 +286,33 @@ class ChunkTrainer:
         dfn = linear_backward(fn, p["unemb"], dlogits, g["unemb"])
         dh = rmsnorm_backward(final_in, p["final_norm"], dfn, g["final_norm"])
         own = self._own_pages(chunk)
+        eng = self.engine
         for l in reversed(range(cfg.n_layers)):
             lp, lg, la = p["layers"][l], g["layers"][l], tape[l]
+            sel = chunk.selected[l]
+            h_cur = None
+            if eng is not None:
+                h_cur, self.pending = self.pending, None
+                if l > 0:
+                    self._lookahead(chunk, l - 1, cached=True, backward_part=True)
+                elif chunk.index > 0:
+                    self._lookahead(self.chunks[chunk.index - 1], 0, cached=True, backward_part=False)
+                eng.advance_compute(2 * self._cost().post_time(), chunk.index, l)
             ds = linear_backward(la["s"], lp["w_down"], dh, lg["w_down"])
             du = silu_backward(la["u"], ds)
             db = linear_backward(la["b"], lp["w_up"], du, lg["w_up"])
             dh2 = rmsnorm_backward(la["h2"], lp["mlp_norm"], db, lg["mlp_norm"]) + dh
             dattn = linear_backward(la["attn_flat"], lp["wo"], dh2, lg["wo"])
             dout = dattn.view(C, hq, hd).to(self.dtype).contiguous()
+            touch = None
+            if eng is not None:
+                sel_union = self._union(sel)
+                touch = sorted(set(sel_union) | set(own.tolist()))
+                self._ensure_resident(l, touch, chunk.index, h_cur)
             ag = A.attn_backward(cfg, dout, la["q"], self.cache, l, la["k"], la["v"], la["saved"])
+            if eng is not None:
+                eng.on_grads_scattered(l, sel_union)
+                eng.advance_compute(2 * self._cost().attn_time(self._attended(sel)), chunk.index, l)
             # dM_i: what later chunks deposited into this chunk's own pages joins dK / dV, and dK is
             # rotated back in the same pass (the reverse projection epilogue)
             self.cache.accumulate_grad_pages_rope(l, own, ag.dk_cur, ag.dv_cur, chunk.pos_offset, cfg.rope_base)
@@ -225,7 +322,18 @@ class ChunkTrainer:
             da = da + linear_backward(la["a"], lp["wk"], dk_pre, lg["wk"])
             da = da + linear_backward(la["a"], lp["wv"], ag.dv_cur.view(C, hk * hd), lg["wv"])
             dh = rmsnorm_backward(la["attn_norm_in"], lp["attn_norm"], da, lg["attn_norm"]) + dh2
-        g["emb"].index_add_(0, chunk.tokens, dh)
+            if eng is not None:
+                eng.advance_compute(2 * (self._cost().q_time() + self._cost().kv_time()), chunk.index, l)
+                eng.end_layer_use(l, touch)
+        # embedding rows (chunk_trainer.hpp:616-621): a one-hot GEMM keeps the sum order fixed (an
+        # atomic index_add would make repeated tokens' sums run-to-run different); large vocabularies
+        # fall back to index_add
+        if cfg.vocab_size * C <= 1 << 24:
+            onehot = torch.zeros(C, cfg.vocab_size, device=dh.device, dtype=dh.dtype)
+            onehot[torch.arange(C, device=dh.device), chunk.tokens] = 1.0
+            g["emb"] += onehot.t() @ dh
+        else:
+            g["emb"].index_add_(0, chunk.tokens, dh)
 
     def train_step(self, p: dict, tokens, grads_out: dict | None = None) -> tuple[StepMetrics, dict]:
         """chunk_trainer.hpp:131-186. Returns (metrics, gradients) with the gradients in the same
@@ -244,14 +352,34 @@ class ChunkTrainer:
                     v.zero_()
         self.cache.reset()
         self.chunks = self.make_chunk_states(tokens)
+        self.pending = None
+        self.engine = None
+        if self.tier is not None:
+            self.engine = TieredEngine(self.cache, self.tier)
+            self.engine.set_prefetch_headroom_pages(self.cfg.pages_per_chunk())
+            self.engine.begin_phase(FORWARD)
         scale = 1.0 / (t_total - 1) if t_total > 1 else 1.0
         loss_sum = 0.0
-        with torch.no_grad():
-            for ch in self.chunks:  # phase A
-                loss_sum += self._run_chunk(p, ch, True, None, 1.0)[0]
-            for ch in reversed(self.chunks):  # recompute + backward, reverse chunk order
-                tape: list = []
-                _, dlogits, final_in, fn = self._run_chunk(p, ch, False, tape, scale)
-                self._backward(p, ch, tape, final_in, fn, dlogits, g)
+        try:
+            with torch.no_grad():
+                for ch in self.chunks:  # phase A
+                    loss_sum += self._run_chunk(p, ch, True, None, 1.0)[0]
+                if self.engine is not None:
+                    self.engine.release_all_reservations()
+                    self.engine.begin_phase(BACKWARD)
+                self.pending = None
+                if self.engine is not None and self.chunks:  # head start for the first recompute step
+                    self._lookahead(self.chunks[-1], 0, cached=True, backward_part=False)
+                for ch in reversed(self.chunks):  # recompute + backward, reverse chunk order
+                    tape: list = []
+                    _, dlogits, final_in, fn = self._run_chunk(p, ch, False, tape, scale)
+                    self._backward(p, ch, tape, final_in, fn, dlogits, g)
+            if self.engine is not None:
+                torch.cuda.synchronize()
+                self.last_log = self.engine.raw_log()
+        finally:
+            if self.engine is not None:
+                self.engine.close()
+                self.engine = None
         loss = loss_sum / (t_total - 1) if t_total > 1 else 0.0
         return StepMetrics(loss), g

@@ -19,10 +19,12 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
-from oracle.oracle import ref_full_forward_backward, ref_init_params, ref_train_step  # noqa: E402
+from oracle.oracle import (ref_full_forward_backward, ref_init_params, ref_train_step,  # noqa: E402
+                           ref_train_step_offload)
 from paper_2602_02108_b200.config import ModelConfig  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
+OFFLOAD_CAPACITY = 20  # device pages (both layers) of the offload variant
 
 
 def model_cfg(mode: str = "dense") -> ModelConfig:
@@ -46,6 +48,11 @@ def main():
         out[f"{mode}_loss_f64"] = np.float64(l64)
         out[f"{mode}_grads_f64"] = g64.astype(np.float32)
         out[f"{mode}_sel_counts"] = cnt
+        # the same step with the TieredEngine protocol at OFFLOAD_CAPACITY device pages: the
+        # ScheduleLog's (kind, layer, page, chunk, phase, bytes) sequence and the (unchanged) gradients
+        lo, go, ev, _ = ref_train_step_offload(mc, mode, params, tokens, OFFLOAD_CAPACITY)
+        assert lo == l32 and np.array_equal(go, g32)
+        out[f"{mode}_offload_events"] = ev
         print(mode, "loss f32", l32, "f64", l64, "grad rel (f32 vs f64)",
               float(np.linalg.norm(g32 - g64) / np.linalg.norm(g64)))
     # the exact non-chunked pass in f64: ground truth for the dense chunked step (acceptance criterion 1)

@@ -65,3 +65,30 @@ def test_gradient_pages_carry_the_cross_chunk_gradient():
     cut = flatten(g_cut, cfg).cpu().numpy()
     assert rel(cut, full) > 1e-3
     assert rel(full, z["dense_grads_f32"]) < 2e-5
+
+
+@pytest.mark.parametrize("mode", ["dense", "topk", "local"])
+def test_offloaded_train_step_follows_the_reference_protocol(mode):
+    """The device trainer with a TieredEngine at 20 device pages (both layers) makes the reference
+    ChunkTrainer's residency decisions event for event: its ScheduleLog's (kind, layer, page, chunk,
+    phase, bytes) sequence equals the reference's (tests/golden/model_step.npz), its gradients are
+    bitwise those of the all-resident run (test_tiered_memory.cpp:429-454 transparency), and the log
+    validates with no violations."""
+    from paper_2602_02108_b200.tiered_memory import TierConfig, validate_schedule
+    from paper_2602_02108_b200.trainer import ChunkTrainer, flatten, unflatten
+    from tests.golden.make_model_golden import OFFLOAD_CAPACITY, model_cfg
+    z = np.load(FIX)
+    cfg = model_cfg(mode)
+    mt = len(z["tokens"]) + cfg.chunk_size
+    plain = ChunkTrainer(cfg, max_tokens=mt, dtype="fp32")
+    _, g0 = plain.train_step(unflatten(z["params"], cfg, plain.dev), z["tokens"])
+    tr = ChunkTrainer(cfg, max_tokens=mt, dtype="fp32",
+                      tier=TierConfig(device_capacity_pages=OFFLOAD_CAPACITY, bandwidth_bytes_per_s=16e9))
+    m, g1 = tr.train_step(unflatten(z["params"], cfg, tr.dev), z["tokens"])
+    assert torch.equal(flatten(g0, cfg), flatten(g1, cfg))
+    got = np.array([(e.kind, e.layer, e.page, e.chunk, e.phase, e.bytes) for e in tr.last_log], np.int64)
+    want = z[f"{mode}_offload_events"]
+    assert got.shape == want.shape, (got.shape, want.shape)
+    assert np.array_equal(got, want), next(i for i in range(len(got)) if not np.array_equal(got[i], want[i]))
+    assert (got[:, 0] == 2).sum() > 0  # evictions happened
+    assert validate_schedule(tr.last_log, 16e9).violations == []
