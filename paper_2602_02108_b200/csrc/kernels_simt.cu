@@ -672,7 +672,7 @@ __global__ void attn_bwd_simt_kernel(AttnGeom g, const T* __restrict__ dout, con
                                      const T* __restrict__ kpool, const T* __restrict__ vpool, float* __restrict__ gk,
                                      float* __restrict__ gv, const T* __restrict__ k_cur, const T* __restrict__ v_cur,
                                      const T* __restrict__ o, const float* __restrict__ lse, float* __restrict__ dq,
-                                     float* __restrict__ dk_cur, float* __restrict__ dv_cur, int* err) {
+                                     float* __restrict__ d_rows, int* err) {
     const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= static_cast<int64_t>(g.C) * g.Hq) return;
@@ -691,8 +691,9 @@ __global__ void attn_bwd_simt_kernel(AttnGeom g, const T* __restrict__ dout, con
         dqa[i] = 0.f;
     }
     const float D = warp_sum(dpart);
+    if (lane == 0) d_rows[row] = D;
     const float L = lse[row];
-    auto visit = [&](const T* kr, const T* vr, float* dkr, float* dvr) {
+    auto visit = [&](const T* kr, const T* vr) {
         float p1 = 0.f, p2 = 0.f;
 #pragma unroll
         for (int i = 0; i < kMaxLaneElems; ++i) {
@@ -711,8 +712,6 @@ __global__ void attn_bwd_simt_kernel(AttnGeom g, const T* __restrict__ dout, con
             const int d = lane + 32 * i;
             if (i < nd && d < hd) {
                 dqa[i] += dlogit * to_f(kr[d]);
-                atomicAdd(dkr + d, dlogit * qv[i]);
-                atomicAdd(dvr + d, p * dov[i]);
             }
         }
     };
@@ -729,22 +728,136 @@ __global__ void attn_bwd_simt_kernel(AttnGeom g, const T* __restrict__ dout, con
         }
         const int vs = valid_in_page(g.filled, pid, g.P);
         const size_t base = (static_cast<size_t>(slot) * g.Hkv + kvh) * g.P * hd;
-        const size_t gbase = (static_cast<size_t>(gs) * g.Hkv + kvh) * g.P * hd;
         for (int s = 0; s < vs; ++s) {
             const size_t so = static_cast<size_t>(s) * hd;
-            visit(kpool + base + so, vpool + base + so, gk + gbase + so, gv + gbase + so);
+            visit(kpool + base + so, vpool + base + so);
         }
     }
     if (g.chunk_keys) {
         for (int s = 0; s <= t; ++s) {
             const size_t so = (static_cast<size_t>(s) * g.Hkv + kvh) * hd;
-            visit(k_cur + so, v_cur + so, dk_cur + so, dv_cur + so);
+            visit(k_cur + so, v_cur + so);
         }
     }
 #pragma unroll
     for (int i = 0; i < kMaxLaneElems; ++i) {
         const int d = lane + 32 * i;
         if (i < nd && d < hd) dq[row * hd + d] = dqa[i];
+    }
+}
+
+// dK / dV, key-major and deterministic: one warp per (key row, kv head) sums its contributions in
+// the reference's order (attention.hpp:239-290): query pages ascending, then rows, then the group's
+// heads. A past page's sum is flushed into its gradient page once per query page that selected it
+// (scatter_add_grads per query page, :288-290); the chunk's own keys sum over every row t >= s
+// into dk_cur / dv_cur. Single writer per element: no atomics. grid.x = past pages (then the
+// chunk's own key blocks of P rows), grid.y = kv head; warp w of the block takes slots w, w+4, ...
+template <typename T>
+__global__ void attn_bwd_kv_simt_kernel(AttnGeom g, const T* __restrict__ dout, const T* __restrict__ q,
+                                        const int32_t* __restrict__ sel_off, const int32_t* __restrict__ sel_ids,
+                                        const int32_t* __restrict__ kvslot, const int32_t* __restrict__ gslot,
+                                        const T* __restrict__ kpool, const T* __restrict__ vpool,
+                                        float* __restrict__ gk, float* __restrict__ gv, const T* __restrict__ k_cur,
+                                        const T* __restrict__ v_cur, const float* __restrict__ lse,
+                                        const float* __restrict__ d_rows, float* __restrict__ dk_cur,
+                                        float* __restrict__ dv_cur, int n_past_pages) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int kvh = blockIdx.y, hd = g.hd, nd = (hd + 31) / 32;
+    const bool past = static_cast<int>(blockIdx.x) < n_past_pages;
+    const int pid = past ? static_cast<int>(blockIdx.x) : -1;
+    const int blk = past ? 0 : static_cast<int>(blockIdx.x) - n_past_pages;  // chunk key block
+    if (!past && !g.chunk_keys) return;
+    int slot = -1, gs = -1, n_keys = g.P;
+    if (past) {
+        slot = kvslot[pid];
+        gs = gslot[pid];
+        if (slot < 0 || gs < 0) return;  // never selected (the query kernel flags selected non-resident pages)
+        n_keys = valid_in_page(g.filled, pid, g.P);
+    } else {
+        n_keys = min(g.P, g.C - blk * g.P);
+    }
+    for (int s = warp; s < n_keys; s += nw) {
+        const T* kr;
+        const T* vr;
+        float* dkr;
+        float* dvr;
+        int key_t = 0;  // chunk keys: the key's row
+        if (past) {
+            const size_t off = ((static_cast<size_t>(slot) * g.Hkv + kvh) * g.P + s) * hd;
+            const size_t goff = ((static_cast<size_t>(gs) * g.Hkv + kvh) * g.P + s) * hd;
+            kr = kpool + off;
+            vr = vpool + off;
+            dkr = gk + goff;
+            dvr = gv + goff;
+        } else {
+            key_t = blk * g.P + s;
+            const size_t off = (static_cast<size_t>(key_t) * g.Hkv + kvh) * hd;
+            kr = k_cur + off;
+            vr = v_cur + off;
+            dkr = dk_cur + off;
+            dvr = dv_cur + off;
+        }
+        float kv[kMaxLaneElems], vv[kMaxLaneElems], ak[kMaxLaneElems], av[kMaxLaneElems];
+#pragma unroll
+        for (int i = 0; i < kMaxLaneElems; ++i) {
+            const int d = lane + 32 * i;
+            const bool ok = i < nd && d < hd;
+            kv[i] = ok ? to_f(kr[d]) : 0.f;
+            vv[i] = ok ? to_f(vr[d]) : 0.f;
+            ak[i] = av[i] = 0.f;
+        }
+        auto rows = [&](int t0, int t1) {  // rows t0..t1-1, the group's heads: accumulate in order
+            for (int t = t0; t < t1; ++t)
+                for (int j = 0; j < g.group; ++j) {
+                    const int64_t row = static_cast<int64_t>(t) * g.Hq + kvh * g.group + j;
+                    float p1 = 0.f, p2 = 0.f, qv[kMaxLaneElems], dv2[kMaxLaneElems];
+#pragma unroll
+                    for (int i = 0; i < kMaxLaneElems; ++i) {
+                        const int d = lane + 32 * i;
+                        const bool ok = i < nd && d < hd;
+                        qv[i] = ok ? to_f(q[row * hd + d]) : 0.f;
+                        dv2[i] = ok ? to_f(dout[row * hd + d]) : 0.f;
+                        p1 += qv[i] * kv[i];
+                        p2 += dv2[i] * vv[i];
+                    }
+                    const float dot = warp_sum(p1);
+                    const float dpv = warp_sum(p2);
+                    const float p = expf(dot * g.scale - lse[row]);
+                    const float dlogit = p * (dpv - d_rows[row]) * g.scale;
+#pragma unroll
+                    for (int i = 0; i < kMaxLaneElems; ++i) {
+                        ak[i] += dlogit * qv[i];
+                        av[i] += p * dv2[i];
+                    }
+                }
+        };
+        if (past) {
+            for (int qp = 0; qp < g.m; ++qp) {
+                bool sel = false;
+                for (int idx = sel_off[qp]; idx < sel_off[qp + 1] && !sel; ++idx) sel = sel_ids[idx] == pid;
+                if (!sel) continue;
+                rows(qp * g.P, min(g.C, (qp + 1) * g.P));
+#pragma unroll
+                for (int i = 0; i < kMaxLaneElems; ++i) {  // this query page's scatter_add
+                    const int d = lane + 32 * i;
+                    if (i < nd && d < hd) {
+                        dkr[d] += ak[i];
+                        dvr[d] += av[i];
+                    }
+                    ak[i] = av[i] = 0.f;
+                }
+            }
+        } else {
+            rows(key_t, g.C);
+#pragma unroll
+            for (int i = 0; i < kMaxLaneElems; ++i) {
+                const int d = lane + 32 * i;
+                if (i < nd && d < hd) {
+                    dkr[d] = ak[i];
+                    dvr[d] = av[i];
+                }
+            }
+        }
     }
 }
 
@@ -774,24 +887,29 @@ void launch_attn_bwd_simt(int dtype, const AttnGeom& g, const void* dout, const 
                           const int32_t* sel_ids, const int32_t* d_kvslot_layer, const int32_t* d_gslot_layer,
                           const void* kpool, const void* vpool, float* gkpool, float* gvpool, const void* k_cur,
                           const void* v_cur, const void* out, const float* lse, float* dq, float* dk_cur,
-                          float* dv_cur, int* d_err, cudaStream_t st) {
+                          float* dv_cur, int* d_err, cudaStream_t st, int n_past_pages) {
     ProfScope prof_(PK_BWD_SIMT, st);
     const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
     const unsigned blocks = static_cast<unsigned>((rows + 3) / 4);
-    if (dtype == OOMB_BF16) {
-        using T = __nv_bfloat16;
+    float* d_rows = nullptr;
+    OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_rows), std::max<int64_t>(rows, 1) * sizeof(float), st));
+    const dim3 kv_grid(static_cast<unsigned>(n_past_pages + (g.C + g.P - 1) / g.P), g.Hkv);
+    auto run = [&](auto zero) {
+        using T = decltype(zero);
         attn_bwd_simt_kernel<T><<<blocks, 128, 0, st>>>(
             g, static_cast<const T*>(dout), static_cast<const T*>(q), sel_off, sel_ids, d_kvslot_layer, d_gslot_layer,
             static_cast<const T*>(kpool), static_cast<const T*>(vpool), gkpool, gvpool, static_cast<const T*>(k_cur),
-            static_cast<const T*>(v_cur), static_cast<const T*>(out), lse, dq, dk_cur, dv_cur, d_err);
-    } else {
-        using T = float;
-        attn_bwd_simt_kernel<T><<<blocks, 128, 0, st>>>(
+            static_cast<const T*>(v_cur), static_cast<const T*>(out), lse, dq, d_rows, d_err);
+        check_launch("attn_bwd_simt_kernel");
+        attn_bwd_kv_simt_kernel<T><<<kv_grid, 128, 0, st>>>(
             g, static_cast<const T*>(dout), static_cast<const T*>(q), sel_off, sel_ids, d_kvslot_layer, d_gslot_layer,
             static_cast<const T*>(kpool), static_cast<const T*>(vpool), gkpool, gvpool, static_cast<const T*>(k_cur),
-            static_cast<const T*>(v_cur), static_cast<const T*>(out), lse, dq, dk_cur, dv_cur, d_err);
-    }
-    check_launch("attn_bwd_simt_kernel");
+            static_cast<const T*>(v_cur), lse, d_rows, dk_cur, dv_cur, n_past_pages);
+        check_launch("attn_bwd_kv_simt_kernel");
+    };
+    if (dtype == OOMB_BF16) run(__nv_bfloat16{});
+    else run(float{});
+    OOMB_CUDA(cudaFreeAsync(d_rows, st));
 }
 
 // ===========================================================================

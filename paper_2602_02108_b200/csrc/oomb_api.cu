@@ -899,7 +899,8 @@ int oomb_attn_backward_ex(oomb_pool_t p, int layer, const void* dout, const void
             OOMB_CUDA(cudaMemsetAsync(dv_cur, 0, kvb, S(stream)));
             launch_attn_bwd_simt(p->cfg.dtype, g, dout, q, sel->d_off, sel->d_ids, p->kvslot_layer(layer),
                                  p->gslot_layer(layer), p->kpool, p->vpool, p->gkpool, p->gvpool, k_cur, v_cur, out,
-                                 lse, dq, dk_cur, dv_cur, p->d_err, S(stream));
+                                 lse, dq, dk_cur, dv_cur, p->d_err, S(stream),
+                                 static_cast<int>(p->pt->pages[layer].size()));
         }
     });
 }

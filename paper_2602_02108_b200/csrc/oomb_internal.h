@@ -203,7 +203,7 @@ void launch_attn_bwd_simt(int dtype, const AttnGeom& g, const void* dout, const 
                           const int32_t* sel_ids, const int32_t* d_kvslot_layer, const int32_t* d_gslot_layer,
                           const void* kpool, const void* vpool, float* gkpool, float* gvpool, const void* k_cur,
                           const void* v_cur, const void* out, const float* lse, float* dq, float* dk_cur,
-                          float* dv_cur, int* d_err, cudaStream_t st);
+                          float* dv_cur, int* d_err, cudaStream_t st, int n_past_pages);
 
 // ---------------------------------------------------------------------------
 // tcgen05 / TMA kernels (attn_tc.cu)

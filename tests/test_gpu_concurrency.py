@@ -54,3 +54,18 @@ def test_concurrent_chunks_bitwise_equal_sequential():
         for u, w in zip(x, y):
             assert torch.equal(u, w)
     assert torch.equal(a_pg[0], b_pg[0]) and torch.equal(a_pg[1], b_pg[1])
+
+
+def test_fp32_backward_replays_bitwise():
+    """The fp32 parity path is deterministic too (SPEC determinism, SURVEY §8b threading): dQ is
+    query-major and dK / dV key-major with one writer per element, summed in the reference's order,
+    so two runs give the same bits for dq, dk_cur, dv_cur and the gradient pages."""
+    import numpy as np
+    from tests.test_gpu_parity import ATTN_CASES, attn_case, run_device
+    mk, past, seed, sel = ATTN_CASES["small_sparse"]
+    c = mk()
+    case = attn_case(c, past, seed=seed, dtype=np.float32, selected=sel)
+    a, _ = run_device(c, case, "fp32")
+    b, _ = run_device(c, case, "fp32")
+    for k in ("out", "lse", "dq", "dk_cur", "dv_cur", "grad_k", "grad_v"):
+        assert np.array_equal(a[k], b[k]), k
