@@ -226,29 +226,32 @@ void launch_gather(int dtype, int grads, const int32_t* d_ids, int n, const int3
 }
 
 // ===========================================================================
-// scatter_add_grads (paged_kv.hpp:135-164): valid slots only, in place.
+// scatter_add_grads (paged_kv.hpp:135-164): valid slots only, in place. One thread per element
+// offset of a page walks the id list in order, so a page listed twice receives its additions in
+// list order (no atomics: deterministic, the reference's order).
 // ===========================================================================
 __global__ void scatter_kernel(const int32_t* __restrict__ ids, int n, const int32_t* __restrict__ gslot,
                                float* __restrict__ gk, float* __restrict__ gv, const float* __restrict__ dk,
                                const float* __restrict__ dv, int64_t filled, int P, int Hkv, int hd, int* err) {
     const int re = Hkv * hd;
-    const int64_t total = static_cast<int64_t>(n) * P * re;
-    for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(idx / (static_cast<int64_t>(P) * re));
-        const int rem = static_cast<int>(idx - static_cast<int64_t>(i) * P * re);
-        const int s = rem / re, e = rem - (rem / re) * re;
-        const int h = e / hd, d = e - (e / hd) * hd;
-        const int pid = ids[i];
-        if (s >= valid_in_page(filled, pid, P)) continue;
-        const int g = gslot[pid];
-        if (g < 0) {
-            atomicOr(err, DERR_NOT_RESIDENT);
-            continue;
+    const int64_t per_page = static_cast<int64_t>(P) * re;
+    for (int64_t off = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; off < per_page;
+         off += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int s = static_cast<int>(off / re), e = static_cast<int>(off - static_cast<int64_t>(s) * re);
+        const int h = e / hd, d = e - h * hd;
+        for (int i = 0; i < n; ++i) {
+            const int pid = ids[i];
+            if (s >= valid_in_page(filled, pid, P)) continue;
+            const int g = gslot[pid];
+            if (g < 0) {
+                atomicOr(err, DERR_NOT_RESIDENT);
+                continue;
+            }
+            const size_t dst = ((static_cast<size_t>(g) * Hkv + h) * P + s) * hd + d;
+            const int64_t src = static_cast<int64_t>(i) * per_page + off;
+            gk[dst] += dk[src];
+            gv[dst] += dv[src];
         }
-        const size_t dst = ((static_cast<size_t>(g) * Hkv + h) * P + s) * hd + d;
-        atomicAdd(gk + dst, dk[idx]);
-        atomicAdd(gv + dst, dv[idx]);
     }
 }
 
@@ -257,8 +260,8 @@ void launch_scatter(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, f
                     cudaStream_t st) {
     if (n <= 0) return;
     ProfScope prof_(PK_GATHER, st);
-    const int64_t total = static_cast<int64_t>(n) * P * Hkv * hd;
-    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 32));
+    const int64_t per_page = static_cast<int64_t>(P) * Hkv * hd;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((per_page + 255) / 256, 148 * 32));
     scatter_kernel<<<blocks, 256, 0, st>>>(d_ids, n, d_gslot_layer, gk, gv, dk, dv, filled, P, Hkv, hd, d_err);
     check_launch("scatter_kernel");
 }

@@ -140,7 +140,7 @@ def test_scatter_lazy_grads_and_reset_reuse():
         assert cache.memory_report().grad_bytes == 0 or step > 0
         gk = cache.gather_grad_pages(0, [0, 1])
         assert float(gk.k.abs().sum()) == 0.0
-        for ids in ([3, 1], [0, 3], [2]):
+        for ids in ([3, 1], [0, 3], [2], [1, 1, 0]):  # a repeated id adds twice, in list order
             dk = det_normal(50 + len(ids) + step, (len(ids) * 16, 2, 16))
             dv = -2 * dk
             cache.scatter_add_grads(0, ids, torch.from_numpy(dk).cuda(), torch.from_numpy(dv).cuda())
