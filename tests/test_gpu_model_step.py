@@ -93,3 +93,26 @@ def test_offloaded_train_step_follows_the_reference_protocol(mode):
     assert np.array_equal(got, want), next(i for i in range(len(got)) if not np.array_equal(got[i], want[i]))
     assert (got[:, 0] == 2).sum() > 0  # evictions happened
     assert validate_schedule(tr.last_log, 16e9).violations == []
+
+
+@pytest.mark.parametrize("mode", ["dense", "topk"])
+def test_bf16_tcgen05_train_step_tracks_reference(mode):
+    """The whole-model step on the tcgen05 path (bf16 pages, hd 128, P 128): loss and gradients follow
+    the reference's fp32 ChunkTrainer::train_step (run live through oracle/_ref) within the bf16
+    tolerance. Parameters come from the reference's init_params."""
+    from oracle.oracle import Ref, ref_init_params, ref_train_step
+    from paper_2602_02108_b200.config import ModelConfig
+    from paper_2602_02108_b200.trainer import ChunkTrainer, flatten, unflatten
+    if not Ref.available():
+        pytest.skip("reference shim not built (oracle/_ref)")
+    cfg = ModelConfig(n_layers=2, d_model=128, n_q_heads=4, n_kv_heads=2, head_dim=128, d_ff=256, vocab_size=64,
+                      chunk_size=256, page_size=128, attention_mode=[mode], retrieval_budget=128, local_window=1,
+                      seed=3)
+    params = ref_init_params(cfg, mode, seed=3)
+    tokens = np.random.default_rng(5).integers(0, 64, size=1100).astype(np.int32)  # 5 chunks, last partial
+    loss_ref, g_ref, _ = ref_train_step(cfg, mode, params, tokens)
+    tr = ChunkTrainer(cfg, max_tokens=len(tokens) + cfg.chunk_size, dtype="bf16")
+    m, g = tr.train_step(unflatten(params, cfg, tr.dev), tokens)
+    gf = flatten(g, cfg).cpu().numpy()
+    assert abs(m.loss - loss_ref) < 1e-3 * abs(loss_ref), (m.loss, loss_ref)
+    assert rel(gf, g_ref) < 2e-2, rel(gf, g_ref)
