@@ -140,11 +140,19 @@ __global__ void __launch_bounds__(1024) bwd_union_kernel(const uint64_t* __restr
 #ifndef OOMB_DQ_KST
 #define OOMB_DQ_KST 3
 #endif
-constexpr int kDqKSt = OOMB_DQ_KST, kDqVSt = 5 - OOMB_DQ_KST;  // K / V stages (3 / 2 kept: 2 / 3 measured 6 % slower)
-constexpr int kDqQ = 0;
+#ifndef OOMB_DQ_ALIAS
+#define OOMB_DQ_ALIAS 0  // measured equal at c3 (468.4 vs 468.7 ms backward pass)
+#endif
+// Q and dO are read from shared memory only once (staged into TMEM at the start), so with
+// OOMB_DQ_ALIAS their tiles double as the 4th K stage and the 1st V stage (layout
+// K0 K1 K2 Q=K3 | dO=V0 V1 V2); the producers wait for the TMEM staging before first reuse.
+constexpr bool kDqAlias = OOMB_DQ_ALIAS != 0;
+constexpr int kDqKSt = kDqAlias ? 4 : OOMB_DQ_KST;
+constexpr int kDqVSt = kDqAlias ? 3 : 5 - OOMB_DQ_KST;  // K / V stages (3 / 2: 2 / 3 measured 6 % slower)
+constexpr int kDqK = kDqAlias ? 0 : 2 * kTileBytes;     // kDqKSt stages
+constexpr int kDqQ = kDqAlias ? 3 * kTileBytes : 0;
 constexpr int kDqDO = kDqQ + kTileBytes;
-constexpr int kDqK = kDqDO + kTileBytes;            // kDqKSt stages
-constexpr int kDqV = kDqK + kDqKSt * kTileBytes;    // kDqVSt stages
+constexpr int kDqV = kDqAlias ? kDqDO : kDqK + kDqKSt * kTileBytes;  // kDqVSt stages
 constexpr int kDqBar = kDqV + kDqVSt * kTileBytes;
 constexpr int kDqNv = kDqBar + 256;                 // uint8 valid-key counts of the past blocks
 constexpr int kDqNvCap = 1024;
@@ -239,6 +247,7 @@ __global__ void __launch_bounds__(384, 1)
             for (int j = 0; j < nb; ++j) {
                 const int st = j % kDqKSt;
                 if (j >= kDqKSt) mbar_wait(&bars->k_empty[st], ((j / kDqKSt) - 1) & 1);
+                if (kDqAlias && j == 3) mbar_wait(&bars->qdo_tmem, 0);  // K stage 3 is the Q tile
                 mbar_expect_tx(&bars->k_full[st], kTileBytes);
                 uint8_t* dst = sK + st * kTileBytes;
                 if (j < n_past) {
@@ -255,6 +264,7 @@ __global__ void __launch_bounds__(384, 1)
             for (int j = 0; j < nb; ++j) {
                 const int st = j % kDqVSt;
                 if (j >= kDqVSt) mbar_wait(&bars->v_empty[st], ((j / kDqVSt) - 1) & 1);
+                if (kDqAlias && j == 0) mbar_wait(&bars->qdo_tmem, 0);  // V stage 0 is the dO tile
                 mbar_expect_tx(&bars->v_full[st], kTileBytes);
                 uint8_t* dst = sV + st * kTileBytes;
                 if (j < n_past) {
