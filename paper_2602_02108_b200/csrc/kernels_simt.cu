@@ -754,7 +754,7 @@ __global__ void attn_bwd_simt_kernel(AttnGeom g, const T* __restrict__ dout, con
 // heads. A past page's sum is flushed into its gradient page once per query page that selected it
 // (scatter_add_grads per query page, :288-290); the chunk's own keys sum over every row t >= s
 // into dk_cur / dv_cur. Single writer per element: no atomics. grid.x = past pages (then the
-// chunk's own key blocks of P rows), grid.y = kv head; warp w of the block takes slots w, w+4, ...
+// chunk's own key blocks of P rows), grid.y = kv head, grid.z = groups of 4 keys (one per warp).
 template <typename T>
 __global__ void attn_bwd_kv_simt_kernel(AttnGeom g, const T* __restrict__ dout, const T* __restrict__ q,
                                         const int32_t* __restrict__ sel_off, const int32_t* __restrict__ sel_ids,
@@ -779,7 +779,7 @@ __global__ void attn_bwd_kv_simt_kernel(AttnGeom g, const T* __restrict__ dout, 
     } else {
         n_keys = min(g.P, g.C - blk * g.P);
     }
-    for (int s = warp; s < n_keys; s += nw) {
+    for (int s = static_cast<int>(blockIdx.z) * nw + warp; s < n_keys; s += nw * static_cast<int>(gridDim.z)) {
         const T* kr;
         const T* vr;
         float* dkr;
@@ -896,7 +896,8 @@ void launch_attn_bwd_simt(int dtype, const AttnGeom& g, const void* dout, const 
     const unsigned blocks = static_cast<unsigned>((rows + 3) / 4);
     float* d_rows = nullptr;
     OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_rows), std::max<int64_t>(rows, 1) * sizeof(float), st));
-    const dim3 kv_grid(static_cast<unsigned>(n_past_pages + (g.C + g.P - 1) / g.P), g.Hkv);
+    const dim3 kv_grid(static_cast<unsigned>(n_past_pages + (g.C + g.P - 1) / g.P), g.Hkv,
+                       static_cast<unsigned>((g.P + 3) / 4));
     auto run = [&](auto zero) {
         using T = decltype(zero);
         attn_bwd_simt_kernel<T><<<blocks, 128, 0, st>>>(
