@@ -12,10 +12,19 @@ tokens/s = context / step time. `value` has every input resident in HBM;
 `e2e` drives the same public API from pinned HOST buffers with the H2D of each
 chunk's q/k/v/dO and the D2H of its out/dq/dk/dv inside the timed region.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c1] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5] [--impl reference]
+                    [--shard replica|kv] [--offload-cap F] [--no-e2e] [--no-cpu]
 
-Under torchrun (N > 1) every rank runs its own layer-sequence (weak scaling:
-per-GPU work fixed), timed on the device and reported as the max over ranks.
+The step keeps every dependency of the sequential loop and overlaps what it does not need:
+chunk i+1's selection runs on a high-priority stream under chunk i's attention, consecutive
+chunks attend on two streams (OOMB_FWD_STREAMS, default 2), and the backward defers dQ joins
+(OOMB_BWD_DEFER=1: chunk i-1's dK/dV runs under chunk i's dQ). Results are bitwise those of the
+sequential loop (tests/test_gpu_concurrency.py).
+
+Under torchrun (N > 1) every rank runs its own layer-sequence by default (weak scaling: per-GPU
+work fixed), timed on the device and reported as the max over ranks; --shard kv splits one
+sequence across the ranks by KV-head group instead (strong scaling, NCCL vote all-gather).
+The CPU baseline and the offload regime are N = 1 measurements.
 """
 from __future__ import annotations
 
