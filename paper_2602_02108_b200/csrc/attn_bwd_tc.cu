@@ -17,6 +17,7 @@
 //                 fp32 gradient pool (past pages) or a store to dk_cur/dv_cur
 //                 (the chunk's own keys). Pages never selected are not touched.
 
+#include <algorithm>
 #include <cub/block/block_scan.cuh>
 
 #include "tc_common.cuh"
@@ -90,6 +91,11 @@ __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_
         Dt[static_cast<int64_t>(h) * C + t] = s;
         Lt[static_cast<int64_t>(h) * C + t] = lse[row] * kLog2e;
     }
+}
+
+// pages the layer holds: ids at or past this are out of range (never past the pool's table)
+inline int layer_pages(const AttnGeom& g) {
+    return static_cast<int>(std::min<int64_t>(g.max_pages, (g.filled + g.P - 1) / g.P));
 }
 
 __global__ void bwd_mask_kernel(const int32_t* __restrict__ off, const int32_t* __restrict__ ids, int max_pages,
@@ -895,7 +901,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     if (n_pages > 0) OOMB_CUDA(cudaMemsetAsync(w.mask, 0, static_cast<size_t>(n_pages) * 8, st));
     OOMB_CUDA(cudaMemsetAsync(w.n_uni, 0, 2 * sizeof(int32_t), st));  // union count + dK/dV work counter
     if (nnz > 0) {
-        bwd_mask_kernel<<<g.m, 128, 0, st>>>(sel_off, sel_ids, g.max_pages, w.mask, d_err);
+        bwd_mask_kernel<<<g.m, 128, 0, st>>>(sel_off, sel_ids, layer_pages(g), w.mask, d_err);
         check_launch("bwd_mask_kernel");
         bwd_union_kernel<<<1, 1024, 0, st>>>(w.mask, n_pages, w.uni, w.n_uni);
         check_launch("bwd_union_kernel");

@@ -640,7 +640,7 @@ __global__ void attn_fwd_simt_kernel(AttnGeom g, const T* __restrict__ q, const 
     };
     for (int idx = sel_off[qp]; idx < sel_off[qp + 1]; ++idx) {
         const int pid = sel_ids[idx];
-        if (pid < 0 || pid >= g.max_pages) {
+        if (pid < 0 || pid >= g.max_pages || static_cast<int64_t>(pid) * g.P >= g.filled) {
             if (lane == 0) atomicOr(err, DERR_BAD_ID);
             continue;
         }
@@ -720,7 +720,7 @@ __global__ void attn_bwd_simt_kernel(AttnGeom g, const T* __restrict__ dout, con
     };
     for (int idx = sel_off[qp]; idx < sel_off[qp + 1]; ++idx) {
         const int pid = sel_ids[idx];
-        if (pid < 0 || pid >= g.max_pages) {
+        if (pid < 0 || pid >= g.max_pages || static_cast<int64_t>(pid) * g.P >= g.filled) {
             if (lane == 0) atomicOr(err, DERR_BAD_ID);
             continue;
         }

@@ -864,7 +864,7 @@ int oomb_attn_backward_ex(oomb_pool_t p, int layer, const void* dout, const void
         sel_host_sync(sel);
         for (int qp = 0; qp < g.m; ++qp)
             p->pt->check_ids(layer, sel->h_ids + sel->h_off[qp], sel->h_off[qp + 1] - sel->h_off[qp], p->enforce,
-                             "gather_pages");
+                             "attn_backward");
         ensure_grad_pages(p, layer, sel->h_off, sel->h_ids, g.m, S(stream));
         const size_t kvb = static_cast<size_t>(tokens) * g.Hkv * g.hd * sizeof(float);
         const bool tc = p->policy != 1 && p->maps.valid && tc_supported(g, p->cfg.dtype) && tc_bwd_available();

@@ -115,7 +115,8 @@ __device__ __forceinline__ PastBlock past_block(const AttnGeom& g, const int32_t
     PastBlock b;
     b.pid = sel_ids[sel_begin + j / bpp];
     const int sub = j % bpp;
-    const bool id_ok = b.pid >= 0 && b.pid < g.max_pages;
+    // ids past the layer's last page are a ShapeError in the reference (paged_kv.hpp page range)
+    const bool id_ok = b.pid >= 0 && b.pid < g.max_pages && static_cast<int64_t>(b.pid) * g.P < g.filled;
     int slot = id_ok ? kvslot[b.pid] : -1;
     const int64_t nv = g.filled - static_cast<int64_t>(b.pid) * g.P - static_cast<int64_t>(sub) * kTile;
     b.n_valid = static_cast<int>(nv < 0 ? 0 : (nv > kTile ? kTile : nv));
