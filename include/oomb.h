@@ -99,7 +99,12 @@ OOMB_API int oomb_pool_reset(oomb_pool_t pool, void* stream);
 OOMB_API int oomb_zero_grad_pages(oomb_pool_t pool, void* stream);
 /* PagedCache::memory_report  paged_kv.hpp:185-197 */
 OOMB_API int oomb_memory_report_get(oomb_pool_t pool, oomb_memory_report* out);
-/* Device-side error flag raised by kernels (e.g. a non-resident page was read). Synchronises. */
+/* Sticky device-side error flag raised by kernels; synchronises, reports, then clears it.
+ * The forward does not copy a selection to the host unless residency is enforced, so a
+ * selected id outside the layer's pages is skipped by the kernel and reported here as
+ * OOMB_SHAPE_ERROR (the reference's gather throws ShapeError at the call); a read of a
+ * non-resident slot is OOMB_RESIDENCY_ERROR. The backward and the enforced forward check the
+ * ids on the host and fail at the call instead. */
 OOMB_API int oomb_check_device_errors(oomb_pool_t pool);
 
 /* ---- page table --------------------------------------------------------- */
