@@ -28,6 +28,8 @@ def test_bench_line_contract():
     r = d["roofline"]
     assert r["bound"] == "tensor" and r["unit"] == "TFLOP/s" and 0 < r["frac"] < 1 and r["peak"] > 0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    # the in-step pair is measured against the sustained peak; the burst figure rides along
+    assert r["peak"] <= r["peak_burst"] and abs(r["frac_of_burst"] - r["achieved"] / r["peak_burst"]) < 1e-9
     assert r["traffic"] is None or r["traffic"] > 0
     cb = d["cpu_baseline"]
     assert cb["value"] > 0 and cb["cores"] >= 1 and cb["kind"] in ("reference", "port") and cb["sample"]
