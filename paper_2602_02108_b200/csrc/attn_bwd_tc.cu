@@ -11,7 +11,7 @@
 //                 dQ += dS K over the query page's selected pages then the
 //                 chunk's causal prefix; dQ written once (fp32).
 //   attn_bwd_dkdv key-major: one CTA owns one (key block, kv head) and loops over
-//                 every (64-row query tile, q-head of the group) that attends it:
+//                 every (128-row query tile, q-head of the group) that attends it:
 //                 S^T = K Q^T, dP^T = V dO^T, dV += P^T dO, dK += dS^T Q with
 //                 dK/dV accumulated in TMEM, then ONE read-modify-write into the
 //                 fp32 gradient pool (past pages) or a store to dk_cur/dv_cur
