@@ -1,5 +1,6 @@
-"""Parity at BASELINE.json's full c3 size (Qwen2.5-7B attention, 1M context, top-k 64 pages per
-query page): the last chunk of a 1M-token sequence, through the public API, against a float64
+"""Parity at BASELINE.json's full sizes — c3 (Qwen2.5-7B attention, 1M context, top-k 64 pages per
+query page), c4 (the same at 4M context) and c5 (Llama-3-8B attention, page 256, 512K context,
+dense): the last chunk of the sequence, through the public API, against a float64
 restatement of the reference's math (attention.hpp:32-96 scoring/selection, :156-208 forward,
 :222-293 backward) evaluated on the GPU for sampled query pages and heads.
 
@@ -16,8 +17,12 @@ import torch
 
 pytestmark = pytest.mark.gpu
 
-T, C, P, HQ, HKV, HD, K_SEL = 1 << 20, 4096, 128, 28, 4, 128, 64
-G = HQ // HKV
+C, HD = 4096, 128
+CONFIGS = {  # bench.py CONFIGS
+    "c3": dict(T=1 << 20, P=128, HQ=28, HKV=4, k=64),
+    "c4": dict(T=1 << 22, P=128, HQ=28, HKV=4, k=64),
+    "c5": dict(T=1 << 19, P=256, HQ=32, HKV=8, k=None),  # dense
+}
 TOL = 2e-2
 
 
@@ -27,10 +32,11 @@ def rel(a, b):
     return float(d / n) if n > 0 else float(d)
 
 
-@pytest.fixture(scope="module")
-def run():
+@pytest.fixture(scope="module", params=sorted(CONFIGS))
+def run(request):
     from paper_2602_02108_b200 import ModelConfig, PagedCache
     from paper_2602_02108_b200 import attention as A
+    T, P, HQ, HKV, K_SEL = (CONFIGS[request.param][k] for k in ("T", "P", "HQ", "HKV", "k"))
     dev = torch.device("cuda")
     g = torch.Generator(device=dev).manual_seed(2602)
     past = T - C
@@ -43,29 +49,36 @@ def run():
     q = torch.randn(C, HQ, HD, device=dev, generator=g).bfloat16()
     do = torch.randn(C, HQ, HD, device=dev, generator=g).bfloat16()
     cfg = ModelConfig(n_layers=1, n_q_heads=HQ, n_kv_heads=HKV, head_dim=HD, chunk_size=C, page_size=P,
-                      retrieval_budget=K_SEL * P, attention_mode=["topk"])
+                      retrieval_budget=(K_SEL or 0) * P, attention_mode=["topk" if K_SEL else "dense"])
     cache = PagedCache(cfg, dtype="bf16", max_tokens=T)
     cache.append_chunk(0, K[:past], V[:past])
-    sel = A.select_pages_topk(cache, 0, q, n_candidates=n_cand)
-    vote = sel.vote.clone()
-    lists = sel.lists()
+    if K_SEL:
+        sel = A.select_pages_topk(cache, 0, q, n_candidates=n_cand)
+        vote = sel.vote.clone()
+    else:
+        sel, vote = [A.select_all(n_cand) for _ in range(C // P)], None
+    lists = sel.lists() if K_SEL else sel
     kc, vc = K[past:], V[past:]
     cache.append_chunk(0, kc, vc)
     saved = A.attn_forward(cfg, q, cache, 0, sel, kc, vc)
     grads = A.attn_backward(cfg, do, q, cache, 0, kc, vc, saved)
     torch.cuda.synchronize()
     cache.check_device_errors()
-    return dict(cache=cache, K=K, V=V, q=q, do=do, past=past, n_cand=n_cand, vote=vote, lists=lists,
-                saved=saved, grads=grads)
+    yield dict(cache=cache, K=K, V=V, q=q, do=do, past=past, n_cand=n_cand, vote=vote, lists=lists,
+               saved=saved, grads=grads, P=P, HQ=HQ, HKV=HKV, G=HQ // HKV, k=K_SEL, name=request.param)
+    del cache, K, V, saved, grads
+    torch.cuda.empty_cache()
 
 
 def _kavg(r):
+    P, HKV = r["P"], r["HKV"]
     Kp = r["K"][: r["past"]].double().view(r["n_cand"], P, HKV, HD)
     return Kp.sum(1) * (1.0 / P)  # paged_kv.hpp:177-180: sum * (1/count)
 
 
 def _ref_rows(r, qp, h):
     """float64 forward + backward of the 128 rows of query page qp, q-head h (attention.hpp)."""
+    P, HKV, G = r["P"], r["HKV"], r["G"]
     kvh = h // G
     ids = r["lists"][qp]
     past, K, V = r["past"], r["K"], r["V"]
@@ -95,6 +108,9 @@ def _ref_rows(r, qp, h):
 
 def test_fullsize_votes_and_topk(run):
     r = run
+    if not r["k"]:
+        pytest.skip("dense config: no scoring")
+    P, HQ, G, K_SEL = r["P"], r["HQ"], r["G"], r["k"]
     assert len(r["lists"]) == C // P and all(len(x) == K_SEL for x in r["lists"])
     kavg = _kavg(r)
     for qp in (0, 13, 31):
@@ -114,9 +130,10 @@ def test_fullsize_votes_and_topk(run):
             assert set(order[:K_SEL - 1]) <= set(r["lists"][qp]), qp
 
 
-@pytest.mark.parametrize("qp,h", [(0, 0), (7, 13), (20, 6), (31, 27)])
+@pytest.mark.parametrize("qp,h", [(0, 0), (7, 13), (13, 6), (-1, -1)])
 def test_fullsize_forward_and_dq_rows(run, qp, h):
     r = run
+    qp, h = qp % (C // r["P"]), h % r["HQ"]
     ref = _ref_rows(r, qp, h)
     rows = ref["rows"]
     assert rel(r["saved"].out[rows, h], ref["out"]) < TOL
@@ -128,6 +145,9 @@ def test_fullsize_grad_page(run):
     """dK / dV of one past page (kv head 1) = sum over every (query page that selected it, q-head
     of the group, row) of dS^T q and P^T dO — the page's gradient block after the backward."""
     r = run
+    if not r["k"]:
+        pytest.skip("dense config: every query page selects every page (covered by the row checks)")
+    P, G = r["P"], r["G"]
     kvh = 1
     counts = {}
     for ids in r["lists"]:
