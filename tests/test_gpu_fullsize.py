@@ -1,5 +1,5 @@
 """Parity at BASELINE.json's full sizes — c3 (Qwen2.5-7B attention, 1M context, top-k 64 pages per
-query page), c4 (the same at 4M context) and c5 (Llama-3-8B attention, page 256, 512K context,
+query page), c2 (the same shape dense at 128K), c4 (c3 at 4M context) and c5 (Llama-3-8B attention, page 256, 512K context,
 dense): the last chunk of the sequence, through the public API, against a float64
 restatement of the reference's math (attention.hpp:32-96 scoring/selection, :156-208 forward,
 :222-293 backward) evaluated on the GPU for sampled query pages and heads.
@@ -19,6 +19,7 @@ pytestmark = pytest.mark.gpu
 
 C, HD = 4096, 128
 CONFIGS = {  # bench.py CONFIGS
+    "c2": dict(T=1 << 17, P=128, HQ=28, HKV=4, k=None),  # dense
     "c3": dict(T=1 << 20, P=128, HQ=28, HKV=4, k=64),
     "c4": dict(T=1 << 22, P=128, HQ=28, HKV=4, k=64),
     "c5": dict(T=1 << 19, P=256, HQ=32, HKV=8, k=None),  # dense
