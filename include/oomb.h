@@ -287,6 +287,11 @@ OOMB_API int oomb_tier_record_access(oomb_tier_t t, int layer, const int32_t* id
 OOMB_API int oomb_tier_advance_compute(oomb_tier_t t, double seconds, int chunk, int layer);
 OOMB_API int oomb_tier_end_layer_use(oomb_tier_t t, int layer, const int32_t* ids_host, int n);
 OOMB_API int oomb_tier_release_all(oomb_tier_t t);
+/* Real engine: fetch every host-tier page back into free device slots (K/V and gradient blocks)
+ * and mark it resident; OOMB_CONFIG_ERROR, moving nothing, if the pool lacks the slots. Not in
+ * the reference (its engine only tags pages); oomb_tier_destroy calls it when the pool has room,
+ * so detaching an engine does not drop the data of pages it left on the host. */
+OOMB_API int oomb_tier_restore_all(oomb_tier_t t);
 /* out[5] = {now, stall_seconds, h2d_bytes forward, h2d_bytes backward, d2h_bytes} */
 OOMB_API int oomb_tier_stats(oomb_tier_t t, double* out);
 OOMB_API int oomb_tier_log(oomb_tier_t t, oomb_event* out, int64_t cap, int64_t* n);

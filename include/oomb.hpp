@@ -856,6 +856,7 @@ public:
         check(oomb_tier_end_layer_use(t_, layer, ids.data(), static_cast<int>(ids.size())));
     }
     void release_all_reservations() { check(oomb_tier_release_all(t_)); }
+    void restore_all() { check(oomb_tier_restore_all(t_)); }
 
     double now() const { return stats()[0]; }
     double stall_seconds() const { return stats()[1]; }

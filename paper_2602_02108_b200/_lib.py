@@ -105,6 +105,7 @@ _PROTOS = {
     "oomb_tier_advance_compute": [VP, C.c_double, I, I],
     "oomb_tier_end_layer_use": [VP, I, VP, I],
     "oomb_tier_release_all": [VP],
+    "oomb_tier_restore_all": [VP],
     "oomb_tier_stats": [VP, VP],
     "oomb_tier_log": [VP, VP, I64, C.POINTER(I64)],
     "oomb_validate_schedule": [VP, I64, C.c_double, VP, C.POINTER(I), VP, VP, I64],

@@ -494,6 +494,40 @@ struct oomb_tier_s {
         flush_table();
     }
 
+    // Real mode: bring every host-tier page back into free device slots so the pool holds all
+    // K/V and gradient data again once the engine detaches (the reference's engine only tags
+    // pages, so its pool never loses them). All-or-nothing: ConfigError, and nothing moves, when
+    // the pool has fewer free slots than host-tier pages.
+    void restore_all() {
+        if (!real()) return;
+        sync_pages();
+        size_t need_kv = 0, need_g = 0;
+        for (int l = 0; l < pt->n_layers; ++l)
+            for (size_t p = 0; p < pages[l].size(); ++p)
+                if (tier(l, static_cast<int>(p)) != 0 && pages[l][p].in_flight_done <= 0) {
+                    ++need_kv;
+                    if (grads_allocated(l, static_cast<int>(p))) ++need_g;
+                }
+        OOMB_REQUIRE(need_kv <= pool->kv_free.size() && need_g <= pool->g_free.size(), OOMB_CONFIG_ERROR,
+                     "restore_all: the pool has fewer free device slots than host-tier pages");
+        for (int l = 0; l < pt->n_layers; ++l)
+            for (size_t i = 0; i < pages[l].size(); ++i) {
+                const int p = static_cast<int>(i);
+                if (tier(l, p) == 0) continue;
+                PageState& ps = pages[l][i];
+                if (ps.in_flight_done <= 0) real_fetch(l, p);  // an in-flight page already has its slots
+                set_tier(l, p, 0);
+                ps.in_flight_done = 0;
+                queue_table(l, p);
+            }
+        flush_copies(0);
+        cudaEvent_t done = new_event();
+        OOMB_CUDA(cudaEventRecord(done, h2d_stream));
+        OOMB_CUDA(cudaStreamWaitEvent(compute, done, 0));
+        spare_events.push_back(done);
+        flush_table();
+    }
+
     void record_access(int layer, const int32_t* ids, int n, int chunk) {  // :256-264
         flush_table();
         cudaEvent_t ev = n > 0 ? stamp(ON_COMPUTE) : nullptr;
@@ -579,6 +613,10 @@ int oomb_tier_destroy(oomb_tier_t t) {
     if (!t) return OOMB_OK;
     if (t->real()) {
         cudaSetDevice(t->pool->device);
+        try {
+            t->restore_all();  // best effort: a pool without room keeps those pages host-tier (data dropped)
+        } catch (...) {
+        }
         cudaDeviceSynchronize();
         t->pool->enforce = false;
         for (auto e : t->log_events) cudaEventDestroy(e);
@@ -624,6 +662,7 @@ int oomb_tier_end_layer_use(oomb_tier_t t, int layer, const int32_t* ids, int n)
     return TIER_CALL(t, t->end_layer_use(layer, ids, n));
 }
 int oomb_tier_release_all(oomb_tier_t t) { return TIER_CALL(t, t->release_all()); }
+int oomb_tier_restore_all(oomb_tier_t t) { return TIER_CALL(t, t->restore_all()); }
 
 int oomb_tier_stats(oomb_tier_t t, double* out) {
     return guard([&] {

@@ -194,6 +194,11 @@ class TieredEngine:
     def release_all_reservations(self):
         call("oomb_tier_release_all", self.handle)
 
+    def restore_all(self):
+        """Real engine: bring every host-tier page back to the device (ConfigError without room).
+        close() does this when the pool has room, so detaching keeps every page's data."""
+        call("oomb_tier_restore_all", self.handle)
+
     def _stats(self):
         out = (C.c_double * 5)()
         call("oomb_tier_stats", self.handle, out)
