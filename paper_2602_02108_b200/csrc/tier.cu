@@ -613,9 +613,14 @@ int oomb_tier_destroy(oomb_tier_t t) {
     if (!t) return OOMB_OK;
     if (t->real()) {
         cudaSetDevice(t->pool->device);
-        try {
-            t->restore_all();  // best effort: a pool without room keeps those pages host-tier (data dropped)
-        } catch (...) {
+#ifndef OOMB_TIER_RESTORE_ON_DESTROY
+#define OOMB_TIER_RESTORE_ON_DESTROY 1
+#endif
+        if (OOMB_TIER_RESTORE_ON_DESTROY) {
+            try {
+                t->restore_all();  // best effort: a pool without room keeps those pages host-tier (data dropped)
+            } catch (...) {
+            }
         }
         cudaDeviceSynchronize();
         t->pool->enforce = false;
