@@ -117,3 +117,50 @@ def test_offload_pages_round_trip_exactly():
         assert torch.equal(got.k[j * 128:(j + 1) * 128], k[p * 128:(p + 1) * 128])
         assert torch.equal(got.v[j * 128:(j + 1) * 128], v[p * 128:(p + 1) * 128])
     eng.close()
+
+
+def test_restore_all_needs_free_slots_and_keeps_data():
+    """oomb_tier_restore_all: all-or-nothing ConfigError when the pool lacks free device slots for
+    the host-tier pages; with room, every page comes back resident with its K/V and gradients
+    bitwise (what engine close() relies on)."""
+    from paper_2602_02108_b200 import ConfigError, ModelConfig, PagedCache
+    from paper_2602_02108_b200.chunk_loop import AttentionChunkLoop
+    from paper_2602_02108_b200.tiered_memory import TierConfig, TieredEngine
+    cfg = ModelConfig(n_layers=1, n_q_heads=28, n_kv_heads=4, head_dim=128, chunk_size=512, page_size=128,
+                      retrieval_budget=3 * 128, local_window=3, attention_mode=["topk"])
+    g = torch.Generator(device="cuda").manual_seed(5)
+    n = 10  # 40 pages: with 36 device slots and capacity 20 the host holds more pages than there are free slots
+    rnd = lambda h: [torch.randn(512, h, 128, device="cuda", generator=g).bfloat16() for _ in range(n)]
+    qs, ks, vs, dos = rnd(28), rnd(4), rnd(4), rnd(28)
+    pools = []
+    for slots, cap in ((-1, None), (20 + 16, 20), (-1, 20)):
+        cache = PagedCache(cfg, dtype="bf16", max_tokens=n * 512, device_capacity_pages=slots)
+        eng = None
+        if cap is not None:
+            eng = TieredEngine(cache, TierConfig(device_capacity_pages=cap, bandwidth_bytes_per_s=25e9))
+            eng.set_prefetch_headroom_pages(cfg.pages_per_chunk())
+        loop = AttentionChunkLoop(cache, engine=eng)
+        for i in range(n):
+            loop.forward_chunk(i, qs[i], ks[i], vs[i])
+        loop.begin_backward()
+        for i in reversed(range(n)):
+            loop.backward_chunk(i, dos[i], qs[i], ks[i], vs[i])
+        torch.cuda.synchronize()
+        if eng is not None:
+            eng.release_all_reservations()
+            host = [p for p in range(cache.n_pages(0)) if cache.tier(0, p) != 0]
+            assert host, "the capacity must leave pages on the host"
+            if slots > 0:
+                with pytest.raises(ConfigError):
+                    eng.restore_all()
+                assert [p for p in range(cache.n_pages(0)) if cache.tier(0, p) != 0] == host  # nothing moved
+                eng.close()
+                continue
+            eng.restore_all()
+            assert all(cache.tier(0, p) == 0 for p in range(cache.n_pages(0)))
+            eng.close()
+        ids = list(range(cache.n_pages(0)))
+        kv, gr = cache.gather_pages(0, ids), cache.gather_grad_pages(0, ids)
+        pools.append((kv.k.clone(), kv.v.clone(), gr.k.clone(), gr.v.clone()))
+    for a, b in zip(*pools):
+        assert torch.equal(a, b)
