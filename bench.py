@@ -209,7 +209,7 @@ BWD_DEFER = os.environ.get("OOMB_BWD_DEFER", "1") != "0"
 class Run:
     RQ = 16  # distinct q / dO chunk buffers (K/V are distinct for every chunk)
 
-    def __init__(self, cfg, seed: int, device, comm=None):
+    def __init__(self, cfg, seed: int, device, layer=None):
         import torch
         from paper_2602_02108_b200 import ModelConfig, PagedCache
         from paper_2602_02108_b200 import attention as A
@@ -220,7 +220,11 @@ class Run:
         self.S, self.m = T // C, C // P
         self.mc = ModelConfig(n_layers=1, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=hd, chunk_size=C, page_size=P,
                               retrieval_budget=cfg["budget"], attention_mode=[cfg["mode"]])
-        self.cache = PagedCache(self.mc, dtype="bf16", max_tokens=T)
+        # a rank of a split sequence (sharding.ShardedLayer): its KV groups' heads, and K/V + gradient
+        # storage only for its page range's pages
+        self.layer = layer
+        self.cache = (PagedCache(self.mc, dtype="bf16", max_tokens=T) if layer is None else
+                      layer.attach(layer.plan.make_cache(layer.cfg, dtype="bf16", max_tokens=T)))
         g = torch.Generator(device=device).manual_seed(seed)
         bf = torch.bfloat16
         self.k_all = torch.randn(T, Hkv, hd, device=device, generator=g).to(bf)
@@ -235,11 +239,22 @@ class Run:
         self.grads = A.AttnGrads(torch.empty(C, Hq, hd, device=device), torch.empty(C, Hkv, hd, device=device),
                                  torch.empty(C, Hkv, hd, device=device))
         self.own = [np.arange(i * self.m, (i + 1) * self.m, dtype=np.int32) for i in range(self.S)]
-        # KV-group sharding (--shard kv): this rank holds Hkv of the model's KV groups; the page vote
-        # sums over every rank's groups (per-group partial votes, NCCL all-gather in group order)
-        self.comm = comm
-        if comm is not None:
+        if layer is not None:
+            # per-group partial votes (exchanged over the ranks of the same page range), the owned part
+            # of each selection, partial (O, LSE) buffers per attention stream and a ring of two flat
+            # [dq | dk | dv] buffers whose ordered reduction overlaps the next chunk's backward
             self.parts = torch.empty(Hkv * self.m * max(T // P, 1), device=device, dtype=torch.float32)
+            self.subs = [A.Selection(self.cache, self.m, kmax) for _ in range(self.S)]
+            self.o_part = [torch.empty(C, Hq, hd, device=device, dtype=bf) for _ in range(2)]
+            self.lse_part = [torch.empty(C, Hq, device=device, dtype=torch.float32) for _ in range(2)]
+            n_flat = C * Hq * hd + 2 * C * Hkv * hd
+            self.flat = [torch.empty(n_flat, device=device) for _ in range(2)]
+            self.flat_grads = [A.AttnGrads(f[:C * Hq * hd].view(C, Hq, hd),
+                                           f[C * Hq * hd:C * Hq * hd + C * Hkv * hd].view(C, Hkv, hd),
+                                           f[C * Hq * hd + C * Hkv * hd:].view(C, Hkv, hd)) for f in self.flat]
+            self.comm_stream = torch.cuda.Stream(device=device)
+            self.ev_part = [None, None]   # merge that last read o_part[b]
+            self.ev_flat = [None, None]   # reduction that last used flat[b]
         self.fwd_phase = []  # (start, end) CUDA events of every step's forward pass
         self.bwd_phase = []  # and of its backward pass
 
@@ -247,15 +262,9 @@ class Run:
         from paper_2602_02108_b200._lib import call
         from paper_2602_02108_b200.paged_kv import stream_handle
         n_cand = i * self.m
-        if self.cfg["mode"] == "topk" and n_cand > 0 and self.comm is not None:
-            from paper_2602_02108_b200.paged_kv import _ptr
-            n, g = min(n_cand, self.cache.n_pages(0)), self.cfg["Hkv"]
-            parts = self.parts[: g * self.m * n].view(g, self.m, n)
-            call("oomb_score_pages_partial", self.cache.handle, 0, _ptr(q), q.shape[0], n, _ptr(parts),
-                 stream_handle(stream))
-            vote = self.comm.vote_allgather(parts, stream=stream, out=self.vote[: self.m * n].view(self.m, n))
-            call("oomb_select_topk", self.sels[i].handle, _ptr(vote), self.m, n, self.cfg["budget"] // self.cfg["P"],
-                 stream_handle(stream))
+        if self.layer is not None:
+            self.layer.select(i, q, self.sels[i], self.subs[i], vote_buf=self.vote, parts_buf=self.parts,
+                              stream=stream)
         elif self.cfg["mode"] == "topk" and n_cand > 0:
             self.A.select_pages_topk(self.cache, 0, q, n_cand, stream=stream, out=self.sels[i], vote=self.vote)
         else:  # dense (select_all) or no candidates yet (chunk_trainer.hpp:297-304)
@@ -264,15 +273,64 @@ class Run:
     def fwd_chunk(self, i, q, k, v, out=None, stream=None):
         self._select(i, q, stream)
         self.cache.append_chunk(0, k, v, stream=stream)
-        return self.A.attn_forward(self.mc, q, self.cache, 0, self.sels[i], k, v, stream=stream,
-                                   out=self.o_all[i] if out is None else out, lse=self.lse_all[i])
+        return self.attend(i, q, k, v, stream, out=self.o_all[i] if out is None else out)
+
+    def attend(self, i, q, k, v, stream, out=None):
+        """Chunk i's attention forward on `stream`; on a page-range shard the partial (O, LSE) of the
+        rank's pages is merged over its range group on the comm stream (writes o_all[i] / lse_all[i])."""
+        torch = self.torch
+        out = self.o_all[i] if out is None else out
+        if self.layer is None or not self.layer.split_pages:
+            sel = self.sels[i] if self.layer is None else self.subs[i]
+            return self.A.attn_forward(self.mc, q, self.cache, 0, sel, k, v, stream=stream, out=out,
+                                       lse=self.lse_all[i])
+        b = i & 1
+        st = stream if stream is not None else torch.cuda.current_stream()
+        if self.ev_part[b] is not None:
+            st.wait_event(self.ev_part[b])  # the merge that last read this partial buffer is done
+        part = self.A.attn_forward(self.mc, q, self.cache, 0, self.subs[i], k, v, stream=st, out=self.o_part[b],
+                                   lse=self.lse_part[b], past_only=self.layer.plan.range_idx != 0)
+        cs = self.comm_stream
+        cs.wait_stream(st)
+        self.layer.range_comm.lse_merge(part.out, part.lse, stream=cs, out=out, lse=self.lse_all[i])
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        self.ev_part[b] = ev
+        return self.A.AttnSaved(out, self.lse_all[i], self.subs[i])
 
     def bwd_chunk(self, i, do, q, k, v, grads=None, stream=None, defer_dq=False):
+        torch = self.torch
+        if self.layer is not None and self.layer.split_pages:
+            # page-range shard: backward into a ring buffer, then the ordered reduction of
+            # [dq | dk_cur | dv_cur] over the range group on the comm stream (it waits for the deferred dQ)
+            b = i & 1
+            st = stream if stream is not None else torch.cuda.current_stream()
+            if self.ev_flat[b] is not None:
+                st.wait_event(self.ev_flat[b])
+            g = self.flat_grads[b]
+            saved = self.A.AttnSaved(self.o_all[i], self.lse_all[i], self.subs[i])
+            self.A.attn_backward(self.mc, do, q, self.cache, 0, k, v, saved, stream=st, grads=g,
+                                 defer_dq=defer_dq, past_only=self.layer.plan.range_idx != 0)
+            self.cache.accumulate_grad_pages(0, self.own[i], g.dk_cur, g.dv_cur, stream=st)
+            cs = self.comm_stream
+            cs.wait_stream(st)
+            if defer_dq:
+                self.A.join_dq(self.cache, cs)
+            self.layer.range_comm.allreduce_ordered(self.flat[b], stream=cs, out=self.flat[b])
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            self.ev_flat[b] = ev
+            return g
         g = self.grads if grads is None else grads
-        saved = self.A.AttnSaved(self.o_all[i], self.lse_all[i], self.sels[i])
+        sel = self.sels[i] if self.layer is None else self.subs[i]
+        saved = self.A.AttnSaved(self.o_all[i], self.lse_all[i], sel)
         self.A.attn_backward(self.mc, do, q, self.cache, 0, k, v, saved, stream=stream, grads=g, defer_dq=defer_dq)
         self.cache.accumulate_grad_pages(0, self.own[i], g.dk_cur, g.dv_cur, stream=stream)
         return g
+
+    def join_comm(self, stream):
+        if self.layer is not None and self.layer.split_pages:
+            stream.wait_stream(self.comm_stream)
 
     def forward_pass(self):
         """All chunks' [select -> append -> attend], with chunk i+1's page selection (score + top-k,
@@ -308,11 +366,11 @@ class Run:
             if ast is not comp:
                 ast.wait_event(self.ev_app[i & 1])
             ast.wait_event(self.ev_sel[i & 1])
-            self.A.attn_forward(self.mc, q, self.cache, 0, self.sels[i], k, v, stream=ast, out=self.o_all[i],
-                                lse=self.lse_all[i])
+            self.attend(i, q, k, v, ast)
         for st in getattr(self, "att_streams", []):
             comp.wait_stream(st)
         comp.wait_stream(ss)
+        self.join_comm(comp)
 
     def step(self):
         torch, C = self.torch, self.cfg["C"]
@@ -330,6 +388,7 @@ class Run:
                            self.v_all[i * C:(i + 1) * C], defer_dq=BWD_DEFER)
         if BWD_DEFER:
             self.A.join_dq(self.cache, comp)
+        self.join_comm(comp)
         b1.record(comp)
         self.fwd_phase.append((f0, b0))
         self.bwd_phase.append((b0, b1))
@@ -425,16 +484,17 @@ class E2E:
             ast = self.att[i % len(self.att)]
             ast.wait_event(ev_app[b])
             ast.wait_event(ev_sel[b])  # (the selection read qd[b] too: ev_used below covers it)
-            r.A.attn_forward(r.mc, self.qd[b], r.cache, 0, r.sels[i], self.kd[b], self.vd[b], stream=ast,
-                             out=r.o_all[i], lse=r.lse_all[i])
+            r.attend(i, self.qd[b], self.kd[b], self.vd[b], ast)
             ev_used[b].record(ast)
             with torch.cuda.stream(self.d2h):
                 self.d2h.wait_event(ev_used[b])
+                r.join_comm(self.d2h)  # a page-range shard's merged out is written on the comm stream
                 self.out_h[b].copy_(r.o_all[i], non_blocking=True)
                 ev_out[b].record(self.d2h)
             d2h_b += 2 * r.o_all[i].numel()
         for st in self.att:
             comp.wait_stream(st)
+        r.join_comm(comp)
 
         def load_bwd(i):
             nonlocal h2d_b
@@ -464,6 +524,7 @@ class E2E:
                 self.d2h.wait_event(ev_used[b])
                 if BWD_DEFER:
                     r.A.join_dq(r.cache, self.d2h)  # dq(i) ran on the library's side stream
+                r.join_comm(self.d2h)  # a page-range shard reduces its grads on the comm stream
                 self.dq_h[b].copy_(g.dq, non_blocking=True)
                 self.dk_h[b].copy_(g.dk_cur, non_blocking=True)
                 self.dv_h[b].copy_(g.dv_cur, non_blocking=True)
@@ -471,6 +532,7 @@ class E2E:
             d2h_b += 4 * (g.dq.numel() + 2 * g.dk_cur.numel())
         if BWD_DEFER:
             r.A.join_dq(r.cache, comp)
+        r.join_comm(comp)
         comp.wait_stream(self.d2h)
         self.h2d_bytes, self.d2h_bytes = h2d_b, d2h_b
 
@@ -552,9 +614,15 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-workers", type=int, default=None)
     ap.add_argument("--tokens", type=int, default=None, help="override the context length (debug)")
-    ap.add_argument("--shard", default="replica", choices=["replica", "kv"],
-                    help="replica: every rank runs its own sequence (weak scaling, the default); kv: one sequence "
-                         "split across the ranks by KV-head group, page votes all-gathered over NCCL (strong scaling)")
+    ap.add_argument("--shard", default="auto",
+                    help="auto (default): at N > 1 ONE sequence is split across the ranks by KV-head group and, "
+                         "when the groups run out, by page range (sharding.ShardPlan: Qwen 8 GPUs = 4 x 2; strong "
+                         "scaling); kv | range | kv+range | KxR: that split explicitly; replica: every rank runs its "
+                         "own sequence (weak scaling)")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "torch"],
+                    help="exchange steps over liboomb_comm.so (NCCL, default) or torch.distributed (gloo, CUDA "
+                         "tensors staged through the host: lets several ranks share one GPU in tests)")
+    ap.add_argument("--same-device", action="store_true", help="every rank on cuda:0 (tests; with --comm torch)")
     ap.add_argument("--offload-cap", type=float, default=0.75,
                     help="device capacity (fraction of the layer's pages) of the offload measurement; 0 = skip")
     args = ap.parse_args()
@@ -564,12 +632,19 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     chunks = workload(cfg)
+    # one sequence split across the ranks (the north-star partition) unless replicas are asked for;
+    # at N = 1 "auto" is the unsplit layer
+    sharded = args.shard != "replica" and (world > 1 or args.shard != "auto")
+    plan = None
+    if sharded:
+        from paper_2602_02108_b200.sharding import ShardPlan
+        plan = ShardPlan(rank, world, cfg["Hkv"], cfg["Hq"], args.shard)
     base_config = {"workload": f"{args.config}: {cfg['desc']}", "context_tokens": cfg["T"],
                    "chunk": cfg["C"], "page": cfg["P"], "q_heads": cfg["Hq"], "kv_heads": cfg["Hkv"],
                    "head_dim": cfg["hd"], "selection": cfg["mode"],
                    "pages_per_query_page": cfg["budget"] // cfg["P"] if cfg["mode"] == "topk" else "all",
                    "layers_per_step": 1,
-                   "parallelism": (f"one sequence split by KV-head group over {world} GPU(s)" if args.shard == "kv"
+                   "parallelism": (plan.describe() if sharded
                                    else f"{world} independent replica(s), one sequence each")}
 
     if args.impl == "reference":
@@ -594,8 +669,8 @@ def main():
     if world > 1:
         import torch.distributed as dist
         local = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(0 if args.same_device else local)
+        dist.init_process_group("nccl" if args.comm == "nccl" else "gloo")
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -612,16 +687,26 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
-    comm = None
     run_cfg = cfg
-    if args.shard == "kv":
-        from paper_2602_02108_b200.sharding import KVGroupShard, OombComm
-        sh = KVGroupShard(rank, world, cfg["Hkv"], cfg["Hq"])  # raises when the groups do not divide
-        comm = (OombComm.from_process_group() if world > 1
-                else OombComm(0, 1, dev.index, OombComm.unique_id()))
-        run_cfg = dict(cfg, Hq=cfg["Hq"] // world, Hkv=sh.kv_local)
-        args.no_e2e, args.no_cpu, args.offload_cap = True, True, 0.0  # the sharded line is throughput only
-    run = Run(run_cfg, seed=1234 + rank, device=dev, comm=comm)
+    layer = None
+    if sharded:
+        from paper_2602_02108_b200 import ModelConfig
+        from paper_2602_02108_b200.sharding import OombComm, ShardedLayer, TorchComm
+        kv_g, rg = plan.new_groups() if world > 1 else (None, None)
+
+        def make_comm(group, size):
+            if size <= 1:
+                return None
+            return OombComm.from_process_group(group) if args.comm == "nccl" else TorchComm(group)
+
+        gcfg = ModelConfig(n_layers=1, n_q_heads=cfg["Hq"], n_kv_heads=cfg["Hkv"], head_dim=cfg["hd"],
+                           chunk_size=cfg["C"], page_size=cfg["P"], retrieval_budget=cfg["budget"],
+                           attention_mode=[cfg["mode"]])
+        layer = ShardedLayer(plan, gcfg, None, make_comm(kv_g, plan.kv_world), make_comm(rg, plan.range_world))
+        run_cfg = dict(cfg, Hq=cfg["Hq"] // plan.kv_world, Hkv=cfg["Hkv"] // plan.kv_world)
+        args.offload_cap = 0.0  # the offload regime is a one-GPU, unsplit measurement
+    # the ranks of one page-range group hold the same heads: they must see the same q / k / v / dO
+    run = Run(run_cfg, seed=1234 + (plan.kv_idx if sharded else rank), device=dev, layer=layer)
     for _ in range(args.warmup):
         run.step()
     torch.cuda.synchronize()
@@ -650,7 +735,7 @@ def main():
     prof = run.cache.profile_collect()
     run.cache.profile_enable(False)
     ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    seqs = 1 if args.shard == "kv" else world  # sequences processed by the whole job per step
+    seqs = 1 if sharded else world  # sequences processed by the whole job per step
     value = seqs * cfg["T"] / (ms_step / 1e3)
 
     # ---- e2e: same API from pinned host buffers
@@ -667,7 +752,7 @@ def main():
         f1.record()
         torch.cuda.synchronize()
         ms_e2e = max_over_ranks(f0.elapsed_time(f1) / args.steps)
-        e2e = {"value": world * cfg["T"] / (ms_e2e / 1e3), "unit": "tokens/s", "ms_per_step": ms_e2e,
+        e2e = {"value": seqs * cfg["T"] / (ms_e2e / 1e3), "unit": "tokens/s", "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": ee.h2d_bytes, "d2h_bytes_per_step": ee.d2h_bytes}
 
     offload = None
@@ -683,9 +768,9 @@ def main():
     peak, peak_sus, hbm, peak_src = peaks()
     fwd_fl = sum(c["fwd"] for c in chunks)
     bwd_fl = sum(c["bwd"] for c in chunks)
-    # per-GPU algorithmic TFLOP/s: a kv shard does 1/world of the sequence's heads
-    tflops = (fwd_fl + bwd_fl) / (ms_step / 1e3) / 1e12 / (world if args.shard == "kv" else 1)
-    if args.shard == "kv":
+    # per-GPU algorithmic TFLOP/s: a shard of a split sequence does 1/world of its work
+    tflops = (fwd_fl + bwd_fl) / (ms_step / 1e3) / 1e12 / (world if sharded else 1)
+    if sharded:
         fwd_fl, bwd_fl = fwd_fl / world, bwd_fl / world
     kernels = {}
     for k, (n, ms) in prof.items():
@@ -750,7 +835,7 @@ def main():
                 "traffic_source": traffic["source"] if traffic else None}
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if args.shard == "kv" else "weak",
+            "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic N(0,1) bf16 q/k/v/dO generated on device (1M-token K/V distinct per chunk; "
                     "16 distinct q/dO chunks cycled); random-init, no checkpoint",
@@ -768,8 +853,24 @@ def main():
                         "included: an upper bound)" if FWD_STREAMS > 1 else
                         "full train step of SURVEY 3.2: 2 forwards (phase A + recompute) + 1 backward per chunk; "
                         "the recompute forward is the same forward kernel, timed above",
-                "tokens_per_s": world * cfg["T"] / ((ms_step + t_fwd) / 1e3),
+                "tokens_per_s": seqs * cfg["T"] / ((ms_step + t_fwd) / 1e3),
                 "ms_per_step": ms_step + t_fwd}}
+    if sharded:
+        from paper_2602_02108_b200.sharding import comm_bytes
+        g_loc, m_q = run_cfg["Hkv"], cfg["C"] // cfg["P"]
+        n_last = chunks[-1]["n_cand"]
+        line["sharding"] = {
+            "kv_world": plan.kv_world, "range_world": plan.range_world, "comm": args.comm,
+            "pool_pages_per_rank": (cfg["T"] // cfg["P"] + plan.range_world - 1) // plan.range_world,
+            "layer_pages": cfg["T"] // cfg["P"],
+            "bytes_sent_per_rank_per_chunk": {
+                **layer.comm_bytes_per_chunk(),
+                "vote_allgather_bytes_last_chunk": (comm_bytes(0, plan.kv_world, g_loc * m_q * n_last, 4)[0]
+                                                    if cfg["mode"] == "topk" else 0)},
+            "note": "vote exchanged over the ranks of one page range (all-gather, then a fixed-order sum); "
+                    "(O, LSE) merge and the [dq | dk_cur | dv_cur] reduction over the ranks of one KV group "
+                    "(ordered reduce-scatter by row slices + all-gather of the slices; *_allgather = the "
+                    "all-gather-then-combine bytes they replace)"}
     if not args.no_cpu and world == 1:  # rank 0 at N = 1 only (the reference arm covers every N)
         try:
             line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_workers)

@@ -67,6 +67,15 @@ typedef struct {
     int dtype;            /* oomb_dtype of the KV pool and the attention inputs */
     int64_t max_tokens;   /* per-layer capacity of the device page table */
     int64_t device_capacity_pages; /* KV page slots on the device, all layers; <= 0: n_layers*max_pages */
+    /* Page-range shard ownership (appended fields, zero = off). With page_owner_stride
+     * R > 1 this pool stores K/V and gradients only for the pages with id % R == page_owner_rank.
+     * Every other page is REMOTE (tier 2): append still adds its rows to the page's K_avg sums
+     * (pinned metadata, replicated on every shard, so every shard scores every candidate) but
+     * stores no K/V, and any read of a REMOTE page raises OOMB_RESIDENCY_ERROR. The arena ids of
+     * the reference page table are still assigned for every page. device_capacity_pages <= 0 then
+     * defaults to the owned share, n_layers * ceil(max_pages / R): per-shard HBM is 1/R. */
+    int page_owner_stride;
+    int page_owner_rank;
 } oomb_config;
 
 typedef struct {
@@ -140,7 +149,11 @@ OOMB_API int oomb_gather_pages(oomb_pool_t pool, int layer, const int32_t* ids_h
 /* PagedCache::scatter_add_grads  paged_kv.hpp:135-164. dk/dv fp32 [n*P][Hkv][hd] device. */
 OOMB_API int oomb_scatter_add_grads(oomb_pool_t pool, int layer, const int32_t* ids_host, int n, const float* dk,
                            const float* dv, void* stream);
-/* Tier tags and residency enforcement  paged_kv.hpp:199-211. */
+/* Tier tags and residency enforcement  paged_kv.hpp:199-211. Tiers: 0 device, 1 host (the
+ * reference's two), 2 remote (owned by another page-range shard), 3 lost (a host-tier page whose
+ * pinned copy was dropped when a real offload engine detached without room to restore it).
+ * Pages in tiers 2 and 3 cannot be re-tagged, and reading them always raises
+ * OOMB_RESIDENCY_ERROR, enforcement or not. */
 OOMB_API int oomb_set_tier(oomb_pool_t pool, int layer, int page, int tier);
 OOMB_API int oomb_get_tier(oomb_pool_t pool, int layer, int page, int* tier);
 OOMB_API int oomb_set_residency_enforced(oomb_pool_t pool, int on);
@@ -161,6 +174,12 @@ OOMB_API int oomb_selection_device(oomb_selection_t sel, const int32_t** offsets
 /* select_all / select_recent  attention.hpp:99-111, broadcast to m query pages (chunk_trainer.hpp:301-304). */
 OOMB_API int oomb_select_all(oomb_selection_t sel, int n_pages, int m, void* stream);
 OOMB_API int oomb_select_recent(oomb_selection_t sel, int n_pages, int window, int m, void* stream);
+/* Page-range shard: dst = the part of src this pool owns (ids with
+ * id % page_owner_stride == page_owner_rank, each list's order kept), built on the device; the
+ * host mirror follows asynchronously, as select_topk's does. A pool that owns every page copies. */
+OOMB_API int oomb_selection_filter_owned(oomb_pool_t pool, oomb_selection_t src, oomb_selection_t dst, void* stream);
+/* The pool's ownership (stride 1 / rank 0 when it owns every page). */
+OOMB_API int oomb_page_owner(oomb_pool_t pool, int* stride, int* rank);
 /* select_topk_row per row of a device vote matrix [m][n] fp32  attention.hpp:71-96:
  * k largest, ties to the lower id, ascending; k >= n -> all; k < 0 -> SHAPE_ERROR. */
 OOMB_API int oomb_select_topk(oomb_selection_t sel, const float* vote, int m, int n, int k, void* stream);

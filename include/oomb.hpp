@@ -313,8 +313,9 @@ public:
     // dtype: bf16 (the tcgen05 path) or f32 (1e-5 parity path). max_tokens: per-layer capacity of
     // the device page table (default 64 chunks). device_capacity_pages: KV page slots on the device
     // for all layers (default: every page resident; a TieredEngine offloads beyond it).
+    // page_owner_stride / page_owner_rank: a page-range shard (oomb_config); 0 = every page.
     explicit PagedCache(const ModelConfig& cfg, DType dtype = DType::bf16, int64_t max_tokens = -1, int device = 0,
-                        int64_t device_capacity_pages = -1)
+                        int64_t device_capacity_pages = -1, int page_owner_stride = 0, int page_owner_rank = 0)
         : cfg_(cfg), dtype_(dtype) {
         cfg.validate();
         if (dtype != DType::bf16 && dtype != DType::f32) throw ConfigError("PagedCache: dtype must be bf16 or f32");
@@ -322,7 +323,7 @@ public:
                       cfg.head_dim,       cfg.chunk_size,   cfg.page_size,
                       cfg.retrieval_budget, cfg.local_window, cfg.score_scale ? 1 : 0,
                       static_cast<int>(dtype), max_tokens > 0 ? max_tokens : 64LL * cfg.chunk_size,
-                      device_capacity_pages};
+                      device_capacity_pages, page_owner_stride, page_owner_rank};
         check(oomb_pool_create(&c, device, &pool_));
     }
     ~PagedCache() {

@@ -55,6 +55,20 @@ OOMB_API int oomb_lse_merge_allgather(oomb_comm_t comm, const void* o_part, cons
 /* dq = sum_r dq_part_r in rank order (fp32, count elements). */
 OOMB_API int oomb_dq_reduce(oomb_comm_t comm, const float* dq_part, int64_t count, float* dq, void* stream);
 
+/* Proportional variants (each rank moves ~2x the tensor instead of (world-1)x), bitwise equal to the
+ * all-gather ones above: the tensor is cut into `world` contiguous row slices; rank s receives slice
+ * s of every rank (grouped ncclSend / ncclRecv), combines it in rank order, and broadcasts the
+ * combined slice back in place (grouped ncclBroadcast).
+ *   oomb_allreduce_ordered: out = sum_r part_r, per element in rank order (dQ, dk_cur / dv_cur of a
+ *                           page-range group). out may alias part.
+ *   oomb_lse_merge_ordered: the exact (O, LSE) merge of oomb_lse_merge_allgather. */
+OOMB_API int oomb_allreduce_ordered(oomb_comm_t comm, const float* part, int64_t count, float* out, void* stream);
+OOMB_API int oomb_lse_merge_ordered(oomb_comm_t comm, const void* o_part, const float* lse_part, int64_t rows, int hd,
+                                    int dtype, void* out, float* lse, void* stream);
+/* Per-rank wire bytes of one exchange of `elems` elements of `elem_bytes` (op 0 = all-gather +
+ * local sum, op 1 = the ordered reduce-scatter + all-gather above), for reports. */
+OOMB_API int oomb_comm_bytes(int op, int world, int64_t elems, int64_t elem_bytes, int64_t* sent, int64_t* received);
+
 #ifdef __cplusplus
 }
 #endif

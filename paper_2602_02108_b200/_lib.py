@@ -22,7 +22,7 @@ class OombConfig(C.Structure):
         ("n_layers", C.c_int), ("n_q_heads", C.c_int), ("n_kv_heads", C.c_int), ("head_dim", C.c_int),
         ("chunk_size", C.c_int), ("page_size", C.c_int), ("retrieval_budget", C.c_int), ("local_window", C.c_int),
         ("score_scale", C.c_int), ("dtype", C.c_int), ("max_tokens", C.c_int64),
-        ("device_capacity_pages", C.c_int64),
+        ("device_capacity_pages", C.c_int64), ("page_owner_stride", C.c_int), ("page_owner_rank", C.c_int),
     ]
 
 
@@ -71,6 +71,8 @@ _PROTOS = {
     "oomb_select_all": [VP, I, I, VP],
     "oomb_select_recent": [VP, I, I, I, VP],
     "oomb_select_topk": [VP, VP, I, I, I, VP],
+    "oomb_selection_filter_owned": [VP, VP, VP, VP],
+    "oomb_page_owner": [VP, C.POINTER(I), C.POINTER(I)],
     "oomb_score_pages": [VP, I64, I, I, VP, I64, I, I, I, I, VP, VP],
     "oomb_select_pages_topk": [VP, I, VP, I64, I, VP, VP, VP],
     "oomb_attn_forward": [VP, I, VP, I64, VP, VP, VP, VP, VP, VP],
@@ -161,6 +163,9 @@ _COMM_PROTOS = {
     "oomb_vote_allgather": [VP, VP, I, I64, I64, VP, VP],
     "oomb_lse_merge_allgather": [VP, VP, VP, I64, I, I, VP, VP, VP],
     "oomb_dq_reduce": [VP, VP, I64, VP, VP],
+    "oomb_allreduce_ordered": [VP, VP, I64, VP, VP],
+    "oomb_lse_merge_ordered": [VP, VP, VP, I64, I, I, VP, VP, VP],
+    "oomb_comm_bytes": [I, I, I64, I64, C.POINTER(I64), C.POINTER(I64)],
 }
 _comm = None
 

@@ -53,6 +53,14 @@ class Selection:
         s._keep = (off, ids)
         return s
 
+    def filter_owned(self, out: "Selection | None" = None, stream=None) -> "Selection":
+        """The part of this selection the cache's page-range shard owns (list order kept), built on
+        the device (oomb_selection_filter_owned); `out` is reused when given."""
+        m, nnz = C.c_int(), C.c_int()
+        dst = out if out is not None else Selection(self.cache, max(len(self), 1), max(self.max_ids, 1))
+        call("oomb_selection_filter_owned", self.cache.handle, self.handle, dst.handle, stream_handle(stream))
+        return dst
+
     def csr(self) -> tuple[np.ndarray, np.ndarray]:
         """(offsets [m+1], ids [nnz]) int32 from the host mirror (waits for the selection's D2H)."""
         m, nnz = C.c_int(), C.c_int()

@@ -76,7 +76,7 @@ template <typename T>
 __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, int64_t rows, int64_t filled,
                               int P, int Hkv, int hd, int first_page, NewSlots ns, int32_t* __restrict__ kvslot,
                               T* __restrict__ kpool, T* __restrict__ vpool, float* __restrict__ ksum,
-                              int32_t* __restrict__ kcnt, const double* __restrict__ rope_inv_freq) {
+                              int32_t* __restrict__ kcnt, int* err, const double* __restrict__ rope_inv_freq) {
     const int re = Hkv * hd;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     const int pg = first_page + blockIdx.y;
@@ -90,10 +90,14 @@ __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, 
     const int64_t s0 = max(filled, static_cast<int64_t>(pg) * P);
     const int64_t s1 = min(filled + rows, static_cast<int64_t>(pg + 1) * P);
     float sum = is_new ? 0.f : ksum[static_cast<int64_t>(pg) * re + e];
+    // a REMOTE page (another page-range shard stores it) only gets its K_avg sums; a page with no
+    // slot at all is not resident (the host checks the tail page first): flag it, write nothing
+    const bool store = slot >= 0;
+    if (slot == -1 && e == 0) atomicOr(err, DERR_NOT_RESIDENT);
     // rows in batches of 16: all loads of a batch are issued before its stores and the
     // in-order (append order, paged_kv.hpp:98-104) fp32 sum, so 32 loads are in flight per thread
     constexpr int kB = 16;
-    const size_t dst0 = ((static_cast<size_t>(slot) * Hkv + h) * P) * hd + d;
+    const size_t dst0 = ((static_cast<size_t>(store ? slot : 0) * Hkv + h) * P) * hd + d;
     for (int64_t sb = s0; sb < s1; sb += kB) {
         T kb[kB], vb[kB];
 #pragma unroll
@@ -112,8 +116,10 @@ __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, 
         for (int u = 0; u < kB; ++u) {
             if (sb + u < s1) {
                 const int off = static_cast<int>(sb + u - static_cast<int64_t>(pg) * P);
-                kpool[dst0 + static_cast<size_t>(off) * hd] = kb[u];
-                vpool[dst0 + static_cast<size_t>(off) * hd] = vb[u];
+                if (store) {
+                    kpool[dst0 + static_cast<size_t>(off) * hd] = kb[u];
+                    vpool[dst0 + static_cast<size_t>(off) * hd] = vb[u];
+                }
                 sum = __fadd_rn(sum, to_f(kb[u]));
             }
         }
@@ -124,8 +130,8 @@ __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, 
 
 void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_t filled_before, int P, int Hkv,
                    int hd, int first_page, int n_pages_touched, const NewSlots& ns, int32_t* d_kvslot_layer,
-                   void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, cudaStream_t st,
-                   const double* rope_inv_freq) {
+                   void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, int* d_err,
+                   cudaStream_t st, const double* rope_inv_freq) {
     if (rows <= 0 || n_pages_touched <= 0) return;
     ProfScope prof_(PK_APPEND, st);
     const int re = Hkv * hd;
@@ -134,13 +140,63 @@ void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_
         append_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(
             static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), rows, filled_before, P, Hkv,
             hd, first_page, ns, d_kvslot_layer, static_cast<__nv_bfloat16*>(kpool), static_cast<__nv_bfloat16*>(vpool),
-            kavg_sum_layer, kavg_cnt_layer, rope_inv_freq);
+            kavg_sum_layer, kavg_cnt_layer, d_err, rope_inv_freq);
     else
         append_kernel<float><<<grid, 128, 0, st>>>(static_cast<const float*>(k), static_cast<const float*>(v), rows,
                                                    filled_before, P, Hkv, hd, first_page, ns, d_kvslot_layer,
                                                    static_cast<float*>(kpool), static_cast<float*>(vpool),
-                                                   kavg_sum_layer, kavg_cnt_layer, rope_inv_freq);
+                                                   kavg_sum_layer, kavg_cnt_layer, d_err, rope_inv_freq);
     check_launch("append_kernel");
+}
+
+// ===========================================================================
+// Page-range shard sub-selection: keep the ids a shard owns (id % stride == rank), list order
+// kept. One CTA walks the query pages in order, compacting 1,024 ids per pass with warp ballots.
+// ===========================================================================
+__global__ void __launch_bounds__(1024) filter_owned_kernel(const int32_t* __restrict__ src_off,
+                                                            const int32_t* __restrict__ src_ids, int m, int stride,
+                                                            int rank, int32_t* __restrict__ dst_off,
+                                                            int32_t* __restrict__ dst_ids) {
+    __shared__ int warp_base[33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int out = 0;
+    for (int qp = 0; qp < m; ++qp) {
+        if (threadIdx.x == 0) dst_off[qp] = out;
+        const int b = src_off[qp], e = src_off[qp + 1];
+        for (int base = b; base < e; base += blockDim.x) {
+            const int i = base + threadIdx.x;
+            int id = 0;
+            bool keep = false;
+            if (i < e) {
+                id = src_ids[i];
+                keep = id % stride == rank;
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (lane == 0) warp_base[warp] = __popc(bal);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int acc = 0;
+                for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+                    const int c = warp_base[w];
+                    warp_base[w] = acc;
+                    acc += c;
+                }
+                warp_base[32] = acc;
+            }
+            __syncthreads();
+            if (keep) dst_ids[out + warp_base[warp] + __popc(bal & ((1u << lane) - 1u))] = id;
+            out += warp_base[32];
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) dst_off[m] = out;
+}
+
+void launch_filter_owned(const int32_t* src_off, const int32_t* src_ids, int m, int stride, int rank,
+                         int32_t* dst_off, int32_t* dst_ids, cudaStream_t st) {
+    ProfScope prof_(PK_OTHER, st);
+    filter_owned_kernel<<<1, 1024, 0, st>>>(src_off, src_ids, m, stride, rank, dst_off, dst_ids);
+    check_launch("filter_owned_kernel");
 }
 
 // ===========================================================================

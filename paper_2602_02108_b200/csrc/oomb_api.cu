@@ -174,6 +174,10 @@ void sel_host_sync(oomb_selection_s* s) {
         OOMB_CUDA(cudaEventSynchronize(s->ev));
         s->host_pending = false;
     }
+    if (s->nnz_from_host) {
+        s->nnz = s->h_off[s->m];
+        s->nnz_from_host = false;
+    }
 }
 
 // Lazy grad pages for every list of the selection, reference order (qp asc, list order).
@@ -304,7 +308,13 @@ int oomb_pool_create(const oomb_config* cfg, int device, oomb_pool_t* out) {
             p->elem = c.dtype == OOMB_BF16 ? 2 : 4;
             p->page_elems = static_cast<int64_t>(c.page_size) * c.n_kv_heads * c.head_dim;
             p->pt = new PageTable(c.n_layers, c.page_size, c.n_kv_heads, c.head_dim, p->elem, 4);
-            p->n_kv_slots = c.device_capacity_pages > 0 ? c.device_capacity_pages : c.n_layers * p->max_pages;
+            OOMB_REQUIRE(c.page_owner_stride >= 0 && (c.page_owner_stride <= 1 ||
+                                                     (c.page_owner_rank >= 0 && c.page_owner_rank < c.page_owner_stride)),
+                         OOMB_CONFIG_ERROR, "page_owner_rank must be in [0, page_owner_stride)");
+            p->owner_stride = std::max(1, c.page_owner_stride);
+            p->owner_rank = p->owner_stride > 1 ? c.page_owner_rank : 0;
+            const int64_t owned_pages = (p->max_pages + p->owner_stride - 1) / p->owner_stride;
+            p->n_kv_slots = c.device_capacity_pages > 0 ? c.device_capacity_pages : c.n_layers * owned_pages;
             p->n_g_slots = p->n_kv_slots;
             // FIFO (pool.h): slot 0 is handed out first.
             for (int64_t i = 0; i < p->n_kv_slots; ++i) p->kv_free.push_back(static_cast<int32_t>(i));
@@ -441,11 +451,32 @@ static int append_impl(oomb_pool_t p, int layer, const void* k, const void* v, i
         int64_t b, e;
         int first_new, n_new;
         const int64_t filled0 = p->pt->filled[layer];
+        if (rows > 0 && filled0 % P != 0) {  // rows land in the partly filled tail page: it must be here
+            const int tail = static_cast<int>(filled0 / P);
+            const uint8_t t = p->pt->pages[layer][tail].tier;
+            OOMB_REQUIRE(t == TIER_REMOTE || (t == TIER_DEVICE && p->kvslot[layer][tail] >= 0), OOMB_RESIDENCY_ERROR,
+                         "append_chunk: the partly filled tail page " + std::to_string(tail) + " of layer " +
+                             std::to_string(layer) + " is not device-resident (fetch it before appending)");
+        }
+        {  // every new page this shard stores needs a free slot: check before touching the page table
+            const int64_t n_before = static_cast<int64_t>(p->pt->pages[layer].size());
+            const int64_t last = rows > 0 ? (filled0 + rows - 1) / P : n_before - 1;
+            int64_t need = 0;
+            for (int64_t pg = n_before; pg <= last; ++pg) need += p->owns(pg);
+            OOMB_REQUIRE(need <= static_cast<int64_t>(p->kv_free.size()), OOMB_CONFIG_ERROR,
+                         "device KV page capacity exhausted (raise device_capacity_pages or offload)");
+        }
         p->pt->append(layer, rows, &b, &e, &first_new, &n_new);
         for (int i = 0; i < n_new; ++i) {
+            const int pg = first_new + i;
+            if (!p->owns(pg)) {  // another page-range shard stores it; K_avg sums are kept here too
+                p->kvslot[layer][pg] = SLOT_REMOTE;
+                p->pt->pages[layer][pg].tier = TIER_REMOTE;
+                continue;
+            }
             const int32_t s = pop_slot(p->kv_free, "KV page");
             p->wait_slot(false, s, S(stream));  // a recycled slot may still be draining to the host
-            p->kvslot[layer][first_new + i] = s;
+            p->kvslot[layer][pg] = s;
         }
         *slot_begin = b;
         *slot_end = e;
@@ -466,7 +497,7 @@ static int append_impl(oomb_pool_t p, int layer, const void* k, const void* v, i
             const char* vb = static_cast<const char*>(v) + done * re * p->elem;
             launch_append(p->cfg.dtype, kb, vb, seg, f, P, p->cfg.n_kv_heads, p->cfg.head_dim, first_page,
                           last_page - first_page + 1, ns, p->kvslot_layer(layer), p->kpool, p->vpool,
-                          p->kavg_sum_layer(layer), p->kavg_cnt_layer(layer), S(stream), inv_freq);
+                          p->kavg_sum_layer(layer), p->kavg_cnt_layer(layer), p->d_err, S(stream), inv_freq);
             published = std::max(published, last_page + 1);
             done += seg;
         }
@@ -587,7 +618,9 @@ int oomb_set_tier(oomb_pool_t p, int layer, int page, int tier) {
         p->pt->check_layer(layer);
         OOMB_REQUIRE(page >= 0 && page < static_cast<int>(p->pt->pages[layer].size()), OOMB_SHAPE_ERROR,
                      "set_tier: page out of range");
-        p->pt->pages[layer][page].tier = tier ? 1 : 0;
+        OOMB_REQUIRE(p->pt->pages[layer][page].tier <= TIER_HOST, OOMB_STATE_ERROR,
+                     "set_tier: page is owned by another shard or lost");
+        p->pt->pages[layer][page].tier = tier ? TIER_HOST : TIER_DEVICE;
     });
 }
 int oomb_get_tier(oomb_pool_t p, int layer, int page, int* tier) {
@@ -650,6 +683,7 @@ int oomb_selection_set_host(oomb_selection_t s, const int32_t* off, const int32_
         OOMB_REQUIRE(nnz >= 0 && nnz <= s->max_ids, OOMB_SHAPE_ERROR, "selection: too many ids");
         OOMB_CUDA(cudaEventSynchronize(s->ev));  // previous async copy out of the pinned mirror is done
         s->host_pending = false;
+        s->nnz_from_host = false;
         std::memcpy(s->h_off, off, (m + 1) * sizeof(int32_t));
         if (nnz) std::memcpy(s->h_ids, ids, nnz * sizeof(int32_t));
         OOMB_CUDA(cudaMemcpyAsync(s->d_off, s->h_off, (m + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, S(stream)));
@@ -682,6 +716,7 @@ static void select_range(oomb_selection_t s, int first, int count, int m, cudaSt
     OOMB_REQUIRE(static_cast<int64_t>(m) * count <= s->max_ids, OOMB_SHAPE_ERROR, "selection: too many ids");
     OOMB_CUDA(cudaEventSynchronize(s->ev));
     s->host_pending = false;
+    s->nnz_from_host = false;
     for (int qp = 0; qp <= m; ++qp) s->h_off[qp] = qp * count;
     for (int qp = 0; qp < m; ++qp)
         for (int i = 0; i < count; ++i) s->h_ids[static_cast<int64_t>(qp) * count + i] = first + i;
@@ -717,8 +752,39 @@ static void select_topk_impl(oomb_selection_t s, const float* vote, int m, int n
                                   cudaMemcpyDeviceToHost, st));
     OOMB_CUDA(cudaEventRecord(s->ev, st));
     s->host_pending = true;
+    s->nnz_from_host = false;
     s->m = m;
     s->nnz = m * kk;
+}
+
+int oomb_selection_filter_owned(oomb_pool_t p, oomb_selection_t src, oomb_selection_t dst, void* stream) {
+    return guard([&] {
+        set_dev(p);
+        OOMB_REQUIRE(src != nullptr && dst != nullptr && src != dst, OOMB_STATE_ERROR,
+                     "filter_owned: needs two distinct selections");
+        OOMB_REQUIRE(src->m <= dst->max_m && src->nnz <= dst->max_ids, OOMB_SHAPE_ERROR,
+                     "filter_owned: destination selection too small");
+        OOMB_CUDA(cudaEventSynchronize(dst->ev));  // the previous mirror copy out of dst is done
+        const int m = src->m;
+        launch_filter_owned(src->d_off, src->d_ids, m, p->owner_stride, p->owner_rank, dst->d_off, dst->d_ids,
+                            S(stream));
+        OOMB_CUDA(cudaMemcpyAsync(dst->h_off, dst->d_off, (m + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                  S(stream)));
+        if (src->nnz)  // an upper bound: the exact count is h_off[m] once the mirror lands
+            OOMB_CUDA(cudaMemcpyAsync(dst->h_ids, dst->d_ids, static_cast<size_t>(src->nnz) * sizeof(int32_t),
+                                      cudaMemcpyDeviceToHost, S(stream)));
+        OOMB_CUDA(cudaEventRecord(dst->ev, S(stream)));
+        dst->host_pending = true;
+        dst->nnz_from_host = true;
+        dst->m = m;
+        dst->nnz = src->nnz;
+    });
+}
+int oomb_page_owner(oomb_pool_t p, int* stride, int* rank) {
+    return guard([&] {
+        if (stride) *stride = p->owner_stride;
+        if (rank) *rank = p->owner_rank;
+    });
 }
 
 int oomb_select_topk(oomb_selection_t s, const float* vote, int m, int n, int k, void* stream) {
@@ -922,7 +988,9 @@ int oomb_accumulate_grad_pages(oomb_pool_t p, int layer, const int32_t* ids, int
                                void* stream) {
     return guard([&] {
         set_dev(p);
-        p->pt->check_ids(layer, ids, n, p->enforce, "gather_grad_pages");
+        // on a page-range shard the REMOTE pages among ids add nothing here: their owners add them to
+        // their partial dk / dv, which the range group sums (sharding.ShardedLayer.backward)
+        p->pt->check_ids(layer, ids, n, p->enforce, "gather_grad_pages", /*allow_remote=*/true);
         if (n == 0) return;
         int32_t* d = upload_ids(ids, n, S(stream));
         launch_accumulate_grads(d, n, p->gslot_layer(layer), p->gkpool, p->gvpool, p->pt->filled[layer],
@@ -935,7 +1003,7 @@ int oomb_accumulate_grad_pages_rope(oomb_pool_t p, int layer, const int32_t* ids
                                     int64_t pos_offset, float rope_base, void* stream) {
     return guard([&] {
         set_dev(p);
-        p->pt->check_ids(layer, ids, n, p->enforce, "gather_grad_pages");
+        p->pt->check_ids(layer, ids, n, p->enforce, "gather_grad_pages", /*allow_remote=*/true);
         OOMB_REQUIRE(rope_base > 1.f, OOMB_CONFIG_ERROR, "rope_base must be > 1");
         if (n == 0) return;
         int32_t* d = upload_ids(ids, n, S(stream));

@@ -162,10 +162,17 @@ struct NewSlots {
     int32_t slot[120];
 };
 
+// Device slot of a page this pool does not store (a page-range shard's REMOTE page): append
+// updates its K_avg sums only. Slot -1 is a page that is not resident (a kernel error to read).
+constexpr int32_t SLOT_REMOTE = -2;
+
 void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_t filled_before, int P, int Hkv,
                    int hd, int first_page, int n_pages_touched, const NewSlots& ns, int32_t* d_kvslot_layer,
-                   void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, cudaStream_t st,
-                   const double* rope_inv_freq = nullptr);
+                   void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, int* d_err,
+                   cudaStream_t st, const double* rope_inv_freq = nullptr);
+// dst CSR = the ids of src with id % stride == rank, list order kept (one CTA).
+void launch_filter_owned(const int32_t* src_off, const int32_t* src_ids, int m, int stride, int rank,
+                         int32_t* dst_off, int32_t* dst_ids, cudaStream_t st);
 void launch_rope(int in_dtype, int out_dtype, const void* x, int64_t rows, int heads, int hd, int64_t pos0, int sign,
                  const double* inv_freq, void* out, cudaStream_t st);
 // Device table inv_freq[i] = base^(-2i/hd) computed on the host with the reference's std::pow

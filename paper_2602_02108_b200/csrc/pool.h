@@ -42,10 +42,17 @@ int guard(F&& f) {
 // at append; gk then gv lazily at first scatter; reset frees k, v, gk, gv per
 // page per layer) so page tables compare bit-exactly.
 // ---------------------------------------------------------------------------
+// Page tiers. DEVICE / HOST are the reference's Tier (paged_kv.hpp:34). REMOTE marks a page whose
+// K/V and gradients live on another page-range shard (pool page ownership, oomb_config
+// page_owner_stride); LOST marks a host-tier page whose host copy was dropped when a real offload
+// engine detached without room to bring it back. Reads of REMOTE / LOST pages always raise
+// ResidencyError, enforcement or not.
+enum : uint8_t { TIER_DEVICE = 0, TIER_HOST = 1, TIER_REMOTE = 2, TIER_LOST = 3 };
+
 struct PageTable {
     struct Entry {
         int32_t k = -1, v = -1, gk = -1, gv = -1;
-        uint8_t tier = 0;  // 0 device, 1 host
+        uint8_t tier = TIER_DEVICE;
     };
     int n_layers, P, kvh, hd, kv_elem, grad_elem;
     std::vector<std::vector<Entry>> pages;
@@ -88,13 +95,22 @@ struct PageTable {
         }
         filled[layer] += rows;
     }
-    void check_ids(int layer, const int32_t* ids, int n, bool enforce, const char* op) const {
+    void check_ids(int layer, const int32_t* ids, int n, bool enforce, const char* op,
+                   bool allow_remote = false) const {
         check_layer(layer);
         const auto& st = pages[layer];
         for (int i = 0; i < n; ++i) {
             OOMB_REQUIRE(ids[i] >= 0 && ids[i] < static_cast<int32_t>(st.size()), OOMB_SHAPE_ERROR,
                          std::string(op) + ": page id out of range");
-            OOMB_REQUIRE(!enforce || st[ids[i]].tier == 0, OOMB_RESIDENCY_ERROR,
+            const uint8_t t = st[ids[i]].tier;
+            if (allow_remote && t == TIER_REMOTE) continue;
+            OOMB_REQUIRE(t != TIER_REMOTE, OOMB_RESIDENCY_ERROR,
+                         std::string(op) + ": page " + std::to_string(ids[i]) + " of layer " + std::to_string(layer) +
+                             " is owned by another page-range shard");
+            OOMB_REQUIRE(t != TIER_LOST, OOMB_RESIDENCY_ERROR,
+                         std::string(op) + ": page " + std::to_string(ids[i]) + " of layer " + std::to_string(layer) +
+                             " lost its data when an offload engine detached without room to restore it");
+            OOMB_REQUIRE(!enforce || t == TIER_DEVICE, OOMB_RESIDENCY_ERROR,
                          std::string(op) + ": page " + std::to_string(ids[i]) + " of layer " + std::to_string(layer) +
                              " is not device-resident");
         }
@@ -133,8 +149,8 @@ struct PageTable {
         for (const auto& st : pages)
             for (const auto& en : st) {
                 r.pages += 1;
-                if (en.tier == 0) r.device_bytes += 2 * pe * kv_elem;
-                else r.host_bytes += 2 * pe * kv_elem;
+                if (en.tier == TIER_DEVICE) r.device_bytes += 2 * pe * kv_elem;
+                else if (en.tier == TIER_HOST) r.host_bytes += 2 * pe * kv_elem;
                 if (en.gk >= 0) r.grad_bytes += 2 * pe * grad_elem;
             }
         r.arena_blocks = arena_n;
@@ -174,6 +190,10 @@ struct oomb_pool_s {
     int* d_err = nullptr;
     bool enforce = false;
     int policy = 0;
+    // page-range shard ownership (oomb_config page_owner_*): this pool stores K/V / gradients only
+    // for pages with id % owner_stride == owner_rank; others are TIER_REMOTE with kvslot SLOT_REMOTE
+    int owner_stride = 1, owner_rank = 0;
+    bool owns(int64_t page) const { return owner_stride <= 1 || page % owner_stride == owner_rank; }
     TcPoolMaps maps;
     // tcgen05 backward: dQ runs on bwd_side concurrently with dK/dV on the caller's stream. Two
     // workspaces alternate between calls so that, with OOMB_ATTN_DEFER_DQ, chunk i-1's prep and
@@ -263,6 +283,7 @@ struct oomb_pool_s {
 
 struct oomb_selection_s {
     oomb_pool_s* pool = nullptr;
+    bool nnz_from_host = false;  // nnz is known only once the host mirror lands (filter_owned)
     int max_m = 0, max_ids = 0;
     int32_t* d_off = nullptr;
     int32_t* d_ids = nullptr;

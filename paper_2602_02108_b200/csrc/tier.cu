@@ -213,12 +213,22 @@ struct oomb_tier_s {
 
     // ---- device table publication (real mode)
     void queue_table(int layer, int page) {
-        if (pending.n == 480) flush_table();
         const int idx = static_cast<int>(layer * pool->max_pages + page);
-        pending.idx[pending.n] = idx;
-        pending.kv[pending.n] = pool->kvslot[layer][page];
-        pending.g[pending.n] = pool->gslot[layer][page];
-        ++pending.n;
+        // one entry per (layer, page) per batch, holding the newest slots: the kernel applies
+        // entries in parallel, so two entries for one page would race (eviction then refetch)
+        int at = -1;
+        for (int i = 0; i < pending.n; ++i)
+            if (pending.idx[i] == idx) {
+                at = i;
+                break;
+            }
+        if (at < 0) {
+            if (pending.n == 480) flush_table();
+            at = pending.n++;
+            pending.idx[at] = idx;
+        }
+        pending.kv[at] = pool->kvslot[layer][page];
+        pending.g[at] = pool->gslot[layer][page];
     }
     void flush_table() {
         if (!real() || pending.n == 0) return;
@@ -351,6 +361,9 @@ struct oomb_tier_s {
         PageState& ps = pages[layer][page];
         // the host block is read only after the write-back that filled it has landed (a page evicted
         // and fetched back soon after); the destination slots wait for their own read-outs in take_slot
+        OOMB_REQUIRE(ps.host_has_kv, OOMB_STATE_ERROR,
+                     "offload: page " + std::to_string(page) + " of layer " + std::to_string(layer) +
+                         " is host-tier but its host block holds no data");
         p.wait_ticket(ps.wb_batch, h2d_stream);
         const int32_t ks = take_slot(false, h2d_stream, "KV");
         p.kvslot[layer][page] = ks;
@@ -401,6 +414,11 @@ struct oomb_tier_s {
             if (p < 0 || p >= static_cast<int32_t>(pt->pages[layer].size()))
                 throw Error(OOMB_STATE_ERROR, "fetch_pages: unknown page " + std::to_string(p));
             PageState& ps = state(layer, p);
+            if (tier(layer, p) >= TIER_REMOTE)
+                throw Error(OOMB_RESIDENCY_ERROR, "fetch_pages: page " + std::to_string(p) +
+                                                      (tier(layer, p) == TIER_REMOTE
+                                                           ? " is owned by another page-range shard"
+                                                           : " lost its data when an engine detached"));
             if (tier(layer, p) == 0) {
                 if (best_effort) {
                     if (!ps.reserved && !ps.pinned) to_pin.push_back(p);
@@ -443,7 +461,9 @@ struct oomb_tier_s {
             ps.in_flight_done = done;
             if (phase == 0) h2d_fwd += bytes;
             else h2d_bwd += bytes;
-            if (real()) real_fetch(layer, p);
+            // a page listed twice is logged twice, as in the reference, but moved once (its second
+            // occurrence finds the slots the first one took)
+            if (real() && pool->kvslot[layer][p] < 0) real_fetch(layer, p);
             push(EV_FETCH_DONE, done, layer, p, bytes, chunk, ev_done);
             ready = std::max(ready, done);
             tr.pages.push_back(p);
@@ -504,7 +524,7 @@ struct oomb_tier_s {
         size_t need_kv = 0, need_g = 0;
         for (int l = 0; l < pt->n_layers; ++l)
             for (size_t p = 0; p < pages[l].size(); ++p)
-                if (tier(l, static_cast<int>(p)) != 0 && pages[l][p].in_flight_done <= 0) {
+                if (tier(l, static_cast<int>(p)) == TIER_HOST && pages[l][p].in_flight_done <= 0) {
                     ++need_kv;
                     if (grads_allocated(l, static_cast<int>(p))) ++need_g;
                 }
@@ -513,7 +533,7 @@ struct oomb_tier_s {
         for (int l = 0; l < pt->n_layers; ++l)
             for (size_t i = 0; i < pages[l].size(); ++i) {
                 const int p = static_cast<int>(i);
-                if (tier(l, p) == 0) continue;
+                if (tier(l, p) != TIER_HOST) continue;
                 PageState& ps = pages[l][i];
                 if (ps.in_flight_done <= 0) real_fetch(l, p);  // an in-flight page already has its slots
                 set_tier(l, p, 0);
@@ -551,6 +571,38 @@ struct oomb_tier_s {
             state(layer, ids[i]).pinned = false;
         }
         enforce_capacity(0);
+        flush_table();
+    }
+
+    // Real mode, at attach: the engine takes over pages the pool already holds. A device page
+    // appended before the engine existed has no host copy yet (its first eviction must write it
+    // back); a page tagged host without an engine (set_tier, as the reference's tests do before
+    // constructing one) still has its data in device slots: it is written back now and its slots
+    // are freed, so the page really lives in the host tier.
+    void adopt_pool_pages() {
+        sync_pages();
+        bool wb = false;
+        for (int l = 0; l < pt->n_layers; ++l)
+            for (size_t i = 0; i < pages[l].size(); ++i) {
+                const int p = static_cast<int>(i);
+                PageState& ps = pages[l][i];
+                const bool has_g = grads_allocated(l, p);
+                if (tier(l, p) == TIER_DEVICE) {
+                    ps.kv_host_valid = false;
+                    ps.grad_host_valid = !has_g;
+                } else if (tier(l, p) == TIER_HOST) {
+                    if (pool->kvslot[l][p] >= 0) {
+                        if (!wb) begin_writeback();
+                        wb = true;
+                        real_evict(l, p, true, has_g);
+                        ps.kv_host_valid = true;
+                        ps.grad_host_valid = true;
+                    } else {
+                        set_tier(l, p, TIER_LOST);  // no copy anywhere (cannot happen through this API)
+                    }
+                }
+            }
+        if (wb) end_writeback();
         flush_table();
     }
 
@@ -600,7 +652,7 @@ int oomb_tier_create(oomb_pool_t pool, const oomb_tier_config* cfg, void* comput
             OOMB_CUDA(cudaEventCreate(&t->t0));
             OOMB_CUDA(cudaEventRecord(t->t0, t->compute));
             pool->enforce = true;  // the engine turns residency enforcement on (tiered_memory.hpp:102-108)
-            t->sync_pages();
+            t->adopt_pool_pages();
         } catch (...) {
             oomb_tier_destroy(t);
             throw;
@@ -616,14 +668,29 @@ int oomb_tier_destroy(oomb_tier_t t) {
 #ifndef OOMB_TIER_RESTORE_ON_DESTROY
 #define OOMB_TIER_RESTORE_ON_DESTROY 1
 #endif
+        int64_t lost = 0;
         if (OOMB_TIER_RESTORE_ON_DESTROY) {
             try {
-                t->restore_all();  // best effort: a pool without room keeps those pages host-tier (data dropped)
+                t->restore_all();
             } catch (...) {
             }
         }
+        // Pages still host-tier now (no room in the pool, or restore disabled) lose their data with
+        // the pinned blocks freed below. They are tagged lost: every later read of their K/V or
+        // gradients raises ResidencyError (pool.h check_ids), whether or not enforcement is on.
+        t->sync_pages();
+        for (int l = 0; l < t->pt->n_layers; ++l)
+            for (size_t i = 0; i < t->pages[l].size(); ++i)
+                if (t->tier(l, static_cast<int>(i)) == TIER_HOST) {
+                    t->set_tier(l, static_cast<int>(i), TIER_LOST);
+                    ++lost;
+                }
         cudaDeviceSynchronize();
         t->pool->enforce = false;
+        if (lost > 0)
+            g_last_error = "tier_destroy: " + std::to_string(lost) +
+                           " host-tier page(s) could not be restored to the device (no free slots) and are marked "
+                           "lost; reads of them raise ResidencyError";
         for (auto e : t->log_events) cudaEventDestroy(e);
         for (auto& tr : t->transfers)
             if (tr.ev) cudaEventDestroy(tr.ev);
@@ -633,6 +700,8 @@ int oomb_tier_destroy(oomb_tier_t t) {
         if (t->d2h_stream) cudaStreamDestroy(t->d2h_stream);
         cudaFreeHost(t->host_kv);
         cudaFreeHost(t->host_grad);
+        delete t;
+        return lost > 0 ? OOMB_RESIDENCY_ERROR : OOMB_OK;
     }
     delete t;
     return OOMB_OK;

@@ -66,11 +66,15 @@ class PagedCache:
 
     dtype: "bf16" (tensor-core path) or "fp32" (1e-5 parity path).
     max_tokens: per-layer capacity of the device page table.
-    device_capacity_pages: KV page slots on the device (all layers); default = all.
+    device_capacity_pages: KV page slots on the device (all layers); default = all (the owned share).
+    page_owner: (stride R, rank r) of a page-range shard: this pool stores K/V and
+        gradients only for pages with id % R == r; the others are REMOTE (tier 2): appends still
+        add their rows to K_avg (so every shard scores every candidate), reads raise ResidencyError.
     """
 
     def __init__(self, cfg: ModelConfig, dtype: str = "bf16", max_tokens: int | None = None,
-                 device: int | None = None, device_capacity_pages: int = -1):
+                 device: int | None = None, device_capacity_pages: int = -1,
+                 page_owner: tuple[int, int] | None = None):
         cfg.validate()
         self.cfg = cfg
         self.dtype_name = dtype
@@ -80,7 +84,9 @@ class PagedCache:
         self.max_tokens = max_tokens if max_tokens is not None else 64 * cfg.chunk_size
         c = OombConfig(cfg.n_layers, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, cfg.chunk_size, cfg.page_size,
                        cfg.retrieval_budget, cfg.local_window, int(cfg.score_scale),
-                       1 if self.dtype == torch.bfloat16 else 0, self.max_tokens, device_capacity_pages)
+                       1 if self.dtype == torch.bfloat16 else 0, self.max_tokens, device_capacity_pages,
+                       *(page_owner if page_owner is not None else (0, 0)))
+        self.owner_stride, self.owner_rank = (max(1, page_owner[0]), page_owner[1]) if page_owner else (1, 0)
         h = C.c_void_p()
         call("oomb_pool_create", C.byref(c), self.device_index, C.byref(h))
         self.handle = h
@@ -130,6 +136,15 @@ class PagedCache:
         out = C.c_int()
         call("oomb_n_pages", self.handle, layer, C.byref(out))
         return out.value
+
+    def owns(self, page: int) -> bool:
+        """Page-range shard ownership: True when this pool stores the page's K/V and gradients."""
+        return self.owner_stride <= 1 or page % self.owner_stride == self.owner_rank
+
+    def owned(self, ids) -> np.ndarray:
+        """The ids this pool stores, order kept (all of them without page ownership)."""
+        a = self._ids(ids)
+        return a if self.owner_stride <= 1 else np.ascontiguousarray(a[a % self.owner_stride == self.owner_rank])
 
     @staticmethod
     def full_pages_before(tokens: int, page_size: int) -> int:

@@ -2,7 +2,14 @@
 
 KV-head-group sharding (KVGroupShard) and, when groups run out (Qwen2.5-7B has 4 groups
 for 8 GPUs; c5 splits page ranges across 2/4/8 GPUs), the page-range split
-(PageRangeShard) with an exact LSE / output merge.
+(PageRangeShard) with an exact LSE / output merge. ShardPlan composes the two
+(world = kv_world x range_world; rank = kv_idx * range_world + range_idx) and
+ShardedLayer runs one chunk of a split layer end to end: selection (vote exchange over
+the ranks holding the same page range), attention over the rank's own pages, the exact
+(O, LSE) merge and the ordered dQ / dk_cur / dv_cur reduction over the ranks holding the
+same KV groups. The merge and reductions are proportional (oomb_comm.h: ordered
+reduce-scatter by row slices + in-place all-gather of the slices, ~2x the tensor per rank)
+and bitwise equal to the all-gather-then-combine versions.
 
 Attention forward / backward and the gradient pool of different KV groups touch
 disjoint K/V/dK/dV head slices and disjoint q-heads, so a rank that owns a
@@ -18,7 +25,8 @@ top-k selections.
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass
+import math
+from dataclasses import dataclass, field
 
 import torch
 
@@ -130,6 +138,48 @@ class OombComm:
         comm_call("oomb_dq_reduce", self.handle, C.c_void_p(p.data_ptr()), p.numel(), C.c_void_p(out.data_ptr()),
                   stream_handle(stream))
         return out
+
+    # ---- proportional exchanges (ordered reduce-scatter by slices + all-gather of the slices)
+    def allreduce_ordered(self, part: torch.Tensor, stream=None, out: torch.Tensor | None = None) -> torch.Tensor:
+        """out = sum over ranks of `part` in rank order (fp32), bitwise equal to dq_reduce; out may be part."""
+        from ._lib import comm_call
+        from .paged_kv import stream_handle
+        p = part if part.is_contiguous() else part.contiguous()
+        o = p if out is None else out
+        comm_call("oomb_allreduce_ordered", self.handle, C.c_void_p(p.data_ptr()), p.numel(),
+                  C.c_void_p(o.data_ptr()), stream_handle(stream))
+        self.bytes_sent += comm_bytes(1, self.world, p.numel(), 4)[0]
+        return o
+
+    def lse_merge(self, o_part: torch.Tensor, lse_part: torch.Tensor, stream=None, out=None, lse=None):
+        """The exact (O, LSE) merge over all ranks, bitwise equal to lse_merge_allgather."""
+        from ._lib import comm_call
+        from .paged_kv import stream_handle
+        c, h, hd = o_part.shape
+        o, l = o_part.contiguous(), lse_part.contiguous()
+        out = torch.empty_like(o) if out is None else out
+        lse = torch.empty_like(l) if lse is None else lse
+        comm_call("oomb_lse_merge_ordered", self.handle, C.c_void_p(o.data_ptr()), C.c_void_p(l.data_ptr()), c * h,
+                  hd, 1 if o.dtype == torch.bfloat16 else 0, C.c_void_p(out.data_ptr()), C.c_void_p(lse.data_ptr()),
+                  stream_handle(stream))
+        self.bytes_sent += comm_bytes(1, self.world, c * h, hd * o.element_size() + 4)[0]
+        return out, lse
+
+    bytes_sent = 0
+
+
+def comm_bytes(op: int, world: int, elems: int, elem_bytes: int) -> tuple[int, int]:
+    """Per-rank (sent, received) wire bytes of one exchange of `elems` elements: op 0 = all-gather +
+    local combine, op 1 = ordered reduce-scatter by slices + all-gather of the slices (oomb_comm.h).
+    Pure arithmetic (the same formula as oomb_comm_bytes), usable without a GPU."""
+    if world <= 1:
+        return 0, 0
+    t = elems * elem_bytes
+    if op == 0:
+        return t * (world - 1), t * (world - 1)
+    chunk = (elems + world - 1) // world
+    mine = min(elems, chunk) * elem_bytes
+    return (t - mine) + mine * (world - 1), mine * (world - 1) + (t - mine)
 
 
 def fixed_order_sum(parts: torch.Tensor) -> torch.Tensor:
@@ -272,3 +322,334 @@ def range_backward(shard: PageRangeShard, cfg, dout, q, cache, layer, k_cur, v_c
     dk = _gather(g.dk_cur, group)[0].clone()
     dv = _gather(g.dv_cur, group)[0].clone()
     return A.AttnGrads(dq, dk, dv)
+
+
+# ---------------------------------------------------------------------------
+# The same exchange steps over torch.distributed (gloo in the CPU tests; CUDA tensors are staged
+# through host memory when the backend cannot carry them, e.g. several ranks sharing one GPU)
+# ---------------------------------------------------------------------------
+def lse_merge_torch(o_parts: torch.Tensor, lse_parts: torch.Tensor):
+    """oomb_lse_merge in torch, with the kernel's fp32 operation order (parts in order)."""
+    r = o_parts.shape[0]
+    lp = lse_parts.float()
+    m = lp[0].clone()
+    for i in range(1, r):
+        m = torch.maximum(m, lp[i])
+    l = torch.zeros_like(m)
+    for i in range(r):
+        l = l + torch.where(lp[i] == float("-inf"), torch.zeros_like(m), torch.exp(lp[i] - m))
+    L = torch.where(m == float("-inf"), m, m + torch.log(l))
+    acc = torch.zeros(o_parts.shape[1:], dtype=torch.float32, device=o_parts.device)
+    for i in range(r):
+        w = torch.where(lp[i] == float("-inf"), torch.zeros_like(m), torch.exp(lp[i] - L))
+        acc = acc + w[..., None] * o_parts[i].float()
+    return acc.to(o_parts.dtype), L
+
+
+def _on_stream(fn):
+    """Run a TorchComm step with `stream` current, so the host staging of CUDA tensors is ordered
+    after the work already enqueued there and its results are consumed in stream order."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(self, *a, stream=None, **kw):
+        if stream is None or not torch.cuda.is_available():
+            return fn(self, *a, **kw)
+        with torch.cuda.stream(stream):
+            return fn(self, *a, **kw)
+    return wrapper
+
+
+class TorchComm:
+    """Exchange steps of the sharded path over a torch.distributed group, with the algorithms of
+    liboomb_comm.so: row slices exchanged all-to-all, combined in rank order by the slice's owner,
+    then all-gathered. Results equal OombComm's bitwise on fp32 sums (same per-element order)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.bytes_sent = 0
+        backend = dist.get_backend(group) if dist.is_initialized() else "gloo"
+        self.stage_cuda = backend != "nccl"
+
+    def _host(self, x):
+        return x.cpu() if (x.is_cuda and self.stage_cuda) else x
+
+    def _slices(self, rows):
+        ch = (rows + self.world - 1) // self.world
+        offs = [min(rows, s * ch) for s in range(self.world)]
+        lens = [min(rows, (s + 1) * ch) - offs[s] for s in range(self.world)]
+        return offs, lens
+
+    def _exchange(self, x2):  # x2 [rows, w] -> packed [world, len(me), w]
+        offs, lens = self._slices(x2.shape[0])
+        me = lens[self.rank]
+        out = torch.empty((self.world * me, x2.shape[1]), dtype=x2.dtype, device=x2.device)
+        self.dist.all_to_all_single(out, x2.contiguous(), output_split_sizes=[me] * self.world,
+                                    input_split_sizes=lens, group=self.group)
+        return out.view(self.world, me, x2.shape[1]), offs, lens
+
+    def _share(self, full, mine, offs, lens):  # all-gather of the slices into full [rows, w]
+        ch = max(lens)
+        pad = torch.zeros((ch, full.shape[1]), dtype=full.dtype, device=full.device)
+        pad[: lens[self.rank]] = mine
+        gath = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(gath, pad, group=self.group)
+        for s in range(self.world):
+            full[offs[s]: offs[s] + lens[s]] = gath[s][: lens[s]]
+
+    @_on_stream
+    def vote_allgather(self, partials_local: torch.Tensor, out=None) -> torch.Tensor:
+        vote = combine_votes(self._host(partials_local.contiguous()), self.group)
+        vote = vote.to(partials_local.device)
+        if out is not None:
+            out.copy_(vote)
+            return out
+        return vote
+
+    @_on_stream
+    def allreduce_ordered(self, part: torch.Tensor, out=None) -> torch.Tensor:
+        dev = part.device
+        x = self._host(part.contiguous()).reshape(-1, 1).float()
+        if self.world == 1:
+            res = x
+        else:
+            packed, offs, lens = self._exchange(x)
+            acc = packed[0].clone()
+            for s in range(1, self.world):
+                acc = acc + packed[s]
+            res = torch.empty_like(x)
+            self._share(res, acc, offs, lens)
+            self.bytes_sent += comm_bytes(1, self.world, x.shape[0], 4)[0]
+        res = res.reshape(part.shape).to(dev)
+        if out is not None:
+            out.copy_(res)
+            return out
+        return res
+
+    @_on_stream
+    def lse_merge(self, o_part: torch.Tensor, lse_part: torch.Tensor, out=None, lse=None):
+        dev = o_part.device
+        c, h, hd = o_part.shape
+        o2 = self._host(o_part.contiguous()).reshape(c * h, hd)
+        l2 = self._host(lse_part.contiguous()).reshape(c * h, 1)
+        if self.world == 1:
+            mo, ml = o2, l2
+        else:
+            po, offs, lens = self._exchange(o2)
+            pl, _, _ = self._exchange(l2)
+            so, sl = lse_merge_torch(po, pl[..., 0])
+            mo, ml = torch.empty_like(o2), torch.empty_like(l2)
+            self._share(mo, so, offs, lens)
+            self._share(ml, sl[:, None], offs, lens)
+            self.bytes_sent += comm_bytes(1, self.world, c * h, hd * o2.element_size() + 4)[0]
+        mo, ml = mo.reshape(c, h, hd).to(dev), ml.reshape(c, h).to(dev)
+        if out is not None:
+            out.copy_(mo)
+            lse.copy_(ml)
+            return out, lse
+        return mo, ml
+
+
+# ---------------------------------------------------------------------------
+# Composed split: KV-head groups x page ranges (SURVEY §8e; BASELINE configs[3] on 8 GPUs)
+# ---------------------------------------------------------------------------
+@dataclass
+class ShardPlan:
+    """world = kv_world x range_world ranks; rank = kv_idx * range_world + range_idx.
+
+    mode "kv": KV-group split only (world must divide n_kv_heads); "range": page-range split only;
+    "kv+range" / "auto": as many KV groups per rank as the world allows (kv_world =
+    gcd(world, n_kv_heads)), the rest of the world splits page ranges; "KxR": explicit. Qwen2.5-7B (4 KV groups):
+    1/2/4 GPUs -> 1/2/4 x 1, 8 GPUs -> 4 x 2. Llama-3-8B c5 (8 groups) with "range": 1 x N.
+
+    kv_ranks(): the ranks holding the same page range (they exchange the page vote);
+    range_ranks(): the ranks holding the same KV groups (they merge O/LSE and reduce dQ and the
+    chunk's dK/dV)."""
+    rank: int
+    world: int
+    n_kv_heads: int
+    n_q_heads: int
+    mode: str = "auto"
+    kv_world: int = field(init=False)
+    range_world: int = field(init=False)
+
+    def __post_init__(self):
+        if self.mode == "kv":
+            if self.n_kv_heads % self.world:
+                raise ValueError(f"{self.n_kv_heads} KV groups cannot be split over {self.world} ranks")
+            self.kv_world, self.range_world = self.world, 1
+        elif self.mode == "range":
+            self.kv_world, self.range_world = 1, self.world
+        elif self.mode in ("auto", "kv+range"):
+            self.kv_world = math.gcd(self.world, self.n_kv_heads)
+            self.range_world = self.world // self.kv_world
+        elif "x" in self.mode:  # explicit "KxR"
+            self.kv_world, self.range_world = (int(x) for x in self.mode.split("x"))
+            if self.kv_world * self.range_world != self.world or self.n_kv_heads % self.kv_world:
+                raise ValueError(f"shard mode {self.mode!r} does not fit world {self.world} / "
+                                 f"{self.n_kv_heads} KV groups")
+        else:
+            raise ValueError(f"unknown shard mode {self.mode!r}")
+        if not 0 <= self.rank < self.world:
+            raise ValueError("rank out of range")
+
+    @property
+    def kv_idx(self) -> int:
+        return self.rank // self.range_world
+
+    @property
+    def range_idx(self) -> int:
+        return self.rank % self.range_world
+
+    @property
+    def kv(self) -> KVGroupShard:
+        return KVGroupShard(self.kv_idx, self.kv_world, self.n_kv_heads, self.n_q_heads)
+
+    @property
+    def pages(self) -> "PageRangeShard":
+        return PageRangeShard(self.range_idx, self.range_world)
+
+    def kv_ranks(self) -> list[int]:
+        return [k * self.range_world + self.range_idx for k in range(self.kv_world)]
+
+    def range_ranks(self) -> list[int]:
+        return [self.kv_idx * self.range_world + j for j in range(self.range_world)]
+
+    def local_config(self, cfg: ModelConfig) -> ModelConfig:
+        return self.kv.local_config(cfg)
+
+    def page_owner(self) -> tuple[int, int] | None:
+        return (self.range_world, self.range_idx) if self.range_world > 1 else None
+
+    def make_cache(self, cfg: ModelConfig, **kw):
+        """The rank's PagedCache: its KV groups' heads, and K/V + gradient storage only for the pages
+        its range owns (HBM per rank = 1/range_world of the pages; K_avg kept for every page)."""
+        from .paged_kv import PagedCache
+        return PagedCache(self.local_config(cfg), page_owner=self.page_owner(), **kw)
+
+    def describe(self) -> str:
+        return (f"one sequence split over {self.world} GPU(s): {self.kv_world} KV-head group shard(s) x "
+                f"{self.range_world} page-range shard(s)")
+
+    def new_groups(self):
+        """(kv_group, range_group) torch.distributed groups of this rank. Every rank must call this
+        (new_group is collective over the world); None for a trivial (size-1) group."""
+        import torch.distributed as dist
+        kv_g = rg = None
+        for j in range(self.range_world):  # groups of ranks sharing page range j
+            ranks = [k * self.range_world + j for k in range(self.kv_world)]
+            g = dist.new_group(ranks) if self.kv_world > 1 else None
+            if j == self.range_idx:
+                kv_g = g
+        for i in range(self.kv_world):  # groups of ranks sharing KV groups i
+            ranks = [i * self.range_world + j for j in range(self.range_world)]
+            g = dist.new_group(ranks) if self.range_world > 1 else None
+            if i == self.kv_idx:
+                rg = g
+        return kv_g, rg
+
+
+class ShardedLayer:
+    """One attention layer of ONE sequence split by a ShardPlan (chunk_trainer.hpp:292-316, 415-439,
+    563-587 on a shard). Per chunk:
+
+      select   per-group partial votes of the rank's groups -> vote exchange over kv_comm (global
+               group order, the 1-GPU order) -> top-k (identical on every rank) -> the sub-selection
+               of pages this rank's range owns (device filter, list order kept)
+      forward  attention over the owned pages (+ the chunk's own keys on range rank 0) -> the exact
+               (O, LSE) merge over range_comm
+      backward attention backward with the merged (O, LSE): dK/dV of owned pages land in the
+               rank's gradient pool; the dM_i read-back adds the owned pages among the chunk's own;
+               then dQ and dk_cur / dv_cur are summed over range_comm in rank order.
+    With range_world == 1 the comm steps vanish and the layer is the KV-group split (or, at world
+    1, the unsplit layer)."""
+
+    def __init__(self, plan: ShardPlan, cfg: ModelConfig, cache=None, kv_comm=None, range_comm=None, layer: int = 0):
+        self.plan, self.cfg, self.layer = plan, cfg, layer
+        self.kv_comm, self.range_comm = kv_comm, range_comm
+        self.m = cfg.chunk_size // cfg.page_size
+        self.cache = self.lcfg = None
+        if cache is not None:
+            self.attach(cache)
+
+    def attach(self, cache):
+        """Use `cache` (plan.make_cache(cfg, ...)) as this rank's pool; returns it."""
+        self.cache, self.lcfg = cache, cache.cfg
+        return cache
+
+    def comm_bytes_per_chunk(self, chunk_tokens: int | None = None) -> dict:
+        """Per-rank wire bytes sent per chunk by each exchange (selection vote, (O, LSE) merge, ordered
+        [dq | dk_cur | dv_cur] reduction), from the exchange algorithms' formulas."""
+        C = chunk_tokens or self.cfg.chunk_size
+        hq, hkv, hd = self.lcfg.n_q_heads, self.lcfg.n_kv_heads, self.lcfg.head_dim
+        ob = 2 if self.cache.dtype == torch.bfloat16 else 4
+        out = {}
+        if self.plan.range_world > 1:
+            R = self.plan.range_world
+            out["olse_merge_bytes"] = comm_bytes(1, R, C * hq, hd * ob + 4)[0]
+            out["grad_reduce_bytes"] = comm_bytes(1, R, C * hq * hd + 2 * C * hkv * hd, 4)[0]
+            out["olse_merge_bytes_allgather"] = comm_bytes(0, R, C * hq, hd * ob + 4)[0]
+            out["grad_reduce_bytes_allgather"] = comm_bytes(0, R, C * hq * hd + 2 * C * hkv * hd, 4)[0]
+        return out
+
+    @property
+    def split_pages(self) -> bool:
+        return self.plan.range_world > 1
+
+    def select(self, i: int, q_local, full, sub=None, vote_buf=None, parts_buf=None, stream=None):
+        """Chunk i's selection into `full` (and the owned part into `sub` on a page-range shard)."""
+        from . import attention as A
+        from .paged_kv import _ptr, stream_handle
+        cfg, cache, m = self.cfg, self.cache, self.m
+        n_cand = i * m
+        mode = cfg.attention_mode[self.layer % len(cfg.attention_mode)]
+        if mode == "topk" and n_cand > 0:
+            n = min(n_cand, cache.n_pages(self.layer))
+            g = self.lcfg.n_kv_heads
+            parts = (torch.empty((g, m, n), dtype=torch.float32, device=cache.device) if parts_buf is None
+                     else parts_buf.reshape(-1)[: g * m * n].view(g, m, n))
+            call("oomb_score_pages_partial", cache.handle, self.layer, _ptr(q_local), q_local.shape[0], n,
+                 _ptr(parts), stream_handle(stream))
+            vote = (torch.empty((m, n), dtype=torch.float32, device=cache.device) if vote_buf is None
+                    else vote_buf.reshape(-1)[: m * n].view(m, n))
+            if self.kv_comm is not None and self.plan.kv_world > 1:
+                self.kv_comm.vote_allgather(parts, stream=stream, out=vote)
+            else:
+                call("oomb_vote_reduce", _ptr(parts), g, m, n, _ptr(vote), stream_handle(stream))
+            call("oomb_select_topk", full.handle, _ptr(vote), m, n, cfg.budget_pages(), stream_handle(stream))
+        elif mode == "local":
+            call("oomb_select_recent", full.handle, n_cand, cfg.local_window, m, stream_handle(stream))
+        else:  # dense, or no candidates yet (chunk_trainer.hpp:297-304)
+            call("oomb_select_all", full.handle, n_cand, m, stream_handle(stream))
+        if self.split_pages:
+            return full.filter_owned(out=sub, stream=stream)
+        return full
+
+    def forward(self, q_local, sel, k_local, v_local, out, lse, o_part=None, lse_part=None, stream=None):
+        from . import attention as A
+        if not self.split_pages:
+            return A.attn_forward(self.lcfg, q_local, self.cache, self.layer, sel, k_local, v_local, stream=stream,
+                                  out=out, lse=lse)
+        part = A.attn_forward(self.lcfg, q_local, self.cache, self.layer, sel, k_local, v_local, stream=stream,
+                              out=o_part, lse=lse_part, past_only=self.plan.range_idx != 0)
+        self.range_comm.lse_merge(part.out, part.lse, stream=stream, out=out, lse=lse)
+        return A.AttnSaved(out, lse, sel)
+
+    def backward(self, do_local, q_local, k_local, v_local, saved, grads, own_pages, stream=None, flat=None):
+        """grads: preallocated AttnGrads; when `flat` is given, grads.dq / dk_cur / dv_cur are views
+        of it and one ordered reduction covers all three."""
+        from . import attention as A
+        A.attn_backward(self.lcfg, do_local, q_local, self.cache, self.layer, k_local, v_local, saved,
+                        stream=stream, grads=grads, past_only=self.plan.range_idx != 0)
+        if len(own_pages):  # remote pages among them add nothing here (their owners add them)
+            self.cache.accumulate_grad_pages(self.layer, own_pages, grads.dk_cur, grads.dv_cur, stream=stream)
+        if self.split_pages:
+            if flat is not None:
+                self.range_comm.allreduce_ordered(flat, stream=stream, out=flat)
+            else:
+                for t in (grads.dq, grads.dk_cur, grads.dv_cur):
+                    self.range_comm.allreduce_ordered(t, stream=stream, out=t)
+        return grads

@@ -148,14 +148,26 @@ class TieredEngine:
         self.cache = cache
         self.cfg = cfg
 
-    def close(self):
+    def close(self, discard: bool = False):
+        """Detach (tiered_memory.hpp:110-113). A real engine brings its host-tier pages back into free
+        device slots first; pages it cannot bring back (no room) lose their data and are tagged lost
+        (tier 3: every later read raises ResidencyError), and close raises ResidencyError saying so
+        unless `discard` (the caller drops the pool's contents anyway, e.g. before reset())."""
         if getattr(self, "handle", None):
-            _lib.lib().oomb_tier_destroy(self.handle)
+            L = _lib.lib()
+            rc = L.oomb_tier_destroy(self.handle)
             self.handle = None
             if hasattr(self.cache, "_enforced"):
                 self.cache._enforced = False
+            if rc != 0 and not discard:
+                from .errors import raise_for_status
+                raise_for_status(rc, L.oomb_last_error().decode(errors="replace"))
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close(discard=True)
+        except Exception:  # interpreter shutdown
+            pass
 
     def begin_phase(self, phase: int):
         call("oomb_tier_begin_phase", self.handle, int(phase))

@@ -36,7 +36,7 @@ def test_comm_library_exports_every_header_symbol():
     """liboomb_comm.so (NCCL exchange steps) loads without a GPU and exports include/oomb_comm.h."""
     src = open(os.path.join(ROOT, "include", "oomb_comm.h")).read()
     syms = sorted(set(re.findall(r"^OOMB_API\s+[\w\s\*]+?\b(oomb_\w+)\s*\(", src, flags=re.M)))
-    assert len(syms) == 8
+    assert len(syms) == 11
     L = _lib.comm_lib()
     for s in syms:
         assert hasattr(L, s), s

@@ -171,4 +171,4 @@ def test_bench_kv_shard_mode_world1():
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["scaling"] == "strong" and line["value"] > 0 and line["gpu_launches"] > 0
-    assert "KV-head group" in line["config"]["parallelism"]
+    assert "KV-head group" in line["config"]["parallelism"] and line["sharding"]["kv_world"] == 1
