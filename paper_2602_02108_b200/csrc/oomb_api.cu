@@ -350,10 +350,13 @@ int oomb_pool_create(const oomb_config* cfg, int device, oomb_pool_t* out) {
     });
 }
 
+void tier_orphan(oomb_tier_s* t);  // tier.cu
+
 int oomb_pool_destroy(oomb_pool_t p) {
     if (!p) return OOMB_OK;
     cudaSetDevice(p->device);
     cudaDeviceSynchronize();
+    if (p->engine) tier_orphan(p->engine);  // an engine outliving its pool frees only its own memory
     cudaFree(p->kpool);
     cudaFree(p->vpool);
     cudaFree(p->gkpool);

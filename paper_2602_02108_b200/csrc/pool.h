@@ -167,8 +167,11 @@ struct oomb_pagetable_s {
     PageTable pt;
 };
 
+struct oomb_tier_s;
+
 struct oomb_pool_s {
     oomb_config cfg{};
+    oomb_tier_s* engine = nullptr;  // the attached real offload engine (orphaned if the pool dies first)
     int device = 0;
     int64_t max_pages = 0;
     int elem = 4;

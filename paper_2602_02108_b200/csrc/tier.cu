@@ -80,6 +80,7 @@ struct oomb_tier_s {
     oomb_tier_config cfg{};
     PageTable* pt = nullptr;
     oomb_pool_s* pool = nullptr;  // nullptr = simulation mode
+    bool orphaned = false;        // real mode: the pool was destroyed before the engine
     int phase = 0;
     double clock = 0, h2d_free = 0, d2h_free = 0, stall_s = 0;
     uint64_t h2d_fwd = 0, h2d_bwd = 0, d2h = 0, lru_counter = 0;
@@ -620,6 +621,12 @@ struct oomb_tier_s {
 
 extern "C" {
 
+// (internal, hidden) oomb_pool_destroy of a pool whose engine is still attached
+void tier_orphan(oomb_tier_s* t) {
+    t->orphaned = true;
+    t->pt = nullptr;
+}
+
 int oomb_tier_create_sim(oomb_pagetable_t pt, const oomb_tier_config* cfg, oomb_tier_t* out) {
     return guard([&] {
         OOMB_REQUIRE(cfg->bandwidth_bytes_per_s > 0, OOMB_CONFIG_ERROR, "tiered_memory: bandwidth must be positive");
@@ -651,7 +658,9 @@ int oomb_tier_create(oomb_pool_t pool, const oomb_tier_config* cfg, void* comput
                 cudaHostAlloc(reinterpret_cast<void**>(&t->host_grad), n_host * t->grad_block, cudaHostAllocDefault));
             OOMB_CUDA(cudaEventCreate(&t->t0));
             OOMB_CUDA(cudaEventRecord(t->t0, t->compute));
+            OOMB_REQUIRE(pool->engine == nullptr, OOMB_STATE_ERROR, "tiered_memory: the pool already has an engine");
             pool->enforce = true;  // the engine turns residency enforcement on (tiered_memory.hpp:102-108)
+            pool->engine = t;
             t->adopt_pool_pages();
         } catch (...) {
             oomb_tier_destroy(t);
@@ -664,29 +673,37 @@ int oomb_tier_create(oomb_pool_t pool, const oomb_tier_config* cfg, void* comput
 int oomb_tier_destroy(oomb_tier_t t) {
     if (!t) return OOMB_OK;
     if (t->real()) {
-        cudaSetDevice(t->pool->device);
 #ifndef OOMB_TIER_RESTORE_ON_DESTROY
 #define OOMB_TIER_RESTORE_ON_DESTROY 1
 #endif
         int64_t lost = 0;
-        if (OOMB_TIER_RESTORE_ON_DESTROY) {
+        if (!t->orphaned) {
+            cudaSetDevice(t->pool->device);
+            if (OOMB_TIER_RESTORE_ON_DESTROY) {
+                try {
+                    t->restore_all();
+                } catch (...) {
+                }
+            }
+            // Pages still host-tier now (no room in the pool, or restore disabled) lose their data with
+            // the pinned blocks freed below. They are tagged lost: every later read of their K/V or
+            // gradients raises ResidencyError (pool.h check_ids), whether or not enforcement is on.
             try {
-                t->restore_all();
+                t->sync_pages();
+                for (int l = 0; l < t->pt->n_layers; ++l)
+                    for (size_t i = 0; i < t->pages[l].size(); ++i)
+                        if (t->tier(l, static_cast<int>(i)) == TIER_HOST) {
+                            t->set_tier(l, static_cast<int>(i), TIER_LOST);
+                            ++lost;
+                        }
             } catch (...) {
             }
+            cudaDeviceSynchronize();
+            t->pool->enforce = false;
+            t->pool->engine = nullptr;
+        } else {
+            cudaDeviceSynchronize();
         }
-        // Pages still host-tier now (no room in the pool, or restore disabled) lose their data with
-        // the pinned blocks freed below. They are tagged lost: every later read of their K/V or
-        // gradients raises ResidencyError (pool.h check_ids), whether or not enforcement is on.
-        t->sync_pages();
-        for (int l = 0; l < t->pt->n_layers; ++l)
-            for (size_t i = 0; i < t->pages[l].size(); ++i)
-                if (t->tier(l, static_cast<int>(i)) == TIER_HOST) {
-                    t->set_tier(l, static_cast<int>(i), TIER_LOST);
-                    ++lost;
-                }
-        cudaDeviceSynchronize();
-        t->pool->enforce = false;
         if (lost > 0)
             g_last_error = "tier_destroy: " + std::to_string(lost) +
                            " host-tier page(s) could not be restored to the device (no free slots) and are marked "
@@ -707,10 +724,11 @@ int oomb_tier_destroy(oomb_tier_t t) {
     return OOMB_OK;
 }
 
-#define TIER_CALL(t, body)                     \
-    guard([&] {                                \
-        if ((t)->real()) set_dev((t)->pool);   \
-        body;                                  \
+#define TIER_CALL(t, body)                                                                          \
+    guard([&] {                                                                                     \
+        OOMB_REQUIRE(!(t)->orphaned, OOMB_STATE_ERROR, "tiered_memory: the engine's pool was destroyed"); \
+        if ((t)->real()) set_dev((t)->pool);                                                        \
+        body;                                                                                       \
     })
 
 int oomb_tier_begin_phase(oomb_tier_t t, int phase) { return TIER_CALL(t, t->phase = phase ? 1 : 0); }

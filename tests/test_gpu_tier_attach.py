@@ -105,13 +105,19 @@ def test_detach_without_room_reports_and_marks_pages_lost():
 
 
 def test_append_into_evicted_tail_page_raises():
+    from paper_2602_02108_b200 import ModelConfig, PagedCache
     from paper_2602_02108_b200.errors import ResidencyError
-    cache = _cache()
-    eng = _engine(cache, 0)
+    cfg = ModelConfig(n_layers=2, n_q_heads=4, n_kv_heads=2, head_dim=128, chunk_size=128, page_size=128,
+                      retrieval_budget=256, attention_mode=["topk"])
+    cache = PagedCache(cfg, dtype="bf16", max_tokens=4 * 128)
+    eng = _engine(cache, 1)
     k, v = _kv(64, 4)  # half a page
     r = cache.append_chunk(0, k, v)
     eng.on_pages_appended(0, r)
-    eng.end_layer_use(0, [0])  # capacity 0: the partly filled page 0 is evicted
+    eng.end_layer_use(0, [0])
+    r1 = cache.append_chunk(1, k, v)  # layer 1's page takes the one device page: layer 0's tail goes out
+    eng.on_pages_appended(1, r1)
+    eng.end_layer_use(1, [0])
     assert cache.tier(0, 0) == 1
     with pytest.raises(ResidencyError):
         cache.append_chunk(0, k, v)
