@@ -176,7 +176,7 @@ def offload_measure(run, cap_frac: float):
         if eng is not None:
             out.update(cap_pages=cap, h2d_bytes=eng.h2d_bytes(0) + eng.h2d_bytes(1), d2h_bytes=eng.d2h_bytes())
             eng.release_all_reservations()
-            eng.close()
+            eng.close(discard=True)  # the measurement is over: host-tier pages are not needed
         del loop, eng, cache
         torch.cuda.empty_cache()
         return out
@@ -281,7 +281,7 @@ class Run:
         torch = self.torch
         out = self.o_all[i] if out is None else out
         if self.layer is None or not self.layer.split_pages:
-            sel = self.sels[i] if self.layer is None else self.subs[i]
+            sel = self.sels[i]
             return self.A.attn_forward(self.mc, q, self.cache, 0, sel, k, v, stream=stream, out=out,
                                        lse=self.lse_all[i])
         b = i & 1
@@ -322,8 +322,7 @@ class Run:
             self.ev_flat[b] = ev
             return g
         g = self.grads if grads is None else grads
-        sel = self.sels[i] if self.layer is None else self.subs[i]
-        saved = self.A.AttnSaved(self.o_all[i], self.lse_all[i], sel)
+        saved = self.A.AttnSaved(self.o_all[i], self.lse_all[i], self.sels[i])
         self.A.attn_backward(self.mc, do, q, self.cache, 0, k, v, saved, stream=stream, grads=g, defer_dq=defer_dq)
         self.cache.accumulate_grad_pages(0, self.own[i], g.dk_cur, g.dv_cur, stream=stream)
         return g

@@ -64,17 +64,17 @@ BwdWs carve(const AttnGeom& g, void* ws) {
 
 // ---------------------------------------------------------------- prep kernels
 __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-                                const float* __restrict__ lse, int C, int Hq, float* __restrict__ Dt,
+                                const float* __restrict__ lse, int C, int Hq, int hd, float* __restrict__ Dt,
                                 float* __restrict__ Lt) {
-    // two (token, head) rows per warp: 16 lanes x 16 B of O and dO each
+    // two (token, head) rows per warp: up to 16 lanes x 16 B of O and dO each (hd 64: 8 lanes)
     const int64_t row = (static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * 2 +
                         ((threadIdx.x >> 4) & 1);
     const int l16 = threadIdx.x & 15;
     const bool ok = row < static_cast<int64_t>(C) * Hq;
     float s = 0.f;
-    if (ok) {
-        const uint4 a = reinterpret_cast<const uint4*>(o + row * kHd)[l16];
-        const uint4 b = reinterpret_cast<const uint4*>(dout + row * kHd)[l16];
+    if (ok && l16 * 8 < hd) {
+        const uint4 a = reinterpret_cast<const uint4*>(o + row * hd)[l16];
+        const uint4 b = reinterpret_cast<const uint4*>(dout + row * hd)[l16];
         const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
         const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
 #pragma unroll
@@ -209,10 +209,9 @@ __global__ void __launch_bounds__(384, 1)
     const int h = blockIdx.x;
     const int qt = (g.C / kTile) - 1 - blockIdx.y;  // longest causal prefixes first
     const int kvh = h / g.group;
+    const bool p64 = g.P == kHalf;  // two query pages per tile, 64-key half blocks (tc_common.cuh)
     const int qp = (qt * kTile) / g.P;
     const int sel_begin = p.sel_off[qp];
-    const int n_past = (p.sel_off[qp + 1] - sel_begin) * (g.P / kTile);
-    const int nb = n_past + (g.chunk_keys ? qt + 1 : 0);
     const int warp = warp_id(), lane = lane_id();
 
     if (threadIdx.x == 0) {
@@ -235,9 +234,13 @@ __global__ void __launch_bounds__(384, 1)
     }
     if (warp == 3) tmem_alloc<512>(&bars->tmem_base);
     tc_fence_before();
-    __syncthreads();
+    HalfList hl{};
+    if (p64) hl = half_list_sync(p.sel_off, p.sel_ids, qt);  // (a barrier, like the one it replaces)
+    else __syncthreads();
     tc_fence_after();
     if (bars->tmem_base != 0) __trap();  // all 512 columns: base column 0 (the constants rely on it)
+    const int n_past = p64 ? hl.blocks() : (p.sel_off[qp + 1] - sel_begin) * (g.P / kTile);
+    const int nb = n_past + (g.chunk_keys ? qt + 1 : 0);
     uint8_t* sQ = smem + kDqQ;
     uint8_t* sDO = smem + kDqDO;
     uint8_t* sK = smem + kDqK;
@@ -256,7 +259,13 @@ __global__ void __launch_bounds__(384, 1)
                 if (kDqAlias && j == 3) mbar_wait(&bars->qdo_tmem, 0);  // K stage 3 is the Q tile
                 mbar_expect_tx(&bars->k_full[st], kTileBytes);
                 uint8_t* dst = sK + st * kTileBytes;
-                if (j < n_past) {
+                if (j < n_past && p64) {
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int row = past_half_row(g, p.sel_ids, p.kvslot, hl, 2 * j + hh, kvh, p.err);
+                        for (int r = 0; r < 2; ++r)
+                            tma_load_2d(dst + r * kRegion + hh * (kRegion / 2), &tm_kp, &bars->k_full[st], r * 64, row);
+                    }
+                } else if (j < n_past) {
                     const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, j, kvh, p.err);
                     for (int r = 0; r < 2; ++r) tma_load_2d(dst + r * kRegion, &tm_kp, &bars->k_full[st], r * 64, b.row);
                 } else {
@@ -273,7 +282,13 @@ __global__ void __launch_bounds__(384, 1)
                 if (kDqAlias && j == 0) mbar_wait(&bars->qdo_tmem, 0);  // V stage 0 is the dO tile
                 mbar_expect_tx(&bars->v_full[st], kTileBytes);
                 uint8_t* dst = sV + st * kTileBytes;
-                if (j < n_past) {
+                if (j < n_past && p64) {
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int row = past_half_row(g, p.sel_ids, p.kvslot, hl, 2 * j + hh, kvh, nullptr);
+                        for (int r = 0; r < 2; ++r)
+                            tma_load_2d(dst + r * kRegion + hh * (kRegion / 2), &tm_vp, &bars->v_full[st], r * 64, row);
+                    }
+                } else if (j < n_past) {
                     const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, j, kvh, nullptr);
                     for (int r = 0; r < 2; ++r) tma_load_2d(dst + r * kRegion, &tm_vp, &bars->v_full[st], r * 64, b.row);
                 } else {
@@ -350,11 +365,15 @@ __global__ void __launch_bounds__(384, 1)
         const float Dr = p.Dt[static_cast<int64_t>(h) * g.C + t];
         const uint32_t tS = kDqTmS + wg * 64 + lane_off, tDP = kDqTmDP + wg * 64 + lane_off;
         uint8_t* nvt = smem + kDqNv;
-        stage_past_valid(g, p.sel_ids, sel_begin, n_past, nvt, kDqNvCap, threadIdx.x - 128, 256);
+        uint16_t* hvt = reinterpret_cast<uint16_t*>(nvt);
+        if (p64) stage_half_valid(g, p.sel_ids, hl, hvt, kDqNvCap / 2, threadIdx.x - 128, 256);
+        else stage_past_valid(g, p.sel_ids, sel_begin, n_past, nvt, kDqNvCap, threadIdx.x - 128, 256);
         named_bar_sync(3, 256);
         for (int j = 0; j < nb; ++j) {
             int lim;  // keep key columns c <= lim (of this group's 64)
-            if (j < n_past) {
+            if (j < n_past && p64) {  // the group's 64 columns are half block 2j + wg
+                lim = half_lim(half_valid(g, p.sel_ids, hl, hvt, kDqNvCap / 2, 2 * j + wg), r);
+            } else if (j < n_past) {
                 lim = past_valid(g, p.sel_ids, sel_begin, nvt, kDqNvCap, j) - 1 - wg * 64;
             } else {
                 lim = ((j - n_past == qt) ? r : kTile - 1) - wg * 64;
@@ -421,7 +440,7 @@ __global__ void __launch_bounds__(384, 1)
         fence_proxy_async_smem();
         named_bar_sync(1, 256);
         if (warp == 4 && lane == 0) {
-            for (int c = 0; c < kHd / 32; ++c) tma_store_3d(&tmap_dq, stage + c * kSliceBytes, c * 32, h, qt * kTile);
+            for (int c = 0; c < g.hd / 32; ++c) tma_store_3d(&tmap_dq, stage + c * kSliceBytes, c * 32, h, qt * kTile);
             bulk_commit();
             bulk_wait_read0();
         }
@@ -463,8 +482,9 @@ constexpr int kKvQ = kKvV + kTileBytes;                  // kKvStages stages of 
 constexpr int kKvDO = kKvQ + kKvStages * kTileBytes;     // kKvStages stages
 constexpr int kKvStage = kKvDO + kKvStages * kTileBytes; // epilogue: one [128 x 32] fp32 slice per warpgroup
 constexpr int kKvLD = kKvStage + 2 * kSliceBytes;        // kKvStages stages of {L[128], D[128]} fp32 (TMA bulk)
+constexpr int kKvUnitBytes = 160;
 constexpr int kKvDesc = kKvLD + kKvStages * 1024;        // 2 unit descriptors
-constexpr int kKvBar = kKvDesc + 256;
+constexpr int kKvBar = kKvDesc + 2 * kKvUnitBytes;
 constexpr int kKvSmem = kKvBar + 256;                    // the dynamic smem base is 1024-aligned (checked)
 static_assert(kKvSmem <= 232448, "dynamic shared memory above the 227 KB opt-in limit");
 constexpr uint32_t kTmS = 0, kTmDP = 128, kTmDK = 256, kTmDV = 384;
@@ -484,15 +504,18 @@ struct KvUnit {
     int past;
     int key0;      // first key of the block (chunk-relative for in-chunk, page-relative for past)
     int n_items;
-    int n_qps;     // past: number of query pages in the list
+    int n_qps;     // past: number of query pages in the list (page size 64: of 128-row query tiles)
     int g_kv;
-    int kv_row;    // pool tensor-map row of the K/V block (past)
-    int g_row;     // grad-pool tensor-map row (past)
-    int n_valid;   // valid keys of the block
+    int kv_row;    // pool tensor-map row of the K/V block (past; page size 64: of the first page)
+    int g_row;     // grad-pool tensor-map row (past; page size 64: of the first page)
+    int n_valid;   // valid keys of the block (page size 64: of the first page)
     int pad;
-    uint8_t qps[64];  // past: the query pages that selected the page, ascending
+    // page size 64: a past unit is two pages of the ascending union, keys [0,64) and [64,128)
+    int kv_row1, g_row1, n_valid1, has1;
+    uint64_t qm0, qm1;  // the query pages that selected each page (bit qp)
+    uint8_t qps[64];  // past: the query pages that selected the page, ascending (page size 64: query tiles)
 };
-static_assert(sizeof(KvUnit) <= 128, "unit descriptor");
+static_assert(sizeof(KvUnit) <= kKvUnitBytes, "unit descriptor");
 
 // K step ks (16 queries) of a packed P^T / dS^T operand: queries [64w, 64w+64) of warpgroup w
 // sit in the first 32 of its own 64 columns.
@@ -538,9 +561,13 @@ struct ItemIter {
 // fastest) into a unit descriptor.
 __device__ void decode_unit(const BwdParams& p, int w, KvUnit& u) {
     const AttnGeom& g = p.g;
+    const bool p64 = g.P == kHalf;
     const int n_chunk_blocks = g.chunk_keys ? g.C / kTile : 0, bpp = g.P / kTile;
-    const int n_units = (n_chunk_blocks + *p.n_uni * bpp) * g.Hkv;
+    const int n_past_units = p64 ? (*p.n_uni + 1) / 2 : *p.n_uni * bpp;
+    const int n_units = (n_chunk_blocks + n_past_units) * g.Hkv;
     u.valid = w < n_units;
+    u.has1 = 0;
+    u.qm0 = u.qm1 = 0ull;
     if (!u.valid) return;
     const int unit = w / g.Hkv;
     u.g_kv = w % g.Hkv;
@@ -553,6 +580,37 @@ __device__ void decode_unit(const BwdParams& p, int w, KvUnit& u) {
         return;
     }
     const int pu = unit - n_chunk_blocks;
+    if (p64) {  // two consecutive pages of the union; items = the 128-row tiles either page is attended by
+        u.past = 1;
+        u.key0 = 0;
+        const int pa = p.uni[2 * pu];
+        u.has1 = 2 * pu + 1 < *p.n_uni;
+        const int pb = u.has1 ? p.uni[2 * pu + 1] : pa;
+        u.qm0 = p.mask[pa];
+        u.qm1 = u.has1 ? p.mask[pb] : 0ull;
+        const uint64_t any = u.qm0 | u.qm1;
+        int k = 0;
+        for (int qt = 0; qt < 32; ++qt)
+            if ((any >> (2 * qt)) & 3ull) u.qps[k++] = static_cast<uint8_t>(qt);
+        u.n_qps = k;
+        u.n_items = k * g.group;
+        const int64_t nva = g.filled - static_cast<int64_t>(pa) * g.P, nvb = g.filled - static_cast<int64_t>(pb) * g.P;
+        u.n_valid = static_cast<int>(nva < 0 ? 0 : (nva > kHalf ? kHalf : nva));
+        u.n_valid1 = u.has1 ? static_cast<int>(nvb < 0 ? 0 : (nvb > kHalf ? kHalf : nvb)) : 0;
+        const int ka = p.kvslot[pa], ga = p.gslot[pa];
+        const int kb = p.kvslot[pb], gb = p.gslot[pb];
+        if (ka < 0 || ga < 0 || (u.has1 && (kb < 0 || gb < 0))) {
+            atomicOr(p.err, DERR_NOT_RESIDENT);
+            u.n_items = 0;
+            u.kv_row = u.g_row = u.kv_row1 = u.g_row1 = 0;
+            return;
+        }
+        u.kv_row = (ka * g.Hkv + u.g_kv) * g.P;
+        u.g_row = (ga * g.Hkv + u.g_kv) * g.P;
+        u.kv_row1 = u.has1 ? (kb * g.Hkv + u.g_kv) * g.P : -2 * kHalf;  // out of bounds: TMA zero fill
+        u.g_row1 = u.has1 ? (gb * g.Hkv + u.g_kv) * g.P : 0;
+        return;
+    }
     const int pid = p.uni[pu / bpp];
     const int sub = pu % bpp;
     u.past = 1;
@@ -585,9 +643,10 @@ __global__ void __launch_bounds__(384, 1)
                          BwdParams p, int* work_counter) {
     extern __shared__ __align__(1024) uint8_t smem[];
     KvBars* bars = reinterpret_cast<KvBars*>(smem + kKvBar);
-    KvUnit* desc = reinterpret_cast<KvUnit*>(smem + kKvDesc);
+    KvUnit* desc = reinterpret_cast<KvUnit*>(smem + kKvDesc);  // 2 x kKvUnitBytes
     const AttnGeom& g = p.g;
-    const int tpq = g.P / kTile;
+    const bool p64 = g.P == kHalf;
+    const int tpq = p64 ? 1 : g.P / kTile;  // page size 64: a past unit lists 128-row query tiles directly
     const int warp = warp_id(), lane = lane_id();
     if (threadIdx.x == 0) {
         if (smem_u32(smem) & 1023) __trap();  // SW128 operands and the smem budget need a 1 KB-aligned base
@@ -632,7 +691,12 @@ __global__ void __launch_bounds__(384, 1)
                 if (un >= 1) mbar_wait(&bars->kv_empty, (un - 1) & 1);  // the previous unit's last S / dP
                 mbar_expect_tx(&bars->kv_full, 2 * kTileBytes);
                 for (int r = 0; r < 2; ++r) {
-                    if (u.past) {
+                    if (u.past && p64) {  // two 64-row pages (pool maps with 64-row boxes)
+                        tma_load_2d(sK + r * kRegion, &tm_kp, &bars->kv_full, r * 64, u.kv_row);
+                        tma_load_2d(sV + r * kRegion, &tm_vp, &bars->kv_full, r * 64, u.kv_row);
+                        tma_load_2d(sK + r * kRegion + kRegion / 2, &tm_kp, &bars->kv_full, r * 64, u.kv_row1);
+                        tma_load_2d(sV + r * kRegion + kRegion / 2, &tm_vp, &bars->kv_full, r * 64, u.kv_row1);
+                    } else if (u.past) {
                         tma_load_2d(sK + r * kRegion, &tm_kp, &bars->kv_full, r * 64, u.kv_row);
                         tma_load_2d(sV + r * kRegion, &tm_vp, &bars->kv_full, r * 64, u.kv_row);
                     } else {
@@ -753,16 +817,22 @@ __global__ void __launch_bounds__(384, 1)
             const int n = u.n_items;
             const bool past = u.past;
             const int key0 = u.key0, g_row = u.g_row, g_kv = u.g_kv;
-            const bool key_ok = kr < u.n_valid;
-            const bool page_full = u.n_valid == kTile;
+            // page size 64: key rows [0,64) are the unit's first page, [64,128) its second
+            const bool half1 = p64 && past && kr >= kHalf;
+            const bool key_ok = p64 && past ? (kr & (kHalf - 1)) < (half1 ? u.n_valid1 : u.n_valid) : kr < u.n_valid;
+            const uint64_t qm = half1 ? u.qm1 : u.qm0;
+            const int g_row1 = u.g_row1, has1 = u.has1;
+            const bool page_full = !(p64 && past) && u.n_valid == kTile;
             ItemIter it;
             it.init(u, g.group, tpq);
             for (int i = 0; i < n; ++i, it.next(u, g.group, tpq)) {
                 const int gj = gi + i;
                 const int st = gj % kKvStages;
                 const uint32_t lrow = smem_u32(smem + kKvLD) + st * 1024 + wg * 256, drow = lrow + 512;
-                // visible iff query column c >= lim (causal diagonal: key row <= query row)
-                const int lim = key_ok ? (it.diag ? kr - wg * 64 : 0) : 1 << 20;
+                // visible iff query column c >= lim (causal diagonal: key row <= query row); page size 64:
+                // this group's 64 query columns are query page 2 qt + wg, which may not have chosen the page
+                const bool ok = key_ok && (!(p64 && past) || ((qm >> (2 * it.qt + wg)) & 1ull));
+                const int lim = ok ? (it.diag ? kr - wg * 64 : 0) : 1 << 20;
                 const bool masked = it.diag || !page_full;
                 mbar_wait(&bars->qdo_full[st], (gj / kKvStages) & 1);  // makes the bulk-copied L / D visible
                 // ---- P^T = exp2(S^T sl2 - L): computed as soon as S^T lands, packed in place
@@ -841,6 +911,7 @@ __global__ void __launch_bounds__(384, 1)
                 // ---- four [128 x 32] slices through this group's staging buffer into L2 / dk_cur / dv_cur
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
+                    if (c * 32 >= g.hd) break;         // head dim 64: columns 64-127 are zero padding
                     if (issuer) bulk_wait_read0();     // the previous slice has left the staging buffer
                     named_bar_sync(4 + wg, 128);
 #pragma unroll
@@ -853,8 +924,14 @@ __global__ void __launch_bounds__(384, 1)
                     fence_proxy_async_smem();
                     named_bar_sync(4 + wg, 128);
                     if (issuer) {
-                        if (past) tma_reduce_add_2d(wg ? &tm_gv : &tm_gk, stage, c * 32, g_row);
-                        else tma_store_3d(wg ? &tm_dvc : &tm_dkc, stage, c * 32, g_kv, key0);
+                        if (past && p64) {  // 64-row boxes into each page's gradient block
+                            tma_reduce_add_2d(wg ? &tm_gv : &tm_gk, stage, c * 32, g_row);
+                            if (has1) tma_reduce_add_2d(wg ? &tm_gv : &tm_gk, stage + kSliceBytes / 2, c * 32, g_row1);
+                        } else if (past) {
+                            tma_reduce_add_2d(wg ? &tm_gv : &tm_gk, stage, c * 32, g_row);
+                        } else {
+                            tma_store_3d(wg ? &tm_dvc : &tm_dkc, stage, c * 32, g_kv, key0);
+                        }
                         bulk_commit();
                     }
                 }
@@ -896,7 +973,8 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     ProfScope* prep_scope = new ProfScope(PK_BWD_PREP, st);
     const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
     bwd_prep_kernel<<<static_cast<unsigned>((rows + 15) / 16), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), lse, g.C, g.Hq, w.Dt, w.Lt);
+        static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), lse, g.C, g.Hq, g.hd, w.Dt,
+        w.Lt);
     check_launch("bwd_prep_kernel");
     if (n_pages > 0) OOMB_CUDA(cudaMemsetAsync(w.mask, 0, static_cast<size_t>(n_pages) * 8, st));
     OOMB_CUDA(cudaMemsetAsync(w.n_uni, 0, 2 * sizeof(int32_t), st));  // union count + dK/dV work counter
@@ -906,10 +984,12 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         bwd_union_kernel<<<1, 1024, 0, st>>>(w.mask, n_pages, w.uni, w.n_uni);
         check_launch("bwd_union_kernel");
     }
-    const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, kHd);
-    const CUtensorMap tdo = map_rows_heads(dout, g.C, g.Hq, kHd);
-    const CUtensorMap tkc = map_rows_heads(k_cur, g.C, g.Hkv, kHd);
-    const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, kHd);
+    // head dim 64: the 128-wide tiles carry zeros in columns 64-127 (TMA out-of-bounds fill) and the
+    // stores of those columns fall outside the tensors (clipped): see launch_attn_fwd_tc4
+    const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, g.hd);
+    const CUtensorMap tdo = map_rows_heads(dout, g.C, g.Hq, g.hd);
+    const CUtensorMap tkc = map_rows_heads(k_cur, g.C, g.Hkv, g.hd);
+    const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, g.hd);
     BwdParams p{g, sel_off, sel_ids, d_kvslot_layer, d_gslot_layer, gkpool, gvpool, w.Dt, w.Lt, w.mask, w.uni,
                 w.n_uni, dq, dk_cur, dv_cur, d_err, CtaTrace{}};
     delete prep_scope;
@@ -925,7 +1005,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     OOMB_CUDA(cudaStreamWaitEvent(side, ev_prep, 0));
     auto launch_dq = [&] {
         ProfScope s_(PK_BWD_DQ, side);
-        const CUtensorMap tdq = map_rows_heads_f32(dq, g.C, g.Hq, kHd);
+        const CUtensorMap tdq = map_rows_heads_f32(dq, g.C, g.Hq, g.hd);
         attn_bwd_dq_kernel<<<dim3(g.Hq, g.C / kTile), 384, kDqSmem, side>>>(tq, tdo, tkc, tvc, maps.kpool,
                                                                             maps.vpool, tdq, p);
         check_launch("attn_bwd_dq_kernel");
@@ -935,13 +1015,14 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         ProfScope s_(PK_BWD_DKDV, st);
         const int max_union = std::min(nnz, n_pages);
         if (!g.chunk_keys) {  // past-only shard: the chunk's own keys are another shard's
-            OOMB_CUDA(cudaMemsetAsync(dk_cur, 0, static_cast<size_t>(g.C) * g.Hkv * kHd * sizeof(float), st));
-            OOMB_CUDA(cudaMemsetAsync(dv_cur, 0, static_cast<size_t>(g.C) * g.Hkv * kHd * sizeof(float), st));
+            OOMB_CUDA(cudaMemsetAsync(dk_cur, 0, static_cast<size_t>(g.C) * g.Hkv * g.hd * sizeof(float), st));
+            OOMB_CUDA(cudaMemsetAsync(dv_cur, 0, static_cast<size_t>(g.C) * g.Hkv * g.hd * sizeof(float), st));
         }
-        const int units = ((g.chunk_keys ? g.C / kTile : 0) + max_union * (g.P / kTile)) * g.Hkv;
+        const int past_units = g.P == kHalf ? (max_union + 1) / 2 : max_union * (g.P / kTile);
+        const int units = ((g.chunk_keys ? g.C / kTile : 0) + past_units) * g.Hkv;
         const int n_ctas = std::max(1, std::min(units, num_sms));
-        const CUtensorMap tdkc = map_rows_heads_f32(dk_cur, g.C, g.Hkv, kHd);
-        const CUtensorMap tdvc = map_rows_heads_f32(dv_cur, g.C, g.Hkv, kHd);
+        const CUtensorMap tdkc = map_rows_heads_f32(dk_cur, g.C, g.Hkv, g.hd);
+        const CUtensorMap tdvc = map_rows_heads_f32(dv_cur, g.C, g.Hkv, g.hd);
         attn_bwd_dkdv_kernel<<<n_ctas, 384, kKvSmem, st>>>(tq, tdo, tkc, tvc, maps.kpool, maps.vpool, maps.gkpool,
                                                             maps.gvpool, tdkc, tdvc, p, w.n_uni + 1);
         check_launch("attn_bwd_dkdv_kernel");

@@ -80,10 +80,9 @@ __global__ void __launch_bounds__(384, 1)
     const int h = blockIdx.x;
     const int qt = (g.C / kTile) - 1 - static_cast<int>(blockIdx.y);  // longest causal prefix first (LPT)
     const int kvh = h / g.group;
+    const bool p64 = g.P == kHalf;  // two query pages per tile, 64-key half blocks (tc_common.cuh)
     const int qp = (qt * kTile) / g.P;
     const int sel_begin = p.sel_off[qp];
-    const int n_past = (p.sel_off[qp + 1] - sel_begin) * (g.P / kTile);
-    const int nb = n_past + (g.chunk_keys ? qt + 1 : 0);
     const int warp = warp_id(), lane = lane_id();
 
     if (threadIdx.x == 0) {
@@ -106,9 +105,13 @@ __global__ void __launch_bounds__(384, 1)
     }
     if (warp == 3) tmem_alloc<512>(&bars->tmem_base);
     tc_fence_before();
-    __syncthreads();
+    HalfList hl{};
+    if (p64) hl = half_list_sync(p.sel_off, p.sel_ids, qt);  // (a barrier, like the one it replaces)
+    else __syncthreads();
     tc_fence_after();
     if (bars->tmem_base != 0) __trap();  // all 512 columns: base column 0 (the constants rely on it)
+    const int n_past = p64 ? hl.blocks() : (p.sel_off[qp + 1] - sel_begin) * (g.P / kTile);
+    const int nb = n_past + (g.chunk_keys ? qt + 1 : 0);
     uint8_t* sQ = smem + kF4Q;
     uint8_t* sK = smem + kF4K;
     uint8_t* sV = smem + kF4V;
@@ -131,7 +134,13 @@ __global__ void __launch_bounds__(384, 1)
                 if (j >= nst) mbar_wait(&empty[st], ((j / nst) - 1) & 1);
                 mbar_expect_tx(&full[st], kTileBytes);
                 uint8_t* dst = base + st * kTileBytes;
-                if (j < n_past) {
+                if (j < n_past && p64) {  // two 64-row half blocks (pool maps with 64-row boxes)
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int row = past_half_row(g, p.sel_ids, p.kvslot, hl, 2 * j + hh, kvh, is_k ? p.err : nullptr);
+                        for (int r = 0; r < 2; ++r)
+                            tma_load_2d(dst + r * kRegion + hh * (kRegion / 2), mp, &full[st], r * 64, row);
+                    }
+                } else if (j < n_past) {
                     const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, j, kvh, is_k ? p.err : nullptr);
                     for (int r = 0; r < 2; ++r) tma_load_2d(dst + r * kRegion, mp, &full[st], r * 64, b.row);
                 } else {
@@ -189,26 +198,34 @@ __global__ void __launch_bounds__(384, 1)
         const int r = quarter * 32 + lane;  // query row = TMEM lane
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         uint8_t* nvt = smem + kF4Nv;
-        stage_past_valid(g, p.sel_ids, sel_begin, n_past, nvt, kF4NvCap, threadIdx.x - 128, 256);
+        uint16_t* hvt = reinterpret_cast<uint16_t*>(nvt);
+        if (p64) stage_half_valid(g, p.sel_ids, hl, hvt, kF4NvCap / 2, threadIdx.x - 128, 256);
+        else stage_past_valid(g, p.sel_ids, sel_begin, n_past, nvt, kF4NvCap, threadIdx.x - 128, 256);
         named_bar_sync(3, 256);
         const float sl2 = g.scale * kLog2e;
         const uint32_t tS = kTmS + wg * 128 + lane_off, tO = kTmO + wg * 128 + lane_off;
         float m = -INFINITY;  // this group's running row max (log2 units) that O_w and l are relative to
         float l = 0.f;
         for (int j = wg; j < nb; j += 2) {
-            int lim;  // keep key columns c <= lim
-            if (j < n_past) lim = past_valid(g, p.sel_ids, sel_begin, nvt, kF4NvCap, j) - 1;
-            else lim = (j - n_past == qt) ? r : kTile - 1;
+            int lo, hi;  // keep key columns c <= lo (c < 64) / c <= hi (c >= 64)
+            if (j < n_past && p64) {
+                lo = half_lim(half_valid(g, p.sel_ids, hl, hvt, kF4NvCap / 2, 2 * j), r);
+                hi = kHalf + half_lim(half_valid(g, p.sel_ids, hl, hvt, kF4NvCap / 2, 2 * j + 1), r);
+            } else {
+                lo = (j < n_past) ? past_valid(g, p.sel_ids, sel_begin, nvt, kF4NvCap, j) - 1
+                                  : ((j - n_past == qt) ? r : kTile - 1);
+                hi = lo;
+            }
             mbar_wait(&bars->s_full[wg], (j >> 1) & 1);
             tc_fence_after();
             uint32_t sr[128];
 #pragma unroll
             for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
             tmem_wait_ld();
-            if (lim < kTile - 1) {
+            if (lo < kHalf - 1 || hi < kTile - 1) {
 #pragma unroll
                 for (int c = 0; c < kTile; ++c)
-                    if (c > lim) sr[c] = __float_as_uint(-INFINITY);
+                    if (c > (c < kHalf ? lo : hi)) sr[c] = __float_as_uint(-INFINITY);
             }
             float mx8[8];
 #pragma unroll
@@ -275,10 +292,11 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(&bars->o_done, 0);
         tc_fence_after();
         const int t = qt * kTile + r;
-        // group w writes output columns [64w, 64w + 64)
-        __nv_bfloat16* orow = p.out + (static_cast<int64_t>(t) * g.Hq + h) * kHd + wg * 64;
+        // group w writes output columns [64w, 64w + 64) (head dim 64: group 0 only; columns 64-127
+        // of O are the zero padding of the 128-wide tiles, see launch_attn_fwd_tc4)
+        __nv_bfloat16* orow = p.out + (static_cast<int64_t>(t) * g.Hq + h) * g.hd + wg * 64;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < (wg * 64 < g.hd ? 4 : 0); ++c) {
             uint32_t x0[16], x1[16];
             tmem_ld16(kTmO + wg * 64 + c * 16 + lane_off, x0);
             tmem_ld16(kTmO + 128 + wg * 64 + c * 16 + lane_off, x1);
@@ -307,9 +325,11 @@ void launch_attn_fwd_tc4(const AttnGeom& g, const TcPoolMaps& maps, const void* 
                          void* out, float* lse, int* d_err, cudaStream_t st) {
     if (first_use_on_device(1))
         OOMB_CUDA(cudaFuncSetAttribute(attn_fwd_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kF4Smem));
-    const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, kHd);
-    const CUtensorMap tkc = map_rows_heads(k_cur, g.C, g.Hkv, kHd);
-    const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, kHd);
+    // Head dim 64 runs the 128-wide tiles with the upper 64 columns zero: TMA fills the boxes past
+    // the tensor's hd columns with zeros, so S = Q K^T is exact and O's upper columns stay 0.
+    const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, g.hd);
+    const CUtensorMap tkc = map_rows_heads(k_cur, g.C, g.Hkv, g.hd);
+    const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, g.hd);
     F4Params p{g, sel_off, sel_ids, d_kvslot_layer, static_cast<__nv_bfloat16*>(out), lse, d_err};
     attn_fwd_tc4_kernel<<<dim3(g.Hq, g.C / kTile), 384, kF4Smem, st>>>(tq, tkc, tvc, maps.kpool, maps.vpool, p);
     check_launch("attn_fwd_tc4_kernel");

@@ -14,10 +14,15 @@ namespace {
 constexpr int kTile = 128;                     // query rows per CTA, keys per block
 constexpr int kHd = 128;                       // head dim of the tensor-core path
 constexpr int kRegion = kTile * 64 * 2;        // one [128 x 64] bf16 SW128 region = 16 KB
+constexpr int kHalf = 64;                      // page size 64: one page per TMA box
 }  // namespace
 
+// Head dim 128, or 64 on the same 128-wide tiles (upper columns zero, TMA out-of-bounds fill);
+// page size a multiple of 128, or 64 (query tiles of two query pages, 64-key half blocks; BASELINE
+// configs[0]). Chunks of whole 128-row tiles.
 bool tc_supported(const AttnGeom& g, int dtype) {
-    return dtype == OOMB_BF16 && g.hd == kHd && g.P % kTile == 0 && g.C % kTile == 0;
+    return dtype == OOMB_BF16 && (g.hd == kHd || g.hd == 64) && (g.P % kTile == 0 || g.P == kHalf) &&
+           g.C % kTile == 0;
 }
 
 static void encode_or_throw(CUtensorMap* m, uint32_t rank, const void* base, const uint64_t* dims,
@@ -31,13 +36,14 @@ void make_pool_maps(TcPoolMaps& maps, const void* kpool, const void* vpool, int6
                     const float* gvpool, int64_t n_g_slots, int Hkv, int P, int hd) {
     const uint64_t dims[2] = {static_cast<uint64_t>(hd), static_cast<uint64_t>(n_slots) * Hkv * P};
     const uint64_t strides[1] = {static_cast<uint64_t>(hd) * 2};
-    const uint32_t box[2] = {64, kTile};
+    const uint32_t rows = P == kHalf ? kHalf : kTile;  // page size 64: one page per box
+    const uint32_t box[2] = {64, rows};
     encode_or_throw(&maps.kpool, 2, kpool, dims, strides, box);
     encode_or_throw(&maps.vpool, 2, vpool, dims, strides, box);
     // fp32 gradient pools: 32-column boxes (128 B rows) for the dK/dV TMA reduce-add epilogue
     const uint64_t gdims[2] = {static_cast<uint64_t>(hd), static_cast<uint64_t>(n_g_slots) * Hkv * P};
     const uint64_t gstrides[1] = {static_cast<uint64_t>(hd) * 4};
-    const uint32_t gbox[2] = {32, kTile};
+    const uint32_t gbox[2] = {32, rows};
     CUresult r = encode_tensor_map(&maps.gkpool, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(gkpool), gdims,
                                    gstrides, gbox, CU_TENSOR_MAP_SWIZZLE_128B);
     if (r == CUDA_SUCCESS)

@@ -339,7 +339,8 @@ int oomb_pool_create(const oomb_config* cfg, int device, oomb_pool_t* out) {
             OOMB_CUDA(cudaMemset(p->d_kavg_cnt, 0, tab));
             OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->d_err), sizeof(int)));
             OOMB_CUDA(cudaMemset(p->d_err, 0, sizeof(int)));
-            if (c.dtype == OOMB_BF16 && c.head_dim == 128 && c.page_size % 128 == 0)
+            if (c.dtype == OOMB_BF16 && (c.head_dim == 128 || c.head_dim == 64) &&
+                (c.page_size % 128 == 0 || c.page_size == 64))
                 make_pool_maps(p->maps, p->kpool, p->vpool, p->n_kv_slots, p->gkpool, p->gvpool, p->n_g_slots,
                                c.n_kv_heads, c.page_size, c.head_dim);
         } catch (...) {

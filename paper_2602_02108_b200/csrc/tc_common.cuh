@@ -167,5 +167,82 @@ __device__ __forceinline__ int past_valid(const AttnGeom& g, const int32_t* sel_
     return j < cap ? tab[j] : past_valid_global(g, sel_ids, sel_begin, j);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Page size 64 (BASELINE configs[0]). A 128-row query tile covers query pages 2qt (rows 0-63) and
+// 2qt+1 (rows 64-127), and its past keys come as 64-key half blocks, paired into the 128-key blocks
+// the kernels consume: when both pages' lists are equal (dense mode, or equal top-k lists) every
+// page of the list applies to all 128 rows; otherwise list A's pages (rows 0-63) come first, then
+// list B's (rows 64-127). A missing second half (odd count) is an out-of-bounds TMA box (zero
+// fill) and is masked. Key visit order does not change the softmax beyond rounding.
+// ---------------------------------------------------------------------------------------------
+constexpr int kHalf = 64;
+struct HalfList {
+    int a0, na, b0, nb, same;
+    __device__ __forceinline__ int count() const { return same ? na : na + nb; }
+    __device__ __forceinline__ int blocks() const { return (count() + 1) >> 1; }
+};
+// Every thread of the CTA must call it (it contains a barrier).
+__device__ __forceinline__ HalfList half_list_sync(const int32_t* off, const int32_t* ids, int qt) {
+    HalfList L;
+    L.a0 = off[2 * qt];
+    L.na = off[2 * qt + 1] - L.a0;
+    L.b0 = off[2 * qt + 1];
+    L.nb = off[2 * qt + 2] - L.b0;
+    int diff = 0;
+    if (L.na == L.nb)
+        for (int i = threadIdx.x; i < L.na; i += blockDim.x) diff |= ids[L.a0 + i] != ids[L.b0 + i];
+    const int any = __syncthreads_or(diff);
+    L.same = L.na == L.nb && !any;
+    return L;
+}
+__device__ __forceinline__ int half_page(const HalfList& L, const int32_t* ids, int h, int* rowmask) {
+    if (L.same) {
+        *rowmask = 3;
+        return ids[L.a0 + h];
+    }
+    if (h < L.na) {
+        *rowmask = 1;
+        return ids[L.a0 + h];
+    }
+    *rowmask = 2;
+    return ids[L.b0 + h - L.na];
+}
+// Table entry of half h: valid keys (0..64) | row-half mask << 8 (bit 0: rows 0-63, bit 1: rows 64-127).
+__device__ __forceinline__ uint16_t half_entry(const AttnGeom& g, const int32_t* ids, const HalfList& L, int h) {
+    if (h >= L.count()) return 0;
+    int mask;
+    const int pid = half_page(L, ids, h, &mask);
+    const int64_t nv = g.filled - static_cast<int64_t>(pid) * g.P;
+    if (pid < 0 || pid >= g.max_pages || nv <= 0) return 0;
+    return static_cast<uint16_t>((nv > kHalf ? kHalf : nv) | (mask << 8));
+}
+// Pool tensor-map row of half h for kv head kvh (an out-of-bounds row when absent / not resident).
+__device__ __forceinline__ int past_half_row(const AttnGeom& g, const int32_t* ids, const int32_t* kvslot,
+                                             const HalfList& L, int h, int kvh, int* err) {
+    if (h >= L.count()) return -2 * kHalf;
+    int mask;
+    const int pid = half_page(L, ids, h, &mask);
+    const bool id_ok = pid >= 0 && pid < g.max_pages && static_cast<int64_t>(pid) * g.P < g.filled;
+    const int slot = id_ok ? kvslot[pid] : -1;
+    if (slot < 0) {
+        if (err) atomicOr(err, id_ok ? DERR_NOT_RESIDENT : DERR_BAD_ID);
+        return -2 * kHalf;
+    }
+    return (slot * g.Hkv + kvh) * g.P;
+}
+__device__ __forceinline__ void stage_half_valid(const AttnGeom& g, const int32_t* ids, const HalfList& L,
+                                                 uint16_t* tab, int cap, int tid, int nthr) {
+    const int n = L.count();
+    for (int h = tid; h < n && h < cap; h += nthr) tab[h] = half_entry(g, ids, L, h);
+}
+__device__ __forceinline__ uint16_t half_valid(const AttnGeom& g, const int32_t* ids, const HalfList& L,
+                                               const uint16_t* tab, int cap, int h) {
+    return h < cap ? (h < L.count() ? tab[h] : 0) : half_entry(g, ids, L, h);
+}
+// Keep-limit of one 64-key half for query row r: keys [0, lim] of the half are visible.
+__device__ __forceinline__ int half_lim(uint16_t e, int r) {
+    return ((e >> 8) >> (r >> 6)) & 1 ? static_cast<int>(e & 0xff) - 1 : -1;
+}
+
 }  // namespace tc
 }  // namespace oomb

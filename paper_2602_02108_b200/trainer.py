@@ -379,7 +379,7 @@ class ChunkTrainer:
                 self.last_log = self.engine.raw_log()
         finally:
             if self.engine is not None:
-                self.engine.close()
+                self.engine.close(discard=True)  # the cache is reset every step (chunk_trainer.hpp:136)
                 self.engine = None
         loss = loss_sum / (t_total - 1) if t_total > 1 else 0.0
         return StepMetrics(loss), g

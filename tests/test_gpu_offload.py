@@ -55,7 +55,9 @@ def run(mode, capacity, n_chunks=6, seed=3, n_layers=2, pipelined=None):
         eng.release_all_reservations()
         log = eng.log()
         stats = (eng.h2d_bytes(0), eng.h2d_bytes(1), eng.d2h_bytes())
-        eng.close()  # the engine leaves; every page must now be readable again
+        # the engine leaves; the pool (capacity + 24 slots) cannot take every page back, and the
+        # outputs were read above: drop what stays on the host (close() would raise ResidencyError)
+        eng.close(discard=True)
     else:
         stats = None
     sels = [s.lists() for loop in loops for s in loop.sels]
@@ -154,7 +156,12 @@ def test_restore_all_needs_free_slots_and_keeps_data():
                 with pytest.raises(ConfigError):
                     eng.restore_all()
                 assert [p for p in range(cache.n_pages(0)) if cache.tier(0, p) != 0] == host  # nothing moved
-                eng.close()
+                from paper_2602_02108_b200.errors import ResidencyError
+                with pytest.raises(ResidencyError):  # detaching without room loses those pages, loudly
+                    eng.close()
+                assert all(cache.tier(0, p) == 3 for p in host)
+                with pytest.raises(ResidencyError):
+                    cache.gather_grad_pages(0, host[:1])
                 continue
             eng.restore_all()
             assert all(cache.tier(0, p) == 0 for p in range(cache.n_pages(0)))

@@ -317,6 +317,79 @@ def test_attention_bf16_parity(name, policy):
         assert rel(got[k], want[k]) < BF16_TOL, (name, policy, k, rel(got[k], want[k]))
 
 
+# tcgen05 path at head dim 64 and / or page size 64 (BASELINE configs[0]): the
+# 128-wide tiles carry zeros past hd 64; a 128-row query tile covers two 64-token query pages whose
+# lists are merged as 64-key half blocks (equal lists: every row; different lists: each page's rows).
+def _hd64_p128():
+    return Cfg(n_layers=1, n_q_heads=8, n_kv_heads=2, head_dim=64, chunk_size=256, page_size=128,
+               retrieval_budget=256, local_window=4)
+
+
+def _hd128_p64():
+    return Cfg(n_layers=1, n_q_heads=4, n_kv_heads=2, head_dim=128, chunk_size=256, page_size=64,
+               retrieval_budget=256, local_window=4)
+
+
+TC_SMALL_CASES = {
+    "c1_dense": (c1_cfg, 6 * 64, 61, None),
+    "c1_nopast": (c1_cfg, 0, 62, [[], [], [], []]),
+    "c1_distinct_lists": (c1_cfg, 7 * 64, 63, [[0, 3, 5], [1, 2], [5], [0, 4, 2, 1]]),  # odd half counts
+    "c1_equal_pairs": (c1_cfg, 7 * 64, 64, [[0, 2, 4], [0, 2, 4], [1, 3, 6, 5], [1, 3, 6, 5]]),
+    "c1_partial": (c1_cfg, 6 * 64 - 17, 65, [[0, 5], [5, 1], [2, 5, 3], [4]]),  # last past page partial
+    "c1_one_side_empty": (c1_cfg, 5 * 64, 66, [[], [0, 1, 2], [4, 3], []]),
+    "hd64_p128": (_hd64_p128, 5 * 128, 67, [[0, 3], [1, 4, 2]]),
+    "hd128_p64": (_hd128_p64, 7 * 64, 68, [[0, 6], [1, 2, 3], [6, 5, 4], [0]]),
+}
+
+
+@pytest.mark.parametrize("name", list(TC_SMALL_CASES))
+def test_tc_small_shapes_bf16_parity(name):
+    """policy "tcgen05" raises ConfigError if the shape would fall back to SIMT: these run on tensor cores."""
+    mk, past, seed, sel = TC_SMALL_CASES[name]
+    c = mk()
+    case = bf16_case(attn_case(c, past, seed=seed, dtype=np.float32, selected=sel))
+    got, _ = run_device(c, case, "bf16", "tcgen05")
+    want = run_oracle(c, case)
+    for k in ("out", "lse", "dq", "dk_cur", "dv_cur", "grad_k", "grad_v"):
+        assert rel(got[k], want[k]) < BF16_TOL, (name, k, rel(got[k], want[k]))
+
+
+def test_tc_c1_multichunk_matches_simt():
+    """A whole c1 layer (8K context, 32 chunks of 256, dense) through the public chunk loop on the
+    tcgen05 policy tracks the SIMT policy's run (itself 1e-5 to the oracle in fp32 elsewhere)."""
+    from paper_2602_02108_b200 import ModelConfig, PagedCache
+    from paper_2602_02108_b200 import attention as A
+    cfg = ModelConfig(n_layers=1, n_q_heads=4, n_kv_heads=1, head_dim=64, chunk_size=256, page_size=64,
+                      retrieval_budget=0, attention_mode=["dense"])
+    g = torch.Generator(device="cuda").manual_seed(7)
+    S = 32
+    q = [torch.randn(256, 4, 64, device="cuda", generator=g).bfloat16() for _ in range(S)]
+    k = [torch.randn(256, 1, 64, device="cuda", generator=g).bfloat16() for _ in range(S)]
+    v = [torch.randn(256, 1, 64, device="cuda", generator=g).bfloat16() for _ in range(S)]
+    do = [torch.randn(256, 4, 64, device="cuda", generator=g).bfloat16() for _ in range(S)]
+    res = {}
+    for policy in ("tcgen05", "simt"):
+        cache = PagedCache(cfg, dtype="bf16", max_tokens=S * 256)
+        cache.set_kernel_policy(policy)
+        saved = []
+        for i in range(S):
+            sel = [list(range(4 * i))] * 4
+            cache.append_chunk(0, k[i], v[i])
+            saved.append(A.attn_forward(cfg, q[i], cache, 0, sel, k[i], v[i]))
+        outs = [s.out.float() for s in saved]
+        dqs, dks = [], []
+        for i in reversed(range(S)):
+            gr = A.attn_backward(cfg, do[i], q[i], cache, 0, k[i], v[i], saved[i])
+            cache.accumulate_grad_pages(0, list(range(4 * i, 4 * i + 4)), gr.dk_cur, gr.dv_cur)
+            dqs.append(gr.dq.clone())
+            dks.append(torch.cat([gr.dk_cur, gr.dv_cur]))
+        torch.cuda.synchronize()
+        cache.check_device_errors()
+        res[policy] = (torch.stack(outs), torch.stack(dqs), torch.stack(dks))
+    for a, b in zip(res["tcgen05"], res["simt"]):
+        assert rel(T(a), T(b)) < BF16_TOL
+
+
 def test_tc_forward_dense_qwen_chunk():
     """Longer key lists (8 past pages x all 4 query pages) through the tcgen05 forward."""
     c = qwen_slice_cfg()
