@@ -38,6 +38,13 @@ class AttentionChunkLoop:
         self._presel: dict[int, A.Selection] = {}  # selections issued one chunk ahead (forward_chunk next_q)
         self._sel_stream = None
         self._votes = None
+        # per-chunk residency statistics when an engine is attached: (phase, chunk, pages the chunk
+        # needs resident, H2D bytes and D2H bytes the engine moved during the chunk's call)
+        self.chunk_stats: list[tuple[str, int, int, int, int]] = []
+
+    def _io(self) -> tuple[int, int]:
+        e = self.engine
+        return (e.h2d_bytes(0) + e.h2d_bytes(1), e.d2h_bytes()) if e is not None else (0, 0)
 
     # ---- selection (chunk_trainer.hpp:292-316)
     def _select(self, i: int, q: torch.Tensor, sel: A.Selection, stream=None) -> A.Selection:
@@ -95,6 +102,7 @@ class AttentionChunkLoop:
             (torch.cuda.current_stream() if stream is None else stream).wait_stream(self._sel_stream)
         eng = self.engine
         h = None
+        io0 = self._io()
         if eng is not None:
             h = eng.fetch_async(self.layer, self.union(sel), i)
         r = self.cache.append_chunk(self.layer, k, v, stream=stream)
@@ -109,6 +117,8 @@ class AttentionChunkLoop:
         saved = A.attn_forward(self.cfg, q, self.cache, self.layer, sel, k, v, stream=stream, out=out, lse=lse)
         if eng is not None:
             eng.end_layer_use(self.layer, np.concatenate([ids, self.own_pages(i)]))
+            io1 = self._io()
+            self.chunk_stats.append(("fwd", i, len(ids), io1[0] - io0[0], io1[1] - io0[1]))
         if i < len(self.saved):
             self.saved[i] = saved
         else:
@@ -119,6 +129,7 @@ class AttentionChunkLoop:
                        grads: A.AttnGrads | None = None) -> A.AttnGrads:
         eng = self.engine
         sel = self.sels[i]
+        io0 = self._io()
         if eng is not None:
             ids = np.union1d(self.union(sel), self.own_pages(i)).astype(np.int32)
             eng.wait(eng.fetch_async(self.layer, ids, i))
@@ -132,6 +143,8 @@ class AttentionChunkLoop:
         self.cache.accumulate_grad_pages(self.layer, self.own_pages(i), g.dk_cur, g.dv_cur, stream=stream)
         if eng is not None:
             eng.end_layer_use(self.layer, ids)
+            io1 = self._io()
+            self.chunk_stats.append(("bwd", i, len(ids), io1[0] - io0[0], io1[1] - io0[1]))
         return g
 
     def check_device_errors(self) -> None:

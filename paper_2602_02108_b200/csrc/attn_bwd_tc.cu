@@ -37,6 +37,22 @@ namespace {
 #endif
 constexpr bool kBwdPoly = OOMB_BWD_POLY != 0;  // one in four exp2 of P on the FMA pipe (ex2_poly)
 
+#ifndef OOMB_KV_TRACE
+#define OOMB_KV_TRACE 0  // per-CTA wait / phase cycle counters of the dK/dV kernel (OOMB_CTA_TRACE=dkdv:i:file)
+#endif
+#if OOMB_KV_TRACE
+#define KVT_WAIT(acc, bar, ph)                      \
+    do {                                            \
+        const long long t0_ = clock64();            \
+        mbar_wait(bar, ph);                         \
+        acc += clock64() - t0_;                     \
+    } while (0)
+#define KVT(...) __VA_ARGS__
+#else
+#define KVT_WAIT(acc, bar, ph) mbar_wait(bar, ph)
+#define KVT(...)
+#endif
+
 
 // ---------------------------------------------------------------- workspace
 struct BwdWs {
@@ -681,14 +697,15 @@ __global__ void __launch_bounds__(384, 1)
     if (warp == 0) {
         if (lane == 0) {  // scheduler + TMA producer
             int gi = 0;
+            KVT(long long w_qe = 0; long long w_kve = 0; long long w_ue = 0;)
             for (int un = 0;; ++un) {
                 const int k = un & 1;
-                if (un >= 2) mbar_wait(&bars->unit_empty[k], ((un >> 1) - 1) & 1);
+                if (un >= 2) KVT_WAIT(w_ue, &bars->unit_empty[k], ((un >> 1) - 1) & 1);
                 KvUnit& u = desc[k];
                 decode_unit(p, atomicAdd(work_counter, 1), u);
                 mbar_arrive(&bars->unit_full[k]);  // release: the descriptor is visible to the waiters
                 if (!u.valid) break;
-                if (un >= 1) mbar_wait(&bars->kv_empty, (un - 1) & 1);  // the previous unit's last S / dP
+                if (un >= 1) KVT_WAIT(w_kve, &bars->kv_empty, (un - 1) & 1);  // the previous unit's last S / dP
                 mbar_expect_tx(&bars->kv_full, 2 * kTileBytes);
                 for (int r = 0; r < 2; ++r) {
                     if (u.past && p64) {  // two 64-row pages (pool maps with 64-row boxes)
@@ -708,7 +725,7 @@ __global__ void __launch_bounds__(384, 1)
                 it.init(u, g.group, tpq);
                 for (int i = 0; i < u.n_items; ++i, ++gi, it.next(u, g.group, tpq)) {
                     const int st = gi % kKvStages;
-                    if (gi >= kKvStages) mbar_wait(&bars->qdo_empty[st], ((gi / kKvStages) - 1) & 1);
+                    if (gi >= kKvStages) KVT_WAIT(w_qe, &bars->qdo_empty[st], ((gi / kKvStages) - 1) & 1);
                     mbar_expect_tx(&bars->qdo_full[st], 2 * kTileBytes + 1024);
                     float* ld = reinterpret_cast<float*>(smem + kKvLD) + st * 256;
                     bulk_load(ld, p.Lt + static_cast<int64_t>(it.h) * g.C + it.qt * kTile, 512, &bars->qdo_full[st]);
@@ -722,6 +739,7 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 }
             }
+            KVT(trace_value(p.tr, 18, w_qe); trace_value(p.tr, 19, w_kve); trace_value(p.tr, 20, w_ue);)
         }
     } else if (warp == 1) {
         // MMA warp (converged).
@@ -730,9 +748,10 @@ __global__ void __launch_bounds__(384, 1)
         const uint64_t dK = sdesc_k(smem_u32(sK)), dV = sdesc_k(smem_u32(sV));
         const uint64_t dQ = sdesc_k(smem_u32(sQ)), dDO = sdesc_k(smem_u32(sDO));
         const uint64_t dQmn = sdesc_mn(smem_u32(sQ), kRegion), dDOmn = sdesc_mn(smem_u32(sDO), kRegion);
+        KVT(long long w_qf = 0; long long w_pf = 0; long long w_dsf = 0; long long w_af = 0; long long w_kvf = 0;)
         auto mma_s = [&](int gi) {
             const int st = gi % kKvStages;
-            mbar_wait(&bars->qdo_full[st], (gi / kKvStages) & 1);
+            KVT_WAIT(w_qf, &bars->qdo_full[st], (gi / kKvStages) & 1);
             tc_fence_after();
             const uint64_t so = boff(st * kTileBytes);
 #pragma unroll
@@ -748,7 +767,7 @@ __global__ void __launch_bounds__(384, 1)
             umma_commit_w(&bars->dp_full);
         };
         auto mma_dv = [&](int gi, uint32_t first) {
-            mbar_wait(&bars->p_full, gi & 1);
+            KVT_WAIT(w_pf, &bars->p_full, gi & 1);
             tc_fence_after();
             const uint64_t so = boff((gi % kKvStages) * kTileBytes);
 #pragma unroll
@@ -757,7 +776,7 @@ __global__ void __launch_bounds__(384, 1)
         };
         auto mma_dk = [&](int gi, uint32_t first) {
             const int st = gi % kKvStages;
-            mbar_wait(&bars->ds_full, gi & 1);
+            KVT_WAIT(w_dsf, &bars->ds_full, gi & 1);
             tc_fence_after();
             const uint64_t so = boff(st * kTileBytes);
 #pragma unroll
@@ -772,7 +791,7 @@ __global__ void __launch_bounds__(384, 1)
             const KvUnit& u = desc[k];
             if (!u.valid) break;
             const int n = u.n_items;
-            mbar_wait(&bars->kv_full, un & 1);
+            KVT_WAIT(w_kvf, &bars->kv_full, un & 1);
             if (n > 0) {
                 mma_s(gi);
                 mma_dp(gi);
@@ -780,7 +799,7 @@ __global__ void __launch_bounds__(384, 1)
                 for (int i = 0; i < n; ++i) {
                     const uint32_t first = i == 0 ? 0u : 1u;
                     if (i == 0 && un > 0) {  // the previous unit's dK / dV have left TMEM
-                        mbar_wait(&bars->acc_free, (un - 1) & 1);
+                        KVT_WAIT(w_af, &bars->acc_free, (un - 1) & 1);
                         tc_fence_after();
                     }
                     mma_dv(gi + i, first);
@@ -799,6 +818,10 @@ __global__ void __launch_bounds__(384, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->unit_empty[k]);
         }
+        KVT(if (lane == 0) {
+            trace_value(p.tr, 13, w_qf); trace_value(p.tr, 14, w_pf); trace_value(p.tr, 15, w_dsf);
+            trace_value(p.tr, 16, w_af); trace_value(p.tr, 17, w_kvf);
+        })
     } else if (warp >= 4) {
         // Warpgroup w: query columns [64w, 64w+64) of every item; thread = key row (TMEM lane).
         const int quarter = warp & 3, wg = (warp - 4) >> 2;
@@ -809,12 +832,16 @@ __global__ void __launch_bounds__(384, 1)
         uint8_t* stage = smem + kKvStage + wg * kSliceBytes;
         const bool issuer = (threadIdx.x & 127) == 0;  // first thread of the warpgroup issues its TMA
         int gi = 0;
+        KVT(const long long c_start = clock64(); long long w_uf = 0, w_s0 = 0, w_s = 0, w_dp = 0, w_ad = 0, c_epi = 0,
+            c_p = 0, c_ds = 0, n_units = 0, n_items_t = 0;
+            if (threadIdx.x == 128) { trace_value(p.tr, 0, smid()); trace_mark(p.tr, 1); })
         for (int un = 0;; ++un) {
             const int k = un & 1;
-            mbar_wait(&bars->unit_full[k], (un >> 1) & 1);
+            KVT_WAIT(w_uf, &bars->unit_full[k], (un >> 1) & 1);
             const KvUnit& u = desc[k];
             if (!u.valid) break;
             const int n = u.n_items;
+            KVT(++n_units; n_items_t += n;)
             const bool past = u.past;
             const int key0 = u.key0, g_row = u.g_row, g_kv = u.g_kv;
             // page size 64: key rows [0,64) are the unit's first page, [64,128) its second
@@ -836,7 +863,9 @@ __global__ void __launch_bounds__(384, 1)
                 const bool masked = it.diag || !page_full;
                 mbar_wait(&bars->qdo_full[st], (gj / kKvStages) & 1);  // makes the bulk-copied L / D visible
                 // ---- P^T = exp2(S^T sl2 - L): computed as soon as S^T lands, packed in place
-                mbar_wait(&bars->s_full, gj & 1);
+                if (i == 0) KVT_WAIT(w_s0, &bars->s_full, gj & 1);
+                else KVT_WAIT(w_s, &bars->s_full, gj & 1);
+                KVT(const long long cp0 = clock64();)
                 tc_fence_after();
                 float pr[64];
 #pragma unroll
@@ -870,8 +899,10 @@ __global__ void __launch_bounds__(384, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(&bars->p_full);
+                KVT(c_p += clock64() - cp0;)
                 // ---- dS^T = P^T (dP^T - D), packed in place of dP^T
-                mbar_wait(&bars->dp_full, gj & 1);
+                KVT_WAIT(w_dp, &bars->dp_full, gj & 1);
+                KVT(const long long cd0 = clock64();)
                 tc_fence_after();
 #pragma unroll
                 for (int c2 = 0; c2 < 2; ++c2) {
@@ -893,10 +924,12 @@ __global__ void __launch_bounds__(384, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(&bars->ds_full);
+                KVT(c_ds += clock64() - cd0;)
             }
             gi += n;
             // ---- epilogue: pull this group's accumulator (dK scaled / dV) into registers, free TMEM
-            mbar_wait(&bars->acc_done, un & 1);
+            KVT_WAIT(w_ad, &bars->acc_done, un & 1);
+            KVT(const long long ce0 = clock64();)
             tc_fence_after();
             const uint32_t acc = (wg ? kTmDV : kTmDK) + lane_off;
             const float sc = key_ok ? (wg ? 1.f : g.scale) : 0.f;
@@ -936,8 +969,15 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 }
             }
+            KVT(c_epi += clock64() - ce0;)
         }
         if (issuer) bulk_wait_read0();
+        KVT(if (threadIdx.x == 128) {
+            trace_mark(p.tr, 2); trace_value(p.tr, 3, n_units); trace_value(p.tr, 4, n_items_t);
+            trace_value(p.tr, 5, w_uf); trace_value(p.tr, 6, w_s0); trace_value(p.tr, 7, w_s);
+            trace_value(p.tr, 8, w_dp); trace_value(p.tr, 9, w_ad); trace_value(p.tr, 10, c_epi);
+            trace_value(p.tr, 11, c_p); trace_value(p.tr, 12, c_ds); trace_value(p.tr, 21, clock64() - c_start);
+        })
     }
     tc_fence_before();
     __syncthreads();
@@ -1023,9 +1063,12 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         const int n_ctas = std::max(1, std::min(units, num_sms));
         const CUtensorMap tdkc = map_rows_heads_f32(dk_cur, g.C, g.Hkv, g.hd);
         const CUtensorMap tdvc = map_rows_heads_f32(dv_cur, g.C, g.Hkv, g.hd);
+        BwdParams pk = p;
+        if (OOMB_KV_TRACE) pk.tr = trace_begin("dkdv", n_ctas, 22);
         attn_bwd_dkdv_kernel<<<n_ctas, 384, kKvSmem, st>>>(tq, tdo, tkc, tvc, maps.kpool, maps.vpool, maps.gkpool,
-                                                            maps.gvpool, tdkc, tdvc, p, w.n_uni + 1);
+                                                            maps.gvpool, tdkc, tdvc, pk, w.n_uni + 1);
         check_launch("attn_bwd_dkdv_kernel");
+        if (OOMB_KV_TRACE) trace_end(pk.tr, n_ctas, st);
     };
     if (OOMB_BWD_KV_FIRST) {
         launch_dkdv();

@@ -76,7 +76,8 @@ template <typename T>
 __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, int64_t rows, int64_t filled,
                               int P, int Hkv, int hd, int first_page, NewSlots ns, int32_t* __restrict__ kvslot,
                               T* __restrict__ kpool, T* __restrict__ vpool, float* __restrict__ ksum,
-                              int32_t* __restrict__ kcnt, int* err, const double* __restrict__ rope_inv_freq) {
+                              int32_t* __restrict__ kcnt, int* err, const double* __restrict__ rope_inv_freq,
+                              __nv_bfloat16* __restrict__ planes, int64_t plane_stride) {
     const int re = Hkv * hd;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     const int pg = first_page + blockIdx.y;
@@ -126,13 +127,24 @@ __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, 
     }
     ksum[static_cast<int64_t>(pg) * re + e] = sum;
     if (e == 0) kcnt[pg] = (is_new ? 0 : kcnt[pg]) + static_cast<int>(s1 - s0);
+    if (planes) {
+        // the tcgen05 scorer's hi / lo bf16 planes of K_avg = sum * (1/count) (paged_kv.hpp:177-180),
+        // [2][Hkv][plane_stride][hd]: kept current here, so scoring never re-splits completed pages
+        const int cnt = static_cast<int>(s1 - static_cast<int64_t>(pg) * P);  // rows the page holds now
+        const float kav = __fmul_rn(sum, __fdiv_rn(1.0f, static_cast<float>(cnt)));
+        const __nv_bfloat16 hi = __float2bfloat16_rn(kav);
+        const size_t at = (static_cast<size_t>(h) * plane_stride + pg) * hd + d;
+        planes[at] = hi;
+        planes[at + static_cast<size_t>(Hkv) * plane_stride * hd] = __float2bfloat16_rn(kav - __bfloat162float(hi));
+    }
 }
 
 void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_t filled_before, int P, int Hkv,
                    int hd, int first_page, int n_pages_touched, const NewSlots& ns, int32_t* d_kvslot_layer,
                    void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, int* d_err,
-                   cudaStream_t st, const double* rope_inv_freq) {
+                   cudaStream_t st, const double* rope_inv_freq, void* kavg_planes_layer, int64_t plane_stride) {
     if (rows <= 0 || n_pages_touched <= 0) return;
+    __nv_bfloat16* planes = static_cast<__nv_bfloat16*>(kavg_planes_layer);
     ProfScope prof_(PK_APPEND, st);
     const int re = Hkv * hd;
     dim3 grid((re + 127) / 128, n_pages_touched);
@@ -140,12 +152,12 @@ void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_
         append_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(
             static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), rows, filled_before, P, Hkv,
             hd, first_page, ns, d_kvslot_layer, static_cast<__nv_bfloat16*>(kpool), static_cast<__nv_bfloat16*>(vpool),
-            kavg_sum_layer, kavg_cnt_layer, d_err, rope_inv_freq);
+            kavg_sum_layer, kavg_cnt_layer, d_err, rope_inv_freq, planes, plane_stride);
     else
         append_kernel<float><<<grid, 128, 0, st>>>(static_cast<const float*>(k), static_cast<const float*>(v), rows,
                                                    filled_before, P, Hkv, hd, first_page, ns, d_kvslot_layer,
                                                    static_cast<float*>(kpool), static_cast<float*>(vpool),
-                                                   kavg_sum_layer, kavg_cnt_layer, d_err, rope_inv_freq);
+                                                   kavg_sum_layer, kavg_cnt_layer, d_err, rope_inv_freq, nullptr, 0);
     check_launch("append_kernel");
 }
 

@@ -337,6 +337,12 @@ int oomb_pool_create(const oomb_config* cfg, int device, oomb_pool_t* out) {
             OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->d_kavg_cnt), tab));
             OOMB_CUDA(cudaMemset(p->d_kavg_sum, 0, ks * sizeof(float)));
             OOMB_CUDA(cudaMemset(p->d_kavg_cnt, 0, tab));
+            if (c.dtype == OOMB_BF16 && c.head_dim == 128 && c.page_size % 128 == 0) {  // the tcgen05 scorer's shape
+                p->plane_stride = (p->max_pages + 127) / 128 * 128;
+                const size_t pb = static_cast<size_t>(c.n_layers) * 2 * c.n_kv_heads * p->plane_stride * c.head_dim * 2;
+                OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->d_kavg_planes), pb));
+                OOMB_CUDA(cudaMemset(p->d_kavg_planes, 0, pb));
+            }
             OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->d_err), sizeof(int)));
             OOMB_CUDA(cudaMemset(p->d_err, 0, sizeof(int)));
             if (c.dtype == OOMB_BF16 && (c.head_dim == 128 || c.head_dim == 64) &&
@@ -366,6 +372,7 @@ int oomb_pool_destroy(oomb_pool_t p) {
     cudaFree(p->d_gslot);
     cudaFree(p->d_kavg_sum);
     cudaFree(p->d_kavg_cnt);
+    cudaFree(p->d_kavg_planes);
     cudaFree(p->d_err);
     for (int b = 0; b < 2; ++b) {
         cudaFree(p->bwd_ws[b]);
@@ -501,7 +508,8 @@ static int append_impl(oomb_pool_t p, int layer, const void* k, const void* v, i
             const char* vb = static_cast<const char*>(v) + done * re * p->elem;
             launch_append(p->cfg.dtype, kb, vb, seg, f, P, p->cfg.n_kv_heads, p->cfg.head_dim, first_page,
                           last_page - first_page + 1, ns, p->kvslot_layer(layer), p->kpool, p->vpool,
-                          p->kavg_sum_layer(layer), p->kavg_cnt_layer(layer), p->d_err, S(stream), inv_freq);
+                          p->kavg_sum_layer(layer), p->kavg_cnt_layer(layer), p->d_err, S(stream), inv_freq,
+                          p->kavg_planes_layer(layer), p->plane_stride);
             published = std::max(published, last_page + 1);
             done += seg;
         }
@@ -806,7 +814,8 @@ int oomb_select_topk(oomb_selection_t s, const float* vote, int m, int n, int k,
 // 128-aligned chunks use the tcgen05 scorer; everything else the exact SIMT scorer.
 static void score_impl(const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, const float* kavg_sum,
                        const int32_t* kavg_cnt, int64_t n, int Hkv, int P, int score_scale, int dtype, bool allow_tc,
-                       float* vote, cudaStream_t st, bool partial_only = false) {
+                       float* vote, cudaStream_t st, bool partial_only = false, const void* planes = nullptr,
+                       int64_t plane_stride = 0) {
     OOMB_REQUIRE(n >= 1, OOMB_SHAPE_ERROR, "score_pages: needs at least one candidate page");
     OOMB_REQUIRE(Hq >= 1 && Hkv >= 1 && Hq % Hkv == 0 && hd >= 1 && hd <= 256 && P >= 1, OOMB_SHAPE_ERROR,
                  "score_pages: bad shape");
@@ -814,7 +823,8 @@ static void score_impl(const void* q, int64_t tokens, int Hq, int hd, const floa
     if (allow_tc && score_tc_supported(dtype, hd, P, tokens)) {
         void* ws = nullptr;
         OOMB_CUDA(cudaMallocAsync(&ws, score_tc_workspace(tokens, Hq, Hkv, n, P), st));
-        launch_score_tc(q, tokens, Hq, Hkv, P, kavg_sum, kavg_cnt, k_avg, n, scale, vote, ws, st, partial_only);
+        launch_score_tc(q, tokens, Hq, Hkv, P, kavg_sum, kavg_cnt, k_avg, n, scale, vote, ws, st, partial_only, planes,
+                        plane_stride);
         OOMB_CUDA(cudaFreeAsync(ws, st));
         return;
     }
@@ -849,7 +859,8 @@ int oomb_score_pages_partial(oomb_pool_t p, int layer, const void* q, int64_t to
         OOMB_REQUIRE(n >= 1, OOMB_SHAPE_ERROR, "score_pages: needs at least one candidate page");
         score_impl(q, tokens, p->cfg.n_q_heads, p->cfg.head_dim, nullptr, p->kavg_sum_layer(layer),
                    p->kavg_cnt_layer(layer), n, p->cfg.n_kv_heads, p->cfg.page_size, p->cfg.score_scale,
-                   p->cfg.dtype, p->policy != 1, partials, S(stream), /*partial_only=*/true);
+                   p->cfg.dtype, p->policy != 1, partials, S(stream), /*partial_only=*/true, p->kavg_planes_layer(layer),
+                   p->plane_stride);
     });
 }
 
@@ -883,7 +894,8 @@ int oomb_select_pages_topk(oomb_pool_t p, int layer, const void* q, int64_t toke
         }
         score_impl(q, tokens, p->cfg.n_q_heads, p->cfg.head_dim, nullptr, p->kavg_sum_layer(layer),
                    p->kavg_cnt_layer(layer), n, p->cfg.n_kv_heads, p->cfg.page_size, p->cfg.score_scale,
-                   p->cfg.dtype, p->policy != 1, vote_scratch, S(stream));
+                   p->cfg.dtype, p->policy != 1, vote_scratch, S(stream), false, p->kavg_planes_layer(layer),
+                   p->plane_stride);
         select_topk_impl(sel, vote_scratch, m, n, p->cfg.retrieval_budget / p->cfg.page_size, S(stream));
     });
 }

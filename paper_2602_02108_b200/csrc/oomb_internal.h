@@ -169,7 +169,8 @@ constexpr int32_t SLOT_REMOTE = -2;
 void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_t filled_before, int P, int Hkv,
                    int hd, int first_page, int n_pages_touched, const NewSlots& ns, int32_t* d_kvslot_layer,
                    void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, int* d_err,
-                   cudaStream_t st, const double* rope_inv_freq = nullptr);
+                   cudaStream_t st, const double* rope_inv_freq = nullptr, void* kavg_planes_layer = nullptr,
+                   int64_t plane_stride = 0);
 // dst CSR = the ids of src with id % stride == rank, list order kept (one CTA).
 void launch_filter_owned(const int32_t* src_off, const int32_t* src_ids, int m, int stride, int rank,
                          int32_t* dst_off, int32_t* dst_ids, cudaStream_t st);
@@ -243,7 +244,8 @@ bool score_tc_supported(int dtype, int hd, int P, int64_t tokens);
 size_t score_tc_workspace(int64_t tokens, int Hq, int Hkv, int64_t n, int P);
 void launch_score_tc(const void* q, int64_t tokens, int Hq, int Hkv, int P, const float* kavg_sum,
                      const int32_t* kavg_cnt, const float* kavg_f32, int64_t n, float scale, float* vote, void* ws,
-                     cudaStream_t st, bool partial_only = false);
+                     cudaStream_t st, bool partial_only = false, const void* planes = nullptr,
+                     int64_t plane_stride = 0);
 void launch_vote_reduce(const float* part, int groups, int64_t mn, float* vote, cudaStream_t st);
 void launch_debug_tc_gemm(int mode, const void* a, const void* b, float* c, int m, int n, int k, cudaStream_t st);
 

@@ -190,6 +190,8 @@ struct oomb_pool_s {
     int32_t* d_gslot = nullptr;
     float* d_kavg_sum = nullptr;
     int32_t* d_kavg_cnt = nullptr;
+    uint8_t* d_kavg_planes = nullptr;  // bf16 (see kavg_planes_layer)
+    int64_t plane_stride = 0;
     int* d_err = nullptr;
     bool enforce = false;
     int policy = 0;
@@ -282,6 +284,13 @@ struct oomb_pool_s {
         return d_kavg_sum + static_cast<int64_t>(l) * max_pages * cfg.n_kv_heads * cfg.head_dim;
     }
     int32_t* kavg_cnt_layer(int l) { return d_kavg_cnt + static_cast<int64_t>(l) * max_pages; }
+    // bf16 hi / lo planes of K_avg for the tcgen05 scorer ([layer][2][Hkv][plane_stride][hd]); null when
+    // the pool's dtype / head dim never use it
+    void* kavg_planes_layer(int l) {
+        return d_kavg_planes ? static_cast<void*>(d_kavg_planes + static_cast<int64_t>(l) * 2 * cfg.n_kv_heads *
+                                                                       plane_stride * cfg.head_dim * 2)
+                             : nullptr;
+    }
 };
 
 struct oomb_selection_s {

@@ -63,7 +63,9 @@ struct ScoreParams {
     float* m2;  // [Hq][C] running max (log2 units)
     float* il;  // [Hq][C] 1 / sum
     float* vote_part;  // [Hkv][m][n]
-    int lo_row;        // first row of the lo plane in the K_avg map (= Hkv * n_pad)
+    int lo_row;        // first row of the lo plane in the K_avg map (= Hkv * kv_stride)
+    int kv_stride;     // rows per kv head in a plane (n_pad for kavg_prep's planes, the pool's page capacity
+                       // rounded to 128 for the planes the append kernel maintains)
 };
 
 // ---------------------------------------------------------------- pass 1
@@ -129,7 +131,7 @@ __global__ void __launch_bounds__(384, 1)
                 for (int pl = 0; pl < 2; ++pl)
                     for (int r = 0; r < 2; ++r)
                         tma_load_2d(sK + (2 * st + pl) * kTileBytes + r * kRegion, &tm_ka, &bars->k_full[st], r * 64,
-                                    pl * p.lo_row + kvh * p.n_pad + j * kTile);
+                                    pl * p.lo_row + kvh * p.kv_stride + j * kTile);
             }
         }
     } else if (warp == 1) {
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(384, 1)
             for (int pl = 0; pl < 2; ++pl)
                 for (int r = 0; r < 2; ++r)
                     tma_load_2d(sK + pl * kTileBytes + r * kRegion, &tm_ka, &bars->ka_full, r * 64,
-                                pl * p.lo_row + kvh * p.n_pad + pb * kTile);
+                                pl * p.lo_row + kvh * p.kv_stride + pb * kTile);
             int qp = qp0, hh = 0, tl = 0;
             for (int i = 0; i < n_items; ++i) {
                 const int st = i % kVoSt;
@@ -406,7 +408,9 @@ void launch_vote_reduce(const float* part, int groups, int64_t mn, float* vote, 
 
 void launch_score_tc(const void* q, int64_t tokens, int Hq, int Hkv, int P, const float* kavg_sum,
                      const int32_t* kavg_cnt, const float* kavg_f32, int64_t n, float scale, float* vote,
-                     void* ws, cudaStream_t st, bool partial_only) {
+                     void* ws, cudaStream_t st, bool partial_only, const void* planes_v,
+                     int64_t plane_stride) {
+    const __nv_bfloat16* planes = static_cast<const __nv_bfloat16*>(planes_v);
     if (first_use_on_device(3)) {
         OOMB_CUDA(cudaFuncSetAttribute(score_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStSmem));
         OOMB_CUDA(cudaFuncSetAttribute(score_vote_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kVoSmem));
@@ -424,20 +428,26 @@ void launch_score_tc(const void* q, int64_t tokens, int Hq, int Hkv, int P, cons
     off += align(static_cast<size_t>(Hq) * tokens * 4);
     float* part = partial_only ? vote : reinterpret_cast<float*>(w + off);  // [Hkv][m][n]
 
-    const int64_t tot = static_cast<int64_t>(Hkv) * n_pad * kHd;
-    kavg_prep_kernel<<<static_cast<unsigned>(std::min<int64_t>((tot + 255) / 256, 4096)), 256, 0, st>>>(
-        kavg_sum, kavg_cnt, kavg_f32, static_cast<int>(n), n_pad, Hkv, kHd, ka);
-    check_launch("kavg_prep_kernel");
+    // the pool's K_avg planes are kept current by the append kernel (completed pages never change):
+    // read them in place; otherwise (fp32 representatives) split K_avg into planes here
+    const bool inplace = planes != nullptr && kavg_f32 == nullptr && plane_stride >= n_pad;
+    const int kv_stride = inplace ? static_cast<int>(plane_stride) : n_pad;
+    if (!inplace) {
+        const int64_t tot = static_cast<int64_t>(Hkv) * n_pad * kHd;
+        kavg_prep_kernel<<<static_cast<unsigned>(std::min<int64_t>((tot + 255) / 256, 4096)), 256, 0, st>>>(
+            kavg_sum, kavg_cnt, kavg_f32, static_cast<int>(n), n_pad, Hkv, kHd, ka);
+        check_launch("kavg_prep_kernel");
+    }
     CUtensorMap tq = map_rows_heads(q, tokens, Hq, kHd);
     CUtensorMap tka;
     {
-        const uint64_t dims[2] = {static_cast<uint64_t>(kHd), 2 * static_cast<uint64_t>(Hkv) * n_pad};
+        const uint64_t dims[2] = {static_cast<uint64_t>(kHd), 2 * static_cast<uint64_t>(Hkv) * kv_stride};
         const uint64_t strides[1] = {static_cast<uint64_t>(kHd) * 2};
         const uint32_t box[2] = {64, kTile};
-        encode_or_throw(&tka, 2, ka, dims, strides, box);
+        encode_or_throw(&tka, 2, inplace ? const_cast<__nv_bfloat16*>(planes) : ka, dims, strides, box);
     }
     ScoreParams p{static_cast<int>(tokens), Hq, Hkv, kHd, P, static_cast<int>(n), n_pad, m, scale * kLog2e, m2, il,
-                  part, Hkv * n_pad};
+                  part, Hkv * kv_stride, kv_stride};
     score_stats_kernel<<<dim3(Hq, static_cast<unsigned>(tokens / kTile)), 384, kStSmem, st>>>(tq, tka, p);
     check_launch("score_stats_kernel");
     score_vote_kernel<<<dim3(n_pad / kTile, Hkv, (m + kQpGroup - 1) / kQpGroup), 384, kVoSmem, st>>>(tq, tka, p);
