@@ -272,6 +272,20 @@ FWD_STREAMS = int(os.environ.get("OOMB_FWD_STREAMS", "2"))
 BWD_DEFER = os.environ.get("OOMB_BWD_DEFER", "1") != "0"
 
 
+def bench_inputs(cfg, seed: int, device, rq: int = 16):
+    """The bench's synthetic inputs: N(0,1) keys / values for the whole context and `rq` distinct
+    query / dO chunks, rounded to bf16 (tests/test_gpu_bench_data.py checks selection on exactly these)."""
+    import torch
+    C, Hq, Hkv, hd, T = cfg["C"], cfg["Hq"], cfg["Hkv"], cfg["hd"], cfg["T"]
+    g = torch.Generator(device=device).manual_seed(seed)
+    bf = torch.bfloat16
+    k_all = torch.randn(T, Hkv, hd, device=device, generator=g).to(bf)
+    v_all = torch.randn(T, Hkv, hd, device=device, generator=g).to(bf)
+    q = [torch.randn(C, Hq, hd, device=device, generator=g).to(bf) for _ in range(rq)]
+    do = [torch.randn(C, Hq, hd, device=device, generator=g).to(bf) for _ in range(rq)]
+    return k_all, v_all, q, do
+
+
 class Run:
     RQ = 16  # distinct q / dO chunk buffers (K/V are distinct for every chunk)
 
@@ -291,12 +305,8 @@ class Run:
         self.layer = layer
         self.cache = (PagedCache(self.mc, dtype="bf16", max_tokens=T) if layer is None else
                       layer.attach(layer.plan.make_cache(layer.cfg, dtype="bf16", max_tokens=T)))
-        g = torch.Generator(device=device).manual_seed(seed)
+        self.k_all, self.v_all, self.q, self.do = bench_inputs(cfg, seed, device, self.RQ)
         bf = torch.bfloat16
-        self.k_all = torch.randn(T, Hkv, hd, device=device, generator=g).to(bf)
-        self.v_all = torch.randn(T, Hkv, hd, device=device, generator=g).to(bf)
-        self.q = [torch.randn(C, Hq, hd, device=device, generator=g).to(bf) for _ in range(self.RQ)]
-        self.do = [torch.randn(C, Hq, hd, device=device, generator=g).to(bf) for _ in range(self.RQ)]
         self.o_all = torch.empty(self.S, C, Hq, hd, device=device, dtype=bf)
         self.lse_all = torch.empty(self.S, C, Hq, device=device, dtype=torch.float32)
         kmax = self.m * (cfg["budget"] // P if cfg["mode"] == "topk" else T // P)

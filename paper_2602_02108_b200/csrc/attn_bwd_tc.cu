@@ -35,7 +35,30 @@ namespace {
 #ifndef OOMB_BWD_POLY
 #define OOMB_BWD_POLY 0  // measured: no gain (the P phase is latency-, not MUFU-bound)
 #endif
-constexpr bool kBwdPoly = OOMB_BWD_POLY != 0;  // one in four exp2 of P on the FMA pipe (ex2_poly)
+#ifndef OOMB_DQ_POLY_N
+#define OOMB_DQ_POLY_N 4  // measured: dQ 44.75 -> 41.67 ms (256K c3, serialized) with OOMB_DQ_X2
+#endif
+#ifndef OOMB_KV_POLY_N
+#define OOMB_KV_POLY_N (OOMB_BWD_POLY ? 4 : 0)
+#endif
+constexpr int kDqPolyN = OOMB_DQ_POLY_N;  // dQ kernel: 1 in N exp2 of P on the FMA pipe (ex2_poly; 0: none)
+constexpr int kKvPolyN = OOMB_KV_POLY_N;  // dK/dV kernel: the same for P^T
+#ifndef OOMB_POLY_LEAN
+#define OOMB_POLY_LEAN 1  // ex2_lean (1 ALU op) instead of ex2_poly (4) for the FMA-pipe share
+#endif
+#ifndef OOMB_DQ_X2
+#define OOMB_DQ_X2 1  // dQ kernel softmax arithmetic as packed fp32 pairs (FFMA2 / FADD2 / FMUL2)
+#endif
+#ifndef OOMB_KV_X2
+#define OOMB_KV_X2 0  // the same in the dK/dV kernel
+#endif
+__device__ __forceinline__ float ex2_mix(float x, int c, int n) {
+    return (n > 0 && c % n == n - 1) ? (OOMB_POLY_LEAN ? ex2_lean(x) : ex2_poly(x)) : ex2(x);
+}
+
+#ifndef OOMB_BWD_LPT
+#define OOMB_BWD_LPT 1  // dK/dV units longest first (bwd_order_kernel); 0: own blocks, then union order
+#endif
 
 #ifndef OOMB_KV_TRACE
 #define OOMB_KV_TRACE 0  // per-CTA wait / phase cycle counters of the dK/dV kernel (OOMB_CTA_TRACE=dkdv:i:file)
@@ -60,8 +83,11 @@ struct BwdWs {
     float* Lt;        // [Hq][C]
     uint64_t* mask;   // [max_pages]
     int32_t* uni;     // [max_pages]
-    int32_t* n_uni;   // [1]
+    int32_t* n_uni;   // [1] (+ the dK/dV work counter)
+    int32_t* order;   // [chunk blocks + max_pages * blocks per page]: dK/dV units, longest first
 };
+
+inline int bwd_blocks_per_page(const AttnGeom& g) { return g.P == kHalf ? 1 : std::max(1, g.P / kTile); }
 
 BwdWs carve(const AttnGeom& g, void* ws) {
     uint8_t* p = static_cast<uint8_t*>(ws);
@@ -75,6 +101,8 @@ BwdWs carve(const AttnGeom& g, void* ws) {
     w.uni = reinterpret_cast<int32_t*>(p + off);
     off += static_cast<size_t>(g.max_pages) * 4;
     w.n_uni = reinterpret_cast<int32_t*>(p + off);
+    off = (off + 8 + 255) & ~size_t(255);
+    w.order = reinterpret_cast<int32_t*>(p + off);
     return w;
 }
 
@@ -144,6 +172,37 @@ __global__ void __launch_bounds__(1024) bwd_union_kernel(const uint64_t* __restr
     if (threadIdx.x == 0) *n_uni = total;
 }
 
+// Order of the dK/dV work units, longest first (LPT), so the persistent grid does not end on a
+// long unit: unit codes [0, ncb) are the chunk's own key blocks (block b is attended by the
+// ncb - b query tiles from its diagonal on), codes ncb + k * bpp + sub the past blocks of the
+// k-th union page (attended by popcount(mask) query pages x tpq tiles each). Units write
+// disjoint gradient rows, so the order changes the schedule only, never a result bit.
+__global__ void __launch_bounds__(1024) bwd_order_kernel(const uint64_t* __restrict__ mask,
+                                                         const int32_t* __restrict__ uni,
+                                                         const int32_t* __restrict__ n_uni, int ncb, int bpp, int tpq,
+                                                         int32_t* __restrict__ order) {
+    constexpr int kKeys = 256;
+    __shared__ int hist[kKeys], cur[kKeys];
+    const int units = ncb + *n_uni * bpp;
+    for (int i = threadIdx.x; i < kKeys; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    auto key = [&](int u) {
+        const int k = u < ncb ? ncb - u : __popcll(mask[uni[(u - ncb) / bpp]]) * tpq;
+        return min(k, kKeys - 1);
+    };
+    for (int u = threadIdx.x; u < units; u += blockDim.x) atomicAdd(&hist[key(u)], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int pos = 0;
+        for (int k = kKeys - 1; k >= 0; --k) {
+            cur[k] = pos;
+            pos += hist[k];
+        }
+    }
+    __syncthreads();
+    for (int u = threadIdx.x; u < units; u += blockDim.x) order[atomicAdd(&cur[key(u)], 1)] = u;
+}
+
 // ===========================================================================
 // dQ kernel (query-major): one CTA per (128-row query tile, q-head), looping over the key
 // blocks the tile attends (its query page's selected pages, then the chunk's causal prefix).
@@ -202,6 +261,7 @@ struct BwdParams {
     const uint64_t* mask;
     const int32_t* uni;
     const int32_t* n_uni;
+    const int32_t* order;  // dK/dV unit order (null: identity)
     float* dq;
     float* dk_cur;
     float* dv_cur;
@@ -405,15 +465,28 @@ __global__ void __launch_bounds__(384, 1)
                 tmem_wait_ld();
                 tc_fence_before();
                 mbar_arrive(&bars->s_free);
+                if (OOMB_DQ_X2) {
+                    const float2 s2 = make_float2(sl2, sl2), nl2 = make_float2(-L2, -L2);
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const float x = fmaf(__uint_as_float(a[c]), sl2, -L2);
-                    pr[c] = (kBwdPoly && (c & 3) == 3) ? ex2_poly(x) : ex2(x);
-                }
+                    for (int c = 0; c < 32; c += 2) {
+                        const float2 x = fma2(make_float2(__uint_as_float(a[c]), __uint_as_float(a[c + 1])), s2, nl2);
+                        pr[c] = ex2_mix(x.x, c, kDqPolyN);
+                        pr[c + 1] = ex2_mix(x.y, c + 1, kDqPolyN);
+                        const float2 y = fma2(make_float2(__uint_as_float(b2[c]), __uint_as_float(b2[c + 1])), s2, nl2);
+                        pr[32 + c] = ex2_mix(y.x, 32 + c, kDqPolyN);
+                        pr[33 + c] = ex2_mix(y.y, 33 + c, kDqPolyN);
+                    }
+                } else {
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const float x = fmaf(__uint_as_float(b2[c]), sl2, -L2);
-                    pr[32 + c] = (kBwdPoly && (c & 3) == 3) ? ex2_poly(x) : ex2(x);
+                    for (int c = 0; c < 32; ++c) {
+                        const float x = fmaf(__uint_as_float(a[c]), sl2, -L2);
+                        pr[c] = ex2_mix(x, c, kDqPolyN);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        const float x = fmaf(__uint_as_float(b2[c]), sl2, -L2);
+                        pr[32 + c] = ex2_mix(x, 32 + c, kDqPolyN);
+                    }
                 }
             }
             if (lim < 63) {
@@ -430,9 +503,17 @@ __global__ void __launch_bounds__(384, 1)
                 tmem_wait_ld();
                 uint32_t pk[16];
 #pragma unroll
-                for (int u = 0; u < 16; ++u)
-                    pk[u] = pack_bf16(pr[c2 * 32 + 2 * u] * (__uint_as_float(d[2 * u]) - Dr),
-                                      pr[c2 * 32 + 2 * u + 1] * (__uint_as_float(d[2 * u + 1]) - Dr));
+                for (int u = 0; u < 16; ++u) {
+                    if (OOMB_DQ_X2) {
+                        const float2 t = add2(make_float2(__uint_as_float(d[2 * u]), __uint_as_float(d[2 * u + 1])),
+                                              make_float2(-Dr, -Dr));
+                        const float2 v = mul2(make_float2(pr[c2 * 32 + 2 * u], pr[c2 * 32 + 2 * u + 1]), t);
+                        pk[u] = pack_bf16(v.x, v.y);
+                    } else {
+                        pk[u] = pack_bf16(pr[c2 * 32 + 2 * u] * (__uint_as_float(d[2 * u]) - Dr),
+                                          pr[c2 * 32 + 2 * u + 1] * (__uint_as_float(d[2 * u + 1]) - Dr));
+                    }
+                }
                 tmem_st16(tDP + c2 * 16, pk);  // below the columns still to be read
             }
             tmem_wait_st();
@@ -472,7 +553,7 @@ __global__ void __launch_bounds__(384, 1)
 // A work unit is one 128-key block (a past page, or a block of the chunk's own keys) of one kv
 // head; its items are the (128-row query tile, q-head of the group) pairs that attend it — the
 // query pages that selected the page, or the chunk's tiles from the diagonal on. One CTA per SM
-// takes units from an atomic counter (the chunk's own blocks, the longest, first) and overlaps
+// takes units from an atomic counter in longest-first order (bwd_order_kernel) and overlaps
 // consecutive units: the next unit's K/V and first Q/dO tiles load, and its first S^T/dP^T MMAs
 // run, while the previous unit finishes and drains its accumulators.
 // Per item:
@@ -573,7 +654,8 @@ struct ItemIter {
     }
 };
 
-// Decode work index w (units of the chunk's own blocks first, then past page blocks; kv head
+// Decode work index w (through the longest-first order when there is one: unit codes are the chunk's
+// own blocks first, then past page blocks; kv head
 // fastest) into a unit descriptor.
 __device__ void decode_unit(const BwdParams& p, int w, KvUnit& u) {
     const AttnGeom& g = p.g;
@@ -585,7 +667,7 @@ __device__ void decode_unit(const BwdParams& p, int w, KvUnit& u) {
     u.has1 = 0;
     u.qm0 = u.qm1 = 0ull;
     if (!u.valid) return;
-    const int unit = w / g.Hkv;
+    const int unit = p.order ? p.order[w / g.Hkv] : w / g.Hkv;
     u.g_kv = w % g.Hkv;
     u.n_valid = kTile;
     if (unit < n_chunk_blocks) {
@@ -876,12 +958,22 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                     for (int c4 = 0; c4 < 8; ++c4) {
                         const float4 l4 = lds128(lrow + (c2 * 32 + c4 * 4) * 4);
-                        pr[c2 * 32 + 4 * c4 + 0] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 0]), sl2, -l4.x));
-                        pr[c2 * 32 + 4 * c4 + 1] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 1]), sl2, -l4.y));
-                        pr[c2 * 32 + 4 * c4 + 2] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 2]), sl2, -l4.z));
-                        {  // one in four exponentials on the FMA pipe (P is rounded to bf16)
-                            const float x3 = fmaf(__uint_as_float(sv[4 * c4 + 3]), sl2, -l4.w);
-                            pr[c2 * 32 + 4 * c4 + 3] = kBwdPoly ? ex2_poly(x3) : ex2(x3);
+                        const int c = c2 * 32 + 4 * c4;
+                        if (OOMB_KV_X2) {
+                            const float2 s2 = make_float2(sl2, sl2);
+                            const float2 x01 = fma2(make_float2(__uint_as_float(sv[4 * c4]), __uint_as_float(sv[4 * c4 + 1])),
+                                                    s2, make_float2(-l4.x, -l4.y));
+                            const float2 x23 = fma2(make_float2(__uint_as_float(sv[4 * c4 + 2]), __uint_as_float(sv[4 * c4 + 3])),
+                                                    s2, make_float2(-l4.z, -l4.w));
+                            pr[c + 0] = ex2_mix(x01.x, c + 0, kKvPolyN);
+                            pr[c + 1] = ex2_mix(x01.y, c + 1, kKvPolyN);
+                            pr[c + 2] = ex2_mix(x23.x, c + 2, kKvPolyN);
+                            pr[c + 3] = ex2_mix(x23.y, c + 3, kKvPolyN);
+                        } else {
+                            pr[c + 0] = ex2_mix(fmaf(__uint_as_float(sv[4 * c4 + 0]), sl2, -l4.x), c + 0, kKvPolyN);
+                            pr[c + 1] = ex2_mix(fmaf(__uint_as_float(sv[4 * c4 + 1]), sl2, -l4.y), c + 1, kKvPolyN);
+                            pr[c + 2] = ex2_mix(fmaf(__uint_as_float(sv[4 * c4 + 2]), sl2, -l4.z), c + 2, kKvPolyN);
+                            pr[c + 3] = ex2_mix(fmaf(__uint_as_float(sv[4 * c4 + 3]), sl2, -l4.w), c + 3, kKvPolyN);
                         }
                     }
                 }
@@ -914,10 +1006,21 @@ __global__ void __launch_bounds__(384, 1)
                     for (int c4 = 0; c4 < 8; ++c4) {
                         const float4 d4 = lds128(drow + (c2 * 32 + c4 * 4) * 4);
                         const int c = c2 * 32 + 4 * c4;
-                        pk[2 * c4] = pack_bf16(pr[c] * (__uint_as_float(dv[4 * c4]) - d4.x),
-                                               pr[c + 1] * (__uint_as_float(dv[4 * c4 + 1]) - d4.y));
-                        pk[2 * c4 + 1] = pack_bf16(pr[c + 2] * (__uint_as_float(dv[4 * c4 + 2]) - d4.z),
-                                                   pr[c + 3] * (__uint_as_float(dv[4 * c4 + 3]) - d4.w));
+                        if (OOMB_KV_X2) {
+                            const float2 a = mul2(make_float2(pr[c], pr[c + 1]),
+                                                  add2(make_float2(__uint_as_float(dv[4 * c4]), __uint_as_float(dv[4 * c4 + 1])),
+                                                       make_float2(-d4.x, -d4.y)));
+                            const float2 b = mul2(make_float2(pr[c + 2], pr[c + 3]),
+                                                  add2(make_float2(__uint_as_float(dv[4 * c4 + 2]), __uint_as_float(dv[4 * c4 + 3])),
+                                                       make_float2(-d4.z, -d4.w)));
+                            pk[2 * c4] = pack_bf16(a.x, a.y);
+                            pk[2 * c4 + 1] = pack_bf16(b.x, b.y);
+                        } else {
+                            pk[2 * c4] = pack_bf16(pr[c] * (__uint_as_float(dv[4 * c4]) - d4.x),
+                                                   pr[c + 1] * (__uint_as_float(dv[4 * c4 + 1]) - d4.y));
+                            pk[2 * c4 + 1] = pack_bf16(pr[c + 2] * (__uint_as_float(dv[4 * c4 + 2]) - d4.z),
+                                                       pr[c + 3] * (__uint_as_float(dv[4 * c4 + 3]) - d4.w));
+                        }
                     }
                     tmem_st16(tDP + c2 * 16, pk);
                 }
@@ -991,7 +1094,8 @@ bool tc_bwd_available() { return true; }
 
 size_t attn_bwd_tc_workspace(const AttnGeom& g, int) {
     const size_t hc = static_cast<size_t>(g.Hq) * g.C * sizeof(float);
-    return ((2 * hc + 255) & ~size_t(255)) + static_cast<size_t>(g.max_pages) * 12 + 256;
+    const size_t order = (static_cast<size_t>(g.C / kTile) + static_cast<size_t>(g.max_pages) * bwd_blocks_per_page(g)) * 4;
+    return ((2 * hc + 255) & ~size_t(255)) + static_cast<size_t>(g.max_pages) * 12 + 512 + order;
 }
 
 void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* dout, const void* q,
@@ -1024,6 +1128,13 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         bwd_union_kernel<<<1, 1024, 0, st>>>(w.mask, n_pages, w.uni, w.n_uni);
         check_launch("bwd_union_kernel");
     }
+    // page size 64 pairs union pages per unit: kept in union order
+    const bool lpt = OOMB_BWD_LPT && g.P != kHalf;
+    if (lpt) {
+        bwd_order_kernel<<<1, 1024, 0, st>>>(w.mask, w.uni, w.n_uni, g.chunk_keys ? g.C / kTile : 0,
+                                             bwd_blocks_per_page(g), std::max(1, g.P / kTile), w.order);
+        check_launch("bwd_order_kernel");
+    }
     // head dim 64: the 128-wide tiles carry zeros in columns 64-127 (TMA out-of-bounds fill) and the
     // stores of those columns fall outside the tensors (clipped): see launch_attn_fwd_tc4
     const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, g.hd);
@@ -1031,7 +1142,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     const CUtensorMap tkc = map_rows_heads(k_cur, g.C, g.Hkv, g.hd);
     const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, g.hd);
     BwdParams p{g, sel_off, sel_ids, d_kvslot_layer, d_gslot_layer, gkpool, gvpool, w.Dt, w.Lt, w.mask, w.uni,
-                w.n_uni, dq, dk_cur, dv_cur, d_err, CtaTrace{}};
+                w.n_uni, lpt ? w.order : nullptr, dq, dk_cur, dv_cur, d_err, CtaTrace{}};
     delete prep_scope;
     // dQ and dK/dV only read the chunk's inputs and the prep outputs: dQ runs on the pool's side
     // stream, launched first, and the persistent dK/dV CTAs pick up SMs as dQ's last wave drains

@@ -52,6 +52,14 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define OOMB_FWD4_POLY 0  // measured: no gain (the softmax phase is latency-bound, not MUFU-bound)
 #endif
 constexpr bool kF4Poly = OOMB_FWD4_POLY != 0;
+#ifndef OOMB_FWD4_LEAN
+#define OOMB_FWD4_LEAN 1  // the FMA-pipe exponential is ex2_lean (one ALU op) rather than ex2_poly
+#endif
+constexpr bool kF4Lean = OOMB_FWD4_LEAN != 0;
+#ifndef OOMB_FWD4_X2
+#define OOMB_FWD4_X2 0  // softmax scale-subtract and row sums as packed fp32 pairs
+#endif
+constexpr bool kF4X2 = OOMB_FWD4_X2 != 0;
 
 struct F4Bars {
     uint64_t q_full;
@@ -256,17 +264,41 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
             float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            float pe0 = 0.f, pe1 = 0.f;  // kF4X2: the even pair of exponentials, summed with the odd one
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) {
                 uint32_t pk[16];
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
-                    const float x0 = fmaf(__uint_as_float(sr[c4 * 32 + 2 * u]), sl2, -m_use);
-                    const float x1 = fmaf(__uint_as_float(sr[c4 * 32 + 2 * u + 1]), sl2, -m_use);
+                    float x0, x1;
+                    if (kF4X2) {  // packed fp32 pair: the same two IEEE FMAs in one issue slot
+                        const float2 x = fma2(make_float2(__uint_as_float(sr[c4 * 32 + 2 * u]),
+                                                          __uint_as_float(sr[c4 * 32 + 2 * u + 1])),
+                                              make_float2(sl2, sl2), make_float2(-m_use, -m_use));
+                        x0 = x.x;
+                        x1 = x.y;
+                    } else {
+                        x0 = fmaf(__uint_as_float(sr[c4 * 32 + 2 * u]), sl2, -m_use);
+                        x1 = fmaf(__uint_as_float(sr[c4 * 32 + 2 * u + 1]), sl2, -m_use);
+                    }
                     const float e0 = ex2(x0);
-                    const float e1 = (kF4Poly && (u & 1)) ? ex2_poly(x1) : ex2(x1);  // 1 in 4 on the FMA pipe
-                    rs8[(2 * u) & 7] += e0;
-                    rs8[(2 * u + 1) & 7] += e1;
+                    // 1 in 4 on the FMA pipe
+                    const float e1 = (kF4Poly && (u & 1)) ? (kF4Lean ? ex2_lean(x1) : ex2_poly(x1)) : ex2(x1);
+                    if (kF4X2 && (u & 1)) {  // row sums as packed pairs too (same additions, same order)
+                        const float2 a = add2(make_float2(rs8[(2 * u - 2) & 7], rs8[(2 * u - 1) & 7]),
+                                              make_float2(pe0, pe1));
+                        const float2 b = add2(make_float2(rs8[(2 * u) & 7], rs8[(2 * u + 1) & 7]), make_float2(e0, e1));
+                        rs8[(2 * u - 2) & 7] = a.x;
+                        rs8[(2 * u - 1) & 7] = a.y;
+                        rs8[(2 * u) & 7] = b.x;
+                        rs8[(2 * u + 1) & 7] = b.y;
+                    } else if (kF4X2) {
+                        pe0 = e0;
+                        pe1 = e1;
+                    } else {
+                        rs8[(2 * u) & 7] += e0;
+                        rs8[(2 * u + 1) & 7] += e1;
+                    }
                     pk[u] = pack_bf16(e0, e1);
                 }
                 tmem_st16(tS + c4 * 16, pk);  // P cols [16 c4, 16 c4 + 16): below the S columns still unread

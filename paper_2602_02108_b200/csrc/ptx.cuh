@@ -292,6 +292,43 @@ __device__ __forceinline__ float ex2_poly(float x) {
     const float r = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
     return x > -126.0f ? r : 0.0f;  // masked (-inf) and underflowing inputs give exactly 0
 }
+// The same split with one ALU instruction (the clamp): the exponent is added with an integer
+// multiply-add (t_bits * 2^23 + p_bits, on the FMA pipe) instead of shift + add + select, so the
+// FMA-pipe exponential does not trade MUFU time for ALU time. Inputs below -125 (incl. -inf)
+// give ~2^-125 instead of 0: callers zero masked entries themselves, and such a P is below
+// every tolerance (it rounds to the bf16 operand's smallest normals).
+__device__ __forceinline__ float ex2_lean(float x) {
+    const float xc = fmaxf(x, -125.0f);
+    const float t = xc + 12582912.0f;
+    const float f = xc - (t - 12582912.0f);
+    const float p = fmaf(fmaf(fmaf(0.0553458875f, f, 0.24260599f), f, 0.69322751f), f, 0.999927776f);
+    int r;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(__float_as_int(t)), "r"(1 << 23), "r"(__float_as_int(p)));
+    return __int_as_float(r);
+}
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2 / FMUL2): the same IEEE results as two scalar ops with
+// half the issue slots.
+__device__ __forceinline__ unsigned long long f2_bits(float a, float b) {
+    return (static_cast<unsigned long long>(__float_as_uint(b)) << 32) | __float_as_uint(a);
+}
+__device__ __forceinline__ float2 f2_of(unsigned long long v) {
+    return make_float2(__uint_as_float(static_cast<uint32_t>(v)), __uint_as_float(static_cast<uint32_t>(v >> 32)));
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_bits(a.x, a.y)), "l"(f2_bits(b.x, b.y)), "l"(f2_bits(c.x, c.y)));
+    return f2_of(d);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a.x, a.y)), "l"(f2_bits(b.x, b.y)));
+    return f2_of(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a.x, a.y)), "l"(f2_bits(b.x, b.y)));
+    return f2_of(d);
+}
 // Degree-4 variant (max relative error 2.9e-6) for paths that accumulate fp32 probabilities
 // (the page vote), where the degree-3 error would approach the scorer's tolerance.
 __device__ __forceinline__ float ex2_poly4(float x) {

@@ -36,6 +36,13 @@ constexpr int kQpGroup = OOMB_VOTE_QPG;  // query pages per vote CTA (4 / 16 mea
 #define OOMB_SCORE_POLY 4
 #endif
 constexpr int kScPoly = OOMB_SCORE_POLY;  // 0: every exp2 on MUFU
+#ifndef OOMB_STATS_PLANES
+#define OOMB_STATS_PLANES 2
+#endif
+// K_avg planes the stats pass multiplies (2: hi + lo; 1: hi only). The row max only has to be
+// consistent between the passes, and the row sum's hi-only error averages out over the
+// 128 tokens x G heads a page's vote sums.
+constexpr int kStPlanes = OOMB_STATS_PLANES;
 
 __global__ void kavg_prep_kernel(const float* __restrict__ sum, const int32_t* __restrict__ cnt,
                                  const float* __restrict__ kavg_f32, int n, int n_pad, int Hkv, int hd,
@@ -127,8 +134,8 @@ __global__ void __launch_bounds__(384, 1)
             for (int j = 0; j < nb; ++j) {
                 const int st = j % kStSt;
                 if (j >= kStSt) mbar_wait(&bars->k_empty[st], ((j / kStSt) - 1) & 1);
-                mbar_expect_tx(&bars->k_full[st], 2 * kTileBytes);
-                for (int pl = 0; pl < 2; ++pl)
+                mbar_expect_tx(&bars->k_full[st], kStPlanes * kTileBytes);
+                for (int pl = 0; pl < kStPlanes; ++pl)
                     for (int r = 0; r < 2; ++r)
                         tma_load_2d(sK + (2 * st + pl) * kTileBytes + r * kRegion, &tm_ka, &bars->k_full[st], r * 64,
                                     pl * p.lo_row + kvh * p.kv_stride + j * kTile);
@@ -145,7 +152,7 @@ __global__ void __launch_bounds__(384, 1)
             if (j >= 2) mbar_wait(&bars->s_free[b], ((j - 2) >> 1) & 1);
             tc_fence_after();
 #pragma unroll
-            for (int pl = 0; pl < 2; ++pl) {  // S = Q hi^T + Q lo^T
+            for (int pl = 0; pl < kStPlanes; ++pl) {  // S = Q hi^T + Q lo^T
                 const uint64_t so = boff((2 * st + pl) * kTileBytes);
 #pragma unroll
                 for (int ks = 0; ks < kHd / 16; ++ks)
