@@ -3,7 +3,7 @@
 // chunktrain/attention.hpp — the reference's attention operators (attention.hpp:32-293) with
 // their host signatures, computed on the B200 by liboomb.so (score_pages, select_topk(_row),
 // select_recent / select_all, attn_forward, attn_backward). Source-compatibility header: see
-// chunktrain/common.hpp. Device arithmetic is the fp32 parity path for every Real.
+// chunktrain/common.hpp. Real = float runs the fp32 device path, Real = double the fp64 one.
 #pragma once
 
 #include <span>

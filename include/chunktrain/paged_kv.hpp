@@ -4,9 +4,9 @@
 // liboomb.so, with the reference's host-tensor signatures. Source-compatibility header: see
 // chunktrain/common.hpp.
 //
-// Real selects the host element type of the call sites; the pages live on the device in fp32
-// (the pool's parity dtype: BASELINE's fp32 tolerance is 1e-5), so a PagedCache<double> computes
-// in fp32 and meets fp32 tolerances, not the reference's f64 ones.
+// Real selects the device pool: PagedCache<float> is an OOMB_F32 pool, PagedCache<double> an
+// OOMB_F64 pool whose pages, K_avg, gradients and attention arithmetic are double, as the
+// reference's Real = double is.
 // key_page_data returns a host mirror of the page in the reference's block layout [P][Hkv][hd],
 // refreshed on every call at a stable address per (layer, page) (the device page itself never
 // moves: slots are stable, paged_kv.hpp:353).
@@ -14,6 +14,7 @@
 
 #include <map>
 #include <span>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -35,12 +36,13 @@ public:
         std::vector<uint8_t> valid;
     };
 
-    explicit PagedCache(const ModelConfig& cfg) : cfg_(cfg), dev_(cfg, oomb::DType::f32) {}
+    static constexpr oomb::DType kDType = std::is_same_v<Real, double> ? oomb::DType::f64 : oomb::DType::f32;
+    explicit PagedCache(const ModelConfig& cfg) : cfg_(cfg), dev_(cfg, kDType) {}
 
     const ModelConfig& config() const { return cfg_; }
     int page_size() const { return cfg_.page_size; }
     int64_t page_elems() const { return dev_.page_elems(); }
-    uint64_t page_buffer_bytes() const { return static_cast<uint64_t>(page_elems()) * sizeof(float); }
+    uint64_t page_buffer_bytes() const { return static_cast<uint64_t>(page_elems()) * sizeof(Real); }
     uint64_t page_kv_bytes() const { return 2 * page_buffer_bytes(); }
     int64_t filled(int layer) const { return dev_.filled(layer); }
     int n_pages(int layer) const { return dev_.n_pages(layer); }
@@ -58,8 +60,8 @@ public:
         const int64_t want = static_cast<int64_t>(ids.size()) * cfg_.page_size;
         if (dk.rank() != 3 || dk.dim(0) != want || dk.shape != dv.shape)
             throw ShapeError("scatter_add_grads: gradient shape does not match gather layout");
-        dev_.scatter_add_grads(layer, ids, oomb::DeviceTensor::from_host(dk, oomb::DType::f32),
-                               oomb::DeviceTensor::from_host(dv, oomb::DType::f32));
+        dev_.scatter_add_grads(layer, ids, oomb::DeviceTensor::from_host(dk, kDType),
+                               oomb::DeviceTensor::from_host(dv, kDType));
     }
     Tensor<Real> page_mean_keys(int layer, int n_candidates = -1) const {
         return dev_.page_mean_keys(layer, n_candidates).template to_tensor<Real>();

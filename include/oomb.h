@@ -19,8 +19,12 @@
  *    Layouts are the reference's row-major ones: q/out/dout/dq [tokens][Hq][hd],
  *    k/v/k_cur/v_cur/dk_cur/dv_cur [rows][Hkv][hd], lse [tokens][Hq].
  *  - Element types: q, k, v, k_cur, v_cur, out, dout use the pool dtype
- *    (OOMB_F32 or OOMB_BF16); lse, votes, dq, dk_cur, dv_cur and the gradient
- *    pool are always fp32.
+ *    (OOMB_F32, OOMB_BF16 or OOMB_F64). lse, votes, dq, dk_cur, dv_cur, K_avg and the
+ *    gradient pool use the pool's ACCUMULATION type: float for OOMB_F32 / OOMB_BF16 pools,
+ *    double for OOMB_F64 pools (the reference's Real = double). Those arguments are
+ *    declared void* (float* / double* convert implicitly). OOMB_F64 pools run the exact
+ *    SIMT kernels; the tcgen05 kernels, RoPE epilogues, real offload and the page-range
+ *    merge are bf16 / fp32 paths.
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
  *    every call is stream-ordered and asynchronous unless documented.
  *  - Handles are not thread-safe.
@@ -51,7 +55,7 @@ typedef enum {
     OOMB_ERROR = 9
 } oomb_status;
 
-typedef enum { OOMB_F32 = 0, OOMB_BF16 = 1 } oomb_dtype;
+typedef enum { OOMB_F32 = 0, OOMB_BF16 = 1, OOMB_F64 = 2 } oomb_dtype;
 
 /* ModelConfig fields on the path (config.hpp:19-49) + device sizing. */
 typedef struct {
@@ -139,16 +143,16 @@ OOMB_API int oomb_page_table_get(oomb_pool_t pool, int layer, int32_t* out_host)
 /* Device slots {kv_slot, grad_slot} per logical page (-1 = none / not resident). */
 OOMB_API int oomb_device_slots_get(oomb_pool_t pool, int layer, int32_t* out_host);
 /* PagedCache::page_mean_keys  paged_kv.hpp:170-183 -> out [n][Hkv][hd] fp32 device. */
-OOMB_API int oomb_page_mean_keys(oomb_pool_t pool, int layer, int n_candidates, float* out, void* stream, int* n_out);
-/* Raw K_avg state (sums fp32 [n][Hkv][hd] device, counts int32 [n] device). */
-OOMB_API int oomb_kavg_raw(oomb_pool_t pool, int layer, float* sum_out, int32_t* count_out, void* stream);
+OOMB_API int oomb_page_mean_keys(oomb_pool_t pool, int layer, int n_candidates, void* out, void* stream, int* n_out);
+/* Raw K_avg state (sums [n][Hkv][hd] in the accumulation type, counts int32 [n]; device). */
+OOMB_API int oomb_kavg_raw(oomb_pool_t pool, int layer, void* sum_out, int32_t* count_out, void* stream);
 /* PagedCache::gather_pages / gather_grad_pages  paged_kv.hpp:118-130. ids on host; k/v out
  * [n*P][Hkv][hd] device (pool dtype for KV, fp32 for grads); valid [n*P] uint8 device. */
 OOMB_API int oomb_gather_pages(oomb_pool_t pool, int layer, const int32_t* ids_host, int n, int grads, void* k_out,
                       void* v_out, uint8_t* valid_out, void* stream);
 /* PagedCache::scatter_add_grads  paged_kv.hpp:135-164. dk/dv fp32 [n*P][Hkv][hd] device. */
-OOMB_API int oomb_scatter_add_grads(oomb_pool_t pool, int layer, const int32_t* ids_host, int n, const float* dk,
-                           const float* dv, void* stream);
+OOMB_API int oomb_scatter_add_grads(oomb_pool_t pool, int layer, const int32_t* ids_host, int n, const void* dk,
+                           const void* dv, void* stream);
 /* Tier tags and residency enforcement  paged_kv.hpp:199-211. Tiers: 0 device, 1 host (the
  * reference's two), 2 remote (owned by another page-range shard), 3 lost (a host-tier page whose
  * pinned copy was dropped when a real offload engine detached without room to restore it).
@@ -182,37 +186,37 @@ OOMB_API int oomb_selection_filter_owned(oomb_pool_t pool, oomb_selection_t src,
 OOMB_API int oomb_page_owner(oomb_pool_t pool, int* stride, int* rank);
 /* select_topk_row per row of a device vote matrix [m][n] fp32  attention.hpp:71-96:
  * k largest, ties to the lower id, ascending; k >= n -> all; k < 0 -> SHAPE_ERROR. */
-OOMB_API int oomb_select_topk(oomb_selection_t sel, const float* vote, int m, int n, int k, void* stream);
+OOMB_API int oomb_select_topk(oomb_selection_t sel, const void* vote, int m, int n, int k, void* stream);
 
 /* ---- scoring ------------------------------------------------------------ */
 /* score_pages  attention.hpp:32-67 on explicit representatives:
  * q [tokens][Hq][hd] (dtype), k_avg [n][Hkv][hd] fp32 -> vote [ceil(tokens/P)][n] fp32 device. */
-OOMB_API int oomb_score_pages(const void* q, int64_t tokens, int n_q_heads, int head_dim, const float* k_avg, int64_t n,
-                     int n_kv_heads, int page_size, int score_scale, int dtype, float* vote, void* stream);
+OOMB_API int oomb_score_pages(const void* q, int64_t tokens, int n_q_heads, int head_dim, const void* k_avg, int64_t n,
+                     int n_kv_heads, int page_size, int score_scale, int dtype, void* vote, void* stream);
 /* The trainer's top-k selector in one call (chunk_trainer.hpp:305-311): K_avg of the first
  * n_candidates pages of `layer` (pinned metadata) -> score_pages -> select_topk_row per query page. */
 OOMB_API int oomb_select_pages_topk(oomb_pool_t pool, int layer, const void* q, int64_t tokens, int n_candidates,
-                           oomb_selection_t sel, float* vote_scratch, void* stream);
+                           oomb_selection_t sel, void* vote_scratch, void* stream);
 
 /* KV-group sharding support: the vote of score_pages sums over ALL q-heads
  * (attention.hpp:44-64). A rank holding a subset of KV groups computes per-group partial votes
  * [Hkv_local][m][n] fp32; after an all-gather in global group order, oomb_vote_reduce sums them in
  * that fixed order, so every rank (and the single-GPU path) selects identically. */
 OOMB_API int oomb_score_pages_partial(oomb_pool_t pool, int layer, const void* q, int64_t tokens, int n_candidates,
-                                      float* partials, void* stream);
+                                      void* partials, void* stream);
 OOMB_API int oomb_vote_reduce(const float* partials, int groups, int64_t m, int64_t n, float* vote, void* stream);
 
 /* ---- attention ---------------------------------------------------------- */
 /* attn_forward  attention.hpp:156-208: q [C][Hq][hd], k_cur/v_cur [C][Hkv][hd] (pool dtype) ->
  * out [C][Hq][hd] (pool dtype), lse [C][Hq] fp32 (natural log). */
 OOMB_API int oomb_attn_forward(oomb_pool_t pool, int layer, const void* q, int64_t tokens, oomb_selection_t sel,
-                      const void* k_cur, const void* v_cur, void* out, float* lse, void* stream);
+                      const void* k_cur, const void* v_cur, void* out, void* lse, void* stream);
 /* attn_backward  attention.hpp:222-293: rebuilds P from the saved lse, D from the saved out;
  * past-page dK/dV are accumulated IN PLACE into the fp32 gradient pool (lazily allocated
  * and zeroed per page, reference order); dq/dk_cur/dv_cur fp32 are overwritten. */
 OOMB_API int oomb_attn_backward(oomb_pool_t pool, int layer, const void* dout, const void* q, int64_t tokens,
                        oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out,
-                       const float* lse, float* dq, float* dk_cur, float* dv_cur, void* stream);
+                       const void* lse, void* dq, void* dk_cur, void* dv_cur, void* stream);
 /* Page-range split: a shard attends only its share of every query page's
  * selected pages. flags = OOMB_ATTN_PAST_ONLY drops the chunk's own causal keys (the shard that
  * owns them passes 0). The forward then writes that shard's partial (out, lse) — lse = -inf and
@@ -227,11 +231,11 @@ OOMB_API int oomb_attn_backward(oomb_pool_t pool, int layer, const void* dout, c
  * the selection and dq must stay untouched until then. */
 #define OOMB_ATTN_DEFER_DQ 2
 OOMB_API int oomb_attn_forward_ex(oomb_pool_t pool, int layer, const void* q, int64_t tokens, oomb_selection_t sel,
-                                  const void* k_cur, const void* v_cur, void* out, float* lse, int flags,
+                                  const void* k_cur, const void* v_cur, void* out, void* lse, int flags,
                                   void* stream);
 OOMB_API int oomb_attn_backward_ex(oomb_pool_t pool, int layer, const void* dout, const void* q, int64_t tokens,
                                    oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out,
-                                   const float* lse, float* dq, float* dk_cur, float* dv_cur, int flags,
+                                   const void* lse, void* dq, void* dk_cur, void* dv_cur, int flags,
                                    void* stream);
 /* Exact merge of page-range shards' partial attention outputs, shards in rank order:
  * o_parts [parts][rows][hd] (dtype), lse_parts [parts][rows] fp32 natural log ->
@@ -246,8 +250,8 @@ OOMB_API int oomb_set_kernel_policy(oomb_pool_t pool, int policy);
 
 /* dM_i read-back (chunk_trainer.hpp:575-587): dk[i*P+s] += grad_k(ids[i], s) and the same for
  * dv, reference layout [n*P][Hkv][hd] fp32 device; pages without gradients add 0. */
-OOMB_API int oomb_accumulate_grad_pages(oomb_pool_t pool, int layer, const int32_t* ids_host, int n, float* dk,
-                                        float* dv, void* stream);
+OOMB_API int oomb_accumulate_grad_pages(oomb_pool_t pool, int layer, const int32_t* ids_host, int n, void* dk,
+                                        void* dv, void* stream);
 /* The reverse projection epilogue (chunk_trainer.hpp:575-592): the dM_i read-back
  * followed by rope_backward of dK (ops.hpp:227-230) in one pass: dk <- rope^-1(dk + grad_k),
  * dv <- dv + grad_v, row r at absolute position pos_offset + r. Bitwise equal to

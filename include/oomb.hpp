@@ -35,6 +35,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -139,8 +140,10 @@ struct ModelConfig {
 };
 
 // ---------------------------------------------------------------------------- tensors
-enum class DType { f32 = OOMB_F32, bf16 = OOMB_BF16, i32 = 2, u8 = 3 };
-inline size_t dtype_size(DType d) { return d == DType::bf16 ? 2 : d == DType::u8 ? 1 : 4; }
+enum class DType { f32 = OOMB_F32, bf16 = OOMB_BF16, f64 = OOMB_F64, i32 = 10, u8 = 11 };
+inline size_t dtype_size(DType d) { return d == DType::bf16 ? 2 : d == DType::u8 ? 1 : d == DType::f64 ? 8 : 4; }
+// Accumulation type of a pool dtype: K_avg, gradient pages, lse / dq / dk_cur / dv_cur and votes.
+inline DType acc_dtype(DType pool) { return pool == DType::f64 ? DType::f64 : DType::f32; }
 
 inline uint16_t f32_to_bf16(float f) {  // round to nearest even (NaN kept quiet)
     uint32_t u;
@@ -208,6 +211,10 @@ public:
             std::vector<float> h(static_cast<size_t>(n));
             for (int64_t i = 0; i < n; ++i) h[i] = static_cast<float>(src[i]);
             t.upload(h.data());
+        } else if (dt == DType::f64) {
+            std::vector<double> h(static_cast<size_t>(n));
+            for (int64_t i = 0; i < n; ++i) h[i] = static_cast<double>(src[i]);
+            t.upload(h.data());
         } else {
             throw ShapeError("from_host: floating-point dtypes only");
         }
@@ -234,6 +241,10 @@ public:
             for (int64_t i = 0; i < n; ++i) out[i] = static_cast<Real>(bf16_to_f32(h[i]));
         } else if (dtype_ == DType::f32) {
             std::vector<float> h(static_cast<size_t>(n));
+            download(h.data());
+            for (int64_t i = 0; i < n; ++i) out[i] = static_cast<Real>(h[i]);
+        } else if (dtype_ == DType::f64) {
+            std::vector<double> h(static_cast<size_t>(n));
             download(h.data());
             for (int64_t i = 0; i < n; ++i) out[i] = static_cast<Real>(h[i]);
         } else if (dtype_ == DType::i32) {
@@ -318,7 +329,8 @@ public:
                         int64_t device_capacity_pages = -1, int page_owner_stride = 0, int page_owner_rank = 0)
         : cfg_(cfg), dtype_(dtype) {
         cfg.validate();
-        if (dtype != DType::bf16 && dtype != DType::f32) throw ConfigError("PagedCache: dtype must be bf16 or f32");
+        if (dtype != DType::bf16 && dtype != DType::f32 && dtype != DType::f64)
+            throw ConfigError("PagedCache: dtype must be bf16, f32 or f64");
         oomb_config c{cfg.n_layers,       cfg.n_q_heads,    cfg.n_kv_heads,
                       cfg.head_dim,       cfg.chunk_size,   cfg.page_size,
                       cfg.retrieval_budget, cfg.local_window, cfg.score_scale ? 1 : 0,
@@ -385,16 +397,16 @@ public:
                            cudaStream_t st = nullptr) {
         const int64_t want = static_cast<int64_t>(ids.size()) * cfg_.page_size;
         if (dk.rank() != 3 || dk.dim(0) != want || dk.dim(1) != cfg_.n_kv_heads || dk.dim(2) != cfg_.head_dim ||
-            !dk.same_shape(dv) || dk.dtype() != DType::f32 || dv.dtype() != DType::f32)
+            !dk.same_shape(dv) || dk.dtype() != acc_dtype(dtype_) || dv.dtype() != acc_dtype(dtype_))
             throw ShapeError("scatter_add_grads: gradient shape does not match gather layout");
-        check(oomb_scatter_add_grads(pool_, layer, ids.data(), static_cast<int>(ids.size()), dk.as<float>(),
-                                     dv.as<float>(), sv(st)));
+        check(oomb_scatter_add_grads(pool_, layer, ids.data(), static_cast<int>(ids.size()), dk.data(), dv.data(),
+                                     sv(st)));
     }
     // dM_i read-back (chunk_trainer.hpp:575-587): dk/dv += the pages' gradient rows.
     void accumulate_grad_pages(int layer, std::span<const int32_t> ids, DeviceTensor& dk, DeviceTensor& dv,
                                cudaStream_t st = nullptr) {
-        check(oomb_accumulate_grad_pages(pool_, layer, ids.data(), static_cast<int>(ids.size()), dk.as<float>(),
-                                         dv.as<float>(), sv(st)));
+        check(oomb_accumulate_grad_pages(pool_, layer, ids.data(), static_cast<int>(ids.size()), dk.data(), dv.data(),
+                                         sv(st)));
     }
     // The same read-back fused with rope_backward of dK (chunk_trainer.hpp:575-592): row r of dk is
     // rotated back from absolute position pos_offset + r.
@@ -406,9 +418,9 @@ public:
     // paged_kv.hpp:170-183: [n][Hkv][hd] fp32.
     DeviceTensor page_mean_keys(int layer, int n_candidates = -1, cudaStream_t st = nullptr) const {
         const int n = n_candidates < 0 ? n_pages(layer) : std::min(n_candidates, n_pages(layer));
-        DeviceTensor out({n, cfg_.n_kv_heads, cfg_.head_dim}, DType::f32, false);
+        DeviceTensor out({n, cfg_.n_kv_heads, cfg_.head_dim}, acc_dtype(dtype_), false);
         int n_out = 0;
-        check(oomb_page_mean_keys(pool_, layer, n_candidates, out.as<float>(), sv(st), &n_out));
+        check(oomb_page_mean_keys(pool_, layer, n_candidates, out.data(), sv(st), &n_out));
         return out;
     }
     MemoryReport memory_report() const {
@@ -452,8 +464,8 @@ private:
     }
     Gathered gather(int layer, std::span<const int32_t> ids, bool grads, cudaStream_t st) const {
         const int64_t rows = static_cast<int64_t>(ids.size()) * cfg_.page_size;
-        Gathered g{DeviceTensor({rows, cfg_.n_kv_heads, cfg_.head_dim}, grads ? DType::f32 : dtype_),
-                   DeviceTensor({rows, cfg_.n_kv_heads, cfg_.head_dim}, grads ? DType::f32 : dtype_),
+        Gathered g{DeviceTensor({rows, cfg_.n_kv_heads, cfg_.head_dim}, grads ? acc_dtype(dtype_) : dtype_),
+                   DeviceTensor({rows, cfg_.n_kv_heads, cfg_.head_dim}, grads ? acc_dtype(dtype_) : dtype_),
                    DeviceTensor({rows}, DType::u8)};
         check(oomb_gather_pages(pool_, layer, ids.data(), static_cast<int>(ids.size()), grads ? 1 : 0, g.k.data(),
                                 g.v.data(), g.valid.as<uint8_t>(), sv(st)));
@@ -513,20 +525,23 @@ inline DeviceTensor score_pages(const DeviceTensor& q, const DeviceTensor& k_avg
     if (q.rank() != 3 || k_avg.rank() != 3) throw ShapeError("score_pages: expected rank-3 inputs");
     if (k_avg.dim(0) < 1) throw ShapeError("score_pages: needs at least one candidate page");
     if (q.dim(1) != static_cast<int64_t>(gqa_group) * k_avg.dim(1) || q.dim(2) != k_avg.dim(2) ||
-        k_avg.dtype() != DType::f32 || (q.dtype() != DType::f32 && q.dtype() != DType::bf16))
+        k_avg.dtype() != acc_dtype(q.dtype()) ||
+        (q.dtype() != DType::f32 && q.dtype() != DType::bf16 && q.dtype() != DType::f64))
         throw ShapeError("score_pages: head counts / dtypes do not match");
     const int64_t m = (q.dim(0) + page_size - 1) / page_size;
-    DeviceTensor vote({m, k_avg.dim(0)}, DType::f32, false);
+    DeviceTensor vote({m, k_avg.dim(0)}, acc_dtype(q.dtype()), false);
     check(oomb_score_pages(q.data(), q.dim(0), static_cast<int>(q.dim(1)), static_cast<int>(q.dim(2)),
-                           k_avg.as<float>(), k_avg.dim(0), static_cast<int>(k_avg.dim(1)), page_size,
-                           score_scale ? 1 : 0, static_cast<int>(q.dtype()), vote.as<float>(), sv(st)));
+                           k_avg.data(), k_avg.dim(0), static_cast<int>(k_avg.dim(1)), page_size,
+                           score_scale ? 1 : 0, static_cast<int>(q.dtype()), vote.data(), sv(st)));
     return vote;
 }
 template <class Real>
 Tensor<Real> score_pages(const Tensor<Real>& q, const Tensor<Real>& k_avg, int page_size, int gqa_group,
                          bool score_scale = false) {
     if (q.rank() != 3 || k_avg.rank() != 3) throw ShapeError("score_pages: expected rank-3 inputs");
-    return score_pages(DeviceTensor::from_host(q, DType::f32), DeviceTensor::from_host(k_avg, DType::f32), page_size,
+    // Real = double computes in double on the device (an OOMB_F64 path), float in fp32
+    const DType dt = std::is_same_v<Real, double> ? DType::f64 : DType::f32;
+    return score_pages(DeviceTensor::from_host(q, dt), DeviceTensor::from_host(k_avg, dt), page_size,
                        gqa_group, score_scale)
         .template to_tensor<Real>();
 }
@@ -548,15 +563,16 @@ inline std::vector<int32_t> select_all(int n_pages) {
 // k largest, ties to the lower id, ascending; k >= n -> all; k < 0 -> ShapeError).
 inline Selection select_topk_rows(const PagedCache& cache, const DeviceTensor& vote, int budget_pages,
                                   cudaStream_t st = nullptr) {
-    if (vote.rank() != 2 || vote.dtype() != DType::f32) throw ShapeError("select_topk: vote must be [m x n] f32");
+    if (vote.rank() != 2 || vote.dtype() != acc_dtype(cache.dtype()))
+        throw ShapeError("select_topk: vote must be [m x n] in the pool's accumulation type");
     const int m = static_cast<int>(vote.dim(0)), n = static_cast<int>(vote.dim(1));
     const int kk = std::min(std::max(budget_pages, 0), n);
     Selection sel(cache, m, m * kk);
-    check(oomb_select_topk(sel.handle(), vote.as<float>(), m, n, budget_pages, sv(st)));
+    check(oomb_select_topk(sel.handle(), vote.data(), m, n, budget_pages, sv(st)));
     return sel;
 }
 // attention.hpp:71-96 with the reference's host signatures, computed by the device selector on a
-// scratch pool. The row is rounded to fp32 first (the device votes are fp32).
+// scratch pool, on the row as double (an fp64 scratch pool), exactly as the reference compares it.
 namespace detail {
 inline const PagedCache& scratch_cache() {
     static PagedCache c([] {
@@ -564,7 +580,7 @@ inline const PagedCache& scratch_cache() {
         m.n_layers = 1, m.n_q_heads = 1, m.n_kv_heads = 1, m.head_dim = 2, m.chunk_size = 1, m.page_size = 1;
         m.retrieval_budget = 0;
         return m;
-    }(), DType::f32, 1);
+    }(), DType::f64, 1);  // the reference compares scores as double (attention.hpp:71-88)
     return c;
 }
 }  // namespace detail
@@ -572,7 +588,7 @@ inline std::vector<int32_t> select_topk(std::span<const double> score_row, int b
     if (budget_pages < 0) throw ShapeError("select_topk: negative budget");
     const int64_t n = static_cast<int64_t>(score_row.size());
     if (n == 0) return {};
-    auto vote = DeviceTensor::from_host(std::vector<int64_t>{1, n}, score_row.data(), DType::f32);
+    auto vote = DeviceTensor::from_host(std::vector<int64_t>{1, n}, score_row.data(), DType::f64);
     return select_topk_rows(detail::scratch_cache(), vote, budget_pages).lists()[0];
 }
 template <class Real>
@@ -591,9 +607,9 @@ inline Selection select_pages_topk(PagedCache& cache, int layer, const DeviceTen
     const int n = std::min(n_candidates, cache.n_pages(layer));
     const int k = std::min(cfg.budget_pages(), std::max(n, 0));
     Selection sel(cache, m, m * k);
-    DeviceTensor vote({m, std::max(n, 1)}, DType::f32, false);
+    DeviceTensor vote({m, std::max(n, 1)}, acc_dtype(cache.dtype()), false);
     check(oomb_select_pages_topk(cache.handle(), layer, q.data(), q.dim(0), n_candidates, sel.handle(),
-                                 vote.as<float>(), sv(st)));
+                                 vote.data(), sv(st)));
     return sel;
 }
 
@@ -633,10 +649,11 @@ inline DeviceAttnSaved attn_forward(const ModelConfig& cfg, const DeviceTensor& 
                                     Selection selected, const DeviceTensor& k_cur, const DeviceTensor& v_cur,
                                     cudaStream_t st = nullptr) {
     detail::check_qkv(cfg, q, k_cur, v_cur, "attn_forward");
-    DeviceAttnSaved s{DeviceTensor(q.shape(), q.dtype(), false), DeviceTensor({q.dim(0), q.dim(1)}, DType::f32, false),
+    DeviceAttnSaved s{DeviceTensor(q.shape(), q.dtype(), false),
+                      DeviceTensor({q.dim(0), q.dim(1)}, acc_dtype(cache.dtype()), false),
                       std::move(selected)};
     check(oomb_attn_forward(cache.handle(), layer, q.data(), q.dim(0), s.selected.handle(), k_cur.data(),
-                            v_cur.data(), s.out.data(), s.lse.as<float>(), sv(st)));
+                            v_cur.data(), s.out.data(), s.lse.data(), sv(st)));
     return s;
 }
 // attention.hpp:222-293 on the device: past-page dK/dV go into the cache's fp32 gradient pages.
@@ -646,11 +663,12 @@ inline DeviceAttnGrads attn_backward(const ModelConfig& cfg, const DeviceTensor&
                                      cudaStream_t st = nullptr) {
     detail::check_qkv(cfg, q, k_cur, v_cur, "attn_backward");
     if (!dout.same_shape(saved.out)) throw ShapeError("attn_backward: dO shape mismatch");
-    DeviceAttnGrads g{DeviceTensor(q.shape(), DType::f32, false), DeviceTensor(k_cur.shape(), DType::f32, false),
-                      DeviceTensor(k_cur.shape(), DType::f32, false)};
+    const DType acc = acc_dtype(cache.dtype());
+    DeviceAttnGrads g{DeviceTensor(q.shape(), acc, false), DeviceTensor(k_cur.shape(), acc, false),
+                      DeviceTensor(k_cur.shape(), acc, false)};
     check(oomb_attn_backward(cache.handle(), layer, dout.data(), q.data(), q.dim(0), saved.selected.handle(),
-                             k_cur.data(), v_cur.data(), saved.out.data(), saved.lse.as<float>(), g.dq.as<float>(),
-                             g.dk_cur.as<float>(), g.dv_cur.as<float>(), sv(st)));
+                             k_cur.data(), v_cur.data(), saved.out.data(), saved.lse.data(), g.dq.data(),
+                             g.dk_cur.data(), g.dv_cur.data(), sv(st)));
     return g;
 }
 
@@ -673,7 +691,7 @@ AttnGrads<Real> attn_backward(const ModelConfig& cfg, const Tensor<Real>& dout, 
                               const AttnSaved<Real>& saved) {
     if (dout.shape != saved.out.shape) throw ShapeError("attn_backward: dO shape mismatch");
     const DType dt = cache.dtype();
-    DeviceAttnSaved ds{DeviceTensor::from_host(saved.out, dt), DeviceTensor::from_host(saved.lse, DType::f32),
+    DeviceAttnSaved ds{DeviceTensor::from_host(saved.out, dt), DeviceTensor::from_host(saved.lse, acc_dtype(dt)),
                        Selection::from_lists(cache, saved.selected)};
     auto g = attn_backward(cfg, DeviceTensor::from_host(dout, dt), DeviceTensor::from_host(q, dt), cache, layer,
                            DeviceTensor::from_host(k_cur, dt), DeviceTensor::from_host(v_cur, dt), ds);

@@ -18,7 +18,7 @@ from . import _lib
 from ._lib import call
 from .config import ModelConfig
 from .errors import ShapeError
-from .paged_kv import PagedCache, _ptr, stream_handle
+from .paged_kv import DTYPE_CODE, PagedCache, _ptr, stream_handle
 
 
 class Selection:
@@ -98,17 +98,18 @@ def score_pages(q: torch.Tensor, k_avg: torch.Tensor, page_size: int, gqa_group:
     if q.dim() != 3 or k_avg.dim() != 3:
         raise ShapeError("score_pages: expected rank-3 inputs")
     dev = q.device if q.is_cuda else torch.device("cuda", torch.cuda.current_device())
-    dt = q.dtype if q.dtype in (torch.bfloat16, torch.float32) else torch.float32
+    dt = q.dtype if q.dtype in (torch.bfloat16, torch.float32, torch.float64) else torch.float32
+    acc = torch.float64 if dt == torch.float64 else torch.float32
     q = q.to(dev, dt).contiguous()
-    k_avg = k_avg.to(dev, torch.float32).contiguous()
+    k_avg = k_avg.to(dev, acc).contiguous()
     tokens, qh, hd = q.shape
     n, kvh = k_avg.shape[0], k_avg.shape[1]
     if qh != gqa_group * kvh:
         raise ShapeError("score_pages: head counts do not match the GQA group")
     m = (tokens + page_size - 1) // page_size
-    vote = torch.empty((m, max(n, 1)), dtype=torch.float32, device=dev)
+    vote = torch.empty((m, max(n, 1)), dtype=acc, device=dev)
     call("oomb_score_pages", _ptr(q), tokens, qh, hd, _ptr(k_avg), n, kvh, page_size, int(score_scale),
-         1 if dt == torch.bfloat16 else 0, _ptr(vote), stream_handle(stream))
+         DTYPE_CODE[dt], _ptr(vote), stream_handle(stream))
     return vote[:, :n]
 
 
@@ -125,7 +126,7 @@ def select_recent(n_pages: int, window: int) -> list[int]:
 
 def select_topk_rows(cache: PagedCache, vote: torch.Tensor, k: int, stream=None) -> Selection:
     """select_topk_row for every row of a device vote matrix, on the device."""
-    vote = vote.to(cache.device, torch.float32).contiguous()
+    vote = vote.to(cache.device, cache.acc_dtype).contiguous()
     m, n = vote.shape
     kk = min(max(k, 0), n)
     sel = Selection(cache, max(m, 1), m * kk)
@@ -137,13 +138,15 @@ def select_topk(score_row, budget_pages: int, cache: PagedCache | None = None) -
     """attention.hpp:71-88 on the device (ties -> lower id, ascending)."""
     if budget_pages < 0:
         raise ShapeError("select_topk: negative budget")
-    row = torch.as_tensor(np.asarray(score_row, dtype=np.float32)).reshape(1, -1)
     c = cache if cache is not None else _scratch_cache()
+    # the reference compares the row as double (attention.hpp:71-88): the scratch pool is fp64
+    row = torch.as_tensor(np.asarray(score_row, dtype=np.float64 if c.acc_dtype == torch.float64 else np.float32))
+    row = row.reshape(1, -1)
     return select_topk_rows(c, row, budget_pages).lists()[0]
 
 
 def select_topk_row(score: torch.Tensor, row: int, budget_pages: int, cache: PagedCache | None = None) -> list[int]:
-    return select_topk(score[row].detach().float().cpu().numpy(), budget_pages, cache)
+    return select_topk(score[row].detach().double().cpu().numpy(), budget_pages, cache)
 
 
 _SCRATCH = {}
@@ -153,7 +156,7 @@ def _scratch_cache() -> PagedCache:
     dev = torch.cuda.current_device()
     if dev not in _SCRATCH:
         _SCRATCH[dev] = PagedCache(ModelConfig(n_layers=1, n_q_heads=1, n_kv_heads=1, head_dim=2, chunk_size=1,
-                                               page_size=1, retrieval_budget=0), dtype="fp32", max_tokens=1)
+                                               page_size=1, retrieval_budget=0), dtype="fp64", max_tokens=1)
     return _SCRATCH[dev]
 
 
@@ -168,7 +171,7 @@ def select_pages_topk(cache: PagedCache, layer: int, q: torch.Tensor, n_candidat
     k = min(cfg.budget_pages(), max(n, 0))
     sel = out if out is not None else Selection(cache, max(m, 1), m * k)
     if vote is None or vote.numel() < m * max(n, 1):
-        vote = torch.empty((m, max(n, 1)), dtype=torch.float32, device=cache.device)
+        vote = torch.empty((m, max(n, 1)), dtype=cache.acc_dtype, device=cache.device)
     else:
         vote = vote.reshape(-1)[: m * max(n, 1)].view(m, max(n, 1))
     call("oomb_select_pages_topk", cache.handle, layer, _ptr(q), q.shape[0], n_candidates, sel.handle, _ptr(vote),
@@ -210,8 +213,8 @@ def attn_forward(cfg: ModelConfig, q, cache: PagedCache, layer: int, selected, k
         raise ShapeError("attn_forward: q / k_cur / v_cur shape mismatch")
     sel = as_selection(cache, selected, stream)
     out = torch.empty_like(q) if out is None else out
-    lse = torch.empty((c, qh), dtype=torch.float32, device=q.device) if lse is None else lse
-    if out.shape != q.shape or out.dtype != q.dtype or lse.shape != (c, qh) or lse.dtype != torch.float32:
+    lse = torch.empty((c, qh), dtype=cache.acc_dtype, device=q.device) if lse is None else lse
+    if out.shape != q.shape or out.dtype != q.dtype or lse.shape != (c, qh) or lse.dtype != cache.acc_dtype:
         raise ShapeError("attn_forward: preallocated out / lse have the wrong shape or dtype")
     # under residency enforcement the library checks the selected pages on the host before the
     # launch (ResidencyError, paged_kv.hpp:301-312); the kernels' device flag is read by
@@ -233,13 +236,13 @@ def attn_backward(cfg: ModelConfig, dout, q, cache: PagedCache, layer: int, k_cu
         raise ShapeError("attn_backward: dO shape mismatch")
     c = q.shape[0]
     if grads is None:
-        dq = torch.empty((c, cfg.n_q_heads, cfg.head_dim), dtype=torch.float32, device=q.device)
-        dk = torch.empty((c, cfg.n_kv_heads, cfg.head_dim), dtype=torch.float32, device=q.device)
+        dq = torch.empty((c, cfg.n_q_heads, cfg.head_dim), dtype=cache.acc_dtype, device=q.device)
+        dk = torch.empty((c, cfg.n_kv_heads, cfg.head_dim), dtype=cache.acc_dtype, device=q.device)
         dv = torch.empty_like(dk)
     else:
         dq, dk, dv = grads.dq, grads.dk_cur, grads.dv_cur
         if dq.shape != (c, cfg.n_q_heads, cfg.head_dim) or dk.shape != (c, cfg.n_kv_heads, cfg.head_dim) or \
-                dv.shape != dk.shape or {dq.dtype, dk.dtype, dv.dtype} != {torch.float32}:
+                dv.shape != dk.shape or {dq.dtype, dk.dtype, dv.dtype} != {cache.acc_dtype}:
             raise ShapeError("attn_backward: preallocated gradients have the wrong shape or dtype")
     sel = saved.selected if selected is None else as_selection(cache, selected, stream)
     call("oomb_attn_backward_ex", cache.handle, layer, _ptr(dout), _ptr(q), c, sel.handle, _ptr(k_cur),

@@ -39,14 +39,64 @@ __device__ __forceinline__ float from_f<float>(float x) { return x; }
 template <>
 __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
 
-__device__ __forceinline__ float warp_sum(float v) {
+// fp64 pools (OOMB_F64: the reference's Real = double) store and accumulate in double; fp32 and
+// bf16 pools accumulate in float. to_f / from_f of double exist only for the RoPE helpers, which the
+// host never runs on an fp64 pool.
+template <>
+__device__ __forceinline__ float to_f<double>(double x) { return static_cast<float>(x); }
+template <>
+__device__ __forceinline__ double from_f<double>(float x) { return x; }
+template <typename T>
+struct AccOf {
+    using type = float;
+};
+template <>
+struct AccOf<double> {
+    using type = double;
+};
+template <typename T>
+using acc_t = typename AccOf<T>::type;
+template <typename A, typename T>
+__device__ __forceinline__ A to_a(T x) { return static_cast<A>(x); }
+template <>
+__device__ __forceinline__ float to_a<float, __nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <typename T, typename A>
+__device__ __forceinline__ T from_a(A x) { return static_cast<T>(x); }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_a<__nv_bfloat16, float>(float x) { return __float2bfloat16_rn(x); }
+__device__ __forceinline__ float exp_a(float x) { return expf(x); }
+__device__ __forceinline__ double exp_a(double x) { return exp(x); }
+__device__ __forceinline__ float log_a(float x) { return logf(x); }
+__device__ __forceinline__ double log_a(double x) { return log(x); }
+__device__ __forceinline__ float max_a(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double max_a(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+template <typename A>
+struct Stat {  // score_pages row statistics: max and 1 / sum
+    A m, il;
+};
+template <typename A>
+__device__ __forceinline__ A scale_of(const AttnGeom& g);
+template <>
+__device__ __forceinline__ float scale_of<float>(const AttnGeom& g) { return g.scale; }
+template <>
+__device__ __forceinline__ double scale_of<double>(const AttnGeom& g) { return g.scale64; }
+
+template <typename A>
+__device__ __forceinline__ A warp_sum(A v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
-__device__ __forceinline__ float warp_max(float v) {
+template <typename A>
+__device__ __forceinline__ A warp_max(A v) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = 16; o > 0; o >>= 1) v = max_a(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 
@@ -75,7 +125,7 @@ __device__ __forceinline__ float rope_elem(const T* __restrict__ row, int d, dou
 template <typename T>
 __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, int64_t rows, int64_t filled,
                               int P, int Hkv, int hd, int first_page, NewSlots ns, int32_t* __restrict__ kvslot,
-                              T* __restrict__ kpool, T* __restrict__ vpool, float* __restrict__ ksum,
+                              T* __restrict__ kpool, T* __restrict__ vpool, acc_t<T>* __restrict__ ksum,
                               int32_t* __restrict__ kcnt, int* err, const double* __restrict__ rope_inv_freq,
                               __nv_bfloat16* __restrict__ planes, int64_t plane_stride) {
     const int re = Hkv * hd;
@@ -90,7 +140,7 @@ __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, 
     const int h = e / hd, d = e - (e / hd) * hd;
     const int64_t s0 = max(filled, static_cast<int64_t>(pg) * P);
     const int64_t s1 = min(filled + rows, static_cast<int64_t>(pg + 1) * P);
-    float sum = is_new ? 0.f : ksum[static_cast<int64_t>(pg) * re + e];
+    acc_t<T> sum = is_new ? acc_t<T>(0) : ksum[static_cast<int64_t>(pg) * re + e];
     // a REMOTE page (another page-range shard stores it) only gets its K_avg sums; a page with no
     // slot at all is not resident (the host checks the tail page first): flag it, write nothing
     const bool store = slot >= 0;
@@ -121,7 +171,7 @@ __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, 
                     kpool[dst0 + static_cast<size_t>(off) * hd] = kb[u];
                     vpool[dst0 + static_cast<size_t>(off) * hd] = vb[u];
                 }
-                sum = __fadd_rn(sum, to_f(kb[u]));
+                sum = add_rn(sum, to_a<acc_t<T>>(kb[u]));
             }
         }
     }
@@ -131,7 +181,7 @@ __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, 
         // the tcgen05 scorer's hi / lo bf16 planes of K_avg = sum * (1/count) (paged_kv.hpp:177-180),
         // [2][Hkv][plane_stride][hd]: kept current here, so scoring never re-splits completed pages
         const int cnt = static_cast<int>(s1 - static_cast<int64_t>(pg) * P);  // rows the page holds now
-        const float kav = __fmul_rn(sum, __fdiv_rn(1.0f, static_cast<float>(cnt)));
+        const float kav = __fmul_rn(static_cast<float>(sum), __fdiv_rn(1.0f, static_cast<float>(cnt)));
         const __nv_bfloat16 hi = __float2bfloat16_rn(kav);
         const size_t at = (static_cast<size_t>(h) * plane_stride + pg) * hd + d;
         planes[at] = hi;
@@ -141,7 +191,7 @@ __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, 
 
 void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_t filled_before, int P, int Hkv,
                    int hd, int first_page, int n_pages_touched, const NewSlots& ns, int32_t* d_kvslot_layer,
-                   void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, int* d_err,
+                   void* kpool, void* vpool, void* kavg_sum_layer, int32_t* kavg_cnt_layer, int* d_err,
                    cudaStream_t st, const double* rope_inv_freq, void* kavg_planes_layer, int64_t plane_stride) {
     if (rows <= 0 || n_pages_touched <= 0) return;
     __nv_bfloat16* planes = static_cast<__nv_bfloat16*>(kavg_planes_layer);
@@ -152,12 +202,19 @@ void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_
         append_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(
             static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), rows, filled_before, P, Hkv,
             hd, first_page, ns, d_kvslot_layer, static_cast<__nv_bfloat16*>(kpool), static_cast<__nv_bfloat16*>(vpool),
-            kavg_sum_layer, kavg_cnt_layer, d_err, rope_inv_freq, planes, plane_stride);
+            static_cast<float*>(kavg_sum_layer), kavg_cnt_layer, d_err, rope_inv_freq, planes, plane_stride);
+    else if (dtype == OOMB_F64)
+        append_kernel<double><<<grid, 128, 0, st>>>(static_cast<const double*>(k), static_cast<const double*>(v), rows,
+                                                    filled_before, P, Hkv, hd, first_page, ns, d_kvslot_layer,
+                                                    static_cast<double*>(kpool), static_cast<double*>(vpool),
+                                                    static_cast<double*>(kavg_sum_layer), kavg_cnt_layer, d_err,
+                                                    nullptr, nullptr, 0);
     else
         append_kernel<float><<<grid, 128, 0, st>>>(static_cast<const float*>(k), static_cast<const float*>(v), rows,
                                                    filled_before, P, Hkv, hd, first_page, ns, d_kvslot_layer,
                                                    static_cast<float*>(kpool), static_cast<float*>(vpool),
-                                                   kavg_sum_layer, kavg_cnt_layer, d_err, rope_inv_freq, nullptr, 0);
+                                                   static_cast<float*>(kavg_sum_layer), kavg_cnt_layer, d_err,
+                                                   rope_inv_freq, nullptr, 0);
     check_launch("append_kernel");
 }
 
@@ -214,22 +271,28 @@ void launch_filter_owned(const int32_t* src_off, const int32_t* src_ids, int m, 
 // ===========================================================================
 // page_mean_keys (paged_kv.hpp:170-183): sum * (1/count), IEEE ops.
 // ===========================================================================
-__global__ void mean_keys_kernel(const float* __restrict__ sum, const int32_t* __restrict__ cnt, int n, int re,
-                                 float* __restrict__ out) {
+template <typename A>
+__global__ void mean_keys_kernel(const A* __restrict__ sum, const int32_t* __restrict__ cnt, int n, int re,
+                                 A* __restrict__ out) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= static_cast<int64_t>(n) * re) return;
     const int p = static_cast<int>(i / re);
-    const float inv = __fdiv_rn(1.0f, static_cast<float>(cnt[p]));
-    out[i] = __fmul_rn(sum[i], inv);
+    const A inv = div_rn(A(1), static_cast<A>(cnt[p]));
+    out[i] = mul_rn(sum[i], inv);
 }
 
-void launch_mean_keys(const float* kavg_sum_layer, const int32_t* kavg_cnt_layer, int n, int row_elems, float* out,
-                      cudaStream_t st) {
+void launch_mean_keys(const void* kavg_sum_layer, const int32_t* kavg_cnt_layer, int n, int row_elems, void* out,
+                      cudaStream_t st, bool f64) {
     if (n <= 0) return;
     ProfScope prof_(PK_OTHER, st);
     const int64_t tot = static_cast<int64_t>(n) * row_elems;
-    mean_keys_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(kavg_sum_layer, kavg_cnt_layer, n,
-                                                                              row_elems, out);
+    const unsigned blocks = static_cast<unsigned>((tot + 255) / 256);
+    if (f64)
+        mean_keys_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(kavg_sum_layer), kavg_cnt_layer, n,
+                                                         row_elems, static_cast<double*>(out));
+    else
+        mean_keys_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(kavg_sum_layer), kavg_cnt_layer, n,
+                                                        row_elems, static_cast<float*>(out));
     check_launch("mean_keys_kernel");
 }
 
@@ -253,16 +316,16 @@ __global__ void gather_kernel(const int32_t* __restrict__ ids, int n, const int3
         const int pid = ids[i];
         const int vs = valid_in_page(filled, pid, P);
         const int slot = slotmap[pid];
-        float kv = 0.f, vv = 0.f;
+        acc_t<TO> kv = 0, vv = 0;
         if (slot < 0) {
             if (!grads) atomicOr(err, DERR_NOT_RESIDENT);
         } else if (s < vs) {
             const size_t src = ((static_cast<size_t>(slot) * Hkv + h) * P + s) * hd + d;
-            kv = to_f(pk[src]);
-            vv = to_f(pv[src]);
+            kv = to_a<acc_t<TO>>(pk[src]);
+            vv = to_a<acc_t<TO>>(pv[src]);
         }
-        ko[idx] = from_f<TO>(kv);
-        vo[idx] = from_f<TO>(vv);
+        ko[idx] = from_a<TO>(kv);
+        vo[idx] = from_a<TO>(vv);
         if (e == 0) valid[static_cast<int64_t>(i) * P + s] = s < vs ? 1 : 0;
     }
 }
@@ -274,7 +337,12 @@ void launch_gather(int dtype, int grads, const int32_t* d_ids, int n, const int3
     ProfScope prof_(PK_GATHER, st);
     const int64_t total = static_cast<int64_t>(n) * P * Hkv * hd;
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 32));
-    if (grads) {
+    if (dtype == OOMB_F64) {  // K/V and gradient pages are both double
+        gather_kernel<double, double><<<blocks, 256, 0, st>>>(d_ids, n, d_slot_layer, static_cast<const double*>(pk),
+                                                              static_cast<const double*>(pv), filled, P, Hkv, hd, grads,
+                                                              static_cast<double*>(k_out), static_cast<double*>(v_out),
+                                                              valid_out, d_err);
+    } else if (grads) {
         gather_kernel<float, float><<<blocks, 256, 0, st>>>(d_ids, n, d_slot_layer, static_cast<const float*>(pk),
                                                             static_cast<const float*>(pv), filled, P, Hkv, hd, 1,
                                                             static_cast<float*>(k_out), static_cast<float*>(v_out),
@@ -298,9 +366,10 @@ void launch_gather(int dtype, int grads, const int32_t* d_ids, int n, const int3
 // offset of a page walks the id list in order, so a page listed twice receives its additions in
 // list order (no atomics: deterministic, the reference's order).
 // ===========================================================================
+template <typename A>
 __global__ void scatter_kernel(const int32_t* __restrict__ ids, int n, const int32_t* __restrict__ gslot,
-                               float* __restrict__ gk, float* __restrict__ gv, const float* __restrict__ dk,
-                               const float* __restrict__ dv, int64_t filled, int P, int Hkv, int hd, int* err) {
+                               A* __restrict__ gk, A* __restrict__ gv, const A* __restrict__ dk,
+                               const A* __restrict__ dv, int64_t filled, int P, int Hkv, int hd, int* err) {
     const int re = Hkv * hd;
     const int64_t per_page = static_cast<int64_t>(P) * re;
     for (int64_t off = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; off < per_page;
@@ -323,21 +392,29 @@ __global__ void scatter_kernel(const int32_t* __restrict__ ids, int n, const int
     }
 }
 
-void launch_scatter(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, float* gk, float* gv,
-                    const float* dk, const float* dv, int64_t filled, int P, int Hkv, int hd, int* d_err,
-                    cudaStream_t st) {
+void launch_scatter(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, void* gk, void* gv,
+                    const void* dk, const void* dv, int64_t filled, int P, int Hkv, int hd, int* d_err,
+                    cudaStream_t st, bool f64) {
     if (n <= 0) return;
     ProfScope prof_(PK_GATHER, st);
     const int64_t per_page = static_cast<int64_t>(P) * Hkv * hd;
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((per_page + 255) / 256, 148 * 32));
-    scatter_kernel<<<blocks, 256, 0, st>>>(d_ids, n, d_gslot_layer, gk, gv, dk, dv, filled, P, Hkv, hd, d_err);
+    if (f64)
+        scatter_kernel<double><<<blocks, 256, 0, st>>>(d_ids, n, d_gslot_layer, static_cast<double*>(gk),
+                                                       static_cast<double*>(gv), static_cast<const double*>(dk),
+                                                       static_cast<const double*>(dv), filled, P, Hkv, hd, d_err);
+    else
+        scatter_kernel<float><<<blocks, 256, 0, st>>>(d_ids, n, d_gslot_layer, static_cast<float*>(gk),
+                                                      static_cast<float*>(gv), static_cast<const float*>(dk),
+                                                      static_cast<const float*>(dv), filled, P, Hkv, hd, d_err);
     check_launch("scatter_kernel");
 }
 
 // dM_i read-back (chunk_trainer.hpp:575-587): dk/dv (reference layout) += grad pages.
+template <typename A>
 __global__ void accumulate_grads_kernel(const int32_t* __restrict__ ids, int n, const int32_t* __restrict__ gslot,
-                                        const float* __restrict__ gk, const float* __restrict__ gv, int64_t filled,
-                                        int P, int Hkv, int hd, float* __restrict__ dk, float* __restrict__ dv) {
+                                        const A* __restrict__ gk, const A* __restrict__ gv, int64_t filled,
+                                        int P, int Hkv, int hd, A* __restrict__ dk, A* __restrict__ dv) {
     const int re = Hkv * hd;
     const int64_t total = static_cast<int64_t>(n) * P * re;
     for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
@@ -390,9 +467,13 @@ __global__ void accumulate_grads_rope_kernel(const int32_t* __restrict__ ids, in
     }
 }
 
-void launch_accumulate_grads(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, const float* gk,
-                             const float* gv, int64_t filled, int P, int Hkv, int hd, float* dk, float* dv,
-                             cudaStream_t st, int64_t rope_pos0, const double* rope_inv_freq) {
+void launch_accumulate_grads(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, const void* gk_v,
+                             const void* gv_v, int64_t filled, int P, int Hkv, int hd, void* dk_v, void* dv_v,
+                             cudaStream_t st, int64_t rope_pos0, const double* rope_inv_freq, bool f64) {
+    const float* gk = static_cast<const float*>(gk_v);
+    const float* gv = static_cast<const float*>(gv_v);
+    float* dk = static_cast<float*>(dk_v);
+    float* dv = static_cast<float*>(dv_v);
     if (n <= 0) return;
     ProfScope prof_(PK_GATHER, st);
     const int64_t total = static_cast<int64_t>(n) * P * Hkv * hd;
@@ -403,39 +484,54 @@ void launch_accumulate_grads(const int32_t* d_ids, int n, const int32_t* d_gslot
         check_launch("accumulate_grads_rope_kernel");
         return;
     }
-    accumulate_grads_kernel<<<blocks, 256, 0, st>>>(d_ids, n, d_gslot_layer, gk, gv, filled, P, Hkv, hd, dk, dv);
+    if (f64)
+        accumulate_grads_kernel<double><<<blocks, 256, 0, st>>>(d_ids, n, d_gslot_layer, static_cast<const double*>(gk_v),
+                                                                static_cast<const double*>(gv_v), filled, P, Hkv, hd,
+                                                                static_cast<double*>(dk_v), static_cast<double*>(dv_v));
+    else
+        accumulate_grads_kernel<float><<<blocks, 256, 0, st>>>(d_ids, n, d_gslot_layer, gk, gv, filled, P, Hkv, hd, dk,
+                                                               dv);
     check_launch("accumulate_grads_kernel");
 }
 
 // Lazy gradient pages: publish slot + zero (paged_kv.hpp:148-153).
 __global__ void grad_init_kernel(const int32_t* __restrict__ pages, const int32_t* __restrict__ slots, int n,
                                  int32_t* __restrict__ gslot, float* __restrict__ gk, float* __restrict__ gv,
-                                 int64_t page_elems) {
+                                 int64_t page_words) {  // page size in 4-byte words (fp64 pages: 2 per element)
     const int i = blockIdx.y;
     if (i >= n) return;
-    const int64_t base = static_cast<int64_t>(slots[i]) * page_elems;
-    float4* pk = reinterpret_cast<float4*>(gk + base);
-    float4* pv = reinterpret_cast<float4*>(gv + base);
+    const int64_t base = static_cast<int64_t>(slots[i]) * page_words;
+    float* pk = gk + base;
+    float* pv = gv + base;
+    const int64_t n4 = (page_words % 4 == 0 && base % 4 == 0) ? page_words / 4 : 0;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < page_elems / 4;
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n4;
          j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        pk[j] = z;
-        pv[j] = z;
+        reinterpret_cast<float4*>(pk)[j] = z;
+        reinterpret_cast<float4*>(pv)[j] = z;
+    }
+    for (int64_t j = 4 * n4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < page_words;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        pk[j] = 0.f;
+        pv[j] = 0.f;
     }
     if (pages != nullptr && blockIdx.x == 0 && threadIdx.x == 0) gslot[pages[i]] = slots[i];
 }
 
-void launch_grad_init(const int32_t* d_pages, const int32_t* d_slots, int n, int32_t* d_gslot_layer, float* gk,
-                      float* gv, int64_t page_elems, cudaStream_t st) {
+void launch_grad_init(const int32_t* d_pages, const int32_t* d_slots, int n, int32_t* d_gslot_layer, void* gk,
+                      void* gv, int64_t page_elems, cudaStream_t st, int elem_bytes) {
     if (n <= 0) return;
     ProfScope prof_(PK_GRAD_INIT, st);
-    dim3 grid(static_cast<unsigned>(std::min<int64_t>((page_elems / 4 + 255) / 256, 16)), n);
-    grad_init_kernel<<<grid, 256, 0, st>>>(d_pages, d_slots, n, d_gslot_layer, gk, gv, page_elems);
+    const int64_t words = page_elems * (elem_bytes / 4);
+    dim3 grid(static_cast<unsigned>(std::min<int64_t>((words / 4 + 255) / 256 + 1, 16)), n);
+    grad_init_kernel<<<grid, 256, 0, st>>>(d_pages, d_slots, n, d_gslot_layer, static_cast<float*>(gk),
+                                           static_cast<float*>(gv), words);
     check_launch("grad_init_kernel");
 }
 
-void launch_zero_slots(const int32_t* d_slots, int n, float* gk, float* gv, int64_t page_elems, cudaStream_t st) {
-    launch_grad_init(nullptr, d_slots, n, nullptr, gk, gv, page_elems, st);
+void launch_zero_slots(const int32_t* d_slots, int n, void* gk, void* gv, int64_t page_elems, cudaStream_t st,
+                       int elem_bytes) {
+    launch_grad_init(nullptr, d_slots, n, nullptr, gk, gv, page_elems, st, elem_bytes);
 }
 
 // ===========================================================================
@@ -446,92 +542,95 @@ void launch_zero_slots(const int32_t* d_slots, int n, float* gk, float* gv, int6
 // Dot products use the reference's sequential order with no FMA contraction.
 // ===========================================================================
 template <typename T>
-__device__ __forceinline__ float dot_seq(const T* __restrict__ q, const float* __restrict__ k, int hd) {
-    float dot = 0.f;
-    for (int j = 0; j < hd; ++j) dot = __fadd_rn(dot, __fmul_rn(to_f(q[j]), k[j]));
+__device__ __forceinline__ acc_t<T> dot_seq(const T* __restrict__ q, const acc_t<T>* __restrict__ k, int hd) {
+    using A = acc_t<T>;
+    A dot = A(0);
+    for (int j = 0; j < hd; ++j) dot = add_rn(dot, mul_rn(to_a<A>(q[j]), k[j]));
     return dot;
 }
 
 template <typename T>
 __global__ void score_stats_kernel(const T* __restrict__ q, int64_t tokens, int Hq, int hd,
-                                   const float* __restrict__ kavg, int64_t n, int Hkv, float scale,
-                                   float2* __restrict__ stats) {
+                                   const acc_t<T>* __restrict__ kavg, int64_t n, int Hkv, acc_t<T> scale,
+                                   Stat<acc_t<T>>* __restrict__ stats) {
+    using A = acc_t<T>;
     const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= tokens * Hq) return;
     const int h = static_cast<int>(row % Hq);
     const int kvh = h / (Hq / Hkv);
     const T* qv = q + row * hd;
-    float mx = -INFINITY;
+    A mx = -INFINITY;
     for (int64_t p = lane; p < n; p += 32) {
-        const float raw = __fmul_rn(dot_seq(qv, kavg + (p * Hkv + kvh) * hd, hd), scale);
-        mx = fmaxf(mx, raw);
+        const A raw = mul_rn(dot_seq(qv, kavg + (p * Hkv + kvh) * hd, hd), scale);
+        mx = max_a(mx, raw);
     }
     mx = warp_max(mx);
-    float sum = 0.f;
+    A sum = A(0);
     for (int64_t p = lane; p < n; p += 32) {
-        const float raw = __fmul_rn(dot_seq(qv, kavg + (p * Hkv + kvh) * hd, hd), scale);
-        sum += expf(raw - mx);
+        const A raw = mul_rn(dot_seq(qv, kavg + (p * Hkv + kvh) * hd, hd), scale);
+        sum += exp_a(raw - mx);
     }
     sum = warp_sum(sum);
-    if (lane == 0) stats[row] = make_float2(mx, __fdiv_rn(1.0f, sum));
+    if (lane == 0) stats[row] = Stat<A>{mx, div_rn(A(1), sum)};
 }
 
 template <typename T>
 __global__ void score_vote_kernel(const T* __restrict__ q, int64_t tokens, int Hq, int hd,
-                                  const float* __restrict__ kavg, int64_t n, int Hkv, int P, float scale,
-                                  const float2* __restrict__ stats, float* __restrict__ vote, int h0, int h1) {
-    extern __shared__ float qs[];  // [hd]
+                                  const acc_t<T>* __restrict__ kavg, int64_t n, int Hkv, int P, acc_t<T> scale,
+                                  const Stat<acc_t<T>>* __restrict__ stats, acc_t<T>* __restrict__ vote, int h0, int h1) {
+    using A = acc_t<T>;
+    extern __shared__ __align__(16) unsigned char qs_raw[];
+    A* qs = reinterpret_cast<A*>(qs_raw);  // [hd]
     const int qp = blockIdx.y;
     const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int group = Hq / Hkv;
-    float acc = 0.f;
+    A acc = A(0);
     const int64_t t0 = static_cast<int64_t>(qp) * P;
     const int64_t t1 = min(tokens, t0 + P);
     for (int64_t t = t0; t < t1; ++t) {
         for (int h = h0; h < h1; ++h) {
             __syncthreads();
-            for (int j = threadIdx.x; j < hd; j += blockDim.x) qs[j] = to_f(q[(t * Hq + h) * hd + j]);
+            for (int j = threadIdx.x; j < hd; j += blockDim.x) qs[j] = to_a<A>(q[(t * Hq + h) * hd + j]);
             __syncthreads();
             if (p < n) {
-                const float* kv = kavg + (p * Hkv + h / group) * hd;
-                float dot = 0.f;
-                for (int j = 0; j < hd; ++j) dot = __fadd_rn(dot, __fmul_rn(qs[j], kv[j]));
-                const float2 st = stats[t * Hq + h];
-                acc = __fadd_rn(acc, __fmul_rn(expf(__fmul_rn(dot, scale) - st.x), st.y));
+                const A* kv = kavg + (p * Hkv + h / group) * hd;
+                A dot = A(0);
+                for (int j = 0; j < hd; ++j) dot = add_rn(dot, mul_rn(qs[j], kv[j]));
+                const Stat<A> st = stats[t * Hq + h];
+                acc = add_rn(acc, mul_rn(exp_a(mul_rn(dot, scale) - st.m), st.il));
             }
         }
     }
     if (p < n) vote[static_cast<int64_t>(qp) * n + p] = acc;
 }
 
-void launch_score_simt(int dtype, const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, int64_t n,
-                       int Hkv, int P, float scale, float* vote, float* stats_scratch, cudaStream_t st,
+void launch_score_simt(int dtype, const void* q, int64_t tokens, int Hq, int hd, const void* k_avg, int64_t n,
+                       int Hkv, int P, float scale, double scale64, void* vote, void* stats_scratch, cudaStream_t st,
                        bool partial_only) {
     ProfScope prof_(PK_SCORE, st);
     const int64_t rows = tokens * Hq;
     const int m = static_cast<int>((tokens + P - 1) / P);
-    float2* stats = reinterpret_cast<float2*>(stats_scratch);
     dim3 g1(static_cast<unsigned>((rows + 7) / 8));
     dim3 g2(static_cast<unsigned>((n + 127) / 128), m);
-    if (dtype == OOMB_BF16) {
-        auto qq = static_cast<const __nv_bfloat16*>(q);
-        score_stats_kernel<<<g1, 256, 0, st>>>(qq, tokens, Hq, hd, k_avg, n, Hkv, scale, stats);
+    auto run = [&](auto tag, auto sc) {
+        using T = decltype(tag);
+        using A = acc_t<T>;
+        auto qq = static_cast<const T*>(q);
+        auto ka = static_cast<const A*>(k_avg);
+        auto stats = static_cast<Stat<A>*>(stats_scratch);
+        auto vo = static_cast<A*>(vote);
+        score_stats_kernel<T><<<g1, 256, 0, st>>>(qq, tokens, Hq, hd, ka, n, Hkv, static_cast<A>(sc), stats);
         check_launch("score_stats_kernel");
         for (int g = 0; g < (partial_only ? Hkv : 1); ++g)
-            score_vote_kernel<<<g2, 128, hd * sizeof(float), st>>>(
-                qq, tokens, Hq, hd, k_avg, n, Hkv, P, scale, stats, vote + (partial_only ? g * m * n : 0),
+            score_vote_kernel<T><<<g2, 128, hd * sizeof(A), st>>>(
+                qq, tokens, Hq, hd, ka, n, Hkv, P, static_cast<A>(sc), stats, vo + (partial_only ? g * m * n : 0),
                 partial_only ? g * (Hq / Hkv) : 0, partial_only ? (g + 1) * (Hq / Hkv) : Hq);
-    } else {
-        auto qq = static_cast<const float*>(q);
-        score_stats_kernel<<<g1, 256, 0, st>>>(qq, tokens, Hq, hd, k_avg, n, Hkv, scale, stats);
-        check_launch("score_stats_kernel");
-        for (int g = 0; g < (partial_only ? Hkv : 1); ++g)
-            score_vote_kernel<<<g2, 128, hd * sizeof(float), st>>>(
-                qq, tokens, Hq, hd, k_avg, n, Hkv, P, scale, stats, vote + (partial_only ? g * m * n : 0),
-                partial_only ? g * (Hq / Hkv) : 0, partial_only ? (g + 1) * (Hq / Hkv) : Hq);
-    }
-    check_launch("score_vote_kernel");
+        check_launch("score_vote_kernel");
+    };
+    if (dtype == OOMB_BF16) run(__nv_bfloat16{}, scale);
+    else if (dtype == OOMB_F64) run(double{}, scale64);
+    else run(float{}, scale);
 }
 
 // ===========================================================================
@@ -545,15 +644,23 @@ __device__ __forceinline__ uint32_t order_key(float f) {
     if (f == 0.f) u = 0u;  // the reference compares doubles: -0 == +0 (tie -> id order)
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
+__device__ __forceinline__ unsigned long long order_key(double f) {  // fp64 pools: 8 radix passes
+    unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(f));
+    if (f == 0.0) u = 0ull;
+    return (u >> 63) ? ~u : (u | (1ull << 63));
+}
 
 constexpr int kTopkThreads = 1024;
 
-__global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restrict__ vote, int m, int n, int k,
+template <typename V>
+__global__ void __launch_bounds__(kTopkThreads) topk_kernel(const V* __restrict__ vote, int m, int n, int k,
                                                             int32_t* __restrict__ off, int32_t* __restrict__ ids) {
+    using K = decltype(order_key(V(0)));
+    constexpr int kPasses = static_cast<int>(sizeof(K));
     using Scan = cub::BlockScan<int, kTopkThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ uint32_t hist[256];
-    __shared__ uint32_t s_prefix, s_mask;
+    __shared__ K s_prefix, s_mask;
     __shared__ int s_remaining;
     const int row = blockIdx.x;
     const int tid = threadIdx.x;
@@ -563,7 +670,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restr
         if (row == m - 1) off[m] = m * kk;
     }
     int32_t* out = ids + static_cast<int64_t>(row) * kk;
-    const float* s = vote + static_cast<int64_t>(row) * n;
+    const V* s = vote + static_cast<int64_t>(row) * n;
     if (kk == n) {
         for (int i = tid; i < n; i += kTopkThreads) out[i] = i;
         return;
@@ -574,14 +681,14 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restr
         s_mask = 0;
         s_remaining = kk;
     }
-    for (int pass = 0; pass < 4; ++pass) {
-        const int shift = 24 - 8 * pass;
+    for (int pass = 0; pass < kPasses; ++pass) {
+        const int shift = 8 * (kPasses - 1 - pass);
         if (tid < 256) hist[tid] = 0;
         __syncthreads();
-        const uint32_t prefix = s_prefix, mask = s_mask;
+        const K prefix = s_prefix, mask = s_mask;
         for (int i = tid; i < n; i += kTopkThreads) {
-            const uint32_t key = order_key(s[i]);
-            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+            const K key = order_key(s[i]);
+            if ((key & mask) == prefix) atomicAdd(&hist[static_cast<uint32_t>(key >> shift) & 255u], 1u);
         }
         __syncthreads();
         if (tid == 0) {
@@ -597,12 +704,12 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restr
                 cum += hist[b];
             }
             s_remaining = rem;
-            s_prefix = prefix | (static_cast<uint32_t>(chosen) << shift);
-            s_mask = mask | (255u << shift);
+            s_prefix = prefix | (static_cast<K>(chosen) << shift);
+            s_mask = mask | (static_cast<K>(255u) << shift);
         }
         __syncthreads();
     }
-    const uint32_t thr = s_prefix;
+    const K thr = s_prefix;
     const int take_eq = s_remaining;  // threshold-equal elements to admit, lowest ids first
     const int ipt = (n + kTopkThreads - 1) / kTopkThreads;
     const int i0 = min(n, tid * ipt), i1 = min(n, i0 + ipt);
@@ -615,7 +722,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restr
     {
         int r = eq_before;
         for (int i = i0; i < i1; ++i) {
-            const uint32_t key = order_key(s[i]);
+            const K key = order_key(s[i]);
             if (key > thr) ++n_sel;
             else if (key == thr) n_sel += (r++ < take_eq);
         }
@@ -624,17 +731,19 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restr
     Scan(scan_tmp).ExclusiveSum(n_sel, pos);
     int r = eq_before;
     for (int i = i0; i < i1; ++i) {
-        const uint32_t key = order_key(s[i]);
+        const K key = order_key(s[i]);
         bool take = key > thr;
         if (key == thr) take = (r++ < take_eq);
         if (take) out[pos++] = i;
     }
 }
 
-void launch_topk(const float* vote, int m, int n, int k, int32_t* sel_off, int32_t* sel_ids, cudaStream_t st) {
+void launch_topk(const void* vote, int m, int n, int k, int32_t* sel_off, int32_t* sel_ids, cudaStream_t st,
+                 bool f64) {
     if (m <= 0) return;
     ProfScope prof_(PK_TOPK, st);
-    topk_kernel<<<m, kTopkThreads, 0, st>>>(vote, m, n, k, sel_off, sel_ids);
+    if (f64) topk_kernel<double><<<m, kTopkThreads, 0, st>>>(static_cast<const double*>(vote), m, n, k, sel_off, sel_ids);
+    else topk_kernel<float><<<m, kTopkThreads, 0, st>>>(static_cast<const float*>(vote), m, n, k, sel_off, sel_ids);
     check_launch("topk_kernel");
 }
 
@@ -668,42 +777,43 @@ __global__ void attn_fwd_simt_kernel(AttnGeom g, const T* __restrict__ q, const 
                                      const int32_t* __restrict__ sel_ids, const int32_t* __restrict__ kvslot,
                                      const T* __restrict__ kpool, const T* __restrict__ vpool,
                                      const T* __restrict__ k_cur, const T* __restrict__ v_cur, T* __restrict__ out,
-                                     float* __restrict__ lse, int* err) {
+                                     acc_t<T>* __restrict__ lse, int* err) {
+    using A = acc_t<T>;
     const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= static_cast<int64_t>(g.C) * g.Hq) return;
     const int t = static_cast<int>(row / g.Hq), h = static_cast<int>(row % g.Hq);
     const int kvh = h / g.group, qp = t / g.P, hd = g.hd;
     const int nd = (hd + 31) / 32;
-    float qv[kMaxLaneElems], acc[kMaxLaneElems];
+    A qv[kMaxLaneElems], acc[kMaxLaneElems];
 #pragma unroll
     for (int i = 0; i < kMaxLaneElems; ++i) {
         const int d = lane + 32 * i;
-        qv[i] = (i < nd && d < hd) ? to_f(q[row * hd + d]) : 0.f;
-        acc[i] = 0.f;
+        qv[i] = (i < nd && d < hd) ? to_a<A>(q[row * hd + d]) : A(0);
+        acc[i] = A(0);
     }
-    float m = -INFINITY, l = 0.f;
+    A m = -INFINITY, l = A(0);
     auto visit = [&](const T* kr, const T* vr) {
-        float part = 0.f;
+        A part = A(0);
 #pragma unroll
         for (int i = 0; i < kMaxLaneElems; ++i) {
             const int d = lane + 32 * i;
-            if (i < nd && d < hd) part += qv[i] * to_f(kr[d]);
+            if (i < nd && d < hd) part += qv[i] * to_a<A>(kr[d]);
         }
-        const float logit = warp_sum(part) * g.scale;
+        const A logit = warp_sum(part) * scale_of<A>(g);
         if (logit > m) {
-            const float corr = (l == 0.f) ? 0.f : expf(m - logit);
+            const A corr = (l == A(0)) ? A(0) : exp_a(m - logit);
 #pragma unroll
             for (int i = 0; i < kMaxLaneElems; ++i) acc[i] *= corr;
             l *= corr;
             m = logit;
         }
-        const float w = expf(logit - m);
+        const A w = exp_a(logit - m);
         l += w;
 #pragma unroll
         for (int i = 0; i < kMaxLaneElems; ++i) {
             const int d = lane + 32 * i;
-            if (i < nd && d < hd) acc[i] += w * to_f(vr[d]);
+            if (i < nd && d < hd) acc[i] += w * to_a<A>(vr[d]);
         }
     };
     for (int idx = sel_off[qp]; idx < sel_off[qp + 1]; ++idx) {
@@ -727,62 +837,63 @@ __global__ void attn_fwd_simt_kernel(AttnGeom g, const T* __restrict__ q, const 
             visit(k_cur + o, v_cur + o);
         }
     }
-    const float inv = l > 0.f ? 1.f / l : 0.f;  // a shard that attended no key: O = 0, lse = -inf
+    const A inv = l > A(0) ? A(1) / l : A(0);  // a shard that attended no key: O = 0, lse = -inf
 #pragma unroll
     for (int i = 0; i < kMaxLaneElems; ++i) {
         const int d = lane + 32 * i;
-        if (i < nd && d < hd) out[row * hd + d] = from_f<T>(acc[i] * inv);
+        if (i < nd && d < hd) out[row * hd + d] = from_a<T>(acc[i] * inv);
     }
-    if (lane == 0) lse[row] = l > 0.f ? m + logf(l) : -INFINITY;
+    if (lane == 0) lse[row] = l > A(0) ? m + log_a(l) : -INFINITY;
 }
 
 template <typename T>
 __global__ void attn_bwd_simt_kernel(AttnGeom g, const T* __restrict__ dout, const T* __restrict__ q,
                                      const int32_t* __restrict__ sel_off, const int32_t* __restrict__ sel_ids,
                                      const int32_t* __restrict__ kvslot, const int32_t* __restrict__ gslot,
-                                     const T* __restrict__ kpool, const T* __restrict__ vpool, float* __restrict__ gk,
-                                     float* __restrict__ gv, const T* __restrict__ k_cur, const T* __restrict__ v_cur,
-                                     const T* __restrict__ o, const float* __restrict__ lse, float* __restrict__ dq,
-                                     float* __restrict__ d_rows, int* err) {
+                                     const T* __restrict__ kpool, const T* __restrict__ vpool, acc_t<T>* __restrict__ gk,
+                                     acc_t<T>* __restrict__ gv, const T* __restrict__ k_cur, const T* __restrict__ v_cur,
+                                     const T* __restrict__ o, const acc_t<T>* __restrict__ lse, acc_t<T>* __restrict__ dq,
+                                     acc_t<T>* __restrict__ d_rows, int* err) {
+    using A = acc_t<T>;
     const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= static_cast<int64_t>(g.C) * g.Hq) return;
     const int t = static_cast<int>(row / g.Hq), h = static_cast<int>(row % g.Hq);
     const int kvh = h / g.group, qp = t / g.P, hd = g.hd;
     const int nd = (hd + 31) / 32;
-    float qv[kMaxLaneElems], dov[kMaxLaneElems], dqa[kMaxLaneElems];
-    float dpart = 0.f;
+    A qv[kMaxLaneElems], dov[kMaxLaneElems], dqa[kMaxLaneElems];
+    A dpart = A(0);
 #pragma unroll
     for (int i = 0; i < kMaxLaneElems; ++i) {
         const int d = lane + 32 * i;
         const bool ok = i < nd && d < hd;
-        qv[i] = ok ? to_f(q[row * hd + d]) : 0.f;
-        dov[i] = ok ? to_f(dout[row * hd + d]) : 0.f;
-        dpart += ok ? dov[i] * to_f(o[row * hd + d]) : 0.f;
-        dqa[i] = 0.f;
+        qv[i] = ok ? to_a<A>(q[row * hd + d]) : A(0);
+        dov[i] = ok ? to_a<A>(dout[row * hd + d]) : A(0);
+        dpart += ok ? dov[i] * to_a<A>(o[row * hd + d]) : A(0);
+        dqa[i] = A(0);
     }
-    const float D = warp_sum(dpart);
+    const A D = warp_sum(dpart);
     if (lane == 0) d_rows[row] = D;
-    const float L = lse[row];
+    const A L = lse[row];
     auto visit = [&](const T* kr, const T* vr) {
-        float p1 = 0.f, p2 = 0.f;
+        A p1 = A(0), p2 = A(0);
 #pragma unroll
         for (int i = 0; i < kMaxLaneElems; ++i) {
             const int d = lane + 32 * i;
             if (i < nd && d < hd) {
-                p1 += qv[i] * to_f(kr[d]);
-                p2 += dov[i] * to_f(vr[d]);
+                p1 += qv[i] * to_a<A>(kr[d]);
+                p2 += dov[i] * to_a<A>(vr[d]);
             }
         }
-        const float dot = warp_sum(p1);
-        const float dpv = warp_sum(p2);
-        const float p = expf(dot * g.scale - L);
-        const float dlogit = p * (dpv - D) * g.scale;
+        const A dot = warp_sum(p1);
+        const A dpv = warp_sum(p2);
+        const A p = exp_a(dot * scale_of<A>(g) - L);
+        const A dlogit = p * (dpv - D) * scale_of<A>(g);
 #pragma unroll
         for (int i = 0; i < kMaxLaneElems; ++i) {
             const int d = lane + 32 * i;
             if (i < nd && d < hd) {
-                dqa[i] += dlogit * to_f(kr[d]);
+                dqa[i] += dlogit * to_a<A>(kr[d]);
             }
         }
     };
@@ -828,10 +939,11 @@ __global__ void attn_bwd_kv_simt_kernel(AttnGeom g, const T* __restrict__ dout, 
                                         const int32_t* __restrict__ sel_off, const int32_t* __restrict__ sel_ids,
                                         const int32_t* __restrict__ kvslot, const int32_t* __restrict__ gslot,
                                         const T* __restrict__ kpool, const T* __restrict__ vpool,
-                                        float* __restrict__ gk, float* __restrict__ gv, const T* __restrict__ k_cur,
-                                        const T* __restrict__ v_cur, const float* __restrict__ lse,
-                                        const float* __restrict__ d_rows, float* __restrict__ dk_cur,
-                                        float* __restrict__ dv_cur, int n_past_pages) {
+                                        acc_t<T>* __restrict__ gk, acc_t<T>* __restrict__ gv, const T* __restrict__ k_cur,
+                                        const T* __restrict__ v_cur, const acc_t<T>* __restrict__ lse,
+                                        const acc_t<T>* __restrict__ d_rows, acc_t<T>* __restrict__ dk_cur,
+                                        acc_t<T>* __restrict__ dv_cur, int n_past_pages) {
+    using A = acc_t<T>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int kvh = blockIdx.y, hd = g.hd, nd = (hd + 31) / 32;
     const bool past = static_cast<int>(blockIdx.x) < n_past_pages;
@@ -850,8 +962,8 @@ __global__ void attn_bwd_kv_simt_kernel(AttnGeom g, const T* __restrict__ dout, 
     for (int s = static_cast<int>(blockIdx.z) * nw + warp; s < n_keys; s += nw * static_cast<int>(gridDim.z)) {
         const T* kr;
         const T* vr;
-        float* dkr;
-        float* dvr;
+        A* dkr;
+        A* dvr;
         int key_t = 0;  // chunk keys: the key's row
         if (past) {
             const size_t off = ((static_cast<size_t>(slot) * g.Hkv + kvh) * g.P + s) * hd;
@@ -868,33 +980,33 @@ __global__ void attn_bwd_kv_simt_kernel(AttnGeom g, const T* __restrict__ dout, 
             dkr = dk_cur + off;
             dvr = dv_cur + off;
         }
-        float kv[kMaxLaneElems], vv[kMaxLaneElems], ak[kMaxLaneElems], av[kMaxLaneElems];
+        A kv[kMaxLaneElems], vv[kMaxLaneElems], ak[kMaxLaneElems], av[kMaxLaneElems];
 #pragma unroll
         for (int i = 0; i < kMaxLaneElems; ++i) {
             const int d = lane + 32 * i;
             const bool ok = i < nd && d < hd;
-            kv[i] = ok ? to_f(kr[d]) : 0.f;
-            vv[i] = ok ? to_f(vr[d]) : 0.f;
-            ak[i] = av[i] = 0.f;
+            kv[i] = ok ? to_a<A>(kr[d]) : A(0);
+            vv[i] = ok ? to_a<A>(vr[d]) : A(0);
+            ak[i] = av[i] = A(0);
         }
         auto rows = [&](int t0, int t1) {  // rows t0..t1-1, the group's heads: accumulate in order
             for (int t = t0; t < t1; ++t)
                 for (int j = 0; j < g.group; ++j) {
                     const int64_t row = static_cast<int64_t>(t) * g.Hq + kvh * g.group + j;
-                    float p1 = 0.f, p2 = 0.f, qv[kMaxLaneElems], dv2[kMaxLaneElems];
+                    A p1 = A(0), p2 = A(0), qv[kMaxLaneElems], dv2[kMaxLaneElems];
 #pragma unroll
                     for (int i = 0; i < kMaxLaneElems; ++i) {
                         const int d = lane + 32 * i;
                         const bool ok = i < nd && d < hd;
-                        qv[i] = ok ? to_f(q[row * hd + d]) : 0.f;
-                        dv2[i] = ok ? to_f(dout[row * hd + d]) : 0.f;
+                        qv[i] = ok ? to_a<A>(q[row * hd + d]) : A(0);
+                        dv2[i] = ok ? to_a<A>(dout[row * hd + d]) : A(0);
                         p1 += qv[i] * kv[i];
                         p2 += dv2[i] * vv[i];
                     }
-                    const float dot = warp_sum(p1);
-                    const float dpv = warp_sum(p2);
-                    const float p = expf(dot * g.scale - lse[row]);
-                    const float dlogit = p * (dpv - d_rows[row]) * g.scale;
+                    const A dot = warp_sum(p1);
+                    const A dpv = warp_sum(p2);
+                    const A p = exp_a(dot * scale_of<A>(g) - lse[row]);
+                    const A dlogit = p * (dpv - d_rows[row]) * scale_of<A>(g);
 #pragma unroll
                     for (int i = 0; i < kMaxLaneElems; ++i) {
                         ak[i] += dlogit * qv[i];
@@ -915,7 +1027,7 @@ __global__ void attn_bwd_kv_simt_kernel(AttnGeom g, const T* __restrict__ dout, 
                         dkr[d] += ak[i];
                         dvr[d] += av[i];
                     }
-                    ak[i] = av[i] = 0.f;
+                    ak[i] = av[i] = A(0);
                 }
             }
         } else {
@@ -934,52 +1046,53 @@ __global__ void attn_bwd_kv_simt_kernel(AttnGeom g, const T* __restrict__ dout, 
 
 void launch_attn_fwd_simt(int dtype, const AttnGeom& g, const void* q, const int32_t* sel_off, const int32_t* sel_ids,
                           const int32_t* d_kvslot_layer, const void* kpool, const void* vpool, const void* k_cur,
-                          const void* v_cur, void* out, float* lse, int* d_err, cudaStream_t st) {
+                          const void* v_cur, void* out, void* lse, int* d_err, cudaStream_t st) {
     ProfScope prof_(PK_FWD, st);
     const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
     const unsigned blocks = static_cast<unsigned>((rows + 3) / 4);
-    if (dtype == OOMB_BF16) {
-        using T = __nv_bfloat16;
+    auto run = [&](auto tag) {
+        using T = decltype(tag);
         attn_fwd_simt_kernel<T><<<blocks, 128, 0, st>>>(g, static_cast<const T*>(q), sel_off, sel_ids, d_kvslot_layer,
                                                         static_cast<const T*>(kpool), static_cast<const T*>(vpool),
                                                         static_cast<const T*>(k_cur), static_cast<const T*>(v_cur),
-                                                        static_cast<T*>(out), lse, d_err);
-    } else {
-        using T = float;
-        attn_fwd_simt_kernel<T><<<blocks, 128, 0, st>>>(g, static_cast<const T*>(q), sel_off, sel_ids, d_kvslot_layer,
-                                                        static_cast<const T*>(kpool), static_cast<const T*>(vpool),
-                                                        static_cast<const T*>(k_cur), static_cast<const T*>(v_cur),
-                                                        static_cast<T*>(out), lse, d_err);
-    }
+                                                        static_cast<T*>(out), static_cast<acc_t<T>*>(lse), d_err);
+    };
+    if (dtype == OOMB_BF16) run(__nv_bfloat16{});
+    else if (dtype == OOMB_F64) run(double{});
+    else run(float{});
     check_launch("attn_fwd_simt_kernel");
 }
 
 void launch_attn_bwd_simt(int dtype, const AttnGeom& g, const void* dout, const void* q, const int32_t* sel_off,
                           const int32_t* sel_ids, const int32_t* d_kvslot_layer, const int32_t* d_gslot_layer,
-                          const void* kpool, const void* vpool, float* gkpool, float* gvpool, const void* k_cur,
-                          const void* v_cur, const void* out, const float* lse, float* dq, float* dk_cur,
-                          float* dv_cur, int* d_err, cudaStream_t st, int n_past_pages) {
+                          const void* kpool, const void* vpool, void* gkpool, void* gvpool, const void* k_cur,
+                          const void* v_cur, const void* out, const void* lse, void* dq, void* dk_cur,
+                          void* dv_cur, int* d_err, cudaStream_t st, int n_past_pages) {
     ProfScope prof_(PK_BWD_SIMT, st);
     const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
     const unsigned blocks = static_cast<unsigned>((rows + 3) / 4);
-    float* d_rows = nullptr;
-    OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_rows), std::max<int64_t>(rows, 1) * sizeof(float), st));
+    void* d_rows = nullptr;
+    OOMB_CUDA(cudaMallocAsync(&d_rows, std::max<int64_t>(rows, 1) * sizeof(double), st));
     const dim3 kv_grid(static_cast<unsigned>(n_past_pages + (g.C + g.P - 1) / g.P), g.Hkv,
                        static_cast<unsigned>((g.P + 3) / 4));
     auto run = [&](auto zero) {
         using T = decltype(zero);
+        using A = acc_t<T>;
         attn_bwd_simt_kernel<T><<<blocks, 128, 0, st>>>(
             g, static_cast<const T*>(dout), static_cast<const T*>(q), sel_off, sel_ids, d_kvslot_layer, d_gslot_layer,
-            static_cast<const T*>(kpool), static_cast<const T*>(vpool), gkpool, gvpool, static_cast<const T*>(k_cur),
-            static_cast<const T*>(v_cur), static_cast<const T*>(out), lse, dq, d_rows, d_err);
+            static_cast<const T*>(kpool), static_cast<const T*>(vpool), static_cast<A*>(gkpool), static_cast<A*>(gvpool),
+            static_cast<const T*>(k_cur), static_cast<const T*>(v_cur), static_cast<const T*>(out),
+            static_cast<const A*>(lse), static_cast<A*>(dq), static_cast<A*>(d_rows), d_err);
         check_launch("attn_bwd_simt_kernel");
         attn_bwd_kv_simt_kernel<T><<<kv_grid, 128, 0, st>>>(
             g, static_cast<const T*>(dout), static_cast<const T*>(q), sel_off, sel_ids, d_kvslot_layer, d_gslot_layer,
-            static_cast<const T*>(kpool), static_cast<const T*>(vpool), gkpool, gvpool, static_cast<const T*>(k_cur),
-            static_cast<const T*>(v_cur), lse, d_rows, dk_cur, dv_cur, n_past_pages);
+            static_cast<const T*>(kpool), static_cast<const T*>(vpool), static_cast<A*>(gkpool), static_cast<A*>(gvpool),
+            static_cast<const T*>(k_cur), static_cast<const T*>(v_cur), static_cast<const A*>(lse),
+            static_cast<const A*>(d_rows), static_cast<A*>(dk_cur), static_cast<A*>(dv_cur), n_past_pages);
         check_launch("attn_bwd_kv_simt_kernel");
     };
     if (dtype == OOMB_BF16) run(__nv_bfloat16{});
+    else if (dtype == OOMB_F64) run(double{});
     else run(float{});
     OOMB_CUDA(cudaFreeAsync(d_rows, st));
 }

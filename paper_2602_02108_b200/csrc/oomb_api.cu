@@ -131,7 +131,7 @@ void validate_cfg(const oomb_config& c) {  // ModelConfig::validate (config.cpp:
     req(c.retrieval_budget >= 0, "retrieval_budget must be >= 0");
     req(c.retrieval_budget % c.page_size == 0, "retrieval_budget must be divisible by page_size");
     req(c.local_window >= 0, "local_window must be >= 0");
-    req(c.dtype == OOMB_F32 || c.dtype == OOMB_BF16, "dtype must be OOMB_F32 or OOMB_BF16");
+    req(c.dtype == OOMB_F32 || c.dtype == OOMB_BF16 || c.dtype == OOMB_F64, "dtype must be OOMB_F32, OOMB_BF16 or OOMB_F64");
     req(c.head_dim <= 256, "head_dim must be <= 256");
     req(c.max_tokens >= 1, "max_tokens must be >= 1");
 }
@@ -164,6 +164,7 @@ AttnGeom geom(oomb_pool_s* p, int64_t tokens, int layer) {
     g.m = static_cast<int>((tokens + g.P - 1) / g.P);
     g.filled = p->pt->filled[layer];
     g.scale = 1.0f / std::sqrt(static_cast<float>(g.hd));
+    g.scale64 = 1.0 / std::sqrt(static_cast<double>(g.hd));
     g.max_pages = static_cast<int>(p->max_pages);
     g.chunk_keys = 1;
     return g;
@@ -202,7 +203,7 @@ void ensure_grad_pages(oomb_pool_s* p, int layer, const int32_t* h_off, const in
     std::vector<int32_t> both(pages);
     both.insert(both.end(), slots.begin(), slots.end());
     OOMB_CUDA(cudaMemcpyAsync(d, both.data(), 2 * n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    launch_grad_init(d, d + n, n, p->gslot_layer(layer), p->gkpool, p->gvpool, p->page_elems, st);
+    launch_grad_init(d, d + n, n, p->gslot_layer(layer), p->gkpool, p->gvpool, p->page_elems, st, p->aelem);
     OOMB_CUDA(cudaFreeAsync(d, st));
 }
 
@@ -305,9 +306,12 @@ int oomb_pool_create(const oomb_config* cfg, int device, oomb_pool_t* out) {
             }
             const auto& c = p->cfg;
             p->max_pages = (c.max_tokens + c.page_size - 1) / c.page_size;
-            p->elem = c.dtype == OOMB_BF16 ? 2 : 4;
+            OOMB_REQUIRE(c.dtype == OOMB_F32 || c.dtype == OOMB_BF16 || c.dtype == OOMB_F64, OOMB_CONFIG_ERROR,
+                         "dtype must be OOMB_F32, OOMB_BF16 or OOMB_F64");
+            p->elem = c.dtype == OOMB_BF16 ? 2 : c.dtype == OOMB_F64 ? 8 : 4;
+            p->aelem = c.dtype == OOMB_F64 ? 8 : 4;
             p->page_elems = static_cast<int64_t>(c.page_size) * c.n_kv_heads * c.head_dim;
-            p->pt = new PageTable(c.n_layers, c.page_size, c.n_kv_heads, c.head_dim, p->elem, 4);
+            p->pt = new PageTable(c.n_layers, c.page_size, c.n_kv_heads, c.head_dim, p->elem, p->aelem);
             OOMB_REQUIRE(c.page_owner_stride >= 0 && (c.page_owner_stride <= 1 ||
                                                      (c.page_owner_rank >= 0 && c.page_owner_rank < c.page_owner_stride)),
                          OOMB_CONFIG_ERROR, "page_owner_rank must be in [0, page_owner_stride)");
@@ -322,7 +326,7 @@ int oomb_pool_create(const oomb_config* cfg, int device, oomb_pool_t* out) {
             p->kvslot.assign(c.n_layers, std::vector<int32_t>(p->max_pages, -1));
             p->gslot.assign(c.n_layers, std::vector<int32_t>(p->max_pages, -1));
             const size_t kv_bytes = static_cast<size_t>(p->n_kv_slots) * p->page_elems * p->elem;
-            const size_t g_bytes = static_cast<size_t>(p->n_g_slots) * p->page_elems * sizeof(float);
+            const size_t g_bytes = static_cast<size_t>(p->n_g_slots) * p->page_elems * p->aelem;
             OOMB_CUDA(cudaMalloc(&p->kpool, kv_bytes));
             OOMB_CUDA(cudaMalloc(&p->vpool, kv_bytes));
             OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->gkpool), g_bytes));
@@ -333,9 +337,9 @@ int oomb_pool_create(const oomb_config* cfg, int device, oomb_pool_t* out) {
             OOMB_CUDA(cudaMemset(p->d_kvslot, 0xFF, tab));
             OOMB_CUDA(cudaMemset(p->d_gslot, 0xFF, tab));
             const size_t ks = static_cast<size_t>(c.n_layers) * p->max_pages * c.n_kv_heads * c.head_dim;
-            OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->d_kavg_sum), ks * sizeof(float)));
+            OOMB_CUDA(cudaMalloc(&p->d_kavg_sum, ks * p->aelem));
             OOMB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p->d_kavg_cnt), tab));
-            OOMB_CUDA(cudaMemset(p->d_kavg_sum, 0, ks * sizeof(float)));
+            OOMB_CUDA(cudaMemset(p->d_kavg_sum, 0, ks * p->aelem));
             OOMB_CUDA(cudaMemset(p->d_kavg_cnt, 0, tab));
             if (c.dtype == OOMB_BF16 && c.head_dim == 128 && c.page_size % 128 == 0) {  // the tcgen05 scorer's shape
                 p->plane_stride = (p->max_pages + 127) / 128 * 128;
@@ -419,7 +423,7 @@ int oomb_zero_grad_pages(oomb_pool_t p, void* stream) {
                 if (p->gslot[l][pg] >= 0) slots.push_back(p->gslot[l][pg]);
         if (slots.empty()) return;
         int32_t* d = upload_ids(slots.data(), static_cast<int>(slots.size()), S(stream));
-        launch_zero_slots(d, static_cast<int>(slots.size()), p->gkpool, p->gvpool, p->page_elems, S(stream));
+        launch_zero_slots(d, static_cast<int>(slots.size()), p->gkpool, p->gvpool, p->page_elems, S(stream), p->aelem);
         OOMB_CUDA(cudaFreeAsync(d, S(stream)));
     });
 }
@@ -524,6 +528,7 @@ int oomb_append_chunk_rope(oomb_pool_t p, int layer, const void* k_raw, const vo
                            void* stream, int64_t* slot_begin, int64_t* slot_end) {
     const int rc = guard([&] {
         OOMB_REQUIRE(rope_base > 0.f, OOMB_CONFIG_ERROR, "append_chunk_rope: rope base must be positive");
+        OOMB_REQUIRE(p->cfg.dtype != OOMB_F64, OOMB_CONFIG_ERROR, "append_chunk_rope: fp32 / bf16 pools");
     });
     if (rc != OOMB_OK) return rc;
     return append_impl(p, layer, k_raw, v, rows, stream, slot_begin, slot_end, rope_base);
@@ -534,6 +539,7 @@ int oomb_rope(const void* x, int64_t rows, int heads, int hd, int64_t pos_offset
         OOMB_REQUIRE(rows >= 0 && heads >= 1 && hd >= 2 && hd % 2 == 0, OOMB_SHAPE_ERROR,
                      "rope: head dimension must be even");  // ops.hpp:194-196
         OOMB_REQUIRE(base > 0.f && (sign == 1 || sign == -1), OOMB_CONFIG_ERROR, "rope: base > 0, sign +-1");
+        OOMB_REQUIRE(in_dtype != OOMB_F64 && out_dtype != OOMB_F64, OOMB_CONFIG_ERROR, "rope: fp32 / bf16");
         launch_rope(in_dtype, out_dtype, x, rows, heads, hd, pos_offset, sign, rope_inv_freq_table(base, hd), out,
                     S(stream));
     });
@@ -572,25 +578,25 @@ int oomb_device_slots_get(oomb_pool_t p, int layer, int32_t* out) {
         }
     });
 }
-int oomb_page_mean_keys(oomb_pool_t p, int layer, int n_candidates, float* out, void* stream, int* n_out) {
+int oomb_page_mean_keys(oomb_pool_t p, int layer, int n_candidates, void* out, void* stream, int* n_out) {
     return guard([&] {
         set_dev(p);
         p->pt->check_layer(layer);
         const int np = static_cast<int>(p->pt->pages[layer].size());
         const int n = n_candidates < 0 ? np : std::min(n_candidates, np);
         launch_mean_keys(p->kavg_sum_layer(layer), p->kavg_cnt_layer(layer), n, p->cfg.n_kv_heads * p->cfg.head_dim,
-                         out, S(stream));
+                         out, S(stream), p->f64());
         *n_out = n;
     });
 }
-int oomb_kavg_raw(oomb_pool_t p, int layer, float* sum_out, int32_t* count_out, void* stream) {
+int oomb_kavg_raw(oomb_pool_t p, int layer, void* sum_out, int32_t* count_out, void* stream) {
     return guard([&] {
         set_dev(p);
         p->pt->check_layer(layer);
         const int64_t np = static_cast<int64_t>(p->pt->pages[layer].size());
         const int64_t re = static_cast<int64_t>(p->cfg.n_kv_heads) * p->cfg.head_dim;
         if (np == 0) return;
-        OOMB_CUDA(cudaMemcpyAsync(sum_out, p->kavg_sum_layer(layer), np * re * sizeof(float),
+        OOMB_CUDA(cudaMemcpyAsync(sum_out, p->kavg_sum_layer(layer), np * re * p->aelem,
                                   cudaMemcpyDeviceToDevice, S(stream)));
         OOMB_CUDA(cudaMemcpyAsync(count_out, p->kavg_cnt_layer(layer), np * sizeof(int32_t), cudaMemcpyDeviceToDevice,
                                   S(stream)));
@@ -611,7 +617,7 @@ int oomb_gather_pages(oomb_pool_t p, int layer, const int32_t* ids, int n, int g
         OOMB_CUDA(cudaFreeAsync(d, S(stream)));
     });
 }
-int oomb_scatter_add_grads(oomb_pool_t p, int layer, const int32_t* ids, int n, const float* dk, const float* dv,
+int oomb_scatter_add_grads(oomb_pool_t p, int layer, const int32_t* ids, int n, const void* dk, const void* dv,
                            void* stream) {
     return guard([&] {
         set_dev(p);
@@ -621,7 +627,7 @@ int oomb_scatter_add_grads(oomb_pool_t p, int layer, const int32_t* ids, int n, 
         ensure_grad_pages(p, layer, off, ids, 1, S(stream));
         int32_t* d = upload_ids(ids, n, S(stream));
         launch_scatter(d, n, p->gslot_layer(layer), p->gkpool, p->gvpool, dk, dv, p->pt->filled[layer],
-                       p->cfg.page_size, p->cfg.n_kv_heads, p->cfg.head_dim, p->d_err, S(stream));
+                       p->cfg.page_size, p->cfg.n_kv_heads, p->cfg.head_dim, p->d_err, S(stream), p->f64());
         OOMB_CUDA(cudaFreeAsync(d, S(stream)));
     });
 }
@@ -751,13 +757,13 @@ int oomb_select_recent(oomb_selection_t s, int n_pages, int window, int m, void*
         select_range(s, n_pages - take, take, m, S(stream));
     });
 }
-static void select_topk_impl(oomb_selection_t s, const float* vote, int m, int n, int k, cudaStream_t st) {
+static void select_topk_impl(oomb_selection_t s, const void* vote, int m, int n, int k, cudaStream_t st) {
     OOMB_REQUIRE(k >= 0, OOMB_SHAPE_ERROR, "select_topk: negative budget");  // attention.hpp:73
     OOMB_REQUIRE(m >= 0 && m <= s->max_m, OOMB_SHAPE_ERROR, "selection: too many query pages");
     const int kk = std::min(k, n);
     OOMB_REQUIRE(static_cast<int64_t>(m) * kk <= s->max_ids, OOMB_SHAPE_ERROR, "selection: too many ids");
     OOMB_CUDA(cudaEventSynchronize(s->ev));
-    launch_topk(vote, m, n, k, s->d_off, s->d_ids, st);
+    launch_topk(vote, m, n, k, s->d_off, s->d_ids, st, s->pool->f64());
     OOMB_CUDA(cudaMemcpyAsync(s->h_off, s->d_off, (m + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     if (m * kk)
         OOMB_CUDA(cudaMemcpyAsync(s->h_ids, s->d_ids, static_cast<size_t>(m) * kk * sizeof(int32_t),
@@ -799,7 +805,7 @@ int oomb_page_owner(oomb_pool_t p, int* stride, int* rank) {
     });
 }
 
-int oomb_select_topk(oomb_selection_t s, const float* vote, int m, int n, int k, void* stream) {
+int oomb_select_topk(oomb_selection_t s, const void* vote, int m, int n, int k, void* stream) {
     return guard([&] {
         set_dev(s->pool);
         select_topk_impl(s, vote, m, n, k, S(stream));
@@ -812,46 +818,50 @@ int oomb_select_topk(oomb_selection_t s, const float* vote, int m, int n, int k,
 // score_pages on fp32 representatives (k_avg [n][Hkv][hd]) or, when kavg_sum/kavg_cnt are given,
 // on the pool's K_avg sums (mean formed on the fly, paged_kv.hpp:170-183). bf16 + hd 128 +
 // 128-aligned chunks use the tcgen05 scorer; everything else the exact SIMT scorer.
-static void score_impl(const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, const float* kavg_sum,
+static void score_impl(const void* q, int64_t tokens, int Hq, int hd, const void* k_avg, const void* kavg_sum,
                        const int32_t* kavg_cnt, int64_t n, int Hkv, int P, int score_scale, int dtype, bool allow_tc,
-                       float* vote, cudaStream_t st, bool partial_only = false, const void* planes = nullptr,
+                       void* vote, cudaStream_t st, bool partial_only = false, const void* planes = nullptr,
                        int64_t plane_stride = 0) {
     OOMB_REQUIRE(n >= 1, OOMB_SHAPE_ERROR, "score_pages: needs at least one candidate page");
     OOMB_REQUIRE(Hq >= 1 && Hkv >= 1 && Hq % Hkv == 0 && hd >= 1 && hd <= 256 && P >= 1, OOMB_SHAPE_ERROR,
                  "score_pages: bad shape");
     const float scale = score_scale ? 1.0f / std::sqrt(static_cast<float>(hd)) : 1.0f;
+    const double scale64 = score_scale ? 1.0 / std::sqrt(static_cast<double>(hd)) : 1.0;
+    const bool f64 = dtype == OOMB_F64;
+    const size_t ae = f64 ? 8 : 4;
     if (allow_tc && score_tc_supported(dtype, hd, P, tokens)) {
         void* ws = nullptr;
         OOMB_CUDA(cudaMallocAsync(&ws, score_tc_workspace(tokens, Hq, Hkv, n, P), st));
-        launch_score_tc(q, tokens, Hq, Hkv, P, kavg_sum, kavg_cnt, k_avg, n, scale, vote, ws, st, partial_only, planes,
-                        plane_stride);
+        launch_score_tc(q, tokens, Hq, Hkv, P, static_cast<const float*>(kavg_sum), kavg_cnt,
+                        static_cast<const float*>(k_avg), n, scale, static_cast<float*>(vote), ws, st, partial_only,
+                        planes, plane_stride);
         OOMB_CUDA(cudaFreeAsync(ws, st));
         return;
     }
-    float* kavg = const_cast<float*>(k_avg);
+    void* kavg = const_cast<void*>(k_avg);
     if (!kavg) {
-        OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&kavg), n * Hkv * hd * sizeof(float), st));
-        launch_mean_keys(kavg_sum, kavg_cnt, static_cast<int>(n), Hkv * hd, kavg, st);
+        OOMB_CUDA(cudaMallocAsync(&kavg, n * Hkv * hd * ae, st));
+        launch_mean_keys(kavg_sum, kavg_cnt, static_cast<int>(n), Hkv * hd, kavg, st, f64);
     }
-    float* stats = nullptr;
-    OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&stats), std::max<int64_t>(tokens * Hq, 1) * 8, st));
-    launch_score_simt(dtype, q, tokens, Hq, hd, kavg, n, Hkv, P, scale, vote, stats, st, partial_only);
+    void* stats = nullptr;
+    OOMB_CUDA(cudaMallocAsync(&stats, std::max<int64_t>(tokens * Hq, 1) * 2 * ae, st));
+    launch_score_simt(dtype, q, tokens, Hq, hd, kavg, n, Hkv, P, scale, scale64, vote, stats, st, partial_only);
     OOMB_CUDA(cudaFreeAsync(stats, st));
     if (!k_avg) OOMB_CUDA(cudaFreeAsync(kavg, st));
 }
 
-int oomb_score_pages(const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, int64_t n, int Hkv,
-                     int page_size, int score_scale, int dtype, float* vote, void* stream) {
+int oomb_score_pages(const void* q, int64_t tokens, int Hq, int hd, const void* k_avg, int64_t n, int Hkv,
+                     int page_size, int score_scale, int dtype, void* vote, void* stream) {
     return guard([&] {
         score_impl(q, tokens, Hq, hd, k_avg, nullptr, nullptr, n, Hkv, page_size, score_scale, dtype, true, vote,
                    S(stream));
     });
 }
 
-static void select_topk_impl(oomb_selection_t s, const float* vote, int m, int n, int k, cudaStream_t st);
+static void select_topk_impl(oomb_selection_t s, const void* vote, int m, int n, int k, cudaStream_t st);
 
 int oomb_score_pages_partial(oomb_pool_t p, int layer, const void* q, int64_t tokens, int n_candidates,
-                             float* partials, void* stream) {
+                             void* partials, void* stream) {
     return guard([&] {
         set_dev(p);
         p->pt->check_layer(layer);
@@ -881,7 +891,7 @@ int oomb_vote_reduce(const float* partials, int groups, int64_t m, int64_t n, fl
 }
 
 int oomb_select_pages_topk(oomb_pool_t p, int layer, const void* q, int64_t tokens, int n_candidates,
-                           oomb_selection_t sel, float* vote_scratch, void* stream) {
+                           oomb_selection_t sel, void* vote_scratch, void* stream) {
     return guard([&] {
         set_dev(p);
         p->pt->check_layer(layer);
@@ -904,7 +914,7 @@ int oomb_select_pages_topk(oomb_pool_t p, int layer, const void* q, int64_t toke
 // attention
 // ---------------------------------------------------------------------------
 int oomb_attn_forward_ex(oomb_pool_t p, int layer, const void* q, int64_t tokens, oomb_selection_t sel,
-                         const void* k_cur, const void* v_cur, void* out, float* lse, int flags, void* stream) {
+                         const void* k_cur, const void* v_cur, void* out, void* lse, int flags, void* stream) {
     return guard([&] {
         set_dev(p);
         p->pt->check_layer(layer);
@@ -920,8 +930,8 @@ int oomb_attn_forward_ex(oomb_pool_t p, int layer, const void* q, int64_t tokens
                                  "gather_pages");
         }
         if (use_tc(p, g))
-            launch_attn_fwd_tc(g, p->maps, q, sel->d_off, sel->d_ids, p->kvslot_layer(layer), k_cur, v_cur, out, lse,
-                               p->d_err, S(stream));
+            launch_attn_fwd_tc(g, p->maps, q, sel->d_off, sel->d_ids, p->kvslot_layer(layer), k_cur, v_cur, out,
+                               static_cast<float*>(lse), p->d_err, S(stream));
         else
             launch_attn_fwd_simt(p->cfg.dtype, g, q, sel->d_off, sel->d_ids, p->kvslot_layer(layer), p->kpool, p->vpool,
                                  k_cur, v_cur, out, lse, p->d_err, S(stream));
@@ -929,13 +939,13 @@ int oomb_attn_forward_ex(oomb_pool_t p, int layer, const void* q, int64_t tokens
 }
 
 int oomb_attn_forward(oomb_pool_t p, int layer, const void* q, int64_t tokens, oomb_selection_t sel,
-                      const void* k_cur, const void* v_cur, void* out, float* lse, void* stream) {
+                      const void* k_cur, const void* v_cur, void* out, void* lse, void* stream) {
     return oomb_attn_forward_ex(p, layer, q, tokens, sel, k_cur, v_cur, out, lse, 0, stream);
 }
 
 int oomb_attn_backward_ex(oomb_pool_t p, int layer, const void* dout, const void* q, int64_t tokens,
-                       oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out, const float* lse,
-                       float* dq, float* dk_cur, float* dv_cur, int flags, void* stream) {
+                       oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out, const void* lse,
+                       void* dq, void* dk_cur, void* dv_cur, int flags, void* stream) {
     return guard([&] {
         set_dev(p);
         p->pt->check_layer(layer);
@@ -948,7 +958,7 @@ int oomb_attn_backward_ex(oomb_pool_t p, int layer, const void* dout, const void
             p->pt->check_ids(layer, sel->h_ids + sel->h_off[qp], sel->h_off[qp + 1] - sel->h_off[qp], p->enforce,
                              "attn_backward");
         ensure_grad_pages(p, layer, sel->h_off, sel->h_ids, g.m, S(stream));
-        const size_t kvb = static_cast<size_t>(tokens) * g.Hkv * g.hd * sizeof(float);
+        const size_t kvb = static_cast<size_t>(tokens) * g.Hkv * g.hd * p->aelem;
         const bool tc = p->policy != 1 && p->maps.valid && tc_supported(g, p->cfg.dtype) && tc_bwd_available();
         if (tc) {
             if (!p->bwd_side) {
@@ -970,8 +980,9 @@ int oomb_attn_backward_ex(oomb_pool_t p, int layer, const void* dout, const void
             // the dQ that last used this workspace has finished reading it
             if (p->bwd_ws_used[b]) OOMB_CUDA(cudaStreamWaitEvent(S(stream), p->bwd_ev_dq[b], 0));
             launch_attn_bwd_tc(g, p->maps, dout, q, sel->d_off, sel->d_ids, p->kvslot_layer(layer),
-                               p->gslot_layer(layer), p->gkpool, p->gvpool, k_cur, v_cur, out, lse, dq, dk_cur,
-                               dv_cur, p->d_err, p->bwd_ws[b], p->bwd_ws_bytes[b], sel->nnz,
+                               p->gslot_layer(layer), p->gkpool, p->gvpool, k_cur, v_cur, out,
+                               static_cast<const float*>(lse), static_cast<float*>(dq), static_cast<float*>(dk_cur),
+                               static_cast<float*>(dv_cur), p->d_err, p->bwd_ws[b], p->bwd_ws_bytes[b], sel->nnz,
                                static_cast<int>(p->pt->pages[layer].size()), S(stream), p->bwd_side,
                                p->bwd_ev_prep, p->bwd_ev_dq[b], !defer);
             p->bwd_ws_used[b] = true;
@@ -988,8 +999,8 @@ int oomb_attn_backward_ex(oomb_pool_t p, int layer, const void* dout, const void
 }
 
 int oomb_attn_backward(oomb_pool_t p, int layer, const void* dout, const void* q, int64_t tokens,
-                       oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out, const float* lse,
-                       float* dq, float* dk_cur, float* dv_cur, void* stream) {
+                       oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out, const void* lse,
+                       void* dq, void* dk_cur, void* dv_cur, void* stream) {
     return oomb_attn_backward_ex(p, layer, dout, q, tokens, sel, k_cur, v_cur, out, lse, dq, dk_cur, dv_cur, 0, stream);
 }
 
@@ -1000,7 +1011,7 @@ int oomb_attn_join_dq(oomb_pool_t p, void* stream) {
     });
 }
 
-int oomb_accumulate_grad_pages(oomb_pool_t p, int layer, const int32_t* ids, int n, float* dk, float* dv,
+int oomb_accumulate_grad_pages(oomb_pool_t p, int layer, const int32_t* ids, int n, void* dk, void* dv,
                                void* stream) {
     return guard([&] {
         set_dev(p);
@@ -1010,7 +1021,8 @@ int oomb_accumulate_grad_pages(oomb_pool_t p, int layer, const int32_t* ids, int
         if (n == 0) return;
         int32_t* d = upload_ids(ids, n, S(stream));
         launch_accumulate_grads(d, n, p->gslot_layer(layer), p->gkpool, p->gvpool, p->pt->filled[layer],
-                                p->cfg.page_size, p->cfg.n_kv_heads, p->cfg.head_dim, dk, dv, S(stream));
+                                p->cfg.page_size, p->cfg.n_kv_heads, p->cfg.head_dim, dk, dv, S(stream), 0, nullptr,
+                                p->f64());
         OOMB_CUDA(cudaFreeAsync(d, S(stream)));
     });
 }
@@ -1021,6 +1033,7 @@ int oomb_accumulate_grad_pages_rope(oomb_pool_t p, int layer, const int32_t* ids
         set_dev(p);
         p->pt->check_ids(layer, ids, n, p->enforce, "gather_grad_pages", /*allow_remote=*/true);
         OOMB_REQUIRE(rope_base > 1.f, OOMB_CONFIG_ERROR, "rope_base must be > 1");
+        OOMB_REQUIRE(!p->f64(), OOMB_CONFIG_ERROR, "the fused RoPE epilogues support fp32 / bf16 pools");
         if (n == 0) return;
         int32_t* d = upload_ids(ids, n, S(stream));
         launch_accumulate_grads(d, n, p->gslot_layer(layer), p->gkpool, p->gvpool, p->pt->filled[layer],

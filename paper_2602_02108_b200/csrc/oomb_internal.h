@@ -151,6 +151,7 @@ struct AttnGeom {
     int max_pages;
     int chunk_keys;  // 1: attend the chunk's causal prefix after the selected pages (attention.hpp:187-199);
                      // 0: selected pages only (a page-range shard other than the one owning the chunk's keys)
+    double scale64;  // 1/sqrt(hd) in double (fp64 pools: the reference's Real = double)
 };
 
 // ---------------------------------------------------------------------------
@@ -168,7 +169,7 @@ constexpr int32_t SLOT_REMOTE = -2;
 
 void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_t filled_before, int P, int Hkv,
                    int hd, int first_page, int n_pages_touched, const NewSlots& ns, int32_t* d_kvslot_layer,
-                   void* kpool, void* vpool, float* kavg_sum_layer, int32_t* kavg_cnt_layer, int* d_err,
+                   void* kpool, void* vpool, void* kavg_sum_layer, int32_t* kavg_cnt_layer, int* d_err,
                    cudaStream_t st, const double* rope_inv_freq = nullptr, void* kavg_planes_layer = nullptr,
                    int64_t plane_stride = 0);
 // dst CSR = the ids of src with id % stride == rank, list order kept (one CTA).
@@ -179,39 +180,45 @@ void launch_rope(int in_dtype, int out_dtype, const void* x, int64_t rows, int h
 // Device table inv_freq[i] = base^(-2i/hd) computed on the host with the reference's std::pow
 // (ops.hpp:198-201); cached per (device, base, hd) for the life of the library.
 const double* rope_inv_freq_table(float base, int hd);
-void launch_mean_keys(const float* kavg_sum_layer, const int32_t* kavg_cnt_layer, int n, int row_elems,
-                      float* out, cudaStream_t st);
+// Buffers typed "void*" below hold the pool's accumulation type: float for OOMB_F32 / OOMB_BF16
+// pools, double for OOMB_F64 pools (f64 = true).
+void launch_mean_keys(const void* kavg_sum_layer, const int32_t* kavg_cnt_layer, int n, int row_elems,
+                      void* out, cudaStream_t st, bool f64 = false);
 void launch_gather(int dtype, int grads, const int32_t* d_ids, int n, const int32_t* d_slot_layer,
                    const void* pk, const void* pv, int64_t filled, int P, int Hkv, int hd, void* k_out,
                    void* v_out, uint8_t* valid_out, int* d_err, cudaStream_t st);
-void launch_scatter(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, float* gk, float* gv,
-                    const float* dk, const float* dv, int64_t filled, int P, int Hkv, int hd, int* d_err,
-                    cudaStream_t st);
-void launch_accumulate_grads(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, const float* gk,
-                             const float* gv, int64_t filled, int P, int Hkv, int hd, float* dk, float* dv,
+void launch_scatter(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, void* gk, void* gv,
+                    const void* dk, const void* dv, int64_t filled, int P, int Hkv, int hd, int* d_err,
+                    cudaStream_t st, bool f64 = false);
+void launch_accumulate_grads(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, const void* gk,
+                             const void* gv, int64_t filled, int P, int Hkv, int hd, void* dk, void* dv,
                              cudaStream_t st, int64_t rope_pos0 = 0,
-                             const double* rope_inv_freq = nullptr);
-void launch_grad_init(const int32_t* d_pages, const int32_t* d_slots, int n, int32_t* d_gslot_layer, float* gk,
-                      float* gv, int64_t page_elems, cudaStream_t st);
-void launch_zero_slots(const int32_t* d_slots, int n, float* gk, float* gv, int64_t page_elems, cudaStream_t st);
+                             const double* rope_inv_freq = nullptr, bool f64 = false);
+void launch_grad_init(const int32_t* d_pages, const int32_t* d_slots, int n, int32_t* d_gslot_layer, void* gk,
+                      void* gv, int64_t page_elems, cudaStream_t st, int elem_bytes = 4);
+void launch_zero_slots(const int32_t* d_slots, int n, void* gk, void* gv, int64_t page_elems, cudaStream_t st,
+                       int elem_bytes = 4);
 
-void launch_score_simt(int dtype, const void* q, int64_t tokens, int Hq, int hd, const float* k_avg, int64_t n,
-                       int Hkv, int P, float scale, float* vote, float* stats_scratch, cudaStream_t st,
+// scale: the float score scale (fp32 / bf16), scale64 the same in double (fp64 pools). stats_scratch:
+// tokens * Hq * 2 elements of the accumulation type.
+void launch_score_simt(int dtype, const void* q, int64_t tokens, int Hq, int hd, const void* k_avg, int64_t n,
+                       int Hkv, int P, float scale, double scale64, void* vote, void* stats_scratch, cudaStream_t st,
                        bool partial_only = false);
 void launch_lse_merge(const void* o_parts, const float* lse_parts, int parts, int64_t rows, int hd, int dtype,
                       void* out, float* lse, cudaStream_t st);
-void launch_topk(const float* vote, int m, int n, int k, int32_t* sel_off, int32_t* sel_ids, cudaStream_t st);
+void launch_topk(const void* vote, int m, int n, int k, int32_t* sel_off, int32_t* sel_ids, cudaStream_t st,
+                 bool f64 = false);
 void launch_fill_csr_all(int32_t* off, int32_t* ids, int m, int first, int count, cudaStream_t st);
 
 void launch_attn_fwd_simt(int dtype, const AttnGeom& g, const void* q, const int32_t* sel_off,
                           const int32_t* sel_ids, const int32_t* d_kvslot_layer, const void* kpool,
-                          const void* vpool, const void* k_cur, const void* v_cur, void* out, float* lse, int* d_err,
+                          const void* vpool, const void* k_cur, const void* v_cur, void* out, void* lse, int* d_err,
                           cudaStream_t st);
 void launch_attn_bwd_simt(int dtype, const AttnGeom& g, const void* dout, const void* q, const int32_t* sel_off,
                           const int32_t* sel_ids, const int32_t* d_kvslot_layer, const int32_t* d_gslot_layer,
-                          const void* kpool, const void* vpool, float* gkpool, float* gvpool, const void* k_cur,
-                          const void* v_cur, const void* out, const float* lse, float* dq, float* dk_cur,
-                          float* dv_cur, int* d_err, cudaStream_t st, int n_past_pages);
+                          const void* kpool, const void* vpool, void* gkpool, void* gvpool, const void* k_cur,
+                          const void* v_cur, const void* out, const void* lse, void* dq, void* dk_cur,
+                          void* dv_cur, int* d_err, cudaStream_t st, int n_past_pages);
 
 // ---------------------------------------------------------------------------
 // tcgen05 / TMA kernels (attn_tc.cu)
@@ -240,6 +247,8 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
                         float* dv_cur, int* d_err, void* workspace, size_t workspace_bytes, int nnz, int n_pages,
                         cudaStream_t st, cudaStream_t side, cudaEvent_t ev_prep, cudaEvent_t ev_dq, bool join_dq);
 size_t attn_bwd_tc_workspace(const AttnGeom& g, int max_sel_ids);
+// Split-K count of the tcgen05 forward / dQ kernels for small grids (attn_fwd4.cu).
+int attn_tc_splits(const AttnGeom& g, int num_sms);
 bool score_tc_supported(int dtype, int hd, int P, int64_t tokens);
 size_t score_tc_workspace(int64_t tokens, int Hq, int Hkv, int64_t n, int P);
 void launch_score_tc(const void* q, int64_t tokens, int Hq, int Hkv, int P, const float* kavg_sum,

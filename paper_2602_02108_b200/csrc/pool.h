@@ -174,7 +174,9 @@ struct oomb_pool_s {
     oomb_tier_s* engine = nullptr;  // the attached real offload engine (orphaned if the pool dies first)
     int device = 0;
     int64_t max_pages = 0;
-    int elem = 4;
+    int elem = 4;   // K/V element bytes (bf16 2, fp32 4, fp64 8)
+    int aelem = 4;  // accumulation element bytes: K_avg sums, gradient pages, lse / dq / votes (fp64 pools: 8)
+    bool f64() const { return aelem == 8; }
     int64_t page_elems = 0;
     PageTable* pt = nullptr;
     int64_t n_kv_slots = 0, n_g_slots = 0;
@@ -188,7 +190,7 @@ struct oomb_pool_s {
     float* gvpool = nullptr;
     int32_t* d_kvslot = nullptr;
     int32_t* d_gslot = nullptr;
-    float* d_kavg_sum = nullptr;
+    void* d_kavg_sum = nullptr;  // accumulation type (see aelem)
     int32_t* d_kavg_cnt = nullptr;
     uint8_t* d_kavg_planes = nullptr;  // bf16 (see kavg_planes_layer)
     int64_t plane_stride = 0;
@@ -280,8 +282,8 @@ struct oomb_pool_s {
 
     int32_t* kvslot_layer(int l) { return d_kvslot + static_cast<int64_t>(l) * max_pages; }
     int32_t* gslot_layer(int l) { return d_gslot + static_cast<int64_t>(l) * max_pages; }
-    float* kavg_sum_layer(int l) {
-        return d_kavg_sum + static_cast<int64_t>(l) * max_pages * cfg.n_kv_heads * cfg.head_dim;
+    void* kavg_sum_layer(int l) {
+        return static_cast<uint8_t*>(d_kavg_sum) + static_cast<int64_t>(l) * max_pages * cfg.n_kv_heads * cfg.head_dim * aelem;
     }
     int32_t* kavg_cnt_layer(int l) { return d_kavg_cnt + static_cast<int64_t>(l) * max_pages; }
     // bf16 hi / lo planes of K_avg for the tcgen05 scorer ([layer][2][Hkv][plane_stride][hd]); null when

@@ -642,6 +642,7 @@ int oomb_tier_create(oomb_pool_t pool, const oomb_tier_config* cfg, void* comput
     return guard([&] {
         set_dev(pool);
         OOMB_REQUIRE(cfg->bandwidth_bytes_per_s > 0, OOMB_CONFIG_ERROR, "tiered_memory: bandwidth must be positive");
+        OOMB_REQUIRE(!pool->f64(), OOMB_CONFIG_ERROR, "tiered_memory: real page moves support fp32 / bf16 pools");
         auto* t = new oomb_tier_s();
         try {
             t->cfg = *cfg;

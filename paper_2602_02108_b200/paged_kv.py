@@ -24,7 +24,11 @@ HOST = 1
 
 
 def torch_dtype(name: str) -> torch.dtype:
-    return {"fp32": torch.float32, "f32": torch.float32, "bf16": torch.bfloat16}[name]
+    return {"fp32": torch.float32, "f32": torch.float32, "bf16": torch.bfloat16, "fp64": torch.float64,
+            "f64": torch.float64}[name]
+
+
+DTYPE_CODE = {torch.float32: 0, torch.bfloat16: 1, torch.float64: 2}  # oomb_dtype
 
 
 def stream_handle(stream: torch.cuda.Stream | None = None) -> C.c_void_p:
@@ -64,7 +68,8 @@ class MemoryReport:
 class PagedCache:
     """Per-layer logical page tables over a device page pool.
 
-    dtype: "bf16" (tensor-core path) or "fp32" (1e-5 parity path).
+    dtype: "bf16" (tensor-core path), "fp32" (1e-5 parity path) or "fp64" (the reference's Real = double:
+    exact SIMT kernels in double; K_avg, gradient pages, lse, dq and votes are double too).
     max_tokens: per-layer capacity of the device page table.
     device_capacity_pages: KV page slots on the device (all layers); default = all (the owned share).
     page_owner: (stride R, rank r) of a page-range shard: this pool stores K/V and
@@ -79,12 +84,14 @@ class PagedCache:
         self.cfg = cfg
         self.dtype_name = dtype
         self.dtype = torch_dtype(dtype)
+        # accumulation type of K_avg, gradient pages, lse / dq / dk_cur / dv_cur and votes
+        self.acc_dtype = torch.float64 if self.dtype == torch.float64 else torch.float32
         self.device_index = torch.cuda.current_device() if device is None else device
         self.device = torch.device("cuda", self.device_index)
         self.max_tokens = max_tokens if max_tokens is not None else 64 * cfg.chunk_size
         c = OombConfig(cfg.n_layers, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, cfg.chunk_size, cfg.page_size,
                        cfg.retrieval_budget, cfg.local_window, int(cfg.score_scale),
-                       1 if self.dtype == torch.bfloat16 else 0, self.max_tokens, device_capacity_pages,
+                       DTYPE_CODE[self.dtype], self.max_tokens, device_capacity_pages,
                        *(page_owner if page_owner is not None else (0, 0)))
         self.owner_stride, self.owner_rank = (max(1, page_owner[0]), page_owner[1]) if page_owner else (1, 0)
         h = C.c_void_p()
@@ -176,7 +183,7 @@ class PagedCache:
     def _gather(self, layer, page_ids, grads, stream):
         ids = self._ids(page_ids)
         rows = len(ids) * self.cfg.page_size
-        dt = torch.float32 if grads else self.dtype
+        dt = self.acc_dtype if grads else self.dtype
         k = torch.zeros((rows, self.cfg.n_kv_heads, self.cfg.head_dim), dtype=dt, device=self.device)
         v = torch.zeros_like(k)
         valid = torch.zeros(rows, dtype=torch.uint8, device=self.device)
@@ -187,7 +194,7 @@ class PagedCache:
     def scatter_add_grads(self, layer: int, page_ids, dk, dv, stream=None) -> None:
         """paged_kv.hpp:135-164 — lazily allocated, zeroed grad pages; valid slots add in place."""
         ids = self._ids(page_ids)
-        dk, dv = self._dev(dk, torch.float32), self._dev(dv, torch.float32)
+        dk, dv = self._dev(dk, self.acc_dtype), self._dev(dv, self.acc_dtype)
         want = len(ids) * self.cfg.page_size
         if (dk.dim() != 3 or dk.shape[0] != want or dk.shape[1] != self.cfg.n_kv_heads
                 or dk.shape[2] != self.cfg.head_dim or dk.shape != dv.shape):
@@ -198,14 +205,14 @@ class PagedCache:
     def page_mean_keys(self, layer: int, n_candidates: int = -1, stream=None) -> torch.Tensor:
         """paged_kv.hpp:170-183 — fp32 [n, kvh, hd]."""
         cap = max(self.n_pages(layer), 1)
-        out = torch.empty((cap, self.cfg.n_kv_heads, self.cfg.head_dim), dtype=torch.float32, device=self.device)
+        out = torch.empty((cap, self.cfg.n_kv_heads, self.cfg.head_dim), dtype=self.acc_dtype, device=self.device)
         n = C.c_int()
         call("oomb_page_mean_keys", self.handle, layer, n_candidates, _ptr(out), stream_handle(stream), C.byref(n))
         return out[: n.value]
 
     def kavg_raw(self, layer: int):
         n = self.n_pages(layer)
-        s = torch.zeros((max(n, 1), self.cfg.n_kv_heads, self.cfg.head_dim), dtype=torch.float32, device=self.device)
+        s = torch.zeros((max(n, 1), self.cfg.n_kv_heads, self.cfg.head_dim), dtype=self.acc_dtype, device=self.device)
         cnt = torch.zeros(max(n, 1), dtype=torch.int32, device=self.device)
         call("oomb_kavg_raw", self.handle, layer, _ptr(s), _ptr(cnt), stream_handle(None))
         return s[:n], cnt[:n]
@@ -259,7 +266,7 @@ class PagedCache:
     def accumulate_grad_pages(self, layer: int, page_ids, dk: torch.Tensor, dv: torch.Tensor, stream=None) -> None:
         """dM_i read-back (chunk_trainer.hpp:575-587): dk += gather_grad_pages(ids).k, same for dv."""
         ids = self._ids(page_ids)
-        if dk.dtype != torch.float32 or not dk.is_cuda or not dk.is_contiguous() or dk.shape != dv.shape:
+        if dk.dtype != self.acc_dtype or not dk.is_cuda or not dk.is_contiguous() or dk.shape != dv.shape:
             raise ShapeError("accumulate_grad_pages: fp32 contiguous CUDA dk/dv of equal shape required")
         call("oomb_accumulate_grad_pages", self.handle, layer, ids.ctypes.data_as(C.c_void_p), len(ids), _ptr(dk),
              _ptr(dv), stream_handle(stream))
@@ -269,7 +276,7 @@ class PagedCache:
         """The dM_i read-back fused with rope_backward of dK (chunk_trainer.hpp:575-592):
         dk <- rope^-1(dk + grad_k(ids)), dv += grad_v(ids); row r at position pos_offset + r."""
         ids = self._ids(page_ids)
-        if dk.dtype != torch.float32 or not dk.is_cuda or not dk.is_contiguous() or dk.shape != dv.shape:
+        if dk.dtype != self.acc_dtype or not dk.is_cuda or not dk.is_contiguous() or dk.shape != dv.shape:
             raise ShapeError("accumulate_grad_pages_rope: fp32 contiguous CUDA dk/dv of equal shape required")
         call("oomb_accumulate_grad_pages_rope", self.handle, layer, ids.ctypes.data_as(C.c_void_p), len(ids),
              _ptr(dk), _ptr(dv), int(pos_offset), C.c_float(rope_base), stream_handle(stream))
