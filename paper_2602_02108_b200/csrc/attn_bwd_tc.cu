@@ -60,6 +60,10 @@ __device__ __forceinline__ float ex2_mix(float x, int c, int n) {
 #define OOMB_BWD_LPT 1  // dK/dV units longest first (bwd_order_kernel); 0: own blocks, then union order
 #endif
 
+#ifndef OOMB_DQ_SPLIT
+#define OOMB_DQ_SPLIT 1  // split-K of the dQ kernel over key blocks when the grid is small (attn_tc_splits)
+#endif
+
 #ifndef OOMB_KV_TRACE
 #define OOMB_KV_TRACE 0  // per-CTA wait / phase cycle counters of the dK/dV kernel (OOMB_CTA_TRACE=dkdv:i:file)
 #endif
@@ -316,7 +320,12 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     if (bars->tmem_base != 0) __trap();  // all 512 columns: base column 0 (the constants rely on it)
     const int n_past = p64 ? hl.blocks() : (p.sel_off[qp + 1] - sel_begin) * (g.P / kTile);
-    const int nb = n_past + (g.chunk_keys ? qt + 1 : 0);
+    const int nb_all = n_past + (g.chunk_keys ? qt + 1 : 0);
+    // split-K (small grids, attn_tc_splits): CTA z attends key blocks [j0, j0 + nb) and stores its
+    // partial dQ at rows z C + t of the partial buffer; dq_split_sum adds the splits in z order
+    const int zs = static_cast<int>(gridDim.z), z = static_cast<int>(blockIdx.z);
+    const int j0 = static_cast<int>(static_cast<int64_t>(nb_all) * z / zs);
+    const int nb = static_cast<int>(static_cast<int64_t>(nb_all) * (z + 1) / zs) - j0;
     uint8_t* sQ = smem + kDqQ;
     uint8_t* sDO = smem + kDqDO;
     uint8_t* sK = smem + kDqK;
@@ -335,18 +344,19 @@ __global__ void __launch_bounds__(384, 1)
                 if (kDqAlias && j == 3) mbar_wait(&bars->qdo_tmem, 0);  // K stage 3 is the Q tile
                 mbar_expect_tx(&bars->k_full[st], kTileBytes);
                 uint8_t* dst = sK + st * kTileBytes;
-                if (j < n_past && p64) {
+                const int jb = j0 + j;
+                if (jb < n_past && p64) {
                     for (int hh = 0; hh < 2; ++hh) {
-                        const int row = past_half_row(g, p.sel_ids, p.kvslot, hl, 2 * j + hh, kvh, p.err);
+                        const int row = past_half_row(g, p.sel_ids, p.kvslot, hl, 2 * jb + hh, kvh, p.err);
                         for (int r = 0; r < 2; ++r)
                             tma_load_2d(dst + r * kRegion + hh * (kRegion / 2), &tm_kp, &bars->k_full[st], r * 64, row);
                     }
-                } else if (j < n_past) {
-                    const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, j, kvh, p.err);
+                } else if (jb < n_past) {
+                    const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, jb, kvh, p.err);
                     for (int r = 0; r < 2; ++r) tma_load_2d(dst + r * kRegion, &tm_kp, &bars->k_full[st], r * 64, b.row);
                 } else {
                     for (int r = 0; r < 2; ++r)
-                        tma_load_3d(dst + r * kRegion, &tm_kc, &bars->k_full[st], r * 64, kvh, (j - n_past) * kTile);
+                        tma_load_3d(dst + r * kRegion, &tm_kc, &bars->k_full[st], r * 64, kvh, (jb - n_past) * kTile);
                 }
             }
         }
@@ -358,18 +368,19 @@ __global__ void __launch_bounds__(384, 1)
                 if (kDqAlias && j == 0) mbar_wait(&bars->qdo_tmem, 0);  // V stage 0 is the dO tile
                 mbar_expect_tx(&bars->v_full[st], kTileBytes);
                 uint8_t* dst = sV + st * kTileBytes;
-                if (j < n_past && p64) {
+                const int jb = j0 + j;
+                if (jb < n_past && p64) {
                     for (int hh = 0; hh < 2; ++hh) {
-                        const int row = past_half_row(g, p.sel_ids, p.kvslot, hl, 2 * j + hh, kvh, nullptr);
+                        const int row = past_half_row(g, p.sel_ids, p.kvslot, hl, 2 * jb + hh, kvh, nullptr);
                         for (int r = 0; r < 2; ++r)
                             tma_load_2d(dst + r * kRegion + hh * (kRegion / 2), &tm_vp, &bars->v_full[st], r * 64, row);
                     }
-                } else if (j < n_past) {
-                    const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, j, kvh, nullptr);
+                } else if (jb < n_past) {
+                    const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, jb, kvh, nullptr);
                     for (int r = 0; r < 2; ++r) tma_load_2d(dst + r * kRegion, &tm_vp, &bars->v_full[st], r * 64, b.row);
                 } else {
                     for (int r = 0; r < 2; ++r)
-                        tma_load_3d(dst + r * kRegion, &tm_vc, &bars->v_full[st], r * 64, kvh, (j - n_past) * kTile);
+                        tma_load_3d(dst + r * kRegion, &tm_vc, &bars->v_full[st], r * 64, kvh, (jb - n_past) * kTile);
                 }
             }
         }
@@ -447,12 +458,13 @@ __global__ void __launch_bounds__(384, 1)
         named_bar_sync(3, 256);
         for (int j = 0; j < nb; ++j) {
             int lim;  // keep key columns c <= lim (of this group's 64)
-            if (j < n_past && p64) {  // the group's 64 columns are half block 2j + wg
-                lim = half_lim(half_valid(g, p.sel_ids, hl, hvt, kDqNvCap / 2, 2 * j + wg), r);
-            } else if (j < n_past) {
-                lim = past_valid(g, p.sel_ids, sel_begin, nvt, kDqNvCap, j) - 1 - wg * 64;
+            const int jb = j0 + j;
+            if (jb < n_past && p64) {  // the group's 64 columns are half block 2 jb + wg
+                lim = half_lim(half_valid(g, p.sel_ids, hl, hvt, kDqNvCap / 2, 2 * jb + wg), r);
+            } else if (jb < n_past) {
+                lim = past_valid(g, p.sel_ids, sel_begin, nvt, kDqNvCap, jb) - 1 - wg * 64;
             } else {
-                lim = ((j - n_past == qt) ? r : kTile - 1) - wg * 64;
+                lim = ((jb - n_past == qt) ? r : kTile - 1) - wg * 64;
             }
             // ---- P = exp2(S * scale * log2e - L) for this group's 64 key columns
             mbar_wait(&bars->s_full, j & 1);
@@ -537,7 +549,8 @@ __global__ void __launch_bounds__(384, 1)
         fence_proxy_async_smem();
         named_bar_sync(1, 256);
         if (warp == 4 && lane == 0) {
-            for (int c = 0; c < g.hd / 32; ++c) tma_store_3d(&tmap_dq, stage + c * kSliceBytes, c * 32, h, qt * kTile);
+            for (int c = 0; c < g.hd / 32; ++c)
+                tma_store_3d(&tmap_dq, stage + c * kSliceBytes, c * 32, h, z * g.C + qt * kTile);
             bulk_commit();
             bulk_wait_read0();
         }
@@ -1090,6 +1103,22 @@ __global__ void __launch_bounds__(384, 1)
 }  // namespace
 
 
+// dQ = sum of the split-K partials in z order (deterministic).
+__global__ void dq_split_sum_kernel(const float4* __restrict__ part, int zs, int64_t n4, float4* __restrict__ dq) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float4 a = part[i];
+        for (int z = 1; z < zs; ++z) {
+            const float4 b = part[z * n4 + i];
+            a.x += b.x;
+            a.y += b.y;
+            a.z += b.z;
+            a.w += b.w;
+        }
+        dq[i] = a;
+    }
+}
+
 bool tc_bwd_available() { return true; }
 
 size_t attn_bwd_tc_workspace(const AttnGeom& g, int) {
@@ -1156,10 +1185,21 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     OOMB_CUDA(cudaStreamWaitEvent(side, ev_prep, 0));
     auto launch_dq = [&] {
         ProfScope s_(PK_BWD_DQ, side);
-        const CUtensorMap tdq = map_rows_heads_f32(dq, g.C, g.Hq, g.hd);
-        attn_bwd_dq_kernel<<<dim3(g.Hq, g.C / kTile), 384, kDqSmem, side>>>(tq, tdo, tkc, tvc, maps.kpool,
-                                                                            maps.vpool, tdq, p);
+        const int zs = OOMB_DQ_SPLIT ? attn_tc_splits(g, num_sms) : 1;
+        float* part = nullptr;
+        const int64_t n = static_cast<int64_t>(g.C) * g.Hq * g.hd;
+        if (zs > 1) OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), zs * n * sizeof(float), side));
+        const CUtensorMap tdq = map_rows_heads_f32(zs > 1 ? part : dq, static_cast<int64_t>(zs) * g.C, g.Hq, g.hd);
+        attn_bwd_dq_kernel<<<dim3(g.Hq, g.C / kTile, zs), 384, kDqSmem, side>>>(tq, tdo, tkc, tvc, maps.kpool,
+                                                                                maps.vpool, tdq, p);
         check_launch("attn_bwd_dq_kernel");
+        if (zs > 1) {
+            dq_split_sum_kernel<<<static_cast<unsigned>(std::min<int64_t>((n / 4 + 255) / 256, 4 * num_sms)), 256, 0,
+                                  side>>>(reinterpret_cast<const float4*>(part), zs, n / 4,
+                                          reinterpret_cast<float4*>(dq));
+            check_launch("dq_split_sum_kernel");
+            OOMB_CUDA(cudaFreeAsync(part, side));
+        }
         OOMB_CUDA(cudaEventRecord(ev_dq, side));
     };
     auto launch_dkdv = [&] {

@@ -18,6 +18,8 @@
 // Warp roles (384 threads): w0 Q + K producer, w1 MMA, w2 V producer, w3 TMEM allocator,
 // w4..w7 softmax group 0 (even blocks), w8..w11 group 1 (odd blocks); thread = query row.
 
+#include <algorithm>
+
 #include "tc_common.cuh"
 
 namespace oomb {
@@ -52,6 +54,9 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define OOMB_FWD4_POLY 0  // measured: no gain (the softmax phase is latency-bound, not MUFU-bound)
 #endif
 constexpr bool kF4Poly = OOMB_FWD4_POLY != 0;
+#ifndef OOMB_FWD_SPLIT
+#define OOMB_FWD_SPLIT 1  // split-K over key blocks when the grid is small (attn_tc_splits)
+#endif
 #ifndef OOMB_FWD4_LEAN
 #define OOMB_FWD4_LEAN 1  // the FMA-pipe exponential is ex2_lean (one ALU op) rather than ex2_poly
 #endif
@@ -76,6 +81,11 @@ struct F4Params {
     __nv_bfloat16* out;
     float* lse;
     int* err;
+    // split-K over the key blocks (few query tiles, long histories: c1): CTA z of gridDim.z attends
+    // blocks [z nb / Z, (z+1) nb / Z) and writes its normalised partial O (fp32) and LSE here; a
+    // merge kernel combines them exactly in z order. Null: one split, O / LSE straight to out / lse.
+    float* o_part;    // [Z][C][Hq][hd]
+    float* lse_part;  // [Z][C][Hq]
 };
 
 __global__ void __launch_bounds__(384, 1)
@@ -119,7 +129,10 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     if (bars->tmem_base != 0) __trap();  // all 512 columns: base column 0 (the constants rely on it)
     const int n_past = p64 ? hl.blocks() : (p.sel_off[qp + 1] - sel_begin) * (g.P / kTile);
-    const int nb = n_past + (g.chunk_keys ? qt + 1 : 0);
+    const int nb_all = n_past + (g.chunk_keys ? qt + 1 : 0);
+    const int zs = static_cast<int>(gridDim.z), z = static_cast<int>(blockIdx.z);
+    const int j0 = static_cast<int>(static_cast<int64_t>(nb_all) * z / zs);  // this split's key blocks
+    const int nb = static_cast<int>(static_cast<int64_t>(nb_all) * (z + 1) / zs) - j0;
     uint8_t* sQ = smem + kF4Q;
     uint8_t* sK = smem + kF4K;
     uint8_t* sV = smem + kF4V;
@@ -142,18 +155,19 @@ __global__ void __launch_bounds__(384, 1)
                 if (j >= nst) mbar_wait(&empty[st], ((j / nst) - 1) & 1);
                 mbar_expect_tx(&full[st], kTileBytes);
                 uint8_t* dst = base + st * kTileBytes;
-                if (j < n_past && p64) {  // two 64-row half blocks (pool maps with 64-row boxes)
+                const int jb = j0 + j;  // the block's index in the tile's full list
+                if (jb < n_past && p64) {  // two 64-row half blocks (pool maps with 64-row boxes)
                     for (int hh = 0; hh < 2; ++hh) {
-                        const int row = past_half_row(g, p.sel_ids, p.kvslot, hl, 2 * j + hh, kvh, is_k ? p.err : nullptr);
+                        const int row = past_half_row(g, p.sel_ids, p.kvslot, hl, 2 * jb + hh, kvh, is_k ? p.err : nullptr);
                         for (int r = 0; r < 2; ++r)
                             tma_load_2d(dst + r * kRegion + hh * (kRegion / 2), mp, &full[st], r * 64, row);
                     }
-                } else if (j < n_past) {
-                    const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, j, kvh, is_k ? p.err : nullptr);
+                } else if (jb < n_past) {
+                    const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, jb, kvh, is_k ? p.err : nullptr);
                     for (int r = 0; r < 2; ++r) tma_load_2d(dst + r * kRegion, mp, &full[st], r * 64, b.row);
                 } else {
                     for (int r = 0; r < 2; ++r)
-                        tma_load_3d(dst + r * kRegion, mc, &full[st], r * 64, kvh, (j - n_past) * kTile);
+                        tma_load_3d(dst + r * kRegion, mc, &full[st], r * 64, kvh, (jb - n_past) * kTile);
                 }
             }
         }
@@ -216,12 +230,13 @@ __global__ void __launch_bounds__(384, 1)
         float l = 0.f;
         for (int j = wg; j < nb; j += 2) {
             int lo, hi;  // keep key columns c <= lo (c < 64) / c <= hi (c >= 64)
-            if (j < n_past && p64) {
-                lo = half_lim(half_valid(g, p.sel_ids, hl, hvt, kF4NvCap / 2, 2 * j), r);
-                hi = kHalf + half_lim(half_valid(g, p.sel_ids, hl, hvt, kF4NvCap / 2, 2 * j + 1), r);
+            const int jb = j0 + j;
+            if (jb < n_past && p64) {
+                lo = half_lim(half_valid(g, p.sel_ids, hl, hvt, kF4NvCap / 2, 2 * jb), r);
+                hi = kHalf + half_lim(half_valid(g, p.sel_ids, hl, hvt, kF4NvCap / 2, 2 * jb + 1), r);
             } else {
-                lo = (j < n_past) ? past_valid(g, p.sel_ids, sel_begin, nvt, kF4NvCap, j) - 1
-                                  : ((j - n_past == qt) ? r : kTile - 1);
+                lo = (jb < n_past) ? past_valid(g, p.sel_ids, sel_begin, nvt, kF4NvCap, jb) - 1
+                                   : ((jb - n_past == qt) ? r : kTile - 1);
                 hi = lo;
             }
             mbar_wait(&bars->s_full[wg], (j >> 1) & 1);
@@ -327,6 +342,7 @@ __global__ void __launch_bounds__(384, 1)
         // group w writes output columns [64w, 64w + 64) (head dim 64: group 0 only; columns 64-127
         // of O are the zero padding of the 128-wide tiles, see launch_attn_fwd_tc4)
         __nv_bfloat16* orow = p.out + (static_cast<int64_t>(t) * g.Hq + h) * g.hd + wg * 64;
+        float* prow = p.o_part ? p.o_part + ((static_cast<int64_t>(z) * g.C + t) * g.Hq + h) * g.hd + wg * 64 : nullptr;
 #pragma unroll 1
         for (int c = 0; c < (wg * 64 < g.hd ? 4 : 0); ++c) {
             uint32_t x0[16], x1[16];
@@ -340,17 +356,72 @@ __global__ void __launch_bounds__(384, 1)
                 const float v1 = s1 != 0.f ? __uint_as_float(x1[u]) * s1 : 0.f;  // garbage: never multiply it
                 f[u] = v0 + v1;
             }
-            *reinterpret_cast<uint4*>(orow + c * 16) = pack8(f);
-            *reinterpret_cast<uint4*>(orow + c * 16 + 8) = pack8(f + 8);
+            if (prow) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    *reinterpret_cast<float4*>(prow + c * 16 + 4 * u) = make_float4(f[4 * u], f[4 * u + 1], f[4 * u + 2], f[4 * u + 3]);
+            } else {
+                *reinterpret_cast<uint4*>(orow + c * 16) = pack8(f);
+                *reinterpret_cast<uint4*>(orow + c * 16 + 8) = pack8(f + 8);
+            }
         }
-        if (wg == 0) p.lse[static_cast<int64_t>(t) * g.Hq + h] = lt > 0.f ? (mt + __log2f(lt)) * kLn2 : -INFINITY;
+        if (wg == 0) {
+            const float L = lt > 0.f ? (mt + __log2f(lt)) * kLn2 : -INFINITY;
+            if (p.lse_part) p.lse_part[(static_cast<int64_t>(z) * g.C + t) * g.Hq + h] = L;
+            else p.lse[static_cast<int64_t>(t) * g.Hq + h] = L;
+        }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 3) tmem_dealloc<512>(0);
 }
 
+// Exact merge of the split-K partials, splits in z order (deterministic): LSE = m + ln sum_z
+// e^(LSE_z - m), O = sum_z e^(LSE_z - LSE) O_z. One warp per (token, head) row; hd <= 128.
+__global__ void fwd_split_merge_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part, int zs,
+                                       int64_t rows, int hd, __nv_bfloat16* __restrict__ out, float* __restrict__ lse) {
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    float m = -INFINITY;
+    for (int z = 0; z < zs; ++z) m = fmaxf(m, lse_part[z * rows + row]);
+    float l = 0.f;
+    for (int z = 0; z < zs; ++z) {
+        const float x = lse_part[z * rows + row];
+        if (x != -INFINITY) l += __expf(x - m);
+    }
+    const float L = m == -INFINITY ? -INFINITY : m + __logf(l);
+    for (int d = lane * 4; d < hd; d += 128) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int z = 0; z < zs; ++z) {
+            const float x = lse_part[z * rows + row];
+            if (x == -INFINITY) continue;
+            const float w = __expf(x - L);
+            const float4 o = *reinterpret_cast<const float4*>(o_part + (z * rows + row) * hd + d);
+            acc.x += w * o.x;
+            acc.y += w * o.y;
+            acc.z += w * o.z;
+            acc.w += w * o.w;
+        }
+        __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(out + row * hd + d);
+        dst[0] = __floats2bfloat162_rn(acc.x, acc.y);
+        dst[1] = __floats2bfloat162_rn(acc.z, acc.w);
+    }
+    if (lane == 0) lse[row] = L;
+}
+
 }  // namespace
+
+// Split count for the forward / dQ kernels: a grid of Hq x C/128 tiles that fills less than half
+// the GPU splits each tile's key blocks over up to 16 CTAs (at least 4 blocks each).
+int attn_tc_splits(const AttnGeom& g, int num_sms) {
+    const int tiles = g.Hq * (g.C / kTile);
+    if (2 * tiles > num_sms) return 1;
+    const int64_t blocks = (g.filled + kTile - 1) / kTile;  // past keys + this chunk's (an upper bound)
+    int64_t z = std::min<int64_t>(16, num_sms / tiles);
+    z = std::min<int64_t>(z, blocks / 4);
+    return static_cast<int>(std::max<int64_t>(1, z));
+}
 
 void launch_attn_fwd_tc4(const AttnGeom& g, const TcPoolMaps& maps, const void* q, const int32_t* sel_off,
                          const int32_t* sel_ids, const int32_t* d_kvslot_layer, const void* k_cur, const void* v_cur,
@@ -362,9 +433,25 @@ void launch_attn_fwd_tc4(const AttnGeom& g, const TcPoolMaps& maps, const void* 
     const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, g.hd);
     const CUtensorMap tkc = map_rows_heads(k_cur, g.C, g.Hkv, g.hd);
     const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, g.hd);
-    F4Params p{g, sel_off, sel_ids, d_kvslot_layer, static_cast<__nv_bfloat16*>(out), lse, d_err};
-    attn_fwd_tc4_kernel<<<dim3(g.Hq, g.C / kTile), 384, kF4Smem, st>>>(tq, tkc, tvc, maps.kpool, maps.vpool, p);
+    int dev = 0, num_sms = 148;
+    OOMB_CUDA(cudaGetDevice(&dev));
+    OOMB_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    const int zs = OOMB_FWD_SPLIT ? attn_tc_splits(g, num_sms) : 1;
+    const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
+    F4Params p{g, sel_off, sel_ids, d_kvslot_layer, static_cast<__nv_bfloat16*>(out), lse, d_err, nullptr, nullptr};
+    if (zs > 1) {
+        OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p.o_part), zs * rows * g.hd * sizeof(float), st));
+        OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p.lse_part), zs * rows * sizeof(float), st));
+    }
+    attn_fwd_tc4_kernel<<<dim3(g.Hq, g.C / kTile, zs), 384, kF4Smem, st>>>(tq, tkc, tvc, maps.kpool, maps.vpool, p);
     check_launch("attn_fwd_tc4_kernel");
+    if (zs > 1) {
+        fwd_split_merge_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(
+            p.o_part, p.lse_part, zs, rows, g.hd, static_cast<__nv_bfloat16*>(out), lse);
+        check_launch("fwd_split_merge_kernel");
+        OOMB_CUDA(cudaFreeAsync(p.o_part, st));
+        OOMB_CUDA(cudaFreeAsync(p.lse_part, st));
+    }
 }
 
 }  // namespace oomb
