@@ -270,6 +270,8 @@ SEL_PRIORITY = os.environ.get("OOMB_SEL_PRIORITY", "1") != "0"
 FWD_STREAMS = int(os.environ.get("OOMB_FWD_STREAMS", "2"))
 # backward with deferred dQ joins: chunk i-1's dK/dV overlaps chunk i's dQ (OOMB_ATTN_DEFER_DQ)
 BWD_DEFER = os.environ.get("OOMB_BWD_DEFER", "1") != "0"
+# the unsplit layer step through the native loop (oomb_layer_step); 0: the Python chunk loop
+NATIVE_LOOP = os.environ.get("OOMB_NATIVE_LOOP", "1") != "0"
 
 
 def bench_inputs(cfg, seed: int, device, rq: int = 16):
@@ -281,8 +283,12 @@ def bench_inputs(cfg, seed: int, device, rq: int = 16):
     bf = torch.bfloat16
     k_all = torch.randn(T, Hkv, hd, device=device, generator=g).to(bf)
     v_all = torch.randn(T, Hkv, hd, device=device, generator=g).to(bf)
-    q = [torch.randn(C, Hq, hd, device=device, generator=g).to(bf) for _ in range(rq)]
-    do = [torch.randn(C, Hq, hd, device=device, generator=g).to(bf) for _ in range(rq)]
+    q = torch.empty(rq, C, Hq, hd, device=device, dtype=bf)  # contiguous: the native loop's [Rq][C][Hq][hd]
+    do = torch.empty(rq, C, Hq, hd, device=device, dtype=bf)
+    for i in range(rq):
+        q[i] = torch.randn(C, Hq, hd, device=device, generator=g).to(bf)
+    for i in range(rq):
+        do[i] = torch.randn(C, Hq, hd, device=device, generator=g).to(bf)
     return k_all, v_all, q, do
 
 
@@ -305,7 +311,8 @@ class Run:
         self.layer = layer
         self.cache = (PagedCache(self.mc, dtype="bf16", max_tokens=T) if layer is None else
                       layer.attach(layer.plan.make_cache(layer.cfg, dtype="bf16", max_tokens=T)))
-        self.k_all, self.v_all, self.q, self.do = bench_inputs(cfg, seed, device, self.RQ)
+        self.k_all, self.v_all, self.q_all, self.do_all = bench_inputs(cfg, seed, device, self.RQ)
+        self.q, self.do = list(self.q_all), list(self.do_all)  # per-chunk views
         bf = torch.bfloat16
         self.o_all = torch.empty(self.S, C, Hq, hd, device=device, dtype=bf)
         self.lse_all = torch.empty(self.S, C, Hq, device=device, dtype=torch.float32)
@@ -452,6 +459,22 @@ class Run:
         self.cache.reset()
         comp = torch.cuda.current_stream()
         f0, b0, b1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        if NATIVE_LOOP and self.layer is None:
+            # the whole layer step in native code (oomb_layer_step): the same work, streams and order
+            # as forward_pass + the reverse bwd_chunk loop below, without ~10 host calls per chunk
+            from paper_2602_02108_b200.chunk_loop import layer_step
+            cfg = self.cfg
+            kv = (self.S, C, cfg["Hkv"], cfg["hd"])
+            args = (self.cache, 0, self.q_all, self.k_all.view(kv), self.v_all.view(kv), self.do_all, self.o_all,
+                    self.lse_all, self.grads)
+            f0.record(comp)
+            layer_step(*args, mode=cfg["mode"], phase="forward")
+            b0.record(comp)
+            layer_step(*args, mode=cfg["mode"], phase="backward")
+            b1.record(comp)
+            self.fwd_phase.append((f0, b0))
+            self.bwd_phase.append((b0, b1))
+            return
         f0.record(comp)
         self.forward_pass()
         b0.record(comp)

@@ -240,6 +240,27 @@ OOMB_API int oomb_attn_backward_ex(oomb_pool_t pool, int layer, const void* dout
 /* Exact merge of page-range shards' partial attention outputs, shards in rank order:
  * o_parts [parts][rows][hd] (dtype), lse_parts [parts][rows] fp32 natural log ->
  * lse = ln sum_r e^{lse_r}, out = sum_r e^{lse_r - lse} o_r. rows = tokens * n_q_heads. */
+/* The attention layer's whole chunk-recurrent step in one native call (chunk_trainer.hpp:131-186,
+ * attention only): for chunks i = 0..n-1 select (mode: dense / top-k K_avg vote / local window over
+ * the pages of chunks < i, :292-316) -> append_chunk -> attn_forward, then for i = n-1..0
+ * attn_backward -> the dM_i read-back of the chunk's own pages into its dk_cur / dv_cur (:575-587).
+ * Chunk i reads q[i % q_cycle], k[i], v[i], dout[i % dout_cycle] ([C][H][hd] blocks, pool dtype)
+ * and writes out[i], lse[i] (accumulation type); its dq / dk_cur / dv_cur go to block
+ * i * grad_stride_chunks of dq / dk_cur / dv_cur (grad_stride_chunks = 0: every chunk reuses block
+ * 0). Selection of chunk i+1 overlaps chunk i's attention on a high-priority stream, consecutive
+ * forwards run on two streams and dQ is deferred under the previous chunk's dK/dV: the same
+ * results as the host loop, bitwise. Requires no attached TieredEngine and no page-range split
+ * (those run their protocol in the host loop). flags: OOMB_LAYER_FORWARD_ONLY runs the forward
+ * alone; OOMB_LAYER_BACKWARD_ONLY then runs the backward of that forward (its selections are kept). */
+#define OOMB_MODE_DENSE 0
+#define OOMB_MODE_TOPK 1
+#define OOMB_MODE_LOCAL 2
+#define OOMB_LAYER_FORWARD_ONLY 1
+#define OOMB_LAYER_BACKWARD_ONLY 2
+OOMB_API int oomb_layer_step(oomb_pool_t pool, int layer, int n_chunks, int mode, const void* q, int q_cycle,
+                             const void* k, const void* v, const void* dout, int dout_cycle, void* out, void* lse,
+                             void* dq, void* dk_cur, void* dv_cur, int64_t grad_stride_chunks, int flags,
+                             void* stream);
 /* Make `stream` wait for the dq of every earlier oomb_attn_backward_ex(..., OOMB_ATTN_DEFER_DQ). */
 OOMB_API int oomb_attn_join_dq(oomb_pool_t pool, void* stream);
 OOMB_API int oomb_lse_merge(const void* o_parts, const float* lse_parts, int parts, int64_t rows, int hd, int dtype,

@@ -22,7 +22,8 @@ LIB = os.path.join(PKG, "liboomb.so")
 COMM_LIB = os.path.join(PKG, "liboomb_comm.so")  # NCCL exchange steps (include/oomb_comm.h)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["oomb_api.cu", "kernels_simt.cu", "attn_tc.cu", "attn_fwd4.cu", "attn_bwd_tc.cu", "score_tc.cu", "tier.cu"]
+SOURCES = ["oomb_api.cu", "kernels_simt.cu", "attn_tc.cu", "attn_fwd4.cu", "attn_bwd_tc.cu", "score_tc.cu", "tier.cu",
+           "layer_loop.cu"]
 HEADERS = ["oomb_internal.h", "ptx.cuh", "tc_common.cuh", "pool.h"]
 
 FLAGS = [

@@ -20,7 +20,7 @@ import torch
 
 from . import attention as A
 from ._lib import call
-from .paged_kv import PagedCache, stream_handle
+from .paged_kv import PagedCache, _ptr, stream_handle
 
 
 class AttentionChunkLoop:
@@ -158,3 +158,29 @@ class AttentionChunkLoop:
             from .tiered_memory import BACKWARD
             self.engine.release_all_reservations()
             self.engine.begin_phase(BACKWARD)
+
+
+MODES = {"dense": 0, "topk": 1, "local": 2}  # OOMB_MODE_*
+
+
+def layer_step(cache: PagedCache, layer: int, q, k, v, dout, out, lse, grads: A.AttnGrads, mode: str | None = None,
+               grad_stride_chunks: int = 0, phase: str = "both", stream=None) -> None:
+    """The attention layer's whole chunk-recurrent step as ONE native call (oomb_layer_step): the
+    same select -> append -> attend forward and reverse backward + dM_i read-back as
+    AttentionChunkLoop without an engine, with the bench's overlaps (selection one chunk ahead on a
+    high-priority stream, two forward streams, deferred dQ). q / dout: [Rq][C][Hq][hd] (chunk i uses
+    block i % Rq), k / v: [S][C][Hkv][hd]; out [S][C][Hq][hd], lse [S][C][Hq]; grads.dq / dk_cur /
+    dv_cur hold one chunk (grad_stride_chunks = 0: every chunk reuses it) or S chunks (= 1).
+    phase: "both", "forward" (OOMB_LAYER_FORWARD_ONLY) or "backward" (the backward of the pool's
+    last forward of the same chunks, OOMB_LAYER_BACKWARD_ONLY)."""
+    cfg = cache.cfg
+    mode = mode or cfg.mode_for_layer(layer)
+    S = k.shape[0]
+    for t, want in ((q, cache.dtype), (k, cache.dtype), (v, cache.dtype), (dout, cache.dtype), (out, cache.dtype),
+                    (lse, cache.acc_dtype), (grads.dq, cache.acc_dtype), (grads.dk_cur, cache.acc_dtype),
+                    (grads.dv_cur, cache.acc_dtype)):
+        if t.dtype != want or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("layer_step: contiguous device tensors of the pool / accumulation dtype expected")
+    call("oomb_layer_step", cache.handle, layer, S, MODES[mode], _ptr(q), q.shape[0], _ptr(k), _ptr(v), _ptr(dout),
+         dout.shape[0], _ptr(out), _ptr(lse), _ptr(grads.dq), _ptr(grads.dk_cur), _ptr(grads.dv_cur),
+         grad_stride_chunks, {"both": 0, "forward": 1, "backward": 2}[phase], stream_handle(stream))

@@ -1,0 +1,182 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// The attention layer's chunk-recurrent step as native code: the hot path's own call sequence of
+// ChunkTrainer::train_step (chunk_trainer.hpp:131-186) restricted to one attention layer, so a
+// whole 1M-token layer pass is one C call instead of ~10 host calls per chunk.
+//
+//   forward, chunks ascending (chunk_trainer.hpp:409-437):
+//       select over the pages of earlier chunks (dense: all; local: recent window; top-k:
+//       K_avg -> score_pages -> select_topk_row, :292-316) -> append_chunk -> attn_forward
+//   backward, chunks descending (:531-592):
+//       attn_backward (past-page dK/dV into the gradient pool) -> dM_i read-back of the chunk's
+//       own pages into its dk_cur / dv_cur (:575-587)
+//
+// The dependencies the loop does NOT have are exploited exactly as bench.py's Python loop does
+// (same results, bitwise): chunk i+1's selection reads only K_avg of chunks <= i, so it runs on a
+// high-priority stream under chunk i's attention; consecutive chunks' forwards run on two streams
+// (chunk i reads pages of chunks < i and its own k / v); each chunk's dQ is deferred
+// (OOMB_ATTN_DEFER_DQ) so it overlaps the previous chunk's dK/dV, whose launches stay ordered.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <memory>
+#include <numeric>
+#include <vector>
+
+#include "oomb_internal.h"
+#include "pool.h"
+
+namespace oomb {
+namespace {
+
+// Streams, events, per-chunk selections and vote buffers of a pool's layer loop, kept across calls
+// (pool->loop_state) so a step issues no allocation and no host synchronisation of its own.
+struct LayerLoop {
+    cudaStream_t sel = nullptr, att[2] = {nullptr, nullptr};
+    cudaEvent_t ev_app[2] = {}, ev_sel[2] = {}, ev_att[2] = {};
+    std::vector<oomb_selection_t> sels;
+    int sel_ids = 0;  // id capacity of every selection
+    void* votes[2] = {nullptr, nullptr};
+    int64_t vote_bytes = 0;
+    int fwd_chunks = 0;  // chunks of the last forward (their selections are kept for the backward)
+    explicit LayerLoop(int device) {
+        cudaSetDevice(device);
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        cudaStreamCreateWithPriority(&sel, cudaStreamNonBlocking, hi);  // selection ahead of the attention
+        for (int i = 0; i < 2; ++i) {
+            cudaStreamCreateWithFlags(&att[i], cudaStreamNonBlocking);
+            cudaEventCreateWithFlags(&ev_app[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&ev_sel[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&ev_att[i], cudaEventDisableTiming);
+        }
+    }
+    ~LayerLoop() {
+        for (auto s : sels) oomb_selection_destroy(s);
+        for (int i = 0; i < 2; ++i) {
+            if (votes[i]) cudaFree(votes[i]);
+            if (ev_app[i]) cudaEventDestroy(ev_app[i]);
+            if (ev_sel[i]) cudaEventDestroy(ev_sel[i]);
+            if (ev_att[i]) cudaEventDestroy(ev_att[i]);
+            if (att[i]) cudaStreamDestroy(att[i]);
+        }
+        if (sel) cudaStreamDestroy(sel);
+    }
+};
+
+void ok(int rc) {
+    if (rc != OOMB_OK) throw Error(rc, oomb_last_error());
+}
+
+}  // namespace
+}  // namespace oomb
+
+using namespace oomb;
+
+extern "C" int oomb_layer_step(oomb_pool_t p, int layer, int n_chunks, int mode, const void* q, int q_cycle,
+                               const void* k, const void* v, const void* dout, int dout_cycle, void* out, void* lse,
+                               void* dq, void* dk_cur, void* dv_cur, int64_t grad_stride_chunks, int flags,
+                               void* stream) {
+    return guard([&] {
+        OOMB_REQUIRE(p != nullptr, OOMB_STATE_ERROR, "layer_step: null pool");
+        OOMB_CUDA(cudaSetDevice(p->device));
+        const oomb_config& c = p->cfg;
+        OOMB_REQUIRE(n_chunks >= 1 && q_cycle >= 1 && dout_cycle >= 1, OOMB_SHAPE_ERROR, "layer_step: bad counts");
+        OOMB_REQUIRE(mode >= OOMB_MODE_DENSE && mode <= OOMB_MODE_LOCAL, OOMB_CONFIG_ERROR, "layer_step: bad mode");
+        OOMB_REQUIRE(p->engine == nullptr, OOMB_STATE_ERROR,
+                     "layer_step: a TieredEngine is attached (its residency protocol runs in the host loop)");
+        OOMB_REQUIRE(p->owner_stride == 1, OOMB_CONFIG_ERROR, "layer_step: page-range shards use the host loop");
+        const int C = c.chunk_size, P = c.page_size, m = C / P;
+        const int64_t qe = static_cast<int64_t>(C) * c.n_q_heads * c.head_dim;   // q / out / dout / dq per chunk
+        const int64_t ke = static_cast<int64_t>(C) * c.n_kv_heads * c.head_dim;  // k / v / dk / dv per chunk
+        const size_t el = static_cast<size_t>(p->elem), ae = static_cast<size_t>(p->aelem);
+        auto at = [](const void* b, int64_t elems, size_t es) {
+            return static_cast<const void*>(static_cast<const uint8_t*>(b) + elems * es);
+        };
+        auto atw = [](void* b, int64_t elems, size_t es) { return static_cast<void*>(static_cast<uint8_t*>(b) + elems * es); };
+        cudaStream_t comp = S(stream);
+        if (!p->loop_state) p->loop_state = std::shared_ptr<void>(new LayerLoop(p->device), [](void* x) {
+            delete static_cast<LayerLoop*>(x);
+        });
+        LayerLoop& L = *static_cast<LayerLoop*>(p->loop_state.get());
+        const int64_t max_pages = p->max_pages;
+        const int k_sel = c.retrieval_budget / P;
+        const int64_t per_qp = mode == OOMB_MODE_TOPK ? k_sel : mode == OOMB_MODE_LOCAL ? c.local_window : max_pages;
+        const int need_ids = static_cast<int>(std::max<int64_t>(1, m * per_qp));
+        if (need_ids > L.sel_ids) {  // (re)size the per-chunk selections
+            for (auto s_ : L.sels) oomb_selection_destroy(s_);
+            L.sels.clear();
+            L.sel_ids = need_ids;
+        }
+        while (static_cast<int>(L.sels.size()) < n_chunks) {
+            oomb_selection_t s_ = nullptr;
+            ok(oomb_selection_create(p, m, L.sel_ids, &s_));
+            L.sels.push_back(s_);
+        }
+        const int64_t vb = std::max<int64_t>(1, m * max_pages) * static_cast<int64_t>(ae);
+        if (mode == OOMB_MODE_TOPK && vb > L.vote_bytes) {
+            for (int i = 0; i < 2; ++i) {
+                if (L.votes[i]) OOMB_CUDA(cudaFree(L.votes[i]));
+                OOMB_CUDA(cudaMalloc(&L.votes[i], vb));
+            }
+            L.vote_bytes = vb;
+        }
+
+        if (flags & OOMB_LAYER_BACKWARD_ONLY) {
+            OOMB_REQUIRE(L.fwd_chunks >= n_chunks, OOMB_STATE_ERROR,
+                         "layer_step: backward-only needs this pool's forward of the same chunks first");
+            goto backward;
+        }
+        // ---- forward
+        OOMB_CUDA(cudaEventRecord(L.ev_app[1], comp));  // earlier work precedes this step's selections
+        OOMB_CUDA(cudaStreamWaitEvent(L.sel, L.ev_app[1], 0));
+        for (int i = 0; i < 2; ++i) OOMB_CUDA(cudaStreamWaitEvent(L.att[i], L.ev_app[1], 0));
+        for (int i = 0; i < n_chunks; ++i) {
+            const void* qi = at(q, (i % q_cycle) * qe, el);
+            const void* ki = at(k, i * ke, el);
+            const void* vi = at(v, i * ke, el);
+            const int n_cand = i * m;
+            if (i > 0) OOMB_CUDA(cudaStreamWaitEvent(L.sel, L.ev_app[(i - 1) & 1], 0));  // K_avg of chunks < i
+            if (mode == OOMB_MODE_TOPK && n_cand > 0)
+                ok(oomb_select_pages_topk(p, layer, qi, C, n_cand, L.sels[i], L.votes[i & 1], L.sel));
+            else if (mode == OOMB_MODE_LOCAL && n_cand > 0)
+                ok(oomb_select_recent(L.sels[i], n_cand, c.local_window, m, L.sel));
+            else
+                ok(oomb_select_all(L.sels[i], n_cand, m, L.sel));
+            OOMB_CUDA(cudaEventRecord(L.ev_sel[i & 1], L.sel));
+            int64_t b = 0, e = 0;
+            ok(oomb_append_chunk(p, layer, ki, vi, C, comp, &b, &e));
+            OOMB_CUDA(cudaEventRecord(L.ev_app[i & 1], comp));
+            cudaStream_t a = L.att[i & 1];
+            OOMB_CUDA(cudaStreamWaitEvent(a, L.ev_app[i & 1], 0));
+            OOMB_CUDA(cudaStreamWaitEvent(a, L.ev_sel[i & 1], 0));
+            ok(oomb_attn_forward_ex(p, layer, qi, C, L.sels[i], ki, vi, atw(out, i * qe, el),
+                                    atw(lse, static_cast<int64_t>(i) * C * c.n_q_heads, ae), 0, a));
+        }
+        for (int i = 0; i < 2; ++i) {
+            OOMB_CUDA(cudaEventRecord(L.ev_att[i], L.att[i]));
+            OOMB_CUDA(cudaStreamWaitEvent(comp, L.ev_att[i], 0));
+        }
+        OOMB_CUDA(cudaEventRecord(L.ev_sel[0], L.sel));
+        OOMB_CUDA(cudaStreamWaitEvent(comp, L.ev_sel[0], 0));
+        L.fwd_chunks = n_chunks;
+        if (flags & OOMB_LAYER_FORWARD_ONLY) return;
+
+    backward:  // ---- backward (dQ deferred: chunk i's dQ overlaps chunk i-1's dK/dV)
+        for (int i = n_chunks - 1; i >= 0; --i) {
+            std::vector<int32_t> own(static_cast<size_t>(m));
+            const int64_t gi = grad_stride_chunks ? i : 0;
+            const void* qi = at(q, (i % q_cycle) * qe, el);
+            const void* di = at(dout, (i % dout_cycle) * qe, el);
+            void* dqi = atw(dq, gi * qe, ae);
+            void* dki = atw(dk_cur, gi * ke, ae);
+            void* dvi = atw(dv_cur, gi * ke, ae);
+            ok(oomb_attn_backward_ex(p, layer, di, qi, C, L.sels[i], at(k, i * ke, el), at(v, i * ke, el),
+                                     at(out, i * qe, el), at(lse, static_cast<int64_t>(i) * C * c.n_q_heads, ae), dqi,
+                                     dki, dvi, OOMB_ATTN_DEFER_DQ, comp));
+            std::iota(own.begin(), own.end(), i * m);
+            ok(oomb_accumulate_grad_pages(p, layer, own.data(), m, dki, dvi, comp));
+        }
+        ok(oomb_attn_join_dq(p, comp));
+    });
+}

@@ -367,6 +367,7 @@ int oomb_pool_destroy(oomb_pool_t p) {
     if (!p) return OOMB_OK;
     cudaSetDevice(p->device);
     cudaDeviceSynchronize();
+    p->loop_state.reset();  // the layer loop's selections refer to the pool
     if (p->engine) tier_orphan(p->engine);  // an engine outliving its pool frees only its own memory
     cudaFree(p->kpool);
     cudaFree(p->vpool);

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <deque>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "oomb_internal.h"
@@ -174,6 +175,7 @@ struct oomb_pool_s {
     oomb_tier_s* engine = nullptr;  // the attached real offload engine (orphaned if the pool dies first)
     int device = 0;
     int64_t max_pages = 0;
+    std::shared_ptr<void> loop_state;  // oomb_layer_step's streams / selections (layer_loop.cu)
     int elem = 4;   // K/V element bytes (bf16 2, fp32 4, fp64 8)
     int aelem = 4;  // accumulation element bytes: K_avg sums, gradient pages, lse / dq / votes (fp64 pools: 8)
     bool f64() const { return aelem == 8; }
