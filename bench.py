@@ -910,7 +910,10 @@ def main():
     achieved = bwd_fl / (t_bwd / 1e3) / 1e12 if t_bwd > 0 else None
     traffic = None
     try:  # DRAM bytes of the dominant kernel pair from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+        tf = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
+        if not os.path.exists(tf):
+            tf = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+        with open(tf) as f:
             tr = json.load(f)
         traffic = {"bytes_per_launch": sum(tr[k]["dram_read_bytes"] + tr[k]["dram_write_bytes"]
                                            for k in ("attn_bwd_dq", "attn_bwd_dkdv")),
