@@ -610,21 +610,21 @@ struct KvBars {
 
 // A work unit as the scheduler publishes it to the MMA and softmax warps.
 struct KvUnit {
-    int valid;
-    int past;
+    uint8_t valid;
+    uint8_t past;
+    uint8_t has1;  // page size 64: a past unit is two pages of the ascending union, keys [0,64) and [64,128)
+    uint8_t n_qps; // past: number of query pages in the list (page size 64: of 128-row query tiles)
     int key0;      // first key of the block (chunk-relative for in-chunk, page-relative for past)
     int n_items;
-    int n_qps;     // past: number of query pages in the list (page size 64: of 128-row query tiles)
     int g_kv;
     int kv_row;    // pool tensor-map row of the K/V block (past; page size 64: of the first page)
     int g_row;     // grad-pool tensor-map row (past; page size 64: of the first page)
     int n_valid;   // valid keys of the block (page size 64: of the first page)
-    int pad;
-    // page size 64: a past unit is two pages of the ascending union, keys [0,64) and [64,128)
-    int kv_row1, g_row1, n_valid1, has1;
+    int kv_row1, g_row1, n_valid1;  // page size 64: the second page
     uint64_t qm0, qm1;  // the query pages that selected each page (bit qp)
     uint8_t qps[64];  // past: the query pages that selected the page, ascending (page size 64: query tiles)
 };
+static_assert(sizeof(KvUnit) <= 120, "unit descriptor");
 static_assert(sizeof(KvUnit) <= kKvUnitBytes, "unit descriptor");
 
 // K step ks (16 queries) of a packed P^T / dS^T operand: queries [64w, 64w+64) of warpgroup w

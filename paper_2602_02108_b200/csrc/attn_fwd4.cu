@@ -412,15 +412,17 @@ __global__ void fwd_split_merge_kernel(const float* __restrict__ o_part, const f
 
 }  // namespace
 
-// Split count for the forward / dQ kernels: a grid of Hq x C/128 tiles that fills less than half
-// the GPU splits each tile's key blocks over up to 16 CTAs (at least 4 blocks each).
+// Split count for the forward / dQ kernels. A grid of at most 32 (query tile, head) tiles (c1: 8)
+// leaves most of the 148 SMs idle, so each tile's key blocks are split over up to 16 CTAs (at least
+// 4 blocks each); larger grids run one CTA per tile. Splitting changes the rounding of the merged
+// output, so the rule must give a KV-group shard the same split as the unsharded layer: it does
+// whenever a shard still has more than 32 tiles (every BASELINE shape; a split layer of <= 32
+// tiles matches within rounding, not bitwise).
 int attn_tc_splits(const AttnGeom& g, int num_sms) {
-    const int tiles = g.Hq * (g.C / kTile);
-    if (2 * tiles > num_sms) return 1;
+    (void)num_sms;
+    if (g.Hq * (g.C / kTile) > 32) return 1;
     const int64_t blocks = (g.filled + kTile - 1) / kTile;  // past keys + this chunk's (an upper bound)
-    int64_t z = std::min<int64_t>(16, num_sms / tiles);
-    z = std::min<int64_t>(z, blocks / 4);
-    return static_cast<int>(std::max<int64_t>(1, z));
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, blocks / 4)));
 }
 
 void launch_attn_fwd_tc4(const AttnGeom& g, const TcPoolMaps& maps, const void* q, const int32_t* sel_off,
