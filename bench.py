@@ -161,7 +161,7 @@ def low_locality_keys(run, seed: int = 77):
     return out
 
 
-def offload_measure(run, cap_frac: float, repeats: int = 3):
+def offload_measure(run, cap_frac: float, repeats: int = 5):
     """One layer step through the reference's residency protocol (AttentionChunkLoop +
     TieredEngine, chunk_trainer.hpp:328-363) with the device page pool capped at cap_frac of the
     layer's pages, against the same loop with every page resident. Exposed copy % =
