@@ -5,8 +5,8 @@
 //
 //   bwd_prep      D[h][t] = sum_d dO*O (saved O, attention.hpp:253-256) and
 //                 L[h][t] = lse*log2(e), head-major for broadcast reads.
-//   bwd_mask      per past page: bitmask of the query pages that selected it.
-//   bwd_union     ascending union of selected pages (the backward's key blocks).
+//   bwd_sched     per past page: bitmask of the query pages that selected it; the ascending union
+//                 of selected pages (the backward's key blocks); the dK/dV units longest first.
 //   attn_bwd_dq   query-major: S = Q K^T, dP = dO V^T, dS = P (dP - D),
 //                 dQ += dS K over the query page's selected pages then the
 //                 chunk's causal prefix; dQ written once (fp32).
@@ -146,65 +146,73 @@ inline int layer_pages(const AttnGeom& g) {
     return static_cast<int>(std::min<int64_t>(g.max_pages, (g.filled + g.P - 1) / g.P));
 }
 
-__global__ void bwd_mask_kernel(const int32_t* __restrict__ off, const int32_t* __restrict__ ids, int max_pages,
-                                uint64_t* __restrict__ mask, int* err) {
-    const int qp = blockIdx.x;
-    for (int i = off[qp] + threadIdx.x; i < off[qp + 1]; i += blockDim.x) {
+
+
+// The backward's schedule in ONE single-CTA launch (a chunk's backward is a dozen small launches
+// on short histories, so each one counts): clear the page -> query-page bitmask and the dK/dV
+// work counter, build the mask from the selection, the ascending union of the selected pages and,
+// when `order` is given, the dK/dV work units longest first (LPT) so the persistent grid does not
+// end on a long unit: unit codes [0, ncb) are the chunk's own key blocks (block b is attended by the
+// ncb - b query tiles from its diagonal on), codes ncb + k * bpp + sub the past blocks of the k-th
+// union page (attended by popcount(mask) query pages x tpq tiles each). Units write disjoint
+// gradient rows, so the order changes the schedule only, never a result bit.
+__global__ void __launch_bounds__(1024) bwd_sched_kernel(const int32_t* __restrict__ off,
+                                                         const int32_t* __restrict__ ids, int m, int layer_pages,
+                                                         int n_pages, uint64_t* __restrict__ mask,
+                                                         int32_t* __restrict__ uni, int32_t* __restrict__ n_uni, int ncb,
+                                                         int bpp, int tpq, int32_t* __restrict__ order, int* err) {
+    using Scan = cub::BlockScan<int, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    constexpr int kKeys = 256;
+    __shared__ int hist[kKeys], cur[kKeys];
+    const int tid = threadIdx.x;
+    for (int p = tid; p < n_pages; p += 1024) mask[p] = 0ull;
+    for (int i = tid; i < kKeys; i += 1024) hist[i] = 0;
+    if (tid == 0) n_uni[1] = 0;  // the dK/dV kernel's work counter
+    __syncthreads();
+    const int nnz = m > 0 ? off[m] : 0;
+    for (int i = tid; i < nnz; i += 1024) {
+        int lo = 0, hi = m;  // the list holding entry i: the last qp with off[qp] <= i
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (off[mid] <= i) lo = mid;
+            else hi = mid;
+        }
         const int pid = ids[i];
-        if (pid < 0 || pid >= max_pages) {
+        if (pid < 0 || pid >= layer_pages) {
             atomicOr(err, DERR_BAD_ID);
             continue;
         }
-        atomicOr(reinterpret_cast<unsigned long long*>(mask + pid), 1ull << qp);
+        atomicOr(reinterpret_cast<unsigned long long*>(mask + pid), 1ull << lo);
     }
-}
-
-__global__ void __launch_bounds__(1024) bwd_union_kernel(const uint64_t* __restrict__ mask, int n_pages,
-                                                         int32_t* __restrict__ uni, int32_t* __restrict__ n_uni) {
-    // ascending list of the pages any query page selected: each thread counts a contiguous
-    // range, one block scan places the ranges, then each thread writes its pages in order
-    using Scan = cub::BlockScan<int, 1024>;
-    __shared__ typename Scan::TempStorage tmp;
+    __syncthreads();
     const int per = (n_pages + 1023) / 1024;
-    const int p0 = min(n_pages, static_cast<int>(threadIdx.x) * per), p1 = min(n_pages, p0 + per);
+    const int p0 = min(n_pages, tid * per), p1 = min(n_pages, p0 + per);
     int cnt = 0;
     for (int p = p0; p < p1; ++p) cnt += mask[p] != 0ull;
     int pos, total;
     Scan(tmp).ExclusiveSum(cnt, pos, total);
     for (int p = p0; p < p1; ++p)
         if (mask[p] != 0ull) uni[pos++] = p;
-    if (threadIdx.x == 0) *n_uni = total;
-}
-
-// Order of the dK/dV work units, longest first (LPT), so the persistent grid does not end on a
-// long unit: unit codes [0, ncb) are the chunk's own key blocks (block b is attended by the
-// ncb - b query tiles from its diagonal on), codes ncb + k * bpp + sub the past blocks of the
-// k-th union page (attended by popcount(mask) query pages x tpq tiles each). Units write
-// disjoint gradient rows, so the order changes the schedule only, never a result bit.
-__global__ void __launch_bounds__(1024) bwd_order_kernel(const uint64_t* __restrict__ mask,
-                                                         const int32_t* __restrict__ uni,
-                                                         const int32_t* __restrict__ n_uni, int ncb, int bpp, int tpq,
-                                                         int32_t* __restrict__ order) {
-    constexpr int kKeys = 256;
-    __shared__ int hist[kKeys], cur[kKeys];
-    const int units = ncb + *n_uni * bpp;
-    for (int i = threadIdx.x; i < kKeys; i += blockDim.x) hist[i] = 0;
+    if (tid == 0) n_uni[0] = total;
+    if (!order) return;
     __syncthreads();
+    const int units = ncb + total * bpp;
     auto key = [&](int u) {
         const int k = u < ncb ? ncb - u : __popcll(mask[uni[(u - ncb) / bpp]]) * tpq;
         return min(k, kKeys - 1);
     };
-    for (int u = threadIdx.x; u < units; u += blockDim.x) atomicAdd(&hist[key(u)], 1);
+    for (int u = tid; u < units; u += 1024) atomicAdd(&hist[key(u)], 1);
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int pos = 0;
+    if (tid == 0) {
+        int at = 0;
         for (int k = kKeys - 1; k >= 0; --k) {
-            cur[k] = pos;
-            pos += hist[k];
+            cur[k] = at;
+            at += hist[k];
         }
     }
     __syncthreads();
-    for (int u = threadIdx.x; u < units; u += blockDim.x) order[atomicAdd(&cur[key(u)], 1)] = u;
+    for (int u = tid; u < units; u += 1024) order[atomicAdd(&cur[key(u)], 1)] = u;
 }
 
 // ===========================================================================
@@ -1149,21 +1157,12 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), lse, g.C, g.Hq, g.hd, w.Dt,
         w.Lt);
     check_launch("bwd_prep_kernel");
-    if (n_pages > 0) OOMB_CUDA(cudaMemsetAsync(w.mask, 0, static_cast<size_t>(n_pages) * 8, st));
-    OOMB_CUDA(cudaMemsetAsync(w.n_uni, 0, 2 * sizeof(int32_t), st));  // union count + dK/dV work counter
-    if (nnz > 0) {
-        bwd_mask_kernel<<<g.m, 128, 0, st>>>(sel_off, sel_ids, layer_pages(g), w.mask, d_err);
-        check_launch("bwd_mask_kernel");
-        bwd_union_kernel<<<1, 1024, 0, st>>>(w.mask, n_pages, w.uni, w.n_uni);
-        check_launch("bwd_union_kernel");
-    }
     // page size 64 pairs union pages per unit: kept in union order
     const bool lpt = OOMB_BWD_LPT && g.P != kHalf;
-    if (lpt) {
-        bwd_order_kernel<<<1, 1024, 0, st>>>(w.mask, w.uni, w.n_uni, g.chunk_keys ? g.C / kTile : 0,
-                                             bwd_blocks_per_page(g), std::max(1, g.P / kTile), w.order);
-        check_launch("bwd_order_kernel");
-    }
+    bwd_sched_kernel<<<1, 1024, 0, st>>>(sel_off, sel_ids, g.m, layer_pages(g), n_pages, w.mask, w.uni, w.n_uni,
+                                         g.chunk_keys ? g.C / kTile : 0, bwd_blocks_per_page(g),
+                                         std::max(1, g.P / kTile), lpt ? w.order : nullptr, d_err);
+    check_launch("bwd_sched_kernel");
     // head dim 64: the 128-wide tiles carry zeros in columns 64-127 (TMA out-of-bounds fill) and the
     // stores of those columns fall outside the tensors (clipped): see launch_attn_fwd_tc4
     const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, g.hd);

@@ -414,8 +414,8 @@ void launch_scatter(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, v
 template <typename A>
 __global__ void accumulate_grads_kernel(const int32_t* __restrict__ ids, int n, const int32_t* __restrict__ gslot,
                                         const A* __restrict__ gk, const A* __restrict__ gv, int64_t filled,
-                                        int P, int Hkv, int hd, A* __restrict__ dk, A* __restrict__ dv) {
-    const int re = Hkv * hd;
+                                        int P, int Hkv, int hd, A* __restrict__ dk, A* __restrict__ dv, int first) {
+    const int re = Hkv * hd;  // ids == null: the pages are first, first + 1, ... (a chunk's own pages)
     const int64_t total = static_cast<int64_t>(n) * P * re;
     for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -423,7 +423,7 @@ __global__ void accumulate_grads_kernel(const int32_t* __restrict__ ids, int n, 
         const int rem = static_cast<int>(idx - static_cast<int64_t>(i) * P * re);
         const int s = rem / re, e = rem - (rem / re) * re;
         const int h = e / hd, d = e - (e / hd) * hd;
-        const int pid = ids[i];
+        const int pid = ids ? ids[i] : first + i;
         const int g = gslot[pid];
         if (g < 0 || s >= valid_in_page(filled, pid, P)) continue;
         const size_t src = ((static_cast<size_t>(g) * Hkv + h) * P + s) * hd + d;
@@ -469,7 +469,7 @@ __global__ void accumulate_grads_rope_kernel(const int32_t* __restrict__ ids, in
 
 void launch_accumulate_grads(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, const void* gk_v,
                              const void* gv_v, int64_t filled, int P, int Hkv, int hd, void* dk_v, void* dv_v,
-                             cudaStream_t st, int64_t rope_pos0, const double* rope_inv_freq, bool f64) {
+                             cudaStream_t st, int64_t rope_pos0, const double* rope_inv_freq, bool f64, int first) {
     const float* gk = static_cast<const float*>(gk_v);
     const float* gv = static_cast<const float*>(gv_v);
     float* dk = static_cast<float*>(dk_v);
@@ -487,10 +487,10 @@ void launch_accumulate_grads(const int32_t* d_ids, int n, const int32_t* d_gslot
     if (f64)
         accumulate_grads_kernel<double><<<blocks, 256, 0, st>>>(d_ids, n, d_gslot_layer, static_cast<const double*>(gk_v),
                                                                 static_cast<const double*>(gv_v), filled, P, Hkv, hd,
-                                                                static_cast<double*>(dk_v), static_cast<double*>(dv_v));
+                                                                static_cast<double*>(dk_v), static_cast<double*>(dv_v), first);
     else
         accumulate_grads_kernel<float><<<blocks, 256, 0, st>>>(d_ids, n, d_gslot_layer, gk, gv, filled, P, Hkv, hd, dk,
-                                                               dv);
+                                                               dv, first);
     check_launch("accumulate_grads_kernel");
 }
 

@@ -1020,11 +1020,14 @@ int oomb_accumulate_grad_pages(oomb_pool_t p, int layer, const int32_t* ids, int
         // their partial dk / dv, which the range group sums (sharding.ShardedLayer.backward)
         p->pt->check_ids(layer, ids, n, p->enforce, "gather_grad_pages", /*allow_remote=*/true);
         if (n == 0) return;
-        int32_t* d = upload_ids(ids, n, S(stream));
+        // a consecutive run of pages (the dM_i read-back of a chunk's own pages) needs no id upload
+        bool run = true;
+        for (int i = 1; i < n && run; ++i) run = ids[i] == ids[0] + i;
+        int32_t* d = run ? nullptr : upload_ids(ids, n, S(stream));
         launch_accumulate_grads(d, n, p->gslot_layer(layer), p->gkpool, p->gvpool, p->pt->filled[layer],
                                 p->cfg.page_size, p->cfg.n_kv_heads, p->cfg.head_dim, dk, dv, S(stream), 0, nullptr,
-                                p->f64());
-        OOMB_CUDA(cudaFreeAsync(d, S(stream)));
+                                p->f64(), ids[0]);
+        if (d) OOMB_CUDA(cudaFreeAsync(d, S(stream)));
     });
 }
 

@@ -193,7 +193,7 @@ void launch_scatter(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, v
 void launch_accumulate_grads(const int32_t* d_ids, int n, const int32_t* d_gslot_layer, const void* gk,
                              const void* gv, int64_t filled, int P, int Hkv, int hd, void* dk, void* dv,
                              cudaStream_t st, int64_t rope_pos0 = 0,
-                             const double* rope_inv_freq = nullptr, bool f64 = false);
+                             const double* rope_inv_freq = nullptr, bool f64 = false, int first = 0);
 void launch_grad_init(const int32_t* d_pages, const int32_t* d_slots, int n, int32_t* d_gslot_layer, void* gk,
                       void* gv, int64_t page_elems, cudaStream_t st, int elem_bytes = 4);
 void launch_zero_slots(const int32_t* d_slots, int n, void* gk, void* gv, int64_t page_elems, cudaStream_t st,
