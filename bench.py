@@ -164,16 +164,19 @@ def low_locality_keys(run, seed: int = 77):
 def offload_measure(run, cap_frac: float, repeats: int = 5):
     """One layer step through the reference's residency protocol (AttentionChunkLoop +
     TieredEngine, chunk_trainer.hpp:328-363) with the device page pool capped at cap_frac of the
-    layer's pages, against the same loop with every page resident. Exposed copy % =
-    (wall capped - wall resident) / wall capped, from the MEDIAN of `repeats` alternating runs
-    (all runs reported); wall clock around a synchronized step (the protocol itself synchronizes
-    the host on every chunk's selection). Two data regimes: the bench's own N(0,1) keys, and
+    layer's pages, against the same protocol with an unlimited tier (every page resident, the same
+    host decisions, no copies). Exposed copy % = (capped - resident) / capped step time, from the
+    MEDIAN of `repeats` alternating runs (all runs reported). The step runs as one native call
+    (oomb_layer_step with the engine attached; OOMB_NATIVE_LOOP=0: the Python AttentionChunkLoop,
+    the same calls) and is timed with CUDA events on the compute stream, so the host's per-chunk
+    wait for the selection's ids shows up as idle time in both arms; the wall clock is reported
+    beside it. Two data regimes: the bench's own N(0,1) keys, and
     low-locality keys (low_locality_keys). The capped pool allocates only the tier capacity plus a
     small slack of device slots (the memory the offload saves is real), and the per-chunk union
     of selected pages and the pages the engine moved are reported."""
     import torch
     from paper_2602_02108_b200 import PagedCache
-    from paper_2602_02108_b200.chunk_loop import AttentionChunkLoop
+    from paper_2602_02108_b200.chunk_loop import AttentionChunkLoop, layer_stats, layer_step
     from paper_2602_02108_b200.tiered_memory import TierConfig, TieredEngine
     cfg, C, P = run.cfg, run.cfg["C"], run.cfg["P"]
     n_pages = cfg["T"] // P
@@ -188,36 +191,43 @@ def offload_measure(run, cap_frac: float, repeats: int = 5):
     def step(frac, K):
         use = frac < 1.0
         cache = PagedCache(run.mc, dtype="bf16", max_tokens=cfg["T"], device_capacity_pages=slots if use else -1)
-        eng = None
-        if use:
-            eng = TieredEngine(cache, TierConfig(device_capacity_pages=cap, bandwidth_bytes_per_s=55e9))
-            eng.set_prefetch_headroom_pages(C // P)
+        eng = TieredEngine(cache, TierConfig(device_capacity_pages=cap if use else -1, bandwidth_bytes_per_s=55e9))
+        eng.set_prefetch_headroom_pages(C // P)
         loop = AttentionChunkLoop(cache, engine=eng)
+        comp = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for i in range(run.S):
-            nq = run.q[(i + 1) % run.RQ] if i + 1 < run.S else None  # selection one chunk ahead
-            loop.forward_chunk(i, run.q[i % run.RQ], K[i * C:(i + 1) * C], run.v_all[i * C:(i + 1) * C],
-                               next_q=nq, out=run.o_all[i], lse=run.lse_all[i])
-        loop.begin_backward()
-        for i in reversed(range(run.S)):
-            loop.backward_chunk(i, run.do[i % run.RQ], run.q[i % run.RQ], K[i * C:(i + 1) * C],
-                                run.v_all[i * C:(i + 1) * C], grads=run.grads)
+        e0.record(comp)
+        if NATIVE_LOOP:  # the same protocol in one native call (oomb_layer_step with the engine attached)
+            kv = (run.S, C, cfg["Hkv"], cfg["hd"])
+            layer_step(cache, 0, run.q_all, K.view(kv), run.v_all.view(kv), run.do_all, run.o_all, run.lse_all,
+                       run.grads, mode=cfg["mode"])
+        else:
+            for i in range(run.S):
+                nq = run.q[(i + 1) % run.RQ] if i + 1 < run.S else None  # selection one chunk ahead
+                loop.forward_chunk(i, run.q[i % run.RQ], K[i * C:(i + 1) * C], run.v_all[i * C:(i + 1) * C],
+                                   next_q=nq, out=run.o_all[i], lse=run.lse_all[i])
+            loop.begin_backward()
+            for i in reversed(range(run.S)):
+                loop.backward_chunk(i, run.do[i % run.RQ], run.q[i % run.RQ], K[i * C:(i + 1) * C],
+                                    run.v_all[i * C:(i + 1) * C], grads=run.grads)
+        e1.record(comp)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-        out = {"wall_s": wall}
-        if eng is not None:
-            kv_page = cache.page_kv_bytes()
-            st = loop.chunk_stats
-            fw = [x for x in st if x[0] == "fwd" and x[1] > 0]
-            bw = [x for x in st if x[0] == "bwd"]
-            out.update(h2d_bytes=eng.h2d_bytes(0) + eng.h2d_bytes(1), d2h_bytes=eng.d2h_bytes(),
-                       fwd_union=[x[2] for x in fw], fwd_fetch_pages=[x[3] / kv_page for x in fw],
-                       bwd_h2d=[x[3] for x in bw], bwd_d2h=[x[4] for x in bw], device_bytes=slots * slot_bytes)
-            eng.release_all_reservations()
-            eng.close(discard=True)  # the measurement is over: host-tier pages are not needed
-        else:
-            out["device_bytes"] = n_pages * slot_bytes
+        # device time of the step on the compute stream (the host's per-chunk fetch decisions show up
+        # as idle gaps in it); the wall clock is reported beside it
+        out = {"wall_s": wall, "gpu_s": e0.elapsed_time(e1) / 1e3}
+        kv_page = cache.page_kv_bytes()
+        st = layer_stats(cache) if NATIVE_LOOP else loop.chunk_stats
+        fw = [x for x in st if x[0] == "fwd" and x[1] > 0]
+        bw = [x for x in st if x[0] == "bwd"]
+        out.update(h2d_bytes=eng.h2d_bytes(0) + eng.h2d_bytes(1), d2h_bytes=eng.d2h_bytes(),
+                   fwd_union=[x[2] for x in fw], fwd_fetch_pages=[x[3] / kv_page for x in fw],
+                   bwd_h2d=[x[3] for x in bw], bwd_d2h=[x[4] for x in bw],
+                   device_bytes=(slots if use else n_pages) * slot_bytes)
+        eng.release_all_reservations()
+        eng.close(discard=True)  # the measurement is over: host-tier pages are not needed
         del loop, eng, cache
         torch.cuda.empty_cache()
         return out
@@ -226,13 +236,16 @@ def offload_measure(run, cap_frac: float, repeats: int = 5):
         step(1.0, K)  # warm-up of the loop path
         step(cap_frac, K)  # and of the engine path (first pinned-tier use)
         runs = [(step(1.0, K), step(cap_frac, K)) for _ in range(repeats)]  # alternating
-        res = [r["wall_s"] for r, _ in runs]
-        off = [o["wall_s"] for _, o in runs]
+        res = [r["gpu_s"] for r, _ in runs]
+        off = [o["gpu_s"] for _, o in runs]
         o = runs[-1][1]
         mres, moff = statistics.median(res), statistics.median(off)
         fu = o["fwd_union"]
-        return {"wall_s_capped_runs": off, "wall_s_resident_runs": res,
-                "wall_s_capped_median": moff, "wall_s_resident_median": mres,
+        return {"step_s_capped_runs": off, "step_s_resident_runs": res,
+                "step_s_capped_median": moff, "step_s_resident_median": mres,
+                "wall_s_capped_runs": [x["wall_s"] for _, x in runs],
+                "wall_s_resident_runs": [x["wall_s"] for x, _ in runs],
+                "resident_moved_bytes": runs[-1][0]["h2d_bytes"] + runs[-1][0]["d2h_bytes"],
                 "exposed_pct": 100.0 * (moff - mres) / moff,
                 "exposed_pct_runs": [100.0 * (a - b) / a for a, b in zip(off, res)],
                 "h2d_bytes": o["h2d_bytes"], "d2h_bytes": o["d2h_bytes"],
@@ -254,7 +267,8 @@ def offload_measure(run, cap_frac: float, repeats: int = 5):
     return {"capacity_frac": cap_frac, "capacity_pages": cap, "device_slots": slots, "layer_pages": n_pages,
             "exposed_pct": bench_data["exposed_pct"], "h2d_bytes": bench_data["h2d_bytes"],
             "d2h_bytes": bench_data["d2h_bytes"], "bench_data": bench_data, "low_locality": lowloc,
-            "note": "exposed_pct = median capped vs median resident wall over alternating runs (all runs listed). "
+            "note": "exposed_pct = median capped vs median resident (unlimited tier, same protocol) step time, "
+                    "CUDA events on the compute stream, over alternating runs (all runs listed). "
                     "The capped pool holds capacity + slack device page slots (pool_bytes_capped vs "
                     "pool_bytes_resident). bench_data: the bench's N(0,1) keys, whose K_avg norms make a "
                     "shared hot set that LRU keeps resident; low_locality: every page mean at the same norm, "

@@ -249,9 +249,18 @@ OOMB_API int oomb_attn_backward_ex(oomb_pool_t pool, int layer, const void* dout
  * i * grad_stride_chunks of dq / dk_cur / dv_cur (grad_stride_chunks = 0: every chunk reuses block
  * 0). Selection of chunk i+1 overlaps chunk i's attention on a high-priority stream, consecutive
  * forwards run on two streams and dQ is deferred under the previous chunk's dK/dV: the same
- * results as the host loop, bitwise. Requires no attached TieredEngine and no page-range split
- * (those run their protocol in the host loop). flags: OOMB_LAYER_FORWARD_ONLY runs the forward
- * alone; OOMB_LAYER_BACKWARD_ONLY then runs the backward of that forward (its selections are kept). */
+ * results as the host loop, bitwise. Requires no page-range split (that runs in the host loop).
+ * With a TieredEngine attached (oomb_tier_create on this pool, `stream` = its compute stream) the
+ * step follows the residency protocol of chunk_trainer.hpp:328-363 / 409-462 / 531-592 exactly as
+ * AttentionChunkLoop does: per chunk, fetch of the selection's union -> append -> on_pages_appended
+ * -> wait + fill fetch + record_access -> attn_forward -> end_layer_use; backward after
+ * release_all + begin_phase(backward): fetch + record_access of union(sel) + own pages, a
+ * best-effort step-ahead prefetch of the previous chunk's, attn_backward (dQ not deferred: the
+ * engine's write-backs follow the compute stream), on_grads_scattered, dM_i read-back,
+ * end_layer_use. Every fetch decision waits for the selection's ids on the host; the selection of
+ * chunk i+1 still runs on the side stream under chunk i's work. flags: OOMB_LAYER_FORWARD_ONLY runs
+ * the forward alone; OOMB_LAYER_BACKWARD_ONLY then runs the backward of that forward (its
+ * selections are kept). */
 #define OOMB_MODE_DENSE 0
 #define OOMB_MODE_TOPK 1
 #define OOMB_MODE_LOCAL 2
@@ -261,6 +270,10 @@ OOMB_API int oomb_layer_step(oomb_pool_t pool, int layer, int n_chunks, int mode
                              const void* k, const void* v, const void* dout, int dout_cycle, void* out, void* lse,
                              void* dq, void* dk_cur, void* dv_cur, int64_t grad_stride_chunks, int flags,
                              void* stream);
+/* Per-chunk residency records of the pool's last engine-attached oomb_layer_step: *n records of 5
+ * int64 {phase (0 forward, 1 backward), chunk, pages the chunk needed resident, H2D bytes, D2H bytes
+ * the engine moved during the chunk}; the first min(*n, cap) are written to out (may be null). */
+OOMB_API int oomb_layer_stats(oomb_pool_t pool, int64_t* out, int64_t cap, int64_t* n);
 /* Make `stream` wait for the dq of every earlier oomb_attn_backward_ex(..., OOMB_ATTN_DEFER_DQ). */
 OOMB_API int oomb_attn_join_dq(oomb_pool_t pool, void* stream);
 OOMB_API int oomb_lse_merge(const void* o_parts, const float* lse_parts, int parts, int64_t rows, int hd, int dtype,

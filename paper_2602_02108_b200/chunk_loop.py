@@ -172,7 +172,10 @@ def layer_step(cache: PagedCache, layer: int, q, k, v, dout, out, lse, grads: A.
     block i % Rq), k / v: [S][C][Hkv][hd]; out [S][C][Hq][hd], lse [S][C][Hq]; grads.dq / dk_cur /
     dv_cur hold one chunk (grad_stride_chunks = 0: every chunk reuses it) or S chunks (= 1).
     phase: "both", "forward" (OOMB_LAYER_FORWARD_ONLY) or "backward" (the backward of the pool's
-    last forward of the same chunks, OOMB_LAYER_BACKWARD_ONLY)."""
+    last forward of the same chunks, OOMB_LAYER_BACKWARD_ONLY). With a TieredEngine attached to the
+    cache the native loop runs AttentionChunkLoop's residency protocol (forward_chunk /
+    begin_backward / backward_chunk with an engine) call for call; `stream` must then be the
+    engine's compute stream, and layer_stats() returns its per-chunk records."""
     cfg = cache.cfg
     mode = mode or cfg.mode_for_layer(layer)
     S = k.shape[0]
@@ -184,3 +187,14 @@ def layer_step(cache: PagedCache, layer: int, q, k, v, dout, out, lse, grads: A.
     call("oomb_layer_step", cache.handle, layer, S, MODES[mode], _ptr(q), q.shape[0], _ptr(k), _ptr(v), _ptr(dout),
          dout.shape[0], _ptr(out), _ptr(lse), _ptr(grads.dq), _ptr(grads.dk_cur), _ptr(grads.dv_cur),
          grad_stride_chunks, {"both": 0, "forward": 1, "backward": 2}[phase], stream_handle(stream))
+
+
+def layer_stats(cache: PagedCache) -> list[tuple[str, int, int, int, int]]:
+    """Per-chunk residency records of the cache's last engine-attached layer_step, in the format of
+    AttentionChunkLoop.chunk_stats: (phase, chunk, pages needed resident, H2D bytes, D2H bytes)."""
+    import ctypes as C
+    n = C.c_int64()
+    call("oomb_layer_stats", cache.handle, None, 0, C.byref(n))
+    buf = np.zeros((max(n.value, 1), 5), np.int64)
+    call("oomb_layer_stats", cache.handle, buf.ctypes.data_as(C.c_void_p), n.value, C.byref(n))
+    return [("fwd" if r[0] == 0 else "bwd", int(r[1]), int(r[2]), int(r[3]), int(r[4])) for r in buf[:n.value]]

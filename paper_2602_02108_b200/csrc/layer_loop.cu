@@ -39,6 +39,9 @@ struct LayerLoop {
     void* votes[2] = {nullptr, nullptr};
     int64_t vote_bytes = 0;
     int fwd_chunks = 0;  // chunks of the last forward (their selections are kept for the backward)
+    // engine path: host copies of selections and per-chunk residency records of the last step
+    std::vector<int32_t> h_off, h_ids;
+    std::vector<int64_t> stats;  // {phase, chunk, pages resident for the chunk, H2D bytes, D2H bytes}
     explicit LayerLoop(int device) {
         cudaSetDevice(device);
         int lo = 0, hi = 0;
@@ -68,10 +71,34 @@ void ok(int rc) {
     if (rc != OOMB_OK) throw Error(rc, oomb_last_error());
 }
 
+// Ascending distinct ids of a selection (waits for its host mirror): the chunk's residency working
+// set (AttentionChunkLoop.union). `extra_from` >= 0 adds the m own pages extra_from.. (union1d).
+std::vector<int32_t> sel_union(LayerLoop& L, oomb_selection_t s, int64_t extra_from = -1, int m = 0) {
+    int mq = 0, nnz = 0;
+    ok(oomb_selection_get_host(s, nullptr, nullptr, &mq, &nnz));
+    L.h_off.resize(static_cast<size_t>(mq) + 1);
+    L.h_ids.resize(static_cast<size_t>(std::max(nnz, 1)));
+    ok(oomb_selection_get_host(s, L.h_off.data(), L.h_ids.data(), &mq, &nnz));
+    std::vector<int32_t> u(L.h_ids.begin(), L.h_ids.begin() + nnz);
+    for (int j = 0; extra_from >= 0 && j < m; ++j) u.push_back(static_cast<int32_t>(extra_from + j));
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    return u;
+}
+
+void tier_io(oomb_tier_t t, int64_t* h2d, int64_t* d2h) {
+    double st[5];
+    ok(oomb_tier_stats(t, st));
+    *h2d = static_cast<int64_t>(st[2] + st[3]);
+    *d2h = static_cast<int64_t>(st[4]);
+}
+
 }  // namespace
 }  // namespace oomb
 
 using namespace oomb;
+
+extern "C" void* tier_compute_stream(oomb_tier_s* t);  // tier.cu (internal)
 
 extern "C" int oomb_layer_step(oomb_pool_t p, int layer, int n_chunks, int mode, const void* q, int q_cycle,
                                const void* k, const void* v, const void* dout, int dout_cycle, void* out, void* lse,
@@ -83,8 +110,9 @@ extern "C" int oomb_layer_step(oomb_pool_t p, int layer, int n_chunks, int mode,
         const oomb_config& c = p->cfg;
         OOMB_REQUIRE(n_chunks >= 1 && q_cycle >= 1 && dout_cycle >= 1, OOMB_SHAPE_ERROR, "layer_step: bad counts");
         OOMB_REQUIRE(mode >= OOMB_MODE_DENSE && mode <= OOMB_MODE_LOCAL, OOMB_CONFIG_ERROR, "layer_step: bad mode");
-        OOMB_REQUIRE(p->engine == nullptr, OOMB_STATE_ERROR,
-                     "layer_step: a TieredEngine is attached (its residency protocol runs in the host loop)");
+        oomb_tier_t eng = p->engine;
+        OOMB_REQUIRE(eng == nullptr || tier_compute_stream(eng) == stream, OOMB_STATE_ERROR,
+                     "layer_step: with a TieredEngine attached, `stream` must be the engine's compute stream");
         OOMB_REQUIRE(p->owner_stride == 1, OOMB_CONFIG_ERROR, "layer_step: page-range shards use the host loop");
         const int C = c.chunk_size, P = c.page_size, m = C / P;
         const int64_t qe = static_cast<int64_t>(C) * c.n_q_heads * c.head_dim;   // q / out / dout / dq per chunk
@@ -125,7 +153,97 @@ extern "C" int oomb_layer_step(oomb_pool_t p, int layer, int n_chunks, int mode,
         if (flags & OOMB_LAYER_BACKWARD_ONLY) {
             OOMB_REQUIRE(L.fwd_chunks >= n_chunks, OOMB_STATE_ERROR,
                          "layer_step: backward-only needs this pool's forward of the same chunks first");
-            goto backward;
+            if (!eng) goto backward;
+        }
+        if (!(flags & OOMB_LAYER_BACKWARD_ONLY)) L.stats.clear();
+        if (eng) {
+            // ---- forward under the residency protocol (AttentionChunkLoop.forward_chunk with an engine;
+            // chunk_trainer.hpp:328-363, 409-462): the selection of chunk i+1 is issued on the side
+            // stream right after chunk i's append; every fetch decision waits for the selection's ids.
+            // The attention runs on the engine's compute stream, which its write-backs follow.
+            auto fwd_engine = [&] {
+                ok(oomb_tier_begin_phase(eng, 0));
+                OOMB_CUDA(cudaEventRecord(L.ev_app[1], comp));
+                OOMB_CUDA(cudaStreamWaitEvent(L.sel, L.ev_app[1], 0));
+                auto select = [&](int i) {
+                    const void* qi = at(q, (i % q_cycle) * qe, el);
+                    const int n_cand = i * m;
+                    if (mode == OOMB_MODE_TOPK && n_cand > 0)
+                        ok(oomb_select_pages_topk(p, layer, qi, C, n_cand, L.sels[i], L.votes[i & 1], L.sel));
+                    else if (mode == OOMB_MODE_LOCAL && n_cand > 0)
+                        ok(oomb_select_recent(L.sels[i], n_cand, c.local_window, m, L.sel));
+                    else
+                        ok(oomb_select_all(L.sels[i], n_cand, m, L.sel));
+                    OOMB_CUDA(cudaEventRecord(L.ev_sel[i & 1], L.sel));
+                };
+                select(0);
+                for (int i = 0; i < n_chunks; ++i) {
+                    const void* qi = at(q, (i % q_cycle) * qe, el);
+                    const void* ki = at(k, i * ke, el);
+                    const void* vi = at(v, i * ke, el);
+                    OOMB_CUDA(cudaStreamWaitEvent(comp, L.ev_sel[i & 1], 0));
+                    int64_t h0 = 0, d0 = 0, h1 = 0, d1 = 0, hnd = 0, hnd2 = 0;
+                    tier_io(eng, &h0, &d0);
+                    std::vector<int32_t> ids = sel_union(L, L.sels[i]);
+                    const int n_ids = static_cast<int>(ids.size());
+                    ok(oomb_tier_fetch_async(eng, layer, ids.data(), n_ids, i, 0, &hnd));
+                    int64_t b = 0, e = 0;
+                    ok(oomb_append_chunk(p, layer, ki, vi, C, comp, &b, &e));
+                    if (i + 1 < n_chunks) {
+                        OOMB_CUDA(cudaEventRecord(L.ev_app[i & 1], comp));
+                        OOMB_CUDA(cudaStreamWaitEvent(L.sel, L.ev_app[i & 1], 0));
+                        select(i + 1);
+                    }
+                    ok(oomb_tier_on_pages_appended(eng, layer, b, e));
+                    ok(oomb_tier_wait(eng, hnd));
+                    ok(oomb_tier_fetch_async(eng, layer, ids.data(), n_ids, i, 0, &hnd2));
+                    ok(oomb_tier_wait(eng, hnd2));
+                    ok(oomb_tier_record_access(eng, layer, ids.data(), n_ids, i));
+                    ok(oomb_attn_forward_ex(p, layer, qi, C, L.sels[i], ki, vi, atw(out, i * qe, el),
+                                            atw(lse, static_cast<int64_t>(i) * C * c.n_q_heads, ae), 0, comp));
+                    for (int j = 0; j < m; ++j) ids.push_back(static_cast<int32_t>(i * m + j));
+                    ok(oomb_tier_end_layer_use(eng, layer, ids.data(), static_cast<int>(ids.size())));
+                    tier_io(eng, &h1, &d1);
+                    L.stats.insert(L.stats.end(), {0, i, n_ids, h1 - h0, d1 - d0});
+                }
+                OOMB_CUDA(cudaEventRecord(L.ev_sel[0], L.sel));
+                OOMB_CUDA(cudaStreamWaitEvent(comp, L.ev_sel[0], 0));
+                L.fwd_chunks = n_chunks;
+            };
+            auto bwd_engine = [&] {  // AttentionChunkLoop.begin_backward + backward_chunk with an engine
+                ok(oomb_tier_release_all(eng));
+                ok(oomb_tier_begin_phase(eng, 1));
+                for (int i = n_chunks - 1; i >= 0; --i) {
+                    const int64_t gi = grad_stride_chunks ? i : 0;
+                    void* dki = atw(dk_cur, gi * ke, ae);
+                    void* dvi = atw(dv_cur, gi * ke, ae);
+                    int64_t h0 = 0, d0 = 0, h1 = 0, d1 = 0, hnd = 0, pend = 0;
+                    tier_io(eng, &h0, &d0);
+                    std::vector<int32_t> ids = sel_union(L, L.sels[i], static_cast<int64_t>(i) * m, m);
+                    ok(oomb_tier_fetch_async(eng, layer, ids.data(), static_cast<int>(ids.size()), i, 0, &hnd));
+                    ok(oomb_tier_wait(eng, hnd));
+                    ok(oomb_tier_record_access(eng, layer, ids.data(), static_cast<int>(ids.size()), i));
+                    if (i > 0) {  // step-ahead prefetch: cached ids of the next (earlier) chunk + its own pages
+                        std::vector<int32_t> nxt = sel_union(L, L.sels[i - 1], static_cast<int64_t>(i - 1) * m, m);
+                        ok(oomb_tier_fetch_async(eng, layer, nxt.data(), static_cast<int>(nxt.size()), i - 1, 1, &pend));
+                    }
+                    ok(oomb_attn_backward_ex(p, layer, at(dout, (i % dout_cycle) * qe, el), at(q, (i % q_cycle) * qe, el),
+                                             C, L.sels[i], at(k, i * ke, el), at(v, i * ke, el), at(out, i * qe, el),
+                                             at(lse, static_cast<int64_t>(i) * C * c.n_q_heads, ae), atw(dq, gi * qe, ae),
+                                             dki, dvi, 0, comp));
+                    std::vector<int32_t> su = sel_union(L, L.sels[i]);
+                    ok(oomb_tier_on_grads_scattered(eng, layer, su.data(), static_cast<int>(su.size())));
+                    std::vector<int32_t> own(static_cast<size_t>(m));
+                    std::iota(own.begin(), own.end(), i * m);
+                    ok(oomb_accumulate_grad_pages(p, layer, own.data(), m, dki, dvi, comp));
+                    ok(oomb_tier_end_layer_use(eng, layer, ids.data(), static_cast<int>(ids.size())));
+                    tier_io(eng, &h1, &d1);
+                    L.stats.insert(L.stats.end(), {1, i, static_cast<int64_t>(ids.size()), h1 - h0, d1 - d0});
+                }
+            };
+            if (!(flags & OOMB_LAYER_BACKWARD_ONLY)) fwd_engine();
+            if (!(flags & OOMB_LAYER_FORWARD_ONLY)) bwd_engine();
+            return;
         }
         // ---- forward
         OOMB_CUDA(cudaEventRecord(L.ev_app[1], comp));  // earlier work precedes this step's selections
@@ -178,5 +296,17 @@ extern "C" int oomb_layer_step(oomb_pool_t p, int layer, int n_chunks, int mode,
             ok(oomb_accumulate_grad_pages(p, layer, own.data(), m, dki, dvi, comp));
         }
         ok(oomb_attn_join_dq(p, comp));
+    });
+}
+
+extern "C" int oomb_layer_stats(oomb_pool_t p, int64_t* out, int64_t cap, int64_t* n) {
+    return guard([&] {
+        OOMB_REQUIRE(p != nullptr && n != nullptr, OOMB_STATE_ERROR, "layer_stats: null argument");
+        const auto* L = static_cast<const LayerLoop*>(p->loop_state.get());
+        const int64_t recs = L ? static_cast<int64_t>(L->stats.size() / 5) : 0;
+        *n = recs;
+        if (out)
+            for (int64_t r = 0; r < std::min(recs, cap); ++r)
+                for (int j = 0; j < 5; ++j) out[r * 5 + j] = L->stats[static_cast<size_t>(r * 5 + j)];
     });
 }

@@ -627,6 +627,9 @@ void tier_orphan(oomb_tier_s* t) {
     t->pt = nullptr;
 }
 
+// (internal, hidden) the stream the engine orders its write-backs after and its fetch waits into
+void* tier_compute_stream(oomb_tier_s* t) { return t->compute; }
+
 int oomb_tier_create_sim(oomb_pagetable_t pt, const oomb_tier_config* cfg, oomb_tier_t* out) {
     return guard([&] {
         OOMB_REQUIRE(cfg->bandwidth_bytes_per_s > 0, OOMB_CONFIG_ERROR, "tiered_memory: bandwidth must be positive");

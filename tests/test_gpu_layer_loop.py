@@ -36,3 +36,70 @@ def test_native_loop_bitwise(name):
     bench.NATIVE_LOOP = True
     for a, b, what in zip(res[False], res[True], ("out", "lse", "dq", "dk_cur", "dv_cur", "grad_k", "grad_v")):
         assert torch.equal(a, b), (name, what)
+
+
+def _engine_run(run, K, native, cap, slots):
+    """One layer step under the residency protocol: the Python AttentionChunkLoop + TieredEngine
+    (bench.offload_measure's loop) or the native loop with the same engine attached."""
+    import bench
+    from paper_2602_02108_b200 import PagedCache
+    from paper_2602_02108_b200.chunk_loop import AttentionChunkLoop, layer_stats, layer_step
+    from paper_2602_02108_b200.tiered_memory import TierConfig, TieredEngine
+    cfg, C = run.cfg, run.cfg["C"]
+    cache = PagedCache(run.mc, dtype="bf16", max_tokens=cfg["T"], device_capacity_pages=slots)
+    eng = TieredEngine(cache, TierConfig(device_capacity_pages=cap, bandwidth_bytes_per_s=55e9))
+    eng.set_prefetch_headroom_pages(C // cfg["P"])
+    run.o_all.zero_()
+    run.lse_all.zero_()
+    if native:
+        kv = (run.S, C, cfg["Hkv"], cfg["hd"])
+        layer_step(cache, 0, run.q_all, K.view(kv), run.v_all.view(kv), run.do_all, run.o_all, run.lse_all,
+                   run.grads, mode=cfg["mode"])
+        stats = layer_stats(cache)
+    else:
+        loop = AttentionChunkLoop(cache, engine=eng)
+        for i in range(run.S):
+            nq = run.q[(i + 1) % run.RQ] if i + 1 < run.S else None
+            loop.forward_chunk(i, run.q[i % run.RQ], K[i * C:(i + 1) * C], run.v_all[i * C:(i + 1) * C],
+                               next_q=nq, out=run.o_all[i], lse=run.lse_all[i])
+        loop.begin_backward()
+        for i in reversed(range(run.S)):
+            loop.backward_chunk(i, run.do[i % run.RQ], run.q[i % run.RQ], K[i * C:(i + 1) * C],
+                                run.v_all[i * C:(i + 1) * C], grads=run.grads)
+        stats = loop.chunk_stats
+    torch.cuda.synchronize()
+    cache.check_device_errors()
+    io = (eng.h2d_bytes(0), eng.h2d_bytes(1), eng.d2h_bytes())
+    eng.release_all_reservations()
+    eng.restore_all()  # every page back on the device (the pool has a slot for each) to compare grads
+    n = cache.n_pages(0)
+    gp = cache.gather_grad_pages(0, list(range(n)))
+    res = [run.o_all.clone(), run.lse_all.clone(), run.grads.dq.clone(), run.grads.dk_cur.clone(),
+           run.grads.dv_cur.clone(), gp.k.clone(), gp.v.clone()]
+    eng.close(discard=True)
+    del cache
+    assert bench is not None
+    return res, stats, io
+
+
+@pytest.mark.parametrize("regime", ["bench_data", "low_locality"])
+def test_native_loop_with_engine_matches_host_loop(regime):
+    """The native loop with a TieredEngine attached makes the host loop's engine calls: the same
+    outputs and gradients bit for bit, the same per-chunk resident-page counts and the same bytes
+    moved, with the tier capped at 75 % of the layer's pages (pages really leave the device)."""
+    import bench
+    cfg = dict(bench.CONFIGS["c3"])
+    # low locality: 64 chunks, so a chunk's working set (the union of 32 near-random top-64 lists
+    # plus its own pages) stays under the 75 % tier (at 16 chunks it approaches every page)
+    cfg["T"] = (16 if regime == "bench_data" else 64) * 4096
+    run = bench.Run(cfg, seed=4321, device=torch.device("cuda", 0))
+    K = run.k_all if regime == "bench_data" else bench.low_locality_keys(run)
+    n_pages = cfg["T"] // cfg["P"]
+    cap = int(0.75 * n_pages)
+    host = _engine_run(run, K, False, cap, n_pages)
+    nat = _engine_run(run, K, True, cap, n_pages)
+    for a, b, what in zip(host[0], nat[0], ("out", "lse", "dq", "dk_cur", "dv_cur", "grad_k", "grad_v")):
+        assert torch.equal(a, b), (regime, what)
+    assert host[1] == nat[1]
+    assert host[2] == nat[2]
+    assert host[2][0] > 0 and host[2][2] > 0, "the capped tier must move pages both ways"
