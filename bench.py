@@ -188,7 +188,7 @@ def offload_measure(run, cap_frac: float, repeats: int = 5):
     # device bytes of one page slot: K + V (bf16) and the dK + dV gradient block (fp32)
     slot_bytes = P * cfg["Hkv"] * cfg["hd"] * (2 * 2 + 2 * 4)
 
-    def step(frac, K):
+    def step(frac, K, slots=slots):
         use = frac < 1.0
         cache = PagedCache(run.mc, dtype="bf16", max_tokens=cfg["T"], device_capacity_pages=slots if use else -1)
         eng = TieredEngine(cache, TierConfig(device_capacity_pages=cap if use else -1, bandwidth_bytes_per_s=55e9))
@@ -223,6 +223,7 @@ def offload_measure(run, cap_frac: float, repeats: int = 5):
         fw = [x for x in st if x[0] == "fwd" and x[1] > 0]
         bw = [x for x in st if x[0] == "bwd"]
         out.update(h2d_bytes=eng.h2d_bytes(0) + eng.h2d_bytes(1), d2h_bytes=eng.d2h_bytes(),
+                   h2d_bytes_moved=eng.h2d_bytes_moved(),
                    fwd_union=[x[2] for x in fw], fwd_fetch_pages=[x[3] / kv_page for x in fw],
                    bwd_h2d=[x[3] for x in bw], bwd_d2h=[x[4] for x in bw],
                    device_bytes=(slots if use else n_pages) * slot_bytes)
@@ -232,10 +233,10 @@ def offload_measure(run, cap_frac: float, repeats: int = 5):
         torch.cuda.empty_cache()
         return out
 
-    def regime(K):
+    def regime(K, slots=slots):
         step(1.0, K)  # warm-up of the loop path
-        step(cap_frac, K)  # and of the engine path (first pinned-tier use)
-        runs = [(step(1.0, K), step(cap_frac, K)) for _ in range(repeats)]  # alternating
+        step(cap_frac, K, slots)  # and of the engine path (first pinned-tier use)
+        runs = [(step(1.0, K), step(cap_frac, K, slots)) for _ in range(repeats)]  # alternating
         res = [r["gpu_s"] for r, _ in runs]
         off = [o["gpu_s"] for _, o in runs]
         o = runs[-1][1]
@@ -248,7 +249,7 @@ def offload_measure(run, cap_frac: float, repeats: int = 5):
                 "resident_moved_bytes": runs[-1][0]["h2d_bytes"] + runs[-1][0]["d2h_bytes"],
                 "exposed_pct": 100.0 * (moff - mres) / moff,
                 "exposed_pct_runs": [100.0 * (a - b) / a for a, b in zip(off, res)],
-                "h2d_bytes": o["h2d_bytes"], "d2h_bytes": o["d2h_bytes"],
+                "h2d_bytes": o["h2d_bytes"], "d2h_bytes": o["d2h_bytes"], "h2d_bytes_moved": o["h2d_bytes_moved"],
                 "fwd_union_pages_per_chunk": {"mean": statistics.mean(fu), "median": statistics.median(fu),
                                               "max": max(fu), "last": fu[-1]} if fu else None,
                 "fwd_fetched_pages_per_chunk": {"mean": statistics.mean(o["fwd_fetch_pages"]),
@@ -258,22 +259,35 @@ def offload_measure(run, cap_frac: float, repeats: int = 5):
                 "pool_bytes_capped": o["device_bytes"], "pool_bytes_resident": runs[-1][0]["device_bytes"]}
 
     bench_data = regime(run.k_all)
-    lowloc = None
+    lowloc, sweep = None, []
     if cfg["mode"] == "topk":
         K = low_locality_keys(run)
         lowloc = regime(K)
+        # more physical slots than the tier's capacity: the extra slots keep evicted pages' data as
+        # victims (a page fetched back before its slot is reused moves nothing), trading device memory
+        # for copies at the same engine decisions
+        for extra in (2, 3):
+            sl = min(n_pages, cap + extra * slack)
+            if sl < n_pages:
+                r = regime(K, sl)
+                sweep.append({"device_slots": sl, "pool_bytes": sl * slot_bytes, "exposed_pct": r["exposed_pct"],
+                              "exposed_pct_runs": r["exposed_pct_runs"], "h2d_bytes_moved": r["h2d_bytes_moved"]})
         del K
         torch.cuda.empty_cache()
     return {"capacity_frac": cap_frac, "capacity_pages": cap, "device_slots": slots, "layer_pages": n_pages,
             "exposed_pct": bench_data["exposed_pct"], "h2d_bytes": bench_data["h2d_bytes"],
             "d2h_bytes": bench_data["d2h_bytes"], "bench_data": bench_data, "low_locality": lowloc,
+            "low_locality_slot_sweep": sweep,
             "note": "exposed_pct = median capped vs median resident (unlimited tier, same protocol) step time, "
                     "CUDA events on the compute stream, over alternating runs (all runs listed). "
                     "The capped pool holds capacity + slack device page slots (pool_bytes_capped vs "
                     "pool_bytes_resident). bench_data: the bench's N(0,1) keys, whose K_avg norms make a "
                     "shared hot set that LRU keeps resident; low_locality: every page mean at the same norm, "
                     "near-random selections. Pinned-host page moves on side streams (one batched copy per "
-                    "engine operation); each chunk's selection is issued one chunk ahead."}
+                    "engine operation); each chunk's selection is issued one chunk ahead. h2d_bytes counts every "
+                    "fetch decision (the reference's accounting); h2d_bytes_moved what was copied (a page fetched "
+                    "back into its not-yet-reused victim slots moves nothing). low_locality_slot_sweep: the same "
+                    "tier capacity with more physical slots."}
 
 
 # ---------------------------------------------------------------------------

@@ -19,6 +19,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <numeric>
 #include <vector>
@@ -99,6 +102,7 @@ void tier_io(oomb_tier_t t, int64_t* h2d, int64_t* d2h) {
 using namespace oomb;
 
 extern "C" void* tier_compute_stream(oomb_tier_s* t);  // tier.cu (internal)
+extern "C" void* tier_t0(oomb_tier_s* t);              // tier.cu (internal)
 
 extern "C" int oomb_layer_step(oomb_pool_t p, int layer, int n_chunks, int mode, const void* q, int q_cycle,
                                const void* k, const void* v, const void* dout, int dout_cycle, void* out, void* lse,
@@ -213,24 +217,45 @@ extern "C" int oomb_layer_step(oomb_pool_t p, int layer, int n_chunks, int mode,
             auto bwd_engine = [&] {  // AttentionChunkLoop.begin_backward + backward_chunk with an engine
                 ok(oomb_tier_release_all(eng));
                 ok(oomb_tier_begin_phase(eng, 1));
+                // OOMB_LOOP_TIMELINE=<file>: every chunk's backward start / end on the compute stream in ms
+                // from the engine log's origin (diagnostics of the copy / compute overlap)
+                const char* tl_path = std::getenv("OOMB_LOOP_TIMELINE");
+                std::vector<cudaEvent_t> tl;
+                std::vector<double> th;  // host ms: fetch + wait + record_access, prefetch, attn_backward, rest
+                auto now_ms = [] {
+                    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch())
+                        .count();
+                };
+                auto mark = [&] {
+                    if (!tl_path) return;
+                    tl.emplace_back();
+                    OOMB_CUDA(cudaEventCreate(&tl.back()));
+                    OOMB_CUDA(cudaEventRecord(tl.back(), comp));
+                };
                 for (int i = n_chunks - 1; i >= 0; --i) {
                     const int64_t gi = grad_stride_chunks ? i : 0;
                     void* dki = atw(dk_cur, gi * ke, ae);
                     void* dvi = atw(dv_cur, gi * ke, ae);
                     int64_t h0 = 0, d0 = 0, h1 = 0, d1 = 0, hnd = 0, pend = 0;
+                    const double hs0 = tl_path ? now_ms() : 0;
                     tier_io(eng, &h0, &d0);
                     std::vector<int32_t> ids = sel_union(L, L.sels[i], static_cast<int64_t>(i) * m, m);
                     ok(oomb_tier_fetch_async(eng, layer, ids.data(), static_cast<int>(ids.size()), i, 0, &hnd));
                     ok(oomb_tier_wait(eng, hnd));
                     ok(oomb_tier_record_access(eng, layer, ids.data(), static_cast<int>(ids.size()), i));
+                    const double hs1 = tl_path ? now_ms() : 0;
                     if (i > 0) {  // step-ahead prefetch: cached ids of the next (earlier) chunk + its own pages
                         std::vector<int32_t> nxt = sel_union(L, L.sels[i - 1], static_cast<int64_t>(i - 1) * m, m);
                         ok(oomb_tier_fetch_async(eng, layer, nxt.data(), static_cast<int>(nxt.size()), i - 1, 1, &pend));
                     }
+                    const double hs2 = tl_path ? now_ms() : 0;
+                    mark();
                     ok(oomb_attn_backward_ex(p, layer, at(dout, (i % dout_cycle) * qe, el), at(q, (i % q_cycle) * qe, el),
                                              C, L.sels[i], at(k, i * ke, el), at(v, i * ke, el), at(out, i * qe, el),
                                              at(lse, static_cast<int64_t>(i) * C * c.n_q_heads, ae), atw(dq, gi * qe, ae),
                                              dki, dvi, 0, comp));
+                    mark();
+                    const double hs3 = tl_path ? now_ms() : 0;
                     std::vector<int32_t> su = sel_union(L, L.sels[i]);
                     ok(oomb_tier_on_grads_scattered(eng, layer, su.data(), static_cast<int>(su.size())));
                     std::vector<int32_t> own(static_cast<size_t>(m));
@@ -239,6 +264,23 @@ extern "C" int oomb_layer_step(oomb_pool_t p, int layer, int n_chunks, int mode,
                     ok(oomb_tier_end_layer_use(eng, layer, ids.data(), static_cast<int>(ids.size())));
                     tier_io(eng, &h1, &d1);
                     L.stats.insert(L.stats.end(), {1, i, static_cast<int64_t>(ids.size()), h1 - h0, d1 - d0});
+                    if (tl_path) th.insert(th.end(), {hs1 - hs0, hs2 - hs1, hs3 - hs2, now_ms() - hs3});
+                }
+                if (tl_path) {
+                    OOMB_CUDA(cudaStreamSynchronize(comp));
+                    auto t0 = static_cast<cudaEvent_t>(tier_t0(eng));
+                    if (FILE* f = std::fopen(tl_path, "w")) {
+                        for (size_t j = 0; j + 1 < tl.size(); j += 2) {
+                            float ta = 0, tb = 0;
+                            cudaEventElapsedTime(&ta, t0, tl[j]);
+                            cudaEventElapsedTime(&tb, t0, tl[j + 1]);
+                            const double* h = th.data() + 4 * (j / 2);
+                            std::fprintf(f, "%d %.4f %.4f %.4f %.4f %.4f %.4f\n", n_chunks - 1 - static_cast<int>(j / 2),
+                                         ta, tb, h[0], h[1], h[2], h[3]);
+                        }
+                        std::fclose(f);
+                    }
+                    for (auto e_ : tl) cudaEventDestroy(e_);
                 }
             };
             if (!(flags & OOMB_LAYER_BACKWARD_ONLY)) fwd_engine();

@@ -137,12 +137,10 @@ void validate_cfg(const oomb_config& c) {  // ModelConfig::validate (config.cpp:
 }
 
 
-int32_t pop_slot(std::deque<int32_t>& fl, const char* what) {
-    OOMB_REQUIRE(!fl.empty(), OOMB_CONFIG_ERROR,
+int32_t pop_slot(oomb_pool_s* p, bool grad, const char* what) {
+    OOMB_REQUIRE(!(grad ? p->g_free : p->kv_free).empty(), OOMB_CONFIG_ERROR,
                  std::string("device ") + what + " capacity exhausted (raise device_capacity_pages or offload)");
-    const int32_t s = fl.front();
-    fl.pop_front();
-    return s;
+    return p->pop_free(grad);
 }
 
 // Copy a small host int32 array into a stream-ordered temporary device buffer.
@@ -189,8 +187,8 @@ void ensure_grad_pages(oomb_pool_s* p, int layer, const int32_t* h_off, const in
         if (n == 0) continue;
         p->pt->check_ids(layer, h_ids + h_off[qp], n, p->enforce, "scatter_add_grads");
         for (int32_t pid : p->pt->scatter(layer, h_ids + h_off[qp], n)) {
-            const int32_t gs = pop_slot(p->g_free, "gradient page");
-            p->wait_slot(true, gs, st);
+            const int32_t gs = pop_slot(p, true, "gradient page");
+            p->compute_ticket_waits += p->wait_slot(true, gs, st);
             p->gslot[layer][pid] = gs;
             pages.push_back(pid);
             slots.push_back(gs);
@@ -408,6 +406,7 @@ int oomb_pool_reset(oomb_pool_t p, void* stream) {
             }
         }
         p->pt->reset();
+        p->clear_holders();  // freed slots hold no page of the new sequence
         const size_t tab = static_cast<size_t>(p->cfg.n_layers) * p->max_pages * sizeof(int32_t);
         OOMB_CUDA(cudaMemsetAsync(p->d_kvslot, 0xFF, tab, S(stream)));
         OOMB_CUDA(cudaMemsetAsync(p->d_gslot, 0xFF, tab, S(stream)));
@@ -490,8 +489,8 @@ static int append_impl(oomb_pool_t p, int layer, const void* k, const void* v, i
                 p->pt->pages[layer][pg].tier = TIER_REMOTE;
                 continue;
             }
-            const int32_t s = pop_slot(p->kv_free, "KV page");
-            p->wait_slot(false, s, S(stream));  // a recycled slot may still be draining to the host
+            const int32_t s = pop_slot(p, false, "KV page");
+            p->compute_ticket_waits += p->wait_slot(false, s, S(stream));  // a recycled slot may still be draining
             p->kvslot[layer][pg] = s;
         }
         *slot_begin = b;
@@ -971,15 +970,14 @@ int oomb_attn_backward_ex(oomb_pool_t p, int layer, const void* dout, const void
             const int b = p->bwd_parity;
             p->bwd_parity ^= 1;
             const size_t need = attn_bwd_tc_workspace(g, sel->nnz);
-            if (need > p->bwd_ws_bytes[b]) {
-                OOMB_CUDA(cudaDeviceSynchronize());  // a deferred dQ may still read the old workspace
-                cudaFree(p->bwd_ws[b]);
-                p->bwd_ws[b] = nullptr;
-                OOMB_CUDA(cudaMalloc(&p->bwd_ws[b], need));
-                p->bwd_ws_bytes[b] = need;
-            }
             // the dQ that last used this workspace has finished reading it
             if (p->bwd_ws_used[b]) OOMB_CUDA(cudaStreamWaitEvent(S(stream), p->bwd_ev_dq[b], 0));
+            if (need > p->bwd_ws_bytes[b]) {  // regrow in stream order: no device-wide synchronisation
+                if (p->bwd_ws[b]) OOMB_CUDA(cudaFreeAsync(p->bwd_ws[b], S(stream)));
+                p->bwd_ws[b] = nullptr;
+                OOMB_CUDA(cudaMallocAsync(&p->bwd_ws[b], need, S(stream)));
+                p->bwd_ws_bytes[b] = need;
+            }
             launch_attn_bwd_tc(g, p->maps, dout, q, sel->d_off, sel->d_ids, p->kvslot_layer(layer),
                                p->gslot_layer(layer), p->gkpool, p->gvpool, k_cur, v_cur, out,
                                static_cast<const float*>(lse), static_cast<float*>(dq), static_cast<float*>(dk_cur),

@@ -224,10 +224,43 @@ struct oomb_pool_s {
     // (and at most once per newer batch).
     std::vector<uint64_t> kv_ticket, g_ticket;
     uint64_t wb_ticket = 0;                                    // newest write-back batch
+    int64_t compute_ticket_waits = 0;                          // diagnostics: waits put on a compute stream
     uint64_t wb_completed = 0;                                 // every batch <= this has drained
     std::deque<std::pair<uint64_t, cudaEvent_t>> wb_events;    // batches not yet seen complete
     std::vector<cudaEvent_t> wb_spare;
     std::vector<std::pair<cudaStream_t, uint64_t>> waited;     // newest batch each stream has waited for
+
+    // Victim slots (offload engine): a slot freed by an eviction keeps the evicted page's data until
+    // it is handed out again; `holder` names that page (layer * max_pages + page, -1: none). A fetch
+    // of the page before then takes the slot back off the free list instead of copying the page in.
+    std::vector<int64_t> kv_holder, g_holder;
+    void set_holder(bool grad, int32_t s, int64_t idx) {
+        auto& h = grad ? g_holder : kv_holder;
+        if (h.empty()) h.assign(grad ? n_g_slots : n_kv_slots, -1);
+        h[s] = idx;
+    }
+    int32_t pop_free(bool grad) {  // the oldest free slot (FIFO), no longer holding any page's data
+        auto& fl = grad ? g_free : kv_free;
+        const int32_t s = fl.front();
+        fl.pop_front();
+        auto& h = grad ? g_holder : kv_holder;
+        if (!h.empty()) h[s] = -1;
+        return s;
+    }
+    bool reclaim(bool grad, int32_t s, int64_t idx) {  // take victim slot s back for page idx
+        auto& h = grad ? g_holder : kv_holder;
+        if (s < 0 || h.empty() || h[s] != idx) return false;
+        auto& fl = grad ? g_free : kv_free;
+        const auto it = std::find(fl.begin(), fl.end(), s);
+        if (it == fl.end()) return false;
+        fl.erase(it);
+        h[s] = -1;
+        return true;
+    }
+    void clear_holders() {
+        kv_holder.clear();
+        g_holder.clear();
+    }
 
     void free_slot_after_writeback(bool grad, int32_t s) {
         auto& v = grad ? g_ticket : kv_ticket;
@@ -255,25 +288,26 @@ struct oomb_pool_s {
             wb_events.pop_front();
         }
     }
-    void wait_slot(bool grad, int32_t s, cudaStream_t st) {
+    bool wait_slot(bool grad, int32_t s, cudaStream_t st) {
         const auto& v = grad ? g_ticket : kv_ticket;
-        if (!v.empty()) wait_ticket(v[s], st);
+        return !v.empty() && wait_ticket(v[s], st);
     }
     // Make stream st wait until write-back batch t has drained (no-op when it has, or when st
     // already waited for a batch >= t).
-    void wait_ticket(uint64_t t, cudaStream_t st) {
-        if (t <= wb_completed) return;
+    bool wait_ticket(uint64_t t, cudaStream_t st) {  // true: st now waits on a pending batch
+        if (t <= wb_completed) return false;
         retire_writebacks();
-        if (t <= wb_completed) return;
+        if (t <= wb_completed) return false;
         auto it = std::find_if(waited.begin(), waited.end(), [&](const auto& w) { return w.first == st; });
-        if (it != waited.end() && it->second >= t) return;
+        if (it != waited.end() && it->second >= t) return false;
         for (const auto& b : wb_events)
             if (b.first >= t) {  // the first pending batch at or after the slot's: covers it (in-order stream)
                 OOMB_CUDA(cudaStreamWaitEvent(st, b.second, 0));
                 if (it != waited.end()) it->second = b.first;
                 else waited.emplace_back(st, b.first);
-                return;
+                return true;
             }
+        return false;
     }
     void destroy_writeback_events() {
         for (auto& b : wb_events) cudaEventDestroy(b.second);

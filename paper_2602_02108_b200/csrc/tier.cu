@@ -22,6 +22,8 @@
 // validate_schedule checks residency-before-use on the real GPU timeline.
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -65,6 +67,7 @@ struct oomb_tier_s {
         bool host_has_kv = false;    // real mode: host block holds data
         bool host_has_grad = false;
         uint64_t wb_batch = 0;       // real mode: the write-back batch that last filled the host block
+        int32_t vkv = -1, vg = -1;   // real mode: the slots the page was evicted from (victim slots)
     };
     struct Transfer {
         int layer = 0;
@@ -91,6 +94,10 @@ struct oomb_tier_s {
 
     // ---- real mode
     cudaStream_t compute = nullptr, h2d_stream = nullptr, d2h_stream = nullptr;
+    // OOMB_TIER_DEBUG counters: best-effort issued / refused, pages prefetched / fetched on demand,
+    // H2D waits on a page's own pending write-back, H2D waits on a recycled slot's write-back
+    int64_t dbg[6] = {};
+    uint64_t h2d_moved = 0;  // real mode: bytes actually copied in (victim-slot reclaims move none)
     cudaEvent_t t0 = nullptr;
     std::vector<cudaEvent_t> spare_events;
     uint8_t* host_kv = nullptr;    // pinned [layer][page] x (K, V) blocks
@@ -331,11 +338,15 @@ struct oomb_tier_s {
         if (ks >= 0) {
             p.free_slot_after_writeback(false, ks);
             p.kv_free.push_back(ks);
+            p.set_holder(false, ks, static_cast<int64_t>(hidx));
         }
         if (gs >= 0) {
             p.free_slot_after_writeback(true, gs);
             p.g_free.push_back(gs);
+            p.set_holder(true, gs, static_cast<int64_t>(hidx));
         }
+        ps.vkv = ks;
+        ps.vg = gs;
         p.kvslot[layer][page] = -1;
         p.gslot[layer][page] = -1;
         queue_table(layer, page);
@@ -347,9 +358,8 @@ struct oomb_tier_s {
                      std::string("offload: no free device ") + what +
                          " slot for an in-flight fetch (raise the pool's device_capacity_pages above the tier "
                          "capacity)");
-        const int32_t s = fl.front();
-        fl.pop_front();
-        pool->wait_slot(grad, s, st);
+        const int32_t s = pool->pop_free(grad);
+        dbg[5] += pool->wait_slot(grad, s, st);
         return s;
     }
 
@@ -365,18 +375,32 @@ struct oomb_tier_s {
         OOMB_REQUIRE(ps.host_has_kv, OOMB_STATE_ERROR,
                      "offload: page " + std::to_string(page) + " of layer " + std::to_string(layer) +
                          " is host-tier but its host block holds no data");
-        p.wait_ticket(ps.wb_batch, h2d_stream);
-        const int32_t ks = take_slot(false, h2d_stream, "KV");
+        // A page whose victim slots were not handed out since its eviction still has its data there
+        // (the write-back only reads them): it takes them back, no copy and no wait for the read-out.
+        // A later write into a reclaimed slot (scatter, append) marks the host copy stale, so a torn
+        // read-out is always written again before the host block is used.
+        const int64_t idx = static_cast<int64_t>(hidx);
+        const bool g_need = grads_allocated(layer, page);
+        const int32_t vkv = ps.vkv, vg = ps.vg;
+        ps.vkv = ps.vg = -1;
+        const bool kv_back = p.reclaim(false, vkv, idx);
+        const bool g_back = g_need && p.reclaim(true, vg, idx);
+        if (!kv_back || (g_need && !g_back && ps.host_has_grad)) dbg[4] += p.wait_ticket(ps.wb_batch, h2d_stream);
+        const int32_t ks = kv_back ? vkv : take_slot(false, h2d_stream, "KV");
         p.kvslot[layer][page] = ks;
-        if (ps.host_has_kv) {
+        if (!kv_back && ps.host_has_kv) {
             const uint8_t* h = host_kv + hidx * kv_block;
             queue_copy(0, static_cast<uint8_t*>(p.kpool) + ks * kvb, h, kvb);
             queue_copy(0, static_cast<uint8_t*>(p.vpool) + ks * kvb, h + kvb, kvb);
+            h2d_moved += 2 * kvb;
         }
-        if (grads_allocated(layer, page)) {
+        if (g_back) {
+            p.gslot[layer][page] = vg;
+        } else if (g_need) {
             const int32_t gs = take_slot(true, h2d_stream, "gradient");
             p.gslot[layer][page] = gs;
             if (ps.host_has_grad) {
+                h2d_moved += 2 * gb;
                 const uint8_t* h = host_grad + hidx * grad_block;
                 queue_copy(0, reinterpret_cast<uint8_t*>(p.gkpool) + gs * gb, h, gb);
                 queue_copy(0, reinterpret_cast<uint8_t*>(p.gvpool) + gs * gb, h + gb, gb);
@@ -440,7 +464,9 @@ struct oomb_tier_s {
         if (best_effort) {
             const int64_t hr = phase == 0 ? headroom : 0;
             const int64_t demand = static_cast<int64_t>(to_transfer.size()) + static_cast<int64_t>(to_pin.size()) + hr;
+            ++dbg[0];
             if (!fits_after_eviction(demand)) {
+                ++dbg[1];
                 to_transfer.clear();
             } else {
                 for (int32_t p : to_pin) {
@@ -450,6 +476,7 @@ struct oomb_tier_s {
                 }
             }
         }
+        dbg[best_effort ? 2 : 3] += static_cast<int64_t>(to_transfer.size());
         cudaEvent_t ev_issue = to_transfer.empty() ? nullptr : stamp(ON_H2D);
         cudaEvent_t ev_done = to_transfer.empty() ? nullptr : later();
         for (int32_t p : to_transfer) {
@@ -629,6 +656,8 @@ void tier_orphan(oomb_tier_s* t) {
 
 // (internal, hidden) the stream the engine orders its write-backs after and its fetch waits into
 void* tier_compute_stream(oomb_tier_s* t) { return t->compute; }
+// (internal) the event real-mode log timestamps are measured from
+void* tier_t0(oomb_tier_s* t) { return t->t0; }
 
 int oomb_tier_create_sim(oomb_pagetable_t pt, const oomb_tier_config* cfg, oomb_tier_t* out) {
     return guard([&] {
@@ -676,6 +705,12 @@ int oomb_tier_create(oomb_pool_t pool, const oomb_tier_config* cfg, void* comput
 
 int oomb_tier_destroy(oomb_tier_t t) {
     if (!t) return OOMB_OK;
+    if (std::getenv("OOMB_TIER_DEBUG"))
+        std::fprintf(stderr, "tier: best-effort %lld refused %lld | pages prefetched %lld on-demand %lld | "
+                     "H2D waits: page write-back %lld, slot write-back %lld | compute-stream slot waits %lld\n",
+                     (long long)t->dbg[0], (long long)t->dbg[1], (long long)t->dbg[2], (long long)t->dbg[3],
+                     (long long)t->dbg[4], (long long)t->dbg[5],
+                     (long long)(t->real() && !t->orphaned ? t->pool->compute_ticket_waits : -1));
     if (t->real()) {
 #ifndef OOMB_TIER_RESTORE_ON_DESTROY
 #define OOMB_TIER_RESTORE_ON_DESTROY 1
@@ -768,6 +803,10 @@ int oomb_tier_stats(oomb_tier_t t, double* out) {
         out[3] = static_cast<double>(t->h2d_bwd);
         out[4] = static_cast<double>(t->d2h);
     });
+}
+
+int oomb_tier_moved_bytes(oomb_tier_t t, int64_t* h2d_moved) {
+    return guard([&] { *h2d_moved = static_cast<int64_t>(t->h2d_moved); });
 }
 
 int oomb_tier_log(oomb_tier_t t, oomb_event* out, int64_t cap, int64_t* n) {

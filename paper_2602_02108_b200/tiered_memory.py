@@ -228,6 +228,13 @@ class TieredEngine:
     def d2h_bytes(self):
         return int(self._stats()[4])
 
+    def h2d_bytes_moved(self) -> int:
+        """Real engine: host->device bytes actually copied (h2d_bytes counts every fetch decision, as the
+        reference does; a page fetched back into its still-unused victim slots moves nothing)."""
+        n = C.c_int64()
+        call("oomb_tier_moved_bytes", self.handle, C.byref(n))
+        return n.value
+
     def raw_log(self) -> np.ndarray:
         n = C.c_int64()
         call("oomb_tier_log", self.handle, None, 0, C.byref(n))

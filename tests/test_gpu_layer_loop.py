@@ -103,3 +103,51 @@ def test_native_loop_with_engine_matches_host_loop(regime):
     assert host[1] == nat[1]
     assert host[2] == nat[2]
     assert host[2][0] > 0 and host[2][2] > 0, "the capped tier must move pages both ways"
+
+
+@pytest.mark.parametrize("slack", [512, 768])
+def test_victim_slot_reclaim_bitwise(slack):
+    """Pages fetched back into their victim slots (the slots their eviction freed, not yet handed out
+    again) and pages copied in from the host tier mix within one step: every chunk's output, LSE,
+    dq and dk_cur / dv_cur (the dM_i read-back of the chunk's own pages: together the whole
+    gradient pool) equal the all-resident run bit for bit, and the engine really did both (moved
+    fewer bytes than the reference's accounting, but some)."""
+    import bench
+    from paper_2602_02108_b200 import PagedCache
+    from paper_2602_02108_b200 import attention as A
+    from paper_2602_02108_b200.chunk_loop import layer_step
+    from paper_2602_02108_b200.tiered_memory import TierConfig, TieredEngine
+    cfg = dict(bench.CONFIGS["c3"])
+    cfg["T"] = 128 * 4096  # 4,096 pages: the tier holds 3,072, the pool 3,072 + slack
+    dev = torch.device("cuda", 0)
+    run = bench.Run(cfg, seed=99, device=dev)
+    K = bench.low_locality_keys(run)
+    C, P, S = cfg["C"], cfg["P"], run.S
+    n_pages = cfg["T"] // P
+    cap = int(0.75 * n_pages)
+    kv = (S, C, cfg["Hkv"], cfg["hd"])
+    grads = A.AttnGrads(torch.empty(S, C, cfg["Hq"], cfg["hd"], device=dev),
+                        torch.empty(S, C, cfg["Hkv"], cfg["hd"], device=dev),
+                        torch.empty(S, C, cfg["Hkv"], cfg["hd"], device=dev))
+    res, moved = {}, None
+    for capped in (False, True):
+        cache = PagedCache(run.mc, dtype="bf16", max_tokens=cfg["T"],
+                           device_capacity_pages=cap + slack if capped else -1)
+        eng = TieredEngine(cache, TierConfig(device_capacity_pages=cap if capped else -1, bandwidth_bytes_per_s=55e9))
+        eng.set_prefetch_headroom_pages(C // P)
+        for t in (run.o_all, run.lse_all, grads.dq, grads.dk_cur, grads.dv_cur):
+            t.zero_()
+        layer_step(cache, 0, run.q_all, K.view(kv), run.v_all.view(kv), run.do_all, run.o_all, run.lse_all,
+                   grads, mode="topk", grad_stride_chunks=1)
+        torch.cuda.synchronize()
+        cache.check_device_errors()
+        if capped:
+            moved = (eng.h2d_bytes(0) + eng.h2d_bytes(1), eng.h2d_bytes_moved())
+        res[capped] = [x.clone() for x in (run.o_all, run.lse_all, grads.dq, grads.dk_cur, grads.dv_cur)]
+        eng.release_all_reservations()
+        eng.close(discard=True)
+        del cache, eng
+        torch.cuda.empty_cache()
+    for a, b, what in zip(res[False], res[True], ("out", "lse", "dq", "dk_cur", "dv_cur")):
+        assert torch.equal(a, b), (slack, what)
+    assert 0 < moved[1] < moved[0], moved
