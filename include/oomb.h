@@ -274,6 +274,15 @@ OOMB_API int oomb_layer_step(oomb_pool_t pool, int layer, int n_chunks, int mode
  * int64 {phase (0 forward, 1 backward), chunk, pages the chunk needed resident, H2D bytes, D2H bytes
  * the engine moved during the chunk}; the first min(*n, cap) are written to out (may be null). */
 OOMB_API int oomb_layer_stats(oomb_pool_t pool, int64_t* out, int64_t cap, int64_t* n);
+/* oomb_attn_backward_ex + the dM_i read-back of the chunk's own pages own_first_page ..
+ * own_first_page + tokens / P - 1 into dk_cur / dv_cur (what oomb_accumulate_grad_pages of those
+ * pages does after the backward, chunk_trainer.hpp:575-587), done in the dK/dV kernel's store of the
+ * chunk's own keys: the same two fp32 roundings, bit for bit, one launch fewer. tokens must be a
+ * multiple of the page size and those pages appended. */
+OOMB_API int oomb_attn_backward_readback(oomb_pool_t pool, int layer, const void* dout, const void* q, int64_t tokens,
+                                         oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out,
+                                         const void* lse, void* dq, void* dk_cur, void* dv_cur, int flags,
+                                         int64_t own_first_page, void* stream);
 /* Make `stream` wait for the dq of every earlier oomb_attn_backward_ex(..., OOMB_ATTN_DEFER_DQ). */
 OOMB_API int oomb_attn_join_dq(oomb_pool_t pool, void* stream);
 OOMB_API int oomb_lse_merge(const void* o_parts, const float* lse_parts, int parts, int64_t rows, int hd, int dtype,

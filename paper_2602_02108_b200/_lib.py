@@ -115,6 +115,7 @@ _PROTOS = {
     "oomb_score_pages_partial": [VP, I, VP, I64, I, VP, VP],
     "oomb_vote_reduce": [VP, I, I64, I64, VP, VP],
     "oomb_attn_join_dq": [VP, VP],
+    "oomb_attn_backward_readback": [VP, I, VP, VP, I64, VP, VP, VP, VP, VP, VP, VP, VP, I, I64, VP],
     "oomb_layer_step": [VP, I, I, I, VP, I, VP, VP, VP, I, VP, VP, VP, VP, VP, I64, I, VP],
     "oomb_layer_stats": [VP, VP, I64, C.POINTER(I64)],
     "oomb_accumulate_grad_pages_rope": [VP, I, VP, I, VP, VP, I64, C.c_float, VP],

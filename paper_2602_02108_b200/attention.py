@@ -226,10 +226,13 @@ def attn_forward(cfg: ModelConfig, q, cache: PagedCache, layer: int, selected, k
 
 def attn_backward(cfg: ModelConfig, dout, q, cache: PagedCache, layer: int, k_cur, v_cur, saved: AttnSaved,
                   stream=None, grads: AttnGrads | None = None, past_only: bool = False,
-                  selected=None, defer_dq: bool = False) -> AttnGrads:
+                  selected=None, defer_dq: bool = False, own_first_page: int | None = None) -> AttnGrads:
     """attention.hpp:222-293 — past-page dK/dV go into the cache's gradient pages.
     `grads` may carry preallocated fp32 output buffers. defer_dq: the stream does not wait for dq
-    (it overlaps the caller's next backward); join_dq(cache, stream) before reading it."""
+    (it overlaps the caller's next backward); join_dq(cache, stream) before reading it.
+    own_first_page: dk_cur / dv_cur also receive the pool gradients of the chunk's own pages
+    own_first_page .. + C / P - 1 (the dM_i read-back, PagedCache.accumulate_grad_pages of those
+    pages, chunk_trainer.hpp:575-587) within the same call (oomb_attn_backward_readback)."""
     dout, q = cache._dev(dout), cache._dev(q)
     k_cur, v_cur = cache._dev(k_cur), cache._dev(v_cur)
     if dout.shape != saved.out.shape:
@@ -245,9 +248,13 @@ def attn_backward(cfg: ModelConfig, dout, q, cache: PagedCache, layer: int, k_cu
                 dv.shape != dk.shape or {dq.dtype, dk.dtype, dv.dtype} != {cache.acc_dtype}:
             raise ShapeError("attn_backward: preallocated gradients have the wrong shape or dtype")
     sel = saved.selected if selected is None else as_selection(cache, selected, stream)
-    call("oomb_attn_backward_ex", cache.handle, layer, _ptr(dout), _ptr(q), c, sel.handle, _ptr(k_cur),
-         _ptr(v_cur), _ptr(saved.out), _ptr(saved.lse), _ptr(dq), _ptr(dk), _ptr(dv),
-         (PAST_ONLY if past_only else 0) | (DEFER_DQ if defer_dq else 0), stream_handle(stream))
+    flags = (PAST_ONLY if past_only else 0) | (DEFER_DQ if defer_dq else 0)
+    args = (cache.handle, layer, _ptr(dout), _ptr(q), c, sel.handle, _ptr(k_cur), _ptr(v_cur), _ptr(saved.out),
+            _ptr(saved.lse), _ptr(dq), _ptr(dk), _ptr(dv), flags)
+    if own_first_page is None:
+        call("oomb_attn_backward_ex", *args, stream_handle(stream))
+    else:
+        call("oomb_attn_backward_readback", *args, own_first_page, stream_handle(stream))
     return AttnGrads(dq, dk, dv)
 
 

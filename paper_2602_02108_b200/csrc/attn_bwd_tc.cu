@@ -111,11 +111,12 @@ BwdWs carve(const AttnGeom& g, void* ws) {
 }
 
 // ---------------------------------------------------------------- prep kernels
-__global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-                                const float* __restrict__ lse, int C, int Hq, int hd, float* __restrict__ Dt,
-                                float* __restrict__ Lt) {
+__device__ __forceinline__ void bwd_prep_body(const __nv_bfloat16* __restrict__ o,
+                                              const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
+                                              int C, int Hq, int hd, float* __restrict__ Dt, float* __restrict__ Lt,
+                                              int block) {
     // two (token, head) rows per warp: up to 16 lanes x 16 B of O and dO each (hd 64: 8 lanes)
-    const int64_t row = (static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * 2 +
+    const int64_t row = (static_cast<int64_t>(block) * (blockDim.x / 32) + (threadIdx.x >> 5)) * 2 +
                         ((threadIdx.x >> 4) & 1);
     const int l16 = threadIdx.x & 15;
     const bool ok = row < static_cast<int64_t>(C) * Hq;
@@ -156,11 +157,10 @@ inline int layer_pages(const AttnGeom& g) {
 // ncb - b query tiles from its diagonal on), codes ncb + k * bpp + sub the past blocks of the k-th
 // union page (attended by popcount(mask) query pages x tpq tiles each). Units write disjoint
 // gradient rows, so the order changes the schedule only, never a result bit.
-__global__ void __launch_bounds__(1024) bwd_sched_kernel(const int32_t* __restrict__ off,
-                                                         const int32_t* __restrict__ ids, int m, int layer_pages,
-                                                         int n_pages, uint64_t* __restrict__ mask,
-                                                         int32_t* __restrict__ uni, int32_t* __restrict__ n_uni, int ncb,
-                                                         int bpp, int tpq, int32_t* __restrict__ order, int* err) {
+__device__ __forceinline__ void bwd_sched_body(const int32_t* __restrict__ off, const int32_t* __restrict__ ids,
+                                               int m, int layer_pages, int n_pages, uint64_t* __restrict__ mask,
+                                               int32_t* __restrict__ uni, int32_t* __restrict__ n_uni, int ncb,
+                                               int bpp, int tpq, int32_t* __restrict__ order, int* err) {
     using Scan = cub::BlockScan<int, 1024>;
     __shared__ typename Scan::TempStorage tmp;
     constexpr int kKeys = 256;
@@ -213,6 +213,19 @@ __global__ void __launch_bounds__(1024) bwd_sched_kernel(const int32_t* __restri
     }
     __syncthreads();
     for (int u = tid; u < units; u += 1024) order[atomicAdd(&cur[key(u)], 1)] = u;
+}
+
+// The backward's two preparation steps in ONE launch of 1024-thread blocks: block 0 builds the
+// schedule (bwd_sched_body) while blocks 1.. compute D = rowsum(dO * O) and the log2 LSE, 64
+// (token, head) rows each.
+__global__ void __launch_bounds__(1024) bwd_prep_sched_kernel(
+    const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse, int C,
+    int Hq, int hd, float* __restrict__ Dt, float* __restrict__ Lt, const int32_t* __restrict__ off,
+    const int32_t* __restrict__ ids, int m, int layer_pages, int n_pages, uint64_t* __restrict__ mask,
+    int32_t* __restrict__ uni, int32_t* __restrict__ n_uni, int ncb, int bpp, int tpq, int32_t* __restrict__ order,
+    int* err) {
+    if (blockIdx.x == 0) bwd_sched_body(off, ids, m, layer_pages, n_pages, mask, uni, n_uni, ncb, bpp, tpq, order, err);
+    else bwd_prep_body(o, dout, lse, C, Hq, hd, Dt, Lt, static_cast<int>(blockIdx.x) - 1);
 }
 
 // ===========================================================================
@@ -279,6 +292,10 @@ struct BwdParams {
     float* dv_cur;
     int* err;
     CtaTrace tr;  // debug CTA timeline (OOMB_CTA_TRACE)
+    // >= 0: first page id of the chunk's own pages; the dK/dV epilogue of the chunk's own key blocks
+    // adds those pages' pool gradients (the dM_i read-back, chunk_trainer.hpp:575-587) before the
+    // store: fl(fl(dK * scale) + pool), the same two roundings as the store + accumulate_grads pass
+    int readback_first;
 };
 
 // dQ-kernel K step ks (16 keys) of the packed dS operand: keys [64w, 64w+64) of warpgroup w
@@ -1065,6 +1082,15 @@ __global__ void __launch_bounds__(384, 1)
             mbar_arrive(&bars->acc_free);
             mbar_arrive(&bars->unit_empty[k]);  // descriptor fields are in registers
             if (n > 0) {
+                // the fused dM_i read-back: this key row's own-page gradient row in the pool
+                const float* rb = nullptr;
+                if (!past && p.readback_first >= 0 && key_ok) {
+                    const int kk = key0 + kr;
+                    const int gs = p.gslot[p.readback_first + kk / g.P];
+                    if (gs >= 0)
+                        rb = (wg ? p.gv : p.gk) +
+                             ((static_cast<size_t>(gs) * g.Hkv + g_kv) * g.P + kk % g.P) * static_cast<size_t>(g.hd);
+                }
                 // ---- four [128 x 32] slices through this group's staging buffer into L2 / dk_cur / dv_cur
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -1072,12 +1098,20 @@ __global__ void __launch_bounds__(384, 1)
                     if (issuer) bulk_wait_read0();     // the previous slice has left the staging buffer
                     named_bar_sync(4 + wg, 128);
 #pragma unroll
-                    for (int u8 = 0; u8 < 8; ++u8)
-                        st_slice_f32(stage, kr, u8,
-                                     make_float4(__uint_as_float(va[c][4 * u8]) * sc,
-                                                 __uint_as_float(va[c][4 * u8 + 1]) * sc,
-                                                 __uint_as_float(va[c][4 * u8 + 2]) * sc,
-                                                 __uint_as_float(va[c][4 * u8 + 3]) * sc));
+                    for (int u8 = 0; u8 < 8; ++u8) {
+                        float4 v4 = make_float4(__fmul_rn(__uint_as_float(va[c][4 * u8]), sc),
+                                                __fmul_rn(__uint_as_float(va[c][4 * u8 + 1]), sc),
+                                                __fmul_rn(__uint_as_float(va[c][4 * u8 + 2]), sc),
+                                                __fmul_rn(__uint_as_float(va[c][4 * u8 + 3]), sc));
+                        if (rb) {
+                            const float4 a4 = __ldg(reinterpret_cast<const float4*>(rb + c * 32) + u8);
+                            v4.x = __fadd_rn(v4.x, a4.x);
+                            v4.y = __fadd_rn(v4.y, a4.y);
+                            v4.z = __fadd_rn(v4.z, a4.z);
+                            v4.w = __fadd_rn(v4.w, a4.w);
+                        }
+                        st_slice_f32(stage, kr, u8, v4);
+                    }
                     fence_proxy_async_smem();
                     named_bar_sync(4 + wg, 128);
                     if (issuer) {
@@ -1140,7 +1174,8 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
                         const int32_t* d_gslot_layer, float* gkpool, float* gvpool, const void* k_cur,
                         const void* v_cur, const void* out, const float* lse, float* dq, float* dk_cur,
                         float* dv_cur, int* d_err, void* workspace, size_t workspace_bytes, int nnz, int n_pages,
-                        cudaStream_t st, cudaStream_t side, cudaEvent_t ev_prep, cudaEvent_t ev_dq, bool join_dq) {
+                        cudaStream_t st, cudaStream_t side, cudaEvent_t ev_prep, cudaEvent_t ev_dq, bool join_dq,
+                        int readback_first) {
     OOMB_REQUIRE(workspace_bytes >= attn_bwd_tc_workspace(g, nnz), OOMB_ERROR, "bwd workspace too small");
     OOMB_REQUIRE(g.m <= 64, OOMB_CONFIG_ERROR, "tcgen05 backward supports at most 64 query pages per chunk");
     if (first_use_on_device(2)) {
@@ -1153,24 +1188,21 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
     BwdWs w = carve(g, workspace);
     ProfScope* prep_scope = new ProfScope(PK_BWD_PREP, st);
     const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
-    bwd_prep_kernel<<<static_cast<unsigned>((rows + 15) / 16), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), lse, g.C, g.Hq, g.hd, w.Dt,
-        w.Lt);
-    check_launch("bwd_prep_kernel");
     // page size 64 pairs union pages per unit: kept in union order
     const bool lpt = OOMB_BWD_LPT && g.P != kHalf;
-    bwd_sched_kernel<<<1, 1024, 0, st>>>(sel_off, sel_ids, g.m, layer_pages(g), n_pages, w.mask, w.uni, w.n_uni,
-                                         g.chunk_keys ? g.C / kTile : 0, bwd_blocks_per_page(g),
-                                         std::max(1, g.P / kTile), lpt ? w.order : nullptr, d_err);
-    check_launch("bwd_sched_kernel");
+    bwd_prep_sched_kernel<<<static_cast<unsigned>(1 + (rows + 63) / 64), 1024, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), lse, g.C, g.Hq, g.hd, w.Dt,
+        w.Lt, sel_off, sel_ids, g.m, layer_pages(g), n_pages, w.mask, w.uni, w.n_uni, g.chunk_keys ? g.C / kTile : 0,
+        bwd_blocks_per_page(g), std::max(1, g.P / kTile), lpt ? w.order : nullptr, d_err);
+    check_launch("bwd_prep_sched_kernel");
     // head dim 64: the 128-wide tiles carry zeros in columns 64-127 (TMA out-of-bounds fill) and the
     // stores of those columns fall outside the tensors (clipped): see launch_attn_fwd_tc4
     const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, g.hd);
     const CUtensorMap tdo = map_rows_heads(dout, g.C, g.Hq, g.hd);
     const CUtensorMap tkc = map_rows_heads(k_cur, g.C, g.Hkv, g.hd);
     const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, g.hd);
-    BwdParams p{g, sel_off, sel_ids, d_kvslot_layer, d_gslot_layer, gkpool, gvpool, w.Dt, w.Lt, w.mask, w.uni,
-                w.n_uni, lpt ? w.order : nullptr, dq, dk_cur, dv_cur, d_err, CtaTrace{}};
+    BwdParams p{g,     sel_off, sel_ids, d_kvslot_layer, d_gslot_layer, gkpool, gvpool, w.Dt, w.Lt, w.mask, w.uni,
+                w.n_uni, lpt ? w.order : nullptr, dq, dk_cur, dv_cur, d_err, CtaTrace{}, readback_first};
     delete prep_scope;
     // dQ and dK/dV only read the chunk's inputs and the prep outputs: dQ runs on the pool's side
     // stream, launched first, and the persistent dK/dV CTAs pick up SMs as dQ's last wave drains

@@ -250,17 +250,16 @@ extern "C" int oomb_layer_step(oomb_pool_t p, int layer, int n_chunks, int mode,
                     }
                     const double hs2 = tl_path ? now_ms() : 0;
                     mark();
-                    ok(oomb_attn_backward_ex(p, layer, at(dout, (i % dout_cycle) * qe, el), at(q, (i % q_cycle) * qe, el),
-                                             C, L.sels[i], at(k, i * ke, el), at(v, i * ke, el), at(out, i * qe, el),
-                                             at(lse, static_cast<int64_t>(i) * C * c.n_q_heads, ae), atw(dq, gi * qe, ae),
-                                             dki, dvi, 0, comp));
+                    ok(oomb_attn_backward_readback(p, layer, at(dout, (i % dout_cycle) * qe, el),
+                                               at(q, (i % q_cycle) * qe, el), C, L.sels[i], at(k, i * ke, el),
+                                               at(v, i * ke, el), at(out, i * qe, el),
+                                               at(lse, static_cast<int64_t>(i) * C * c.n_q_heads, ae),
+                                               atw(dq, gi * qe, ae), dki, dvi, 0, static_cast<int64_t>(i) * m,
+                                               comp));  // + the dM_i read-back
                     mark();
                     const double hs3 = tl_path ? now_ms() : 0;
                     std::vector<int32_t> su = sel_union(L, L.sels[i]);
                     ok(oomb_tier_on_grads_scattered(eng, layer, su.data(), static_cast<int>(su.size())));
-                    std::vector<int32_t> own(static_cast<size_t>(m));
-                    std::iota(own.begin(), own.end(), i * m);
-                    ok(oomb_accumulate_grad_pages(p, layer, own.data(), m, dki, dvi, comp));
                     ok(oomb_tier_end_layer_use(eng, layer, ids.data(), static_cast<int>(ids.size())));
                     tier_io(eng, &h1, &d1);
                     L.stats.insert(L.stats.end(), {1, i, static_cast<int64_t>(ids.size()), h1 - h0, d1 - d0});
@@ -324,18 +323,16 @@ extern "C" int oomb_layer_step(oomb_pool_t p, int layer, int n_chunks, int mode,
 
     backward:  // ---- backward (dQ deferred: chunk i's dQ overlaps chunk i-1's dK/dV)
         for (int i = n_chunks - 1; i >= 0; --i) {
-            std::vector<int32_t> own(static_cast<size_t>(m));
             const int64_t gi = grad_stride_chunks ? i : 0;
             const void* qi = at(q, (i % q_cycle) * qe, el);
             const void* di = at(dout, (i % dout_cycle) * qe, el);
             void* dqi = atw(dq, gi * qe, ae);
             void* dki = atw(dk_cur, gi * ke, ae);
             void* dvi = atw(dv_cur, gi * ke, ae);
-            ok(oomb_attn_backward_ex(p, layer, di, qi, C, L.sels[i], at(k, i * ke, el), at(v, i * ke, el),
-                                     at(out, i * qe, el), at(lse, static_cast<int64_t>(i) * C * c.n_q_heads, ae), dqi,
-                                     dki, dvi, OOMB_ATTN_DEFER_DQ, comp));
-            std::iota(own.begin(), own.end(), i * m);
-            ok(oomb_accumulate_grad_pages(p, layer, own.data(), m, dki, dvi, comp));
+            // dQ deferred; the dM_i read-back of the chunk's own pages runs in the dK/dV kernel's store
+            ok(oomb_attn_backward_readback(p, layer, di, qi, C, L.sels[i], at(k, i * ke, el), at(v, i * ke, el),
+                                           at(out, i * qe, el), at(lse, static_cast<int64_t>(i) * C * c.n_q_heads, ae),
+                                           dqi, dki, dvi, OOMB_ATTN_DEFER_DQ, static_cast<int64_t>(i) * m, comp));
         }
         ok(oomb_attn_join_dq(p, comp));
     });

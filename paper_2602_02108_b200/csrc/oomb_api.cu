@@ -943,9 +943,10 @@ int oomb_attn_forward(oomb_pool_t p, int layer, const void* q, int64_t tokens, o
     return oomb_attn_forward_ex(p, layer, q, tokens, sel, k_cur, v_cur, out, lse, 0, stream);
 }
 
-int oomb_attn_backward_ex(oomb_pool_t p, int layer, const void* dout, const void* q, int64_t tokens,
+namespace {
+int attn_backward_impl(oomb_pool_t p, int layer, const void* dout, const void* q, int64_t tokens,
                        oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out, const void* lse,
-                       void* dq, void* dk_cur, void* dv_cur, int flags, void* stream) {
+                       void* dq, void* dk_cur, void* dv_cur, int flags, int64_t own_first, void* stream) {
     return guard([&] {
         set_dev(p);
         p->pt->check_layer(layer);
@@ -958,6 +959,20 @@ int oomb_attn_backward_ex(oomb_pool_t p, int layer, const void* dout, const void
             p->pt->check_ids(layer, sel->h_ids + sel->h_off[qp], sel->h_off[qp + 1] - sel->h_off[qp], p->enforce,
                              "attn_backward");
         ensure_grad_pages(p, layer, sel->h_off, sel->h_ids, g.m, S(stream));
+        // own_first >= 0: the dM_i read-back of the chunk's own pages (oomb_accumulate_grad_pages of
+        // pages own_first .. own_first + tokens / P - 1) folded into this call
+        int rb_first = -1, rb_n = 0;
+        if (own_first >= 0) {
+            OOMB_REQUIRE(!(flags & OOMB_ATTN_PAST_ONLY) && tokens % g.P == 0 &&
+                             (own_first + tokens / g.P) * g.P <= p->pt->filled[layer],
+                         OOMB_SHAPE_ERROR,
+                         "attn_backward_readback: the chunk's own keys must fill whole appended pages");
+            rb_first = static_cast<int>(own_first);
+            rb_n = static_cast<int>(tokens / g.P);
+            std::vector<int32_t> own(static_cast<size_t>(rb_n));
+            for (int i = 0; i < rb_n; ++i) own[static_cast<size_t>(i)] = rb_first + i;
+            p->pt->check_ids(layer, own.data(), rb_n, p->enforce, "gather_grad_pages", /*allow_remote=*/true);
+        }
         const size_t kvb = static_cast<size_t>(tokens) * g.Hkv * g.hd * p->aelem;
         const bool tc = p->policy != 1 && p->maps.valid && tc_supported(g, p->cfg.dtype) && tc_bwd_available();
         if (tc) {
@@ -983,7 +998,7 @@ int oomb_attn_backward_ex(oomb_pool_t p, int layer, const void* dout, const void
                                static_cast<const float*>(lse), static_cast<float*>(dq), static_cast<float*>(dk_cur),
                                static_cast<float*>(dv_cur), p->d_err, p->bwd_ws[b], p->bwd_ws_bytes[b], sel->nnz,
                                static_cast<int>(p->pt->pages[layer].size()), S(stream), p->bwd_side,
-                               p->bwd_ev_prep, p->bwd_ev_dq[b], !defer);
+                               p->bwd_ev_prep, p->bwd_ev_dq[b], !defer, rb_first);
             p->bwd_ws_used[b] = true;
             p->bwd_last_dq = p->bwd_ev_dq[b];
         } else {
@@ -993,8 +1008,31 @@ int oomb_attn_backward_ex(oomb_pool_t p, int layer, const void* dout, const void
                                  p->gslot_layer(layer), p->kpool, p->vpool, p->gkpool, p->gvpool, k_cur, v_cur, out,
                                  lse, dq, dk_cur, dv_cur, p->d_err, S(stream),
                                  static_cast<int>(p->pt->pages[layer].size()));
+            if (rb_first >= 0)
+                launch_accumulate_grads(nullptr, rb_n, p->gslot_layer(layer), p->gkpool, p->gvpool,
+                                        p->pt->filled[layer], p->cfg.page_size, p->cfg.n_kv_heads, p->cfg.head_dim,
+                                        dk_cur, dv_cur, S(stream), 0, nullptr, p->f64(), rb_first);
         }
     });
+}
+
+}  // namespace
+
+int oomb_attn_backward_ex(oomb_pool_t p, int layer, const void* dout, const void* q, int64_t tokens,
+                          oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out, const void* lse,
+                          void* dq, void* dk_cur, void* dv_cur, int flags, void* stream) {
+    return attn_backward_impl(p, layer, dout, q, tokens, sel, k_cur, v_cur, out, lse, dq, dk_cur, dv_cur, flags, -1,
+                              stream);
+}
+
+int oomb_attn_backward_readback(oomb_pool_t p, int layer, const void* dout, const void* q, int64_t tokens,
+                                oomb_selection_t sel, const void* k_cur, const void* v_cur, const void* out,
+                                const void* lse, void* dq, void* dk_cur, void* dv_cur, int flags, int64_t own_first_page,
+                                void* stream) {
+    if (own_first_page < 0)
+        return guard([&] { OOMB_REQUIRE(false, OOMB_SHAPE_ERROR, "attn_backward_readback: negative own_first_page"); });
+    return attn_backward_impl(p, layer, dout, q, tokens, sel, k_cur, v_cur, out, lse, dq, dk_cur, dv_cur, flags,
+                              own_first_page, stream);
 }
 
 int oomb_attn_backward(oomb_pool_t p, int layer, const void* dout, const void* q, int64_t tokens,

@@ -245,7 +245,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
                         const int32_t* d_gslot_layer, float* gkpool, float* gvpool, const void* k_cur,
                         const void* v_cur, const void* out, const float* lse, float* dq, float* dk_cur,
                         float* dv_cur, int* d_err, void* workspace, size_t workspace_bytes, int nnz, int n_pages,
-                        cudaStream_t st, cudaStream_t side, cudaEvent_t ev_prep, cudaEvent_t ev_dq, bool join_dq);
+                        cudaStream_t st, cudaStream_t side, cudaEvent_t ev_prep, cudaEvent_t ev_dq, bool join_dq, int readback_first = -1);
 size_t attn_bwd_tc_workspace(const AttnGeom& g, int max_sel_ids);
 // Split-K count of the tcgen05 forward / dQ kernels for small grids (attn_fwd4.cu).
 int attn_tc_splits(const AttnGeom& g, int num_sms);

@@ -19,6 +19,17 @@ __global__ void k(float* out, int iters) {
                 asm volatile("fma.rn.f32x2 %0, %0, %0, %0;" : "+l"(v));
                 *reinterpret_cast<unsigned long long*>(&a[i & 6]) = v;
             }
+            if (OP == 4) {  // F2FP.BF16.F32.PACK_AB alone
+                unsigned int h;
+                asm volatile("cvt.rn.bf16x2.f32 %0, %1, %1;" : "=r"(h) : "f"(a[i]));
+                a[i] = __uint_as_float(h) + 1e-30f;
+            }
+            if (OP == 5) {  // one ex2 and one bf16x2 pack per element, independent chains
+                asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+                unsigned int h;
+                asm volatile("cvt.rn.bf16x2.f32 %0, %1, %1;" : "=r"(h) : "f"(a[(i + 4) & 7]));
+                a[(i + 4) & 7] = __uint_as_float(h ^ 0x1u);
+            }
             if (OP == 3) {
                 unsigned int h;
                 asm volatile("cvt.rn.f16x2.f32 %0, %1, %1;" : "=r"(h) : "f"(a[i]));
@@ -45,6 +56,8 @@ int main() {
         k<1><<<148, w * 32>>>(out, 4096);
         k<2><<<148, w * 32>>>(out, 4096);
         k<3><<<148, w * 32>>>(out, 4096);
+        k<4><<<148, w * 32>>>(out, 4096);
+        k<5><<<148, w * 32>>>(out, 4096);
         cudaDeviceSynchronize();
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
