@@ -623,6 +623,20 @@ constexpr int kKvBar = kKvDesc + 2 * kKvUnitBytes;
 constexpr int kKvSmem = kKvBar + 256;                    // the dynamic smem base is 1024-aligned (checked)
 static_assert(kKvSmem <= 232448, "dynamic shared memory above the 227 KB opt-in limit");
 constexpr uint32_t kTmS = 0, kTmDP = 128, kTmDK = 256, kTmDV = 384;
+// Softmax warpgroups of the dK/dV kernel: each owns kKvCols query columns of every item (2: 64
+// columns each; 4: 32 each, half the per-thread exp / dS chain). With 4 the epilogue stays on
+// warpgroups 0 / 1 (dK / dV) in two TMEM-load rounds (register budget). Measured: 4 is bitwise
+// equal and 2.6 % slower at c3 (the P^T phase only drops 1,388 -> 1,316 clk per item: it is bound
+// by the SM's 16 exp2/clk, 1,024 clk for an item's 16K exponentials, not by the per-thread chain).
+#ifndef OOMB_KV_WG
+#define OOMB_KV_WG 2
+#endif
+constexpr int kKvWg = OOMB_KV_WG;
+static_assert(kKvWg == 2 || kKvWg == 4, "dK/dV softmax warpgroups: 2 or 4");
+constexpr int kKvCols = kTile / kKvWg;
+constexpr int kKvThreads = 128 + 128 * kKvWg;
+constexpr int kKvEpR = kKvWg == 4 ? 2 : 1;  // epilogue TMEM-load rounds
+constexpr int kKvEpC = 4 / kKvEpR;          // 32-column slices per round
 
 struct KvBars {
     uint64_t unit_full[2], unit_empty[2];
@@ -652,9 +666,11 @@ struct KvUnit {
 static_assert(sizeof(KvUnit) <= 120, "unit descriptor");
 static_assert(sizeof(KvUnit) <= kKvUnitBytes, "unit descriptor");
 
-// K step ks (16 queries) of a packed P^T / dS^T operand: queries [64w, 64w+64) of warpgroup w
-// sit in the first 32 of its own 64 columns.
-__host__ __device__ constexpr uint32_t pk_col(int ks) { return (ks >> 2) * 64 + (ks & 3) * 8; }
+// K step ks (16 queries) of a packed P^T / dS^T operand: queries [kKvCols w, kKvCols (w + 1)) of
+// warpgroup w sit in the first kKvCols / 2 of its own kKvCols columns.
+__host__ __device__ constexpr uint32_t pk_col(int ks) {
+    return (ks / (kKvCols / 16)) * kKvCols + (ks % (kKvCols / 16)) * 8;
+}
 
 // Items of a unit in order: past units walk (query page of the list, 128-row tile of the page,
 // q-head of the group) head-fastest; in-chunk units walk (128-row tile from the key block's
@@ -770,7 +786,7 @@ __device__ void decode_unit(const BwdParams& p, int w, KvUnit& u) {
     u.g_row = (g_slot * g.Hkv + u.g_kv) * g.P + u.key0;
 }
 
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(kKvThreads, 1)
     attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                          const __grid_constant__ CUtensorMap tm_kc, const __grid_constant__ CUtensorMap tm_vc,
                          const __grid_constant__ CUtensorMap tm_kp, const __grid_constant__ CUtensorMap tm_vp,
@@ -788,7 +804,7 @@ __global__ void __launch_bounds__(384, 1)
         if (smem_u32(smem) & 1023) __trap();  // SW128 operands and the smem budget need a 1 KB-aligned base
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bars->unit_full[i], 1);
-            mbar_init(&bars->unit_empty[i], 1 + 256);
+            mbar_init(&bars->unit_empty[i], 1 + 128 * kKvWg);
         }
         mbar_init(&bars->kv_full, 1);
         mbar_init(&bars->kv_empty, 1);
@@ -798,10 +814,10 @@ __global__ void __launch_bounds__(384, 1)
         }
         mbar_init(&bars->s_full, 1);
         mbar_init(&bars->dp_full, 1);
-        mbar_init(&bars->p_full, 256);
-        mbar_init(&bars->ds_full, 256);
+        mbar_init(&bars->p_full, 128 * kKvWg);
+        mbar_init(&bars->ds_full, 128 * kKvWg);
         mbar_init(&bars->acc_done, 1);
-        mbar_init(&bars->acc_free, 256);
+        mbar_init(&bars->acc_free, 128 * kKvWg);
         fence_barrier_init();
     }
     if (warp == 3) tmem_alloc<512>(&bars->tmem_base);
@@ -943,13 +959,13 @@ __global__ void __launch_bounds__(384, 1)
             trace_value(p.tr, 16, w_af); trace_value(p.tr, 17, w_kvf);
         })
     } else if (warp >= 4) {
-        // Warpgroup w: query columns [64w, 64w+64) of every item; thread = key row (TMEM lane).
+        // Warpgroup w: query columns [kKvCols w, kKvCols (w + 1)) of every item; thread = key row (TMEM lane).
         const int quarter = warp & 3, wg = (warp - 4) >> 2;
         const int kr = quarter * 32 + lane;  // key row of the block
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         const float sl2 = g.scale * kLog2e;
-        const uint32_t tS = kTmS + wg * 64 + lane_off, tDP = kTmDP + wg * 64 + lane_off;
-        uint8_t* stage = smem + kKvStage + wg * kSliceBytes;
+        const uint32_t tS = kTmS + wg * kKvCols + lane_off, tDP = kTmDP + wg * kKvCols + lane_off;
+        uint8_t* stage = smem + kKvStage + (wg & 1) * kSliceBytes;  // epilogue: warpgroups 0 / 1
         const bool issuer = (threadIdx.x & 127) == 0;  // first thread of the warpgroup issues its TMA
         int gi = 0;
         KVT(const long long c_start = clock64(); long long w_uf = 0, w_s0 = 0, w_s = 0, w_dp = 0, w_ad = 0, c_epi = 0,
@@ -975,11 +991,12 @@ __global__ void __launch_bounds__(384, 1)
             for (int i = 0; i < n; ++i, it.next(u, g.group, tpq)) {
                 const int gj = gi + i;
                 const int st = gj % kKvStages;
-                const uint32_t lrow = smem_u32(smem + kKvLD) + st * 1024 + wg * 256, drow = lrow + 512;
+                const uint32_t lrow = smem_u32(smem + kKvLD) + st * 1024 + wg * kKvCols * 4, drow = lrow + 512;
                 // visible iff query column c >= lim (causal diagonal: key row <= query row); page size 64:
-                // this group's 64 query columns are query page 2 qt + wg, which may not have chosen the page
-                const bool ok = key_ok && (!(p64 && past) || ((qm >> (2 * it.qt + wg)) & 1ull));
-                const int lim = ok ? (it.diag ? kr - wg * 64 : 0) : 1 << 20;
+                // this group's query columns lie in query page 2 qt + wg kKvCols / 64, which may not have
+                // chosen the page
+                const bool ok = key_ok && (!(p64 && past) || ((qm >> (2 * it.qt + wg * kKvCols / 64)) & 1ull));
+                const int lim = ok ? (it.diag ? kr - wg * kKvCols : 0) : 1 << 20;
                 const bool masked = it.diag || !page_full;
                 mbar_wait(&bars->qdo_full[st], (gj / kKvStages) & 1);  // makes the bulk-copied L / D visible
                 // ---- P^T = exp2(S^T sl2 - L): computed as soon as S^T lands, packed in place
@@ -987,9 +1004,9 @@ __global__ void __launch_bounds__(384, 1)
                 else KVT_WAIT(w_s, &bars->s_full, gj & 1);
                 KVT(const long long cp0 = clock64();)
                 tc_fence_after();
-                float pr[64];
+                float pr[kKvCols];
 #pragma unroll
-                for (int c2 = 0; c2 < 2; ++c2) {
+                for (int c2 = 0; c2 < kKvCols / 32; ++c2) {
                     uint32_t sv[32];
                     tmem_ld32(tS + c2 * 32, sv);
                     tmem_wait_ld();
@@ -1017,10 +1034,10 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 if (masked) {
 #pragma unroll
-                    for (int c = 0; c < 64; ++c) pr[c] = (c >= lim) ? pr[c] : 0.f;
+                    for (int c = 0; c < kKvCols; ++c) pr[c] = (c >= lim) ? pr[c] : 0.f;
                 }
 #pragma unroll
-                for (int c2 = 0; c2 < 2; ++c2) {
+                for (int c2 = 0; c2 < kKvCols / 32; ++c2) {
                     uint32_t pk[16];
 #pragma unroll
                     for (int u2 = 0; u2 < 16; ++u2) pk[u2] = pack_bf16(pr[c2 * 32 + 2 * u2], pr[c2 * 32 + 2 * u2 + 1]);
@@ -1035,7 +1052,7 @@ __global__ void __launch_bounds__(384, 1)
                 KVT(const long long cd0 = clock64();)
                 tc_fence_after();
 #pragma unroll
-                for (int c2 = 0; c2 < 2; ++c2) {
+                for (int c2 = 0; c2 < kKvCols / 32; ++c2) {
                     uint32_t dv[32];
                     tmem_ld32(tDP + c2 * 32, dv);
                     tmem_wait_ld();
@@ -1072,58 +1089,69 @@ __global__ void __launch_bounds__(384, 1)
             KVT_WAIT(w_ad, &bars->acc_done, un & 1);
             KVT(const long long ce0 = clock64();)
             tc_fence_after();
-            const uint32_t acc = (wg ? kTmDV : kTmDK) + lane_off;
-            const float sc = key_ok ? (wg ? 1.f : g.scale) : 0.f;
-            uint32_t va[4][32];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32(acc + c * 32, va[c]);
-            tmem_wait_ld();
-            tc_fence_before();
-            mbar_arrive(&bars->acc_free);
-            mbar_arrive(&bars->unit_empty[k]);  // descriptor fields are in registers
-            if (n > 0) {
+            if (wg >= 2) {  // four softmax groups: the epilogue is warpgroups 0 (dK) and 1 (dV)
+                mbar_arrive(&bars->acc_free);
+                mbar_arrive(&bars->unit_empty[k]);
+            } else {
+                const uint32_t acc = (wg ? kTmDV : kTmDK) + lane_off;
+                const float sc = key_ok ? (wg ? 1.f : g.scale) : 0.f;
                 // the fused dM_i read-back: this key row's own-page gradient row in the pool
                 const float* rb = nullptr;
-                if (!past && p.readback_first >= 0 && key_ok) {
+                if (n > 0 && !past && p.readback_first >= 0 && key_ok) {
                     const int kk = key0 + kr;
                     const int gs = p.gslot[p.readback_first + kk / g.P];
                     if (gs >= 0)
                         rb = (wg ? p.gv : p.gk) +
                              ((static_cast<size_t>(gs) * g.Hkv + g_kv) * g.P + kk % g.P) * static_cast<size_t>(g.hd);
                 }
-                // ---- four [128 x 32] slices through this group's staging buffer into L2 / dk_cur / dv_cur
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    if (c * 32 >= g.hd) break;         // head dim 64: columns 64-127 are zero padding
-                    if (issuer) bulk_wait_read0();     // the previous slice has left the staging buffer
-                    named_bar_sync(4 + wg, 128);
+                for (int r = 0; r < kKvEpR; ++r) {
+                    uint32_t va[kKvEpC][32];
 #pragma unroll
-                    for (int u8 = 0; u8 < 8; ++u8) {
-                        float4 v4 = make_float4(__fmul_rn(__uint_as_float(va[c][4 * u8]), sc),
-                                                __fmul_rn(__uint_as_float(va[c][4 * u8 + 1]), sc),
-                                                __fmul_rn(__uint_as_float(va[c][4 * u8 + 2]), sc),
-                                                __fmul_rn(__uint_as_float(va[c][4 * u8 + 3]), sc));
-                        if (rb) {
-                            const float4 a4 = __ldg(reinterpret_cast<const float4*>(rb + c * 32) + u8);
-                            v4.x = __fadd_rn(v4.x, a4.x);
-                            v4.y = __fadd_rn(v4.y, a4.y);
-                            v4.z = __fadd_rn(v4.z, a4.z);
-                            v4.w = __fadd_rn(v4.w, a4.w);
-                        }
-                        st_slice_f32(stage, kr, u8, v4);
+                    for (int c = 0; c < kKvEpC; ++c) tmem_ld32(acc + (r * kKvEpC + c) * 32, va[c]);
+                    tmem_wait_ld();
+                    if (r == kKvEpR - 1) {
+                        tc_fence_before();
+                        mbar_arrive(&bars->acc_free);
                     }
-                    fence_proxy_async_smem();
-                    named_bar_sync(4 + wg, 128);
-                    if (issuer) {
-                        if (past && p64) {  // 64-row boxes into each page's gradient block
-                            tma_reduce_add_2d(wg ? &tm_gv : &tm_gk, stage, c * 32, g_row);
-                            if (has1) tma_reduce_add_2d(wg ? &tm_gv : &tm_gk, stage + kSliceBytes / 2, c * 32, g_row1);
-                        } else if (past) {
-                            tma_reduce_add_2d(wg ? &tm_gv : &tm_gk, stage, c * 32, g_row);
-                        } else {
-                            tma_store_3d(wg ? &tm_dvc : &tm_dkc, stage, c * 32, g_kv, key0);
+                    if (r == 0) mbar_arrive(&bars->unit_empty[k]);  // descriptor fields are in registers
+                    if (n > 0) {
+                        // ---- [128 x 32] slices through this group's staging buffer into L2 / dk_cur / dv_cur
+#pragma unroll
+                        for (int c0 = 0; c0 < kKvEpC; ++c0) {
+                            const int c = r * kKvEpC + c0;
+                            if (c * 32 >= g.hd) break;         // head dim 64: columns 64-127 are zero padding
+                            if (issuer) bulk_wait_read0();     // the previous slice has left the staging buffer
+                            named_bar_sync(4 + wg, 128);
+#pragma unroll
+                            for (int u8 = 0; u8 < 8; ++u8) {
+                                float4 v4 = make_float4(__fmul_rn(__uint_as_float(va[c0][4 * u8]), sc),
+                                                        __fmul_rn(__uint_as_float(va[c0][4 * u8 + 1]), sc),
+                                                        __fmul_rn(__uint_as_float(va[c0][4 * u8 + 2]), sc),
+                                                        __fmul_rn(__uint_as_float(va[c0][4 * u8 + 3]), sc));
+                                if (rb) {
+                                    const float4 a4 = __ldg(reinterpret_cast<const float4*>(rb + c * 32) + u8);
+                                    v4.x = __fadd_rn(v4.x, a4.x);
+                                    v4.y = __fadd_rn(v4.y, a4.y);
+                                    v4.z = __fadd_rn(v4.z, a4.z);
+                                    v4.w = __fadd_rn(v4.w, a4.w);
+                                }
+                                st_slice_f32(stage, kr, u8, v4);
+                            }
+                            fence_proxy_async_smem();
+                            named_bar_sync(4 + wg, 128);
+                            if (issuer) {
+                                if (past && p64) {  // 64-row boxes into each page's gradient block
+                                    tma_reduce_add_2d(wg ? &tm_gv : &tm_gk, stage, c * 32, g_row);
+                                    if (has1) tma_reduce_add_2d(wg ? &tm_gv : &tm_gk, stage + kSliceBytes / 2, c * 32, g_row1);
+                                } else if (past) {
+                                    tma_reduce_add_2d(wg ? &tm_gv : &tm_gk, stage, c * 32, g_row);
+                                } else {
+                                    tma_store_3d(wg ? &tm_dvc : &tm_dkc, stage, c * 32, g_kv, key0);
+                                }
+                                bulk_commit();
+                            }
                         }
-                        bulk_commit();
                     }
                 }
             }
@@ -1247,7 +1275,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         const CUtensorMap tdvc = map_rows_heads_f32(dv_cur, g.C, g.Hkv, g.hd);
         BwdParams pk = p;
         if (OOMB_KV_TRACE) pk.tr = trace_begin("dkdv", n_ctas, 22);
-        attn_bwd_dkdv_kernel<<<n_ctas, 384, kKvSmem, st>>>(tq, tdo, tkc, tvc, maps.kpool, maps.vpool, maps.gkpool,
+        attn_bwd_dkdv_kernel<<<n_ctas, kKvThreads, kKvSmem, st>>>(tq, tdo, tkc, tvc, maps.kpool, maps.vpool, maps.gkpool,
                                                             maps.gvpool, tdkc, tdvc, pk, w.n_uni + 1);
         check_launch("attn_bwd_dkdv_kernel");
         if (OOMB_KV_TRACE) trace_end(pk.tr, n_ctas, st);
