@@ -2,7 +2,7 @@ set -u
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 cp paper_2602_02108_b200/liboomb.so /tmp/liboomb_base.so
-for v in kvtrace kvtrace4; do
+for v in kvtrace kvtp4 kvtp2 kvtp4x2; do
 cp tools/liboomb_$v.so paper_2602_02108_b200/liboomb.so
 for idx in 200; do
 echo "== $v chunk-launch $idx"
