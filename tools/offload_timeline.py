@@ -88,6 +88,20 @@ for capped in (False, True):
             cur = e.chunk
         if e.kind == 2 and cur is not None:
             wb[cur] = max(wb.get(cur, 0.0), e.t * 1e3)
+    # write-backs of pages already dead for this step (owned by a chunk whose backward, and so its
+    # read-back, is done): nothing reads them again before the step ends
+    cur, dead_b, all_b, dead_n, all_n = None, 0, 0, 0, 0
+    m_ = C // P
+    for e in log:
+        if e.kind == 5 and e.phase == 1:
+            cur = e.chunk
+        if e.kind == 2 and e.phase == 1 and e.bytes > 0 and cur is not None:
+            all_b += e.bytes
+            all_n += 1
+            if e.page // m_ > cur:
+                dead_b += e.bytes
+                dead_n += 1
+    print(f"backward write-backs: {all_n} pages {all_b / 1e9:.2f} GB, of dead pages {dead_n} ({dead_b / 1e9:.2f} GB)")
     # victim reuse estimate: fetches (backward) of a page evicted at most D evictions earlier (its old
     # slots would still be unused in a FIFO free list holding ~D slots)
     for D in (128, 256, 400):
