@@ -223,7 +223,7 @@ def offload_measure(run, cap_frac: float, repeats: int = 5):
         fw = [x for x in st if x[0] == "fwd" and x[1] > 0]
         bw = [x for x in st if x[0] == "bwd"]
         out.update(h2d_bytes=eng.h2d_bytes(0) + eng.h2d_bytes(1), d2h_bytes=eng.d2h_bytes(),
-                   h2d_bytes_moved=eng.h2d_bytes_moved(),
+                   h2d_bytes_moved=eng.h2d_bytes_moved(), d2h_bytes_moved=eng.d2h_bytes_moved(),
                    fwd_union=[x[2] for x in fw], fwd_fetch_pages=[x[3] / kv_page for x in fw],
                    bwd_h2d=[x[3] for x in bw], bwd_d2h=[x[4] for x in bw],
                    device_bytes=(slots if use else n_pages) * slot_bytes)
@@ -250,6 +250,7 @@ def offload_measure(run, cap_frac: float, repeats: int = 5):
                 "exposed_pct": 100.0 * (moff - mres) / moff,
                 "exposed_pct_runs": [100.0 * (a - b) / a for a, b in zip(off, res)],
                 "h2d_bytes": o["h2d_bytes"], "d2h_bytes": o["d2h_bytes"], "h2d_bytes_moved": o["h2d_bytes_moved"],
+                "d2h_bytes_moved": o["d2h_bytes_moved"],
                 "fwd_union_pages_per_chunk": {"mean": statistics.mean(fu), "median": statistics.median(fu),
                                               "max": max(fu), "last": fu[-1]} if fu else None,
                 "fwd_fetched_pages_per_chunk": {"mean": statistics.mean(o["fwd_fetch_pages"]),
@@ -271,7 +272,8 @@ def offload_measure(run, cap_frac: float, repeats: int = 5):
             if sl < n_pages:
                 r = regime(K, sl)
                 sweep.append({"device_slots": sl, "pool_bytes": sl * slot_bytes, "exposed_pct": r["exposed_pct"],
-                              "exposed_pct_runs": r["exposed_pct_runs"], "h2d_bytes_moved": r["h2d_bytes_moved"]})
+                              "exposed_pct_runs": r["exposed_pct_runs"], "h2d_bytes_moved": r["h2d_bytes_moved"],
+                              "d2h_bytes_moved": r["d2h_bytes_moved"]})
         del K
         torch.cuda.empty_cache()
     return {"capacity_frac": cap_frac, "capacity_pages": cap, "device_slots": slots, "layer_pages": n_pages,

@@ -361,10 +361,14 @@ OOMB_API int oomb_tier_restore_all(oomb_tier_t t);
 /* out[5] = {now, stall_seconds, h2d_bytes forward, h2d_bytes backward, d2h_bytes} */
 OOMB_API int oomb_tier_stats(oomb_tier_t t, double* out);
 OOMB_API int oomb_tier_log(oomb_tier_t t, oomb_event* out, int64_t cap, int64_t* n);
-/* Real engine: host->device bytes actually copied. oomb_tier_stats counts the reference's transfer
- * bytes (every fetch decision, tiered_memory.hpp:322-326); a page fetched back before its victim
- * slots (the device slots its eviction freed) were handed out again takes them back without a copy. */
-OOMB_API int oomb_tier_moved_bytes(oomb_tier_t t, int64_t* h2d_moved);
+/* Real engine: bytes actually copied host->device and device->host (d2h_moved may be null).
+ * oomb_tier_stats counts the reference's transfer bytes (every fetch and write-back decision,
+ * tiered_memory.hpp:322-326, 386-403). A page fetched back before the device slots its eviction
+ * freed are handed out again takes them back without a copy. With OOMB_TIER_LAZY_WB=1 in the
+ * environment at engine creation, the write-back itself is deferred until the freed slot nears the
+ * front of its free list (OOMB_TIER_CLEAN_AHEAD slots, default 256) or is handed out, and dropped
+ * if the page is fetched back first. */
+OOMB_API int oomb_tier_moved_bytes(oomb_tier_t t, int64_t* h2d_moved, int64_t* d2h_moved);
 /* validate_schedule (tiered_memory.cpp:47-138): out[6] = {stall_s, transfer_bytes, h2d_fwd, h2d_bwd,
  * d2h, overlap_fraction}; n_violations = residency/order violations found. When viol_event / viol_code
  * are non-null, the first viol_cap violations are described by the index of the offending event (-1 for

@@ -110,7 +110,7 @@ _PROTOS = {
     "oomb_tier_restore_all": [VP],
     "oomb_tier_stats": [VP, VP],
     "oomb_tier_log": [VP, VP, I64, C.POINTER(I64)],
-    "oomb_tier_moved_bytes": [VP, C.POINTER(I64)],
+    "oomb_tier_moved_bytes": [VP, C.POINTER(I64), C.POINTER(I64)],
     "oomb_validate_schedule": [VP, I64, C.c_double, VP, C.POINTER(I), VP, VP, I64],
     "oomb_score_pages_partial": [VP, I, VP, I64, I, VP, VP],
     "oomb_vote_reduce": [VP, I, I64, I64, VP, VP],

@@ -360,6 +360,7 @@ int oomb_pool_create(const oomb_config* cfg, int device, oomb_pool_t* out) {
 }
 
 void tier_orphan(oomb_tier_s* t);  // tier.cu
+void tier_on_pool_reset(oomb_tier_s* t);  // tier.cu
 
 int oomb_pool_destroy(oomb_pool_t p) {
     if (!p) return OOMB_OK;
@@ -407,6 +408,7 @@ int oomb_pool_reset(oomb_pool_t p, void* stream) {
         }
         p->pt->reset();
         p->clear_holders();  // freed slots hold no page of the new sequence
+        if (p->engine) tier_on_pool_reset(p->engine);
         const size_t tab = static_cast<size_t>(p->cfg.n_layers) * p->max_pages * sizeof(int32_t);
         OOMB_CUDA(cudaMemsetAsync(p->d_kvslot, 0xFF, tab, S(stream)));
         OOMB_CUDA(cudaMemsetAsync(p->d_gslot, 0xFF, tab, S(stream)));

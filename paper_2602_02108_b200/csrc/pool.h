@@ -239,13 +239,22 @@ struct oomb_pool_s {
         if (h.empty()) h.assign(grad ? n_g_slots : n_kv_slots, -1);
         h[s] = idx;
     }
+    // Deferred write-back (offload engine): a victim slot may hold the only current copy of its page;
+    // the engine's hook copies it out before the slot is handed to anything else.
+    void* victim_ctx = nullptr;
+    void (*victim_flush)(void* ctx, bool grad, int32_t slot) = nullptr;
     int32_t pop_free(bool grad) {  // the oldest free slot (FIFO), no longer holding any page's data
         auto& fl = grad ? g_free : kv_free;
         const int32_t s = fl.front();
-        fl.pop_front();
         auto& h = grad ? g_holder : kv_holder;
+        if (victim_flush && !h.empty() && h[s] >= 0) victim_flush(victim_ctx, grad, s);
+        fl.pop_front();
         if (!h.empty()) h[s] = -1;
         return s;
+    }
+    bool holds(bool grad, int32_t s, int64_t idx) const {  // free slot s still holds page idx's data
+        const auto& h = grad ? g_holder : kv_holder;
+        return s >= 0 && !h.empty() && h[s] == idx;
     }
     bool reclaim(bool grad, int32_t s, int64_t idx) {  // take victim slot s back for page idx
         auto& h = grad ? g_holder : kv_holder;

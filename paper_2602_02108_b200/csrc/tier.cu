@@ -68,6 +68,8 @@ struct oomb_tier_s {
         bool host_has_grad = false;
         uint64_t wb_batch = 0;       // real mode: the write-back batch that last filled the host block
         int32_t vkv = -1, vg = -1;   // real mode: the slots the page was evicted from (victim slots)
+        bool pend_kv = false, pend_g = false;  // real mode: the host block is stale, the victim slot (or,
+                                               // once fetched back, the page's slot) holds the data
     };
     struct Transfer {
         int layer = 0;
@@ -98,6 +100,17 @@ struct oomb_tier_s {
     // H2D waits on a page's own pending write-back, H2D waits on a recycled slot's write-back
     int64_t dbg[6] = {};
     uint64_t h2d_moved = 0;  // real mode: bytes actually copied in (victim-slot reclaims move none)
+    uint64_t d2h_moved = 0;  // real mode: bytes actually copied out (deferred write-backs of reclaimed pages: none)
+    // Deferred write-back (OOMB_TIER_LAZY_WB=1; default off): an eviction frees the page's slots
+    // without copying them out; a victim slot is copied out only when it comes within clean_ahead
+    // (OOMB_TIER_CLEAN_AHEAD) slots of the front of its free list, or is handed out, so a page fetched
+    // back before then moves nothing either way. The engine's decisions and its transfer accounting
+    // are the reference's. Measured at c3 low locality (profiles/r02_perf_notes.md): 22-56 % less D2H,
+    // but a copy-out issued close to the slot's reuse makes the taker wait for it, so the step is
+    // faster only with spare slots (7,168: 549 vs 561 ms backward) and slower with the bench's 6,656.
+    bool lazy_wb = false;
+    int64_t forced_flushes = 0;  // deferred victims copied out only when their slot was handed out
+    int64_t clean_ahead = 256;
     cudaEvent_t t0 = nullptr;
     std::vector<cudaEvent_t> spare_events;
     uint8_t* host_kv = nullptr;    // pinned [layer][page] x (K, V) blocks
@@ -288,6 +301,7 @@ struct oomb_tier_s {
             evict(cand[i].l, cand[i].p);
         }
         end_writeback();
+        clean_front();
         if (static_cast<int64_t>(k) < need)
             throw Error(OOMB_CONFIG_ERROR, "tiered_memory: device capacity smaller than the working set (capacity " +
                                                std::to_string(cfg.device_capacity_pages) + " pages)");
@@ -321,19 +335,27 @@ struct oomb_tier_s {
         const size_t kvb = static_cast<size_t>(p.page_elems) * p.elem;
         const size_t gb = static_cast<size_t>(p.page_elems) * sizeof(float);
         PageState& ps = pages[layer][page];
-        if (wb_kv && ks >= 0) {
+        // a page fetched back into its victim slots with a write-back still deferred has a stale host
+        // block even when the reference's flags say clean
+        const bool need_kv = (wb_kv || ps.pend_kv) && ks >= 0;
+        const bool need_g = (wb_grad || ps.pend_g) && gs >= 0;
+        ps.pend_kv = lazy_wb && need_kv;
+        ps.pend_g = lazy_wb && need_g;
+        if (need_kv && !lazy_wb) {
             uint8_t* h = host_kv + hidx * kv_block;
             queue_copy(1, h, static_cast<uint8_t*>(p.kpool) + ks * kvb, kvb);
             queue_copy(1, h + kvb, static_cast<uint8_t*>(p.vpool) + ks * kvb, kvb);
             ps.host_has_kv = true;
             ps.wb_batch = p.wb_ticket;
+            d2h_moved += 2 * kvb;
         }
-        if (wb_grad && gs >= 0) {
+        if (need_g && !lazy_wb) {
             uint8_t* h = host_grad + hidx * grad_block;
             queue_copy(1, h, reinterpret_cast<uint8_t*>(p.gkpool) + gs * gb, gb);
             queue_copy(1, h + gb, reinterpret_cast<uint8_t*>(p.gvpool) + gs * gb, gb);
             ps.host_has_grad = true;
             ps.wb_batch = p.wb_ticket;
+            d2h_moved += 2 * gb;
         }
         if (ks >= 0) {
             p.free_slot_after_writeback(false, ks);
@@ -363,6 +385,73 @@ struct oomb_tier_s {
         return s;
     }
 
+    // Copy a deferred victim out of free slot s into its page's host block (inside a write-back
+    // batch: the D2H stream already follows the compute stream). The slot's ticket moves to this batch.
+    void flush_victim(bool grad, int32_t s) {
+        auto& p = *pool;
+        const auto& hold = grad ? p.g_holder : p.kv_holder;
+        if (hold.empty() || hold[s] < 0) return;
+        const int64_t idx = hold[s];
+        const int layer = static_cast<int>(idx / p.max_pages), page = static_cast<int>(idx % p.max_pages);
+        PageState& ps = pages[layer][page];
+        if (grad ? !(ps.pend_g && ps.vg == s) : !(ps.pend_kv && ps.vkv == s)) return;
+        const size_t kvb = static_cast<size_t>(p.page_elems) * p.elem;
+        const size_t gb = static_cast<size_t>(p.page_elems) * sizeof(float);
+        if (grad) {
+            uint8_t* h = host_grad + static_cast<size_t>(idx) * grad_block;
+            queue_copy(1, h, reinterpret_cast<uint8_t*>(p.gkpool) + s * gb, gb);
+            queue_copy(1, h + gb, reinterpret_cast<uint8_t*>(p.gvpool) + s * gb, gb);
+            ps.host_has_grad = true;
+            ps.pend_g = false;
+            d2h_moved += 2 * gb;
+        } else {
+            uint8_t* h = host_kv + static_cast<size_t>(idx) * kv_block;
+            queue_copy(1, h, static_cast<uint8_t*>(p.kpool) + s * kvb, kvb);
+            queue_copy(1, h + kvb, static_cast<uint8_t*>(p.vpool) + s * kvb, kvb);
+            ps.host_has_kv = true;
+            ps.pend_kv = false;
+            d2h_moved += 2 * kvb;
+        }
+        ps.wb_batch = p.wb_ticket;
+        p.free_slot_after_writeback(grad, s);
+    }
+    // Copy out the deferred victims among the first clean_ahead slots of both free lists.
+    void clean_front() {
+        if (!real() || !lazy_wb) return;
+        bool open = false;
+        for (int g = 0; g < 2; ++g) {
+            const auto& fl = g ? pool->g_free : pool->kv_free;
+            const auto& hold = g ? pool->g_holder : pool->kv_holder;
+            if (hold.empty()) continue;
+            int64_t n = 0;
+            for (auto it = fl.begin(); it != fl.end() && n < clean_ahead; ++it, ++n) {
+                const int64_t idx = hold[*it];
+                if (idx < 0) continue;
+                const PageState& ps = pages[idx / pool->max_pages][idx % pool->max_pages];
+                if (!(g ? (ps.pend_g && ps.vg == *it) : (ps.pend_kv && ps.vkv == *it))) continue;
+                if (!open) begin_writeback();
+                open = true;
+                flush_victim(g != 0, *it);
+            }
+        }
+        if (open) end_writeback();
+    }
+    // The pool hands out a free slot that still holds a deferred victim: copy it out first (its own
+    // batch; the taker waits for it through the slot's ticket).
+    static void forced_flush(void* ctx, bool grad, int32_t s) {
+        auto* t = static_cast<oomb_tier_s*>(ctx);
+        const auto& hold = grad ? t->pool->g_holder : t->pool->kv_holder;
+        const int64_t idx = hold[s];
+        const PageState& ps = t->pages[idx / t->pool->max_pages][idx % t->pool->max_pages];
+        if (!(grad ? (ps.pend_g && ps.vg == s) : (ps.pend_kv && ps.vkv == s))) return;
+        // slots are only handed out outside a write-back batch (evictions and clean-ahead take none)
+        OOMB_REQUIRE(t->d2h_batch_ev == nullptr, OOMB_STATE_ERROR, "offload: slot taken inside a write-back batch");
+        t->begin_writeback();
+        t->flush_victim(grad, s);
+        t->end_writeback();
+        ++t->forced_flushes;
+    }
+
     // H2D of one page into fresh device slots (real mode).
     void real_fetch(int layer, int page) {
         auto& p = *pool;
@@ -370,21 +459,24 @@ struct oomb_tier_s {
         const size_t kvb = static_cast<size_t>(p.page_elems) * p.elem;
         const size_t gb = static_cast<size_t>(p.page_elems) * sizeof(float);
         PageState& ps = pages[layer][page];
-        // the host block is read only after the write-back that filled it has landed (a page evicted
-        // and fetched back soon after); the destination slots wait for their own read-outs in take_slot
-        OOMB_REQUIRE(ps.host_has_kv, OOMB_STATE_ERROR,
-                     "offload: page " + std::to_string(page) + " of layer " + std::to_string(layer) +
-                         " is host-tier but its host block holds no data");
         // A page whose victim slots were not handed out since its eviction still has its data there
-        // (the write-back only reads them): it takes them back, no copy and no wait for the read-out.
-        // A later write into a reclaimed slot (scatter, append) marks the host copy stale, so a torn
-        // read-out is always written again before the host block is used.
+        // (a write-back, deferred or not, only reads them): it takes them back, no copy and no wait for
+        // the read-out. A later write into a reclaimed slot (scatter, append) marks the host copy
+        // stale, so a torn read-out is always written again before the host block is used. Otherwise
+        // the host block is read, only after the write-back that filled it has landed; the
+        // destination slots wait for their own read-outs in take_slot.
         const int64_t idx = static_cast<int64_t>(hidx);
         const bool g_need = grads_allocated(layer, page);
         const int32_t vkv = ps.vkv, vg = ps.vg;
+        const bool kv_held = p.holds(false, vkv, idx), g_held = g_need && p.holds(true, vg, idx);
+        OOMB_REQUIRE(kv_held || ps.host_has_kv, OOMB_STATE_ERROR,
+                     "offload: page " + std::to_string(page) + " of layer " + std::to_string(layer) +
+                         " is host-tier but its host block holds no data");
+        OOMB_REQUIRE((kv_held || !ps.pend_kv) && (g_held || !g_need || !ps.pend_g), OOMB_STATE_ERROR,
+                     "offload: page " + std::to_string(page) + " has a deferred write-back but no victim slot");
         ps.vkv = ps.vg = -1;
-        const bool kv_back = p.reclaim(false, vkv, idx);
-        const bool g_back = g_need && p.reclaim(true, vg, idx);
+        const bool kv_back = kv_held && p.reclaim(false, vkv, idx);
+        const bool g_back = g_held && p.reclaim(true, vg, idx);
         if (!kv_back || (g_need && !g_back && ps.host_has_grad)) dbg[4] += p.wait_ticket(ps.wb_batch, h2d_stream);
         const int32_t ks = kv_back ? vkv : take_slot(false, h2d_stream, "KV");
         p.kvslot[layer][page] = ks;
@@ -649,9 +741,16 @@ struct oomb_tier_s {
 extern "C" {
 
 // (internal, hidden) oomb_pool_destroy of a pool whose engine is still attached
+// (internal, hidden) oomb_pool_reset with an engine attached: the pages are new, so are their states
+void tier_on_pool_reset(oomb_tier_s* t) {
+    for (auto& l : t->pages) l.clear();
+}
+
 void tier_orphan(oomb_tier_s* t) {
     t->orphaned = true;
     t->pt = nullptr;
+    t->pool->victim_flush = nullptr;
+    t->pool->victim_ctx = nullptr;
 }
 
 // (internal, hidden) the stream the engine orders its write-backs after and its fetch waits into
@@ -694,6 +793,10 @@ int oomb_tier_create(oomb_pool_t pool, const oomb_tier_config* cfg, void* comput
             OOMB_REQUIRE(pool->engine == nullptr, OOMB_STATE_ERROR, "tiered_memory: the pool already has an engine");
             pool->enforce = true;  // the engine turns residency enforcement on (tiered_memory.hpp:102-108)
             pool->engine = t;
+            if (const char* e = std::getenv("OOMB_TIER_LAZY_WB")) t->lazy_wb = e[0] != '0';
+            if (const char* e = std::getenv("OOMB_TIER_CLEAN_AHEAD")) t->clean_ahead = std::atoll(e);
+            pool->victim_ctx = t;
+            pool->victim_flush = &oomb_tier_s::forced_flush;
             t->adopt_pool_pages();
         } catch (...) {
             oomb_tier_destroy(t);
@@ -707,10 +810,12 @@ int oomb_tier_destroy(oomb_tier_t t) {
     if (!t) return OOMB_OK;
     if (std::getenv("OOMB_TIER_DEBUG"))
         std::fprintf(stderr, "tier: best-effort %lld refused %lld | pages prefetched %lld on-demand %lld | "
-                     "H2D waits: page write-back %lld, slot write-back %lld | compute-stream slot waits %lld\n",
+                     "H2D waits: page write-back %lld, slot write-back %lld | compute-stream slot waits %lld | "
+                     "forced victim flushes %lld, d2h moved %.2f GB\n",
                      (long long)t->dbg[0], (long long)t->dbg[1], (long long)t->dbg[2], (long long)t->dbg[3],
                      (long long)t->dbg[4], (long long)t->dbg[5],
-                     (long long)(t->real() && !t->orphaned ? t->pool->compute_ticket_waits : -1));
+                     (long long)(t->real() && !t->orphaned ? t->pool->compute_ticket_waits : -1),
+                     (long long)t->forced_flushes, static_cast<double>(t->d2h_moved) / 1e9);
     if (t->real()) {
 #ifndef OOMB_TIER_RESTORE_ON_DESTROY
 #define OOMB_TIER_RESTORE_ON_DESTROY 1
@@ -740,6 +845,9 @@ int oomb_tier_destroy(oomb_tier_t t) {
             cudaDeviceSynchronize();
             t->pool->enforce = false;
             t->pool->engine = nullptr;
+            t->pool->victim_flush = nullptr;
+            t->pool->victim_ctx = nullptr;
+            t->pool->clear_holders();  // victim data dies with the engine's host blocks
         } else {
             cudaDeviceSynchronize();
         }
@@ -805,8 +913,11 @@ int oomb_tier_stats(oomb_tier_t t, double* out) {
     });
 }
 
-int oomb_tier_moved_bytes(oomb_tier_t t, int64_t* h2d_moved) {
-    return guard([&] { *h2d_moved = static_cast<int64_t>(t->h2d_moved); });
+int oomb_tier_moved_bytes(oomb_tier_t t, int64_t* h2d_moved, int64_t* d2h_moved) {
+    return guard([&] {
+        *h2d_moved = static_cast<int64_t>(t->h2d_moved);
+        if (d2h_moved) *d2h_moved = static_cast<int64_t>(t->d2h_moved);
+    });
 }
 
 int oomb_tier_log(oomb_tier_t t, oomb_event* out, int64_t cap, int64_t* n) {

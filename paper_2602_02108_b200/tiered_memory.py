@@ -228,12 +228,21 @@ class TieredEngine:
     def d2h_bytes(self):
         return int(self._stats()[4])
 
+    def _moved(self) -> tuple[int, int]:
+        h, d = C.c_int64(), C.c_int64()
+        call("oomb_tier_moved_bytes", self.handle, C.byref(h), C.byref(d))
+        return h.value, d.value
+
     def h2d_bytes_moved(self) -> int:
         """Real engine: host->device bytes actually copied (h2d_bytes counts every fetch decision, as the
         reference does; a page fetched back into its still-unused victim slots moves nothing)."""
-        n = C.c_int64()
-        call("oomb_tier_moved_bytes", self.handle, C.byref(n))
-        return n.value
+        return self._moved()[0]
+
+    def d2h_bytes_moved(self) -> int:
+        """Real engine: device->host bytes actually copied (d2h_bytes counts every write-back decision;
+        a write-back is deferred until the freed slot is about to be reused, and dropped if the page is
+        fetched back first)."""
+        return self._moved()[1]
 
     def raw_log(self) -> np.ndarray:
         n = C.c_int64()

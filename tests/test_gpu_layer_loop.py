@@ -108,7 +108,8 @@ def test_native_loop_with_engine_matches_host_loop(regime):
 @pytest.mark.parametrize("slack", [512, 768])
 def test_victim_slot_reclaim_bitwise(slack):
     """Pages fetched back into their victim slots (the slots their eviction freed, not yet handed out
-    again) and pages copied in from the host tier mix within one step: every chunk's output, LSE,
+    again; their write-back deferred and then dropped, or already done) and pages copied in from the
+    host tier mix within one step: every chunk's output, LSE,
     dq and dk_cur / dv_cur (the dM_i read-back of the chunk's own pages: together the whole
     gradient pool) equal the all-resident run bit for bit, and the engine really did both (moved
     fewer bytes than the reference's accounting, but some)."""
@@ -142,7 +143,8 @@ def test_victim_slot_reclaim_bitwise(slack):
         torch.cuda.synchronize()
         cache.check_device_errors()
         if capped:
-            moved = (eng.h2d_bytes(0) + eng.h2d_bytes(1), eng.h2d_bytes_moved())
+            moved = (eng.h2d_bytes(0) + eng.h2d_bytes(1), eng.h2d_bytes_moved(), eng.d2h_bytes(),
+                     eng.d2h_bytes_moved())
         res[capped] = [x.clone() for x in (run.o_all, run.lse_all, grads.dq, grads.dk_cur, grads.dv_cur)]
         eng.release_all_reservations()
         eng.close(discard=True)
@@ -151,3 +153,4 @@ def test_victim_slot_reclaim_bitwise(slack):
     for a, b, what in zip(res[False], res[True], ("out", "lse", "dq", "dk_cur", "dv_cur")):
         assert torch.equal(a, b), (slack, what)
     assert 0 < moved[1] < moved[0], moved
+    assert 0 < moved[3] <= moved[2], moved  # deferred write-backs of pages fetched back are dropped

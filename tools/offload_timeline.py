@@ -38,7 +38,7 @@ def one(capped, timeline):
     log = eng.raw_log() if timeline else None
     if capped:
         print(f"h2d reference bytes {eng.h2d_bytes(0) + eng.h2d_bytes(1)}, moved {eng.h2d_bytes_moved()}, "
-              f"d2h {eng.d2h_bytes()}")
+              f"d2h {eng.d2h_bytes()}, moved {eng.d2h_bytes_moved()}")
     eng.release_all_reservations()
     eng.close(discard=True)
     del cache
