@@ -154,3 +154,43 @@ def test_victim_slot_reclaim_bitwise(slack):
         assert torch.equal(a, b), (slack, what)
     assert 0 < moved[1] < moved[0], moved
     assert 0 < moved[3] <= moved[2], moved  # deferred write-backs of pages fetched back are dropped
+
+
+def test_engine_loop_phase_split_equals_whole_step():
+    """With an engine attached, the forward-only call followed by the backward-only call is the same
+    step as one call: the same outputs, gradients, bytes moved and per-chunk records."""
+    import bench
+    from paper_2602_02108_b200 import PagedCache
+    from paper_2602_02108_b200.chunk_loop import layer_stats, layer_step
+    from paper_2602_02108_b200.tiered_memory import TierConfig, TieredEngine
+    cfg = dict(bench.CONFIGS["c3"])
+    cfg["T"] = 16 * 4096
+    run = bench.Run(cfg, seed=2024, device=torch.device("cuda", 0))
+    K = run.k_all
+    C, P = cfg["C"], cfg["P"]
+    n_pages = cfg["T"] // P
+    cap = int(0.75 * n_pages)
+    kv = (run.S, C, cfg["Hkv"], cfg["hd"])
+    res = []
+    for split in (False, True):
+        cache = PagedCache(run.mc, dtype="bf16", max_tokens=cfg["T"], device_capacity_pages=n_pages)
+        eng = TieredEngine(cache, TierConfig(device_capacity_pages=cap, bandwidth_bytes_per_s=55e9))
+        eng.set_prefetch_headroom_pages(C // P)
+        args = (cache, 0, run.q_all, K.view(kv), run.v_all.view(kv), run.do_all, run.o_all, run.lse_all, run.grads)
+        if split:
+            layer_step(*args, mode="topk", phase="forward")
+            layer_step(*args, mode="topk", phase="backward")
+        else:
+            layer_step(*args, mode="topk")
+        torch.cuda.synchronize()
+        cache.check_device_errors()
+        res.append(([x.clone() for x in (run.o_all, run.lse_all, run.grads.dq, run.grads.dk_cur, run.grads.dv_cur)],
+                    layer_stats(cache), (eng.h2d_bytes(0), eng.h2d_bytes(1), eng.d2h_bytes())))
+        eng.release_all_reservations()
+        eng.close(discard=True)
+        del cache, eng
+        torch.cuda.empty_cache()
+    for a, b in zip(res[0][0], res[1][0]):
+        assert torch.equal(a, b)
+    assert res[0][1] == res[1][1] and res[0][2] == res[1][2]
+    assert res[0][2][0] > 0
