@@ -65,9 +65,7 @@ constexpr bool kF4Lean = OOMB_FWD4_LEAN != 0;
 #define OOMB_FWD4_X2 0  // softmax scale-subtract and row sums as packed fp32 pairs
 #endif
 constexpr bool kF4X2 = OOMB_FWD4_X2 != 0;
-#ifndef OOMB_FWD5
-#define OOMB_FWD5 0  // the shared-accumulator, three-S-buffer forward (attn_fwd_tc5_kernel)
-#endif
+
 
 struct F4Bars {
     uint64_t q_full;
@@ -379,306 +377,6 @@ __global__ void __launch_bounds__(384, 1)
     if (warp == 3) tmem_dealloc<512>(0);
 }
 
-// ===========================================================================
-// Variant 5 (OOMB_FWD5=1): one shared output accumulator, three S buffers.
-// TMEM: S0 [0,128) S1 [128,256) S2 [256,384) O [384,512). Block j goes to S buffer j % 3 and to
-// softmax group j % 2, so when a group finishes block j its next block's S (j + 2) was issued as
-// soon as PV(j - 1) freed that buffer: the group never waits for its own PV. Both groups' PV MMAs add
-// into the one O, so every row uses ONE reference max m_ref, fixed before any P: the max of the
-// row's logits in blocks 0 and 1 (one exchange between the groups). No rescale ever. A row whose
-// later logits exceed m_ref by more than kF5Guard (log2), or whose first two blocks were fully masked,
-// flags the tile; a flagged tile runs a second pass over the same blocks with m_ref = its exact row
-// max from the first, so P <= 1 there. O = acc / (l_0 + l_1), LSE = (m_ref + log2 l) ln 2.
-// ===========================================================================
-constexpr float kF5Guard = 64.0f;
-constexpr uint32_t kF5TmO = 384;
-
-struct F5Bars {
-    uint64_t q_full;
-    uint64_t k_full[kKSt], k_empty[kKSt], v_full[kVSt], v_empty[kVSt];
-    uint64_t s_full[3], p_full[3][kPChunks], o_done;
-    uint32_t tmem_base;
-    int again;  // a row of the tile needs the second pass
-};
-
-__global__ void __launch_bounds__(384, 1)
-    attn_fwd_tc5_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kc,
-                        const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kp,
-                        const __grid_constant__ CUtensorMap tm_vp, F4Params p) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    F5Bars* bars = reinterpret_cast<F5Bars*>(smem + kF4Bar);
-    const AttnGeom& g = p.g;
-    const int h = blockIdx.x;
-    const int qt = (g.C / kTile) - 1 - static_cast<int>(blockIdx.y);  // longest causal prefix first (LPT)
-    const int kvh = h / g.group;
-    const bool p64 = g.P == kHalf;
-    const int qp = (qt * kTile) / g.P;
-    const int sel_begin = p.sel_off[qp];
-    const int warp = warp_id(), lane = lane_id();
-
-    if (threadIdx.x == 0) {
-        if (smem_u32(smem) & 1023) __trap();
-        mbar_init(&bars->q_full, 1);
-        for (int i = 0; i < kKSt; ++i) {
-            mbar_init(&bars->k_full[i], 1);
-            mbar_init(&bars->k_empty[i], 1);
-        }
-        for (int i = 0; i < kVSt; ++i) {
-            mbar_init(&bars->v_full[i], 1);
-            mbar_init(&bars->v_empty[i], 1);
-        }
-        for (int i = 0; i < 3; ++i) {
-            mbar_init(&bars->s_full[i], 1);
-            for (int c = 0; c < kPChunks; ++c) mbar_init(&bars->p_full[i][c], 128);
-        }
-        mbar_init(&bars->o_done, 1);
-        bars->again = 0;
-        fence_barrier_init();
-    }
-    if (warp == 3) tmem_alloc<512>(&bars->tmem_base);
-    tc_fence_before();
-    HalfList hl{};
-    if (p64) hl = half_list_sync(p.sel_off, p.sel_ids, qt);
-    else __syncthreads();
-    tc_fence_after();
-    if (bars->tmem_base != 0) __trap();
-    const int n_past = p64 ? hl.blocks() : (p.sel_off[qp + 1] - sel_begin) * (g.P / kTile);
-    const int nb_all = n_past + (g.chunk_keys ? qt + 1 : 0);
-    const int zs = static_cast<int>(gridDim.z), z = static_cast<int>(blockIdx.z);
-    const int j0 = static_cast<int>(static_cast<int64_t>(nb_all) * z / zs);
-    const int nb = static_cast<int>(static_cast<int64_t>(nb_all) * (z + 1) / zs) - j0;
-    uint8_t* sQ = smem + kF4Q;
-    uint8_t* sK = smem + kF4K;
-    uint8_t* sV = smem + kF4V;
-    // softmax state that survives the pass boundary (a thread = a query row)
-    float m_true = -INFINITY;  // the row's exact max over all its blocks (log2 units), after pass 0
-
-    for (int pass = 0; pass < 2; ++pass) {
-        const int base = pass * nb;  // running block counter: every barrier phase continues across passes
-        if (warp == 0 || warp == 2) {
-            if (lane == 0) {  // w0: Q (pass 0) + K, w2: V
-                const bool is_k = warp == 0;
-                const int nst = is_k ? kKSt : kVSt;
-                uint8_t* sb = is_k ? sK : sV;
-                uint64_t* full = is_k ? bars->k_full : bars->v_full;
-                uint64_t* empty = is_k ? bars->k_empty : bars->v_empty;
-                const CUtensorMap* mp = is_k ? &tm_kp : &tm_vp;
-                const CUtensorMap* mc = is_k ? &tm_kc : &tm_vc;
-                if (is_k && pass == 0) {
-                    mbar_expect_tx(&bars->q_full, kTileBytes);
-                    for (int r = 0; r < 2; ++r) tma_load_3d(sQ + r * kRegion, &tm_q, &bars->q_full, r * 64, h, qt * kTile);
-                }
-                for (int j = 0; j < nb; ++j) {
-                    const int jj = base + j, st = jj % nst;
-                    if (jj >= nst) mbar_wait(&empty[st], ((jj / nst) - 1) & 1);
-                    mbar_expect_tx(&full[st], kTileBytes);
-                    uint8_t* dst = sb + st * kTileBytes;
-                    const int jb = j0 + j;
-                    if (jb < n_past && p64) {
-                        for (int hh = 0; hh < 2; ++hh) {
-                            const int row = past_half_row(g, p.sel_ids, p.kvslot, hl, 2 * jb + hh, kvh, is_k ? p.err : nullptr);
-                            for (int r = 0; r < 2; ++r)
-                                tma_load_2d(dst + r * kRegion + hh * (kRegion / 2), mp, &full[st], r * 64, row);
-                        }
-                    } else if (jb < n_past) {
-                        const PastBlock b = past_block(g, p.sel_ids, p.kvslot, sel_begin, jb, kvh, is_k ? p.err : nullptr);
-                        for (int r = 0; r < 2; ++r) tma_load_2d(dst + r * kRegion, mp, &full[st], r * 64, b.row);
-                    } else {
-                        for (int r = 0; r < 2; ++r)
-                            tma_load_3d(dst + r * kRegion, mc, &full[st], r * 64, kvh, (jb - n_past) * kTile);
-                    }
-                }
-            }
-        } else if (warp == 1) {
-            // MMA warp: S(0) S(1) S(2) | PV(0) S(3) | PV(1) S(4) | ... | PV(nb-1)
-            constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kTile, 0, 0);
-            constexpr uint32_t idesc_o = make_idesc_bf16(kTile, kHd, 0, 1);
-            const uint64_t dQ = sdesc_k(smem_u32(sQ));
-            const uint64_t dK = sdesc_k(smem_u32(sK));
-            const uint64_t dVmn = sdesc_mn(smem_u32(sV), kRegion);
-            if (pass == 0) mbar_wait(&bars->q_full, 0);
-            auto mma_s = [&](int j) {
-                const int jj = base + j, st = jj % kKSt, b = jj % 3;
-                mbar_wait(&bars->k_full[st], (jj / kKSt) & 1);
-                tc_fence_after();
-                const uint64_t so = boff(st * kTileBytes);
-#pragma unroll
-                for (int ks = 0; ks < kHd / 16; ++ks)
-                    umma_ss_w(kTmS + b * 128, dQ + koff(ks, kRegion), dK + so + koff(ks, kRegion), idesc_s, ks);
-                umma_commit_w(&bars->s_full[b]);
-                umma_commit_w(&bars->k_empty[st]);
-            };
-            auto mma_pv = [&](int j) {
-                const int jj = base + j, st = jj % kVSt, b = jj % 3;
-                mbar_wait(&bars->v_full[st], (jj / kVSt) & 1);
-                const uint64_t so = boff(st * kTileBytes);
-                const uint32_t first = j == 0 ? 0u : 1u;  // the pass's first block overwrites O
-                constexpr int kStepsPerChunk = kTile / 16 / kPChunks;
-#pragma unroll
-                for (int c = 0; c < kPChunks; ++c) {
-                    mbar_wait(&bars->p_full[b][c], (jj / 3) & 1);
-                    tc_fence_after();
-#pragma unroll
-                    for (int i = 0; i < kStepsPerChunk; ++i) {
-                        const int ks = c * kStepsPerChunk + i;
-                        umma_ts_w(kF5TmO, kTmS + b * 128 + ks * 8, dVmn + so + mnoff(ks), idesc_o, (c | i) ? 1u : first);
-                    }
-                }
-                umma_commit_w(&bars->v_empty[st]);
-            };
-            for (int j = 0; j < 3 && j < nb; ++j) mma_s(j);
-            for (int j = 0; j < nb; ++j) {
-                mma_pv(j);
-                if (j + 3 < nb) mma_s(j + 3);  // S(j+3) rewrites the buffer PV(j) read: issued after it
-            }
-            umma_commit_w(&bars->o_done);
-        } else if (warp >= 4) {
-            const int quarter = warp & 3, wg = (warp - 4) >> 2;
-            const int r = quarter * 32 + lane;  // query row = TMEM lane
-            const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-            uint8_t* nvt = smem + kF4Nv;
-            uint16_t* hvt = reinterpret_cast<uint16_t*>(nvt);
-            if (pass == 0) {
-                if (p64) stage_half_valid(g, p.sel_ids, hl, hvt, kF4NvCap / 2, threadIdx.x - 128, 256);
-                else stage_past_valid(g, p.sel_ids, sel_begin, n_past, nvt, kF4NvCap, threadIdx.x - 128, 256);
-                named_bar_sync(3, 256);
-            }
-            const float sl2 = g.scale * kLog2e;
-            float2* red = reinterpret_cast<float2*>(smem + kF4Red);
-            float m_ref = pass == 0 ? -INFINITY : m_true;
-            float m_seen = -INFINITY;
-            float l = 0.f;
-            for (int j = wg; j < nb || (pass == 0 && j == wg); j += 2) {
-                const bool have = j < nb;
-                float mx = -INFINITY;
-                uint32_t sr[128];
-                const int jj = base + j, b = jj % 3;
-                const uint32_t tS = kTmS + b * 128 + lane_off;
-                if (have) {
-                    int lo, hi;
-                    const int jb = j0 + j;
-                    if (jb < n_past && p64) {
-                        lo = half_lim(half_valid(g, p.sel_ids, hl, hvt, kF4NvCap / 2, 2 * jb), r);
-                        hi = kHalf + half_lim(half_valid(g, p.sel_ids, hl, hvt, kF4NvCap / 2, 2 * jb + 1), r);
-                    } else {
-                        lo = (jb < n_past) ? past_valid(g, p.sel_ids, sel_begin, nvt, kF4NvCap, jb) - 1
-                                           : ((jb - n_past == qt) ? r : kTile - 1);
-                        hi = lo;
-                    }
-                    mbar_wait(&bars->s_full[b], (jj / 3) & 1);
-                    tc_fence_after();
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-                    tmem_wait_ld();
-                    if (lo < kHalf - 1 || hi < kTile - 1) {
-#pragma unroll
-                        for (int c = 0; c < kTile; ++c)
-                            if (c > (c < kHalf ? lo : hi)) sr[c] = __float_as_uint(-INFINITY);
-                    }
-                    float mx8[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) mx8[u] = __uint_as_float(sr[u]);
-#pragma unroll
-                    for (int c = 8; c < kTile; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
-                    mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
-                    m_seen = fmaxf(m_seen, mx);
-                }
-                if (pass == 0 && j == wg) {  // the reference max: the row's max over blocks 0 and 1
-                    red[wg * 128 + r] = make_float2(mx, 0.f);
-                    named_bar_sync(2, 256);
-                    m_ref = fmaxf(mx, red[(wg ^ 1) * 128 + r].x);
-                    named_bar_sync(2, 256);  // both read before the slots are reused below
-                    if (!have) break;
-                }
-                const float m_use = m_ref == -INFINITY ? 0.f : m_ref;  // (a fully masked row: pass 1 redoes it)
-                float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-                for (int c4 = 0; c4 < 4; ++c4) {
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) {
-                        const float x0 = fmaf(__uint_as_float(sr[c4 * 32 + 2 * u]), sl2, -m_use);
-                        const float x1 = fmaf(__uint_as_float(sr[c4 * 32 + 2 * u + 1]), sl2, -m_use);
-                        const float e0 = ex2(x0);
-                        const float e1 = (kF4Poly && (u & 1)) ? (kF4Lean ? ex2_lean(x1) : ex2_poly(x1)) : ex2(x1);
-                        rs8[(2 * u) & 7] += e0;
-                        rs8[(2 * u + 1) & 7] += e1;
-                        pk[u] = pack_bf16(e0, e1);
-                    }
-                    tmem_st16(tS + c4 * 16, pk);
-                    if ((c4 + 1) % (4 / kPChunks) == 0) {
-                        tmem_wait_st();
-                        tc_fence_before();
-                        mbar_arrive(&bars->p_full[b][c4 / (4 / kPChunks)]);
-                    }
-                }
-                l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
-            }
-            // both groups' row maxima and row sums
-            red[wg * 128 + r] = make_float2(m_seen, l);
-            named_bar_sync(2, 256);
-            const float2 o = red[(wg ^ 1) * 128 + r];
-            const float l0 = wg ? o.y : l, l1 = wg ? l : o.y;
-            const float lt = l0 + l1;  // 0 only for a page-range shard that attended no key
-            if (pass == 0) {
-                m_true = fmaxf(m_seen, o.x);
-                if ((m_ref == -INFINITY && m_true != -INFINITY) || m_true > m_ref + kF5Guard) bars->again = 1;
-            }
-            named_bar_sync(2, 256);
-            if (pass == 0) {
-                __syncthreads();  // (A) the decision, with the other warps
-                if (bars->again) {
-                    __syncthreads();  // (B)
-                    continue;
-                }
-            }
-            mbar_wait(&bars->o_done, pass & 1);
-            tc_fence_after();
-            const int t = qt * kTile + r;
-            __nv_bfloat16* orow = p.out + (static_cast<int64_t>(t) * g.Hq + h) * g.hd + wg * 64;
-            float* prow = p.o_part ? p.o_part + ((static_cast<int64_t>(z) * g.C + t) * g.Hq + h) * g.hd + wg * 64 : nullptr;
-            const float sc = lt > 0.f ? 1.f / lt : 0.f;
-#pragma unroll 1
-            for (int c = 0; c < (wg * 64 < g.hd ? 4 : 0); ++c) {
-                uint32_t x0[16];
-                tmem_ld16(kF5TmO + wg * 64 + c * 16 + lane_off, x0);
-                tmem_wait_ld();
-                float f[16];
-#pragma unroll
-                for (int u = 0; u < 16; ++u) f[u] = sc != 0.f ? __uint_as_float(x0[u]) * sc : 0.f;
-                if (prow) {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        *reinterpret_cast<float4*>(prow + c * 16 + 4 * u) = make_float4(f[4 * u], f[4 * u + 1], f[4 * u + 2], f[4 * u + 3]);
-                } else {
-                    *reinterpret_cast<uint4*>(orow + c * 16) = pack8(f);
-                    *reinterpret_cast<uint4*>(orow + c * 16 + 8) = pack8(f + 8);
-                }
-            }
-            if (wg == 0) {
-                const float L = lt > 0.f ? (m_ref + __log2f(lt)) * kLn2 : -INFINITY;
-                if (p.lse_part) p.lse_part[(static_cast<int64_t>(z) * g.C + t) * g.Hq + h] = L;
-                else p.lse[static_cast<int64_t>(t) * g.Hq + h] = L;
-            }
-            break;
-        }
-        if (warp < 4) {  // producers, MMA, allocator: the same decision points as the softmax warps
-            if (pass == 0) {
-                __syncthreads();  // (A)
-                if (bars->again) {
-                    __syncthreads();  // (B)
-                    continue;
-                }
-            }
-            break;
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 3) tmem_dealloc<512>(0);
-}
-
 // Exact merge of the split-K partials, splits in z order (deterministic): LSE = m + ln sum_z
 // e^(LSE_z - m), O = sum_z e^(LSE_z - LSE) O_z. One warp per (token, head) row; hd <= 128.
 __global__ void fwd_split_merge_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part, int zs,
@@ -748,15 +446,8 @@ void launch_attn_fwd_tc4(const AttnGeom& g, const TcPoolMaps& maps, const void* 
         OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p.o_part), zs * rows * g.hd * sizeof(float), st));
         OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p.lse_part), zs * rows * sizeof(float), st));
     }
-    if (OOMB_FWD5) {
-        if (first_use_on_device(5))
-            OOMB_CUDA(cudaFuncSetAttribute(attn_fwd_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kF4Smem));
-        attn_fwd_tc5_kernel<<<dim3(g.Hq, g.C / kTile, zs), 384, kF4Smem, st>>>(tq, tkc, tvc, maps.kpool, maps.vpool, p);
-        check_launch("attn_fwd_tc5_kernel");
-    } else {
-        attn_fwd_tc4_kernel<<<dim3(g.Hq, g.C / kTile, zs), 384, kF4Smem, st>>>(tq, tkc, tvc, maps.kpool, maps.vpool, p);
-        check_launch("attn_fwd_tc4_kernel");
-    }
+    attn_fwd_tc4_kernel<<<dim3(g.Hq, g.C / kTile, zs), 384, kF4Smem, st>>>(tq, tkc, tvc, maps.kpool, maps.vpool, p);
+    check_launch("attn_fwd_tc4_kernel");
     if (zs > 1) {
         fwd_split_merge_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(
             p.o_part, p.lse_part, zs, rows, g.hd, static_cast<__nv_bfloat16*>(out), lse);
