@@ -105,18 +105,21 @@ def test_native_loop_with_engine_matches_host_loop(regime):
     assert host[2][0] > 0 and host[2][2] > 0, "the capped tier must move pages both ways"
 
 
+@pytest.mark.parametrize("lazy", [False, True])
 @pytest.mark.parametrize("slack", [512, 768])
-def test_victim_slot_reclaim_bitwise(slack):
+def test_victim_slot_reclaim_bitwise(slack, lazy, monkeypatch):
     """Pages fetched back into their victim slots (the slots their eviction freed, not yet handed out
-    again; their write-back deferred and then dropped, or already done) and pages copied in from the
-    host tier mix within one step: every chunk's output, LSE,
+    again) and pages copied in from the host tier mix within one step: every chunk's output, LSE,
     dq and dk_cur / dv_cur (the dM_i read-back of the chunk's own pages: together the whole
     gradient pool) equal the all-resident run bit for bit, and the engine really did both (moved
-    fewer bytes than the reference's accounting, but some)."""
+    fewer bytes than the reference's accounting, but some). lazy: write-backs deferred until a
+    freed slot nears reuse and dropped for pages fetched back first (OOMB_TIER_LAZY_WB=1, read at
+    engine creation)."""
     import bench
     from paper_2602_02108_b200 import PagedCache
     from paper_2602_02108_b200 import attention as A
     from paper_2602_02108_b200.chunk_loop import layer_step
+    monkeypatch.setenv("OOMB_TIER_LAZY_WB", "1" if lazy else "0")
     from paper_2602_02108_b200.tiered_memory import TierConfig, TieredEngine
     cfg = dict(bench.CONFIGS["c3"])
     cfg["T"] = 128 * 4096  # 4,096 pages: the tier holds 3,072, the pool 3,072 + slack
@@ -154,6 +157,8 @@ def test_victim_slot_reclaim_bitwise(slack):
         assert torch.equal(a, b), (slack, what)
     assert 0 < moved[1] < moved[0], moved
     assert 0 < moved[3] <= moved[2], moved  # deferred write-backs of pages fetched back are dropped
+    if lazy:
+        assert moved[3] < moved[2], moved
 
 
 def test_engine_loop_phase_split_equals_whole_step():
