@@ -55,6 +55,20 @@ constexpr int kKvPolyN = OOMB_KV_POLY_N;  // dK/dV kernel: the same for P^T
 __device__ __forceinline__ float ex2_mix(float x, int c, int n) {
     return (n > 0 && c % n == n - 1) ? (OOMB_POLY_LEAN ? ex2_lean(x) : ex2_poly(x)) : ex2(x);
 }
+// Elements c, c + 1 (c even): 1 pair in n on the FMA pipe as a packed pair (ex2_lean2: 10 issue
+// slots for two exponentials instead of 16), the others on the MUFU. n = 0: all on the MUFU.
+__device__ __forceinline__ float2 ex2_pair(float2 x, int c, int n) {
+    if (n > 0 && (c >> 1) % n == n - 1) return ex2_lean2(x);
+    return make_float2(ex2(x.x), ex2(x.y));
+}
+#ifndef OOMB_DQ_PAIR_N
+#define OOMB_DQ_PAIR_N 4  // dQ: 1 pair in N of P's exponentials as an FMA-pipe packed pair (replaces
+                          // OOMB_DQ_POLY_N): 42.13 -> 41.62 ms serialized (256K c3)
+#endif
+#ifndef OOMB_KV_PAIR_N
+#define OOMB_KV_PAIR_N 4  // the same for the dK/dV kernel's P^T: 57.53 -> 56.01 ms (N = 2: 56.30)
+#endif
+constexpr int kDqPairN = OOMB_DQ_PAIR_N, kKvPairN = OOMB_KV_PAIR_N;
 
 #ifndef OOMB_BWD_LPT
 #define OOMB_BWD_LPT 1  // dK/dV units longest first (bwd_order_kernel); 0: own blocks, then union order
@@ -507,11 +521,19 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                     for (int c = 0; c < 32; c += 2) {
                         const float2 x = fma2(make_float2(__uint_as_float(a[c]), __uint_as_float(a[c + 1])), s2, nl2);
-                        pr[c] = ex2_mix(x.x, c, kDqPolyN);
-                        pr[c + 1] = ex2_mix(x.y, c + 1, kDqPolyN);
                         const float2 y = fma2(make_float2(__uint_as_float(b2[c]), __uint_as_float(b2[c + 1])), s2, nl2);
-                        pr[32 + c] = ex2_mix(y.x, 32 + c, kDqPolyN);
-                        pr[33 + c] = ex2_mix(y.y, 33 + c, kDqPolyN);
+                        if (kDqPairN > 0) {
+                            const float2 ex = ex2_pair(x, c, kDqPairN), ey = ex2_pair(y, 32 + c, kDqPairN);
+                            pr[c] = ex.x;
+                            pr[c + 1] = ex.y;
+                            pr[32 + c] = ey.x;
+                            pr[33 + c] = ey.y;
+                        } else {
+                            pr[c] = ex2_mix(x.x, c, kDqPolyN);
+                            pr[c + 1] = ex2_mix(x.y, c + 1, kDqPolyN);
+                            pr[32 + c] = ex2_mix(y.x, 32 + c, kDqPolyN);
+                            pr[33 + c] = ex2_mix(y.y, 33 + c, kDqPolyN);
+                        }
                     }
                 } else {
 #pragma unroll
@@ -1020,10 +1042,29 @@ __global__ void __launch_bounds__(kKvThreads, 1)
                                                     s2, make_float2(-l4.x, -l4.y));
                             const float2 x23 = fma2(make_float2(__uint_as_float(sv[4 * c4 + 2]), __uint_as_float(sv[4 * c4 + 3])),
                                                     s2, make_float2(-l4.z, -l4.w));
-                            pr[c + 0] = ex2_mix(x01.x, c + 0, kKvPolyN);
-                            pr[c + 1] = ex2_mix(x01.y, c + 1, kKvPolyN);
-                            pr[c + 2] = ex2_mix(x23.x, c + 2, kKvPolyN);
-                            pr[c + 3] = ex2_mix(x23.y, c + 3, kKvPolyN);
+                            if (kKvPairN > 0) {
+                                const float2 e01 = ex2_pair(x01, c, kKvPairN), e23 = ex2_pair(x23, c + 2, kKvPairN);
+                                pr[c + 0] = e01.x;
+                                pr[c + 1] = e01.y;
+                                pr[c + 2] = e23.x;
+                                pr[c + 3] = e23.y;
+                            } else {
+                                pr[c + 0] = ex2_mix(x01.x, c + 0, kKvPolyN);
+                                pr[c + 1] = ex2_mix(x01.y, c + 1, kKvPolyN);
+                                pr[c + 2] = ex2_mix(x23.x, c + 2, kKvPolyN);
+                                pr[c + 3] = ex2_mix(x23.y, c + 3, kKvPolyN);
+                            }
+                        } else if (kKvPairN > 0) {
+                            const float2 e01 = ex2_pair(make_float2(fmaf(__uint_as_float(sv[4 * c4 + 0]), sl2, -l4.x),
+                                                                    fmaf(__uint_as_float(sv[4 * c4 + 1]), sl2, -l4.y)),
+                                                        c, kKvPairN);
+                            const float2 e23 = ex2_pair(make_float2(fmaf(__uint_as_float(sv[4 * c4 + 2]), sl2, -l4.z),
+                                                                    fmaf(__uint_as_float(sv[4 * c4 + 3]), sl2, -l4.w)),
+                                                        c + 2, kKvPairN);
+                            pr[c + 0] = e01.x;
+                            pr[c + 1] = e01.y;
+                            pr[c + 2] = e23.x;
+                            pr[c + 3] = e23.y;
                         } else {
                             pr[c + 0] = ex2_mix(fmaf(__uint_as_float(sv[4 * c4 + 0]), sl2, -l4.x), c + 0, kKvPolyN);
                             pr[c + 1] = ex2_mix(fmaf(__uint_as_float(sv[4 * c4 + 1]), sl2, -l4.y), c + 1, kKvPolyN);

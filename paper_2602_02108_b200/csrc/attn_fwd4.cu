@@ -65,6 +65,11 @@ constexpr bool kF4Lean = OOMB_FWD4_LEAN != 0;
 #define OOMB_FWD4_X2 0  // softmax scale-subtract and row sums as packed fp32 pairs
 #endif
 constexpr bool kF4X2 = OOMB_FWD4_X2 != 0;
+#ifndef OOMB_FWD4_PAIR_N
+#define OOMB_FWD4_PAIR_N 0  // 1 pair in N of the exponentials as an FMA-pipe packed pair (ex2_lean2);
+                            // measured N = 4: 38.54 vs 35.85 ms serialized (slower)
+#endif
+constexpr int kF4PairN = OOMB_FWD4_PAIR_N;
 
 
 struct F4Bars {
@@ -297,9 +302,16 @@ __global__ void __launch_bounds__(384, 1)
                         x0 = fmaf(__uint_as_float(sr[c4 * 32 + 2 * u]), sl2, -m_use);
                         x1 = fmaf(__uint_as_float(sr[c4 * 32 + 2 * u + 1]), sl2, -m_use);
                     }
-                    const float e0 = ex2(x0);
-                    // 1 in 4 on the FMA pipe
-                    const float e1 = (kF4Poly && (u & 1)) ? (kF4Lean ? ex2_lean(x1) : ex2_poly(x1)) : ex2(x1);
+                    float e0, e1;
+                    if (kF4PairN > 0 && (u % kF4PairN) == kF4PairN - 1) {  // a packed pair on the FMA pipe
+                        const float2 e = ex2_lean2(make_float2(x0, x1));
+                        e0 = e.x;
+                        e1 = e.y;
+                    } else {
+                        e0 = ex2(x0);
+                        // 1 in 4 on the FMA pipe
+                        e1 = (kF4Poly && (u & 1)) ? (kF4Lean ? ex2_lean(x1) : ex2_poly(x1)) : ex2(x1);
+                    }
                     if (kF4X2 && (u & 1)) {  // row sums as packed pairs too (same additions, same order)
                         const float2 a = add2(make_float2(rs8[(2 * u - 2) & 7], rs8[(2 * u - 1) & 7]),
                                               make_float2(pe0, pe1));

@@ -49,6 +49,10 @@ __global__ void k(int iters, float* out, long long* clk) {
             } else if (V == 7) {
                 e0 = (u & 1) ? ex2_lean(x0) : ex2(x0);
                 e1 = ex2_lean(x1);
+            } else if ((V == 9 && (u & 3) == 3) || (V == 10 && (u & 1))) {
+                const float2 e = ex2_lean2(make_float2(x0, x1));
+                e0 = e.x;
+                e1 = e.y;
             } else {
                 e0 = ex2(x0);
                 e1 = ex2(x1);
@@ -79,10 +83,12 @@ int main() {
     cudaMalloc(&clk, 148 * sizeof(long long));
     const char* nm[] = {"full (ld32, 32 FFMA+ex2, pack, st16)", "no MUFU (FMA instead of ex2)", "no TMEM store",
                         "no TMEM load (registers)", "no pack / store", "1 in 4 exp2 on FMA (lean)",
-                        "1 in 2 exp2 on FMA (lean)", "3 in 4 exp2 on FMA (lean)"};
+                        "1 in 2 exp2 on FMA (lean)", "3 in 4 exp2 on FMA (lean)", "", "1 in 4 on FMA, packed pairs",
+                        "1 in 2 on FMA, packed pairs"};
     const int iters = 4096;
     for (int w : {4, 8, 16}) {
-        for (int v = 0; v < 8; ++v) {
+        for (int v = 0; v < 11; ++v) {
+            if (v == 8) continue;
             if (v == 0) k<0><<<148, w * 32>>>(iters, out, clk);
             if (v == 1) k<1><<<148, w * 32>>>(iters, out, clk);
             if (v == 2) k<2><<<148, w * 32>>>(iters, out, clk);
@@ -91,6 +97,8 @@ int main() {
             if (v == 5) k<5><<<148, w * 32>>>(iters, out, clk);
             if (v == 6) k<6><<<148, w * 32>>>(iters, out, clk);
             if (v == 7) k<7><<<148, w * 32>>>(iters, out, clk);
+            if (v == 9) k<9><<<148, w * 32>>>(iters, out, clk);
+            if (v == 10) k<10><<<148, w * 32>>>(iters, out, clk);
             long long c = 0;
             cudaMemcpy(&c, clk, sizeof(c), cudaMemcpyDeviceToHost);
             // elements per SM per clock: w warps x 32 lanes x 32 elements per iteration
