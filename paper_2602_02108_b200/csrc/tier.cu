@@ -191,23 +191,33 @@ struct oomb_tier_s {
         log.push_back(le);
     }
 
-    // ---- batched page copies (real mode): one cudaMemcpyBatchAsync per direction and operation
+    // ---- queued page copies (real mode): flushed per direction and operation as one
+    // cudaMemcpyAsync per run of copies that are contiguous on both sides (adjacent slots of
+    // adjacent host blocks merge into one transfer)
     std::vector<void*> cp_dst[2], cp_src[2];
     std::vector<size_t> cp_size[2];
+    int64_t copy_calls = 0;              // diagnostics: cudaMemcpyAsync calls issued by flushes
     cudaEvent_t d2h_batch_ev = nullptr;  // the current write-back batch's completion stamp
     void queue_copy(int dir, void* dst, const void* src, size_t n) {  // dir 0: H2D, 1: D2H
-        cp_dst[dir].push_back(dst);
-        cp_src[dir].push_back(const_cast<void*>(src));
-        cp_size[dir].push_back(n);
+        auto& d = cp_dst[dir];
+        auto& s = cp_src[dir];
+        auto& z = cp_size[dir];
+        if (!d.empty() && static_cast<uint8_t*>(d.back()) + z.back() == dst &&
+            static_cast<const uint8_t*>(s.back()) + z.back() == src) {
+            z.back() += n;  // extends the previous run on both sides
+            return;
+        }
+        d.push_back(dst);
+        s.push_back(const_cast<void*>(src));
+        z.push_back(n);
     }
     void flush_copies(int dir) {
         if (cp_dst[dir].empty()) return;
-        cudaMemcpyAttributes attr{};
-        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-        size_t idx0 = 0, fail = 0;
-        OOMB_CUDA(cudaMemcpyBatchAsync(cp_dst[dir].data(), cp_src[dir].data(), cp_size[dir].data(), cp_dst[dir].size(),
-                                       &attr, &idx0, 1, &fail, dir ? d2h_stream : h2d_stream));
+        const cudaStream_t st = dir ? d2h_stream : h2d_stream;
+        const cudaMemcpyKind kind = dir ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice;
+        for (size_t i = 0; i < cp_dst[dir].size(); ++i)
+            OOMB_CUDA(cudaMemcpyAsync(cp_dst[dir][i], cp_src[dir][i], cp_size[dir][i], kind, st));
+        copy_calls += static_cast<int64_t>(cp_dst[dir].size());
         cp_dst[dir].clear();
         cp_src[dir].clear();
         cp_size[dir].clear();

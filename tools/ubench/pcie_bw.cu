@@ -1,5 +1,6 @@
 // Host<->device copy throughput on the box: one large copy per direction, both directions at
-// once, and batches of page-sized copies (cudaMemcpyBatchAsync, as the offload engine issues them).
+// once, and runs of page-sized copies (one cudaMemcpyAsync per page-sized copy, as the offload engine
+// issues them).
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -75,17 +76,14 @@ int main() {
                     off += sizes[j];
                 }
             }
-            cudaMemcpyAttributes attr{};
-            attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-            attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-            size_t idx0 = 0, fail = 0;
             float best = 1e9, best2 = 1e9;
             for (int rep = 0; rep < 5; ++rep) {
                 CK(cudaEventRecord(a, s1));
                 CK(cudaStreamWaitEvent(s2, a, 0));
-                CK(cudaMemcpyBatchAsync(dst.data(), src.data(), sz.data(), sz.size(), &attr, &idx0, 1, &fail, s1));
-                if (both)
-                    CK(cudaMemcpyBatchAsync(dst2.data(), src2.data(), sz.data(), sz.size(), &attr, &idx0, 1, &fail, s2));
+                for (size_t j = 0; j < sz.size(); ++j) {
+                    CK(cudaMemcpyAsync(dst[j], src[j], sz[j], cudaMemcpyHostToDevice, s1));
+                    if (both) CK(cudaMemcpyAsync(dst2[j], src2[j], sz[j], cudaMemcpyDeviceToHost, s2));
+                }
                 CK(cudaEventRecord(b, s1));
                 CK(cudaEventRecord(c, s2));
                 CK(cudaEventSynchronize(b));
