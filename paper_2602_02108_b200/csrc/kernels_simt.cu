@@ -10,6 +10,7 @@
 // gradient pool dK, dV [Hkv][P][hd] fp32. Page tables map logical page ->
 // slot per layer (d_kvslot / d_gslot, -1 = none).
 
+#include <cstdlib>
 #include <cub/block/block_scan.cuh>
 
 #include "oomb_internal.h"
@@ -189,6 +190,72 @@ __global__ void append_kernel(const T* __restrict__ k, const T* __restrict__ v, 
     }
 }
 
+// Staged variant (no RoPE, 64-column slices, 16-byte aligned K / V): a CTA owns one page touched
+// and 64 columns of its [Hkv x hd] row. All rows of a 64-row segment are loaded at once with
+// 16-byte vectors (copied to the page as they arrive, K also into shared memory), then one thread
+// per column adds the segment's K rows in append order: the same add_rn sequence as append_kernel,
+// so the sums are bit-identical, with one load latency per segment instead of one per row batch.
+constexpr int kAppCols = 64, kAppRows = 64, kAppThreads = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kAppThreads)
+    append_staged_kernel(const T* __restrict__ k, const T* __restrict__ v, int64_t rows, int64_t filled, int P,
+                         int Hkv, int hd, int first_page, NewSlots ns, int32_t* __restrict__ kvslot,
+                         T* __restrict__ kpool, T* __restrict__ vpool, acc_t<T>* __restrict__ ksum,
+                         int32_t* __restrict__ kcnt, int* err, __nv_bfloat16* __restrict__ planes,
+                         int64_t plane_stride) {
+    constexpr int VE = 16 / sizeof(T);   // elements per 16-byte vector
+    constexpr int VPR = kAppCols / VE;   // vectors per 64-column row slice
+    __shared__ __align__(16) T sk[kAppRows][kAppCols];
+    const int re = Hkv * hd;
+    const int c0 = blockIdx.x * kAppCols;
+    const int h = c0 / hd, d0 = c0 - h * hd;
+    const int pg = first_page + blockIdx.y;
+    const int tid = threadIdx.x;
+    if (blockIdx.x == 0 && blockIdx.y == 0)
+        for (int i = tid; i < ns.n; i += blockDim.x) kvslot[ns.first_page + i] = ns.slot[i];
+    const bool is_new = pg >= ns.first_page && pg < ns.first_page + ns.n;
+    const int slot = is_new ? ns.slot[pg - ns.first_page] : kvslot[pg];
+    const int64_t s0 = max(filled, static_cast<int64_t>(pg) * P);
+    const int64_t s1 = min(filled + rows, static_cast<int64_t>(pg + 1) * P);
+    const bool store = slot >= 0;  // REMOTE pages get only their sums; -1: not resident (flagged)
+    if (slot == -1 && tid == 0 && blockIdx.x == 0) atomicOr(err, DERR_NOT_RESIDENT);
+    acc_t<T> sum = acc_t<T>(0);
+    if (tid < kAppCols && !is_new) sum = ksum[static_cast<int64_t>(pg) * re + c0 + tid];
+    const size_t dst0 = ((static_cast<size_t>(store ? slot : 0) * Hkv + h) * P) * hd + d0;
+    for (int64_t sb = s0; sb < s1; sb += kAppRows) {
+        const int n = static_cast<int>(min(static_cast<int64_t>(kAppRows), s1 - sb));
+        for (int idx = tid; idx < n * VPR; idx += kAppThreads) {
+            const int u = idx / VPR, j = idx - (idx / VPR) * VPR;
+            const int64_t r = sb + u - filled;
+            const uint4 kv = *reinterpret_cast<const uint4*>(k + r * re + c0 + j * VE);
+            const uint4 vv = *reinterpret_cast<const uint4*>(v + r * re + c0 + j * VE);
+            if (store) {
+                const size_t off = dst0 + static_cast<size_t>(sb + u - static_cast<int64_t>(pg) * P) * hd + j * VE;
+                *reinterpret_cast<uint4*>(kpool + off) = kv;
+                *reinterpret_cast<uint4*>(vpool + off) = vv;
+            }
+            *reinterpret_cast<uint4*>(&sk[u][j * VE]) = kv;
+        }
+        __syncthreads();
+        if (tid < kAppCols)
+            for (int u = 0; u < n; ++u) sum = add_rn(sum, to_a<acc_t<T>>(sk[u][tid]));
+        __syncthreads();
+    }
+    if (tid < kAppCols) {
+        ksum[static_cast<int64_t>(pg) * re + c0 + tid] = sum;
+        if (planes) {  // as append_kernel: the scorer's hi / lo bf16 planes of K_avg
+            const int cnt = static_cast<int>(s1 - static_cast<int64_t>(pg) * P);
+            const float kav = __fmul_rn(static_cast<float>(sum), __fdiv_rn(1.0f, static_cast<float>(cnt)));
+            const __nv_bfloat16 hi = __float2bfloat16_rn(kav);
+            const size_t at = (static_cast<size_t>(h) * plane_stride + pg) * hd + d0 + tid;
+            planes[at] = hi;
+            planes[at + static_cast<size_t>(Hkv) * plane_stride * hd] = __float2bfloat16_rn(kav - __bfloat162float(hi));
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0) kcnt[pg] = (is_new ? 0 : kcnt[pg]) + static_cast<int>(s1 - s0);
+}
+
 void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_t filled_before, int P, int Hkv,
                    int hd, int first_page, int n_pages_touched, const NewSlots& ns, int32_t* d_kvslot_layer,
                    void* kpool, void* vpool, void* kavg_sum_layer, int32_t* kavg_cnt_layer, int* d_err,
@@ -197,6 +264,28 @@ void launch_append(int dtype, const void* k, const void* v, int64_t rows, int64_
     __nv_bfloat16* planes = static_cast<__nv_bfloat16*>(kavg_planes_layer);
     ProfScope prof_(PK_APPEND, st);
     const int re = Hkv * hd;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+    if (!rope_inv_freq && hd % kAppCols == 0 && aligned && !std::getenv("OOMB_APPEND_UNSTAGED")) {
+        const dim3 sg(re / kAppCols, n_pages_touched);
+        if (dtype == OOMB_BF16)
+            append_staged_kernel<__nv_bfloat16><<<sg, kAppThreads, 0, st>>>(
+                static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), rows, filled_before, P,
+                Hkv, hd, first_page, ns, d_kvslot_layer, static_cast<__nv_bfloat16*>(kpool),
+                static_cast<__nv_bfloat16*>(vpool), static_cast<float*>(kavg_sum_layer), kavg_cnt_layer, d_err, planes,
+                plane_stride);
+        else if (dtype == OOMB_F64)
+            append_staged_kernel<double><<<sg, kAppThreads, 0, st>>>(
+                static_cast<const double*>(k), static_cast<const double*>(v), rows, filled_before, P, Hkv, hd,
+                first_page, ns, d_kvslot_layer, static_cast<double*>(kpool), static_cast<double*>(vpool),
+                static_cast<double*>(kavg_sum_layer), kavg_cnt_layer, d_err, nullptr, 0);
+        else
+            append_staged_kernel<float><<<sg, kAppThreads, 0, st>>>(
+                static_cast<const float*>(k), static_cast<const float*>(v), rows, filled_before, P, Hkv, hd,
+                first_page, ns, d_kvslot_layer, static_cast<float*>(kpool), static_cast<float*>(vpool),
+                static_cast<float*>(kavg_sum_layer), kavg_cnt_layer, d_err, nullptr, 0);
+        check_launch("append_staged_kernel");
+        return;
+    }
     dim3 grid((re + 127) / 128, n_pages_touched);
     if (dtype == OOMB_BF16)
         append_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(
