@@ -426,7 +426,11 @@ __global__ void __launch_bounds__(384, 1)
     } else if (warp == 1) {
         // MMA warp (converged). Order: S(0) dP(0) | S(1) dQ(0) dP(1) | S(2) dQ(1) dP(2) | ... dQ(nb-1).
         constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kTile, 0, 0);  // [128 q] x [128 keys], K = hd
-        constexpr uint32_t idesc_q = make_idesc_bf16(kTile, kHd, 0, 1);    // [128 q] x [hd], K = keys
+        // N = hd: at head dim 64 only the 64 real columns (the epilogue never reads the others)
+        const uint32_t idesc_q = make_idesc_bf16(kTile, g.hd == 64 ? 64 : kHd, 0, 1);  // [128 q] x [hd], K = keys
+        // K = hd contractions: at head dim 64 the k-steps over the zero-padded columns 64-127 would
+        // add exact zeros, so they are not issued
+        const int nks_hd = g.hd / 16;
         const uint64_t dK = sdesc_k(smem_u32(sK)), dV = sdesc_k(smem_u32(sV));
         const uint64_t dKmn = sdesc_mn(smem_u32(sK), kRegion);
         mbar_wait(&bars->qdo_tmem, 0);
@@ -439,7 +443,7 @@ __global__ void __launch_bounds__(384, 1)
             const uint64_t so = boff(st * kTileBytes);
 #pragma unroll
             for (int ks = 0; ks < kHd / 16; ++ks)
-                umma_ts_w(kDqTmS, kDqTmQ + ks * 8, dK + so + koff(ks, kRegion), idesc_s, ks);
+                if (ks < nks_hd) umma_ts_w(kDqTmS, kDqTmQ + ks * 8, dK + so + koff(ks, kRegion), idesc_s, ks);
             umma_commit_w(&bars->s_full);
         };
         auto mma_dp = [&](int j) {
@@ -449,7 +453,7 @@ __global__ void __launch_bounds__(384, 1)
             const uint64_t so = boff(st * kTileBytes);
 #pragma unroll
             for (int ks = 0; ks < kHd / 16; ++ks)
-                umma_ts_w(kDqTmDP, kDqTmDO + ks * 8, dV + so + koff(ks, kRegion), idesc_s, ks);
+                if (ks < nks_hd) umma_ts_w(kDqTmDP, kDqTmDO + ks * 8, dV + so + koff(ks, kRegion), idesc_s, ks);
             umma_commit_w(&bars->dp_full);
             umma_commit_w(&bars->v_empty[st]);
         };
@@ -902,7 +906,11 @@ __global__ void __launch_bounds__(kKvThreads, 1)
     } else if (warp == 1) {
         // MMA warp (converged).
         constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kTile, 0, 0);  // [128 keys] x [128 q], K = hd
-        constexpr uint32_t idesc_g = make_idesc_bf16(kTile, kHd, 0, 1);    // [128 keys] x [hd], K = q
+        // N = hd: at head dim 64 only the 64 real columns (the epilogue never reads the others)
+        const uint32_t idesc_g = make_idesc_bf16(kTile, g.hd == 64 ? 64 : kHd, 0, 1);  // [128 keys] x [hd], K = q
+        // K = hd contractions: at head dim 64 the k-steps over the zero-padded columns 64-127 would
+        // add exact zeros, so they are not issued
+        const int nks_hd = g.hd / 16;
         const uint64_t dK = sdesc_k(smem_u32(sK)), dV = sdesc_k(smem_u32(sV));
         const uint64_t dQ = sdesc_k(smem_u32(sQ)), dDO = sdesc_k(smem_u32(sDO));
         const uint64_t dQmn = sdesc_mn(smem_u32(sQ), kRegion), dDOmn = sdesc_mn(smem_u32(sDO), kRegion);
@@ -914,14 +922,14 @@ __global__ void __launch_bounds__(kKvThreads, 1)
             const uint64_t so = boff(st * kTileBytes);
 #pragma unroll
             for (int ks = 0; ks < kHd / 16; ++ks)
-                umma_ss_w(kTmS, dK + koff(ks, kRegion), dQ + so + koff(ks, kRegion), idesc_s, ks);
+                if (ks < nks_hd) umma_ss_w(kTmS, dK + koff(ks, kRegion), dQ + so + koff(ks, kRegion), idesc_s, ks);
             umma_commit_w(&bars->s_full);
         };
         auto mma_dp = [&](int gi) {
             const uint64_t so = boff((gi % kKvStages) * kTileBytes);
 #pragma unroll
             for (int ks = 0; ks < kHd / 16; ++ks)
-                umma_ss_w(kTmDP, dV + koff(ks, kRegion), dDO + so + koff(ks, kRegion), idesc_s, ks);
+                if (ks < nks_hd) umma_ss_w(kTmDP, dV + koff(ks, kRegion), dDO + so + koff(ks, kRegion), idesc_s, ks);
             umma_commit_w(&bars->dp_full);
         };
         auto mma_dv = [&](int gi, uint32_t first) {

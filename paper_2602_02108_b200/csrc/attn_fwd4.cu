@@ -180,7 +180,11 @@ __global__ void __launch_bounds__(384, 1)
     } else if (warp == 1) {
         // MMA warp (converged): S(0) S(1) | PV(0) S(2) | PV(1) S(3) | ... | PV(nb-1)
         constexpr uint32_t idesc_s = make_idesc_bf16(kTile, kTile, 0, 0);  // [128 q] x [128 keys], K = hd
-        constexpr uint32_t idesc_o = make_idesc_bf16(kTile, kHd, 0, 1);    // [128 q] x [hd], K = keys
+        // N = hd: at head dim 64 only the 64 real columns (the merge never reads the others)
+        const uint32_t idesc_o = make_idesc_bf16(kTile, g.hd == 64 ? 64 : kHd, 0, 1);  // [128 q] x [hd], K = keys
+        // K = hd contractions: at head dim 64 the k-steps over the zero-padded columns 64-127 would
+        // add exact zeros, so they are not issued
+        const int nks_hd = g.hd / 16;
         const uint64_t dQ = sdesc_k(smem_u32(sQ));
         const uint64_t dK = sdesc_k(smem_u32(sK));
         const uint64_t dVmn = sdesc_mn(smem_u32(sV), kRegion);
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(384, 1)
             const uint64_t so = boff(st * kTileBytes);
 #pragma unroll
             for (int ks = 0; ks < kHd / 16; ++ks)
-                umma_ss_w(kTmS + b * 128, dQ + koff(ks, kRegion), dK + so + koff(ks, kRegion), idesc_s, ks);
+                if (ks < nks_hd) umma_ss_w(kTmS + b * 128, dQ + koff(ks, kRegion), dK + so + koff(ks, kRegion), idesc_s, ks);
             umma_commit_w(&bars->s_full[b]);
             umma_commit_w(&bars->k_empty[st]);
         };

@@ -51,6 +51,23 @@ __global__ void table_update_kernel(TableUpdates u, int32_t* kvslot, int32_t* gs
     }
 }
 
+// Staged page moves: a flush's pieces are packed back to back in a device staging buffer, so the
+// host link sees one cudaMemcpyAsync per run of host-contiguous pieces (a page's K | V, or dK | dV,
+// and pages with adjacent ids) instead of one per piece, and the scatter into (gather out of) the
+// pool's slots is one kernel over HBM. One CTA per piece, 16-byte vectors.
+struct StagePiece {
+    uint8_t* dev;  // the piece's place in a pool (K, V, dK or dV slot)
+    int64_t off;   // its offset in the staging buffer
+    int64_t n;     // bytes (a multiple of 16)
+};
+
+__global__ void stage_move_kernel(const StagePiece* __restrict__ pc, uint8_t* __restrict__ stg, int to_pool) {
+    const StagePiece q = pc[blockIdx.x];
+    uint4* a = reinterpret_cast<uint4*>(to_pool ? q.dev : stg + q.off);
+    const uint4* b = reinterpret_cast<const uint4*>(to_pool ? stg + q.off : q.dev);
+    for (int64_t i = threadIdx.x; i < q.n / 16; i += blockDim.x) a[i] = b[i];
+}
+
 }  // namespace oomb
 
 using namespace oomb;
@@ -211,16 +228,74 @@ struct oomb_tier_s {
         s.push_back(const_cast<void*>(src));
         z.push_back(n);
     }
+    // OOMB_TIER_STAGED=0: one cudaMemcpyAsync per queued run, straight between host block and slot
+    const bool staged = [] {
+        const char* e = std::getenv("OOMB_TIER_STAGED");
+        return !(e && e[0] == '0');
+    }();
+    std::vector<StagePiece> stage_pcs;
     void flush_copies(int dir) {
-        if (cp_dst[dir].empty()) return;
+        auto& dv = cp_dst[dir];
+        auto& sv = cp_src[dir];
+        auto& zv = cp_size[dir];
+        if (dv.empty()) return;
         const cudaStream_t st = dir ? d2h_stream : h2d_stream;
         const cudaMemcpyKind kind = dir ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice;
-        for (size_t i = 0; i < cp_dst[dir].size(); ++i)
-            OOMB_CUDA(cudaMemcpyAsync(cp_dst[dir][i], cp_src[dir][i], cp_size[dir][i], kind, st));
-        copy_calls += static_cast<int64_t>(cp_dst[dir].size());
-        cp_dst[dir].clear();
-        cp_src[dir].clear();
-        cp_size[dir].clear();
+        const size_t n = dv.size();
+        bool aligned = true;
+        for (size_t i = 0; i < n; ++i)
+            aligned = aligned && ((reinterpret_cast<uintptr_t>(dv[i]) | reinterpret_cast<uintptr_t>(sv[i]) | zv[i]) & 15) == 0;
+        if (!staged || n < 3 || !aligned) {
+            for (size_t i = 0; i < n; ++i) OOMB_CUDA(cudaMemcpyAsync(dv[i], sv[i], zv[i], kind, st));
+            copy_calls += static_cast<int64_t>(n);
+        } else {
+            // pieces back to back in staging; the device side of each piece is the pool side
+            stage_pcs.resize(n);
+            int64_t total = 0;
+            for (size_t i = 0; i < n; ++i) {
+                stage_pcs[i].dev = static_cast<uint8_t*>(dir ? sv[i] : dv[i]);
+                stage_pcs[i].off = total;
+                stage_pcs[i].n = static_cast<int64_t>(zv[i]);
+                total += stage_pcs[i].n;
+            }
+            const int64_t desc_off = (total + 255) & ~int64_t(255);
+            uint8_t* stg = nullptr;
+            OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&stg), desc_off + n * sizeof(StagePiece), st));
+            auto* desc = reinterpret_cast<StagePiece*>(stg + desc_off);
+            // pageable source: the call returns once the descriptors are staged by the driver
+            OOMB_CUDA(cudaMemcpyAsync(desc, stage_pcs.data(), n * sizeof(StagePiece), cudaMemcpyHostToDevice, st));
+            // host runs: consecutive pieces whose host blocks are adjacent move in one copy
+            auto host_runs = [&](auto&& copy) {
+                size_t i = 0;
+                while (i < n) {
+                    uint8_t* h = static_cast<uint8_t*>(dir ? dv[i] : sv[i]);
+                    int64_t len = stage_pcs[i].n;
+                    size_t j = i + 1;
+                    while (j < n && static_cast<uint8_t*>(dir ? dv[j] : sv[j]) == h + len) len += stage_pcs[j++].n;
+                    copy(h, stage_pcs[i].off, len);
+                    i = j;
+                }
+            };
+            if (dir) {  // D2H: gather the slots, then the runs to their host blocks
+                stage_move_kernel<<<static_cast<unsigned>(n), 256, 0, st>>>(desc, stg, 0);
+                OOMB_CUDA(cudaGetLastError());
+                host_runs([&](uint8_t* h, int64_t off, int64_t len) {
+                    OOMB_CUDA(cudaMemcpyAsync(h, stg + off, len, cudaMemcpyDeviceToHost, st));
+                    ++copy_calls;
+                });
+            } else {  // H2D: the runs into staging, then scatter into the slots
+                host_runs([&](uint8_t* h, int64_t off, int64_t len) {
+                    OOMB_CUDA(cudaMemcpyAsync(stg + off, h, len, cudaMemcpyHostToDevice, st));
+                    ++copy_calls;
+                });
+                stage_move_kernel<<<static_cast<unsigned>(n), 256, 0, st>>>(desc, stg, 1);
+                OOMB_CUDA(cudaGetLastError());
+            }
+            OOMB_CUDA(cudaFreeAsync(stg, st));
+        }
+        dv.clear();
+        sv.clear();
+        zv.clear();
     }
     // A write-back batch: the D2H stream follows everything enqueued on the compute stream so
     // far, then copies every evicted page, then stamps the batch; slots freed by it carry its
