@@ -441,9 +441,13 @@ __global__ void __launch_bounds__(384, 1)
             if (j >= 1) mbar_wait(&bars->s_free, (j - 1) & 1);  // softmax read S(j-1) into registers
             tc_fence_after();
             const uint64_t so = boff(st * kTileBytes);
+            if (nks_hd == kHd / 16) {
 #pragma unroll
-            for (int ks = 0; ks < kHd / 16; ++ks)
-                if (ks < nks_hd) umma_ts_w(kDqTmS, kDqTmQ + ks * 8, dK + so + koff(ks, kRegion), idesc_s, ks);
+                for (int ks = 0; ks < kHd / 16; ++ks) umma_ts_w(kDqTmS, kDqTmQ + ks * 8, dK + so + koff(ks, kRegion), idesc_s, ks);
+            } else {  // head dim 64
+#pragma unroll
+                for (int ks = 0; ks < kHd / 32; ++ks) umma_ts_w(kDqTmS, kDqTmQ + ks * 8, dK + so + koff(ks, kRegion), idesc_s, ks);
+            }
             umma_commit_w(&bars->s_full);
         };
         auto mma_dp = [&](int j) {
@@ -451,9 +455,13 @@ __global__ void __launch_bounds__(384, 1)
             mbar_wait(&bars->v_full[st], (j / kDqVSt) & 1);
             tc_fence_after();
             const uint64_t so = boff(st * kTileBytes);
+            if (nks_hd == kHd / 16) {
 #pragma unroll
-            for (int ks = 0; ks < kHd / 16; ++ks)
-                if (ks < nks_hd) umma_ts_w(kDqTmDP, kDqTmDO + ks * 8, dV + so + koff(ks, kRegion), idesc_s, ks);
+                for (int ks = 0; ks < kHd / 16; ++ks) umma_ts_w(kDqTmDP, kDqTmDO + ks * 8, dV + so + koff(ks, kRegion), idesc_s, ks);
+            } else {  // head dim 64
+#pragma unroll
+                for (int ks = 0; ks < kHd / 32; ++ks) umma_ts_w(kDqTmDP, kDqTmDO + ks * 8, dV + so + koff(ks, kRegion), idesc_s, ks);
+            }
             umma_commit_w(&bars->dp_full);
             umma_commit_w(&bars->v_empty[st]);
         };
@@ -920,16 +928,24 @@ __global__ void __launch_bounds__(kKvThreads, 1)
             KVT_WAIT(w_qf, &bars->qdo_full[st], (gi / kKvStages) & 1);
             tc_fence_after();
             const uint64_t so = boff(st * kTileBytes);
+            if (nks_hd == kHd / 16) {
 #pragma unroll
-            for (int ks = 0; ks < kHd / 16; ++ks)
-                if (ks < nks_hd) umma_ss_w(kTmS, dK + koff(ks, kRegion), dQ + so + koff(ks, kRegion), idesc_s, ks);
+                for (int ks = 0; ks < kHd / 16; ++ks) umma_ss_w(kTmS, dK + koff(ks, kRegion), dQ + so + koff(ks, kRegion), idesc_s, ks);
+            } else {  // head dim 64
+#pragma unroll
+                for (int ks = 0; ks < kHd / 32; ++ks) umma_ss_w(kTmS, dK + koff(ks, kRegion), dQ + so + koff(ks, kRegion), idesc_s, ks);
+            }
             umma_commit_w(&bars->s_full);
         };
         auto mma_dp = [&](int gi) {
             const uint64_t so = boff((gi % kKvStages) * kTileBytes);
+            if (nks_hd == kHd / 16) {
 #pragma unroll
-            for (int ks = 0; ks < kHd / 16; ++ks)
-                if (ks < nks_hd) umma_ss_w(kTmDP, dV + koff(ks, kRegion), dDO + so + koff(ks, kRegion), idesc_s, ks);
+                for (int ks = 0; ks < kHd / 16; ++ks) umma_ss_w(kTmDP, dV + koff(ks, kRegion), dDO + so + koff(ks, kRegion), idesc_s, ks);
+            } else {  // head dim 64
+#pragma unroll
+                for (int ks = 0; ks < kHd / 32; ++ks) umma_ss_w(kTmDP, dV + koff(ks, kRegion), dDO + so + koff(ks, kRegion), idesc_s, ks);
+            }
             umma_commit_w(&bars->dp_full);
         };
         auto mma_dv = [&](int gi, uint32_t first) {

@@ -194,9 +194,13 @@ __global__ void __launch_bounds__(384, 1)
             mbar_wait(&bars->k_full[st], (j / kKSt) & 1);
             tc_fence_after();
             const uint64_t so = boff(st * kTileBytes);
+            if (nks_hd == kHd / 16) {
 #pragma unroll
-            for (int ks = 0; ks < kHd / 16; ++ks)
-                if (ks < nks_hd) umma_ss_w(kTmS + b * 128, dQ + koff(ks, kRegion), dK + so + koff(ks, kRegion), idesc_s, ks);
+                for (int ks = 0; ks < kHd / 16; ++ks) umma_ss_w(kTmS + b * 128, dQ + koff(ks, kRegion), dK + so + koff(ks, kRegion), idesc_s, ks);
+            } else {  // head dim 64
+#pragma unroll
+                for (int ks = 0; ks < kHd / 32; ++ks) umma_ss_w(kTmS + b * 128, dQ + koff(ks, kRegion), dK + so + koff(ks, kRegion), idesc_s, ks);
+            }
             umma_commit_w(&bars->s_full[b]);
             umma_commit_w(&bars->k_empty[st]);
         };

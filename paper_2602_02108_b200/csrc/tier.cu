@@ -130,9 +130,11 @@ struct oomb_tier_s {
     int64_t clean_ahead = 256;
     cudaEvent_t t0 = nullptr;
     std::vector<cudaEvent_t> spare_events;
-    uint8_t* host_kv = nullptr;    // pinned [layer][page] x (K, V) blocks
-    uint8_t* host_grad = nullptr;  // pinned [layer][page] x (dK, dV) blocks
-    size_t kv_block = 0, grad_block = 0;
+    // pinned [layer][page] x (K, V, dK, dV) blocks, one allocation: a page's four pieces are adjacent,
+    // so a move of its K/V and gradients is one host-contiguous run (one copy, staged flushes)
+    uint8_t* host_kv = nullptr;    // K, V of block 0 (stride page_block)
+    uint8_t* host_grad = nullptr;  // dK, dV of block 0 (host_kv + kv_block, stride page_block)
+    size_t kv_block = 0, grad_block = 0, page_block = 0;
     TableUpdates pending{};
 
     bool real() const { return pool != nullptr; }
@@ -427,7 +429,7 @@ struct oomb_tier_s {
         ps.pend_kv = lazy_wb && need_kv;
         ps.pend_g = lazy_wb && need_g;
         if (need_kv && !lazy_wb) {
-            uint8_t* h = host_kv + hidx * kv_block;
+            uint8_t* h = host_kv + hidx * page_block;
             queue_copy(1, h, static_cast<uint8_t*>(p.kpool) + ks * kvb, kvb);
             queue_copy(1, h + kvb, static_cast<uint8_t*>(p.vpool) + ks * kvb, kvb);
             ps.host_has_kv = true;
@@ -435,7 +437,7 @@ struct oomb_tier_s {
             d2h_moved += 2 * kvb;
         }
         if (need_g && !lazy_wb) {
-            uint8_t* h = host_grad + hidx * grad_block;
+            uint8_t* h = host_grad + hidx * page_block;
             queue_copy(1, h, reinterpret_cast<uint8_t*>(p.gkpool) + gs * gb, gb);
             queue_copy(1, h + gb, reinterpret_cast<uint8_t*>(p.gvpool) + gs * gb, gb);
             ps.host_has_grad = true;
@@ -483,14 +485,14 @@ struct oomb_tier_s {
         const size_t kvb = static_cast<size_t>(p.page_elems) * p.elem;
         const size_t gb = static_cast<size_t>(p.page_elems) * sizeof(float);
         if (grad) {
-            uint8_t* h = host_grad + static_cast<size_t>(idx) * grad_block;
+            uint8_t* h = host_grad + static_cast<size_t>(idx) * page_block;
             queue_copy(1, h, reinterpret_cast<uint8_t*>(p.gkpool) + s * gb, gb);
             queue_copy(1, h + gb, reinterpret_cast<uint8_t*>(p.gvpool) + s * gb, gb);
             ps.host_has_grad = true;
             ps.pend_g = false;
             d2h_moved += 2 * gb;
         } else {
-            uint8_t* h = host_kv + static_cast<size_t>(idx) * kv_block;
+            uint8_t* h = host_kv + static_cast<size_t>(idx) * page_block;
             queue_copy(1, h, static_cast<uint8_t*>(p.kpool) + s * kvb, kvb);
             queue_copy(1, h + kvb, static_cast<uint8_t*>(p.vpool) + s * kvb, kvb);
             ps.host_has_kv = true;
@@ -566,7 +568,7 @@ struct oomb_tier_s {
         const int32_t ks = kv_back ? vkv : take_slot(false, h2d_stream, "KV");
         p.kvslot[layer][page] = ks;
         if (!kv_back && ps.host_has_kv) {
-            const uint8_t* h = host_kv + hidx * kv_block;
+            const uint8_t* h = host_kv + hidx * page_block;
             queue_copy(0, static_cast<uint8_t*>(p.kpool) + ks * kvb, h, kvb);
             queue_copy(0, static_cast<uint8_t*>(p.vpool) + ks * kvb, h + kvb, kvb);
             h2d_moved += 2 * kvb;
@@ -578,7 +580,7 @@ struct oomb_tier_s {
             p.gslot[layer][page] = gs;
             if (ps.host_has_grad) {
                 h2d_moved += 2 * gb;
-                const uint8_t* h = host_grad + hidx * grad_block;
+                const uint8_t* h = host_grad + hidx * page_block;
                 queue_copy(0, reinterpret_cast<uint8_t*>(p.gkpool) + gs * gb, h, gb);
                 queue_copy(0, reinterpret_cast<uint8_t*>(p.gvpool) + gs * gb, h + gb, gb);
             } else {
@@ -870,9 +872,9 @@ int oomb_tier_create(oomb_pool_t pool, const oomb_tier_config* cfg, void* comput
             t->kv_block = 2 * static_cast<size_t>(pool->page_elems) * pool->elem;
             t->grad_block = 2 * static_cast<size_t>(pool->page_elems) * sizeof(float);
             const size_t n_host = static_cast<size_t>(pool->cfg.n_layers) * pool->max_pages;
-            OOMB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&t->host_kv), n_host * t->kv_block, cudaHostAllocDefault));
-            OOMB_CUDA(
-                cudaHostAlloc(reinterpret_cast<void**>(&t->host_grad), n_host * t->grad_block, cudaHostAllocDefault));
+            t->page_block = t->kv_block + t->grad_block;
+            OOMB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&t->host_kv), n_host * t->page_block, cudaHostAllocDefault));
+            t->host_grad = t->host_kv + t->kv_block;
             OOMB_CUDA(cudaEventCreate(&t->t0));
             OOMB_CUDA(cudaEventRecord(t->t0, t->compute));
             OOMB_REQUIRE(pool->engine == nullptr, OOMB_STATE_ERROR, "tiered_memory: the pool already has an engine");
@@ -947,8 +949,7 @@ int oomb_tier_destroy(oomb_tier_t t) {
         if (t->t0) cudaEventDestroy(t->t0);
         if (t->h2d_stream) cudaStreamDestroy(t->h2d_stream);
         if (t->d2h_stream) cudaStreamDestroy(t->d2h_stream);
-        cudaFreeHost(t->host_kv);
-        cudaFreeHost(t->host_grad);
+        cudaFreeHost(t->host_kv);  // host_grad points into the same allocation
         delete t;
         return lost > 0 ? OOMB_RESIDENCY_ERROR : OOMB_OK;
     }
