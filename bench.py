@@ -841,8 +841,6 @@ def main():
 
     # ---- timed region: device-resident inputs
     clocks = Clocks(dev.index)
-    run.cache.profile_enable(True)
-    run.cache.profile_collect()
     barrier()
     torch.cuda.synchronize()
     clocks.start()
@@ -860,8 +858,19 @@ def main():
     launches = _lib.kernel_launches() - launches0
     barrier()
     clk = clocks.stop()
+    # per-kernel breakdown: as many steps again with the library's event profiler on (two timing
+    # events per launch add host work that a 2 ms c1 step notices), so the timed steps above run
+    # without it
+    run.cache.profile_enable(True)
+    run.cache.profile_collect()
+    for _ in range(args.steps):
+        run.step()
+    torch.cuda.synchronize()
     prof = run.cache.profile_collect()
     run.cache.profile_enable(False)
+    run.fwd_phase.clear()
+    run.bwd_phase.clear()
+    barrier()
     ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     seqs = 1 if sharded else world  # sequences processed by the whole job per step
     value = seqs * cfg["T"] / (ms_step / 1e3)

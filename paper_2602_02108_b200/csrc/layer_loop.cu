@@ -286,7 +286,20 @@ extern "C" int oomb_layer_step(oomb_pool_t p, int layer, int n_chunks, int mode,
             if (!(flags & OOMB_LAYER_FORWARD_ONLY)) bwd_engine();
             return;
         }
-        // ---- forward
+        {  // ---- forward (a block: the backward-only goto skips it whole)
+        // OOMB_LOOP_HOSTPROF=1: host microseconds spent issuing each part of the forward (stderr)
+        static const bool host_prof = std::getenv("OOMB_LOOP_HOSTPROF") != nullptr;
+        double hp[4] = {0, 0, 0, 0};  // select, append, attn_forward, events
+        auto hnow = [] {
+            return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+        };
+        double ht = host_prof ? hnow() : 0;
+        auto hmark = [&](int k) {
+            if (!host_prof) return;
+            const double t = hnow();
+            hp[k] += t - ht;
+            ht = t;
+        };
         OOMB_CUDA(cudaEventRecord(L.ev_app[1], comp));  // earlier work precedes this step's selections
         OOMB_CUDA(cudaStreamWaitEvent(L.sel, L.ev_app[1], 0));
         for (int i = 0; i < 2; ++i) OOMB_CUDA(cudaStreamWaitEvent(L.att[i], L.ev_app[1], 0));
@@ -296,22 +309,31 @@ extern "C" int oomb_layer_step(oomb_pool_t p, int layer, int n_chunks, int mode,
             const void* vi = at(v, i * ke, el);
             const int n_cand = i * m;
             if (i > 0) OOMB_CUDA(cudaStreamWaitEvent(L.sel, L.ev_app[(i - 1) & 1], 0));  // K_avg of chunks < i
+            hmark(3);
             if (mode == OOMB_MODE_TOPK && n_cand > 0)
                 ok(oomb_select_pages_topk(p, layer, qi, C, n_cand, L.sels[i], L.votes[i & 1], L.sel));
             else if (mode == OOMB_MODE_LOCAL && n_cand > 0)
                 ok(oomb_select_recent(L.sels[i], n_cand, c.local_window, m, L.sel));
             else
                 ok(oomb_select_all(L.sels[i], n_cand, m, L.sel));
+            hmark(0);
             OOMB_CUDA(cudaEventRecord(L.ev_sel[i & 1], L.sel));
+            hmark(3);
             int64_t b = 0, e = 0;
             ok(oomb_append_chunk(p, layer, ki, vi, C, comp, &b, &e));
+            hmark(1);
             OOMB_CUDA(cudaEventRecord(L.ev_app[i & 1], comp));
             cudaStream_t a = L.att[i & 1];
             OOMB_CUDA(cudaStreamWaitEvent(a, L.ev_app[i & 1], 0));
             OOMB_CUDA(cudaStreamWaitEvent(a, L.ev_sel[i & 1], 0));
+            hmark(3);
             ok(oomb_attn_forward_ex(p, layer, qi, C, L.sels[i], ki, vi, atw(out, i * qe, el),
                                     atw(lse, static_cast<int64_t>(i) * C * c.n_q_heads, ae), 0, a));
+            hmark(2);
         }
+        if (host_prof)
+            std::fprintf(stderr, "layer_step forward host us: select %.1f append %.1f attn_forward %.1f events %.1f (%d chunks)\n",
+                         hp[0], hp[1], hp[2], hp[3], n_chunks);
         for (int i = 0; i < 2; ++i) {
             OOMB_CUDA(cudaEventRecord(L.ev_att[i], L.att[i]));
             OOMB_CUDA(cudaStreamWaitEvent(comp, L.ev_att[i], 0));
@@ -320,6 +342,7 @@ extern "C" int oomb_layer_step(oomb_pool_t p, int layer, int n_chunks, int mode,
         OOMB_CUDA(cudaStreamWaitEvent(comp, L.ev_sel[0], 0));
         L.fwd_chunks = n_chunks;
         if (flags & OOMB_LAYER_FORWARD_ONLY) return;
+        }
 
     backward:  // ---- backward (dQ deferred: chunk i's dQ overlaps chunk i-1's dK/dV)
         for (int i = n_chunks - 1; i >= 0; --i) {
