@@ -1275,9 +1275,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         OOMB_CUDA(cudaFuncSetAttribute(attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDqSmem));
         OOMB_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kKvSmem));
     }
-    int dev = 0, num_sms = 148;
-    OOMB_CUDA(cudaGetDevice(&dev));
-    OOMB_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    const int num_sms = device_sms();
     BwdWs w = carve(g, workspace);
     ProfScope* prep_scope = new ProfScope(PK_BWD_PREP, st);
     const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
@@ -1312,7 +1310,7 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
         const int zs = OOMB_DQ_SPLIT ? attn_tc_splits(g, num_sms) : 1;
         float* part = nullptr;
         const int64_t n = static_cast<int64_t>(g.C) * g.Hq * g.hd;
-        if (zs > 1) OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), zs * n * sizeof(float), side));
+        if (zs > 1) part = static_cast<float*>(stream_scratch(side, 1, static_cast<size_t>(zs) * n * sizeof(float)));
         const CUtensorMap tdq = map_rows_heads_f32(zs > 1 ? part : dq, static_cast<int64_t>(zs) * g.C, g.Hq, g.hd);
         attn_bwd_dq_kernel<<<dim3(g.Hq, g.C / kTile, zs), 384, kDqSmem, side>>>(tq, tdo, tkc, tvc, maps.kpool,
                                                                                 maps.vpool, tdq, p);
@@ -1322,7 +1320,6 @@ void launch_attn_bwd_tc(const AttnGeom& g, const TcPoolMaps& maps, const void* d
                                   side>>>(reinterpret_cast<const float4*>(part), zs, n / 4,
                                           reinterpret_cast<float4*>(dq));
             check_launch("dq_split_sum_kernel");
-            OOMB_CUDA(cudaFreeAsync(part, side));
         }
         OOMB_CUDA(cudaEventRecord(ev_dq, side));
     };

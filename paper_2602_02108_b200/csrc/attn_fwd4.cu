@@ -456,15 +456,15 @@ void launch_attn_fwd_tc4(const AttnGeom& g, const TcPoolMaps& maps, const void* 
     const CUtensorMap tq = map_rows_heads(q, g.C, g.Hq, g.hd);
     const CUtensorMap tkc = map_rows_heads(k_cur, g.C, g.Hkv, g.hd);
     const CUtensorMap tvc = map_rows_heads(v_cur, g.C, g.Hkv, g.hd);
-    int dev = 0, num_sms = 148;
-    OOMB_CUDA(cudaGetDevice(&dev));
-    OOMB_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    const int num_sms = device_sms();
     const int zs = OOMB_FWD_SPLIT ? attn_tc_splits(g, num_sms) : 1;
     const int64_t rows = static_cast<int64_t>(g.C) * g.Hq;
     F4Params p{g, sel_off, sel_ids, d_kvslot_layer, static_cast<__nv_bfloat16*>(out), lse, d_err, nullptr, nullptr};
-    if (zs > 1) {
-        OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p.o_part), zs * rows * g.hd * sizeof(float), st));
-        OOMB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p.lse_part), zs * rows * sizeof(float), st));
+    if (zs > 1) {  // partials in the stream's scratch: [Z][rows][hd] O, then [Z][rows] LSE
+        const size_t ob = static_cast<size_t>(zs) * rows * g.hd * sizeof(float);
+        uint8_t* w = static_cast<uint8_t*>(stream_scratch(st, 0, ob + static_cast<size_t>(zs) * rows * sizeof(float)));
+        p.o_part = reinterpret_cast<float*>(w);
+        p.lse_part = reinterpret_cast<float*>(w + ob);
     }
     attn_fwd_tc4_kernel<<<dim3(g.Hq, g.C / kTile, zs), 384, kF4Smem, st>>>(tq, tkc, tvc, maps.kpool, maps.vpool, p);
     check_launch("attn_fwd_tc4_kernel");
@@ -472,8 +472,6 @@ void launch_attn_fwd_tc4(const AttnGeom& g, const TcPoolMaps& maps, const void* 
         fwd_split_merge_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(
             p.o_part, p.lse_part, zs, rows, g.hd, static_cast<__nv_bfloat16*>(out), lse);
         check_launch("fwd_split_merge_kernel");
-        OOMB_CUDA(cudaFreeAsync(p.o_part, st));
-        OOMB_CUDA(cudaFreeAsync(p.lse_part, st));
     }
 }
 

@@ -10,6 +10,8 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <map>
+#include <tuple>
 #include <mutex>
 #include <set>
 #include <utility>
@@ -48,6 +50,38 @@ struct Error : std::runtime_error {
         if (e_ != cudaSuccess)                                                                   \
             throw ::oomb::Error(OOMB_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
+
+// Scratch buffer per (device, stream, slot), reused by later work on the same stream (stream order
+// makes the reuse safe): the split-K partials of the forward / dQ launches, which would otherwise
+// cost a cudaMallocAsync + cudaFreeAsync pair per chunk on the host. It only grows (the old buffer
+// is freed in stream order) and lives until process exit.
+inline void* stream_scratch(cudaStream_t st, int slot, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, cudaStream_t, int>, std::pair<void*, size_t>> bufs;
+    int dev = 0;
+    OOMB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    auto& b = bufs[std::make_tuple(dev, st, slot)];
+    if (b.second < bytes) {
+        if (b.first) OOMB_CUDA(cudaFreeAsync(b.first, st));
+        OOMB_CUDA(cudaMallocAsync(&b.first, bytes, st));
+        b.second = bytes;
+    }
+    return b.first;
+}
+
+// SM count of the current device, queried once per device.
+inline int device_sms() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    OOMB_CUDA(cudaGetDevice(&dev));
+    int n = dev < 64 ? cache[dev].load(std::memory_order_relaxed) : 0;
+    if (n == 0) {
+        OOMB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+        if (dev < 64) cache[dev].store(n, std::memory_order_relaxed);
+    }
+    return n;
+}
 
 extern std::atomic<int64_t> g_kernel_launches;
 inline void count_launch(int n = 1) { g_kernel_launches.fetch_add(n, std::memory_order_relaxed); }

@@ -230,10 +230,11 @@ struct oomb_tier_s {
         s.push_back(const_cast<void*>(src));
         z.push_back(n);
     }
-    // OOMB_TIER_STAGED=0: one cudaMemcpyAsync per queued run, straight between host block and slot
-    const bool staged = [] {
+    // OOMB_TIER_STAGED: bit 0 stages H2D flushes, bit 1 D2H flushes (default 3); an unstaged flush
+    // is one cudaMemcpyAsync per queued run, straight between host block and slot
+    const int staged_dirs = [] {
         const char* e = std::getenv("OOMB_TIER_STAGED");
-        return !(e && e[0] == '0');
+        return e ? std::atoi(e) : 3;
     }();
     std::vector<StagePiece> stage_pcs;
     void flush_copies(int dir) {
@@ -247,7 +248,7 @@ struct oomb_tier_s {
         bool aligned = true;
         for (size_t i = 0; i < n; ++i)
             aligned = aligned && ((reinterpret_cast<uintptr_t>(dv[i]) | reinterpret_cast<uintptr_t>(sv[i]) | zv[i]) & 15) == 0;
-        if (!staged || n < 3 || !aligned) {
+        if (!(staged_dirs & (1 << dir)) || n < 3 || !aligned) {
             for (size_t i = 0; i < n; ++i) OOMB_CUDA(cudaMemcpyAsync(dv[i], sv[i], zv[i], kind, st));
             copy_calls += static_cast<int64_t>(n);
         } else {
