@@ -559,8 +559,56 @@ class E2E:
         self.d2h = torch.cuda.Stream(device=d)
         self.h2d_bytes = 0
         self.d2h_bytes = 0
+        # small steps (c1: 32 chunks of 256 tokens) through the native layer loop with whole-step
+        # copies: the per-chunk Python loop above would make the host, not the copies, the bound
+        S = run.S
+        self.native = (NATIVE_LOOP and run.layer is None and
+                       S * C * (Hq + 2 * Hkv) * hd * 4 <= (256 << 20))
+        if self.native:
+            RQ = run.RQ
+            self.qa_h = run.q_all.cpu().pin_memory()
+            self.doa_h = run.do_all.cpu().pin_memory()
+            self.qa_d, self.doa_d = torch.empty_like(run.q_all), torch.empty_like(run.do_all)
+            self.ka_d, self.va_d = torch.empty_like(run.k_all), torch.empty_like(run.v_all)
+            self.ga = run.A.AttnGrads(torch.empty(S, C, Hq, hd, device=d), torch.empty(S, C, Hkv, hd, device=d),
+                                      torch.empty(S, C, Hkv, hd, device=d))
+            self.oa_h = torch.empty(S, C, Hq, hd, dtype=bf, **pin)
+            self.lsea_h = torch.empty(S, C, Hq, **pin)
+            self.ga_h = [torch.empty(S, C, Hq, hd, **pin), torch.empty(S, C, Hkv, hd, **pin),
+                         torch.empty(S, C, Hkv, hd, **pin)]
+            self.ev_in = torch.cuda.Event()
+
+    def step_native(self):
+        """Every step: H2D of the step's q / dO blocks and K / V from pinned memory, the native layer
+        step (chunk_loop.layer_step, every chunk's dq / dk_cur / dv_cur kept), D2H of out, lse and
+        the gradients."""
+        from paper_2602_02108_b200.chunk_loop import layer_step
+        torch, r = self.torch, self.r
+        cfg, C, S = r.cfg, r.cfg["C"], r.S
+        comp = torch.cuda.current_stream()
+        r.cache.reset()
+        with torch.cuda.stream(self.h2d):
+            self.h2d.wait_stream(comp)
+            for dst, src in ((self.qa_d, self.qa_h), (self.doa_d, self.doa_h), (self.ka_d, self.k_h),
+                             (self.va_d, self.v_h)):
+                dst.copy_(src, non_blocking=True)
+            self.ev_in.record(self.h2d)
+        comp.wait_event(self.ev_in)
+        kv = (S, C, cfg["Hkv"], cfg["hd"])
+        layer_step(r.cache, 0, self.qa_d, self.ka_d.view(kv), self.va_d.view(kv), self.doa_d, r.o_all, r.lse_all,
+                   self.ga, mode=cfg["mode"], grad_stride_chunks=1)
+        with torch.cuda.stream(self.d2h):
+            self.d2h.wait_stream(comp)
+            for dst, src in ((self.oa_h, r.o_all), (self.lsea_h, r.lse_all), (self.ga_h[0], self.ga.dq),
+                             (self.ga_h[1], self.ga.dk_cur), (self.ga_h[2], self.ga.dv_cur)):
+                dst.copy_(src, non_blocking=True)
+        comp.wait_stream(self.d2h)
+        self.h2d_bytes = sum(t.numel() * t.element_size() for t in (self.qa_h, self.doa_h, self.k_h, self.v_h))
+        self.d2h_bytes = sum(t.numel() * t.element_size() for t in (self.oa_h, self.lsea_h, *self.ga_h))
 
     def step(self):
+        if self.native:
+            return self.step_native()
         torch, r = self.torch, self.r
         C = r.cfg["C"]
         comp = torch.cuda.current_stream()
@@ -890,7 +938,9 @@ def main():
         torch.cuda.synchronize()
         ms_e2e = max_over_ranks(f0.elapsed_time(f1) / args.steps)
         e2e = {"value": seqs * cfg["T"] / (ms_e2e / 1e3), "unit": "tokens/s", "ms_per_step": ms_e2e,
-               "h2d_bytes_per_step": ee.h2d_bytes, "d2h_bytes_per_step": ee.d2h_bytes}
+               "h2d_bytes_per_step": ee.h2d_bytes, "d2h_bytes_per_step": ee.d2h_bytes,
+               "path": ("native layer loop (chunk_loop.layer_step), whole-step copies" if ee.native else
+                        "public per-chunk API, copies one chunk ahead on side streams")}
 
     offload = None
     # the offload regime is a one-GPU measurement (wall clock, pinned host tier per process)
