@@ -868,8 +868,15 @@ int oomb_tier_create(oomb_pool_t pool, const oomb_tier_config* cfg, void* comput
             t->pt = pool->pt;
             t->pool = pool;
             t->compute = S(compute_stream);
-            OOMB_CUDA(cudaStreamCreateWithFlags(&t->h2d_stream, cudaStreamNonBlocking));
-            OOMB_CUDA(cudaStreamCreateWithFlags(&t->d2h_stream, cudaStreamNonBlocking));
+            // OOMB_TIER_PRIO=1: the copy streams at the highest priority, so the staged flushes'
+            // scatter / gather CTAs take SMs ahead of the attention's queued CTAs; measured neutral at
+            // c3 (profiles/r03_perf_notes.md), so default priority
+            int prio_lo = 0, prio_hi = 0;
+            OOMB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+            const char* pe = std::getenv("OOMB_TIER_PRIO");
+            const int prio = (pe && pe[0] == '1') ? prio_hi : 0;
+            OOMB_CUDA(cudaStreamCreateWithPriority(&t->h2d_stream, cudaStreamNonBlocking, prio));
+            OOMB_CUDA(cudaStreamCreateWithPriority(&t->d2h_stream, cudaStreamNonBlocking, prio));
             t->kv_block = 2 * static_cast<size_t>(pool->page_elems) * pool->elem;
             t->grad_block = 2 * static_cast<size_t>(pool->page_elems) * sizeof(float);
             const size_t n_host = static_cast<size_t>(pool->cfg.n_layers) * pool->max_pages;
